@@ -1,0 +1,196 @@
+/*
+ * sphg.h — C ABI of the B200-native SPH hot path (arXiv 2103.07925).
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++ or torch
+ * types.  The reference ships no hot-path code, only header building blocks
+ * (/root/reference/proj/include/sphfsi, *.hpp) plus SPEC operations; each
+ * entry point below names the reference interface it replaces.
+ *
+ *   host layout    = sphfsi::ParticleStore<3> (store.hpp:24-46): SoA, gid order,
+ *                    Vec<3> fields interleaved xyz (24 B), kind u8, group u32,
+ *                    material u16, dirichlet_T u8.
+ *   device layout  = private, cell-sorted, packed.
+ *
+ * Return codes: 0 ok, 2 config violation (validate_config,
+ * config.hpp:108-167), 3 runtime assertion (escaped / coincident particle,
+ * NaN, neighbour-list overflow that could not be recovered), 4 CUDA/NCCL failure.
+ * The message is available from sphg_last_error().  One host thread drives
+ * one context; nothing is retained from caller buffers after return.
+ *
+ * The CPU oracle (oracle/sph_oracle.cpp, test infrastructure only) exports the
+ * same entry points with the prefix `orc_` instead of `sphg_`.
+ */
+#ifndef SPHG_H
+#define SPHG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPHG_MAX_MAT 8
+#define SPHG_MAX_DIRICHLET 8
+#define SPHG_MAX_PIECES 8
+#define SPHG_NO_MATERIAL (-1)
+#define SPHG_NO_DIRICHLET 0xff /* store.hpp:20 kNoDirichlet */
+
+enum { SPHG_FLUID = 0, SPHG_RIGID = 1, SPHG_BOUNDARY = 2 }; /* store.hpp:11 Kind */
+
+enum {
+  SPHG_OK = 0,
+  SPHG_ERR_CONFIG = 2,
+  SPHG_ERR_RUNTIME = 3,
+  SPHG_ERR_CUDA = 4
+};
+
+/* POD mirror of sphfsi::Material (material.hpp:17-36) plus the per-material
+ * body force of ScenarioConfig::body_force (config.hpp:79,102-104). */
+typedef struct {
+  double rho0;       /* reference_density */
+  double nu;         /* kinematic_viscosity; eta = rho0*nu (material.hpp:32) */
+  double cp;         /* heat_capacity */
+  double kappa;      /* conductivity */
+  double c;          /* speed_of_sound */
+  double pb;         /* background_pressure (transport velocity) */
+  double T_t;        /* transition_temperature, NaN = none */
+  int32_t melt_target;      /* SPHG_NO_MATERIAL = none */
+  int32_t solidify_target;  /* SPHG_NO_MATERIAL = none */
+  double body_force[3];
+} sphg_material;
+
+/* sphfsi::Schedule (config.hpp:20-33): value of the first piece with t <= t_end. */
+typedef struct {
+  int32_t n;
+  int32_t pad;
+  double t_end[SPHG_MAX_PIECES];
+  double value[SPHG_MAX_PIECES];
+} sphg_schedule;
+
+/* Flat POD derived from sphfsi::ScenarioConfig<3> (config.hpp:68-106). */
+typedef struct {
+  double dx;                 /* initial spacing */
+  double h;                  /* smoothing length (0 = dx, config.hpp:100) */
+  double dt;                 /* fixed time step (dt_override, config.hpp:85) */
+  double t0;                 /* start time */
+  double lo[3], hi[3];       /* domain box (must contain walls) */
+  int32_t periodic[3];
+  int32_t n_mat;
+  double cell_edge_override; /* 0 = derive from the Verlet radius */
+  sphg_material mat[SPHG_MAX_MAT];
+  double kc, dc;             /* contact stiffness / damping (config.hpp:81-82) */
+  int32_t tvf;               /* transport_velocity (config.hpp:90) */
+  int32_t thermal;           /* solve the heat equation */
+  int32_t transitions;       /* 0 none, 1 temperature (config.hpp:61) */
+  int32_t n_dirichlet;
+  sphg_schedule dirichlet_T[SPHG_MAX_DIRICHLET]; /* config.hpp:94 */
+  int32_t default_fluid_mat; /* EOS used for wall density when a wall has no fluid support */
+  int32_t nlist_capacity;    /* 0 = auto; grown on overflow */
+  int32_t rank, nranks;      /* domain decomposition (1 rank: 0,1) */
+} sphg_params;
+
+/* Host SoA views in gid order — the ParticleStore<3> layout (store.hpp:26-46).
+ * Vec<3> fields are 3*n doubles, interleaved xyz.  `force` is an optional
+ * extension (resultant f_r on rigid particles); may be NULL. */
+typedef struct {
+  size_t n;
+  double *pos, *vel, *vel_adv, *acc, *acc_bg;
+  double *density, *pressure, *mass, *temperature, *dT_dt;
+  uint8_t *kind;
+  uint32_t *group;
+  uint16_t *material;
+  double *body_frame_pos;
+  double *wall_pressure;
+  double *wall_velocity;
+  uint8_t *dirichlet_T;
+  double *force;
+} sphg_soa;
+
+/* RigidBody.  inertia = world frame about com: xx yy zz xy xz yz. */
+typedef struct {
+  double mass;
+  double com[3];
+  double inertia[6];
+  double q[4];        /* quaternion w x y z (quaternion.hpp:10-15) */
+  double vel[3];
+  double omega[3];
+  double force[3];
+  double torque[3];
+  double acc[3];      /* a_k = f_k/m_k + b_k */
+  double alpha[3];    /* I_k^{-1} torque */
+  int32_t material;
+  int32_t mobile;
+  int32_t alive;
+  int32_t pad;
+} sphg_body;
+
+/* Stages of one kick-drift-kick step.  A full step
+ * is KICK_DRIFT, REBUILD (if the Verlet trigger fired), DENSITY, HEAT,
+ * EXTRAPOLATE, FORCES, BODIES, FINAL_KICK, TRANSITIONS. */
+enum {
+  SPHG_STAGE_REBUILD = 0,     /* cell keys + radix sort + reorder + neighbour list */
+  SPHG_STAGE_DENSITY = 1,     /* density_summation + eos_pressure */
+  SPHG_STAGE_HEAT = 2,        /* apply_thermal_dirichlet + conduction_rhs + T update */
+  SPHG_STAGE_EXTRAPOLATE = 3, /* extrapolate_wall_quantities */
+  SPHG_STAGE_FORCES = 4,      /* momentum_rhs + coupling_force_on_rigid + contact_force */
+  SPHG_STAGE_BODIES = 5,      /* reduce_force_torque -> a_k, alpha_k */
+  SPHG_STAGE_KICK_DRIFT = 6,  /* half kick, drift, orientation, slave positions */
+  SPHG_STAGE_FINAL_KICK = 7,  /* final half kick + slave velocities */
+  SPHG_STAGE_TRANSITIONS = 8, /* detect + apply transitions */
+  SPHG_STAGE_MASS = 9         /* reduce_mass_quantities for every live body */
+};
+
+typedef struct {
+  int64_t steps;
+  int64_t rebuilds;
+  int64_t n_pairs_candidate;  /* at the last rebuild */
+  int64_t transitions_melt;
+  int64_t transitions_solidify;
+  int64_t bodies_alive;
+  int32_t nlist_capacity;
+  int32_t max_neighbours;
+  int32_t cells[3];
+  int32_t pad;
+  double time;
+  double max_displacement;    /* since the last rebuild */
+  double u_max;               /* max |u| of fluid particles at the last kick */
+  double stage_ms[10];        /* accumulated device time per stage (if timing enabled) */
+  int64_t kernel_launches;
+} sphg_stats_t;
+
+typedef struct sphg_ctx sphg_ctx;
+
+/* validate_config (config.hpp:110-167) + device setup.  2 = config violation. */
+int sphg_create(const sphg_params* params, int device, sphg_ctx** out);
+/* Copies a ParticleStore<3> + body table to the device (caller keeps ownership). */
+int sphg_upload(sphg_ctx* ctx, const sphg_soa* soa, const sphg_body* bodies, size_t n_bodies);
+/* a^0 for the first kick: REBUILD, DENSITY, EXTRAPOLATE, FORCES, BODIES. */
+int sphg_initialize(sphg_ctx* ctx);
+/* nsteps full KDK steps, stream-ordered. */
+int sphg_step(sphg_ctx* ctx, int nsteps);
+/* One stage (parity hook; also the per-op evaluator API of SPEC:243-363). */
+int sphg_run_stage(sphg_ctx* ctx, int stage);
+/* Copies the state back in gid order into caller-allocated buffers (NULL fields skipped). */
+int sphg_download(sphg_ctx* ctx, sphg_soa* out, sphg_body* bodies_out, size_t* n_bodies_inout);
+/* Cell of every particle (by gid) and the canonical (cell, gid) order. */
+int sphg_get_cells(sphg_ctx* ctx, int64_t* cell_of_gid, uint32_t* sorted_gid);
+/* Verlet candidate lists in CSR, by gid, each list sorted by gid.  Call with
+ * nbr_gid == NULL to get offsets only (offsets has n+1 entries). */
+int sphg_get_nlist(sphg_ctx* ctx, int64_t* offsets, uint32_t* nbr_gid);
+int sphg_stats(sphg_ctx* ctx, sphg_stats_t* out);
+/* Enables per-stage CUDA-event timing (adds event records; off by default). */
+int sphg_set_timing(sphg_ctx* ctx, int enabled);
+/* Number of bodies in the device table (live or dead). */
+int sphg_num_bodies(sphg_ctx* ctx, size_t* n_bodies);
+/* compute_dt terms: cfl, viscous, body force, contact, conduction; +inf = absent. */
+int sphg_compute_dt(sphg_ctx* ctx, double limits[5]);
+const char* sphg_last_error(const sphg_ctx* ctx);
+void sphg_destroy(sphg_ctx* ctx);
+/* Messages of validate_config for `params` joined by '\n' (empty = valid). */
+int sphg_validate(const sphg_params* params, char* buf, size_t buflen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPHG_H */

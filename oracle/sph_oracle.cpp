@@ -1,0 +1,1205 @@
+// sph_oracle.cpp — CPU ORACLE FOR THE SPH HOT PATH.  TEST INFRASTRUCTURE ONLY.
+//
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+// reference leg may load this library, and only as the checker / the timed CPU
+// baseline.  The product path (paper_2103_07925_b200) never calls it.
+//
+// What it is: a plain, sequential-per-particle restatement of the reference's
+// hot path (arXiv 2103.07925 §3; /root/reference/SPEC.md modules
+// decomposition/fluid/rigid/thermal/transition/integrator) written ON TOP OF
+// the reference's own header building blocks, which are compiled in from
+// /root/reference/proj/include (see oracle/Makefile):
+//   sphfsi::QuinticKernel<3>      kernel.hpp:15-81     (w, dw_dr, sigma)
+//   sphfsi::eos_pressure/density  material.hpp:59-68
+//   sphfsi::Material::dynamic_viscosity material.hpp:32
+//   sphfsi::KahanSum / KahanVec   kahan.hpp:9-36       (body reductions)
+//   sphfsi::Quaternion, quat_exp, rotate, orientation_step  quaternion.hpp:10-76
+//   sphfsi::cross / moment        vec.hpp:84-106
+//   sphfsi::ParticleStore<3>      store.hpp:24-100     (the state container)
+//   sphfsi::validate_config       config.hpp:110-167
+//   sphfsi::seed_lattice          lattice.hpp:71-82    (exported for pinning the generator)
+// The reference leaves several details open; every pin is listed in DESIGN.md §2
+// ("pins") and cited inline as [Pn].  OpenMP parallelises over particles only;
+// every per-particle sum is sequential in gid order, so results do not depend
+// on the thread count.  Compile with -ffp-contract=off (no FMA contraction).
+//
+// Exported C ABI: the entry points of include/sphg.h with prefix orc_, plus KAT
+// helpers (orc_kernel_w, orc_seed_lattice_box, ...).
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "sphfsi/config.hpp"
+#include "sphfsi/kahan.hpp"
+#include "sphfsi/kernel.hpp"
+#include "sphfsi/lattice.hpp"
+#include "sphfsi/material.hpp"
+#include "sphfsi/quaternion.hpp"
+#include "sphfsi/store.hpp"
+#include "sphfsi/vec.hpp"
+
+#include "../include/sphg.h"
+
+using sphfsi::Kind;
+using V3 = sphfsi::Vec<3>;
+
+namespace {
+
+constexpr double kNaN = std::numeric_limits<double>::quiet_NaN();
+
+struct Ctx {
+    sphg_params P{};
+    sphfsi::MaterialTable mats;
+    sphfsi::ParticleStore<3> S;
+    std::vector<V3> force;          // f_r on rigid particles
+    std::vector<double> rho_w, V_w; // wall/rigid interaction density & volume [P7]
+    std::vector<int> wall_mat;      // EOS material used for the wall [P7]
+    std::vector<V3> pos_ref;        // positions at the last rebuild (Verlet)
+    std::vector<sphg_body> bodies;
+    std::vector<std::vector<uint32_t>> members; // rigid particles of each body, gid order
+    std::vector<std::vector<uint32_t>> nl;      // Verlet candidates, gid-sorted
+    std::vector<int64_t> cell_of;
+    std::vector<uint32_t> sorted;
+    // tolerance scales (sum of |pair contributions|)
+    std::vector<double> acc_scale, accbg_scale, dT_scale, force_scale, rho_scale;
+    std::vector<double> body_fscale, body_tscale;
+    double t = 0.0;
+    int64_t steps = 0, rebuilds = 0, n_melt = 0, n_solid = 0;
+    int ncell[3] = {1, 1, 1};
+    double inv_edge[3] = {0, 0, 0}, L[3] = {0, 0, 0}, halfL[3] = {0, 0, 0};
+    double h = 0, rc = 0, rv = 0, dt = 0;
+    double max_disp = 0, u_max = 0;
+    bool built = false;
+    std::string err;
+    int threads = 0;
+};
+
+inline double mi(const Ctx& c, double d, int a) {  // minimum image [P2]
+    if (c.P.periodic[a]) {
+        if (d > c.halfL[a]) d -= c.L[a];
+        else if (d < -c.halfL[a]) d += c.L[a];
+    }
+    return d;
+}
+inline V3 mi3(const Ctx& c, const V3& a, const V3& b) {
+    return V3{mi(c, a[0] - b[0], 0), mi(c, a[1] - b[1], 1), mi(c, a[2] - b[2], 2)};
+}
+inline double r2of(const V3& d) { return (d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]; }  // [P2]
+inline double wrap1(const Ctx& c, double x, int a) {  // [P14]
+    if (c.P.periodic[a]) {
+        if (x < c.P.lo[a]) x += c.L[a];
+        else if (x >= c.P.hi[a]) x -= c.L[a];
+    }
+    return x;
+}
+inline V3 wrap3(const Ctx& c, V3 x) {
+    for (int a = 0; a < 3; ++a) x[a] = wrap1(c, x[a], a);
+    return x;
+}
+inline sphfsi::Quaternion qof(const sphg_body& b) { return {b.q[0], b.q[1], b.q[2], b.q[3]}; }
+inline V3 v3(const double* p) { return V3{p[0], p[1], p[2]}; }
+inline void put3(double* p, const V3& v) { p[0] = v[0]; p[1] = v[1]; p[2] = v[2]; }
+
+sphfsi::ScenarioConfig<3> to_config(const sphg_params& P) {
+    sphfsi::ScenarioConfig<3> cfg;
+    cfg.dx = P.dx;
+    cfg.smoothing_length = P.h;
+    for (int a = 0; a < 3; ++a) {
+        cfg.domain.lo[a] = P.lo[a];
+        cfg.domain.hi[a] = P.hi[a];
+        cfg.periodic[a] = P.periodic[a] != 0;
+    }
+    cfg.cell_edge_override = P.cell_edge_override;
+    for (int m = 0; m < P.n_mat && m < SPHG_MAX_MAT; ++m) {
+        sphfsi::Material mt;
+        mt.name = "m" + std::to_string(m);
+        mt.reference_density = P.mat[m].rho0;
+        mt.kinematic_viscosity = P.mat[m].nu;
+        mt.heat_capacity = P.mat[m].cp;
+        mt.conductivity = P.mat[m].kappa;
+        mt.speed_of_sound = P.mat[m].c;
+        mt.background_pressure = P.mat[m].pb;
+        mt.transition_temperature = P.mat[m].T_t;
+        mt.melt_target = P.mat[m].melt_target < 0 ? sphfsi::kNoMaterial : (sphfsi::MaterialId)P.mat[m].melt_target;
+        mt.solidify_target =
+            P.mat[m].solidify_target < 0 ? sphfsi::kNoMaterial : (sphfsi::MaterialId)P.mat[m].solidify_target;
+        cfg.materials.add(mt);
+        cfg.body_force.push_back(V3{P.mat[m].body_force[0], P.mat[m].body_force[1], P.mat[m].body_force[2]});
+    }
+    cfg.contact_stiffness = P.kc;
+    cfg.contact_damping = P.dc;
+    cfg.dt_override = P.dt;
+    cfg.workers = P.nranks > 0 ? P.nranks : 1;
+    cfg.transport_velocity = P.tvf != 0;
+    for (int g = 0; g < P.n_dirichlet && g < SPHG_MAX_DIRICHLET; ++g) {
+        sphfsi::Schedule s;
+        for (int k = 0; k < P.dirichlet_T[g].n && k < SPHG_MAX_PIECES; ++k)
+            s.pieces.push_back({P.dirichlet_T[g].t_end[k], P.dirichlet_T[g].value[k]});
+        cfg.dirichlet_temperature.push_back(s);
+    }
+    return cfg;
+}
+
+std::vector<std::string> validate(const sphg_params& P) {
+    std::vector<std::string> v;
+    if (P.n_mat < 0 || P.n_mat > SPHG_MAX_MAT) {
+        v.push_back("material count out of range");
+        return v;
+    }
+    v = sphfsi::validate_config(to_config(P));
+    if (!(P.dt > 0.0)) v.push_back("time step dt must be positive");
+    const double h = P.h > 0.0 ? P.h : P.dx;
+    const double rv = sphfsi::kKernelSupportScale * h + sphfsi::kVerletSkinFactor * h;
+    for (int a = 0; a < 3; ++a) {
+        const double ext = P.hi[a] - P.lo[a];
+        const double e0 = P.cell_edge_override > 0.0 ? P.cell_edge_override : rv;
+        if (P.periodic[a] && ext > 0.0 && std::floor(ext / e0) < 3.0)
+            v.push_back("periodic axis " + std::to_string(a) + " has fewer than 3 cells");
+    }
+    if (P.n_dirichlet < 0 || P.n_dirichlet > SPHG_MAX_DIRICHLET) v.push_back("dirichlet group count out of range");
+    if (P.default_fluid_mat < 0 || P.default_fluid_mat >= P.n_mat) v.push_back("default fluid material missing");
+    return v;
+}
+
+void setup_geometry(Ctx& c) {
+    c.h = c.P.h > 0.0 ? c.P.h : c.P.dx;
+    c.rc = sphfsi::kKernelSupportScale * c.h;
+    c.rv = c.rc + sphfsi::kVerletSkinFactor * c.h;
+    c.dt = c.P.dt;
+    for (int a = 0; a < 3; ++a) {
+        c.L[a] = c.P.hi[a] - c.P.lo[a];
+        c.halfL[a] = 0.5 * c.L[a];
+        const double e0 = c.P.cell_edge_override > 0.0 ? c.P.cell_edge_override : c.rv;  // [P1]
+        int n = (int)std::floor(c.L[a] / e0);
+        if (n < 1) n = 1;
+        c.ncell[a] = n;
+        c.inv_edge[a] = (double)n / c.L[a];
+    }
+}
+
+bool fail(Ctx& c, const std::string& m) {
+    c.err = m;
+    return false;
+}
+
+// ---------------------------------------------------------------- rebuild
+// DomainGrid binning, build_pairs with Verlet skin.
+bool stage_rebuild(Ctx& c) {
+    const size_t n = c.S.size();
+    c.cell_of.assign(n, 0);
+    for (size_t i = 0; i < n; ++i) {
+        int64_t ci[3];
+        for (int a = 0; a < 3; ++a) {
+            const double x = c.S.pos[i][a];
+            if (!c.P.periodic[a] && (x < c.P.lo[a] || x > c.P.hi[a]))
+                return fail(c, "escaped particle " + std::to_string(i) + " at step " + std::to_string(c.steps));
+            int64_t k = (int64_t)std::floor((x - c.P.lo[a]) * c.inv_edge[a]);  // [P1]
+            if (k < 0) k = 0;
+            if (k >= c.ncell[a]) k = c.ncell[a] - 1;
+            ci[a] = k;
+        }
+        c.cell_of[i] = (ci[0] * c.ncell[1] + ci[1]) * c.ncell[2] + ci[2];
+    }
+    const int64_t ncells = (int64_t)c.ncell[0] * c.ncell[1] * c.ncell[2];
+    std::vector<int64_t> start(ncells + 1, 0);
+    for (size_t i = 0; i < n; ++i) start[c.cell_of[i] + 1]++;
+    for (int64_t k = 0; k < ncells; ++k) start[k + 1] += start[k];
+    c.sorted.assign(n, 0);
+    {
+        std::vector<int64_t> fill(start.begin(), start.end() - 1);
+        for (size_t i = 0; i < n; ++i) c.sorted[fill[c.cell_of[i]]++] = (uint32_t)i;  // (cell, gid) order [P1]
+    }
+    c.nl.assign(n, {});
+    const double rv2 = c.rv * c.rv;
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t ii = 0; ii < (int64_t)n; ++ii) {
+        const size_t i = (size_t)ii;
+        const int64_t cid = c.cell_of[i];
+        const int64_t cz = cid % c.ncell[2], cy = (cid / c.ncell[2]) % c.ncell[1], cx = cid / ((int64_t)c.ncell[2] * c.ncell[1]);
+        auto& out = c.nl[i];
+        for (int ox = -1; ox <= 1; ++ox)
+            for (int oy = -1; oy <= 1; ++oy)
+                for (int oz = -1; oz <= 1; ++oz) {
+                    int64_t q[3] = {cx + ox, cy + oy, cz + oz};
+                    bool skip = false;
+                    for (int a = 0; a < 3; ++a) {
+                        if (q[a] < 0 || q[a] >= c.ncell[a]) {
+                            if (!c.P.periodic[a]) { skip = true; break; }
+                            q[a] = (q[a] + c.ncell[a]) % c.ncell[a];
+                        }
+                    }
+                    if (skip) continue;
+                    const int64_t cj = (q[0] * c.ncell[1] + q[1]) * c.ncell[2] + q[2];
+                    for (int64_t s = start[cj]; s < start[cj + 1]; ++s) {
+                        const uint32_t j = c.sorted[s];
+                        if (j == i) continue;
+                        if (c.S.kind[i] == Kind::Boundary && c.S.kind[j] == Kind::Boundary) continue;  // [P2]
+                        const V3 d = mi3(c, c.S.pos[i], c.S.pos[j]);
+                        if (r2of(d) <= rv2) out.push_back(j);  // inclusive
+                    }
+                }
+        std::sort(out.begin(), out.end());
+    }
+    c.pos_ref = c.S.pos;
+    c.max_disp = 0.0;
+    c.built = true;
+    c.rebuilds++;
+    return true;
+}
+
+// -------------------------------------------------------------- density
+// density_summation + eos_pressure (material.hpp:59-62)
+bool stage_density(Ctx& c) {
+    const sphfsi::QuinticKernel<3> K(c.h);
+    const double rc2 = c.rc * c.rc;
+    const int64_t n = (int64_t)c.S.size();
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        if (c.S.kind[i] != Kind::Fluid) continue;
+        double s = K.w(0.0);  // self term first
+        for (uint32_t j : c.nl[i]) {
+            const V3 d = mi3(c, c.S.pos[i], c.S.pos[j]);
+            const double r2 = r2of(d);
+            if (r2 > rc2) continue;
+            s += K.w(std::sqrt(r2));
+        }
+        const double rho = c.S.mass[i] * s;
+        c.S.density[i] = rho;
+        c.S.pressure[i] = sphfsi::eos_pressure(rho, c.mats[c.S.material[i]]);
+        c.rho_scale[i] = rho;
+    }
+    return true;
+}
+
+// ------------------------------------------------------------------ heat
+double sched_value(const sphg_schedule& s, double t) {  // Schedule::value_at (config.hpp:28-32)
+    sphfsi::Schedule sc;
+    for (int k = 0; k < s.n; ++k) sc.pieces.push_back({s.t_end[k], s.value[k]});
+    return sc.value_at(t);
+}
+
+// apply_thermal_dirichlet at t^{n+1} [P9]; conduction_rhs (SPEC:398-406,
+// PAPER:399-405) with T^n, r^{n+1}, rho^{n+1}; T^{n+1} = T^n + dt rate.
+bool stage_heat(Ctx& c) {
+    const size_t n = c.S.size();
+    const double t_new = c.t + c.dt;
+    for (size_t i = 0; i < n; ++i) {
+        if (c.S.kind[i] == Kind::Boundary && c.S.dirichlet_T[i] != sphfsi::kNoDirichlet) {
+            const int g = c.S.dirichlet_T[i];
+            if (g < c.P.n_dirichlet && c.P.dirichlet_T[g].n > 0) c.S.temperature[i] = sched_value(c.P.dirichlet_T[g], t_new);
+        }
+    }
+    const std::vector<double> Tn = c.S.temperature;  // double buffer [P9]
+    const sphfsi::QuinticKernel<3> K(c.h);
+    const double rc2 = c.rc * c.rc;
+    bool coincident = false;
+    size_t bad_i = 0, bad_j = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t ii = 0; ii < (int64_t)n; ++ii) {
+        const size_t a = (size_t)ii;
+        if (c.S.kind[a] == Kind::Boundary) continue;
+        const sphfsi::Material& ma = c.mats[c.S.material[a]];
+        double s = 0.0, sc = 0.0;
+        for (uint32_t b : c.nl[a]) {
+            const bool bd = c.S.kind[b] == Kind::Boundary;
+            if (bd && c.S.dirichlet_T[b] == sphfsi::kNoDirichlet) continue;
+            const V3 d = mi3(c, c.S.pos[a], c.S.pos[b]);
+            const double r2 = r2of(d);
+            if (r2 > rc2) continue;
+            const double r = std::sqrt(r2);
+            if (r == 0.0) {
+#pragma omp critical
+                { coincident = true; bad_i = a; bad_j = b; }
+                continue;
+            }
+            const sphfsi::Material& mb = c.mats[c.S.material[b]];
+            const double ksum = ma.conductivity + mb.conductivity;
+            if (ksum == 0.0) continue;
+            const double kt = 4.0 * ma.conductivity * mb.conductivity / ksum;
+            const double rho_b = bd ? mb.reference_density : c.S.density[b];  // [P9]
+            const double Vb = c.S.mass[b] / rho_b;
+            const double term = Vb * kt * ((Tn[a] - Tn[b]) / r) * K.dw_dr(r);
+            s += term;
+            sc += std::abs(term);
+        }
+        double rate = 0.0, scale = 0.0;
+        if (ma.heat_capacity > 0.0) {
+            const double den = c.S.density[a] * ma.heat_capacity;
+            rate = s / den;
+            scale = sc / den;
+        }
+        c.S.dT_dt[a] = rate;
+        c.S.temperature[a] = Tn[a] + c.dt * rate;
+        c.dT_scale[a] = scale;
+    }
+    if (coincident)
+        return fail(c, "coincident particles " + std::to_string(bad_i) + " and " + std::to_string(bad_j) +
+                           " at step " + std::to_string(c.steps));
+    return true;
+}
+
+// ----------------------------------------------------------- extrapolate
+V3 rigid_rk(const Ctx& c, size_t r) {
+    const sphg_body& b = c.bodies[c.S.group[r]];
+    return sphfsi::rotate(qof(b), c.S.body_frame_pos[r]);
+}
+
+// extrapolate_wall_quantities (Adami 2012) [P6][P7]
+bool stage_extrapolate(Ctx& c) {
+    const sphfsi::QuinticKernel<3> K(c.h);
+    const double rc2 = c.rc * c.rc;
+    const double dx3 = c.P.dx * c.P.dx * c.P.dx;
+    const int64_t n = (int64_t)c.S.size();
+#pragma omp parallel for schedule(static)
+    for (int64_t w = 0; w < n; ++w) {
+        if (c.S.kind[w] == Kind::Fluid) continue;
+        V3 uw = V3::zero(), aw = V3::zero();
+        if (c.S.kind[w] == Kind::Rigid) {
+            const sphg_body& b = c.bodies[c.S.group[w]];
+            const V3 rk = rigid_rk(c, (size_t)w);
+            const V3 om = v3(b.omega);
+            uw = c.S.vel[w];
+            aw = v3(b.acc) + sphfsi::cross(v3(b.alpha), rk) + sphfsi::cross(om, sphfsi::cross(om, rk));  // [P6]
+        }
+        double sw = 0.0, sp = 0.0;
+        V3 su = V3::zero();
+        double smat[SPHG_MAX_MAT] = {0};
+        for (uint32_t f : c.nl[w]) {
+            if (c.S.kind[f] != Kind::Fluid) continue;
+            const V3 d = mi3(c, c.S.pos[w], c.S.pos[f]);  // r_w - r_f
+            const double r2 = r2of(d);
+            if (r2 > rc2) continue;
+            const double W = K.w(std::sqrt(r2));
+            const V3 g = v3(c.P.mat[c.S.material[f]].body_force);
+            sw += W;
+            sp += W * (c.S.pressure[f] + c.S.density[f] * sphfsi::dot(g - aw, d));
+            su += W * c.S.vel[f];
+            smat[c.S.material[f]] += W;
+        }
+        int m = c.P.default_fluid_mat;
+        if (sw > 0.0) {
+            double best = -1.0;
+            for (int k = 0; k < c.P.n_mat; ++k)
+                if (smat[k] > best) { best = smat[k]; m = k; }
+        }
+        const double pw = sw > 0.0 ? sp / sw : 0.0;
+        const V3 ut = sw > 0.0 ? 2.0 * uw - su / sw : uw;
+        const sphfsi::Material& fm = c.mats[(sphfsi::MaterialId)m];
+        const double rhow = std::max(fm.reference_density, sphfsi::eos_density(pw, fm));
+        c.S.wall_pressure[w] = pw;
+        c.S.wall_velocity[w] = ut;
+        c.rho_w[w] = rhow;
+        c.V_w[w] = fm.reference_density * dx3 / rhow;
+        c.wall_mat[w] = m;
+        if (c.S.kind[w] == Kind::Boundary) c.S.density[w] = rhow;
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------- forces
+struct Side {  // interaction values of one pair partner [P7]
+    double rho, p, V, eta;
+    V3 u, du;  // velocity and (u_adv - u) for the TVF A term
+    bool fluid;
+};
+
+inline Side side_of(const Ctx& c, size_t j, const sphfsi::Material* eta_from) {
+    Side s;
+    if (c.S.kind[j] == Kind::Fluid) {
+        s.rho = c.S.density[j];
+        s.p = c.S.pressure[j];
+        s.V = c.S.mass[j] / s.rho;
+        s.eta = c.mats[c.S.material[j]].dynamic_viscosity();
+        s.u = c.S.vel[j];
+        s.du = c.S.vel_adv[j] - c.S.vel[j];
+        s.fluid = true;
+    } else {
+        s.rho = c.rho_w[j];
+        s.p = c.S.wall_pressure[j];
+        s.V = c.V_w[j];
+        s.eta = eta_from ? eta_from->dynamic_viscosity() : 0.0;  // eta_w := eta_i [P7]
+        s.u = c.S.wall_velocity[j];
+        s.du = V3::zero();  // A_w = 0 [P5]
+        s.fluid = false;
+    }
+    return s;
+}
+
+// pair acceleration a_ij of fluid i due to j (momentum_rhs, PAPER:240-246 + TVF [P5]);
+// returns a_ij and adds V2*gradW to bg.
+inline V3 pair_acc(const Ctx& c, const sphfsi::QuinticKernel<3>& K, const Side& I, double mi_, const Side& J,
+                   const V3& d, double r, V3& bgsum) {
+    const double dW = K.dw_dr(r);
+    const V3 e = d / r;
+    const V3 gW = dW * e;
+    const double V2 = I.V * I.V + J.V * J.V;
+    const double pt = (J.rho * I.p + I.rho * J.p) / (I.rho + J.rho);
+    const double es = I.eta + J.eta;
+    const double et = es > 0.0 ? 2.0 * I.eta * J.eta / es : 0.0;
+    V3 term = (-pt) * gW + (et * dW / r) * (I.u - J.u);
+    if (c.P.tvf) {
+        // 0.5 (A_i + A_j) . gradW with A = rho u (u_adv - u)^T
+        const V3 Ai = (I.rho * sphfsi::dot(I.du, gW)) * I.u;
+        const V3 Aj = (J.rho * sphfsi::dot(J.du, gW)) * J.u;
+        term += 0.5 * (Ai + Aj);
+    }
+    bgsum += V2 * gW;
+    return (V2 / mi_) * term;
+}
+
+inline double norm3(const V3& v) { return std::sqrt(r2of(v)); }
+
+bool stage_forces(Ctx& c) {
+    const sphfsi::QuinticKernel<3> K(c.h);
+    const double rc2 = c.rc * c.rc;
+    const int64_t n = (int64_t)c.S.size();
+    bool coincident = false;
+    int64_t bad_i = 0, bad_j = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        const Kind ki = c.S.kind[i];
+        if (ki == Kind::Fluid) {
+            const sphfsi::Material& mi_ = c.mats[c.S.material[i]];
+            const Side I = side_of(c, (size_t)i, nullptr);
+            V3 sum = V3::zero(), bg = V3::zero();
+            double sc = 0.0, bgsc = 0.0;
+            for (uint32_t j : c.nl[i]) {
+                const V3 d = mi3(c, c.S.pos[i], c.S.pos[j]);
+                const double r2 = r2of(d);
+                if (r2 > rc2) continue;
+                const double r = std::sqrt(r2);
+                if (r == 0.0) {
+#pragma omp critical
+                    { coincident = true; bad_i = i; bad_j = j; }
+                    continue;
+                }
+                const Side J = side_of(c, j, &mi_);
+                V3 bgp = V3::zero();
+                const V3 a = pair_acc(c, K, I, c.S.mass[i], J, d, r, bgp);
+                sum += a;
+                bg += bgp;
+                sc += norm3(a);
+                bgsc += norm3(bgp);
+            }
+            const V3 b = v3(c.P.mat[c.S.material[i]].body_force);
+            c.S.acc[i] = sum + b;
+            const double f = c.P.tvf ? -mi_.background_pressure / c.S.mass[i] : 0.0;
+            c.S.acc_bg[i] = f * bg;
+            c.acc_scale[i] = sc + norm3(b);
+            c.accbg_scale[i] = std::abs(f) * bgsc;
+        } else if (ki == Kind::Rigid) {
+            // coupling_force_on_rigid f_ri = -m_i a_ir + contact_force
+            V3 f = V3::zero();
+            double sc = 0.0;
+            const uint32_t body = c.S.group[i];
+            for (uint32_t j : c.nl[i]) {
+                const Kind kj = c.S.kind[j];
+                if (kj == Kind::Fluid) {
+                    const V3 d = mi3(c, c.S.pos[j], c.S.pos[i]);  // r_j - r_r, from the fluid's view
+                    const double r2 = r2of(d);
+                    if (r2 > rc2) continue;
+                    const double r = std::sqrt(r2);
+                    if (r == 0.0) {
+#pragma omp critical
+                        { coincident = true; bad_i = i; bad_j = j; }
+                        continue;
+                    }
+                    const sphfsi::Material& mj = c.mats[c.S.material[j]];
+                    const Side Jf = side_of(c, j, nullptr);
+                    const Side R = side_of(c, (size_t)i, &mj);
+                    V3 bgp = V3::zero();
+                    const V3 a = pair_acc(c, K, Jf, c.S.mass[j], R, d, r, bgp);
+                    const V3 fr = (-c.S.mass[j]) * a;
+                    f += fr;
+                    sc += norm3(fr);
+                } else if (kj == Kind::Boundary || c.S.group[j] != body) {
+                    const V3 d = mi3(c, c.S.pos[i], c.S.pos[j]);
+                    const double r2 = r2of(d);
+                    const double r = std::sqrt(r2);
+                    if (!(r < c.P.dx)) continue;
+                    if (r == 0.0) {
+#pragma omp critical
+                        { coincident = true; bad_i = i; bad_j = j; }
+                        continue;
+                    }
+                    const V3 e = d / r;
+                    const V3 vrel = c.S.vel[i] - c.S.vel[j];
+                    const double s = c.P.kc * (r - c.P.dx) + c.P.dc * sphfsi::dot(e, vrel);
+                    const V3 fc = (-std::min(0.0, s)) * e;
+                    f += fc;
+                    sc += norm3(fc);
+                }
+            }
+            c.force[i] = f;
+            c.force_scale[i] = sc;
+        }
+    }
+    if (coincident)
+        return fail(c, "coincident particles " + std::to_string(bad_i) + " and " + std::to_string(bad_j) +
+                           " at step " + std::to_string(c.steps));
+    return true;
+}
+
+// ---------------------------------------------------------------- bodies
+double particle_inertia(double m, double dx) {  // SPEC:337-345 (3D, r_eff squared)
+    const double reff = std::cbrt(0.75 / std::numbers::pi) * dx;
+    return 0.4 * m * reff * reff;
+}
+
+void inverse_apply(const double I[6], const V3& t, V3& out, bool& singular) {  // [P11]
+    const double xx = I[0], yy = I[1], zz = I[2], xy = I[3], xz = I[4], yz = I[5];
+    const double c00 = yy * zz - yz * yz, c01 = xz * yz - xy * zz, c02 = xy * yz - xz * yy;
+    const double c11 = xx * zz - xz * xz, c12 = xy * xz - xx * yz, c22 = xx * yy - xy * xy;
+    const double det = xx * c00 + xy * c01 + xz * c02;
+    const double tr = xx + yy + zz;
+    if (!(std::abs(det) > 1e-12 * tr * tr * tr)) {
+        singular = true;
+        out = V3::zero();
+        return;
+    }
+    singular = false;
+    out = V3{(c00 * t[0] + c01 * t[1] + c02 * t[2]) / det, (c01 * t[0] + c11 * t[1] + c12 * t[2]) / det,
+             (c02 * t[0] + c12 * t[1] + c22 * t[2]) / det};
+}
+
+// reduce_force_torque with compensated sums (kahan.hpp) about
+// the integrated COM; world-frame inertia recomputed every step [P11].
+bool stage_bodies(Ctx& c) {
+    const int64_t nb = (int64_t)c.bodies.size();
+    c.body_fscale.resize(c.bodies.size());
+    c.body_tscale.resize(c.bodies.size());
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t k = 0; k < nb; ++k) {
+        sphg_body& b = c.bodies[k];
+        if (!b.alive) continue;
+        sphfsi::KahanVec<3> F, T;
+        sphfsi::KahanSum I6[6];
+        double fs = 0.0, ts = 0.0;
+        const sphfsi::Quaternion q = qof(b);
+        for (uint32_t r : c.members[k]) {
+            const V3 rk = sphfsi::rotate(q, c.S.body_frame_pos[r]);
+            const V3& f = c.force[r];
+            F.add(f);
+            const V3 tq = sphfsi::moment(rk, f);
+            T.add(tq);
+            fs += norm3(f);
+            ts += norm3(rk) * norm3(f);
+            const double m = c.S.mass[r];
+            const double Ir = particle_inertia(m, c.P.dx);
+            const double d2 = r2of(rk);
+            I6[0].add(Ir + m * (d2 - rk[0] * rk[0]));
+            I6[1].add(Ir + m * (d2 - rk[1] * rk[1]));
+            I6[2].add(Ir + m * (d2 - rk[2] * rk[2]));
+            I6[3].add(-m * rk[0] * rk[1]);
+            I6[4].add(-m * rk[0] * rk[2]);
+            I6[5].add(-m * rk[1] * rk[2]);
+        }
+        const V3 f = F.value(), t = T.value();
+        put3(b.force, f);
+        put3(b.torque, t);
+        for (int q6 = 0; q6 < 6; ++q6) b.inertia[q6] = I6[q6].value();
+        c.body_fscale[k] = fs;
+        c.body_tscale[k] = ts;
+        if (b.mobile && b.mass > 0.0) {
+            const V3 a = f / b.mass + v3(c.P.mat[b.material].body_force);
+            put3(b.acc, a);
+            V3 al;
+            bool sing;
+            inverse_apply(b.inertia, t, al, sing);
+            put3(b.alpha, al);
+        } else {
+            put3(b.acc, V3::zero());
+            put3(b.alpha, V3::zero());
+        }
+    }
+    return true;
+}
+
+// reduce_mass_quantities (PAPER:303-325 single-processor form, Remark 3.10)
+// anchored at the body's min-gid particle with minimum image; chi recomputed (Remark 3.7).
+void mass_quantities(Ctx& c, size_t k) {
+    sphg_body& b = c.bodies[k];
+    const auto& mem = c.members[k];
+    if (mem.empty()) {
+        b.alive = 0;
+        b.mass = 0.0;
+        return;
+    }
+    const V3 anchor = c.S.pos[mem[0]];
+    sphfsi::KahanSum M;
+    sphfsi::KahanVec<3> MR;
+    for (uint32_t r : mem) {
+        const double m = c.S.mass[r];
+        M.add(m);
+        MR.add(m * mi3(c, c.S.pos[r], anchor));
+    }
+    const double m = M.value();
+    const V3 com = wrap3(c, anchor + MR.value() / m);
+    sphfsi::KahanSum I6[6];
+    const sphfsi::Quaternion qc = qof(b).conjugate();
+    for (uint32_t r : mem) {
+        const double mr = c.S.mass[r];
+        const V3 d = mi3(c, c.S.pos[r], com);
+        const double Ir = particle_inertia(mr, c.P.dx);
+        const double d2 = r2of(d);
+        I6[0].add(Ir + mr * (d2 - d[0] * d[0]));
+        I6[1].add(Ir + mr * (d2 - d[1] * d[1]));
+        I6[2].add(Ir + mr * (d2 - d[2] * d[2]));
+        I6[3].add(-mr * d[0] * d[1]);
+        I6[4].add(-mr * d[0] * d[2]);
+        I6[5].add(-mr * d[1] * d[2]);
+        c.S.body_frame_pos[r] = sphfsi::rotate(qc, d);
+    }
+    b.mass = m;
+    put3(b.com, com);
+    for (int q6 = 0; q6 < 6; ++q6) b.inertia[q6] = I6[q6].value();
+    b.alive = 1;
+}
+
+void rebuild_members(Ctx& c) {
+    c.members.assign(c.bodies.size(), {});
+    for (size_t i = 0; i < c.S.size(); ++i)
+        if (c.S.kind[i] == Kind::Rigid) c.members[c.S.group[i]].push_back((uint32_t)i);
+}
+
+bool stage_mass(Ctx& c) {
+    rebuild_members(c);
+    for (size_t k = 0; k < c.bodies.size(); ++k)
+        if (c.bodies[k].alive) mass_quantities(c, k);
+    return true;
+}
+
+// ------------------------------------------------------------ integrator
+// step(): half kick, drift, orientation, slave [P14]
+bool stage_kick_drift(Ctx& c) {
+    const double hdt = 0.5 * c.dt, dt = c.dt;
+    const int64_t n = (int64_t)c.S.size();
+    double umax = 0.0;
+    for (auto& b : c.bodies) {
+        if (!b.alive || !b.mobile) continue;
+        const V3 u = v3(b.vel) + hdt * v3(b.acc);
+        const V3 w = v3(b.omega) + hdt * v3(b.alpha);
+        put3(b.vel, u);
+        put3(b.omega, w);
+        put3(b.com, wrap3(c, v3(b.com) + dt * u));
+        const sphfsi::Quaternion q = sphfsi::orientation_step<3>(qof(b), w, dt);
+        b.q[0] = q.w; b.q[1] = q.x; b.q[2] = q.y; b.q[3] = q.z;
+    }
+    bool escaped = false;
+    int64_t bad = 0;
+    double md2 = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : umax, md2)
+    for (int64_t i = 0; i < n; ++i) {
+        const Kind k = c.S.kind[i];
+        if (k == Kind::Fluid) {
+            const V3 uh = c.S.vel[i] + hdt * c.S.acc[i];
+            const V3 ua = c.P.tvf ? uh + hdt * c.S.acc_bg[i] : uh;
+            c.S.vel[i] = uh;
+            c.S.vel_adv[i] = ua;
+            c.S.pos[i] = wrap3(c, c.S.pos[i] + dt * ua);
+            umax = std::max(umax, r2of(uh));
+        } else if (k == Kind::Rigid) {
+            const sphg_body& b = c.bodies[c.S.group[i]];
+            const V3 rk = sphfsi::rotate(qof(b), c.S.body_frame_pos[i]);
+            c.S.pos[i] = wrap3(c, v3(b.com) + rk);
+            const V3 u = v3(b.vel) + sphfsi::cross(v3(b.omega), rk);
+            c.S.vel[i] = u;
+            c.S.vel_adv[i] = u;
+        } else {
+            continue;
+        }
+        for (int a = 0; a < 3; ++a)
+            if (!c.P.periodic[a] && (c.S.pos[i][a] < c.P.lo[a] || c.S.pos[i][a] > c.P.hi[a])) {
+#pragma omp critical
+                { escaped = true; bad = i; }
+            }
+        if (c.built) md2 = std::max(md2, r2of(mi3(c, c.S.pos[i], c.pos_ref[i])));
+    }
+    c.u_max = std::sqrt(umax);
+    c.max_disp = std::sqrt(md2);
+    c.t += c.dt;
+    if (escaped) return fail(c, "escaped particle " + std::to_string(bad) + " at step " + std::to_string(c.steps + 1));
+    return true;
+}
+
+bool stage_final_kick(Ctx& c) {
+    const double hdt = 0.5 * c.dt;
+    for (auto& b : c.bodies) {
+        if (!b.alive || !b.mobile) continue;
+        put3(b.vel, v3(b.vel) + hdt * v3(b.acc));
+        put3(b.omega, v3(b.omega) + hdt * v3(b.alpha));
+    }
+    const int64_t n = (int64_t)c.S.size();
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        if (c.S.kind[i] == Kind::Fluid) {
+            c.S.vel[i] = c.S.vel[i] + hdt * c.S.acc[i];
+        } else if (c.S.kind[i] == Kind::Rigid) {
+            const sphg_body& b = c.bodies[c.S.group[i]];
+            const V3 rk = sphfsi::rotate(qof(b), c.S.body_frame_pos[i]);
+            c.S.vel[i] = v3(b.vel) + sphfsi::cross(v3(b.omega), rk);
+        }
+    }
+    return true;
+}
+
+// ------------------------------------------------------------ transitions
+// detect_transitions / apply_transitions / post_transition_body_velocity /
+// split_disconnected_bodies [P12]
+bool stage_transitions(Ctx& c) {
+    if (c.P.transitions != 1) return true;
+    const size_t n = c.S.size();
+    std::vector<uint32_t> melt, solid;
+    for (size_t i = 0; i < n; ++i) {
+        const sphg_material& m = c.P.mat[c.S.material[i]];
+        if (std::isnan(m.T_t)) continue;
+        if (c.S.kind[i] == Kind::Rigid && m.melt_target >= 0 && c.S.temperature[i] > m.T_t) melt.push_back((uint32_t)i);
+        else if (c.S.kind[i] == Kind::Fluid && m.solidify_target >= 0 && c.S.temperature[i] < m.T_t)
+            solid.push_back((uint32_t)i);
+    }
+    if (melt.empty() && solid.empty()) return true;
+    c.n_melt += (int64_t)melt.size();
+    c.n_solid += (int64_t)solid.size();
+    const size_t nb0 = c.bodies.size();
+    std::vector<sphg_body> old = c.bodies;   // pre-batch body state (u'_k, r'_k)
+    std::vector<char> affected(nb0, 0), lost(nb0, 0);
+    std::vector<uint32_t> src_body;          // for each body id: the pre-batch body it came from (or self)
+    // 1. melts: rigid -> fluid with the body's rigid-motion velocity
+    std::vector<char> melting(n, 0);
+    for (uint32_t r : melt) melting[r] = 1;
+    for (uint32_t r : melt) {
+        const uint32_t k = c.S.group[r];
+        const sphg_body& b = c.bodies[k];
+        const V3 rk = sphfsi::rotate(qof(b), c.S.body_frame_pos[r]);
+        const V3 u = v3(b.vel) + sphfsi::cross(v3(b.omega), rk);
+        const int tgt = c.P.mat[c.S.material[r]].melt_target;
+        c.S.kind[r] = Kind::Fluid;
+        c.S.material[r] = (uint16_t)tgt;
+        c.S.group[r] = 0;
+        c.S.vel[r] = u;
+        c.S.vel_adv[r] = u;
+        c.S.acc[r] = V3::zero();
+        c.S.acc_bg[r] = V3::zero();
+        c.S.density[r] = c.P.mat[tgt].rho0;
+        c.S.pressure[r] = 0.0;
+        c.S.body_frame_pos[r] = V3::zero();
+        c.force[r] = V3::zero();
+        affected[k] = 1;
+        lost[k] = 1;
+    }
+    // 2. solidification: attach to the body of the nearest pre-batch rigid particle within r_c
+    //    (ties by gid), else spawn; new ids ascending in gid (solid is gid-sorted).
+    const double rc2 = c.rc * c.rc;
+    std::vector<int64_t> target(solid.size(), -1);
+    for (size_t e = 0; e < solid.size(); ++e) {
+        const uint32_t i = solid[e];
+        double best = std::numeric_limits<double>::infinity();
+        int64_t bj = -1;
+        for (uint32_t j : c.nl[i]) {
+            if (c.S.kind[j] != Kind::Rigid || melting[j]) continue;
+            const double r2 = r2of(mi3(c, c.S.pos[i], c.S.pos[j]));
+            if (r2 > rc2) continue;
+            if (r2 < best || (r2 == best && (int64_t)j < bj)) { best = r2; bj = j; }
+        }
+        target[e] = bj >= 0 ? (int64_t)c.S.group[bj] : -1;
+    }
+    for (size_t e = 0; e < solid.size(); ++e) {
+        const uint32_t i = solid[e];
+        const int tgt = c.P.mat[c.S.material[i]].solidify_target;
+        uint32_t k;
+        if (target[e] >= 0) {
+            k = (uint32_t)target[e];
+        } else {
+            sphg_body nbd{};
+            nbd.q[0] = 1.0;
+            put3(nbd.vel, c.S.vel[i]);
+            nbd.material = tgt;
+            nbd.mobile = 1;
+            nbd.alive = 1;
+            c.bodies.push_back(nbd);
+            old.push_back(nbd);
+            k = (uint32_t)(c.bodies.size() - 1);
+            affected.push_back(1);
+            lost.push_back(0);
+        }
+        affected[k] = 1;
+        c.S.kind[i] = Kind::Rigid;
+        c.S.material[i] = (uint16_t)tgt;
+        c.S.group[i] = k;
+        c.S.density[i] = c.P.mat[tgt].rho0;
+        c.S.pressure[i] = 0.0;
+        c.S.acc[i] = V3::zero();
+        c.S.acc_bg[i] = V3::zero();
+    }
+    rebuild_members(c);
+    src_body.resize(c.bodies.size());
+    std::iota(src_body.begin(), src_body.end(), 0u);
+    // 3. split bodies that lost particles into connected components (adjacency <= 1.5 dx);
+    //    the component holding the min gid keeps the id, others get new ids by min gid.
+    const double adj2 = (1.5 * c.P.dx) * (1.5 * c.P.dx);
+    const size_t nb1 = c.bodies.size();
+    for (size_t k = 0; k < nb1; ++k) {
+        if (k >= lost.size() || !lost[k] || c.members[k].empty()) continue;
+        const auto mem = c.members[k];
+        std::vector<uint32_t> lab(mem.size());
+        std::iota(lab.begin(), lab.end(), 0u);
+        std::function<uint32_t(uint32_t)> find = [&](uint32_t x) {
+            while (lab[x] != x) { lab[x] = lab[lab[x]]; x = lab[x]; }
+            return x;
+        };
+        std::vector<int64_t> pos_in(n, -1);
+        for (size_t a = 0; a < mem.size(); ++a) pos_in[mem[a]] = (int64_t)a;
+        for (size_t a = 0; a < mem.size(); ++a)
+            for (uint32_t j : c.nl[mem[a]]) {
+                const int64_t b = pos_in[j];
+                if (b < 0) continue;
+                if (r2of(mi3(c, c.S.pos[mem[a]], c.S.pos[j])) > adj2) continue;
+                uint32_t ra = find((uint32_t)a), rb = find((uint32_t)b);
+                if (ra != rb) lab[std::max(ra, rb)] = std::min(ra, rb);  // root = min index = min gid
+            }
+        std::vector<uint32_t> roots;
+        for (size_t a = 0; a < mem.size(); ++a)
+            if (find((uint32_t)a) == a) roots.push_back((uint32_t)a);
+        if (roots.size() <= 1) continue;
+        // roots ascending = components ordered by min gid; roots[0] keeps id k
+        for (size_t q = 1; q < roots.size(); ++q) {
+            sphg_body nbd = c.bodies[k];
+            c.bodies.push_back(nbd);
+            const uint32_t nk = (uint32_t)(c.bodies.size() - 1);
+            src_body.push_back((uint32_t)k);
+            old.push_back(old[k]);
+            affected.push_back(1);
+            lost.push_back(0);
+            for (size_t a = 0; a < mem.size(); ++a)
+                if (find((uint32_t)a) == roots[q]) c.S.group[mem[a]] = nk;
+        }
+    }
+    rebuild_members(c);
+    // 4. mass quantities + post-transition velocity u_k = u'_k + w x (r_k - r'_k) [P12]
+    for (size_t k = 0; k < c.bodies.size(); ++k) {
+        if (k >= affected.size() || !affected[k]) continue;
+        const sphg_body& o = old[k];
+        // chi must be measured in the (unchanged) body orientation
+        mass_quantities(c, k);
+        sphg_body& b = c.bodies[k];
+        if (!b.alive) continue;
+        const bool spawned = (k >= nb0) && (src_body[k] == k);
+        if (!spawned) {
+            const V3 shift = mi3(c, v3(b.com), v3(o.com));
+            put3(b.vel, v3(o.vel) + sphfsi::cross(v3(o.omega), shift));
+        }
+        // particle velocities follow the body's rigid motion
+        for (uint32_t r : c.members[k]) {
+            const V3 rk = sphfsi::rotate(qof(b), c.S.body_frame_pos[r]);
+            const V3 u = v3(b.vel) + sphfsi::cross(v3(b.omega), rk);
+            c.S.vel[r] = u;
+            c.S.vel_adv[r] = u;
+        }
+    }
+    // 5. force/torque of the new membership (accelerations for the next kick)
+    return stage_bodies(c);
+}
+
+void resize_aux(Ctx& c) {
+    const size_t n = c.S.size();
+    c.force.assign(n, V3::zero());
+    c.rho_w.assign(n, 0.0);
+    c.V_w.assign(n, 0.0);
+    c.wall_mat.assign(n, 0);
+    c.acc_scale.assign(n, 0.0);
+    c.accbg_scale.assign(n, 0.0);
+    c.dT_scale.assign(n, 0.0);
+    c.force_scale.assign(n, 0.0);
+    c.rho_scale.assign(n, 0.0);
+}
+
+bool run_stage(Ctx& c, int s) {
+    if (s != SPHG_STAGE_REBUILD && s != SPHG_STAGE_KICK_DRIFT && s != SPHG_STAGE_MASS && !c.built)
+        if (!stage_rebuild(c)) return false;
+    switch (s) {
+        case SPHG_STAGE_REBUILD: return stage_rebuild(c);
+        case SPHG_STAGE_DENSITY: return stage_density(c);
+        case SPHG_STAGE_HEAT: return c.P.thermal ? stage_heat(c) : true;
+        case SPHG_STAGE_EXTRAPOLATE: return stage_extrapolate(c);
+        case SPHG_STAGE_FORCES: return stage_forces(c);
+        case SPHG_STAGE_BODIES: return stage_bodies(c);
+        case SPHG_STAGE_KICK_DRIFT: return stage_kick_drift(c);
+        case SPHG_STAGE_FINAL_KICK: return stage_final_kick(c);
+        case SPHG_STAGE_TRANSITIONS: return stage_transitions(c);
+        case SPHG_STAGE_MASS: return stage_mass(c);
+    }
+    return fail(c, "unknown stage");
+}
+
+bool one_step(Ctx& c) {
+    if (!stage_kick_drift(c)) return false;
+    const double half_skin = 0.5 * (c.rv - c.rc);
+    if (!c.built || c.max_disp > half_skin)  // SPEC:212 [P3]
+        if (!stage_rebuild(c)) return false;
+    if (!stage_density(c)) return false;
+    if (c.P.thermal && !stage_heat(c)) return false;
+    if (!stage_extrapolate(c)) return false;
+    if (!stage_forces(c)) return false;
+    if (!stage_bodies(c)) return false;
+    if (!stage_final_kick(c)) return false;
+    if (c.P.transitions == 1 && !stage_transitions(c)) return false;
+    c.steps++;
+    return true;
+}
+
+void copy3(std::vector<V3>& dst, const double* src, size_t n) {
+    dst.resize(n);
+    if (!src) { std::fill(dst.begin(), dst.end(), V3::zero()); return; }
+    for (size_t i = 0; i < n; ++i) dst[i] = V3{src[3 * i], src[3 * i + 1], src[3 * i + 2]};
+}
+template <class T>
+void copy1(std::vector<T>& dst, const T* src, size_t n, T dflt) {
+    dst.resize(n);
+    if (!src) { std::fill(dst.begin(), dst.end(), dflt); return; }
+    std::copy(src, src + n, dst.begin());
+}
+void out3(double* dst, const std::vector<V3>& src) {
+    if (!dst) return;
+    for (size_t i = 0; i < src.size(); ++i) put3(dst + 3 * i, src[i]);
+}
+template <class T>
+void out1(T* dst, const std::vector<T>& src) {
+    if (dst) std::copy(src.begin(), src.end(), dst);
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+struct orc_ctx;
+
+int orc_validate(const sphg_params* p, char* buf, size_t len) {
+    const auto v = validate(*p);
+    std::string s;
+    for (size_t i = 0; i < v.size(); ++i) s += (i ? "\n" : "") + v[i];
+    if (buf && len) {
+        std::strncpy(buf, s.c_str(), len - 1);
+        buf[len - 1] = 0;
+    }
+    return v.empty() ? SPHG_OK : SPHG_ERR_CONFIG;
+}
+
+int orc_create(const sphg_params* p, int /*device*/, orc_ctx** out) {
+    *out = nullptr;
+    const auto v = validate(*p);
+    if (!v.empty()) return SPHG_ERR_CONFIG;
+    Ctx* c = new Ctx();
+    c->P = *p;
+    if (c->P.h <= 0.0) c->P.h = c->P.dx;
+    c->mats = to_config(c->P).materials;
+    setup_geometry(*c);
+    c->t = c->P.t0;
+    *out = reinterpret_cast<orc_ctx*>(c);
+    return SPHG_OK;
+}
+
+int orc_upload(orc_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t nb) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    const size_t n = s->n;
+    auto& S = c.S;
+    copy3(S.pos, s->pos, n);
+    copy3(S.vel, s->vel, n);
+    copy3(S.vel_adv, s->vel_adv, n);
+    copy3(S.acc, s->acc, n);
+    copy3(S.acc_bg, s->acc_bg, n);
+    copy1(S.density, s->density, n, 0.0);
+    copy1(S.pressure, s->pressure, n, 0.0);
+    copy1(S.mass, s->mass, n, 0.0);
+    copy1(S.temperature, s->temperature, n, 0.0);
+    copy1(S.dT_dt, s->dT_dt, n, 0.0);
+    S.concentration.assign(n, 0.0);
+    S.dC_dt.assign(n, 0.0);
+    S.kind.resize(n);
+    for (size_t i = 0; i < n; ++i) S.kind[i] = static_cast<Kind>(s->kind[i]);
+    copy1(S.group, s->group, n, 0u);
+    copy1(S.material, s->material, n, (uint16_t)0);
+    copy3(S.body_frame_pos, s->body_frame_pos, n);
+    copy1(S.wall_pressure, s->wall_pressure, n, 0.0);
+    copy3(S.wall_velocity, s->wall_velocity, n);
+    copy1(S.dirichlet_T, s->dirichlet_T, n, (uint8_t)0xff);
+    S.dirichlet_C.assign(n, 0xff);
+    S.owner.assign(n, 0);
+    resize_aux(c);
+    if (s->force) copy3(c.force, s->force, n);
+    c.bodies.assign(bodies, bodies + nb);
+    c.body_fscale.assign(nb, 0.0);
+    c.body_tscale.assign(nb, 0.0);
+    rebuild_members(c);
+    c.built = false;
+    return SPHG_OK;
+}
+
+int orc_run_stage(orc_ctx* h, int stage) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    return run_stage(c, stage) ? SPHG_OK : SPHG_ERR_RUNTIME;
+}
+
+int orc_initialize(orc_ctx* h) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    for (int s : {SPHG_STAGE_REBUILD, SPHG_STAGE_DENSITY, SPHG_STAGE_EXTRAPOLATE, SPHG_STAGE_FORCES, SPHG_STAGE_BODIES})
+        if (!run_stage(c, s)) return SPHG_ERR_RUNTIME;
+    return SPHG_OK;
+}
+
+int orc_step(orc_ctx* h, int nsteps) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    for (int k = 0; k < nsteps; ++k)
+        if (!one_step(c)) return SPHG_ERR_RUNTIME;
+    return SPHG_OK;
+}
+
+int orc_download(orc_ctx* h, sphg_soa* o, sphg_body* bodies, size_t* nb) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    const auto& S = c.S;
+    out3(o->pos, S.pos);
+    out3(o->vel, S.vel);
+    out3(o->vel_adv, S.vel_adv);
+    out3(o->acc, S.acc);
+    out3(o->acc_bg, S.acc_bg);
+    out1(o->density, S.density);
+    out1(o->pressure, S.pressure);
+    out1(o->mass, S.mass);
+    out1(o->temperature, S.temperature);
+    out1(o->dT_dt, S.dT_dt);
+    if (o->kind)
+        for (size_t i = 0; i < S.size(); ++i) o->kind[i] = static_cast<uint8_t>(S.kind[i]);
+    out1(o->group, S.group);
+    out1(o->material, S.material);
+    out3(o->body_frame_pos, S.body_frame_pos);
+    out1(o->wall_pressure, S.wall_pressure);
+    out3(o->wall_velocity, S.wall_velocity);
+    out1(o->dirichlet_T, S.dirichlet_T);
+    out3(o->force, c.force);
+    if (nb) {
+        if (bodies) {
+            const size_t m = std::min(*nb, c.bodies.size());
+            std::copy(c.bodies.begin(), c.bodies.begin() + m, bodies);
+        }
+        *nb = c.bodies.size();
+    }
+    return SPHG_OK;
+}
+
+int orc_num_bodies(orc_ctx* h, size_t* nb) {
+    *nb = reinterpret_cast<Ctx*>(h)->bodies.size();
+    return SPHG_OK;
+}
+
+int orc_get_cells(orc_ctx* h, int64_t* cell_of_gid, uint32_t* sorted_gid) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (!c.built && !stage_rebuild(c)) return SPHG_ERR_RUNTIME;
+    if (cell_of_gid) std::copy(c.cell_of.begin(), c.cell_of.end(), cell_of_gid);
+    if (sorted_gid) std::copy(c.sorted.begin(), c.sorted.end(), sorted_gid);
+    return SPHG_OK;
+}
+
+int orc_get_nlist(orc_ctx* h, int64_t* offsets, uint32_t* nbr) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (!c.built && !stage_rebuild(c)) return SPHG_ERR_RUNTIME;
+    int64_t o = 0;
+    for (size_t i = 0; i < c.nl.size(); ++i) {
+        if (offsets) offsets[i] = o;
+        if (nbr) std::copy(c.nl[i].begin(), c.nl[i].end(), nbr + o);
+        o += (int64_t)c.nl[i].size();
+    }
+    if (offsets) offsets[c.nl.size()] = o;
+    return SPHG_OK;
+}
+
+// tolerance scales, gid order
+int orc_get_scales(orc_ctx* h, double* acc, double* accbg, double* dT, double* force, double* rho, double* body_f,
+                   double* body_t) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    out1(acc, c.acc_scale);
+    out1(accbg, c.accbg_scale);
+    out1(dT, c.dT_scale);
+    out1(force, c.force_scale);
+    out1(rho, c.rho_scale);
+    out1(body_f, c.body_fscale);
+    out1(body_t, c.body_tscale);
+    return SPHG_OK;
+}
+
+int orc_stats(orc_ctx* h, sphg_stats_t* s) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    std::memset(s, 0, sizeof(*s));
+    s->steps = c.steps;
+    s->rebuilds = c.rebuilds;
+    int64_t np = 0;
+    int mx = 0;
+    for (auto& l : c.nl) { np += (int64_t)l.size(); mx = std::max(mx, (int)l.size()); }
+    s->n_pairs_candidate = np;
+    s->max_neighbours = mx;
+    s->transitions_melt = c.n_melt;
+    s->transitions_solidify = c.n_solid;
+    for (auto& b : c.bodies) s->bodies_alive += b.alive ? 1 : 0;
+    for (int a = 0; a < 3; ++a) s->cells[a] = c.ncell[a];
+    s->time = c.t;
+    s->max_displacement = c.max_disp;
+    s->u_max = c.u_max;
+    return SPHG_OK;
+}
+
+const char* orc_last_error(const orc_ctx* h) { return reinterpret_cast<const Ctx*>(h)->err.c_str(); }
+void orc_destroy(orc_ctx* h) { delete reinterpret_cast<Ctx*>(h); }
+
+// ---------------- KAT helpers: the reference's own building blocks, unchanged
+double orc_kernel_w(double h, double r) { return sphfsi::QuinticKernel<3>(h).w(r); }
+double orc_kernel_dw(double h, double r) { return sphfsi::QuinticKernel<3>(h).dw_dr(r); }
+double orc_kernel_sigma(double h) { return sphfsi::QuinticKernel<3>::sigma(h); }
+double orc_eos_pressure(double rho, double rho0, double c) {
+    sphfsi::Material m;
+    m.reference_density = rho0;
+    m.speed_of_sound = c;
+    return sphfsi::eos_pressure(rho, m);
+}
+void orc_orientation_step(const double q[4], const double w[3], double dt, double out[4]) {
+    const sphfsi::Quaternion r = sphfsi::orientation_step<3>({q[0], q[1], q[2], q[3]}, V3{w[0], w[1], w[2]}, dt);
+    out[0] = r.w; out[1] = r.x; out[2] = r.y; out[3] = r.z;
+}
+void orc_rotate(const double q[4], const double v[3], double out[3]) {
+    put3(out, sphfsi::rotate({q[0], q[1], q[2], q[3]}, V3{v[0], v[1], v[2]}));
+}
+double orc_kahan_sum(const double* x, size_t n) {
+    sphfsi::KahanSum s;
+    for (size_t i = 0; i < n; ++i) s.add(x[i]);
+    return s.value();
+}
+double orc_particle_inertia(double m, double dx) { return particle_inertia(m, dx); }
+// lattice.hpp seed_lattice over a box or ball; returns the count, writes up to cap points
+size_t orc_seed_lattice_box(const double lo[3], const double hi[3], double dx, double* out, size_t cap) {
+    sphfsi::ParticleStore<3> s;
+    sphfsi::Box<3> b;
+    for (int a = 0; a < 3; ++a) { b.lo[a] = lo[a]; b.hi[a] = hi[a]; }
+    sphfsi::Material m;
+    sphfsi::seed_lattice<3>(s, sphfsi::box_region<3>(b), dx, {Kind::Fluid, 0}, 0, m);
+    for (size_t i = 0; i < s.size() && i < cap; ++i) put3(out + 3 * i, s.pos[i]);
+    return s.size();
+}
+size_t orc_seed_lattice_ball(const double center[3], double diameter, double dx, double* out, size_t cap) {
+    sphfsi::ParticleStore<3> s;
+    sphfsi::Material m;
+    sphfsi::seed_lattice<3>(s, sphfsi::ball_region<3>(V3{center[0], center[1], center[2]}, diameter), dx,
+                            {Kind::Rigid, 0}, 0, m);
+    for (size_t i = 0; i < s.size() && i < cap; ++i) put3(out + 3 * i, s.pos[i]);
+    return s.size();
+}
+size_t orc_sizeof_params(void) { return sizeof(sphg_params); }
+size_t orc_sizeof_body(void) { return sizeof(sphg_body); }
+size_t orc_sizeof_soa(void) { return sizeof(sphg_soa); }
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+"""ctypes mirror of include/sphg.h (the C ABI of the hot path).
+
+Struct layouts must match the header exactly; tests/test_abi.py checks the
+sizes against the compiled libraries.
+"""
+import ctypes as C
+
+MAX_MAT = 8
+MAX_DIRICHLET = 8
+MAX_PIECES = 8
+NO_MATERIAL = -1
+NO_DIRICHLET = 0xFF
+
+FLUID, RIGID, BOUNDARY = 0, 1, 2  # store.hpp:11 Kind
+
+OK, ERR_CONFIG, ERR_RUNTIME, ERR_CUDA = 0, 2, 3, 4
+
+STAGE_REBUILD = 0
+STAGE_DENSITY = 1
+STAGE_HEAT = 2
+STAGE_EXTRAPOLATE = 3
+STAGE_FORCES = 4
+STAGE_BODIES = 5
+STAGE_KICK_DRIFT = 6
+STAGE_FINAL_KICK = 7
+STAGE_TRANSITIONS = 8
+STAGE_MASS = 9
+
+STAGE_NAMES = ["rebuild", "density", "heat", "extrapolate", "forces", "bodies",
+               "kick_drift", "final_kick", "transitions", "mass"]
+
+
+class Material(C.Structure):
+    """sphfsi::Material (material.hpp:17-36) + per-material body force (config.hpp:79)."""
+    _fields_ = [("rho0", C.c_double), ("nu", C.c_double), ("cp", C.c_double),
+                ("kappa", C.c_double), ("c", C.c_double), ("pb", C.c_double),
+                ("T_t", C.c_double), ("melt_target", C.c_int32),
+                ("solidify_target", C.c_int32), ("body_force", C.c_double * 3)]
+
+
+class Schedule(C.Structure):
+    """sphfsi::Schedule (config.hpp:20-33)."""
+    _fields_ = [("n", C.c_int32), ("pad", C.c_int32),
+                ("t_end", C.c_double * MAX_PIECES), ("value", C.c_double * MAX_PIECES)]
+
+
+class Params(C.Structure):
+    """Flat POD of sphfsi::ScenarioConfig<3> (config.hpp:68-106)."""
+    _fields_ = [("dx", C.c_double), ("h", C.c_double), ("dt", C.c_double), ("t0", C.c_double),
+                ("lo", C.c_double * 3), ("hi", C.c_double * 3),
+                ("periodic", C.c_int32 * 3), ("n_mat", C.c_int32),
+                ("cell_edge_override", C.c_double),
+                ("mat", Material * MAX_MAT),
+                ("kc", C.c_double), ("dc", C.c_double),
+                ("tvf", C.c_int32), ("thermal", C.c_int32), ("transitions", C.c_int32),
+                ("n_dirichlet", C.c_int32),
+                ("dirichlet_T", Schedule * MAX_DIRICHLET),
+                ("default_fluid_mat", C.c_int32), ("nlist_capacity", C.c_int32),
+                ("rank", C.c_int32), ("nranks", C.c_int32)]
+
+
+_dp = C.POINTER(C.c_double)
+
+
+class SoA(C.Structure):
+    """Host views of a ParticleStore<3> (store.hpp:26-46), gid order."""
+    _fields_ = [("n", C.c_size_t),
+                ("pos", _dp), ("vel", _dp), ("vel_adv", _dp), ("acc", _dp), ("acc_bg", _dp),
+                ("density", _dp), ("pressure", _dp), ("mass", _dp), ("temperature", _dp),
+                ("dT_dt", _dp),
+                ("kind", C.POINTER(C.c_uint8)), ("group", C.POINTER(C.c_uint32)),
+                ("material", C.POINTER(C.c_uint16)),
+                ("body_frame_pos", _dp), ("wall_pressure", _dp), ("wall_velocity", _dp),
+                ("dirichlet_T", C.POINTER(C.c_uint8)), ("force", _dp)]
+
+
+class Body(C.Structure):
+    """RigidBody."""
+    _fields_ = [("mass", C.c_double), ("com", C.c_double * 3), ("inertia", C.c_double * 6),
+                ("q", C.c_double * 4), ("vel", C.c_double * 3), ("omega", C.c_double * 3),
+                ("force", C.c_double * 3), ("torque", C.c_double * 3),
+                ("acc", C.c_double * 3), ("alpha", C.c_double * 3),
+                ("material", C.c_int32), ("mobile", C.c_int32), ("alive", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("rebuilds", C.c_int64), ("n_pairs_candidate", C.c_int64),
+                ("transitions_melt", C.c_int64), ("transitions_solidify", C.c_int64),
+                ("bodies_alive", C.c_int64), ("nlist_capacity", C.c_int32),
+                ("max_neighbours", C.c_int32), ("cells", C.c_int32 * 3), ("pad", C.c_int32),
+                ("time", C.c_double), ("max_displacement", C.c_double), ("u_max", C.c_double),
+                ("stage_ms", C.c_double * 10), ("kernel_launches", C.c_int64)]
+
+
+def declare(lib, prefix):
+    """Attach argtypes/restypes for the sphg_* (or orc_*) entry points."""
+    vp = C.c_void_p
+    sig = {
+        "create": (C.c_int, [C.POINTER(Params), C.c_int, C.POINTER(vp)]),
+        "upload": (C.c_int, [vp, C.POINTER(SoA), C.POINTER(Body), C.c_size_t]),
+        "initialize": (C.c_int, [vp]),
+        "step": (C.c_int, [vp, C.c_int]),
+        "run_stage": (C.c_int, [vp, C.c_int]),
+        "download": (C.c_int, [vp, C.POINTER(SoA), C.POINTER(Body), C.POINTER(C.c_size_t)]),
+        "get_cells": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_uint32)]),
+        "get_nlist": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_uint32)]),
+        "stats": (C.c_int, [vp, C.POINTER(Stats)]),
+        "num_bodies": (C.c_int, [vp, C.POINTER(C.c_size_t)]),
+        "last_error": (C.c_char_p, [vp]),
+        "destroy": (None, [vp]),
+        "validate": (C.c_int, [C.POINTER(Params), C.c_char_p, C.c_size_t]),
+    }
+    optional = {
+        "set_timing": (C.c_int, [vp, C.c_int]),
+        "compute_dt": (C.c_int, [vp, C.POINTER(C.c_double)]),
+    }
+    for name, (res, args) in list(sig.items()) + list(optional.items()):
+        fn = getattr(lib, prefix + name, None)
+        if fn is None:
+            if name in optional:
+                continue
+            raise ImportError(f"{prefix}{name} missing from {lib._name}")
+        fn.restype = res
+        fn.argtypes = args
+    return lib

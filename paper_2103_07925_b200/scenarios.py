@@ -1,0 +1,393 @@
+"""Seeded synthetic scenarios for the BASELINE.json configs (inputs only; untimed).
+
+The reference publishes no dataset: BASELINE.json's configs *are* the inputs.
+Positions follow the lattice convention of the reference's seed_lattice /
+for_each_lattice_point (lattice.hpp:38-82: points at lo + (k + 1/2) dx, last
+axis fastest, mass rho0 dx^3); tests/test_oracle_pins.py checks the generator
+against the reference's own seed_lattice bit for bit.  Random numbers come from
+a counter-based SplitMix64 (53-bit mantissa mapping), so the same arrays are
+produced on any host and are uploaded identically to the GPU and the oracle
+(SURVEY App. A13).  Streams: 0 jitter, 1 velocities, 2 body placement,
+3 temperatures.
+
+Pinned choices for under-specified configs are listed in DESIGN.md §6.
+"""
+from dataclasses import dataclass, field
+import math
+
+import numpy as np
+
+from . import abi
+from .store import ParticleStore, empty_bodies
+
+_GAMMA = np.uint64(0x9E3779B97F4A7C15)
+_STREAM = np.uint64(0xD1B54A32D192ED03)
+
+
+def splitmix_u01(seed, stream, idx):
+    """Counter-based SplitMix64 -> uniform [0,1) with 53-bit mantissa."""
+    idx = np.asarray(idx, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        base = np.array([seed], np.uint64) ^ (np.array([stream], np.uint64) * _STREAM)
+        z = base + (idx + np.uint64(1)) * _GAMMA
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
+def lattice_counts(lo, hi, dx):
+    """Points per axis, restating for_each_lattice_point (lattice.hpp:43-52)."""
+    n = []
+    for a in range(3):
+        ext = hi[a] - lo[a]
+        if ext < 0.0:
+            return [0, 0, 0]
+        k = int(math.floor(ext / dx + 1e-12))
+        if lo[a] + (0.5 + float(k)) * dx > hi[a] + 1e-9 * dx:
+            k -= 1
+        k += 1
+        if k <= 0:
+            return [0, 0, 0]
+        n.append(k)
+    return n
+
+
+def lattice_box(lo, hi, dx):
+    """All lattice points of a box, lexicographic (last axis fastest) — lattice.hpp:53-65."""
+    n = lattice_counts(lo, hi, dx)
+    if min(n) <= 0:
+        return np.zeros((0, 3))
+    axes = [lo[a] + (0.5 + np.arange(n[a], dtype=np.float64)) * dx for a in range(3)]
+    g = np.meshgrid(*axes, indexing="ij")
+    return np.stack([g[0].ravel(), g[1].ravel(), g[2].ravel()], axis=1)
+
+
+def material(rho0, nu=0.0, cp=0.0, kappa=0.0, c=0.0, pb=0.0, T_t=float("nan"),
+             melt=-1, solidify=-1, g=(0.0, 0.0, 0.0)):
+    m = abi.Material()
+    m.rho0, m.nu, m.cp, m.kappa, m.c, m.pb, m.T_t = rho0, nu, cp, kappa, c, pb, T_t
+    m.melt_target, m.solidify_target = melt, solidify
+    for a in range(3):
+        m.body_force[a] = g[a]
+    return m
+
+
+@dataclass
+class Scenario:
+    name: str
+    params: abi.Params
+    store: ParticleStore
+    bodies: np.ndarray
+    steps: int
+    info: dict = field(default_factory=dict)
+
+
+def _params(dx, dt, lo, hi, periodic, mats, kc=0.0, dc=0.0, tvf=1, thermal=0, transitions=0):
+    p = abi.Params()
+    p.dx, p.h, p.dt, p.t0 = dx, dx, dt, 0.0
+    for a in range(3):
+        p.lo[a], p.hi[a], p.periodic[a] = lo[a], hi[a], int(periodic[a])
+    p.n_mat = len(mats)
+    for i, m in enumerate(mats):
+        p.mat[i] = m
+    p.kc, p.dc, p.tvf, p.thermal, p.transitions = kc, dc, tvf, thermal, transitions
+    p.default_fluid_mat = 0
+    p.nranks = 1
+    return p
+
+
+def damping_from_ratio(zeta, kc, m_r):
+    """d_c = 2 zeta sqrt(k_c m_eff), m_eff = m_r/2 for equal rigid particles."""
+    return 2.0 * zeta * math.sqrt(kc * 0.5 * m_r)
+
+
+def place_spheres(seed, n_spheres, lo, L, r_lo, r_hi, dx, periodic=True, max_tries=None):
+    """Rejection-sampled non-overlapping spheres: (periodic) centre distance > R1+R2+dx.
+
+    Candidates are consumed in order from stream 2 (4 draws each: x, y, z, radius).
+    """
+    lo = np.asarray(lo, float)
+    L = np.asarray(L, float)
+    rmax = r_hi * dx
+    cell = 2.0 * rmax + dx
+    ng = np.maximum(1, np.floor(L / cell).astype(int))
+    grid = {}
+    centers, radii = [], []
+    tries = 0
+    max_tries = max_tries or 50 * n_spheres + 1000
+    batch = 8192
+    while len(centers) < n_spheres and tries < max_tries:
+        u = splitmix_u01(seed, 2, np.arange(4 * tries, 4 * (tries + batch), dtype=np.uint64)).reshape(batch, 4)
+        for k in range(batch):
+            tries += 1
+            c = lo + u[k, :3] * L
+            R = (r_lo + u[k, 3] * (r_hi - r_lo)) * dx
+            if not periodic:
+                if np.any(c - R < lo + dx) or np.any(c + R > lo + L - dx):
+                    continue
+            gi = np.floor((c - lo) / L * ng).astype(int) % ng
+            ok = True
+            for ox in (-1, 0, 1):
+                for oy in (-1, 0, 1):
+                    for oz in (-1, 0, 1):
+                        key = tuple((gi + (ox, oy, oz)) % ng)
+                        for s in grid.get(key, ()):
+                            d = c - centers[s]
+                            if periodic:
+                                d = d - L * np.round(d / L)
+                            if d @ d <= (R + radii[s] + dx) ** 2:
+                                ok = False
+                                break
+                        if not ok:
+                            break
+                    if not ok:
+                        break
+                if not ok:
+                    break
+            if ok:
+                grid.setdefault(tuple(gi), []).append(len(centers))
+                centers.append(c)
+                radii.append(R)
+                if len(centers) == n_spheres:
+                    break
+    return np.array(centers).reshape(-1, 3), np.array(radii)
+
+
+def mark_spheres(nlat, lo, dx, L, centers, radii, periodic):
+    """Body id (or -1) per lattice point (lattice order) for points inside a sphere.
+
+    Membership is tested on the unjittered lattice point with the minimum-image
+    distance, |d|^2 = (dx^2 + dy^2) + dz^2 <= R^2 (ball_region, lattice.hpp:28-36).
+    """
+    nx, ny, nz = nlat
+    owner = np.full(nx * ny * nz, -1, np.int64)
+    for k, (c, R) in enumerate(zip(centers, radii)):
+        idx = []
+        for a, na in enumerate(nlat):
+            i0 = int(math.floor((c[a] - R - lo[a]) / dx - 0.5)) - 1
+            i1 = int(math.ceil((c[a] + R - lo[a]) / dx - 0.5)) + 1
+            ii = np.arange(i0, i1 + 1)
+            if periodic[a]:
+                ii = np.unique(ii % na)
+            else:
+                ii = ii[(ii >= 0) & (ii < na)]
+            idx.append(ii)
+        gx, gy, gz = np.meshgrid(*idx, indexing="ij")
+        gx, gy, gz = gx.ravel(), gy.ravel(), gz.ravel()
+        p = np.stack([lo[a] + (0.5 + g.astype(np.float64)) * dx for a, g in enumerate((gx, gy, gz))], 1)
+        d = p - c
+        for a in range(3):
+            if periodic[a]:
+                d[:, a] -= L[a] * np.round(d[:, a] / L[a])
+        inside = ((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]) <= R * R
+        lin = ((gx * ny + gy) * nz + gz)[inside]
+        owner[lin] = k
+    return owner
+
+
+def particle_inertia(m, dx):
+    reff = (0.75 / math.pi) ** (1.0 / 3.0) * dx
+    return 0.4 * m * reff * reff
+
+
+def body_quantities(store, bodies, params):
+    """reduce_mass_quantities on the host for the initial state; sets chi (Remark 3.7)."""
+    L = np.array([params.hi[a] - params.lo[a] for a in range(3)])
+    per = np.array([params.periodic[a] for a in range(3)], bool)
+    rig = np.nonzero(store.kind == abi.RIGID)[0]
+    if len(rig) == 0:
+        return
+    order = rig[np.lexsort((rig, store.group[rig]))]
+    grp = store.group[order].astype(np.int64)
+    starts = np.r_[0, np.nonzero(np.diff(grp))[0] + 1]
+    anchor = np.repeat(store.pos[order[starts]], np.diff(np.r_[starts, len(order)]), axis=0)
+
+    def mimg(d):
+        d = d.copy()
+        for a in range(3):
+            if per[a]:
+                d[:, a] -= L[a] * np.round(d[:, a] / L[a])
+        return d
+
+    m = store.mass[order]
+    rel = mimg(store.pos[order] - anchor)
+    M = np.add.reduceat(m, starts)
+    com = store.pos[order[starts]] + np.add.reduceat(m[:, None] * rel, starts, axis=0) / M[:, None]
+    for a in range(3):
+        if per[a]:
+            lo, hi = params.lo[a], params.hi[a]
+            com[:, a] = np.where(com[:, a] < lo, com[:, a] + L[a], np.where(com[:, a] >= hi, com[:, a] - L[a], com[:, a]))
+    comp = np.repeat(com, np.diff(np.r_[starts, len(order)]), axis=0)
+    d = mimg(store.pos[order] - comp)
+    Ir = particle_inertia(m, params.dx)
+    d2 = (d[:, 0] ** 2 + d[:, 1] ** 2) + d[:, 2] ** 2
+    I6 = np.stack([Ir + m * (d2 - d[:, 0] ** 2), Ir + m * (d2 - d[:, 1] ** 2), Ir + m * (d2 - d[:, 2] ** 2),
+                   -m * d[:, 0] * d[:, 1], -m * d[:, 0] * d[:, 2], -m * d[:, 1] * d[:, 2]], 1)
+    ids = grp[starts]
+    bodies["mass"][ids] = M
+    bodies["com"][ids] = com
+    bodies["inertia"][ids] = np.add.reduceat(I6, starts, axis=0)
+    store.body_frame_pos[order] = d  # q = identity at setup
+
+
+def _finish(store, bodies):
+    rig = store.kind == abi.RIGID
+    store.vel[rig] = 0.0
+    store.vel_adv[:] = store.vel
+    return store, bodies
+
+
+def periodic_spheres(nside=32, n_spheres=4, r_range=(4.0, 4.0), dx=1e-3, dt=1e-5, seed=2103,
+                     rho_f=1000.0, c=10.0, eta=1e-3, rho_s=2000.0, kc=1e3, zeta=0.1, u0=0.01,
+                     jitter=0.05, name="c1", steps=100):
+    """BASELINE configs[0] (C1: 32^3, 4 spheres R=4dx) and configs[4] (C5: 400^3, ~20k spheres R~U[3,6]dx).
+
+    Periodic cube, lattice + uniform jitter, fluid u ~ U(-u0, u0), spheres
+    relabelled rigid (mass rho_s dx^3), linear EOS (material.hpp:59-62; BASELINE
+    says 'Tait'), p_b = p0 = rho0 c^2.
+    """
+    L = nside * dx
+    lo, hi = (0.0, 0.0, 0.0), (L, L, L)
+    p0 = rho_f * c * c
+    mats = [material(rho_f, nu=eta / rho_f, c=c, pb=p0),   # 0 fluid
+            material(rho_s, c=0.0)]                          # 1 solid
+    m_r = rho_s * dx ** 3
+    params = _params(dx, dt, lo, hi, (1, 1, 1), mats, kc=kc, dc=damping_from_ratio(zeta, kc, m_r))
+    pos = lattice_box(lo, hi, dx)
+    n = len(pos)
+    centers, radii = place_spheres(seed, n_spheres, lo, (L, L, L), r_range[0], r_range[1], dx, True)
+    owner = mark_spheres((nside,) * 3, lo, dx, (L, L, L), centers, radii, (True, True, True))
+    s = ParticleStore(n)
+    u = splitmix_u01(seed, 0, np.arange(3 * n, dtype=np.uint64)).reshape(n, 3)
+    pos = pos + (2.0 * u - 1.0) * (jitter * dx)
+    pos = np.where(pos < 0.0, pos + L, np.where(pos >= L, pos - L, pos))
+    s.pos[:] = pos
+    v = splitmix_u01(seed, 1, np.arange(3 * n, dtype=np.uint64)).reshape(n, 3)
+    s.vel[:] = (2.0 * v - 1.0) * u0
+    rig = owner >= 0
+    s.kind[:] = abi.FLUID
+    s.kind[rig] = abi.RIGID
+    s.group[rig] = owner[rig].astype(np.uint32)
+    s.material[rig] = 1
+    s.mass[:] = rho_f * dx ** 3
+    s.mass[rig] = rho_s * dx ** 3
+    s.density[:] = rho_f
+    s.density[rig] = rho_s
+    bodies = empty_bodies(len(centers))
+    bodies["material"] = 1
+    body_quantities(s, bodies, params)
+    _finish(s, bodies)
+    info = dict(n=n, n_fluid=int((~rig).sum()), n_rigid=int(rig.sum()), n_boundary=0,
+                n_bodies=len(centers), rigid_fraction=float(rig.mean()))
+    return Scenario(name, params, s, bodies, steps, info)
+
+
+def config1(**kw):
+    """BASELINE configs[0]: 32^3 periodic, 4 spheres R=4dx, dt=1e-5, 100 steps."""
+    kw.setdefault("name", "c1")
+    return periodic_spheres(**kw)
+
+
+def config5(nside=400, n_spheres=20000, **kw):
+    """BASELINE configs[4]: 400^3 = 64M periodic, ~20k spheres R~U[3,6]dx (App. B8: sphere count kept)."""
+    kw.setdefault("name", "c5")
+    kw.setdefault("steps", 100)
+    return periodic_spheres(nside=nside, n_spheres=n_spheres, r_range=(3.0, 6.0), **kw)
+
+
+def closed_box_melting(nside=64, dx=1e-3, dt=5e-6, seed=2107, n_grid=3, r_range=(3.0, 6.0),
+                       T0=300.0, T_hot=1800.0, T_t=1700.0, rho=7900.0, c=20.0, nu=1e-6, cp=700.0,
+                       kappa=20.0, g=-9.81, kc=10.0, zeta=0.1, jitter=0.05, melt_forcing=False,
+                       name="c2", steps=500):
+    """BASELINE configs[1] (C2): closed box, 3-layer walls, 27 spheres on a jittered 3x3x3 grid.
+
+    Materials: 0 carrier liquid (no transition),
+    1 solid metal (T_t, melts into 2), 2 melt liquid (T_t, solidifies into 1),
+    3 wall.  Bottom wall = Dirichlet group 0 at T_hot.  melt_forcing=True is
+    the parity variant of App. B5: sphere temperatures ~ U[T_t-5, T_t+5] and a
+    melt-liquid layer at the same temperatures, so flags flip at step 1.
+    """
+    L = nside * dx
+    nl = 3  # wall_layers = floor(r_c/dx) (config.hpp:105)
+    lo = (-nl * dx,) * 3
+    hi = (L + nl * dx,) * 3
+    p0 = rho * c * c
+    grav = (0.0, 0.0, g)
+    mats = [material(rho, nu=nu, cp=cp, kappa=kappa, c=c, pb=p0, g=grav),                        # 0 carrier
+            material(rho, cp=cp, kappa=kappa, c=c, T_t=T_t, melt=2, g=grav),                     # 1 solid
+            material(rho, nu=nu, cp=cp, kappa=kappa, c=c, pb=p0, T_t=T_t, solidify=1, g=grav),  # 2 melt
+            material(rho, cp=cp, kappa=kappa, c=c)]                                               # 3 wall
+    m_r = rho * dx ** 3
+    params = _params(dx, dt, lo, hi, (0, 0, 0), mats, kc=kc, dc=damping_from_ratio(zeta, kc, m_r),
+                     thermal=1, transitions=1)
+    params.n_dirichlet = 1
+    params.dirichlet_T[0].n = 1
+    params.dirichlet_T[0].t_end[0] = 1e30
+    params.dirichlet_T[0].value[0] = T_hot
+    fl = lattice_box((0.0,) * 3, (L,) * 3, dx)
+    wl = lattice_box(lo, hi, dx)
+    outside = np.any((wl < 0.0) | (wl > L), axis=1)
+    wl = wl[outside]
+    nf, nw = len(fl), len(wl)
+    # spheres on a jittered grid
+    ug = splitmix_u01(seed, 2, np.arange(4 * n_grid ** 3, dtype=np.uint64)).reshape(-1, 4)
+    centers, radii = [], []
+    sp = L / n_grid
+    k = 0
+    for i in range(n_grid):
+        for j in range(n_grid):
+            for l in range(n_grid):
+                c0 = np.array([(i + 0.5) * sp, (j + 0.5) * sp, (l + 0.5) * sp])
+                centers.append(c0 + (2.0 * ug[k, :3] - 1.0) * 2.0 * dx)
+                radii.append((r_range[0] + ug[k, 3] * (r_range[1] - r_range[0])) * dx)
+                k += 1
+    centers, radii = np.array(centers), np.array(radii)
+    owner = mark_spheres((nside,) * 3, (0.0,) * 3, dx, (L,) * 3, centers, radii, (False,) * 3)
+    n = nf + nw
+    s = ParticleStore(n)
+    u = splitmix_u01(seed, 0, np.arange(3 * nf, dtype=np.uint64)).reshape(nf, 3)
+    s.pos[:nf] = fl + (2.0 * u - 1.0) * (jitter * dx)
+    s.pos[nf:] = wl
+    rig = np.zeros(n, bool)
+    rig[:nf] = owner >= 0
+    s.kind[:nf] = abi.FLUID
+    s.kind[nf:] = abi.BOUNDARY
+    s.kind[rig] = abi.RIGID
+    s.group[rig] = owner[owner >= 0].astype(np.uint32)
+    s.material[:nf] = 0
+    s.material[rig] = 1
+    s.material[nf:] = 3
+    s.mass[:] = rho * dx ** 3
+    s.density[:] = rho
+    s.temperature[:] = T0
+    bottom = np.zeros(n, bool)
+    bottom[nf:] = wl[:, 2] < 0.0
+    s.dirichlet_T[bottom] = 0
+    s.temperature[bottom] = T_hot
+    if melt_forcing:
+        tu = splitmix_u01(seed, 3, np.arange(n, dtype=np.uint64))
+        Tf = (T_t - 5.0) + 10.0 * tu
+        s.temperature[rig] = Tf[rig]
+        band = np.zeros(n, bool)
+        band[:nf] = (fl[:, 2] > 0.35 * L) & (fl[:, 2] < 0.65 * L)
+        band &= s.kind == abi.FLUID
+        s.material[band] = 2
+        s.temperature[band] = Tf[band]
+        s.temperature[(s.kind == abi.FLUID) & ~band] = T_t
+    bodies = empty_bodies(len(centers))
+    bodies["material"] = 1
+    body_quantities(s, bodies, params)
+    _finish(s, bodies)
+    info = dict(n=n, n_fluid=int((s.kind == abi.FLUID).sum()), n_rigid=int(rig.sum()), n_boundary=nw,
+                n_bodies=len(centers), rigid_fraction=float(rig.mean()))
+    return Scenario(name, params, s, bodies, steps, info)
+
+
+def config2(**kw):
+    """BASELINE configs[1]: 64^3 + walls, 27 spheres, bottom wall 1800 K, 500 steps of 5e-6 s."""
+    return closed_box_melting(**kw)
+
+
+def by_name(name, **kw):
+    return {"c1": config1, "c2": config2, "c5": config5}[name](**kw)

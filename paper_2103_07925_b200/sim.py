@@ -1,0 +1,168 @@
+"""Host-side mirror of the reference's interaction-evaluator and rigid-body API.
+
+`Simulation` drives one device context through the C ABI (include/sphg.h).
+Method names follow SPEC's operations so callers read like the reference's
+scenario driver (SPEC:525-533 `step`, SPEC:243-363 per-op evaluators,
+SPEC:328-354 body reductions); each evaluator runs the corresponding bulk
+stage over the whole store on the GPU.
+
+There is no CPU fallback: constructing a Simulation without the CUDA library
+(libsphg.so) raises.
+"""
+import ctypes as C
+
+import numpy as np
+
+from . import abi
+from .store import ParticleStore, BODY_DTYPE, bodies_ptr
+
+
+class SPHError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class Simulation:
+    prefix = "sphg_"
+
+    def __init__(self, params, device=0, lib=None):
+        if lib is None:
+            from ._lib import load
+            lib = load()
+        self.lib = lib
+        self.params = params
+        self._h = C.c_void_p()
+        rc = self._fn("create")(C.byref(params), int(device), C.byref(self._h))
+        if rc != 0:
+            raise SPHError(rc, "create failed: " + self.validate(params, lib, self.prefix))
+        self.n = 0
+
+    # ------------------------------------------------------------ plumbing
+    def _fn(self, name):
+        return getattr(self.lib, self.prefix + name)
+
+    def _check(self, rc, what):
+        if rc != 0:
+            msg = self._fn("last_error")(self._h)
+            raise SPHError(rc, f"{what}: {msg.decode() if msg else ''}")
+
+    @classmethod
+    def validate(cls, params, lib=None, prefix=None):
+        """validate_config (config.hpp:110-167): '' if valid, else messages joined by newlines."""
+        if lib is None:
+            from ._lib import load
+            lib = load()
+        buf = C.create_string_buffer(4096)
+        getattr(lib, (prefix or cls.prefix) + "validate")(C.byref(params), buf, len(buf))
+        return buf.value.decode()
+
+    def close(self):
+        if self._h:
+            self._fn("destroy")(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ------------------------------------------------------------ state
+    def upload(self, store, bodies=None):
+        soa = store.soa()
+        nb = 0 if bodies is None else len(bodies)
+        self._check(self._fn("upload")(self._h, C.byref(soa), bodies_ptr(bodies), nb), "upload")
+        self.n = store.n
+
+    def num_bodies(self):
+        nb = C.c_size_t(0)
+        self._check(self._fn("num_bodies")(self._h, C.byref(nb)), "num_bodies")
+        return nb.value
+
+    def download(self, store=None, fields=None):
+        """Returns (ParticleStore, bodies) in gid order."""
+        if store is None:
+            store = ParticleStore(self.n)
+        soa = store.soa(fields)
+        nb = C.c_size_t(self.num_bodies())
+        bodies = np.zeros(nb.value, BODY_DTYPE)
+        self._check(self._fn("download")(self._h, C.byref(soa), bodies_ptr(bodies), C.byref(nb)), "download")
+        return store, bodies
+
+    # ------------------------------------------------------------ stepping
+    def initialize(self):
+        self._check(self._fn("initialize")(self._h), "initialize")
+
+    def step(self, nsteps=1):
+        """step(state, dt), nsteps times."""
+        self._check(self._fn("step")(self._h, int(nsteps)), "step")
+
+    def run_stage(self, stage):
+        self._check(self._fn("run_stage")(self._h, int(stage)), abi.STAGE_NAMES[stage])
+
+    # SPEC operation names (bulk over the store)
+    def build_pairs(self):
+        """partition/migrate rebin + build_pairs."""
+        self.run_stage(abi.STAGE_REBUILD)
+
+    def density_summation(self):
+        """density_summation + eos_pressure."""
+        self.run_stage(abi.STAGE_DENSITY)
+
+    def conduction_rhs(self):
+        """apply_thermal_dirichlet + conduction_rhs + explicit T update."""
+        self.run_stage(abi.STAGE_HEAT)
+
+    def extrapolate_wall_quantities(self):
+        self.run_stage(abi.STAGE_EXTRAPOLATE)
+
+    def momentum_rhs(self):
+        """momentum_rhs + coupling_force_on_rigid + contact_force."""
+        self.run_stage(abi.STAGE_FORCES)
+
+    def reduce_force_torque(self):
+        self.run_stage(abi.STAGE_BODIES)
+
+    def reduce_mass_quantities(self):
+        self.run_stage(abi.STAGE_MASS)
+
+    def apply_transitions(self):
+        """detect_transitions + apply_transitions + split_disconnected_bodies."""
+        self.run_stage(abi.STAGE_TRANSITIONS)
+
+    # ------------------------------------------------------------ inspection
+    def get_cells(self):
+        cell = np.zeros(self.n, np.int64)
+        order = np.zeros(self.n, np.uint32)
+        self._check(self._fn("get_cells")(self._h, cell.ctypes.data_as(C.POINTER(C.c_int64)),
+                                          order.ctypes.data_as(C.POINTER(C.c_uint32))), "get_cells")
+        return cell, order
+
+    def get_nlist(self):
+        off = np.zeros(self.n + 1, np.int64)
+        self._check(self._fn("get_nlist")(self._h, off.ctypes.data_as(C.POINTER(C.c_int64)), None), "get_nlist")
+        nbr = np.zeros(int(off[-1]), np.uint32)
+        self._check(self._fn("get_nlist")(self._h, off.ctypes.data_as(C.POINTER(C.c_int64)),
+                                          nbr.ctypes.data_as(C.POINTER(C.c_uint32))), "get_nlist")
+        return off, nbr
+
+    def stats(self):
+        s = abi.Stats()
+        self._check(self._fn("stats")(self._h, C.byref(s)), "stats")
+        return s
+
+    def set_timing(self, enabled=True):
+        self._check(self._fn("set_timing")(self._h, int(bool(enabled))), "set_timing")
+
+    def compute_dt(self):
+        """compute_dt terms: cfl, viscous, body force, contact, conduction."""
+        out = (C.c_double * 5)()
+        self._check(self._fn("compute_dt")(self._h, out), "compute_dt")
+        return list(out)
