@@ -1,0 +1,281 @@
+#!/usr/bin/env python
+"""bench.py — particle-steps/s of the full fp64 SPH step (BASELINE.json metric).
+
+Workload at N=1: BASELINE configs[4] (C5), 400^3 = 64M particles, periodic, ~20k
+rigid spheres R~U[3,6]dx, config-1 physics (fluid + rigid + contact, TVF, no
+thermal), synthetic seeded inputs (no dataset exists for this path).
+
+A "step" is one full kick-drift-kick step over the whole store:
+half kick + drift + body integration, Verlet check (rebuild when triggered),
+density, wall/rigid extrapolation, forces (fluid + coupling + contact), body
+reduction, final kick.  Timed with CUDA events on the library's stream.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+--impl reference times the CPU oracle (oracle/_ref, the reference headers +
+the SPEC restatement, OpenMP on all host cores) on a bounded sample of the
+same workload.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-steps/sec (full SPH step, fp64)"
+UNIT = "particle-steps/s"
+# compulsory-state bytes per particle for the forces pass:
+# R r, u, u~, rho, p, V, m, mat; W a, a_bg
+FORCES_BYTES_PER_FLUID = 156.0
+FLOPS_PER_PAIR_FORCES = 91.0   # SURVEY §8(d) counting convention
+FLOPS_PER_PAIR_DENSITY = 17.0
+STEP_BYTES_PER_PARTICLE = 480.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="sph", choices=["sph", "reference"])
+    ap.add_argument("--nside", type=int, default=400)
+    ap.add_argument("--spheres", type=int, default=20000)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-nside", type=int, default=96)
+    return ap.parse_args()
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6553.3, "source": "BASELINE.md (MEASURED_PEAKS.json absent)"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        peaks["hbm_gbs"] = d.get("hbm_gbs", peaks["hbm_gbs"])
+        peaks["source"] = "MEASURED_PEAKS.json"
+    fp = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(fp):
+        with open(fp) as f:
+            peaks["fp64_tflops"] = json.load(f)["fp64_tflops"]
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and r[3 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(nside, spheres_total, nside_total, steps_max=20, budget_s=15.0):
+    """The oracle (reference headers + SPEC restatement, OpenMP) on a bounded sample of C5."""
+    from paper_2103_07925_b200 import scenarios
+    from oracle.oracle import Oracle
+    ns = max(1, int(round(spheres_total * (nside / nside_total) ** 3)))
+    sc = scenarios.config5(nside=nside, n_spheres=ns)
+    o = Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.initialize()
+    o.step(1)  # warm-up
+    t0 = time.perf_counter()
+    k = 0
+    while k < steps_max:
+        o.step(1)
+        k += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": sc.store.n * k / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"C5 physics, {nside}^3={sc.store.n} particles periodic, {ns} spheres, {k} steps "
+                      f"(oracle: SPEC restatement on the reference headers, OpenMP)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    nside = args.cpu_nside
+    from paper_2103_07925_b200 import scenarios
+    from oracle.oracle import Oracle
+    ns = max(1, int(round(args.spheres * (nside / args.nside) ** 3)))
+    sc = scenarios.config5(nside=nside, n_spheres=ns)
+    o = Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.initialize()
+    for _ in range(args.warmup):
+        o.step(1)
+    t0 = time.perf_counter()
+    o.step(args.steps)
+    dt = time.perf_counter() - t0
+    v = sc.store.n * args.steps / dt
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
+            "impl": "reference",
+            "config": {"workload": f"C5 sample {nside}^3 periodic + {ns} spheres (config-1 physics)",
+                       "particles": sc.store.n, "parallelism": f"openmp x{cores}"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{nside}^3 sample of C5, {args.steps} timed steps"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def store_bytes(store):
+    return store.nbytes()
+
+
+def run_sph(args):
+    import torch
+    from paper_2103_07925_b200 import scenarios, Simulation, abi
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        from paper_2103_07925_b200 import parallel
+        return parallel.bench_multi(args)
+    torch.cuda.set_device(local)
+    t_gen = time.perf_counter()
+    sc = scenarios.config5(nside=args.nside, n_spheres=args.spheres)
+    t_gen = time.perf_counter() - t_gen
+    n = sc.store.n
+    sim = Simulation(sc.params, device=local)
+    sim.upload(sc.store, sc.bodies)
+    sim.initialize()
+    for _ in range(args.warmup):
+        sim.step(1)
+    cand, inter = sim.count_pairs()
+    # timed region: K full steps, CUDA events recorded on the library's stream around sphg_step
+    st0 = sim.stats()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        sim.step(args.steps)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    st1 = sim.stats()
+    ms_step = st1.last_step_call_ms / args.steps
+    # per-stage breakdown (separate pass; per-stage events on the same stream)
+    sim.set_timing(True)
+    sa = sim.stats()
+    sim.step(max(2, args.steps // 2))
+    sb = sim.stats()
+    sim.set_timing(False)
+    kk = max(2, args.steps // 2)
+    stage_ms = {abi.STAGE_NAMES[k]: (sb.stage_ms[k] - sa.stage_ms[k]) / kk for k in range(10)}
+    launches = (st1.kernel_launches - st0.kernel_launches)
+    value = n * args.steps / (ms_step * 1e-3)
+    peaks = load_peaks()
+    info = sc.info
+    nf = info["n_fluid"]
+    frac_fluid_pairs = inter / max(n, 1)  # interacting pairs per particle (all kinds)
+    t_forces = stage_ms["forces"] * 1e-3
+    t_density = stage_ms["density"] * 1e-3
+    forces_bytes = FORCES_BYTES_PER_FLUID * nf
+    achieved = forces_bytes / t_forces / 1e9
+    roofline = {"bound": "hbm", "kernel": "forces (k_forces_fluid + k_forces_rigid)",
+                "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "bytes_model": f"{FORCES_BYTES_PER_FLUID:g} B per fluid particle (SURVEY 8(d) CSM)",
+                "peak_source": peaks["source"]}
+    flops = FLOPS_PER_PAIR_FORCES * inter * (nf / n)
+    fp64 = {"kernel": "forces", "achieved_tflops": flops / t_forces / 1e12,
+            "interacting_pairs": inter, "candidate_pairs": cand,
+            "flops_model": f"{FLOPS_PER_PAIR_FORCES:g} flop per interacting pair (SURVEY 8(d))"}
+    if "fp64_tflops" in peaks:
+        fp64["peak_tflops"] = peaks["fp64_tflops"]
+        fp64["frac"] = fp64["achieved_tflops"] / peaks["fp64_tflops"]
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64 lattice + jitter)",
+            "config": {"workload": f"C5 {args.nside}^3 periodic, {info['n_bodies']} rigid spheres R~U[3,6]dx",
+                       "particles": n, "fluid": nf, "rigid": info["n_rigid"],
+                       "rigid_fraction": round(info["rigid_fraction"], 4), "parallelism": "1 GPU",
+                       "l2": "inputs larger than L2 (state ~%.1f GB)" % (store_bytes(sc.store) / 1e9)},
+            "roofline": roofline, "fp64": fp64, "stage_ms": stage_ms,
+            "step_roofline": {"bytes_per_particle": STEP_BYTES_PER_PARTICLE,
+                              "achieved_gbs": STEP_BYTES_PER_PARTICLE * n / (ms_step * 1e-3) / 1e9},
+            "wall_s_timed": wall, "gpu_launches": int(launches),
+            "rebuilds_in_timed_region": int(st1.rebuilds - st0.rebuilds),
+            "clocks": clk.summary(), "gen_s": t_gen}
+    # e2e: through the public API with host buffers each step (upload -> step -> download)
+    if not args.no_e2e and args.e2e_steps > 0:
+        store = sc.store
+        fields = None
+        sim.download(store)
+        nbytes = store_bytes(store)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            sim.upload(store, sc.bodies)
+            sim.step(1)
+            store, _ = sim.download(store)
+        e2e_s = time.perf_counter() - t0
+        line["e2e"] = {"value": n * args.e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(nbytes),
+                       "d2h_bytes_per_step": int(nbytes), "steps": args.e2e_steps,
+                       "path": "Simulation.upload(ParticleStore) -> step(1) -> download(ParticleStore), pinned staging"}
+    if not args.no_cpu_baseline and rank == 0:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_nside, args.spheres, args.nside)
+    sim.close()
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_sph(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -157,6 +157,7 @@ typedef struct {
   double u_max;               /* max |u| of fluid particles at the last kick */
   double stage_ms[10];        /* accumulated device time per stage (if timing enabled) */
   int64_t kernel_launches;
+  double last_step_call_ms;   /* device time of the last sphg_step call (CUDA events on the stream) */
 } sphg_stats_t;
 
 typedef struct sphg_ctx sphg_ctx;
@@ -185,6 +186,11 @@ int sphg_set_timing(sphg_ctx* ctx, int enabled);
 int sphg_num_bodies(sphg_ctx* ctx, size_t* n_bodies);
 /* compute_dt terms: cfl, viscous, body force, contact, conduction; +inf = absent. */
 int sphg_compute_dt(sphg_ctx* ctx, double limits[5]);
+/* The five limits of compute_dt without a context (pure host function):
+ * u_max = max fluid speed, m_r = smallest rigid particle mass (<= 0: no contact term). */
+int sphg_dt_limits(const sphg_params* params, double u_max, double m_r, double limits[5]);
+/* Candidate pairs of the current Verlet list and pairs within r_c (interacting). */
+int sphg_count_pairs(sphg_ctx* ctx, int64_t* candidates, int64_t* interacting);
 const char* sphg_last_error(const sphg_ctx* ctx);
 void sphg_destroy(sphg_ctx* ctx);
 /* Messages of validate_config for `params` joined by '\n' (empty = valid). */

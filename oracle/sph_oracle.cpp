@@ -746,6 +746,7 @@ bool stage_final_kick(Ctx& c) {
             const sphg_body& b = c.bodies[c.S.group[i]];
             const V3 rk = sphfsi::rotate(qof(b), c.S.body_frame_pos[i]);
             c.S.vel[i] = v3(b.vel) + sphfsi::cross(v3(b.omega), rk);
+            c.S.vel_adv[i] = c.S.vel[i];  // rigid vel_adv mirrors vel
         }
     }
     return true;

@@ -90,7 +90,8 @@ class Stats(C.Structure):
                 ("bodies_alive", C.c_int64), ("nlist_capacity", C.c_int32),
                 ("max_neighbours", C.c_int32), ("cells", C.c_int32 * 3), ("pad", C.c_int32),
                 ("time", C.c_double), ("max_displacement", C.c_double), ("u_max", C.c_double),
-                ("stage_ms", C.c_double * 10), ("kernel_launches", C.c_int64)]
+                ("stage_ms", C.c_double * 10), ("kernel_launches", C.c_int64),
+                ("last_step_call_ms", C.c_double)]
 
 
 def declare(lib, prefix):
@@ -114,6 +115,8 @@ def declare(lib, prefix):
     optional = {
         "set_timing": (C.c_int, [vp, C.c_int]),
         "compute_dt": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "dt_limits": (C.c_int, [C.POINTER(Params), C.c_double, C.c_double, C.POINTER(C.c_double)]),
+        "count_pairs": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     }
     for name, (res, args) in list(sig.items()) + list(optional.items()):
         fn = getattr(lib, prefix + name, None)

@@ -1,0 +1,822 @@
+// api.cu — the C ABI of include/sphg.h: context lifetime, upload/download in
+// the ParticleStore<3> layout, and the stream-ordered step driver.
+//
+// Replaces (reference interfaces):
+//   sphg_create     validate_config (config.hpp:110-167) + decomposition setup
+//   sphg_upload     ParticleStore<3> (store.hpp:24-100) -> device SoA
+//   sphg_step       step(state, dt)
+//   sphg_run_stage  build_pairs / density_summation / conduction_rhs / extrapolate_wall_quantities /
+//                   momentum_rhs+coupling+contact / reduce_force_torque / transitions / reduce_mass_quantities
+//   sphg_download   device SoA -> ParticleStore<3>
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <numeric>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "context.cuh"
+
+using namespace sphg;
+
+struct sphg_ctx {
+  Ctx c;
+  bool mid_step = false;
+};
+
+namespace {
+
+constexpr double kSkin = 0.1;     // config.hpp:16 kVerletSkinFactor
+constexpr double kSupport = 3.0;  // config.hpp:15 kKernelSupportScale
+
+std::vector<std::string> validate(const sphg_params& P) {  // restates config.hpp:110-167 + extras
+  std::vector<std::string> v;
+  auto fail = [&](std::string m) { v.push_back(std::move(m)); };
+  if (P.n_mat < 0 || P.n_mat > SPHG_MAX_MAT) {
+    fail("material count out of range");
+    return v;
+  }
+  if (!(P.dx > 0.0)) fail("initial particle spacing dx must be positive");
+  if (P.h < 0.0) fail("smoothing length must be non-negative");
+  const double h = P.h > 0.0 ? P.h : P.dx;
+  const double rc = kSupport * h;
+  if (P.cell_edge_override > 0.0 && P.cell_edge_override < rc) fail("cell edge < support radius");
+  for (int a = 0; a < 3; ++a) {
+    const double extent = P.hi[a] - P.lo[a];
+    if (!(extent > 0.0)) fail("domain extent must be positive on axis " + std::to_string(a));
+    if (P.periodic[a]) {
+      if (extent < 2.0 * rc) fail("periodic axis " + std::to_string(a) + " shorter than twice the support radius");
+      if (P.dx > 0.0) {
+        const double cells = extent / P.dx;
+        if (std::abs(cells - std::round(cells)) > 1e-9 * cells)
+          fail("periodic axis " + std::to_string(a) + " extent is not a multiple of dx");
+      }
+    }
+  }
+  if (P.n_mat == 0) fail("no materials defined");
+  for (int m = 0; m < P.n_mat; ++m) {
+    const sphg_material& mt = P.mat[m];
+    const std::string name = "m" + std::to_string(m);
+    if (!(mt.rho0 > 0.0)) fail("material '" + name + "' has non-positive reference density");
+    if (mt.melt_target >= 0 && mt.melt_target >= P.n_mat) fail("material '" + name + "' melts into a missing material");
+    if (mt.solidify_target >= 0 && mt.solidify_target >= P.n_mat)
+      fail("material '" + name + "' solidifies into a missing material");
+  }
+  if ((P.nranks > 0 ? P.nranks : 1) < 1) fail("worker count must be at least 1");
+  if (P.kc < 0.0) fail("contact stiffness must be non-negative");
+  if (P.dc < 0.0) fail("contact damping must be non-negative");
+  for (int g = 0; g < P.n_dirichlet && g < SPHG_MAX_DIRICHLET; ++g)
+    for (int i = 1; i < P.dirichlet_T[g].n && i < SPHG_MAX_PIECES; ++i)
+      if (P.dirichlet_T[g].t_end[i] < P.dirichlet_T[g].t_end[i - 1]) fail("temperature schedule pieces out of order");
+  // extras (oracle/sph_oracle.cpp validate)
+  if (!(P.dt > 0.0)) fail("time step dt must be positive");
+  const double rv = kSupport * h + kSkin * h;
+  for (int a = 0; a < 3; ++a) {
+    const double ext = P.hi[a] - P.lo[a];
+    const double e0 = P.cell_edge_override > 0.0 ? P.cell_edge_override : rv;
+    if (P.periodic[a] && ext > 0.0 && std::floor(ext / e0) < 3.0)
+      fail("periodic axis " + std::to_string(a) + " has fewer than 3 cells");
+  }
+  if (P.n_dirichlet < 0 || P.n_dirichlet > SPHG_MAX_DIRICHLET) fail("dirichlet group count out of range");
+  if (P.default_fluid_mat < 0 || P.default_fluid_mat >= P.n_mat) fail("default fluid material missing");
+  return v;
+}
+
+DevParams make_dev_params(const sphg_params& p) {
+  DevParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.n_mat = p.n_mat;
+  bool first_fluid = true;
+  double eta0 = 0, rho00 = 0, c0 = 0;
+  P.single_eta = 1;
+  P.single_eos = 1;
+  P.single_kappa = 1;
+  for (int m = 0; m < p.n_mat; ++m) {
+    const sphg_material& s = p.mat[m];
+    DevMat& d = P.mat[m];
+    d.rho0 = s.rho0;
+    d.eta = s.rho0 * s.nu;  // material.hpp:32
+    d.cp = s.cp;
+    d.kappa = s.kappa;
+    d.c2 = s.c * s.c;
+    d.pb = s.pb;
+    d.T_t = s.T_t;
+    d.has_Tt = std::isnan(s.T_t) ? 0 : 1;
+    for (int a = 0; a < 3; ++a) d.g[a] = s.body_force[a];
+    d.p0 = s.rho0 * s.c * s.c;
+    d.inv_c2 = s.c != 0.0 ? 1.0 / (s.c * s.c) : 0.0;
+    d.melt = s.melt_target;
+    d.solid = s.solidify_target;
+    if (m > 0 && s.kappa != p.mat[0].kappa) P.single_kappa = 0;
+    if (s.c > 0.0 && s.nu >= 0.0) {  // a fluid-capable material
+      if (first_fluid) {
+        eta0 = d.eta;
+        rho00 = s.rho0;
+        c0 = s.c;
+        first_fluid = false;
+      } else {
+        if (d.eta != eta0) P.single_eta = 0;
+        if (s.rho0 != rho00 || s.c != c0) P.single_eos = 0;
+      }
+    }
+  }
+  // a wall without support falls back to default_fluid_mat; with single_eos the EOS is the same anyway
+  if (P.single_eos && p.n_mat > 0) {
+    const sphg_material& dm = p.mat[p.default_fluid_mat];
+    if (!first_fluid && (dm.rho0 != rho00 || dm.c != c0)) P.single_eos = 0;
+  }
+  P.n_sched = p.n_dirichlet;
+  for (int g = 0; g < p.n_dirichlet && g < SPHG_MAX_DIRICHLET; ++g) {
+    P.sched[g].n = p.dirichlet_T[g].n;
+    for (int k = 0; k < SPHG_MAX_PIECES; ++k) {
+      P.sched[g].t_end[k] = p.dirichlet_T[g].t_end[k];
+      P.sched[g].value[k] = p.dirichlet_T[g].value[k];
+    }
+  }
+  P.h = p.h > 0.0 ? p.h : p.dx;
+  P.inv_h = 1.0 / P.h;  // kernel.hpp:20 inv_h_
+  P.rc = kSupport * P.h;
+  P.rc2 = P.rc * P.rc;
+  P.rv = P.rc + kSkin * P.h;
+  P.rv2 = P.rv * P.rv;
+  P.sigma = 1.0 / (120.0 * M_PI * P.h * P.h * P.h);  // kernel.hpp:44
+  P.sig_h = P.sigma * P.inv_h;
+  P.w0 = P.sigma * 66.0;
+  P.dx = p.dx;
+  P.dx3 = p.dx * p.dx * p.dx;
+  P.dt = p.dt;
+  P.hdt = 0.5 * p.dt;
+  P.kc = p.kc;
+  P.dc = p.dc;
+  P.half_skin = 0.5 * (P.rv - P.rc);
+  const double reff = std::cbrt(0.75 / M_PI) * p.dx;
+  P.Ir_over_m = 0.4 * reff * reff;
+  P.tvf = p.tvf;
+  P.thermal = p.thermal;
+  P.transitions = p.transitions;
+  P.default_fluid_mat = p.default_fluid_mat;
+  for (int a = 0; a < 3; ++a) {
+    P.lo[a] = p.lo[a];
+    P.hi[a] = p.hi[a];
+    P.L[a] = p.hi[a] - p.lo[a];
+    P.halfL[a] = 0.5 * P.L[a];
+    P.periodic[a] = p.periodic[a];
+    const double e0 = p.cell_edge_override > 0.0 ? p.cell_edge_override : P.rv;  // [P1]
+    int nc = (int)std::floor(P.L[a] / e0);
+    if (nc < 1) nc = 1;
+    P.ncell[a] = nc;
+    P.inv_edge[a] = (double)nc / P.L[a];
+  }
+  return P;
+}
+
+double bits_to_double(unsigned long long b) {
+  double d;
+  std::memcpy(&d, &b, sizeof(d));
+  return d;
+}
+
+int fail(sphg_ctx* h, int code, const std::string& m) {
+  if (h) h->c.err = m;
+  return code;
+}
+
+template <class F>
+int guarded(sphg_ctx* h, F&& f) {
+  try {
+    return f();
+  } catch (const CudaError& e) {
+    return fail(h, SPHG_ERR_CUDA, "CUDA error: " + e.what);
+  } catch (const std::exception& e) {
+    return fail(h, SPHG_ERR_RUNTIME, e.what());
+  }
+}
+
+void ensure_bodies(Ctx& c, size_t need) {
+  if (need <= c.bodies_cap && c.bodies.p) return;
+  size_t cap = std::max<size_t>(need * 2, 64);
+  sphg_body* nb = nullptr;
+  SPHG_CUDA_CHECK(cudaMalloc(&nb, cap * sizeof(sphg_body)));
+  SPHG_CUDA_CHECK(cudaMemsetAsync(nb, 0, cap * sizeof(sphg_body), c.stream));
+  if (c.bodies.p && c.nb) SPHG_CUDA_CHECK(cudaMemcpyAsync(nb, c.bodies.p, c.nb * sizeof(sphg_body), cudaMemcpyDeviceToDevice, c.stream));
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  c.bodies.free();
+  c.bodies.p = nb;
+  c.bodies.n = cap;
+  c.bodies_cap = cap;
+}
+
+// reads the flag block; returns SPHG_OK or a runtime error with a one-line message
+int check_flags(sphg_ctx* h, bool sync) {
+  Ctx& c = h->c;
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(c.hflags, c.dflags, sizeof(DevFlags), cudaMemcpyDeviceToHost, c.stream));
+  if (sync) SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  SPHG_CUDA_CHECK(cudaGetLastError());
+  const DevFlags& f = *c.hflags;
+  c.max_disp = std::sqrt(bits_to_double(f.max_disp2_bits));
+  c.u_max = std::sqrt(bits_to_double(f.umax2_bits));
+  if (f.err) {
+    std::string what = (f.err & kErrEscape) ? "escaped particle " : (f.err & kErrCoincident) ? "coincident particles at particle " : "runtime assertion at particle ";
+    return fail(h, SPHG_ERR_RUNTIME, what + std::to_string(f.err_gid) + " at step " + std::to_string(c.steps + (h->mid_step ? 1 : 0)));
+  }
+  return SPHG_OK;
+}
+
+void reset_step_flags(Ctx& c) {
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.dflags, 0, 2 * sizeof(unsigned long long), c.stream));
+}
+
+void timed(Ctx& c, int stage, void (*fn)(Ctx&)) {
+  if (!c.timing) {
+    fn(c);
+    return;
+  }
+  SPHG_CUDA_CHECK(cudaEventRecord(c.ev[0], c.stream));
+  fn(c);
+  SPHG_CUDA_CHECK(cudaEventRecord(c.ev[1], c.stream));
+  SPHG_CUDA_CHECK(cudaEventSynchronize(c.ev[1]));
+  float ms = 0.f;
+  SPHG_CUDA_CHECK(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+  c.stage_ms[stage] += ms;
+}
+
+void kick_all(Ctx& c) {
+  launch_body_kick(c);
+  launch_kick_drift(c);
+}
+
+int do_stage(sphg_ctx* h, int stage) {
+  Ctx& c = h->c;
+  if (!c.have_state) return fail(h, SPHG_ERR_RUNTIME, "no particle state uploaded");
+  if (c.n == 0) {  // empty store: every stage is a no-op
+    if (stage == SPHG_STAGE_KICK_DRIFT) c.t += c.P.dt;
+    return SPHG_OK;
+  }
+  if (stage != SPHG_STAGE_REBUILD && stage != SPHG_STAGE_KICK_DRIFT && stage != SPHG_STAGE_MASS && !c.built)
+    timed(c, SPHG_STAGE_REBUILD, launch_rebuild);
+  switch (stage) {
+    case SPHG_STAGE_REBUILD: timed(c, stage, launch_rebuild); break;
+    case SPHG_STAGE_DENSITY: timed(c, stage, launch_density); break;
+    case SPHG_STAGE_HEAT:
+      if (c.P.thermal) timed(c, stage, launch_heat);
+      break;
+    case SPHG_STAGE_EXTRAPOLATE: timed(c, stage, launch_extrapolate); break;
+    case SPHG_STAGE_FORCES: timed(c, stage, launch_forces); break;
+    case SPHG_STAGE_BODIES: timed(c, stage, launch_bodies); break;
+    case SPHG_STAGE_KICK_DRIFT:
+      reset_step_flags(c);
+      timed(c, stage, kick_all);
+      c.t += c.P.dt;
+      h->mid_step = true;
+      break;
+    case SPHG_STAGE_FINAL_KICK:
+      timed(c, stage, launch_final_kick);
+      h->mid_step = false;
+      break;
+    case SPHG_STAGE_TRANSITIONS:
+      if (c.P.transitions == 1) {
+        const int rc = launch_transitions(c);
+        if (rc) return fail(h, rc, c.err);
+      }
+      break;
+    case SPHG_STAGE_MASS:
+      if (!c.built) launch_rigid_index(c);
+      launch_mass(c, nullptr);
+      break;
+    default: return fail(h, SPHG_ERR_RUNTIME, "unknown stage");
+  }
+  return check_flags(h, true);
+}
+
+int one_step(sphg_ctx* h) {
+  Ctx& c = h->c;
+  reset_step_flags(c);
+  timed(c, SPHG_STAGE_KICK_DRIFT, kick_all);
+  c.t += c.P.dt;
+  h->mid_step = true;
+  int rc = check_flags(h, true);  // one 48-byte readback per step: Verlet trigger + escape check
+  if (rc) return rc;
+  if (!c.built || c.max_disp > c.P.half_skin) timed(c, SPHG_STAGE_REBUILD, launch_rebuild);
+  timed(c, SPHG_STAGE_DENSITY, launch_density);
+  if (c.P.thermal) timed(c, SPHG_STAGE_HEAT, launch_heat);
+  timed(c, SPHG_STAGE_EXTRAPOLATE, launch_extrapolate);
+  timed(c, SPHG_STAGE_FORCES, launch_forces);
+  timed(c, SPHG_STAGE_BODIES, launch_bodies);
+  timed(c, SPHG_STAGE_FINAL_KICK, launch_final_kick);
+  h->mid_step = false;
+  if (c.P.transitions == 1) {
+    rc = launch_transitions(c);
+    if (rc) return fail(h, rc, c.err);
+  }
+  c.steps++;
+  return SPHG_OK;
+}
+
+template <class T>
+void d2h(T* dst, const T* src, size_t n, cudaStream_t s) {
+  if (n) SPHG_CUDA_CHECK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+template <class T>
+void h2d(T* dst, const T* src, size_t n, cudaStream_t s) {
+  if (n) SPHG_CUDA_CHECK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+// ------------------------------------------------------- host <-> device staging
+// The host store is packed/unpacked in chunks through two pinned staging slots
+// (OpenMP over particles) so the PCIe copies overlap the packing of the next
+// chunk.  Device order == gid order on a cold upload; a warm upload lands in
+// the alternate buffers and is gathered through the gid permutation.
+constexpr size_t kChunk = 1u << 18;  // particles per staging chunk
+constexpr size_t kPackBytes = 8 * sizeof(double4) + sizeof(double2) + 2 * sizeof(double) + 2 * sizeof(uint32_t);
+
+struct Slot {
+  double4 *G0, *G1, *G2, *V4, *A4, *B4, *F4, *X4;
+  double2* H2;
+  double *dT, *ps;
+  uint32_t *kmd, *grp, *gid;
+};
+
+Slot slot_view(char* base) {
+  Slot s;
+  size_t o = 0;
+  auto take = [&](auto*& p, size_t bytes) {
+    p = reinterpret_cast<std::remove_reference_t<decltype(p)>>(base + o);
+    o += bytes;
+  };
+  take(s.G0, kChunk * 32); take(s.G1, kChunk * 32); take(s.G2, kChunk * 32); take(s.V4, kChunk * 32);
+  take(s.A4, kChunk * 32); take(s.B4, kChunk * 32); take(s.F4, kChunk * 32); take(s.X4, kChunk * 32);
+  take(s.H2, kChunk * 16); take(s.dT, kChunk * 8); take(s.ps, kChunk * 8);
+  take(s.kmd, kChunk * 4); take(s.grp, kChunk * 4); take(s.gid, kChunk * 4);
+  return s;
+}
+
+void ensure_staging(Ctx& c) {
+  if (c.hstage) return;
+  SPHG_CUDA_CHECK(cudaMallocHost(&c.hstage, 2 * kChunk * (kPackBytes + 4)));
+  for (auto& e : c.slot_ev) SPHG_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+void stage_upload(Ctx& c, const sphg_soa* s, Particles& dst) {
+  ensure_staging(c);
+  const size_t n = s->n;
+  const size_t slot_bytes = kChunk * (kPackBytes + 4);
+  auto v3 = [](const double* p, size_t i) {
+    return p ? make_double3(p[3 * i], p[3 * i + 1], p[3 * i + 2]) : make_double3(0, 0, 0);
+  };
+  auto s1 = [](const double* p, size_t i) { return p ? p[i] : 0.0; };
+  int slot = 0;
+  for (size_t k0 = 0; k0 < n; k0 += kChunk, slot ^= 1) {
+    const size_t m = std::min(kChunk, n - k0);
+    SPHG_CUDA_CHECK(cudaEventSynchronize(c.slot_ev[slot]));
+    Slot S = slot_view(static_cast<char*>(c.hstage) + slot * slot_bytes);
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < (int64_t)m; ++q) {
+      const size_t i = k0 + (size_t)q;
+      const uint32_t kind = s->kind ? s->kind[i] : 0;
+      const uint32_t mat = s->material ? s->material[i] : 0;
+      const uint32_t dir = s->dirichlet_T ? s->dirichlet_T[i] : SPHG_NO_DIRICHLET;
+      const double3 x = v3(s->pos, i), u = v3(s->vel, i), ua = v3(s->vel_adv, i);
+      const double mass = s1(s->mass, i), rho = s1(s->density, i), p = s1(s->pressure, i);
+      const DevMat& M = c.P.mat[mat];
+      const double V = rho > 0.0 ? mass / rho : 0.0;
+      S.G0[q] = make_double4(x.x, x.y, x.z, V * V);
+      if (kind == SPHG_FLUID) {
+        S.G1[q] = make_double4(u.x, u.y, u.z, rho);
+        S.G2[q] = make_double4(ua.x - u.x, ua.y - u.y, ua.z - u.z, p);
+      } else {
+        const double3 wv = v3(s->wall_velocity, i);
+        S.G1[q] = make_double4(wv.x, wv.y, wv.z, rho);
+        S.G2[q] = make_double4(0, 0, 0, s1(s->wall_pressure, i));
+      }
+      S.V4[q] = make_double4(u.x, u.y, u.z, mass);
+      const double3 a = v3(s->acc, i), bg = v3(s->acc_bg, i), f = v3(s->force, i), chi = v3(s->body_frame_pos, i);
+      S.A4[q] = make_double4(a.x, a.y, a.z, 0);
+      S.B4[q] = make_double4(bg.x, bg.y, bg.z, 0);
+      S.F4[q] = make_double4(f.x, f.y, f.z, 0);
+      S.X4[q] = make_double4(chi.x, chi.y, chi.z, 0);
+      double Vh = 0.0;
+      if (kind == SPHG_FLUID) Vh = V;
+      else if (kind == SPHG_RIGID) Vh = mass / M.rho0;
+      else if (dir != SPHG_NO_DIRICHLET) Vh = mass / M.rho0;  // [P9]
+      S.H2[q] = make_double2(s1(s->temperature, i), Vh);
+      S.dT[q] = s1(s->dT_dt, i);
+      S.ps[q] = p;
+      S.kmd[q] = make_kmd(kind, mat, dir);
+      S.grp[q] = s->group ? s->group[i] : 0;
+    }
+    cudaStream_t st = c.stream;
+    h2d(dst.G0.p + k0, S.G0, m, st); h2d(dst.G1.p + k0, S.G1, m, st); h2d(dst.G2.p + k0, S.G2, m, st);
+    h2d(dst.V4.p + k0, S.V4, m, st); h2d(dst.A4.p + k0, S.A4, m, st); h2d(dst.B4.p + k0, S.B4, m, st);
+    h2d(dst.F4.p + k0, S.F4, m, st); h2d(dst.X4.p + k0, S.X4, m, st); h2d(dst.H2.p + k0, S.H2, m, st);
+    h2d(dst.dTdt.p + k0, S.dT, m, st); h2d(dst.p_static.p + k0, S.ps, m, st);
+    h2d(dst.kmd.p + k0, S.kmd, m, st); h2d(dst.group.p + k0, S.grp, m, st);
+    SPHG_CUDA_CHECK(cudaEventRecord(c.slot_ev[slot], st));
+  }
+}
+
+void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
+  ensure_staging(c);
+  const size_t n = c.n;
+  const size_t slot_bytes = kChunk * (kPackBytes + 4);
+  cudaStream_t st = c.stream;
+  auto put = [](double* p, size_t g, double x, double y, double z) {
+    if (p) {
+      p[3 * g] = x;
+      p[3 * g + 1] = y;
+      p[3 * g + 2] = z;
+    }
+  };
+  int slot = 0;
+  size_t prev_k0 = 0, prev_m = 0;
+  int prev_slot = -1;
+  auto unpack = [&](int sl, size_t k0, size_t m) {
+    SPHG_CUDA_CHECK(cudaEventSynchronize(c.slot_ev[sl]));
+    Slot S = slot_view(static_cast<char*>(c.hstage) + sl * slot_bytes);
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < (int64_t)m; ++q) {
+      const size_t g = S.gid[q];
+      const uint32_t kmd = S.kmd[q];
+      const uint32_t kind = kind_of(kmd), mat = mat_of(kmd);
+      const bool fl = kind == SPHG_FLUID;
+      const double4 G0 = S.G0[q], G1 = S.G1[q], G2 = S.G2[q], V4 = S.V4[q];
+      put(o->pos, g, G0.x, G0.y, G0.z);
+      if (fl && mid_step) put(o->vel, g, G1.x, G1.y, G1.z);
+      else put(o->vel, g, V4.x, V4.y, V4.z);
+      if (fl) put(o->vel_adv, g, G1.x + G2.x, G1.y + G2.y, G1.z + G2.z);
+      else if (kind == SPHG_RIGID) put(o->vel_adv, g, V4.x, V4.y, V4.z);
+      else put(o->vel_adv, g, 0, 0, 0);
+      put(o->acc, g, S.A4[q].x, S.A4[q].y, S.A4[q].z);
+      put(o->acc_bg, g, S.B4[q].x, S.B4[q].y, S.B4[q].z);
+      put(o->force, g, S.F4[q].x, S.F4[q].y, S.F4[q].z);
+      put(o->body_frame_pos, g, S.X4[q].x, S.X4[q].y, S.X4[q].z);
+      if (fl) put(o->wall_velocity, g, 0, 0, 0);
+      else put(o->wall_velocity, g, G1.x, G1.y, G1.z);
+      if (o->density) o->density[g] = kind == SPHG_RIGID ? c.P.mat[mat].rho0 : G1.w;
+      if (o->pressure) o->pressure[g] = fl ? G2.w : S.ps[q];
+      if (o->wall_pressure) o->wall_pressure[g] = fl ? 0.0 : G2.w;
+      if (o->mass) o->mass[g] = V4.w;
+      if (o->temperature) o->temperature[g] = S.H2[q].x;
+      if (o->dT_dt) o->dT_dt[g] = S.dT[q];
+      if (o->kind) o->kind[g] = (uint8_t)kind;
+      if (o->group) o->group[g] = S.grp[q];
+      if (o->material) o->material[g] = (uint16_t)mat;
+      if (o->dirichlet_T) o->dirichlet_T[g] = (uint8_t)dir_of(kmd);
+    }
+  };
+  for (size_t k0 = 0; k0 < n; k0 += kChunk, slot ^= 1) {
+    const size_t m = std::min(kChunk, n - k0);
+    Slot S = slot_view(static_cast<char*>(c.hstage) + slot * slot_bytes);
+    SPHG_CUDA_CHECK(cudaEventSynchronize(c.slot_ev[slot]));
+    d2h(S.G0, c.cur.G0.p + k0, m, st); d2h(S.G1, c.cur.G1.p + k0, m, st); d2h(S.G2, c.cur.G2.p + k0, m, st);
+    d2h(S.V4, c.cur.V4.p + k0, m, st); d2h(S.A4, c.cur.A4.p + k0, m, st); d2h(S.B4, c.cur.B4.p + k0, m, st);
+    d2h(S.F4, c.cur.F4.p + k0, m, st); d2h(S.X4, c.cur.X4.p + k0, m, st); d2h(S.H2, c.cur.H2.p + k0, m, st);
+    d2h(S.dT, c.cur.dTdt.p + k0, m, st); d2h(S.ps, c.cur.p_static.p + k0, m, st);
+    d2h(S.kmd, c.cur.kmd.p + k0, m, st); d2h(S.grp, c.cur.group.p + k0, m, st); d2h(S.gid, c.cur.gid.p + k0, m, st);
+    SPHG_CUDA_CHECK(cudaEventRecord(c.slot_ev[slot], st));
+    if (prev_slot >= 0) unpack(prev_slot, prev_k0, prev_m);  // overlaps with the copy just issued
+    prev_slot = slot;
+    prev_k0 = k0;
+    prev_m = m;
+  }
+  if (prev_slot >= 0) unpack(prev_slot, prev_k0, prev_m);
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int sphg_validate(const sphg_params* p, char* buf, size_t len) {
+  const auto v = validate(*p);
+  std::string s;
+  for (size_t i = 0; i < v.size(); ++i) s += (i ? "\n" : "") + v[i];
+  if (buf && len) {
+    std::strncpy(buf, s.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return v.empty() ? SPHG_OK : SPHG_ERR_CONFIG;
+}
+
+int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
+  *out = nullptr;
+  if (!validate(*p).empty()) return SPHG_ERR_CONFIG;
+  sphg_ctx* h = new sphg_ctx();
+  Ctx& c = h->c;
+  c.params = *p;
+  if (c.params.h <= 0.0) c.params.h = c.params.dx;
+  c.P = make_dev_params(c.params);
+  c.device = device;
+  c.t = p->t0;
+  c.ncells = (int64_t)c.P.ncell[0] * c.P.ncell[1] * c.P.ncell[2];
+  try {
+    SPHG_CUDA_CHECK(cudaSetDevice(device));
+    SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    SPHG_CUDA_CHECK(cudaMalloc(&c.dflags, sizeof(DevFlags)));
+    SPHG_CUDA_CHECK(cudaMemset(c.dflags, 0, sizeof(DevFlags)));
+    SPHG_CUDA_CHECK(cudaMallocHost(&c.hflags, sizeof(DevFlags)));
+    std::memset(c.hflags, 0, sizeof(DevFlags));
+    SPHG_CUDA_CHECK(cudaEventCreate(&c.ev[0]));
+    SPHG_CUDA_CHECK(cudaEventCreate(&c.ev[1]));
+  } catch (const CudaError& e) {
+    delete h;
+    return SPHG_ERR_CUDA;
+  }
+  *out = h;
+  return SPHG_OK;
+}
+
+int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t nb) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    SPHG_CUDA_CHECK(cudaSetDevice(c.device));
+    const size_t n = s->n;
+    if (n >= (size_t)UINT32_MAX) return fail(h, SPHG_ERR_CONFIG, "too many particles for 32-bit gids");
+    // validate tags first (nothing is modified on failure)
+    for (size_t i = 0; i < n; ++i) {
+      const uint32_t kind = s->kind ? s->kind[i] : 0;
+      const uint32_t mat = s->material ? s->material[i] : 0;
+      if (kind > 2 || (int)mat >= c.params.n_mat)
+        return fail(h, SPHG_ERR_CONFIG, "particle " + std::to_string(i) + " has an invalid kind/material");
+      if (kind == SPHG_RIGID && (s->group ? s->group[i] : 0) >= nb)
+        return fail(h, SPHG_ERR_CONFIG, "rigid particle " + std::to_string(i) + " refers to a missing body");
+    }
+    // warm upload: same store size and a valid Verlet list -> keep the device order and the list,
+    // scatter the host (gid-ordered) data through the gid permutation
+    const bool warm = c.built && c.have_state && n == c.n && n > 0;
+    c.n = n;
+    const size_t na = std::max<size_t>(n, 1);
+    c.cur.alloc(na);
+    c.alt.alloc(na);
+    c.H2new.alloc(na);
+    c.keys.alloc(na);
+    c.keys_alt.alloc(na);
+    c.vals.alloc(na);
+    c.vals_alt.alloc(na);
+    c.hist.alloc(radix_scratch_words(na));
+    c.scan_tmp.alloc(radix_scratch_words(na));
+    c.cell_start.alloc(c.ncells);
+    c.cell_end.alloc(c.ncells);
+    c.cell_key.alloc(na);
+    c.cnt.alloc(na);
+    Particles& dst = warm ? c.alt : c.cur;
+    stage_upload(c, s, dst);
+    if (warm) {
+      gather_by_gid(c);  // cur[k] <- alt[gid[k]] (keeps gid, R4, list)
+      if (displacement_exceeds(c)) c.built = false;
+    } else {
+      iota_gid(c);
+      SPHG_CUDA_CHECK(cudaMemcpyAsync(c.cur.R4.p, c.cur.G0.p, n * sizeof(double4), cudaMemcpyDeviceToDevice, c.stream));
+      c.built = false;
+    }
+    c.nb = 0;
+    ensure_bodies(c, nb);
+    c.nb = nb;
+    h2d(c.bodies.p, bodies, nb, c.stream);
+    SPHG_CUDA_CHECK(cudaMemsetAsync(c.dflags, 0, sizeof(DevFlags), c.stream));
+    if (c.built) launch_rigid_index(c);  // kinds / bodies may have changed
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    c.have_state = true;
+    h->mid_step = false;
+    return SPHG_OK;
+  });
+}
+
+int sphg_initialize(sphg_ctx* h) {
+  return guarded(h, [&]() -> int {
+    for (int s : {SPHG_STAGE_REBUILD, SPHG_STAGE_DENSITY, SPHG_STAGE_EXTRAPOLATE, SPHG_STAGE_FORCES, SPHG_STAGE_BODIES}) {
+      const int rc = do_stage(h, s);
+      if (rc) return rc;
+    }
+    return SPHG_OK;
+  });
+}
+
+int sphg_step(sphg_ctx* h, int nsteps) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (!c.have_state) return fail(h, SPHG_ERR_RUNTIME, "no particle state uploaded");
+    SPHG_CUDA_CHECK(cudaSetDevice(c.device));
+    if (c.n == 0) {
+      c.steps += nsteps;
+      c.t += nsteps * c.P.dt;
+      return SPHG_OK;
+    }
+    if (!c.step_ev[0]) {
+      SPHG_CUDA_CHECK(cudaEventCreate(&c.step_ev[0]));
+      SPHG_CUDA_CHECK(cudaEventCreate(&c.step_ev[1]));
+    }
+    SPHG_CUDA_CHECK(cudaEventRecord(c.step_ev[0], c.stream));
+    for (int k = 0; k < nsteps; ++k) {
+      const int rc = one_step(h);
+      if (rc) return rc;
+    }
+    SPHG_CUDA_CHECK(cudaEventRecord(c.step_ev[1], c.stream));
+    const int rc = check_flags(h, true);
+    float ms = 0.f;
+    SPHG_CUDA_CHECK(cudaEventElapsedTime(&ms, c.step_ev[0], c.step_ev[1]));
+    c.last_step_ms = ms;
+    return rc;
+  });
+}
+
+int sphg_run_stage(sphg_ctx* h, int stage) {
+  return guarded(h, [&]() -> int {
+    SPHG_CUDA_CHECK(cudaSetDevice(h->c.device));
+    return do_stage(h, stage);
+  });
+}
+
+int sphg_num_bodies(sphg_ctx* h, size_t* nb) {
+  *nb = h->c.nb;
+  return SPHG_OK;
+}
+
+int sphg_download(sphg_ctx* h, sphg_soa* o, sphg_body* bodies, size_t* nb_io) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    SPHG_CUDA_CHECK(cudaSetDevice(c.device));
+    if (o->n != c.n) return fail(h, SPHG_ERR_RUNTIME, "download: store size mismatch");
+    stage_download(c, o, h->mid_step);
+    if (nb_io) {
+      if (bodies) d2h(bodies, c.bodies.p, std::min(*nb_io, c.nb), c.stream);
+      SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      *nb_io = c.nb;
+    }
+    return SPHG_OK;
+  });
+}
+
+int sphg_get_cells(sphg_ctx* h, int64_t* cell_of_gid, uint32_t* sorted_gid) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (!c.built) {
+      const int rc = do_stage(h, SPHG_STAGE_REBUILD);
+      if (rc) return rc;
+    }
+    const size_t n = c.n;
+    std::vector<uint32_t> key(n), gid(n);
+    d2h(key.data(), c.cell_key.p, n, c.stream);
+    d2h(gid.data(), c.cur.gid.p, n, c.stream);
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    for (size_t k = 0; k < n; ++k) {
+      if (cell_of_gid) cell_of_gid[gid[k]] = key[k];
+      if (sorted_gid) sorted_gid[k] = gid[k];
+    }
+    return SPHG_OK;
+  });
+}
+
+int sphg_get_nlist(sphg_ctx* h, int64_t* offsets, uint32_t* nbr_gid) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (!c.built) {
+      const int rc = do_stage(h, SPHG_STAGE_REBUILD);
+      if (rc) return rc;
+    }
+    const size_t n = c.n;
+    std::vector<uint32_t> cnt(n), gid(n);
+    d2h(cnt.data(), c.cnt.p, n, c.stream);
+    d2h(gid.data(), c.cur.gid.p, n, c.stream);
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    std::vector<int64_t> cnt_g(n);
+    for (size_t k = 0; k < n; ++k) cnt_g[gid[k]] = cnt[k];
+    int64_t o = 0;
+    for (size_t g = 0; g < n; ++g) {
+      if (offsets) offsets[g] = o;
+      o += cnt_g[g];
+    }
+    if (offsets) offsets[n] = o;
+    if (!nbr_gid) return SPHG_OK;
+    std::vector<uint32_t> ell((size_t)c.cap * n);
+    d2h(ell.data(), c.nbr.p, ell.size(), c.stream);
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    for (size_t k = 0; k < n; ++k) {
+      const int64_t base = offsets[gid[k]];
+      for (uint32_t q = 0; q < cnt[k]; ++q) nbr_gid[base + q] = gid[ell[(size_t)q * n + k]];
+      std::sort(nbr_gid + base, nbr_gid + base + cnt[k]);
+    }
+    return SPHG_OK;
+  });
+}
+
+int sphg_stats(sphg_ctx* h, sphg_stats_t* s) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    std::memset(s, 0, sizeof(*s));
+    s->steps = c.steps;
+    s->rebuilds = c.rebuilds;
+    s->transitions_melt = c.n_melt;
+    s->transitions_solidify = c.n_solid;
+    s->nlist_capacity = c.cap;
+    s->max_neighbours = c.max_count;
+    for (int a = 0; a < 3; ++a) s->cells[a] = c.P.ncell[a];
+    s->time = c.t;
+    s->max_displacement = c.max_disp;
+    s->u_max = c.u_max;
+    for (int k = 0; k < 10; ++k) s->stage_ms[k] = c.stage_ms[k];
+    s->kernel_launches = c.launches;
+    s->last_step_call_ms = c.last_step_ms;
+    if (c.built && c.n) {
+      std::vector<uint32_t> cnt(c.n);
+      d2h(cnt.data(), c.cnt.p, c.n, c.stream);
+      SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      s->n_pairs_candidate = std::accumulate(cnt.begin(), cnt.end(), (int64_t)0);
+    }
+    if (c.nb) {
+      std::vector<sphg_body> b(c.nb);
+      d2h(b.data(), c.bodies.p, c.nb, c.stream);
+      SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      for (auto& x : b) s->bodies_alive += x.alive ? 1 : 0;
+    }
+    return SPHG_OK;
+  });
+}
+
+int sphg_set_timing(sphg_ctx* h, int enabled) {
+  h->c.timing = enabled != 0;
+  return SPHG_OK;
+}
+
+int sphg_dt_limits(const sphg_params* p, double u_max, double m_r, double lim[5]) {
+  const double inf = std::numeric_limits<double>::infinity();
+  for (int k = 0; k < 5; ++k) lim[k] = inf;
+  const double hh = p->h > 0.0 ? p->h : p->dx;
+  double bmax = 0.0;
+  for (int m = 0; m < p->n_mat && m < SPHG_MAX_MAT; ++m) {
+    const sphg_material& M = p->mat[m];
+    if (M.c > 0.0) lim[0] = std::min(lim[0], 0.25 * hh / (M.c + u_max));  // CFL
+    if (M.nu > 0.0) lim[1] = std::min(lim[1], 0.125 * hh * hh / M.nu);    // viscous
+    const double b = std::sqrt(M.body_force[0] * M.body_force[0] + M.body_force[1] * M.body_force[1] +
+                               M.body_force[2] * M.body_force[2]);
+    bmax = std::max(bmax, b);
+    if (M.kappa > 0.0 && M.cp > 0.0 && p->thermal)
+      lim[4] = std::min(lim[4], 0.1 * M.rho0 * M.cp * hh * hh / M.kappa);  // conduction
+  }
+  if (bmax > 0.0) lim[2] = 0.25 * std::sqrt(hh / bmax);                    // body force
+  if (p->kc > 0.0 && m_r > 0.0) lim[3] = 0.22 * std::sqrt(m_r / p->kc);    // contact
+  return SPHG_OK;
+}
+
+int sphg_compute_dt(sphg_ctx* h, double lim[5]) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    double mr = 0.0;
+    if (c.params.kc > 0.0 && c.nb > 0) {
+      std::vector<sphg_body> b(c.nb);
+      d2h(b.data(), c.bodies.p, c.nb, c.stream);
+      SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      double best = std::numeric_limits<double>::infinity();
+      for (auto& x : b)
+        if (x.alive) best = std::min(best, c.params.mat[x.material].rho0 * c.P.dx3);
+      if (best < std::numeric_limits<double>::infinity()) mr = best;
+    }
+    return sphg_dt_limits(&c.params, c.u_max, mr, lim);
+  });
+}
+
+int sphg_count_pairs(sphg_ctx* h, int64_t* candidates, int64_t* interacting) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    *candidates = *interacting = 0;
+    if (c.n == 0) return SPHG_OK;
+    if (!c.built) {
+      const int rc = do_stage(h, SPHG_STAGE_REBUILD);
+      if (rc) return rc;
+    }
+    count_pairs(c, candidates, interacting);
+    return SPHG_OK;
+  });
+}
+
+const char* sphg_last_error(const sphg_ctx* h) { return h ? h->c.err.c_str() : "null context"; }
+
+void sphg_destroy(sphg_ctx* h) {
+  if (!h) return;
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  if (c.stream) cudaStreamSynchronize(c.stream);
+  c.cur.free(); c.alt.free(); c.H2new.free(); c.bodies.free();
+  c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
+  c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();
+  c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();
+  if (c.dflags) cudaFree(c.dflags);
+  if (c.hflags) cudaFreeHost(c.hflags);
+  if (c.hbodies) cudaFreeHost(c.hbodies);
+  if (c.hstage) cudaFreeHost(c.hstage);
+  for (auto& e : c.slot_ev) if (e) cudaEventDestroy(e);
+  if (c.dcount) cudaFree(c.dcount);
+  for (auto& e : c.step_ev) if (e) cudaEventDestroy(e);
+  for (auto& e : c.ev) if (e) cudaEventDestroy(e);
+  if (c.stream) cudaStreamDestroy(c.stream);
+  delete h;
+}
+
+size_t sphg_sizeof_params(void) { return sizeof(sphg_params); }
+size_t sphg_sizeof_body(void) { return sizeof(sphg_body); }
+size_t sphg_sizeof_soa(void) { return sizeof(sphg_soa); }
+
+}  // extern "C"

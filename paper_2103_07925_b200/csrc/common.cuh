@@ -1,0 +1,215 @@
+// common.cuh — device-side parameters and math shared by all sm_100a kernels.
+//
+// Pinned arithmetic is mirrored from the CPU oracle so that the
+// bit-exact stages (cell keys, Verlet candidate tests, minimum image, periodic
+// wrap, kick/drift) produce identical doubles: those use explicit
+// round-to-nearest intrinsics (__dadd_rn/__dmul_rn/__dsub_rn), which ptxas
+// never contracts into FMA.  The tolerance stages (pair sums) use FMA freely.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/sphg.h"
+
+namespace sphg {
+
+constexpr int kMaxMat = SPHG_MAX_MAT;
+
+struct DevMat {
+  double rho0, eta, cp, kappa, c2, pb, T_t;
+  double g[3];
+  double p0;           // rho0 c^2
+  double inv_c2;       // 1/c^2 (0 when c == 0)
+  int32_t melt, solid;
+  int32_t has_Tt;
+  int32_t pad;
+};
+
+struct DevSchedule {
+  int32_t n, pad;
+  double t_end[SPHG_MAX_PIECES];
+  double value[SPHG_MAX_PIECES];
+};
+
+struct DevParams {
+  DevMat mat[kMaxMat];
+  DevSchedule sched[SPHG_MAX_DIRICHLET];
+  double lo[3], hi[3], L[3], halfL[3], inv_edge[3];
+  int32_t ncell[3];
+  int32_t periodic[3];
+  int32_t n_mat, n_sched;
+  double h, inv_h, rc, rc2, rv, rv2, sigma, sig_h, w0;
+  double dx, dx3, dt, hdt;
+  double kc, dc;
+  double half_skin;
+  double Ir_over_m;     // particle inertia / mass
+  int32_t tvf, thermal, transitions, default_fluid_mat;
+  int32_t single_eta;   // all fluid materials share eta   -> eta~ = eta_i
+  int32_t single_kappa; // all materials share kappa       -> kappa~ = 2 kappa
+  int32_t single_eos;   // all fluid materials share rho0,c -> wall EOS material fixed
+  int32_t pad;
+};
+
+// ---------------------------------------------------------------- tags
+// kmd word: bits 0-1 kind, 2-7 material, 8-15 dirichlet group (0xff none)
+__host__ __device__ __forceinline__ uint32_t kind_of(uint32_t kmd) { return kmd & 3u; }
+__host__ __device__ __forceinline__ uint32_t mat_of(uint32_t kmd) { return (kmd >> 2) & 63u; }
+__host__ __device__ __forceinline__ uint32_t dir_of(uint32_t kmd) { return (kmd >> 8) & 255u; }
+__host__ __device__ __forceinline__ uint32_t make_kmd(uint32_t kind, uint32_t mat, uint32_t dir) {
+  return (kind & 3u) | ((mat & 63u) << 2) | ((dir & 255u) << 8);
+}
+
+// ------------------------------------------------- pinned (no-FMA) helpers
+// minimum image along one axis [P2]
+__device__ __forceinline__ double mimg(const DevParams& P, double d, int a) {
+  if (P.periodic[a]) {
+    if (d > P.halfL[a]) d = __dsub_rn(d, P.L[a]);
+    else if (d < -P.halfL[a]) d = __dadd_rn(d, P.L[a]);
+  }
+  return d;
+}
+__device__ __forceinline__ double3 mimg3(const DevParams& P, double ax, double ay, double az, double bx, double by,
+                                         double bz) {
+  return make_double3(mimg(P, __dsub_rn(ax, bx), 0), mimg(P, __dsub_rn(ay, by), 1), mimg(P, __dsub_rn(az, bz), 2));
+}
+// (dx*dx + dy*dy) + dz*dz without contraction [P2]
+__device__ __forceinline__ double r2_exact(double3 d) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(d.x, d.x), __dmul_rn(d.y, d.y)), __dmul_rn(d.z, d.z));
+}
+// periodic wrap, one conditional shift [P14]
+__device__ __forceinline__ double wrap1(const DevParams& P, double x, int a) {
+  if (P.periodic[a]) {
+    if (x < P.lo[a]) x = __dadd_rn(x, P.L[a]);
+    else if (x >= P.hi[a]) x = __dsub_rn(x, P.L[a]);
+  }
+  return x;
+}
+// a + s*b with explicit rounding (matches Vec operator+ / operator* in the oracle)
+__device__ __forceinline__ double axpy_rn(double a, double s, double b) { return __dadd_rn(a, __dmul_rn(s, b)); }
+
+// ---------------------------------------------------------- kernel (fp64)
+// Quintic spline (kernel.hpp:47-75), branch-free: the missing branches add exact zeros.
+__device__ __forceinline__ double shape_q(double q) {
+  const double a = 3.0 - q;
+  const double b = fmax(2.0 - q, 0.0);
+  const double c = fmax(1.0 - q, 0.0);
+  const double a2 = a * a, b2 = b * b, c2 = c * c;
+  return a2 * a2 * a - 6.0 * (b2 * b2 * b) + 15.0 * (c2 * c2 * c);
+}
+__device__ __forceinline__ double shape_deriv_q(double q) {
+  const double a = 3.0 - q;
+  const double b = fmax(2.0 - q, 0.0);
+  const double c = fmax(1.0 - q, 0.0);
+  const double a2 = a * a, b2 = b * b, c2 = c * c;
+  return -5.0 * (a2 * a2) + 30.0 * (b2 * b2) - 75.0 * (c2 * c2);
+}
+
+// fast fp64 reciprocal: MUFU seed + 2 Newton steps (~1 ulp; tolerance stages only)
+__device__ __forceinline__ double rcp_fast(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  return y;
+}
+
+// ------------------------------------------------------------ quaternion
+struct Quat {
+  double w, x, y, z;
+};
+__device__ __forceinline__ double3 cross3(double3 a, double3 b) {
+  return make_double3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+// rotate (quaternion.hpp:55-59): t = 2 u x p; p + w t + u x t
+__device__ __forceinline__ double3 qrotate(const Quat& q, double3 p) {
+  const double3 u = make_double3(q.x, q.y, q.z);
+  double3 t = cross3(u, p);
+  t.x *= 2.0; t.y *= 2.0; t.z *= 2.0;
+  const double3 c = cross3(u, t);
+  return make_double3(p.x + q.w * t.x + c.x, p.y + q.w * t.y + c.y, p.z + q.w * t.z + c.z);
+}
+__device__ __forceinline__ Quat qmul(const Quat& a, const Quat& b) {  // quaternion.hpp:27-32
+  return {a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z, a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y,
+          a.w * b.y - a.x * b.z + a.y * b.w + a.z * b.x, a.w * b.z + a.x * b.y - a.y * b.x + a.z * b.w};
+}
+// orientation_step (quaternion.hpp:67-76) with quat_exp (37-50)
+__device__ __forceinline__ Quat orientation_step(const Quat& q, double3 w, double dt) {
+  const double3 phi = make_double3(dt * w.x, dt * w.y, dt * w.z);
+  const double ang = sqrt(phi.x * phi.x + phi.y * phi.y + phi.z * phi.z);
+  double hs, ch;
+  if (ang < 1e-8) {
+    const double a2 = ang * ang;
+    hs = 0.5 - a2 / 48.0;
+    ch = 1.0 - a2 / 8.0;
+  } else {
+    double s, c;
+    sincos(0.5 * ang, &s, &c);
+    hs = s / ang;
+    ch = c;
+  }
+  const Quat tr{ch, hs * phi.x, hs * phi.y, hs * phi.z};
+  Quat r = qmul(tr, q);
+  const double nrm = sqrt(r.w * r.w + r.x * r.x + r.y * r.y + r.z * r.z);
+  return {r.w / nrm, r.x / nrm, r.y / nrm, r.z / nrm};
+}
+
+// --------------------------------------------- compensated sums (kahan.hpp)
+// Neumaier accumulator (kahan.hpp:9-22) and an error-free pairwise merge for
+// warp trees: merge((s1,c1),(s2,c2)) = TwoSum(s1,s2) + (c1 + c2).
+struct KSum {
+  double s, c;
+  __device__ __forceinline__ void add(double x) {
+    const double t = __dadd_rn(s, x);
+    if (fabs(s) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), x));
+    else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), s));
+    s = t;
+  }
+  __device__ __forceinline__ void merge(double s2, double c2) {
+    const double t = __dadd_rn(s, s2);
+    const double bp = __dsub_rn(t, s);
+    const double e = __dadd_rn(__dsub_rn(s, __dsub_rn(t, bp)), __dsub_rn(s2, bp));
+    s = t;
+    c = __dadd_rn(__dadd_rn(c, c2), e);
+  }
+  __device__ __forceinline__ double value() const { return __dadd_rn(s, c); }
+};
+
+__device__ __forceinline__ KSum warp_merge(KSum k) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double s2 = __shfl_down_sync(0xffffffffu, k.s, o);
+    const double c2 = __shfl_down_sync(0xffffffffu, k.c, o);
+    k.merge(s2, c2);
+  }
+  return k;
+}
+
+// ------------------------------------------------------- device error word
+enum : uint32_t { kErrEscape = 1u, kErrCoincident = 2u, kErrNaN = 4u, kErrOverflow = 8u };
+
+struct DevFlags {
+  unsigned long long max_disp2_bits;  // atomicMax on non-negative double bits
+  unsigned long long umax2_bits;
+  uint32_t err;
+  uint32_t err_gid;                   // min gid involved (atomicMin)
+  uint32_t err_gid2;
+  uint32_t max_count;                 // neighbour list max length
+  uint32_t n_events;                  // transition events
+  uint32_t changed;                   // label propagation
+  uint32_t pad[2];
+};
+
+__device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, double v) {
+  atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+
+}  // namespace sphg
+
+#define SPHG_CUDA_CHECK(expr)                                                 \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess) throw ::sphg::CudaError(_e, #expr, __FILE__, __LINE__); \
+  } while (0)

@@ -1,0 +1,145 @@
+// context.cuh — device-resident state of one sphg context (one GPU / one rank).
+//
+// HBM layout: every per-particle array is in cell-sorted order
+// (key = (cell, gid)) and packed for the pair-gather kernels:
+//   G0 = (x, y, z, V^2)        interaction volume squared (fluid: (m/rho)^2, wall/rigid: V_w^2)
+//   G1 = (u, rho)              interaction velocity/density (fluid: u^{n+1/2}, rho; wall/rigid: u~_w, rho_w)
+//   G2 = (du, p)               du = u_adv - u (TVF A term; 0 for wall/rigid), pressure (wall/rigid: p_w)
+//   V4 = (vel, mass)           true velocity (fluid u^n between steps, rigid u_r, boundary 0)
+//   A4 = (acc, -)  B4 = (acc_bg, -)  F4 = (f_r, -)  X4 = (chi, -)  R4 = (pos at last rebuild, -)
+//   H2 = (T, V_heat)           temperature and the conduction volume V_b (0 for non-Dirichlet walls)
+//   kmd (kind|mat|dirichlet), group, gid : uint32
+// Verlet candidates are ELL: nbr[k * N + i] for k < cnt[i] (coalesced across i).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sphg {
+
+struct CudaError {
+  cudaError_t code;
+  std::string what;
+  CudaError(cudaError_t c, const char* expr, const char* file, int line)
+      : code(c), what(std::string(cudaGetErrorString(c)) + " at " + file + ":" + std::to_string(line) + " (" + expr + ")") {}
+};
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    free();
+    if (count == 0) return;
+    SPHG_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct Particles {  // one buffer set (double-buffered for the rebuild reorder)
+  DBuf<double4> G0, G1, G2, V4, A4, B4, F4, X4, R4;
+  DBuf<double2> H2;
+  DBuf<double> dTdt, p_static;
+  DBuf<uint32_t> kmd, group, gid;
+  void alloc(size_t n) {
+    G0.alloc(n); G1.alloc(n); G2.alloc(n); V4.alloc(n); A4.alloc(n); B4.alloc(n); F4.alloc(n);
+    X4.alloc(n); R4.alloc(n); H2.alloc(n); dTdt.alloc(n); p_static.alloc(n);
+    kmd.alloc(n); group.alloc(n); gid.alloc(n);
+  }
+  void free() {
+    G0.free(); G1.free(); G2.free(); V4.free(); A4.free(); B4.free(); F4.free(); X4.free(); R4.free();
+    H2.free(); dTdt.free(); p_static.free(); kmd.free(); group.free(); gid.free();
+  }
+};
+
+struct Ctx {
+  sphg_params params{};
+  DevParams P{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  size_t n = 0;            // particles
+  size_t nb = 0;           // bodies (live or dead)
+  Particles cur, alt;      // alt = reorder target / scratch
+  DBuf<double2> H2new;     // heat double buffer
+  DBuf<sphg_body> bodies;
+  size_t bodies_cap = 0;
+  // rebuild scratch
+  DBuf<unsigned long long> keys, keys_alt;
+  DBuf<uint32_t> vals, vals_alt, hist, scan_tmp;
+  DBuf<uint32_t> cell_start, cell_end, cell_key;
+  int64_t ncells = 0;
+  // neighbour list (ELL)
+  DBuf<uint32_t> nbr, cnt;
+  int cap = 0;
+  // body-major rigid index
+  DBuf<uint32_t> ridx, body_start;
+  size_t nrigid = 0;
+  // transitions scratch
+  DBuf<uint32_t> ev_idx, ev_flag, label, tscratch;
+  // flags
+  DevFlags* dflags = nullptr;   // device
+  DevFlags* hflags = nullptr;   // pinned host mirror
+  bool built = false;
+  bool have_state = false;
+  double t = 0.0;
+  int64_t steps = 0, rebuilds = 0, n_melt = 0, n_solid = 0, launches = 0;
+  double max_disp = 0.0, u_max = 0.0;
+  int64_t pairs = 0;
+  int max_count = 0;
+  bool timing = false;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  double stage_ms[10] = {0};
+  std::string err;
+  // host staging for body table (pinned)
+  sphg_body* hbodies = nullptr;
+  size_t hbodies_cap = 0;
+  void* hstage = nullptr;          // 2 pinned staging slots (upload/download)
+  cudaEvent_t slot_ev[2] = {nullptr, nullptr};
+  unsigned long long* dcount = nullptr;  // pair counters
+  cudaEvent_t step_ev[2] = {nullptr, nullptr};
+  double last_step_ms = 0.0;
+};
+
+// ------------------------------------------------------------ launchers
+// radix_sort.cu
+size_t radix_scratch_words(size_t n);
+// Sorts (keys, vals) by the low `bits` bits of keys, stable.  Returns true if
+// the result ended in the *_alt buffers.
+bool radix_sort_pairs(unsigned long long* keys, uint32_t* vals, unsigned long long* keys_alt, uint32_t* vals_alt,
+                      size_t n, int bits, uint32_t* hist, uint32_t* scan_tmp, cudaStream_t s, int64_t* launches);
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, uint32_t* tmp, cudaStream_t s,
+                        int64_t* launches);
+
+// kernels_rebuild.cu
+void launch_rebuild(Ctx& c);
+void launch_rigid_index(Ctx& c);
+
+// kernels_step.cu
+void launch_body_kick(Ctx& c);
+void launch_kick_drift(Ctx& c);
+void launch_density(Ctx& c);
+void launch_heat(Ctx& c);
+void launch_extrapolate(Ctx& c);
+void launch_forces(Ctx& c);
+void launch_bodies(Ctx& c);
+void launch_final_kick(Ctx& c);
+void launch_mass(Ctx& c, const uint32_t* body_mask);
+void gather_by_gid(Ctx& c);          // cur[k] <- alt[gid[k]] for every field but gid/R4
+bool displacement_exceeds(Ctx& c);   // max |r - r_ref| > half skin (syncs)
+void iota_gid(Ctx& c);
+void count_pairs(Ctx& c, int64_t* candidates, int64_t* interacting);
+
+// kernels_transition.cu
+int launch_transitions(Ctx& c);  // 0 ok, else error code
+
+inline int grid_for(size_t n, int block) { return (int)((n + block - 1) / block); }
+
+}  // namespace sphg

@@ -1,0 +1,242 @@
+// kernels_rebuild.cu — cell binning, radix sort, SoA reorder and Verlet
+// neighbour-list build (SPEC:154-166 DomainGrid/NeighborList, 187-195
+// build_pairs, 212-214 Verlet skin/inclusive cut-off/rebinning).
+//
+// Cell key [P1]: c_a = floor((x_a - lo_a) * inv_edge_a) clamped to [0, n_a),
+// linearised (c0*n1 + c1)*n2 + c2.  Keys are scattered into gid order and
+// stably radix-sorted, so the particle order is canonical (cell, gid) — the
+// same on any GPU count and identical to the oracle's (bit-exact test).
+// Candidates: j != i, not both boundary, r^2 <= (r_c + 0.1 h)^2 evaluated as
+// (dx*dx + dy*dy) + dz*dz in round-to-nearest without contraction [P2].
+#include <algorithm>
+
+#include "context.cuh"
+
+namespace sphg {
+
+namespace {
+
+__device__ __forceinline__ int64_t cell_of(const DevParams& P, double x, double y, double z, uint32_t* escaped) {
+  const double xs[3] = {x, y, z};
+  int64_t c[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (!P.periodic[a] && (xs[a] < P.lo[a] || xs[a] > P.hi[a])) *escaped = 1;
+    int64_t k = (int64_t)floor(__dmul_rn(__dsub_rn(xs[a], P.lo[a]), P.inv_edge[a]));
+    k = k < 0 ? 0 : (k >= P.ncell[a] ? P.ncell[a] - 1 : k);
+    c[a] = k;
+  }
+  return (c[0] * P.ncell[1] + c[1]) * P.ncell[2] + c[2];
+}
+
+__global__ void k_keys_by_gid(const __grid_constant__ DevParams P, const double4* __restrict__ G0,
+                              const uint32_t* __restrict__ gid, size_t n, unsigned long long* __restrict__ keys,
+                              uint32_t* __restrict__ vals, DevFlags* __restrict__ fl) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double4 p = G0[k];
+  uint32_t esc = 0;
+  const int64_t c = cell_of(P, p.x, p.y, p.z, &esc);
+  const uint32_t g = gid[k];
+  keys[g] = (unsigned long long)c;
+  vals[g] = (uint32_t)k;
+  if (esc) {
+    atomicOr(&fl->err, kErrEscape);
+    atomicMin(&fl->err_gid, g);
+  }
+}
+
+// gather every per-particle field through the permutation; pos_ref := pos
+__global__ void k_reorder(const uint32_t* __restrict__ perm, const unsigned long long* __restrict__ skeys, size_t n,
+                          Particles src, Particles dst, uint32_t* __restrict__ cell_key) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t o = perm[k];
+  const double4 g0 = src.G0.p[o];
+  dst.G0.p[k] = g0;
+  dst.R4.p[k] = g0;
+  dst.G1.p[k] = src.G1.p[o];
+  dst.G2.p[k] = src.G2.p[o];
+  dst.V4.p[k] = src.V4.p[o];
+  dst.A4.p[k] = src.A4.p[o];
+  dst.B4.p[k] = src.B4.p[o];
+  dst.F4.p[k] = src.F4.p[o];
+  dst.X4.p[k] = src.X4.p[o];
+  dst.H2.p[k] = src.H2.p[o];
+  dst.dTdt.p[k] = src.dTdt.p[o];
+  dst.p_static.p[k] = src.p_static.p[o];
+  dst.kmd.p[k] = src.kmd.p[o];
+  dst.group.p[k] = src.group.p[o];
+  dst.gid.p[k] = src.gid.p[o];
+  cell_key[k] = (uint32_t)skeys[k];
+}
+
+__global__ void k_cell_ranges(const uint32_t* __restrict__ key, size_t n, uint32_t* __restrict__ cstart,
+                              uint32_t* __restrict__ cend) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t c = key[k];
+  if (k == 0 || key[k - 1] != c) cstart[c] = (uint32_t)k;
+  if (k == n - 1 || key[k + 1] != c) cend[c] = (uint32_t)(k + 1);
+}
+
+__global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ DevParams P, const double4* __restrict__ G0,
+                                                      const uint32_t* __restrict__ kmd,
+                                                      const uint32_t* __restrict__ cell_key,
+                                                      const uint32_t* __restrict__ cstart,
+                                                      const uint32_t* __restrict__ cend, uint32_t* __restrict__ nbr,
+                                                      uint32_t* __restrict__ cnt, int cap, size_t n,
+                                                      DevFlags* __restrict__ fl) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 pi = G0[i];
+  const bool bi = kind_of(kmd[i]) == SPHG_BOUNDARY;
+  const int64_t c = cell_key[i];
+  const int64_t nz = P.ncell[2], ny = P.ncell[1];
+  const int64_t cz = c % nz, cy = (c / nz) % ny, cx = c / (nz * ny);
+  uint32_t count = 0;
+  for (int ox = -1; ox <= 1; ++ox) {
+    int64_t qx = cx + ox;
+    if (qx < 0 || qx >= P.ncell[0]) {
+      if (!P.periodic[0]) continue;
+      qx = (qx + P.ncell[0]) % P.ncell[0];
+    }
+    for (int oy = -1; oy <= 1; ++oy) {
+      int64_t qy = cy + oy;
+      if (qy < 0 || qy >= ny) {
+        if (!P.periodic[1]) continue;
+        qy = (qy + ny) % ny;
+      }
+      for (int oz = -1; oz <= 1; ++oz) {
+        int64_t qz = cz + oz;
+        if (qz < 0 || qz >= nz) {
+          if (!P.periodic[2]) continue;
+          qz = (qz + nz) % nz;
+        }
+        const int64_t cj = (qx * ny + qy) * nz + qz;
+        const uint32_t j0 = cstart[cj], j1 = cend[cj];
+        for (uint32_t j = j0; j < j1; ++j) {
+          if (j == i) continue;
+          if (bi && kind_of(kmd[j]) == SPHG_BOUNDARY) continue;
+          const double4 pj = G0[j];
+          const double3 d = mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z);
+          if (r2_exact(d) <= P.rv2) {
+            if ((int)count < cap) nbr[(size_t)count * n + i] = j;
+            ++count;
+          }
+        }
+      }
+    }
+  }
+  cnt[i] = count;
+  atomicMax(&fl->max_count, count);
+}
+
+// ------------------------------------------------------- rigid index
+__global__ void k_rigid_flags(const uint32_t* __restrict__ kmd, size_t n, uint32_t* __restrict__ flag) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) flag[k] = kind_of(kmd[k]) == SPHG_RIGID ? 1u : 0u;
+}
+
+__global__ void k_rigid_compact(const uint32_t* __restrict__ kmd, const uint32_t* __restrict__ group,
+                                const uint32_t* __restrict__ gid, const uint32_t* __restrict__ pos, size_t n,
+                                int gbits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || kind_of(kmd[k]) != SPHG_RIGID) return;
+  const uint32_t s = pos[k];
+  keys[s] = ((unsigned long long)group[k] << gbits) | gid[k];
+  vals[s] = (uint32_t)k;
+}
+
+__global__ void k_body_ranges(const unsigned long long* __restrict__ keys, size_t m, int gbits,
+                              uint32_t* __restrict__ bstart, uint32_t* __restrict__ bend) {
+  const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  const unsigned long long g = keys[s] >> gbits;
+  if (s == 0 || (keys[s - 1] >> gbits) != g) bstart[g] = (uint32_t)s;
+  if (s == m - 1 || (keys[s + 1] >> gbits) != g) bend[g] = (uint32_t)(s + 1);
+}
+
+int bits_for(uint64_t maxval) {  // bits needed to represent values in [0, maxval]
+  int b = 0;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+}  // namespace
+
+void launch_rigid_index(Ctx& c) {
+  const size_t n = c.n;
+  cudaStream_t s = c.stream;
+  c.ridx.alloc(std::max<size_t>(n, 1));
+  c.body_start.alloc(2 * std::max<size_t>(c.nb, 1));
+  uint32_t* flag = c.vals_alt.p;  // scratch
+  uint32_t* pos = c.vals.p;
+  k_rigid_flags<<<grid_for(n, 256), 256, 0, s>>>(c.cur.kmd.p, n, flag);
+  exclusive_scan_u32(flag, pos, n, c.scan_tmp.p, s, &c.launches);
+  uint32_t last_pos = 0, last_flag = 0;
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&last_pos, pos + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&last_flag, flag + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+  const size_t m = (size_t)last_pos + last_flag;
+  c.nrigid = m;
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.body_start.p, 0, 2 * std::max<size_t>(c.nb, 1) * sizeof(uint32_t), s));
+  c.launches += 2;
+  if (m == 0) return;
+  const int gbits = bits_for(n > 0 ? n - 1 : 0);
+  k_rigid_compact<<<grid_for(n, 256), 256, 0, s>>>(c.cur.kmd.p, c.cur.group.p, c.cur.gid.p, pos, n, gbits, c.keys.p,
+                                                   c.vals_alt.p);
+  // vals_alt now holds particle indices (flag scratch consumed by the scan already)
+  const int bits = gbits + bits_for(c.nb > 0 ? c.nb - 1 : 0);
+  unsigned long long* k0 = c.keys.p;
+  uint32_t* v0 = c.vals_alt.p;
+  const bool flipped = radix_sort_pairs(k0, v0, c.keys_alt.p, c.vals.p, m, bits, c.hist.p, c.scan_tmp.p, s, &c.launches);
+  unsigned long long* ks = flipped ? c.keys_alt.p : k0;
+  uint32_t* vs = flipped ? c.vals.p : v0;
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(c.ridx.p, vs, m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  k_body_ranges<<<grid_for(m, 256), 256, 0, s>>>(ks, m, gbits, c.body_start.p, c.body_start.p + c.nb);
+  c.launches += 3;
+}
+
+void launch_rebuild(Ctx& c) {
+  const size_t n = c.n;
+  cudaStream_t s = c.stream;
+  if (n == 0) return;
+  // 1. keys in gid order
+  k_keys_by_gid<<<grid_for(n, 256), 256, 0, s>>>(c.P, c.cur.G0.p, c.cur.gid.p, n, c.keys.p, c.vals.p, c.dflags);
+  // 2. stable radix sort by cell
+  const int bits = bits_for((uint64_t)(c.ncells - 1));
+  const bool flipped = radix_sort_pairs(c.keys.p, c.vals.p, c.keys_alt.p, c.vals_alt.p, n, std::max(bits, 1), c.hist.p,
+                                        c.scan_tmp.p, s, &c.launches);
+  const unsigned long long* skeys = flipped ? c.keys_alt.p : c.keys.p;
+  const uint32_t* perm = flipped ? c.vals_alt.p : c.vals.p;
+  // 3. reorder into the alternate buffer set, swap
+  k_reorder<<<grid_for(n, 256), 256, 0, s>>>(perm, skeys, n, c.cur, c.alt, c.cell_key.p);
+  std::swap(c.cur, c.alt);
+  // 4. cell ranges
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.cell_start.p, 0, c.ncells * sizeof(uint32_t), s));
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.cell_end.p, 0, c.ncells * sizeof(uint32_t), s));
+  k_cell_ranges<<<grid_for(n, 256), 256, 0, s>>>(c.cell_key.p, n, c.cell_start.p, c.cell_end.p);
+  c.launches += 5;
+  // 5. neighbour list, grown on overflow
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    if (c.cap <= 0) c.cap = c.params.nlist_capacity > 0 ? c.params.nlist_capacity : 144;
+    c.nbr.alloc((size_t)c.cap * n);
+    SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->max_count, 0, sizeof(uint32_t), s));
+    k_build_nlist<<<grid_for(n, 128), 128, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_key.p, c.cell_start.p,
+                                                   c.cell_end.p, c.nbr.p, c.cnt.p, c.cap, n, c.dflags);
+    c.launches += 2;
+    uint32_t mc = 0;
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(&mc, &c.dflags->max_count, 4, cudaMemcpyDeviceToHost, s));
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+    c.max_count = (int)mc;
+    if ((int)mc <= c.cap) break;
+    c.cap = (int)((mc + 15) / 8 * 8);
+    c.nbr.free();
+  }
+  launch_rigid_index(c);
+  c.built = true;
+  c.rebuilds++;
+}
+
+}  // namespace sphg

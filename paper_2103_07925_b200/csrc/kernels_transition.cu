@@ -1,0 +1,391 @@
+// kernels_transition.cu — temperature-driven melt/solidify reclassification
+// on the device.
+//
+// Pinned rules [P12] (identical in oracle/sph_oracle.cpp stage_transitions):
+//  * detect: rigid T > T_t -> melt (into melt_target); fluid T < T_t -> solidify; strict
+//  * batch is a set: melting particles are no attach targets, solidifying ones neither
+//  * melt: kind F, velocity u_k + w_k x r_rk, acc = 0
+//  * solidify: attach to the body of the nearest pre-batch rigid particle within r_c
+//    (ties by gid), else spawn; spawned ids = nb + rank in gid order
+//  * split bodies that lost particles: components with adjacency r <= 1.5 dx, found
+//    by min-gid label propagation; the min-gid component keeps the id, others get
+//    new ids ordered by (source body, min gid)
+//  * affected bodies: reduce_mass_quantities (chi recomputed), u_k = u'_k + w x (r_k - r'_k),
+//    members follow the rigid motion, then reduce_force_torque for all bodies.
+#include <algorithm>
+
+#include "context.cuh"
+
+namespace sphg {
+
+namespace {
+
+__device__ __forceinline__ Quat body_q(const sphg_body& b) { return {b.q[0], b.q[1], b.q[2], b.q[3]}; }
+
+__global__ void k_detect(const __grid_constant__ DevParams P, Particles D, size_t n, uint32_t* __restrict__ ev,
+                         DevFlags* __restrict__ fl) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t kmd = D.kmd.p[k];
+  const uint32_t kind = kind_of(kmd);
+  const DevMat& M = P.mat[mat_of(kmd)];
+  uint32_t e = 0;
+  if (M.has_Tt) {
+    const double T = D.H2.p[k].x;
+    if (kind == SPHG_RIGID && M.melt >= 0 && T > M.T_t) e = 1;
+    else if (kind == SPHG_FLUID && M.solid >= 0 && T < M.T_t) e = 2;
+  }
+  ev[k] = e;
+  if (e == 1) atomicAdd(&fl->n_events, 1u);
+  if (e == 2) atomicAdd(&fl->pad[0], 1u);
+}
+
+__global__ void k_melt(const __grid_constant__ DevParams P, Particles D, size_t n, const uint32_t* __restrict__ ev,
+                       const sphg_body* __restrict__ B, uint32_t* __restrict__ bmask, uint32_t* __restrict__ blost) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || ev[k] != 1) return;
+  const uint32_t kmd = D.kmd.p[k];
+  const uint32_t body = D.group.p[k];
+  const sphg_body& b = B[body];
+  const double4 x = D.X4.p[k];
+  const double3 rk = qrotate(body_q(b), make_double3(x.x, x.y, x.z));
+  const double3 w = cross3(make_double3(b.omega[0], b.omega[1], b.omega[2]), rk);
+  const double3 u = make_double3(b.vel[0] + w.x, b.vel[1] + w.y, b.vel[2] + w.z);
+  const int tgt = P.mat[mat_of(kmd)].melt;
+  const double m = D.V4.p[k].w;
+  const double rho0 = P.mat[tgt].rho0;
+  D.kmd.p[k] = make_kmd(SPHG_FLUID, (uint32_t)tgt, dir_of(kmd));
+  D.group.p[k] = 0;
+  D.V4.p[k] = make_double4(u.x, u.y, u.z, m);
+  const double V = m / rho0;
+  reinterpret_cast<double*>(&D.G0.p[k])[3] = V * V;
+  D.G1.p[k] = make_double4(u.x, u.y, u.z, rho0);
+  D.G2.p[k] = make_double4(0, 0, 0, 0);
+  D.A4.p[k] = make_double4(0, 0, 0, 0);
+  D.B4.p[k] = make_double4(0, 0, 0, 0);
+  D.F4.p[k] = make_double4(0, 0, 0, 0);
+  D.X4.p[k] = make_double4(0, 0, 0, 0);
+  D.p_static.p[k] = 0.0;
+  reinterpret_cast<double*>(&D.H2.p[k])[1] = V;
+  bmask[body] = 1;
+  blost[body] = 1;
+}
+
+__global__ void k_flag_eq(const uint32_t* __restrict__ ev, size_t n, uint32_t v, uint32_t* __restrict__ out) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) out[k] = ev[k] == v ? 1u : 0u;
+}
+
+__global__ void k_compact_by_gid(const uint32_t* __restrict__ ev, const uint32_t* __restrict__ pos, size_t n, uint32_t v,
+                                 const uint32_t* __restrict__ gid, unsigned long long* __restrict__ keys,
+                                 uint32_t* __restrict__ vals) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || ev[k] != v) return;
+  keys[pos[k]] = gid[k];
+  vals[pos[k]] = (uint32_t)k;
+}
+
+// nearest pre-batch rigid particle within r_c (r^2, gid), from the Verlet list
+__global__ void k_solid_target(const __grid_constant__ DevParams P, Particles D, const uint32_t* __restrict__ list,
+                               size_t m, const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ cnt, size_t n,
+                               int* __restrict__ target, uint32_t* __restrict__ spawn) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const uint32_t i = list[e];
+  const double4 pi = D.G0.p[i];
+  double best = 1e300;
+  uint32_t bg = 0xffffffffu;
+  int tb = -1;
+  for (uint32_t k = 0; k < cnt[i]; ++k) {
+    const uint32_t j = nbr[(size_t)k * n + i];
+    if (kind_of(D.kmd.p[j]) != SPHG_RIGID) continue;
+    const double4 pj = D.G0.p[j];
+    const double r2 = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z));
+    if (r2 > P.rc2) continue;
+    const uint32_t gj = D.gid.p[j];
+    if (r2 < best || (r2 == best && gj < bg)) {
+      best = r2;
+      bg = gj;
+      tb = (int)D.group.p[j];
+    }
+  }
+  target[e] = tb;
+  spawn[e] = tb < 0 ? 1u : 0u;
+}
+
+__global__ void k_solid_apply(const __grid_constant__ DevParams P, Particles D, const uint32_t* __restrict__ list,
+                              size_t m, const int* __restrict__ target, const uint32_t* __restrict__ rank, size_t nb0,
+                              sphg_body* __restrict__ B, uint32_t* __restrict__ bmask, uint32_t* __restrict__ src) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const uint32_t i = list[e];
+  const uint32_t kmd = D.kmd.p[i];
+  const int tgt = P.mat[mat_of(kmd)].solid;
+  uint32_t body;
+  const double4 v = D.V4.p[i];
+  if (target[e] >= 0) {
+    body = (uint32_t)target[e];
+  } else {
+    body = (uint32_t)(nb0 + rank[e]);
+    sphg_body nbd;
+    memset(&nbd, 0, sizeof(nbd));
+    nbd.q[0] = 1.0;
+    nbd.vel[0] = v.x;
+    nbd.vel[1] = v.y;
+    nbd.vel[2] = v.z;
+    nbd.material = tgt;
+    nbd.mobile = 1;
+    nbd.alive = 1;
+    B[body] = nbd;
+    src[body] = body;
+  }
+  bmask[body] = 1;
+  const double rho0 = P.mat[tgt].rho0;
+  D.kmd.p[i] = make_kmd(SPHG_RIGID, (uint32_t)tgt, dir_of(kmd));
+  D.group.p[i] = body;
+  D.A4.p[i] = make_double4(0, 0, 0, 0);
+  D.B4.p[i] = make_double4(0, 0, 0, 0);
+  D.p_static.p[i] = 0.0;
+  reinterpret_cast<double*>(&D.H2.p[i])[1] = v.w / rho0;
+}
+
+__global__ void k_iota(uint32_t* __restrict__ a, size_t n, size_t from) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) a[from + k] = (uint32_t)(from + k);
+}
+
+// ---------------------------------------------------- connected components
+__global__ void k_label_init(Particles D, size_t n, const uint32_t* __restrict__ blost, uint32_t* __restrict__ label) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  label[k] = (kind_of(D.kmd.p[k]) == SPHG_RIGID && blost[D.group.p[k]]) ? D.gid.p[k] : 0xffffffffu;
+}
+
+__global__ void k_label_iter(const __grid_constant__ DevParams P, Particles D, size_t n,
+                             const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ cnt,
+                             uint32_t* __restrict__ label, double adj2, DevFlags* __restrict__ fl) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t l = label[i];
+  if (l == 0xffffffffu) return;
+  const uint32_t body = D.group.p[i];
+  const double4 pi = D.G0.p[i];
+  uint32_t best = l;
+  for (uint32_t k = 0; k < cnt[i]; ++k) {
+    const uint32_t j = nbr[(size_t)k * n + i];
+    if (kind_of(D.kmd.p[j]) != SPHG_RIGID || D.group.p[j] != body) continue;
+    const double4 pj = D.G0.p[j];
+    if (r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) > adj2) continue;
+    best = min(best, label[j]);
+  }
+  if (best < l) {
+    atomicMin(&label[i], best);
+    fl->changed = 1;
+  }
+}
+
+__global__ void k_split_roots(Particles D, size_t n, const uint32_t* __restrict__ label,
+                              const uint32_t* __restrict__ ridx, const uint32_t* __restrict__ bstart, int gbits,
+                              unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+                              DevFlags* __restrict__ fl) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t l = label[i];
+  if (l == 0xffffffffu || l != D.gid.p[i]) return;
+  const uint32_t body = D.group.p[i];
+  const uint32_t minimal = D.gid.p[ridx[bstart[body]]];
+  if (l == minimal) return;
+  const uint32_t s = atomicAdd(&fl->pad[1], 1u);
+  keys[s] = ((unsigned long long)body << gbits) | l;
+  vals[s] = body;
+}
+
+__global__ void k_split_bodies(const unsigned long long* __restrict__ keys, size_t m, int gbits, size_t nb0,
+                               sphg_body* __restrict__ B, uint32_t* __restrict__ bmask, uint32_t* __restrict__ src) {
+  const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  const uint32_t body = (uint32_t)(keys[s] >> gbits);
+  B[nb0 + s] = B[body];
+  bmask[nb0 + s] = 1;
+  src[nb0 + s] = body;
+}
+
+__global__ void k_split_relabel(Particles D, size_t n, const uint32_t* __restrict__ label,
+                                const uint32_t* __restrict__ ridx, const uint32_t* __restrict__ bstart,
+                                const unsigned long long* __restrict__ keys, size_t m, int gbits, size_t nb0) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t l = label[i];
+  if (l == 0xffffffffu) return;
+  const uint32_t body = D.group.p[i];
+  if (l == D.gid.p[ridx[bstart[body]]]) return;
+  const unsigned long long key = ((unsigned long long)body << gbits) | l;
+  size_t lo = 0, hi = m;
+  while (lo < hi) {
+    const size_t mid = (lo + hi) / 2;
+    if (keys[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  D.group.p[i] = (uint32_t)(nb0 + lo);
+}
+
+// u_k = u'_k + w'_k x (r_k - r'_k) for affected, non-spawned bodies
+__global__ void k_post_velocity(const __grid_constant__ DevParams P, sphg_body* __restrict__ B,
+                                const sphg_body* __restrict__ old, const uint32_t* __restrict__ bmask,
+                                const uint32_t* __restrict__ src, size_t nb, size_t nb0) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb || !bmask[k]) return;
+  sphg_body& b = B[k];
+  if (!b.alive) return;
+  const uint32_t s = src[k];
+  if (k >= nb0 && s == k) return;  // spawned: keeps the particle's velocity, w = 0
+  const sphg_body& o = old[s];
+  const double3 sh = mimg3(P, b.com[0], b.com[1], b.com[2], o.com[0], o.com[1], o.com[2]);
+  const double3 w = cross3(make_double3(o.omega[0], o.omega[1], o.omega[2]), sh);
+  b.vel[0] = o.vel[0] + w.x;
+  b.vel[1] = o.vel[1] + w.y;
+  b.vel[2] = o.vel[2] + w.z;
+}
+
+__global__ void k_member_velocity(Particles D, size_t n, const sphg_body* __restrict__ B,
+                                  const uint32_t* __restrict__ bmask) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || kind_of(D.kmd.p[k]) != SPHG_RIGID) return;
+  const uint32_t body = D.group.p[k];
+  if (!bmask[body]) return;
+  const sphg_body& b = B[body];
+  const double4 x = D.X4.p[k];
+  const double3 rk = qrotate(body_q(b), make_double3(x.x, x.y, x.z));
+  const double3 w = cross3(make_double3(b.omega[0], b.omega[1], b.omega[2]), rk);
+  const double m = D.V4.p[k].w;
+  D.V4.p[k] = make_double4(b.vel[0] + w.x, b.vel[1] + w.y, b.vel[2] + w.z, m);
+}
+
+int bits_for(uint64_t maxval) {
+  int b = 0;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+uint32_t read_u32(Ctx& c, const uint32_t* p) {
+  uint32_t v = 0;
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&v, p, 4, cudaMemcpyDeviceToHost, c.stream));
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  return v;
+}
+
+void grow_bodies(Ctx& c, size_t need) {
+  if (need <= c.bodies_cap && c.bodies.p) return;
+  const size_t cap = std::max<size_t>(need * 2, 64);
+  sphg_body* nb = nullptr;
+  SPHG_CUDA_CHECK(cudaMalloc(&nb, cap * sizeof(sphg_body)));
+  SPHG_CUDA_CHECK(cudaMemsetAsync(nb, 0, cap * sizeof(sphg_body), c.stream));
+  if (c.bodies.p && c.nb)
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(nb, c.bodies.p, c.nb * sizeof(sphg_body), cudaMemcpyDeviceToDevice, c.stream));
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  c.bodies.free();
+  c.bodies.p = nb;
+  c.bodies.n = cap;
+  c.bodies_cap = cap;
+}
+
+}  // namespace
+
+int launch_transitions(Ctx& c) {
+  const size_t n = c.n;
+  cudaStream_t s = c.stream;
+  if (n == 0) return 0;
+  c.ev_flag.alloc(n);
+  SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->n_events, 0, sizeof(uint32_t), s));
+  SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->pad[0], 0, 2 * sizeof(uint32_t), s));
+  k_detect<<<grid_for(n, 256), 256, 0, s>>>(c.P, c.cur, n, c.ev_flag.p, c.dflags);
+  c.launches++;
+  const uint32_t nmelt = read_u32(c, &c.dflags->n_events);
+  const uint32_t nsolid = read_u32(c, &c.dflags->pad[0]);
+  if (nmelt == 0 && nsolid == 0) return 0;
+  if (!c.built) launch_rebuild(c);
+  const size_t nb0 = c.nb;
+  // capacity: spawned + split products are bounded by the rigid count after the batch
+  grow_bodies(c, nb0 + nsolid + c.nrigid + nsolid + 1);
+  const size_t cap = c.bodies_cap;
+  DBuf<sphg_body> old;
+  old.alloc(cap);
+  c.tscratch.alloc(3 * cap + 3 * (size_t)std::max<uint32_t>(nsolid, 1));
+  uint32_t* bmask = c.tscratch.p;
+  uint32_t* blost = bmask + cap;
+  uint32_t* src = blost + cap;
+  int* target = reinterpret_cast<int*>(src + cap);
+  uint32_t* spawn = reinterpret_cast<uint32_t*>(target + std::max<uint32_t>(nsolid, 1));
+  uint32_t* rank = spawn + std::max<uint32_t>(nsolid, 1);
+  SPHG_CUDA_CHECK(cudaMemsetAsync(bmask, 0, 2 * cap * sizeof(uint32_t), s));
+  k_iota<<<grid_for(cap, 256), 256, 0, s>>>(src, cap, 0);
+  if (nb0) SPHG_CUDA_CHECK(cudaMemcpyAsync(old.p, c.bodies.p, nb0 * sizeof(sphg_body), cudaMemcpyDeviceToDevice, s));
+  // 1. melt
+  if (nmelt) k_melt<<<grid_for(n, 256), 256, 0, s>>>(c.P, c.cur, n, c.ev_flag.p, c.bodies.p, bmask, blost);
+  // 2. solidify: events in gid order, attach or spawn
+  size_t nspawn = 0;
+  if (nsolid) {
+    uint32_t* flag = c.vals_alt.p;
+    uint32_t* pos = c.vals.p;
+    k_flag_eq<<<grid_for(n, 256), 256, 0, s>>>(c.ev_flag.p, n, 2u, flag);
+    exclusive_scan_u32(flag, pos, n, c.scan_tmp.p, s, &c.launches);
+    k_compact_by_gid<<<grid_for(n, 256), 256, 0, s>>>(c.ev_flag.p, pos, n, 2u, c.cur.gid.p, c.keys.p, c.vals_alt.p);
+    const bool fl = radix_sort_pairs(c.keys.p, c.vals_alt.p, c.keys_alt.p, c.vals.p, nsolid, bits_for(n - 1), c.hist.p,
+                                     c.scan_tmp.p, s, &c.launches);
+    uint32_t* list = fl ? c.vals.p : c.vals_alt.p;
+    c.ev_idx.alloc(nsolid);
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(c.ev_idx.p, list, nsolid * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    k_solid_target<<<grid_for(nsolid, 128), 128, 0, s>>>(c.P, c.cur, c.ev_idx.p, nsolid, c.nbr.p, c.cnt.p, n, target,
+                                                         spawn);
+    exclusive_scan_u32(spawn, rank, nsolid, c.scan_tmp.p, s, &c.launches);
+    nspawn = read_u32(c, rank + nsolid - 1) + read_u32(c, spawn + nsolid - 1);
+    k_solid_apply<<<grid_for(nsolid, 128), 128, 0, s>>>(c.P, c.cur, c.ev_idx.p, nsolid, target, rank, nb0,
+                                                        c.bodies.p, bmask, src);
+    c.launches += 5;
+  }
+  c.nb = nb0 + nspawn;
+  launch_rigid_index(c);
+  // 3. split bodies that lost particles
+  if (nmelt) {
+    c.label.alloc(n);
+    k_label_init<<<grid_for(n, 256), 256, 0, s>>>(c.cur, n, blost, c.label.p);
+    const double adj2 = (1.5 * c.P.dx) * (1.5 * c.P.dx);
+    for (int it = 0; it < 100000; ++it) {
+      SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->changed, 0, sizeof(uint32_t), s));
+      k_label_iter<<<grid_for(n, 128), 128, 0, s>>>(c.P, c.cur, n, c.nbr.p, c.cnt.p, c.label.p, adj2, c.dflags);
+      c.launches += 2;
+      if (!read_u32(c, &c.dflags->changed)) break;
+    }
+    const int gbits = bits_for(n - 1);
+    k_split_roots<<<grid_for(n, 256), 256, 0, s>>>(c.cur, n, c.label.p, c.ridx.p, c.body_start.p, gbits, c.keys.p,
+                                                   c.vals.p, c.dflags);
+    const uint32_t nsplit = read_u32(c, &c.dflags->pad[1]);
+    if (nsplit) {
+      const int bits = gbits + bits_for(c.nb);
+      const bool fl = radix_sort_pairs(c.keys.p, c.vals.p, c.keys_alt.p, c.vals_alt.p, nsplit, bits, c.hist.p,
+                                       c.scan_tmp.p, s, &c.launches);
+      const unsigned long long* keys = fl ? c.keys_alt.p : c.keys.p;
+      k_split_bodies<<<grid_for(nsplit, 128), 128, 0, s>>>(keys, nsplit, gbits, c.nb, c.bodies.p, bmask, src);
+      k_split_relabel<<<grid_for(n, 256), 256, 0, s>>>(c.cur, n, c.label.p, c.ridx.p, c.body_start.p, keys, nsplit,
+                                                       gbits, c.nb);
+      // old state of split products = their source body's pre-batch state (via src)
+      c.nb += nsplit;
+      launch_rigid_index(c);
+      c.launches += 2;
+    }
+  }
+  // 4. mass quantities + post-transition velocity + member velocities
+  launch_mass(c, bmask);
+  k_post_velocity<<<grid_for(c.nb, 128), 128, 0, s>>>(c.P, c.bodies.p, old.p, bmask, src, c.nb, nb0);
+  k_member_velocity<<<grid_for(n, 256), 256, 0, s>>>(c.cur, n, c.bodies.p, bmask);
+  c.launches += 4;
+  // 5. force/torque with the new membership
+  launch_bodies(c);
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+  old.free();
+  c.n_melt += nmelt;
+  c.n_solid += nsolid;
+  return 0;
+}
+
+}  // namespace sphg

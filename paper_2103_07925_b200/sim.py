@@ -23,6 +23,16 @@ class SPHError(RuntimeError):
         self.code = code
 
 
+def dt_limits(params, u_max, m_r, lib=None):
+    """compute_dt terms without a device: cfl, viscous, body force, contact, conduction."""
+    if lib is None:
+        from ._lib import load
+        lib = load()
+    out = (C.c_double * 5)()
+    lib.sphg_dt_limits(C.byref(params), float(u_max), float(m_r), out)
+    return list(out)
+
+
 class Simulation:
     prefix = "sphg_"
 
@@ -160,6 +170,12 @@ class Simulation:
 
     def set_timing(self, enabled=True):
         self._check(self._fn("set_timing")(self._h, int(bool(enabled))), "set_timing")
+
+    def count_pairs(self):
+        """(Verlet candidates, pairs within r_c) of the current list."""
+        a, b = C.c_int64(), C.c_int64()
+        self._check(self._fn("count_pairs")(self._h, C.byref(a), C.byref(b)), "count_pairs")
+        return a.value, b.value
 
     def compute_dt(self):
         """compute_dt terms: cfl, viscous, body force, contact, conduction."""

@@ -1,0 +1,83 @@
+"""Comparison helpers for GPU-vs-oracle parity (DESIGN.md §5 tolerance metric).
+
+A field passes when |x_gpu - x_cpu| <= tol * max(|x_cpu|, S) per particle, where
+S is the oracle's sum of |pair contributions| for that particle:
+interior accelerations cancel to a small residual, so plain relative error is not
+a meaningful bar for them.
+"""
+import numpy as np
+
+TOL = 1e-10  # BASELINE north_star: fp64 fields within 1e-10 relative
+
+
+def vec_err(g, o, scale, tol=TOL):
+    """max over particles of |g-o| / (tol * max(|o|, scale)); <= 1 passes."""
+    g = np.asarray(g, float)
+    o = np.asarray(o, float)
+    if g.ndim == 1:
+        d = np.abs(g - o)
+        ref = np.maximum(np.abs(o), scale)
+    else:
+        d = np.linalg.norm(g - o, axis=1)
+        ref = np.maximum(np.linalg.norm(o, axis=1), scale)
+    ref = np.maximum(ref, 1e-300)
+    return float(np.max(d / (tol * ref))) if len(d) else 0.0
+
+
+def assert_close(name, g, o, scale, tol=TOL):
+    e = vec_err(g, o, scale, tol)
+    assert e <= 1.0, f"{name}: max error {e:.3g} x tolerance ({tol:g})"
+    return e
+
+
+def run_pair(sc, lib_sim, oracle_cls, init=True):
+    sim = lib_sim(sc.params)
+    orc = oracle_cls(sc.params)
+    for e in (sim, orc):
+        e.upload(sc.store, sc.bodies)
+        if init:
+            e.initialize()
+    return sim, orc
+
+
+def compare_state(sim, orc, params, tol=TOL, what=""):
+    """Compares every hot-path field of the two engines; returns the error table."""
+    g, gb = sim.download()
+    o, ob = orc.download()
+    s = orc.scales()
+    out = {}
+    fl = o.kind == 0
+    rg = o.kind == 1
+    wl = o.kind != 0
+    assert np.array_equal(g.kind, o.kind), f"{what}: kind flags differ"
+    assert np.array_equal(g.material, o.material), f"{what}: materials differ"
+    assert np.array_equal(g.group[rg], o.group[rg]), f"{what}: body ids differ"
+    rho0 = np.array([params.mat[m].rho0 for m in range(params.n_mat)])
+    c2 = np.array([params.mat[m].c ** 2 for m in range(params.n_mat)])
+    p0 = (rho0 * c2)[o.material]
+    out["density"] = assert_close(f"{what} density", g.density[fl], o.density[fl], 0.0, tol)
+    out["pressure"] = assert_close(f"{what} pressure", g.pressure[fl], o.pressure[fl],
+                                   (c2[o.material] * o.density)[fl], tol)
+    out["acc"] = assert_close(f"{what} acc", g.acc[fl], o.acc[fl], s["acc"][fl], tol)
+    out["acc_bg"] = assert_close(f"{what} acc_bg", g.acc_bg[fl], o.acc_bg[fl], s["acc_bg"][fl], tol)
+    out["wall_pressure"] = assert_close(f"{what} wall_pressure", g.wall_pressure[wl], o.wall_pressure[wl],
+                                        np.maximum(p0[wl], 1e-300), tol)
+    uscale = max(float(np.max(np.abs(o.vel))), 1e-12)
+    out["wall_velocity"] = assert_close(f"{what} wall_velocity", g.wall_velocity[wl], o.wall_velocity[wl], uscale, tol)
+    out["force"] = assert_close(f"{what} force", g.force[rg], o.force[rg], s["force"][rg], tol)
+    out["dT_dt"] = assert_close(f"{what} dT_dt", g.dT_dt, o.dT_dt, s["dT_dt"], tol)
+    out["temperature"] = assert_close(f"{what} T", g.temperature, o.temperature, 0.0, tol)
+    L = np.array([params.hi[a] - params.lo[a] for a in range(3)])
+    out["pos"] = assert_close(f"{what} pos", g.pos, o.pos, float(np.max(L)), 1e-14)
+    out["vel"] = assert_close(f"{what} vel", g.vel, o.vel, uscale, 1e-9)
+    if len(ob):
+        assert np.array_equal(gb["alive"], ob["alive"]), f"{what}: alive bodies differ"
+        al = ob["alive"] == 1
+        out["body_mass"] = assert_close(f"{what} body mass", gb["mass"][al], ob["mass"][al], 0.0, 1e-12)
+        out["body_force"] = assert_close(f"{what} body force", gb["force"][al], ob["force"][al],
+                                         s["body_force"][al], tol)
+        out["body_torque"] = assert_close(f"{what} body torque", gb["torque"][al], ob["torque"][al],
+                                          s["body_torque"][al], tol)
+        out["body_inertia"] = assert_close(f"{what} body inertia", gb["inertia"][al], ob["inertia"][al],
+                                           np.abs(ob["inertia"][al][:, :3]).max(axis=1), 1e-12)
+    return out

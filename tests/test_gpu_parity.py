@@ -1,0 +1,181 @@
+"""GPU (sm_100a, through the C ABI) vs the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE north_star): cells, sort order and Verlet lists bit-exact;
+density / acceleration / temperature rate / body force & torque within 1e-10
+(DESIGN.md §5 metric); phase flags bit-exact after step 1.
+"""
+import numpy as np
+import pytest
+
+from paper_2103_07925_b200 import scenarios, Simulation, SPHError, abi
+from tests.helpers import compare_state, run_pair, vec_err
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "c1_small": lambda: scenarios.config1(nside=20, n_spheres=3, r_range=(3.0, 4.0), seed=11),
+    "c1": lambda: scenarios.config1(),
+    "c2_small": lambda: scenarios.config2(nside=18, n_grid=2, r_range=(2.0, 3.0), seed=5),
+    "c2_melt": lambda: scenarios.config2(nside=18, n_grid=2, r_range=(2.0, 3.0), seed=5, melt_forcing=True),
+}
+
+
+@pytest.fixture(scope="module")
+def Oracle():
+    from oracle.oracle import Oracle as O
+    return O
+
+
+def sim_factory(params):
+    return Simulation(params, device=0)
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_cells_and_nlist_bitexact(case, Oracle):
+    sc = CASES[case]()
+    sim, orc = run_pair(sc, sim_factory, Oracle, init=False)
+    for e in (sim, orc):
+        e.build_pairs()
+    cg, og = sim.get_cells()
+    co, oo = orc.get_cells()
+    assert np.array_equal(cg, co), "cell ids differ"
+    assert np.array_equal(og, oo), "(cell, gid) order differs"
+    offg, nbg = sim.get_nlist()
+    offo, nbo = orc.get_nlist()
+    assert np.array_equal(offg, offo), "neighbour counts differ"
+    assert np.array_equal(nbg, nbo), "neighbour lists differ"
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_initialize_parity(case, Oracle):
+    sc = CASES[case]()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    compare_state(sim, orc, sc.params, what=f"{case} init")
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_step1_parity(case, Oracle):
+    sc = CASES[case]()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    sim.step(1)
+    orc.step(1)
+    compare_state(sim, orc, sc.params, what=f"{case} step1")
+
+
+def test_phase_flags_bitexact_step1(Oracle):
+    sc = CASES["c2_melt"]()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    sim.step(1)
+    orc.step(1)
+    g, gb = sim.download()
+    o, ob = orc.download()
+    assert orc.stats().transitions_melt > 0 and orc.stats().transitions_solidify > 0
+    assert np.array_equal(g.kind, o.kind)
+    assert np.array_equal(g.group, o.group)
+    assert np.array_equal(g.material, o.material)
+    assert len(gb) == len(ob)
+    assert np.array_equal(gb["alive"], ob["alive"])
+    assert sim.stats().transitions_melt == orc.stats().transitions_melt
+    assert sim.stats().transitions_solidify == orc.stats().transitions_solidify
+    # mass and particle count conserved exactly
+    assert g.mass.sum() == sc.store.mass.sum()
+
+
+def test_multistep_c1_small(Oracle):
+    sc = CASES["c1_small"]()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    sim.step(10)
+    orc.step(10)
+    # chaotic growth of round-off over 10 steps: 1e-7 of the pair-sum scale
+    compare_state(sim, orc, sc.params, tol=1e-7, what="c1_small 10 steps")
+    assert sim.stats().rebuilds == orc.stats().rebuilds
+
+
+def test_stage_by_stage(Oracle):
+    sc = CASES["c2_small"]()
+    sim, orc = run_pair(sc, sim_factory, Oracle, init=False)
+    for st in (abi.STAGE_REBUILD, abi.STAGE_DENSITY, abi.STAGE_EXTRAPOLATE, abi.STAGE_FORCES, abi.STAGE_BODIES,
+               abi.STAGE_KICK_DRIFT):
+        sim.run_stage(st)
+        orc.run_stage(st)
+    compare_state(sim, orc, sc.params, what="stages")
+    for st in (abi.STAGE_DENSITY, abi.STAGE_HEAT, abi.STAGE_EXTRAPOLATE, abi.STAGE_FORCES, abi.STAGE_BODIES,
+               abi.STAGE_FINAL_KICK, abi.STAGE_MASS):
+        sim.run_stage(st)
+        orc.run_stage(st)
+    compare_state(sim, orc, sc.params, what="stages2")
+
+
+def test_isolated_particle_density():
+    from paper_2103_07925_b200.store import ParticleStore
+    sc = scenarios.config1(nside=16, n_spheres=0)
+    s = ParticleStore(1)
+    s.pos[0] = [0.008, 0.008, 0.008]
+    s.mass[0] = 1e-6
+    s.density[0] = 1000.0
+    sim = Simulation(sc.params)
+    sim.upload(s, None)
+    sim.density_summation()
+    g, _ = sim.download()
+    h = sc.params.dx
+    w0 = 66.0 / (120.0 * np.pi * h ** 3)
+    assert abs(g.density[0] - 1e-6 * w0) <= 1e-14 * g.density[0]
+
+
+def test_empty_store():
+    from paper_2103_07925_b200.store import ParticleStore
+    sc = scenarios.config1(nside=16, n_spheres=0)
+    sim = Simulation(sc.params)
+    sim.upload(ParticleStore(0), None)
+    sim.initialize()
+    sim.step(3)
+    assert sim.stats().steps == 3
+
+
+def test_coincident_particles_fail():
+    sc = scenarios.config1(nside=16, n_spheres=0)
+    sc.store.pos[5] = sc.store.pos[6]
+    sim = Simulation(sc.params)
+    sim.upload(sc.store, sc.bodies)
+    with pytest.raises(SPHError) as e:
+        sim.initialize()
+    assert e.value.code == 3 and "coincident" in str(e.value)
+
+
+def test_escaped_particle_fail():
+    sc = scenarios.config2(nside=12, n_grid=1, r_range=(2.0, 2.0))
+    sc.store.pos[0, 2] = sc.params.hi[2] + 1e-3
+    sim = Simulation(sc.params)
+    sim.upload(sc.store, sc.bodies)
+    with pytest.raises(SPHError) as e:
+        sim.initialize()
+    assert e.value.code == 3 and "escaped" in str(e.value)
+
+
+def test_nlist_capacity_growth(Oracle):
+    sc = scenarios.config1(nside=16, n_spheres=1, r_range=(3.0, 3.0))
+    sc.params.nlist_capacity = 8
+    sim, orc = run_pair(sc, sim_factory, Oracle, init=False)
+    sim.build_pairs()
+    orc.build_pairs()
+    assert sim.stats().nlist_capacity >= sim.stats().max_neighbours > 8
+    assert np.array_equal(sim.get_nlist()[1], orc.get_nlist()[1])
+
+
+def test_warm_upload_roundtrip(Oracle):
+    sc = CASES["c1_small"]()
+    sim = Simulation(sc.params)
+    sim.upload(sc.store, sc.bodies)
+    sim.initialize()
+    sim.step(2)
+    s, b = sim.download()
+    sim.upload(s, b)  # warm: same size, list kept
+    s2, b2 = sim.download()
+    for f in ("pos", "vel", "acc", "density", "temperature", "mass"):
+        assert np.array_equal(getattr(s, f), getattr(s2, f)), f
+    sim.step(1)
+    orc = Oracle(sc.params)
+    orc.upload(sc.store, sc.bodies)
+    orc.initialize()
+    orc.step(3)
+    compare_state(sim, orc, sc.params, tol=1e-7, what="warm upload")
