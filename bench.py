@@ -213,7 +213,7 @@ def run_sph(args):
     kk = max(2, args.steps // 2)
     stage_ms = {abi.STAGE_NAMES[k]: (sb.stage_ms[k] - sa.stage_ms[k]) / kk for k in range(10)}
     launches = (st1.kernel_launches - st0.kernel_launches)
-    value = n * args.steps / (ms_step * 1e-3)
+    value = n / (ms_step * 1e-3)
     peaks = load_peaks()
     info = sc.info
     nf = info["n_fluid"]

@@ -792,6 +792,8 @@ bool stage_transitions(Ctx& c) {
         c.S.density[r] = c.P.mat[tgt].rho0;
         c.S.pressure[r] = 0.0;
         c.S.body_frame_pos[r] = V3::zero();
+        c.S.wall_pressure[r] = 0.0;
+        c.S.wall_velocity[r] = V3::zero();
         c.force[r] = V3::zero();
         affected[k] = 1;
         lost[k] = 1;
@@ -839,6 +841,8 @@ bool stage_transitions(Ctx& c) {
         c.S.pressure[i] = 0.0;
         c.S.acc[i] = V3::zero();
         c.S.acc_bg[i] = V3::zero();
+        c.S.wall_pressure[i] = 0.0;
+        c.S.wall_velocity[i] = V3::zero();
     }
     rebuild_members(c);
     src_body.resize(c.bodies.size());

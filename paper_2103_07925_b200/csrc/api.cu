@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -512,6 +513,8 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
   c.device = device;
   c.t = p->t0;
   c.ncells = (int64_t)c.P.ncell[0] * c.P.ncell[1] * c.P.ncell[2];
+  if (const char* e = std::getenv("SPHG_GROUP_DENSITY")) c.group_density = std::atoi(e);
+  if (const char* e = std::getenv("SPHG_GROUP_FORCES")) c.group_forces = std::atoi(e);
   try {
     SPHG_CUDA_CHECK(cudaSetDevice(device));
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
@@ -562,9 +565,15 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     c.cell_end.alloc(c.ncells);
     c.cell_key.alloc(na);
     c.cnt.alloc(na);
-    Particles& dst = warm ? c.alt : c.cur;
+    const bool any_periodic = c.P.periodic[0] || c.P.periodic[1] || c.P.periodic[2];
+    const int mode = !any_periodic ? kImgNone : (n < (size_t(1) << 26) ? kImgCode : kImgMin);
+    if (mode != c.P.img_mode) {
+      c.P.img_mode = mode;
+      c.built = false;
+    }
+    Particles& dst = (warm && c.built) ? c.alt : c.cur;
     stage_upload(c, s, dst);
-    if (warm) {
+    if (warm && c.built) {
       gather_by_gid(c);  // cur[k] <- alt[gid[k]] (keeps gid, R4, list)
       if (displacement_exceeds(c)) c.built = false;
     } else {
@@ -691,12 +700,13 @@ int sphg_get_nlist(sphg_ctx* h, int64_t* offsets, uint32_t* nbr_gid) {
     }
     if (offsets) offsets[n] = o;
     if (!nbr_gid) return SPHG_OK;
-    std::vector<uint32_t> ell((size_t)c.cap * n);
-    d2h(ell.data(), c.nbr.p, ell.size(), c.stream);
+    std::vector<uint32_t> rows((size_t)c.cap * n);
+    d2h(rows.data(), c.nbr.p, rows.size(), c.stream);
     SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    const uint32_t mask = c.P.img_mode == kImgCode ? kIdxMask : 0xffffffffu;
     for (size_t k = 0; k < n; ++k) {
       const int64_t base = offsets[gid[k]];
-      for (uint32_t q = 0; q < cnt[k]; ++q) nbr_gid[base + q] = gid[ell[(size_t)q * n + k]];
+      for (uint32_t q = 0; q < cnt[k]; ++q) nbr_gid[base + q] = gid[rows[k * (size_t)c.cap + q] & mask];
       std::sort(nbr_gid + base, nbr_gid + base + cnt[k]);
     }
     return SPHG_OK;

@@ -48,7 +48,7 @@ struct DevParams {
   int32_t single_eta;   // all fluid materials share eta   -> eta~ = eta_i
   int32_t single_kappa; // all materials share kappa       -> kappa~ = 2 kappa
   int32_t single_eos;   // all fluid materials share rho0,c -> wall EOS material fixed
-  int32_t pad;
+  int32_t img_mode;     // neighbour-entry image mode (kImgNone / kImgCode / kImgMin)
 };
 
 // ---------------------------------------------------------------- tags
@@ -90,30 +90,88 @@ __device__ __forceinline__ double axpy_rn(double a, double s, double b) { return
 
 // ---------------------------------------------------------- kernel (fp64)
 // Quintic spline (kernel.hpp:47-75), branch-free: the missing branches add exact zeros.
+// max(x, 0) on the integer pipe (keeps DSETP/FSEL off the FP64 pipe; x is never NaN here)
+__device__ __forceinline__ double clamp0(double x) {
+  const long long b = __double_as_longlong(x);
+  return __longlong_as_double(b & ~(b >> 63));
+}
 __device__ __forceinline__ double shape_q(double q) {
   const double a = 3.0 - q;
-  const double b = fmax(2.0 - q, 0.0);
-  const double c = fmax(1.0 - q, 0.0);
+  const double b = clamp0(2.0 - q);
+  const double c = clamp0(1.0 - q);
   const double a2 = a * a, b2 = b * b, c2 = c * c;
   return a2 * a2 * a - 6.0 * (b2 * b2 * b) + 15.0 * (c2 * c2 * c);
 }
 __device__ __forceinline__ double shape_deriv_q(double q) {
   const double a = 3.0 - q;
-  const double b = fmax(2.0 - q, 0.0);
-  const double c = fmax(1.0 - q, 0.0);
+  const double b = clamp0(2.0 - q);
+  const double c = clamp0(1.0 - q);
   const double a2 = a * a, b2 = b * b, c2 = c * c;
   return -5.0 * (a2 * a2) + 30.0 * (b2 * b2) - 75.0 * (c2 * c2);
 }
 
-// fast fp64 reciprocal: MUFU seed + 2 Newton steps (~1 ulp; tolerance stages only)
+// fast fp64 reciprocal / reciprocal square root for the tolerance stages:
+// MUFU seed (~2^-22) + one Newton step (~1e-13 relative, far inside the 1e-10
+// bar of the pair sums); 2 + 4 FP64 instructions instead of the IEEE sequences.
 __device__ __forceinline__ double rcp_fast(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  return y;
+  const double e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = x * y;
+  const double e = fma(-h, y, 1.0);  // 1 - x y^2
+  return fma(0.5 * y, e, y);
+}
+// r = sqrt(x) to ~0.5 ulp and 1/r to ~1e-11 (x > 0).  The kernel argument q =
+// r/h needs the accurate root: W ~ (3-q)^5 amplifies relative errors of q near
+// the cut-off, and wall extrapolation divides by sums of such weights.
+__device__ __forceinline__ double sqrt_and_rinv(double x, double& rinv) {
+  const double y = rsqrt_fast(x);
+  const double r0 = x * y;
+  const double e = fma(-r0, r0, x);
+  rinv = y;
+  return fma(0.5 * y, e, r0);
+}
+
+// ------------------------------------------------- neighbour-list entries
+// Row-major Verlet list: nbr[i * cap + k], k < cnt[i].  With periodic axes and
+// N < 2^26 an entry packs the neighbour index (26 bits) with the periodic image
+// of its cell (2 bits per axis: 0 none, 1 +L, 2 -L), fixed at build time.  For
+// any pair inside r_v + skin < L/2 this reproduces the minimum image of the
+// oracle; the pair kernels then need 3 adds instead of 6 compares + selects.
+enum { kImgNone = 0, kImgCode = 1, kImgMin = 2 };
+constexpr uint32_t kIdxMask = 0x03FFFFFFu;
+
+template <int M>
+__device__ __forceinline__ uint32_t nb_index(uint32_t e) {
+  return M == kImgCode ? (e & kIdxMask) : e;
+}
+__device__ __forceinline__ double img_shift(uint32_t code, double L) {
+  return code == 1u ? L : (code == 2u ? -L : 0.0);
+}
+// r_a - r_b under the entry's image convention (tolerance stages; FMA allowed)
+template <int M>
+__device__ __forceinline__ double3 pair_delta(const DevParams& P, double3 a, double3 b, uint32_t e) {
+  if (M == kImgMin) return make_double3(mimg(P, a.x - b.x, 0), mimg(P, a.y - b.y, 1), mimg(P, a.z - b.z, 2));
+  double3 d = make_double3(a.x - b.x, a.y - b.y, a.z - b.z);
+  if (M == kImgCode && (e >> 26) != 0u) {  // only entries in wrapped cells (rare, mostly warp-uniform)
+    d.x += img_shift((e >> 26) & 3u, P.L[0]);
+    d.y += img_shift((e >> 28) & 3u, P.L[1]);
+    d.z += img_shift(e >> 30, P.L[2]);
+  }
+  return d;
+}
+
+// sum over a group of G consecutive lanes (every lane of the warp must call it)
+template <int G>
+__device__ __forceinline__ double gsum(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
 // ------------------------------------------------------------ quaternion

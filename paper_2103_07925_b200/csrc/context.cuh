@@ -9,7 +9,9 @@
 //   A4 = (acc, -)  B4 = (acc_bg, -)  F4 = (f_r, -)  X4 = (chi, -)  R4 = (pos at last rebuild, -)
 //   H2 = (T, V_heat)           temperature and the conduction volume V_b (0 for non-Dirichlet walls)
 //   kmd (kind|mat|dirichlet), group, gid : uint32
-// Verlet candidates are ELL: nbr[k * N + i] for k < cnt[i] (coalesced across i).
+// Verlet candidates are row-major: nbr[i * cap + k] for k < cnt[i]; entries pack
+// the periodic image code (common.cuh kImgCode).  Per-kind index lists (fluid,
+// non-fluid, rigid body-major) drive the pair kernels.
 #pragma once
 
 #include <string>
@@ -24,6 +26,12 @@ struct CudaError {
   std::string what;
   CudaError(cudaError_t c, const char* expr, const char* file, int line)
       : code(c), what(std::string(cudaGetErrorString(c)) + " at " + file + ":" + std::to_string(line) + " (" + expr + ")") {}
+};
+
+struct NbrList {
+  const uint32_t* nbr;
+  const uint32_t* cnt;
+  size_t cap;
 };
 
 template <class T>
@@ -76,12 +84,14 @@ struct Ctx {
   DBuf<uint32_t> vals, vals_alt, hist, scan_tmp;
   DBuf<uint32_t> cell_start, cell_end, cell_key;
   int64_t ncells = 0;
-  // neighbour list (ELL)
+  // neighbour list (row-major)
   DBuf<uint32_t> nbr, cnt;
   int cap = 0;
-  // body-major rigid index
-  DBuf<uint32_t> ridx, body_start;
-  size_t nrigid = 0;
+  NbrList nl() const { return {nbr.p, cnt.p, (size_t)cap}; }
+  // per-kind index lists: fluid, non-fluid (rigid + boundary), rigid body-major
+  DBuf<uint32_t> fidx, widx, ridx, body_start;
+  size_t nf = 0, nw = 0, nrigid = 0;
+  int group_density = 8, group_forces = 8;  // lanes per particle in the pair kernels
   // transitions scratch
   DBuf<uint32_t> ev_idx, ev_flag, label, tscratch;
   // flags

@@ -1,0 +1,594 @@
+// kernels_pairs.cu — the pair-sum kernels of the SPH hot path on sm_100a.
+//
+//   k_density       density_summation + eos_pressure
+//   k_heat          conduction_rhs + explicit T update
+//   k_extrapolate   extrapolate_wall_quantities                 (Adami 2012)
+//   k_forces_fluid  momentum_rhs with transport velocity
+//   k_forces_rigid  coupling_force_on_rigid + contact_force
+//
+// Parallelisation: a group of G consecutive lanes owns one particle i and
+// strides over its Verlet row (nbr[i*cap + k]); the rows list neighbours in
+// cell-run order, so the G lanes gather G (mostly) consecutive particles — a
+// few cache lines per warp load instead of one line per lane.  Partial sums
+// are combined with warp shuffles (gsum); lane 0 of the group writes.  Every
+// sum is a gather (no fp64 atomics), hence deterministic.  Groups iterate over
+// compact per-kind index lists (fluid / non-fluid / rigid) built at rebuild.
+#include <cmath>
+#include <cstring>
+
+#include "context.cuh"
+
+namespace sphg {
+
+namespace {
+
+constexpr int kBlock = 128;
+
+__device__ __forceinline__ double3 ld3(const double4& v) { return make_double3(v.x, v.y, v.z); }
+__device__ __forceinline__ double3 ldpos(const double4* p) {  // xyz only (never touches .w)
+  const double2 xy = *reinterpret_cast<const double2*>(p);
+  const double z = reinterpret_cast<const double*>(p)[2];
+  return make_double3(xy.x, xy.y, z);
+}
+__device__ __forceinline__ double4 ldg4(const double4* p) {  // read-only path, 2 x 16 B
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ Quat body_q(const sphg_body& b) { return {b.q[0], b.q[1], b.q[2], b.q[3]}; }
+__device__ __forceinline__ double3 bv(const double* p) { return make_double3(p[0], p[1], p[2]); }
+
+struct Row {
+  const uint32_t* e;
+  int n;
+};
+__device__ __forceinline__ Row row_of(const NbrList& L, uint32_t i) {
+  return {L.nbr + (size_t)i * L.cap, (int)L.cnt[i]};
+}
+
+// ---------------------------------------------------------------- density
+// rho_i = m_i sigma (66 + sum_j shape(r_ij/h)); p_i = c^2 (rho_i - rho0); V_i = m_i/rho_i
+template <int G, int M>
+__global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                     const uint32_t* __restrict__ list, size_t nlist) {
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  const size_t g = t / G;
+  const int lane = (int)(t % G);
+  const bool active = g < nlist;
+  const uint32_t i = active ? list[g] : 0u;
+  double s = 0.0;
+  if (active) {
+    const double3 pi = ldpos(&D.G0.p[i]);
+    const Row R = row_of(L, i);
+    for (int k = lane; k < R.n; k += G) {
+      const uint32_t e = __ldg(R.e + k);
+      const double3 pj = ldpos(&D.G0.p[nb_index<M>(e)]);
+      const double3 d = pair_delta<M>(P, pi, pj, e);
+      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+      if (r2 <= P.rc2) {
+        double ri;
+        s += shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);  // + tiny: coincident -> W(0)
+      }
+    }
+  }
+  s = gsum<G>(s);
+  if (!active || lane != 0) return;
+  const uint32_t kmd = D.kmd.p[i];
+  const DevMat& Mt = P.mat[mat_of(kmd)];
+  const double m = D.V4.p[i].w;
+  const double rho = m * (P.sigma * (66.0 + s));  // self term shape(0) = 66
+  const double V = m / rho;
+  reinterpret_cast<double*>(&D.G0.p[i])[3] = V * V;
+  reinterpret_cast<double*>(&D.G1.p[i])[3] = rho;
+  reinterpret_cast<double*>(&D.G2.p[i])[3] = Mt.c2 * (rho - Mt.rho0);
+  if (P.thermal) reinterpret_cast<double*>(&D.H2.p[i])[1] = V;
+}
+
+// ------------------------------------------------------------------- heat
+// c_p,a dT_a/dt = (1/rho_a) sum_b V_b 4 k_a k_b/(k_a+k_b) (T_ab/r_ab) dW/dr (Cleary & Monaghan).
+// b over fluid, rigid and Dirichlet boundary particles (V_heat == 0 marks the others).
+template <int G, int M>
+__global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                  const uint32_t* __restrict__ list, size_t nlist,
+                                                  double2* __restrict__ Hout, DevFlags* __restrict__ fl) {
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  const size_t g = t / G;
+  const int lane = (int)(t % G);
+  const bool active = g < nlist;
+  const uint32_t i = active ? list[g] : 0u;
+  double s = 0.0;
+  bool coincident = false;
+  uint32_t kmd = 0;
+  double2 hi = make_double2(0, 0);
+  if (active) {
+    kmd = D.kmd.p[i];
+    const DevMat& Ma = P.mat[mat_of(kmd)];
+    hi = D.H2.p[i];
+    const double3 pi = ldpos(&D.G0.p[i]);
+    const Row R = row_of(L, i);
+    for (int k = lane; k < R.n; k += G) {
+      const uint32_t e = __ldg(R.e + k);
+      const uint32_t j = nb_index<M>(e);
+      const double2 hj = D.H2.p[j];
+      if (hj.y == 0.0) continue;  // non-Dirichlet wall: no conduction
+      const double3 d = pair_delta<M>(P, pi, ldpos(&D.G0.p[j]), e);
+      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+      if (r2 > P.rc2) continue;
+      if (r2 == 0.0) {
+        coincident = true;
+        continue;
+      }
+      double kt;
+      if (P.single_kappa) {
+        kt = 2.0 * Ma.kappa;  // 4 k k / (k + k)
+      } else {
+        const double kb = P.mat[mat_of(D.kmd.p[j])].kappa;
+        const double ks = Ma.kappa + kb;
+        if (ks == 0.0) continue;
+        kt = 4.0 * Ma.kappa * kb / ks;
+      }
+      double rinv;
+      const double dW = P.sig_h * shape_deriv_q(sqrt_and_rinv(r2, rinv) * P.inv_h);
+      s += hj.y * kt * ((hi.x - hj.x) * rinv) * dW;
+    }
+  }
+  s = gsum<G>(s);
+  if (!active) return;
+  if (coincident) {
+    atomicOr(&fl->err, kErrCoincident);
+    atomicMin(&fl->err_gid, D.gid.p[i]);
+  }
+  if (lane != 0) return;
+  const DevMat& Ma = P.mat[mat_of(kmd)];
+  const uint32_t kind = kind_of(kmd);
+  const double rho_a = kind == SPHG_FLUID ? D.G1.p[i].w : Ma.rho0;
+  double rate = 0.0;
+  if (Ma.cp > 0.0) rate = s / (rho_a * Ma.cp);
+  Hout[i] = make_double2(hi.x + P.dt * rate, hi.y);
+  D.dTdt.p[i] = rate;
+}
+
+// ---------------------------------------------------------- extrapolation
+// p_w = sum_f W (p_f + rho_f (g_f - a_w).(r_w - r_f)) / sum_f W;  u~_w = 2 u_w - sum_f W u_f / sum_f W;
+// rho_w = max(rho0, rho0 + p_w/c^2) of the dominant fluid material; V_w = rho0 dx^3 / rho_w  [P6][P7]
+template <int G, int M, bool kMultiEos>
+__global__ void __launch_bounds__(kBlock) k_extrapolate(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                         const sphg_body* __restrict__ B,
+                                                         const uint32_t* __restrict__ list, size_t nlist) {
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  const size_t g = t / G;
+  const int lane = (int)(t % G);
+  const bool active = g < nlist;
+  const uint32_t w = active ? list[g] : 0u;
+  double3 uw = make_double3(0, 0, 0), aw = make_double3(0, 0, 0);
+  double sw = 0.0, sp = 0.0;
+  double3 su = make_double3(0, 0, 0);
+  double smat[kMultiEos ? kMaxMat : 1];
+#pragma unroll
+  for (int m = 0; m < (kMultiEos ? kMaxMat : 1); ++m) smat[m] = 0.0;
+  if (active) {
+    const uint32_t kmd = D.kmd.p[w];
+    if (kind_of(kmd) == SPHG_RIGID) {
+      const sphg_body& b = B[D.group.p[w]];
+      const double3 rk = qrotate(body_q(b), ld3(D.X4.p[w]));
+      const double3 om = bv(b.omega);
+      const double3 t1 = cross3(bv(b.alpha), rk);
+      const double3 t2 = cross3(om, cross3(om, rk));
+      aw = make_double3(b.acc[0] + t1.x + t2.x, b.acc[1] + t1.y + t2.y, b.acc[2] + t1.z + t2.z);
+      uw = ldpos(&D.V4.p[w]);
+    }
+    const double3 pw = ldpos(&D.G0.p[w]);
+    const Row R = row_of(L, w);
+    for (int k = lane; k < R.n; k += G) {
+      const uint32_t e = __ldg(R.e + k);
+      const uint32_t f = nb_index<M>(e);
+      const uint32_t kf = D.kmd.p[f];
+      if (kind_of(kf) != SPHG_FLUID) continue;
+      const double3 d = pair_delta<M>(P, pw, ldpos(&D.G0.p[f]), e);
+      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+      if (r2 > P.rc2) continue;
+      double ri;
+      const double W = shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);  // sigma cancels in the ratios
+      const double4 g1 = D.G1.p[f];
+      const double pf = D.G2.p[f].w;
+      const DevMat& Mf = P.mat[mat_of(kf)];
+      const double ga = (Mf.g[0] - aw.x) * d.x + (Mf.g[1] - aw.y) * d.y + (Mf.g[2] - aw.z) * d.z;
+      sw += W;
+      sp += W * (pf + g1.w * ga);
+      su.x += W * g1.x;
+      su.y += W * g1.y;
+      su.z += W * g1.z;
+      if (kMultiEos) smat[mat_of(kf)] += W;
+    }
+  }
+  sw = gsum<G>(sw);
+  sp = gsum<G>(sp);
+  su.x = gsum<G>(su.x);
+  su.y = gsum<G>(su.y);
+  su.z = gsum<G>(su.z);
+  if (kMultiEos) {
+#pragma unroll
+    for (int m = 0; m < kMaxMat; ++m) smat[m] = gsum<G>(smat[m]);
+  }
+  if (!active || lane != 0) return;
+  int m = P.default_fluid_mat;
+  if (kMultiEos && sw > 0.0) {
+    double best = -1.0;
+    for (int q = 0; q < P.n_mat; ++q)
+      if (smat[q] > best) {
+        best = smat[q];
+        m = q;
+      }
+  }
+  const DevMat& Mt = P.mat[m];
+  double p_w = 0.0;
+  double3 ut = uw;
+  if (sw > 0.0) {
+    const double inv = 1.0 / sw;
+    p_w = sp * inv;
+    ut = make_double3(2.0 * uw.x - su.x * inv, 2.0 * uw.y - su.y * inv, 2.0 * uw.z - su.z * inv);
+  }
+  const double rho_w = fmax(Mt.rho0, Mt.rho0 + p_w * Mt.inv_c2);
+  const double V_w = Mt.rho0 * P.dx3 / rho_w;
+  reinterpret_cast<double*>(&D.G0.p[w])[3] = V_w * V_w;
+  D.G1.p[w] = make_double4(ut.x, ut.y, ut.z, rho_w);
+  D.G2.p[w] = make_double4(0.0, 0.0, 0.0, p_w);
+}
+
+// ---------------------------------------------------------------- forces
+// a_ij = (V_i^2 + V_j^2)/m_i [ -p~ gradW + eta~ (u_i-u_j) (dW/dr)/r + 1/2 (A_i + A_j) gradW ],
+// A = rho u (u~ - u)^T, gradW = dW/dr e_ij;  a_bg,i = -(p_b/m_i) sum (V_i^2+V_j^2) gradW.
+struct PairSide {
+  double3 u, du;
+  double rho, p, V2, eta, hrho;  // hrho = rho/2 (TVF)
+};
+
+template <bool kTvf, bool kSingleEta>
+__device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, double3 d, double r2,
+                                          const DevParams& P, double3& acc, double3& bg) {
+  double rinv;
+  const double dW = P.sig_h * shape_deriv_q(sqrt_and_rinv(r2, rinv) * P.inv_h);
+  const double fac = dW * rinv;  // gradW = fac * d
+  const double3 gW = make_double3(fac * d.x, fac * d.y, fac * d.z);
+  const double V2 = I.V2 + J.V2;
+  const double pt = fma(J.rho, I.p, I.rho * J.p) * rcp_fast(I.rho + J.rho);
+  double et;
+  if (kSingleEta) {
+    et = I.eta;  // 2 eta eta / (eta + eta)
+  } else {
+    const double es = I.eta + J.eta;
+    et = es > 0.0 ? 2.0 * I.eta * J.eta * rcp_fast(es) : 0.0;
+  }
+  const double vf = et * fac;
+  double3 t = make_double3(fma(vf, I.u.x - J.u.x, -pt * gW.x), fma(vf, I.u.y - J.u.y, -pt * gW.y),
+                           fma(vf, I.u.z - J.u.z, -pt * gW.z));
+  if (kTvf) {
+    const double ai = I.hrho * (I.du.x * gW.x + I.du.y * gW.y + I.du.z * gW.z);
+    const double aj = J.hrho * (J.du.x * gW.x + J.du.y * gW.y + J.du.z * gW.z);
+    t.x += ai * I.u.x + aj * J.u.x;
+    t.y += ai * I.u.y + aj * J.u.y;
+    t.z += ai * I.u.z + aj * J.u.z;
+  }
+  acc.x = fma(V2, t.x, acc.x);
+  acc.y = fma(V2, t.y, acc.y);
+  acc.z = fma(V2, t.z, acc.z);
+  bg.x = fma(V2, gW.x, bg.x);
+  bg.y = fma(V2, gW.y, bg.y);
+  bg.z = fma(V2, gW.z, bg.z);
+}
+
+template <int G, int M, bool kTvf, bool kSingleEta>
+__global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                          const uint32_t* __restrict__ list, size_t nlist,
+                                                          DevFlags* __restrict__ fl) {
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  const size_t g = t / G;
+  const int lane = (int)(t % G);
+  const bool active = g < nlist;
+  const uint32_t i = active ? list[g] : 0u;
+  double3 acc = make_double3(0, 0, 0), bg = make_double3(0, 0, 0);
+  bool coincident = false;
+  uint32_t kmd = 0;
+  if (active) {
+    kmd = D.kmd.p[i];
+    const double4 g0 = ldg4(&D.G0.p[i]), g1 = ldg4(&D.G1.p[i]), g2 = ldg4(&D.G2.p[i]);
+    PairSide I;
+    I.u = ld3(g1);
+    I.du = ld3(g2);
+    I.rho = g1.w;
+    I.hrho = 0.5 * g1.w;
+    I.p = g2.w;
+    I.V2 = g0.w;
+    I.eta = P.mat[mat_of(kmd)].eta;
+    const double3 pi = ld3(g0);
+    const Row R = row_of(L, i);
+    for (int k = lane; k < R.n; k += G) {
+      const uint32_t e = __ldg(R.e + k);
+      const uint32_t j = nb_index<M>(e);
+      const double4 h0 = ldg4(&D.G0.p[j]);
+      const double3 d = pair_delta<M>(P, pi, ld3(h0), e);
+      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+      if (r2 > P.rc2) continue;
+      if (r2 == 0.0) {
+        coincident = true;
+        continue;
+      }
+      const double4 h1 = ldg4(&D.G1.p[j]);
+      const double4 h2 = ldg4(&D.G2.p[j]);
+      PairSide J;
+      J.u = ld3(h1);
+      J.du = ld3(h2);
+      J.rho = h1.w;
+      J.hrho = 0.5 * h1.w;
+      J.p = h2.w;
+      J.V2 = h0.w;
+      if (kSingleEta) {
+        J.eta = I.eta;
+      } else {
+        const uint32_t kj = __ldg(&D.kmd.p[j]);
+        J.eta = kind_of(kj) == SPHG_FLUID ? P.mat[mat_of(kj)].eta : I.eta;  // eta_w := eta_i [P7]
+      }
+      pair_term<kTvf, kSingleEta>(I, J, d, r2, P, acc, bg);
+    }
+  }
+  acc.x = gsum<G>(acc.x);
+  acc.y = gsum<G>(acc.y);
+  acc.z = gsum<G>(acc.z);
+  bg.x = gsum<G>(bg.x);
+  bg.y = gsum<G>(bg.y);
+  bg.z = gsum<G>(bg.z);
+  if (!active) return;
+  if (coincident) {
+    atomicOr(&fl->err, kErrCoincident);
+    atomicMin(&fl->err_gid, D.gid.p[i]);
+  }
+  if (lane != 0) return;
+  const DevMat& Mt = P.mat[mat_of(kmd)];
+  const double im = 1.0 / D.V4.p[i].w;
+  D.A4.p[i] = make_double4(acc.x * im + Mt.g[0], acc.y * im + Mt.g[1], acc.z * im + Mt.g[2], 0.0);
+  const double f = kTvf ? -Mt.pb * im : 0.0;
+  D.B4.p[i] = make_double4(f * bg.x, f * bg.y, f * bg.z, 0.0);
+}
+
+// f_r = sum_i -m_i a_ir (fluid neighbours, a_ir from the fluid's view) + contact
+template <int G, int M, bool kTvf, bool kSingleEta>
+__global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                          const uint32_t* __restrict__ list, size_t nlist,
+                                                          DevFlags* __restrict__ fl) {
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  const size_t g = t / G;
+  const int lane = (int)(t % G);
+  const bool active = g < nlist;
+  const uint32_t r = active ? list[g] : 0u;
+  double3 f = make_double3(0, 0, 0);
+  bool coincident = false;
+  if (active) {
+    const double4 g0 = ldg4(&D.G0.p[r]), g1 = ldg4(&D.G1.p[r]), g2 = ldg4(&D.G2.p[r]);
+    const double3 vr = ldpos(&D.V4.p[r]);
+    const uint32_t body = D.group.p[r];
+    PairSide R;
+    R.u = ld3(g1);
+    R.du = make_double3(0, 0, 0);
+    R.rho = g1.w;
+    R.hrho = 0.5 * g1.w;
+    R.p = g2.w;
+    R.V2 = g0.w;
+    const double3 pr = ld3(g0);
+    const Row Rw = row_of(L, r);
+    for (int k = lane; k < Rw.n; k += G) {
+      const uint32_t e = __ldg(Rw.e + k);
+      const uint32_t j = nb_index<M>(e);
+      const uint32_t kj = D.kmd.p[j];
+      const uint32_t kindj = kind_of(kj);
+      const double4 h0 = ldg4(&D.G0.p[j]);
+      if (kindj == SPHG_FLUID) {
+        // from the fluid's view: d = r_j - r_r (the entry's image is defined for r - j: negate)
+        const double3 dd = pair_delta<M>(P, pr, ld3(h0), e);
+        const double3 d = make_double3(-dd.x, -dd.y, -dd.z);
+        const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+        if (r2 > P.rc2) continue;
+        if (r2 == 0.0) {
+          coincident = true;
+          continue;
+        }
+        const double4 h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
+        PairSide J;
+        J.u = ld3(h1);
+        J.du = ld3(h2);
+        J.rho = h1.w;
+        J.hrho = 0.5 * h1.w;
+        J.p = h2.w;
+        J.V2 = h0.w;
+        J.eta = P.mat[mat_of(kj)].eta;
+        R.eta = J.eta;  // eta_w := eta_i
+        double3 a = make_double3(0, 0, 0), bgd = make_double3(0, 0, 0);
+        pair_term<kTvf, true>(J, R, d, r2, P, a, bgd);
+        // f_ri = -m_i a_ir = -(V2 term): pair_term accumulates V2*term (a_ir = V2/m_i * term)
+        f.x -= a.x;
+        f.y -= a.y;
+        f.z -= a.z;
+      } else if (kindj == SPHG_BOUNDARY || D.group.p[j] != body) {
+        const double3 d = pair_delta<M>(P, pr, ld3(h0), e);  // r_r - r_j
+        const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+        if (!(r2 < P.dx * P.dx)) continue;
+        if (r2 == 0.0) {
+          coincident = true;
+          continue;
+        }
+        const double rr = sqrt(r2);
+        const double ri = 1.0 / rr;
+        const double3 e3 = make_double3(d.x * ri, d.y * ri, d.z * ri);
+        const double3 vj = ldpos(&D.V4.p[j]);
+        const double s = P.kc * (rr - P.dx) + P.dc * (e3.x * (vr.x - vj.x) + e3.y * (vr.y - vj.y) + e3.z * (vr.z - vj.z));
+        const double fm = -fmin(0.0, s);
+        f.x += fm * e3.x;
+        f.y += fm * e3.y;
+        f.z += fm * e3.z;
+      }
+    }
+  }
+  f.x = gsum<G>(f.x);
+  f.y = gsum<G>(f.y);
+  f.z = gsum<G>(f.z);
+  if (!active) return;
+  if (coincident) {
+    atomicOr(&fl->err, kErrCoincident);
+    atomicMin(&fl->err_gid, D.gid.p[r]);
+  }
+  if (lane == 0) D.F4.p[r] = make_double4(f.x, f.y, f.z, 0.0);
+}
+
+// Verlet candidates and pairs within r_c (exact test), all particles
+template <int G, int M>
+__global__ void __launch_bounds__(kBlock) k_count_pairs(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                         size_t n, unsigned long long* __restrict__ out) {
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  const size_t i = t / G;
+  const int lane = (int)(t % G);
+  double c = 0, in = 0;
+  if (i < n) {
+    const double3 pi = ldpos(&D.G0.p[i]);
+    const Row R = row_of(L, (uint32_t)i);
+    for (int k = lane; k < R.n; k += G) {
+      const uint32_t e = R.e[k];
+      const double3 pj = ldpos(&D.G0.p[nb_index<M>(e)]);
+      const double3 d = M == kImgNone ? make_double3(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z)
+                                      : mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z);
+      c += 1.0;
+      if (r2_exact(d) <= P.rc2) in += 1.0;
+    }
+  }
+  c = gsum<G>(c);
+  in = gsum<G>(in);
+  if (i < n && lane == 0) {
+    atomicAdd(out, (unsigned long long)c);
+    atomicAdd(out + 1, (unsigned long long)in);
+  }
+}
+
+__global__ void k_copy_boundary_T(Particles D, const uint32_t* __restrict__ list, size_t nlist,
+                                  double2* __restrict__ Hout) {
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nlist) return;
+  const uint32_t i = list[g];
+  if (kind_of(D.kmd.p[i]) == SPHG_BOUNDARY) Hout[i] = D.H2.p[i];
+}
+
+__device__ __forceinline__ double sched_value(const DevSchedule& s, double t) {  // Schedule::value_at
+  for (int k = 0; k < s.n; ++k)
+    if (t <= s.t_end[k]) return s.value[k];
+  return s.value[s.n - 1];
+}
+
+__global__ void k_dirichlet(const __grid_constant__ DevParams P, Particles D, const uint32_t* __restrict__ list,
+                            size_t nlist, double t_new) {
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nlist) return;
+  const uint32_t i = list[g];
+  const uint32_t kmd = D.kmd.p[i];
+  if (kind_of(kmd) != SPHG_BOUNDARY) return;
+  const uint32_t gr = dir_of(kmd);
+  if (gr == SPHG_NO_DIRICHLET || (int)gr >= P.n_sched || P.sched[gr].n <= 0) return;
+  reinterpret_cast<double*>(&D.H2.p[i])[0] = sched_value(P.sched[gr], t_new);
+}
+
+template <int G>
+int blocks_for(size_t groups) {
+  return grid_for(groups * G, kBlock);
+}
+
+}  // namespace
+
+// ============================================================= launchers
+// Lanes per particle (G): 8, 16 or 32, per kernel family (Ctx::group_*; default
+// from measurements; SPHG_GROUP_* environment overrides for tuning).
+#define SPHG_G_DISPATCH(GV, CALL)                       \
+  do {                                                  \
+    if ((GV) == 8) { constexpr int G = 8; CALL; }        \
+    else if ((GV) == 4) { constexpr int G = 4; CALL; }   \
+    else if ((GV) == 32) { constexpr int G = 32; CALL; } \
+    else { constexpr int G = 16; CALL; }                 \
+  } while (0)
+constexpr int kGOther = 8;
+
+#define SPHG_IMG_DISPATCH(MODE, CALL)                             \
+  do {                                                            \
+    switch (MODE) {                                               \
+      case kImgNone: { constexpr int M = kImgNone; CALL; break; } \
+      case kImgCode: { constexpr int M = kImgCode; CALL; break; } \
+      default: { constexpr int M = kImgMin; CALL; break; }        \
+    }                                                             \
+  } while (0)
+
+void launch_density(Ctx& c) {
+  if (c.nf == 0) return;
+  SPHG_G_DISPATCH(c.group_density,
+                  SPHG_IMG_DISPATCH(c.P.img_mode, (k_density<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                                       c.P, c.cur, c.nl(), c.fidx.p, c.nf))));
+  c.launches++;
+}
+
+void launch_heat(Ctx& c) {
+  if (c.n == 0) return;
+  const double t_new = c.t + c.P.dt;
+  constexpr int G = kGOther;
+  if (c.nw) k_dirichlet<<<grid_for(c.nw, 256), 256, 0, c.stream>>>(c.P, c.cur, c.widx.p, c.nw, t_new);
+  if (c.nf)
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.H2new.p, c.dflags)));
+  if (c.nrigid)
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.H2new.p, c.dflags)));
+  if (c.nw) k_copy_boundary_T<<<grid_for(c.nw, 256), 256, 0, c.stream>>>(c.cur, c.widx.p, c.nw, c.H2new.p);
+  std::swap(c.cur.H2, c.H2new);
+  c.launches += 4;
+}
+
+void launch_extrapolate(Ctx& c) {
+  if (c.nw == 0) return;
+  constexpr int G = kGOther;
+  if (c.P.single_eos)
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_extrapolate<G, M, false><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw)));
+  else
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_extrapolate<G, M, true><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw)));
+  c.launches++;
+}
+
+template <bool kTvf, bool kSingleEta>
+static void launch_forces_t(Ctx& c) {
+  if (c.nf)
+    SPHG_G_DISPATCH(c.group_forces,
+                    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta>
+                                                     <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
+  if (c.nrigid)
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGOther, M, kTvf, kSingleEta><<<blocks_for<kGOther>(c.nrigid), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.dflags)));
+  c.launches += 2;
+}
+
+void launch_forces(Ctx& c) {
+  if (c.n == 0) return;
+  const bool tvf = c.P.tvf != 0, single = c.P.single_eta != 0;
+  if (tvf && single) launch_forces_t<true, true>(c);
+  else if (tvf) launch_forces_t<true, false>(c);
+  else if (single) launch_forces_t<false, true>(c);
+  else launch_forces_t<false, false>(c);
+}
+
+void count_pairs(Ctx& c, int64_t* candidates, int64_t* interacting) {
+  if (!c.dcount) SPHG_CUDA_CHECK(cudaMalloc(&c.dcount, 2 * sizeof(unsigned long long)));
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.dcount, 0, 2 * sizeof(unsigned long long), c.stream));
+  constexpr int G = 16;
+  SPHG_IMG_DISPATCH(c.P.img_mode, (k_count_pairs<G, M><<<blocks_for<G>(c.n), kBlock, 0, c.stream>>>(
+                                       c.P, c.cur, c.nl(), c.n, c.dcount)));
+  unsigned long long h[2];
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(h, c.dcount, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  *candidates = (int64_t)h[0];
+  *interacting = (int64_t)h[1];
+}
+
+}  // namespace sphg

@@ -80,6 +80,10 @@ __global__ void k_cell_ranges(const uint32_t* __restrict__ key, size_t n, uint32
   if (k == n - 1 || key[k + 1] != c) cend[c] = (uint32_t)(k + 1);
 }
 
+// One warp per particle i: the 27 neighbour cells are scanned with the lanes
+// over the cell's particles (coalesced), hits are compacted with a ballot and
+// written contiguously into row i.  Entries carry the periodic image code of
+// the neighbour cell (kImgCode) so pair kernels skip the minimum-image tests.
 __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ DevParams P, const double4* __restrict__ G0,
                                                       const uint32_t* __restrict__ kmd,
                                                       const uint32_t* __restrict__ cell_key,
@@ -87,49 +91,66 @@ __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ Dev
                                                       const uint32_t* __restrict__ cend, uint32_t* __restrict__ nbr,
                                                       uint32_t* __restrict__ cnt, int cap, size_t n,
                                                       DevFlags* __restrict__ fl) {
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;  // warp-uniform
   const double4 pi = G0[i];
   const bool bi = kind_of(kmd[i]) == SPHG_BOUNDARY;
   const int64_t c = cell_key[i];
-  const int64_t nz = P.ncell[2], ny = P.ncell[1];
+  const int64_t nz = P.ncell[2], ny = P.ncell[1], nx = P.ncell[0];
   const int64_t cz = c % nz, cy = (c / nz) % ny, cx = c / (nz * ny);
+  const bool code = P.img_mode == kImgCode;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t* row = nbr + i * (size_t)cap;
   uint32_t count = 0;
   for (int ox = -1; ox <= 1; ++ox) {
     int64_t qx = cx + ox;
-    if (qx < 0 || qx >= P.ncell[0]) {
+    uint32_t ix = 0;
+    if (qx < 0 || qx >= nx) {
       if (!P.periodic[0]) continue;
-      qx = (qx + P.ncell[0]) % P.ncell[0];
+      ix = qx < 0 ? 1u : 2u;
+      qx = (qx + nx) % nx;
     }
     for (int oy = -1; oy <= 1; ++oy) {
       int64_t qy = cy + oy;
+      uint32_t iy = 0;
       if (qy < 0 || qy >= ny) {
         if (!P.periodic[1]) continue;
+        iy = qy < 0 ? 1u : 2u;
         qy = (qy + ny) % ny;
       }
       for (int oz = -1; oz <= 1; ++oz) {
         int64_t qz = cz + oz;
+        uint32_t iz = 0;
         if (qz < 0 || qz >= nz) {
           if (!P.periodic[2]) continue;
+          iz = qz < 0 ? 1u : 2u;
           qz = (qz + nz) % nz;
         }
+        const uint32_t tag = code ? ((ix << 26) | (iy << 28) | (iz << 30)) : 0u;
         const int64_t cj = (qx * ny + qy) * nz + qz;
         const uint32_t j0 = cstart[cj], j1 = cend[cj];
-        for (uint32_t j = j0; j < j1; ++j) {
-          if (j == i) continue;
-          if (bi && kind_of(kmd[j]) == SPHG_BOUNDARY) continue;
-          const double4 pj = G0[j];
-          const double3 d = mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z);
-          if (r2_exact(d) <= P.rv2) {
-            if ((int)count < cap) nbr[(size_t)count * n + i] = j;
-            ++count;
+        for (uint32_t jb = j0; jb < j1; jb += 32) {
+          const uint32_t j = jb + lane;
+          bool hit = false;
+          if (j < j1 && j != i && !(bi && kind_of(kmd[j]) == SPHG_BOUNDARY)) {
+            const double4 pj = G0[j];
+            hit = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) <= P.rv2;  // bit-exact test [P2]
           }
+          const uint32_t m = __ballot_sync(0xffffffffu, hit);
+          if (hit) {
+            const uint32_t pos = count + __popc(m & lt);
+            if ((int)pos < cap) row[pos] = j | tag;
+          }
+          count += __popc(m);
         }
       }
     }
   }
-  cnt[i] = count;
-  atomicMax(&fl->max_count, count);
+  if (lane == 0) {
+    cnt[i] = count;
+    atomicMax(&fl->max_count, count);
+  }
 }
 
 // ------------------------------------------------------- rigid index
@@ -163,11 +184,54 @@ int bits_for(uint64_t maxval) {  // bits needed to represent values in [0, maxva
   return b;
 }
 
+__global__ void k_kind_flags(const uint32_t* __restrict__ kmd, size_t n, uint32_t* __restrict__ ff,
+                             uint32_t* __restrict__ wf) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const bool fl = kind_of(kmd[k]) == SPHG_FLUID;
+  ff[k] = fl ? 1u : 0u;
+  wf[k] = fl ? 0u : 1u;
+}
+
+__global__ void k_kind_scatter(const uint32_t* __restrict__ kmd, const uint32_t* __restrict__ fpos,
+                               const uint32_t* __restrict__ wpos, size_t n, uint32_t* __restrict__ fidx,
+                               uint32_t* __restrict__ widx) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  if (kind_of(kmd[k]) == SPHG_FLUID) fidx[fpos[k]] = (uint32_t)k;
+  else widx[wpos[k]] = (uint32_t)k;
+}
+
 }  // namespace
+
+// fluid / non-fluid index lists (cell order) for the pair kernels
+static void launch_kind_lists(Ctx& c) {
+  const size_t n = c.n;
+  cudaStream_t s = c.stream;
+  c.fidx.alloc(std::max<size_t>(n, 1));
+  c.widx.alloc(std::max<size_t>(n, 1));
+  uint32_t* ff = c.vals.p;
+  uint32_t* wf = c.vals_alt.p;
+  uint32_t* fpos = reinterpret_cast<uint32_t*>(c.keys.p);
+  uint32_t* wpos = reinterpret_cast<uint32_t*>(c.keys_alt.p);
+  k_kind_flags<<<grid_for(n, 256), 256, 0, s>>>(c.cur.kmd.p, n, ff, wf);
+  exclusive_scan_u32(ff, fpos, n, c.scan_tmp.p, s, &c.launches);
+  exclusive_scan_u32(wf, wpos, n, c.scan_tmp.p, s, &c.launches);
+  uint32_t lastp = 0, lastf = 0;
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&lastp, fpos + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&lastf, ff + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  k_kind_scatter<<<grid_for(n, 256), 256, 0, s>>>(c.cur.kmd.p, fpos, wpos, n, c.fidx.p, c.widx.p);
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+  c.nf = (size_t)lastp + lastf;
+  c.nw = n - c.nf;
+  c.launches += 2;
+}
 
 void launch_rigid_index(Ctx& c) {
   const size_t n = c.n;
   cudaStream_t s = c.stream;
+  if (n == 0) return;
+  launch_kind_lists(c);
   c.ridx.alloc(std::max<size_t>(n, 1));
   c.body_start.alloc(2 * std::max<size_t>(c.nb, 1));
   uint32_t* flag = c.vals_alt.p;  // scratch
@@ -223,8 +287,8 @@ void launch_rebuild(Ctx& c) {
     if (c.cap <= 0) c.cap = c.params.nlist_capacity > 0 ? c.params.nlist_capacity : 144;
     c.nbr.alloc((size_t)c.cap * n);
     SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->max_count, 0, sizeof(uint32_t), s));
-    k_build_nlist<<<grid_for(n, 128), 128, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_key.p, c.cell_start.p,
-                                                   c.cell_end.p, c.nbr.p, c.cnt.p, c.cap, n, c.dflags);
+    k_build_nlist<<<grid_for(n * 32, 128), 128, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_key.p, c.cell_start.p,
+                                                        c.cell_end.p, c.nbr.p, c.cnt.p, c.cap, n, c.dflags);
     c.launches += 2;
     uint32_t mc = 0;
     SPHG_CUDA_CHECK(cudaMemcpyAsync(&mc, &c.dflags->max_count, 4, cudaMemcpyDeviceToHost, s));

@@ -86,9 +86,12 @@ __global__ void k_compact_by_gid(const uint32_t* __restrict__ ev, const uint32_t
 }
 
 // nearest pre-batch rigid particle within r_c (r^2, gid), from the Verlet list
+__device__ __forceinline__ uint32_t entry_index(const DevParams& P, uint32_t e) {
+  return P.img_mode == kImgCode ? (e & kIdxMask) : e;
+}
+
 __global__ void k_solid_target(const __grid_constant__ DevParams P, Particles D, const uint32_t* __restrict__ list,
-                               size_t m, const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ cnt, size_t n,
-                               int* __restrict__ target, uint32_t* __restrict__ spawn) {
+                               size_t m, NbrList L, int* __restrict__ target, uint32_t* __restrict__ spawn) {
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m) return;
   const uint32_t i = list[e];
@@ -96,8 +99,8 @@ __global__ void k_solid_target(const __grid_constant__ DevParams P, Particles D,
   double best = 1e300;
   uint32_t bg = 0xffffffffu;
   int tb = -1;
-  for (uint32_t k = 0; k < cnt[i]; ++k) {
-    const uint32_t j = nbr[(size_t)k * n + i];
+  for (uint32_t k = 0; k < L.cnt[i]; ++k) {
+    const uint32_t j = entry_index(P, L.nbr[(size_t)i * L.cap + k]);
     if (kind_of(D.kmd.p[j]) != SPHG_RIGID) continue;
     const double4 pj = D.G0.p[j];
     const double r2 = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z));
@@ -146,6 +149,9 @@ __global__ void k_solid_apply(const __grid_constant__ DevParams P, Particles D, 
   D.A4.p[i] = make_double4(0, 0, 0, 0);
   D.B4.p[i] = make_double4(0, 0, 0, 0);
   D.p_static.p[i] = 0.0;
+  // wall quantities are undefined until the next extrapolation: zero (oracle does the same)
+  D.G1.p[i] = make_double4(0, 0, 0, rho0);
+  D.G2.p[i] = make_double4(0, 0, 0, 0);
   reinterpret_cast<double*>(&D.H2.p[i])[1] = v.w / rho0;
 }
 
@@ -161,8 +167,7 @@ __global__ void k_label_init(Particles D, size_t n, const uint32_t* __restrict__
   label[k] = (kind_of(D.kmd.p[k]) == SPHG_RIGID && blost[D.group.p[k]]) ? D.gid.p[k] : 0xffffffffu;
 }
 
-__global__ void k_label_iter(const __grid_constant__ DevParams P, Particles D, size_t n,
-                             const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ cnt,
+__global__ void k_label_iter(const __grid_constant__ DevParams P, Particles D, size_t n, NbrList L,
                              uint32_t* __restrict__ label, double adj2, DevFlags* __restrict__ fl) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -171,8 +176,8 @@ __global__ void k_label_iter(const __grid_constant__ DevParams P, Particles D, s
   const uint32_t body = D.group.p[i];
   const double4 pi = D.G0.p[i];
   uint32_t best = l;
-  for (uint32_t k = 0; k < cnt[i]; ++k) {
-    const uint32_t j = nbr[(size_t)k * n + i];
+  for (uint32_t k = 0; k < L.cnt[i]; ++k) {
+    const uint32_t j = entry_index(P, L.nbr[i * L.cap + k]);
     if (kind_of(D.kmd.p[j]) != SPHG_RIGID || D.group.p[j] != body) continue;
     const double4 pj = D.G0.p[j];
     if (r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) > adj2) continue;
@@ -335,8 +340,7 @@ int launch_transitions(Ctx& c) {
     uint32_t* list = fl ? c.vals.p : c.vals_alt.p;
     c.ev_idx.alloc(nsolid);
     SPHG_CUDA_CHECK(cudaMemcpyAsync(c.ev_idx.p, list, nsolid * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    k_solid_target<<<grid_for(nsolid, 128), 128, 0, s>>>(c.P, c.cur, c.ev_idx.p, nsolid, c.nbr.p, c.cnt.p, n, target,
-                                                         spawn);
+    k_solid_target<<<grid_for(nsolid, 128), 128, 0, s>>>(c.P, c.cur, c.ev_idx.p, nsolid, c.nl(), target, spawn);
     exclusive_scan_u32(spawn, rank, nsolid, c.scan_tmp.p, s, &c.launches);
     nspawn = read_u32(c, rank + nsolid - 1) + read_u32(c, spawn + nsolid - 1);
     k_solid_apply<<<grid_for(nsolid, 128), 128, 0, s>>>(c.P, c.cur, c.ev_idx.p, nsolid, target, rank, nb0,
@@ -352,7 +356,7 @@ int launch_transitions(Ctx& c) {
     const double adj2 = (1.5 * c.P.dx) * (1.5 * c.P.dx);
     for (int it = 0; it < 100000; ++it) {
       SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->changed, 0, sizeof(uint32_t), s));
-      k_label_iter<<<grid_for(n, 128), 128, 0, s>>>(c.P, c.cur, n, c.nbr.p, c.cnt.p, c.label.p, adj2, c.dflags);
+      k_label_iter<<<grid_for(n, 128), 128, 0, s>>>(c.P, c.cur, n, c.nl(), c.label.p, adj2, c.dflags);
       c.launches += 2;
       if (!read_u32(c, &c.dflags->changed)) break;
     }
