@@ -6,7 +6,7 @@ import os
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsphg.so")
+LIB_PATH = os.path.join(HERE, os.environ.get("SPHG_LIB", "libsphg.so"))
 _lib = None
 
 

@@ -13,21 +13,21 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-ccbin", "/usr/bin/g++"]
 
 
-def build(verbose=False, force=False):
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose=False, force=False, out=OUT, extra=(), build_dir=BUILD):
+    os.makedirs(build_dir, exist_ok=True)
     objs = []
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     deps.append(os.path.join(HERE, "..", "include", "sphg.h"))
     dep_t = max(os.path.getmtime(d) for d in deps)
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(obj)
         if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(sp), dep_t):
             continue
-        cmd = [NVCC] + FLAGS + ["-c", sp, "-o", obj]
+        cmd = [NVCC] + FLAGS + list(extra) + ["-c", sp, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        log = os.path.join(BUILD, src + ".log")
+        log = os.path.join(build_dir, src + ".log")
         with open(log, "w") as f:
             f.write(r.stdout + r.stderr)
         if r.returncode != 0:
@@ -35,12 +35,12 @@ def build(verbose=False, force=False):
             raise RuntimeError(f"nvcc failed for {src}")
         if verbose:
             print(r.stderr)
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-ccbin", "/usr/bin/g++", "-Xcompiler", "-fopenmp", "-o", OUT] + objs + ["-lgomp"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-ccbin", "/usr/bin/g++", "-Xcompiler", "-fopenmp", "-o", out] + objs + ["-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -515,6 +515,7 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
   c.ncells = (int64_t)c.P.ncell[0] * c.P.ncell[1] * c.P.ncell[2];
   if (const char* e = std::getenv("SPHG_GROUP_DENSITY")) c.group_density = std::atoi(e);
   if (const char* e = std::getenv("SPHG_GROUP_FORCES")) c.group_forces = std::atoi(e);
+  if (const char* e = std::getenv("SPHG_UNROLL_FORCES")) c.unroll_forces = std::atoi(e);
   try {
     SPHG_CUDA_CHECK(cudaSetDevice(device));
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));

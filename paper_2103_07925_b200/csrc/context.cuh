@@ -91,7 +91,8 @@ struct Ctx {
   // per-kind index lists: fluid, non-fluid (rigid + boundary), rigid body-major
   DBuf<uint32_t> fidx, widx, ridx, body_start;
   size_t nf = 0, nw = 0, nrigid = 0;
-  int group_density = 8, group_forces = 8;  // lanes per particle in the pair kernels
+  int group_density = 4, group_forces = 4;  // lanes per particle in the pair kernels
+  int unroll_forces = 1;
   // transitions scratch
   DBuf<uint32_t> ev_idx, ev_flag, label, tscratch;
   // flags

@@ -23,18 +23,26 @@ namespace sphg {
 namespace {
 
 constexpr int kBlock = 128;
+#ifndef SPHG_FORCES_MINB
+#define SPHG_FORCES_MINB 1
+#endif
 
 __device__ __forceinline__ double3 ld3(const double4& v) { return make_double3(v.x, v.y, v.z); }
-__device__ __forceinline__ double3 ldpos(const double4* p) {  // xyz only (never touches .w)
-  const double2 xy = *reinterpret_cast<const double2*>(p);
-  const double z = reinterpret_cast<const double*>(p)[2];
-  return make_double3(xy.x, xy.y, z);
+// One 32-byte load per particle record (sm_100 LDG.E.ENL2.256): a record is one
+// sector, so a gather costs one sector instead of two 16-byte requests.
+__device__ __forceinline__ double4 ldg4(const double4* p) {  // read-only (non-coherent) path
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
 }
-__device__ __forceinline__ double4 ldg4(const double4* p) {  // read-only path, 2 x 16 B
-  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-  return make_double4(a.x, a.y, b.x, b.y);
+__device__ __forceinline__ double4 ld4(const double4* p) {  // coherent path (array written in-kernel)
+  double4 v;
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
 }
+// xyz of a record whose .w may be written concurrently by its owner (density,
+// extrapolation): the 32-byte load is atomic per 8-byte word and .w is unused.
+__device__ __forceinline__ double3 ldpos(const double4* p) { return ld3(ld4(p)); }
 __device__ __forceinline__ Quat body_q(const sphg_body& b) { return {b.q[0], b.q[1], b.q[2], b.q[3]}; }
 __device__ __forceinline__ double3 bv(const double* p) { return make_double3(p[0], p[1], p[2]); }
 
@@ -47,6 +55,15 @@ __device__ __forceinline__ Row row_of(const NbrList& L, uint32_t i) {
 }
 
 // ---------------------------------------------------------------- density
+template <int M>
+__device__ __forceinline__ double density_term(const DevParams& P, double3 pi, double3 pj, uint32_t e) {
+  const double3 d = pair_delta<M>(P, pi, pj, e);
+  const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+  if (r2 > P.rc2) return 0.0;
+  double ri;
+  return shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);  // + tiny: coincident -> W(0)
+}
+
 // rho_i = m_i sigma (66 + sum_j shape(r_ij/h)); p_i = c^2 (rho_i - rho0); V_i = m_i/rho_i
 template <int G, int M>
 __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevParams P, Particles D, NbrList L,
@@ -60,15 +77,17 @@ __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevP
   if (active) {
     const double3 pi = ldpos(&D.G0.p[i]);
     const Row R = row_of(L, i);
-    for (int k = lane; k < R.n; k += G) {
+    int k = lane;
+    for (; k + G < R.n; k += 2 * G) {  // two independent gathers in flight
+      const uint32_t e0 = __ldg(R.e + k), e1 = __ldg(R.e + k + G);
+      const double3 p0 = ldpos(&D.G0.p[nb_index<M>(e0)]);
+      const double3 p1 = ldpos(&D.G0.p[nb_index<M>(e1)]);
+      s += density_term<M>(P, pi, p0, e0);
+      s += density_term<M>(P, pi, p1, e1);
+    }
+    if (k < R.n) {
       const uint32_t e = __ldg(R.e + k);
-      const double3 pj = ldpos(&D.G0.p[nb_index<M>(e)]);
-      const double3 d = pair_delta<M>(P, pi, pj, e);
-      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
-      if (r2 <= P.rc2) {
-        double ri;
-        s += shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);  // + tiny: coincident -> W(0)
-      }
+      s += density_term<M>(P, pi, ldpos(&D.G0.p[nb_index<M>(e)]), e);
     }
   }
   s = gsum<G>(s);
@@ -277,10 +296,40 @@ __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, 
   bg.z = fma(V2, gW.z, bg.z);
 }
 
-template <int G, int M, bool kTvf, bool kSingleEta>
-__global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__ DevParams P, Particles D, NbrList L,
-                                                          const uint32_t* __restrict__ list, size_t nlist,
-                                                          DevFlags* __restrict__ fl) {
+template <int M, bool kTvf, bool kSingleEta>
+__device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
+                                           uint32_t e, double4 h0, double4 h1, double4 h2, double3& acc,
+                                           double3& bg, bool& coincident) {
+  const double3 d = pair_delta<M>(P, pi, ld3(h0), e);
+  const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+  if (r2 > P.rc2) return;
+  if (r2 == 0.0) {
+    coincident = true;
+    return;
+  }
+  PairSide J;
+  J.u = ld3(h1);
+  J.du = ld3(h2);
+  J.rho = h1.w;
+  J.hrho = 0.5 * h1.w;
+  J.p = h2.w;
+  J.V2 = h0.w;
+  if (kSingleEta) {
+    J.eta = I.eta;
+  } else {
+    const uint32_t kj = __ldg(&D.kmd.p[nb_index<M>(e)]);
+    J.eta = kind_of(kj) == SPHG_FLUID ? P.mat[mat_of(kj)].eta : I.eta;  // eta_w := eta_i [P7]
+  }
+  pair_term<kTvf, kSingleEta>(I, J, d, r2, P, acc, bg);
+}
+
+// kUnroll = 2: two neighbours per iteration, all six 32-byte records requested
+// before any arithmetic (memory-level parallelism against the gather latency).
+template <int G, int M, bool kTvf, bool kSingleEta, int kUnroll>
+__global__ void __launch_bounds__(kBlock, SPHG_FORCES_MINB) k_forces_fluid(const __grid_constant__ DevParams P,
+                                                                            Particles D, NbrList L,
+                                                                            const uint32_t* __restrict__ list,
+                                                                            size_t nlist, DevFlags* __restrict__ fl) {
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
@@ -302,33 +351,23 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
     I.eta = P.mat[mat_of(kmd)].eta;
     const double3 pi = ld3(g0);
     const Row R = row_of(L, i);
-    for (int k = lane; k < R.n; k += G) {
+    int k = lane;
+    if (kUnroll == 2) {
+      for (; k + G < R.n; k += 2 * G) {
+        const uint32_t e0 = __ldg(R.e + k), e1 = __ldg(R.e + k + G);
+        const uint32_t j0 = nb_index<M>(e0), j1 = nb_index<M>(e1);
+        const double4 a0 = ldg4(&D.G0.p[j0]), b0 = ldg4(&D.G0.p[j1]);
+        const double4 a1 = ldg4(&D.G1.p[j0]), b1 = ldg4(&D.G1.p[j1]);
+        const double4 a2 = ldg4(&D.G2.p[j0]), b2 = ldg4(&D.G2.p[j1]);
+        fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e0, a0, a1, a2, acc, bg, coincident);
+        fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e1, b0, b1, b2, acc, bg, coincident);
+      }
+    }
+    for (; k < R.n; k += G) {
       const uint32_t e = __ldg(R.e + k);
       const uint32_t j = nb_index<M>(e);
-      const double4 h0 = ldg4(&D.G0.p[j]);
-      const double3 d = pair_delta<M>(P, pi, ld3(h0), e);
-      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
-      if (r2 > P.rc2) continue;
-      if (r2 == 0.0) {
-        coincident = true;
-        continue;
-      }
-      const double4 h1 = ldg4(&D.G1.p[j]);
-      const double4 h2 = ldg4(&D.G2.p[j]);
-      PairSide J;
-      J.u = ld3(h1);
-      J.du = ld3(h2);
-      J.rho = h1.w;
-      J.hrho = 0.5 * h1.w;
-      J.p = h2.w;
-      J.V2 = h0.w;
-      if (kSingleEta) {
-        J.eta = I.eta;
-      } else {
-        const uint32_t kj = __ldg(&D.kmd.p[j]);
-        J.eta = kind_of(kj) == SPHG_FLUID ? P.mat[mat_of(kj)].eta : I.eta;  // eta_w := eta_i [P7]
-      }
-      pair_term<kTvf, kSingleEta>(I, J, d, r2, P, acc, bg);
+      const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
+      fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
     }
   }
   acc.x = gsum<G>(acc.x);
@@ -505,11 +544,10 @@ int blocks_for(size_t groups) {
 #define SPHG_G_DISPATCH(GV, CALL)                       \
   do {                                                  \
     if ((GV) == 8) { constexpr int G = 8; CALL; }        \
-    else if ((GV) == 4) { constexpr int G = 4; CALL; }   \
-    else if ((GV) == 32) { constexpr int G = 32; CALL; } \
-    else { constexpr int G = 16; CALL; }                 \
+    else if ((GV) == 2) { constexpr int G = 2; CALL; }   \
+    else { constexpr int G = 4; CALL; }                  \
   } while (0)
-constexpr int kGOther = 8;
+constexpr int kGOther = 4;
 
 #define SPHG_IMG_DISPATCH(MODE, CALL)                             \
   do {                                                            \
@@ -558,9 +596,14 @@ void launch_extrapolate(Ctx& c) {
 
 template <bool kTvf, bool kSingleEta>
 static void launch_forces_t(Ctx& c) {
-  if (c.nf)
+  if (c.nf && c.unroll_forces == 2)
     SPHG_G_DISPATCH(c.group_forces,
-                    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta>
+                    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 2>
+                                                     <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
+  else if (c.nf)
+    SPHG_G_DISPATCH(c.group_forces,
+                    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 1>
                                                      <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
   if (c.nrigid)
