@@ -193,7 +193,7 @@ def run_sph(args):
     sim.initialize()
     for _ in range(args.warmup):
         sim.step(1)
-    cand, inter = sim.count_pairs()
+    cand, inter, inter_fluid, inter_other = sim.count_pairs()
     # timed region: K full steps, CUDA events recorded on the library's stream around sphg_step
     st0 = sim.stats()
     torch.cuda.synchronize()
@@ -211,29 +211,33 @@ def run_sph(args):
     sb = sim.stats()
     sim.set_timing(False)
     kk = max(2, args.steps // 2)
-    stage_ms = {abi.STAGE_NAMES[k]: (sb.stage_ms[k] - sa.stage_ms[k]) / kk for k in range(10)}
+    stage_ms = {abi.STAGE_NAMES[k]: (sb.stage_ms[k] - sa.stage_ms[k]) / kk for k in range(12)}
     launches = (st1.kernel_launches - st0.kernel_launches)
     value = n / (ms_step * 1e-3)
     peaks = load_peaks()
     info = sc.info
     nf = info["n_fluid"]
-    frac_fluid_pairs = inter / max(n, 1)  # interacting pairs per particle (all kinds)
-    t_forces = stage_ms["forces"] * 1e-3
-    t_density = stage_ms["density"] * 1e-3
-    forces_bytes = FORCES_BYTES_PER_FLUID * nf
-    achieved = forces_bytes / t_forces / 1e9
-    roofline = {"bound": "hbm", "kernel": "forces (k_forces_fluid + k_forces_rigid)",
-                "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-                "bytes_model": f"{FORCES_BYTES_PER_FLUID:g} B per fluid particle (SURVEY 8(d) CSM)",
-                "peak_source": peaks["source"]}
-    flops = FLOPS_PER_PAIR_FORCES * inter * (nf / n)
-    fp64 = {"kernel": "forces", "achieved_tflops": flops / t_forces / 1e12,
-            "interacting_pairs": inter, "candidate_pairs": cand,
-            "flops_model": f"{FLOPS_PER_PAIR_FORCES:g} flop per interacting pair (SURVEY 8(d))"}
-    if "fp64_tflops" in peaks:
-        fp64["peak_tflops"] = peaks["fp64_tflops"]
-        fp64["frac"] = fp64["achieved_tflops"] / peaks["fp64_tflops"]
+    # dominant kernel: k_forces_fluid (stage 10), average launch duration from CUDA events on
+    # the library stream over the breakdown pass; algorithmic flops = 91 per interacting pair
+    # with a fluid i; algorithmic bytes = 156 B per fluid particle (CSM model).
+    t_ff = stage_ms["forces_fluid"] * 1e-3
+    flops = FLOPS_PER_PAIR_FORCES * inter_fluid
+    achieved_tf = flops / t_ff / 1e12
+    fp64_peak = peaks.get("fp64_tflops")
+    hbm_achieved = FORCES_BYTES_PER_FLUID * nf / t_ff / 1e9
+    roofline = {"bound": "fp64", "kernel": "k_forces_fluid (momentum_rhs + TVF)",
+                "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": (achieved_tf / fp64_peak) if fp64_peak else None,
+                "traffic": None, "launch_ms": stage_ms["forces_fluid"],
+                "flops_per_launch": flops, "flops_model": "91 flop per interacting fluid pair (SURVEY 8(d))",
+                "peak_source": "profiles/fp64_peak.json (DFMA microbenchmark, tools/fp64_peak.cu)",
+                "hbm": {"achieved": hbm_achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": hbm_achieved / peaks["hbm_gbs"], "bytes_model": "156 B per fluid particle (CSM)",
+                        "peak_source": peaks["source"]}}
+    fp64 = {"pairs_candidate": cand, "pairs_interacting": inter, "pairs_fluid_i": inter_fluid,
+            "pairs_nonfluid_i": inter_other,
+            "step_tflops": (FLOPS_PER_PAIR_FORCES * inter_fluid + FLOPS_PER_PAIR_DENSITY * inter_fluid)
+                           / (ms_step * 1e-3) / 1e12}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64 lattice + jitter)",

@@ -1,0 +1,164 @@
+// device_simulation.hpp — drop-in C++ adapter: the reference's own container
+// and configuration types (sphfsi::ParticleStore<3>, sphfsi::ScenarioConfig<3>,
+// /root/reference/proj/include/sphfsi) driven through the C ABI of sphg.h.
+//
+// A C++ caller of the reference keeps its ParticleStore and calls the SPEC
+// operation names (density_summation, momentum_rhs, reduce_force_torque, step,
+// ...); the store's vectors are handed to the device unchanged — Vec<3> is
+// std::array<double,3> (24 B), so pos.data() is the interleaved xyz layout the
+// ABI expects (store.hpp:26-46).  Header-only; link with libsphg.so.
+#pragma once
+
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sphfsi/config.hpp"
+#include "sphfsi/store.hpp"
+#include "sphg.h"
+
+namespace sphfsi_gpu {
+
+static_assert(sizeof(sphfsi::Vec<3>) == 3 * sizeof(double), "Vec<3> must be 24 bytes (interleaved xyz)");
+static_assert(sizeof(sphfsi::Kind) == 1 && sizeof(sphfsi::MaterialId) == 2, "ParticleStore tag widths");
+
+class Error : public std::runtime_error {
+ public:
+  Error(int code, const std::string& m) : std::runtime_error(m), code(code) {}
+  int code;
+};
+
+/// sphfsi::ScenarioConfig<3> (config.hpp:68-106) -> flat POD of the C ABI.
+inline sphg_params to_params(const sphfsi::ScenarioConfig<3>& cfg, double dt, int thermal, int transitions,
+                             double contact_damping_override = -1.0) {
+  sphg_params p;
+  std::memset(&p, 0, sizeof(p));
+  p.dx = cfg.dx;
+  p.h = cfg.smoothing_length;
+  p.dt = dt;
+  for (int a = 0; a < 3; ++a) {
+    p.lo[a] = cfg.domain.lo[a];
+    p.hi[a] = cfg.domain.hi[a];
+    p.periodic[a] = cfg.periodic[a] ? 1 : 0;
+  }
+  p.cell_edge_override = cfg.cell_edge_override;
+  p.n_mat = (int32_t)cfg.materials.size();
+  if (p.n_mat > SPHG_MAX_MAT) throw Error(SPHG_ERR_CONFIG, "too many materials for the device table");
+  for (sphfsi::MaterialId m = 0; m < cfg.materials.size(); ++m) {
+    const sphfsi::Material& s = cfg.materials[m];
+    sphg_material& d = p.mat[m];
+    d.rho0 = s.reference_density;
+    d.nu = s.kinematic_viscosity;
+    d.cp = s.heat_capacity;
+    d.kappa = s.conductivity;
+    d.c = s.speed_of_sound;
+    d.pb = s.background_pressure;
+    d.T_t = s.transition_temperature;
+    d.melt_target = s.melt_target == sphfsi::kNoMaterial ? SPHG_NO_MATERIAL : s.melt_target;
+    d.solidify_target = s.solidify_target == sphfsi::kNoMaterial ? SPHG_NO_MATERIAL : s.solidify_target;
+    const sphfsi::Vec<3> b = cfg.body_force_of(m);
+    for (int a = 0; a < 3; ++a) d.body_force[a] = b[a];
+  }
+  p.kc = cfg.contact_stiffness;
+  p.dc = contact_damping_override >= 0.0 ? contact_damping_override : cfg.contact_damping;
+  p.tvf = cfg.transport_velocity ? 1 : 0;
+  p.thermal = thermal;
+  p.transitions = transitions;
+  p.n_dirichlet = (int32_t)cfg.dirichlet_temperature.size();
+  for (int g = 0; g < p.n_dirichlet && g < SPHG_MAX_DIRICHLET; ++g) {
+    const auto& pcs = cfg.dirichlet_temperature[g].pieces;
+    p.dirichlet_T[g].n = (int32_t)pcs.size();
+    for (size_t k = 0; k < pcs.size() && k < SPHG_MAX_PIECES; ++k) {
+      p.dirichlet_T[g].t_end[k] = pcs[k].t_end;
+      p.dirichlet_T[g].value[k] = pcs[k].value;
+    }
+  }
+  p.rank = 0;
+  p.nranks = cfg.workers;
+  return p;
+}
+
+/// Views of a ParticleStore<3> for the ABI (no copies).
+inline sphg_soa views(sphfsi::ParticleStore<3>& s, std::vector<sphfsi::Vec<3>>* force = nullptr) {
+  sphg_soa v;
+  std::memset(&v, 0, sizeof(v));
+  v.n = s.size();
+  auto d3 = [](std::vector<sphfsi::Vec<3>>& x) { return reinterpret_cast<double*>(x.data()); };
+  v.pos = d3(s.pos);
+  v.vel = d3(s.vel);
+  v.vel_adv = d3(s.vel_adv);
+  v.acc = d3(s.acc);
+  v.acc_bg = d3(s.acc_bg);
+  v.density = s.density.data();
+  v.pressure = s.pressure.data();
+  v.mass = s.mass.data();
+  v.temperature = s.temperature.data();
+  v.dT_dt = s.dT_dt.data();
+  v.kind = reinterpret_cast<uint8_t*>(s.kind.data());
+  v.group = s.group.data();
+  v.material = s.material.data();
+  v.body_frame_pos = d3(s.body_frame_pos);
+  v.wall_pressure = s.wall_pressure.data();
+  v.wall_velocity = d3(s.wall_velocity);
+  v.dirichlet_T = s.dirichlet_T.data();
+  if (force) {
+    force->resize(s.size());
+    v.force = d3(*force);
+  }
+  return v;
+}
+
+/// One device (rank) running the hot path over a reference ParticleStore.
+class DeviceSimulation {
+ public:
+  DeviceSimulation(const sphg_params& p, int device = 0) {
+    const int rc = sphg_create(&p, device, &ctx_);
+    if (rc != SPHG_OK) {
+      char buf[2048];
+      sphg_validate(&p, buf, sizeof(buf));
+      throw Error(rc, std::string("sphg_create: ") + buf);
+    }
+  }
+  ~DeviceSimulation() { sphg_destroy(ctx_); }
+  DeviceSimulation(const DeviceSimulation&) = delete;
+  DeviceSimulation& operator=(const DeviceSimulation&) = delete;
+
+  void upload(sphfsi::ParticleStore<3>& s, const std::vector<sphg_body>& bodies) {
+    sphg_soa v = views(s);
+    check(sphg_upload(ctx_, &v, bodies.data(), bodies.size()), "upload");
+  }
+  void download(sphfsi::ParticleStore<3>& s, std::vector<sphg_body>& bodies, std::vector<sphfsi::Vec<3>>* force = nullptr) {
+    sphg_soa v = views(s, force);
+    size_t nb = 0;
+    check(sphg_num_bodies(ctx_, &nb), "num_bodies");
+    bodies.resize(nb);
+    check(sphg_download(ctx_, &v, bodies.data(), &nb), "download");
+  }
+  // SPEC operations, bulk over the store
+  void build_pairs() { stage(SPHG_STAGE_REBUILD); }
+  void density_summation() { stage(SPHG_STAGE_DENSITY); }
+  void conduction_rhs() { stage(SPHG_STAGE_HEAT); }
+  void extrapolate_wall_quantities() { stage(SPHG_STAGE_EXTRAPOLATE); }
+  void momentum_rhs() { stage(SPHG_STAGE_FORCES); }
+  void reduce_force_torque() { stage(SPHG_STAGE_BODIES); }
+  void reduce_mass_quantities() { stage(SPHG_STAGE_MASS); }
+  void apply_transitions() { stage(SPHG_STAGE_TRANSITIONS); }
+  void initialize() { check(sphg_initialize(ctx_), "initialize"); }
+  void step(int n = 1) { check(sphg_step(ctx_, n), "step"); }
+  sphg_stats_t stats() {
+    sphg_stats_t s;
+    check(sphg_stats(ctx_, &s), "stats");
+    return s;
+  }
+
+ private:
+  void stage(int s) { check(sphg_run_stage(ctx_, s), "run_stage"); }
+  void check(int rc, const char* what) {
+    if (rc != SPHG_OK) throw Error(rc, std::string(what) + ": " + sphg_last_error(ctx_));
+  }
+  sphg_ctx* ctx_ = nullptr;
+};
+
+}  // namespace sphfsi_gpu

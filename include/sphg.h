@@ -155,7 +155,8 @@ typedef struct {
   double time;
   double max_displacement;    /* since the last rebuild */
   double u_max;               /* max |u| of fluid particles at the last kick */
-  double stage_ms[10];        /* accumulated device time per stage (if timing enabled) */
+  double stage_ms[16];        /* accumulated device time per stage (if timing enabled);
+                                 10 = fluid forces kernel, 11 = rigid forces kernel (both inside 4) */
   int64_t kernel_launches;
   double last_step_call_ms;   /* device time of the last sphg_step call (CUDA events on the stream) */
 } sphg_stats_t;
@@ -189,8 +190,9 @@ int sphg_compute_dt(sphg_ctx* ctx, double limits[5]);
 /* The five limits of compute_dt without a context (pure host function):
  * u_max = max fluid speed, m_r = smallest rigid particle mass (<= 0: no contact term). */
 int sphg_dt_limits(const sphg_params* params, double u_max, double m_r, double limits[5]);
-/* Candidate pairs of the current Verlet list and pairs within r_c (interacting). */
-int sphg_count_pairs(sphg_ctx* ctx, int64_t* candidates, int64_t* interacting);
+/* Pair counts of the current Verlet list: [0] candidates, [1] within r_c (interacting),
+ * [2] interacting with a fluid particle i (the fluid force kernel's pairs), [3] with a non-fluid i. */
+int sphg_count_pairs(sphg_ctx* ctx, int64_t counts[4]);
 const char* sphg_last_error(const sphg_ctx* ctx);
 void sphg_destroy(sphg_ctx* ctx);
 /* Messages of validate_config for `params` joined by '\n' (empty = valid). */

@@ -27,7 +27,8 @@ STAGE_TRANSITIONS = 8
 STAGE_MASS = 9
 
 STAGE_NAMES = ["rebuild", "density", "heat", "extrapolate", "forces", "bodies",
-               "kick_drift", "final_kick", "transitions", "mass"]
+               "kick_drift", "final_kick", "transitions", "mass", "forces_fluid", "forces_rigid",
+               "", "", "", ""]
 
 
 class Material(C.Structure):
@@ -90,7 +91,7 @@ class Stats(C.Structure):
                 ("bodies_alive", C.c_int64), ("nlist_capacity", C.c_int32),
                 ("max_neighbours", C.c_int32), ("cells", C.c_int32 * 3), ("pad", C.c_int32),
                 ("time", C.c_double), ("max_displacement", C.c_double), ("u_max", C.c_double),
-                ("stage_ms", C.c_double * 10), ("kernel_launches", C.c_int64),
+                ("stage_ms", C.c_double * 16), ("kernel_launches", C.c_int64),
                 ("last_step_call_ms", C.c_double)]
 
 
@@ -116,7 +117,7 @@ def declare(lib, prefix):
         "set_timing": (C.c_int, [vp, C.c_int]),
         "compute_dt": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "dt_limits": (C.c_int, [C.POINTER(Params), C.c_double, C.c_double, C.POINTER(C.c_double)]),
-        "count_pairs": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+        "count_pairs": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     }
     for name, (res, args) in list(sig.items()) + list(optional.items()):
         fn = getattr(lib, prefix + name, None)

@@ -244,6 +244,13 @@ void timed(Ctx& c, int stage, void (*fn)(Ctx&)) {
   c.stage_ms[stage] += ms;
 }
 
+void timed_forces(Ctx& c) {  // stage 4 = 10 (fluid kernel) + 11 (rigid kernel)
+  const double before10 = c.stage_ms[10], before11 = c.stage_ms[11];
+  timed(c, 10, launch_forces_fluid);
+  timed(c, 11, launch_forces_rigid);
+  c.stage_ms[SPHG_STAGE_FORCES] += (c.stage_ms[10] - before10) + (c.stage_ms[11] - before11);
+}
+
 void kick_all(Ctx& c) {
   launch_body_kick(c);
   launch_kick_drift(c);
@@ -265,7 +272,7 @@ int do_stage(sphg_ctx* h, int stage) {
       if (c.P.thermal) timed(c, stage, launch_heat);
       break;
     case SPHG_STAGE_EXTRAPOLATE: timed(c, stage, launch_extrapolate); break;
-    case SPHG_STAGE_FORCES: timed(c, stage, launch_forces); break;
+    case SPHG_STAGE_FORCES: timed_forces(c); break;
     case SPHG_STAGE_BODIES: timed(c, stage, launch_bodies); break;
     case SPHG_STAGE_KICK_DRIFT:
       reset_step_flags(c);
@@ -304,7 +311,7 @@ int one_step(sphg_ctx* h) {
   timed(c, SPHG_STAGE_DENSITY, launch_density);
   if (c.P.thermal) timed(c, SPHG_STAGE_HEAT, launch_heat);
   timed(c, SPHG_STAGE_EXTRAPOLATE, launch_extrapolate);
-  timed(c, SPHG_STAGE_FORCES, launch_forces);
+  timed_forces(c);
   timed(c, SPHG_STAGE_BODIES, launch_bodies);
   timed(c, SPHG_STAGE_FINAL_KICK, launch_final_kick);
   h->mid_step = false;
@@ -728,7 +735,7 @@ int sphg_stats(sphg_ctx* h, sphg_stats_t* s) {
     s->time = c.t;
     s->max_displacement = c.max_disp;
     s->u_max = c.u_max;
-    for (int k = 0; k < 10; ++k) s->stage_ms[k] = c.stage_ms[k];
+    for (int k = 0; k < 16; ++k) s->stage_ms[k] = c.stage_ms[k];
     s->kernel_launches = c.launches;
     s->last_step_call_ms = c.last_step_ms;
     if (c.built && c.n) {
@@ -789,16 +796,16 @@ int sphg_compute_dt(sphg_ctx* h, double lim[5]) {
   });
 }
 
-int sphg_count_pairs(sphg_ctx* h, int64_t* candidates, int64_t* interacting) {
+int sphg_count_pairs(sphg_ctx* h, int64_t out[4]) {
   return guarded(h, [&]() -> int {
     Ctx& c = h->c;
-    *candidates = *interacting = 0;
+    for (int k = 0; k < 4; ++k) out[k] = 0;
     if (c.n == 0) return SPHG_OK;
     if (!c.built) {
       const int rc = do_stage(h, SPHG_STAGE_REBUILD);
       if (rc) return rc;
     }
-    count_pairs(c, candidates, interacting);
+    count_pairs(c, out);
     return SPHG_OK;
   });
 }

@@ -107,7 +107,7 @@ struct Ctx {
   int max_count = 0;
   bool timing = false;
   cudaEvent_t ev[2] = {nullptr, nullptr};
-  double stage_ms[10] = {0};
+  double stage_ms[16] = {0};
   std::string err;
   // host staging for body table (pinned)
   sphg_body* hbodies = nullptr;
@@ -140,13 +140,15 @@ void launch_density(Ctx& c);
 void launch_heat(Ctx& c);
 void launch_extrapolate(Ctx& c);
 void launch_forces(Ctx& c);
+void launch_forces_fluid(Ctx& c);
+void launch_forces_rigid(Ctx& c);
 void launch_bodies(Ctx& c);
 void launch_final_kick(Ctx& c);
 void launch_mass(Ctx& c, const uint32_t* body_mask);
 void gather_by_gid(Ctx& c);          // cur[k] <- alt[gid[k]] for every field but gid/R4
 bool displacement_exceeds(Ctx& c);   // max |r - r_ref| > half skin (syncs)
 void iota_gid(Ctx& c);
-void count_pairs(Ctx& c, int64_t* candidates, int64_t* interacting);
+void count_pairs(Ctx& c, int64_t out[4]);
 
 // kernels_transition.cu
 int launch_transitions(Ctx& c);  // 0 ok, else error code

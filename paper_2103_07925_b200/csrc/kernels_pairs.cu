@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
   if (lane == 0) D.F4.p[r] = make_double4(f.x, f.y, f.z, 0.0);
 }
 
-// Verlet candidates and pairs within r_c (exact test), all particles
+// Verlet candidates and pairs within r_c (exact test), all particles; split by kind of i
 template <int G, int M>
 __global__ void __launch_bounds__(kBlock) k_count_pairs(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                          size_t n, unsigned long long* __restrict__ out) {
@@ -485,7 +485,9 @@ __global__ void __launch_bounds__(kBlock) k_count_pairs(const __grid_constant__ 
   const size_t i = t / G;
   const int lane = (int)(t % G);
   double c = 0, in = 0;
+  bool fluid = false;
   if (i < n) {
+    fluid = kind_of(D.kmd.p[i]) == SPHG_FLUID;
     const double3 pi = ldpos(&D.G0.p[i]);
     const Row R = row_of(L, (uint32_t)i);
     for (int k = lane; k < R.n; k += G) {
@@ -502,6 +504,7 @@ __global__ void __launch_bounds__(kBlock) k_count_pairs(const __grid_constant__ 
   if (i < n && lane == 0) {
     atomicAdd(out, (unsigned long long)c);
     atomicAdd(out + 1, (unsigned long long)in);
+    atomicAdd(out + (fluid ? 2 : 3), (unsigned long long)in);
   }
 }
 
@@ -595,7 +598,7 @@ void launch_extrapolate(Ctx& c) {
 }
 
 template <bool kTvf, bool kSingleEta>
-static void launch_forces_t(Ctx& c) {
+static void launch_forces_fluid_t(Ctx& c) {
   if (c.nf && c.unroll_forces == 2)
     SPHG_G_DISPATCH(c.group_forces,
                     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 2>
@@ -606,32 +609,47 @@ static void launch_forces_t(Ctx& c) {
                     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 1>
                                                      <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
+  c.launches++;
+}
+
+template <bool kTvf>
+static void launch_forces_rigid_t(Ctx& c) {
   if (c.nrigid)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGOther, M, kTvf, kSingleEta><<<blocks_for<kGOther>(c.nrigid), kBlock, 0, c.stream>>>(
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGOther, M, kTvf, true><<<blocks_for<kGOther>(c.nrigid), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.dflags)));
-  c.launches += 2;
+  c.launches++;
+}
+
+void launch_forces_fluid(Ctx& c) {
+  if (c.n == 0) return;
+  const bool tvf = c.P.tvf != 0, single = c.P.single_eta != 0;
+  if (tvf && single) launch_forces_fluid_t<true, true>(c);
+  else if (tvf) launch_forces_fluid_t<true, false>(c);
+  else if (single) launch_forces_fluid_t<false, true>(c);
+  else launch_forces_fluid_t<false, false>(c);
+}
+
+void launch_forces_rigid(Ctx& c) {
+  if (c.n == 0) return;
+  if (c.P.tvf) launch_forces_rigid_t<true>(c);
+  else launch_forces_rigid_t<false>(c);
 }
 
 void launch_forces(Ctx& c) {
-  if (c.n == 0) return;
-  const bool tvf = c.P.tvf != 0, single = c.P.single_eta != 0;
-  if (tvf && single) launch_forces_t<true, true>(c);
-  else if (tvf) launch_forces_t<true, false>(c);
-  else if (single) launch_forces_t<false, true>(c);
-  else launch_forces_t<false, false>(c);
+  launch_forces_fluid(c);
+  launch_forces_rigid(c);
 }
 
-void count_pairs(Ctx& c, int64_t* candidates, int64_t* interacting) {
-  if (!c.dcount) SPHG_CUDA_CHECK(cudaMalloc(&c.dcount, 2 * sizeof(unsigned long long)));
-  SPHG_CUDA_CHECK(cudaMemsetAsync(c.dcount, 0, 2 * sizeof(unsigned long long), c.stream));
-  constexpr int G = 16;
+void count_pairs(Ctx& c, int64_t out[4]) {
+  if (!c.dcount) SPHG_CUDA_CHECK(cudaMalloc(&c.dcount, 4 * sizeof(unsigned long long)));
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.dcount, 0, 4 * sizeof(unsigned long long), c.stream));
+  constexpr int G = 4;
   SPHG_IMG_DISPATCH(c.P.img_mode, (k_count_pairs<G, M><<<blocks_for<G>(c.n), kBlock, 0, c.stream>>>(
                                        c.P, c.cur, c.nl(), c.n, c.dcount)));
-  unsigned long long h[2];
+  unsigned long long h[4];
   SPHG_CUDA_CHECK(cudaMemcpyAsync(h, c.dcount, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
   SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-  *candidates = (int64_t)h[0];
-  *interacting = (int64_t)h[1];
+  for (int k = 0; k < 4; ++k) out[k] = (int64_t)h[k];
 }
 
 }  // namespace sphg

@@ -172,10 +172,10 @@ class Simulation:
         self._check(self._fn("set_timing")(self._h, int(bool(enabled))), "set_timing")
 
     def count_pairs(self):
-        """(Verlet candidates, pairs within r_c) of the current list."""
-        a, b = C.c_int64(), C.c_int64()
-        self._check(self._fn("count_pairs")(self._h, C.byref(a), C.byref(b)), "count_pairs")
-        return a.value, b.value
+        """(candidates, interacting, interacting with fluid i, interacting with non-fluid i)."""
+        out = (C.c_int64 * 4)()
+        self._check(self._fn("count_pairs")(self._h, out), "count_pairs")
+        return tuple(out)
 
     def compute_dt(self):
         """compute_dt terms: cfl, viscous, body force, contact, conduction."""

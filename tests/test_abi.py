@@ -81,3 +81,13 @@ def test_create_rejects_invalid_config_without_touching_the_device():
     with pytest.raises(SPHError) as e:
         Simulation(p)
     assert e.value.code == 2 and "dx must be positive" in str(e.value)
+
+
+def test_cpp_dropin_header_compiles():
+    """include/sphfsi_gpu/device_simulation.hpp over the reference's ParticleStore<3> (needs the headers)."""
+    ref = "/root/reference/proj/include"
+    if not os.path.isdir(ref):
+        pytest.skip("reference headers not present (GPU box uses the prebuilt binary)")
+    r = subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "cpp"), "-s"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert os.path.exists(os.path.join(ROOT, "tests", "cpp", "_build", "test_dropin"))

@@ -179,3 +179,13 @@ def test_warm_upload_roundtrip(Oracle):
     orc.initialize()
     orc.step(3)
     compare_state(sim, orc, sc.params, tol=1e-7, what="warm upload")
+
+
+def test_cpp_dropin_on_device():
+    """The C++ adapter over sphfsi::ParticleStore<3> (tests/cpp/test_dropin.cpp) runs the GPU path."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "_build", "test_dropin")
+    assert os.path.exists(exe), "build() compiles tests/cpp/test_dropin"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
