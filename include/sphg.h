@@ -105,6 +105,7 @@ typedef struct {
   double *wall_velocity;
   uint8_t *dirichlet_T;
   double *force;
+  uint32_t *owner;   /* owning rank (store.hpp:46); != params.rank marks a ghost copy; NULL = all owned */
 } sphg_soa;
 
 /* RigidBody.  inertia = world frame about com: xx yy zz xy xz yz. */
@@ -193,6 +194,26 @@ int sphg_dt_limits(const sphg_params* params, double u_max, double m_r, double l
 /* Pair counts of the current Verlet list: [0] candidates, [1] within r_c (interacting),
  * [2] interacting with a fluid particle i (the fluid force kernel's pairs), [3] with a non-fluid i. */
 int sphg_count_pairs(sphg_ctx* ctx, int64_t counts[4]);
+/* ---- domain decomposition primitives (one context per rank).
+ * The host layer (paper_2103_07925_b200/parallel.py) owns the exchange; these move data between the
+ * context and contiguous halo records.  Ghosts are the uploaded particles with owner != rank: they are
+ * read by the pair kernels, never integrated, and refreshed by halo unpacks.  Index lists are local ids
+ * (positions in the uploaded store); buffers are device pointers for sphg_ (host pointers for orc_). */
+#define SPHG_MAX_HALO_SLOTS 64
+enum { SPHG_HALO_STATE = 0,    /* after the drift: pos, u_int, du, vel, T           (13 doubles) */
+       SPHG_HALO_DENSITY = 1,  /* after density: V^2, rho, p, V_heat                (4 doubles)  */
+       SPHG_HALO_WALL = 2 };   /* after extrapolation: V_w^2, u~_w, rho_w, p_w      (6 doubles)  */
+int sphg_halo_doubles(int phase);
+int sphg_halo_set(sphg_ctx* ctx, int slot, const uint32_t* local_ids, size_t n);
+int sphg_halo_pack(sphg_ctx* ctx, int phase, int slot, double* buf);
+int sphg_halo_unpack(sphg_ctx* ctx, int phase, int slot, const double* buf);
+/* Per-body compensated partial sums over owned rigid particles: nb x 24 doubles (12 x (sum, comp):
+ * f xyz, torque xyz, inertia xx yy zz xy xz yz), written to host memory. */
+int sphg_body_partials(sphg_ctx* ctx, double* out);
+/* Global per-body sums (nb x 12, merged by the caller in rank order) -> f, tau, I, a_k, alpha_k. */
+int sphg_body_apply_totals(sphg_ctx* ctx, const double* totals);
+/* Max displacement since the last rebuild over owned particles (after a KICK_DRIFT stage). */
+int sphg_max_displacement(sphg_ctx* ctx, double* out);
 const char* sphg_last_error(const sphg_ctx* ctx);
 void sphg_destroy(sphg_ctx* ctx);
 /* Messages of validate_config for `params` joined by '\n' (empty = valid). */

@@ -66,6 +66,7 @@ struct Ctx {
     std::vector<sphg_body> bodies;
     std::vector<std::vector<uint32_t>> members; // rigid particles of each body, gid order
     std::vector<std::vector<uint32_t>> nl;      // Verlet candidates, gid-sorted
+    std::vector<std::vector<uint32_t>> halo;    // halo index lists (local ids) per slot
     std::vector<int64_t> cell_of;
     std::vector<uint32_t> sorted;
     // tolerance scales (sum of |pair contributions|)
@@ -81,6 +82,8 @@ struct Ctx {
     std::string err;
     int threads = 0;
 };
+
+inline bool ghost(const Ctx& c, size_t i) { return c.S.owner[i] != (uint32_t)c.P.rank; }
 
 inline double mi(const Ctx& c, double d, int a) {  // minimum image [P2]
     if (c.P.periodic[a]) {
@@ -222,6 +225,7 @@ bool stage_rebuild(Ctx& c) {
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t ii = 0; ii < (int64_t)n; ++ii) {
         const size_t i = (size_t)ii;
+        if (ghost(c, i)) continue;  // ghosts are read, never evaluated here
         const int64_t cid = c.cell_of[i];
         const int64_t cz = cid % c.ncell[2], cy = (cid / c.ncell[2]) % c.ncell[1], cx = cid / ((int64_t)c.ncell[2] * c.ncell[1]);
         auto& out = c.nl[i];
@@ -263,7 +267,7 @@ bool stage_density(Ctx& c) {
     const int64_t n = (int64_t)c.S.size();
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
-        if (c.S.kind[i] != Kind::Fluid) continue;
+        if (c.S.kind[i] != Kind::Fluid || ghost(c, (size_t)i)) continue;
         double s = K.w(0.0);  // self term first
         for (uint32_t j : c.nl[i]) {
             const V3 d = mi3(c, c.S.pos[i], c.S.pos[j]);
@@ -305,7 +309,7 @@ bool stage_heat(Ctx& c) {
 #pragma omp parallel for schedule(static)
     for (int64_t ii = 0; ii < (int64_t)n; ++ii) {
         const size_t a = (size_t)ii;
-        if (c.S.kind[a] == Kind::Boundary) continue;
+        if (c.S.kind[a] == Kind::Boundary || ghost(c, a)) continue;
         const sphfsi::Material& ma = c.mats[c.S.material[a]];
         double s = 0.0, sc = 0.0;
         for (uint32_t b : c.nl[a]) {
@@ -360,7 +364,7 @@ bool stage_extrapolate(Ctx& c) {
     const int64_t n = (int64_t)c.S.size();
 #pragma omp parallel for schedule(static)
     for (int64_t w = 0; w < n; ++w) {
-        if (c.S.kind[w] == Kind::Fluid) continue;
+        if (c.S.kind[w] == Kind::Fluid || ghost(c, (size_t)w)) continue;
         V3 uw = V3::zero(), aw = V3::zero();
         if (c.S.kind[w] == Kind::Rigid) {
             const sphg_body& b = c.bodies[c.S.group[w]];
@@ -466,6 +470,7 @@ bool stage_forces(Ctx& c) {
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
         const Kind ki = c.S.kind[i];
+        if (ghost(c, (size_t)i)) continue;
         if (ki == Kind::Fluid) {
             const sphfsi::Material& mi_ = c.mats[c.S.material[i]];
             const Side I = side_of(c, (size_t)i, nullptr);
@@ -667,7 +672,7 @@ void mass_quantities(Ctx& c, size_t k) {
 void rebuild_members(Ctx& c) {
     c.members.assign(c.bodies.size(), {});
     for (size_t i = 0; i < c.S.size(); ++i)
-        if (c.S.kind[i] == Kind::Rigid) c.members[c.S.group[i]].push_back((uint32_t)i);
+        if (c.S.kind[i] == Kind::Rigid && !ghost(c, i)) c.members[c.S.group[i]].push_back((uint32_t)i);
 }
 
 bool stage_mass(Ctx& c) {
@@ -698,7 +703,7 @@ bool stage_kick_drift(Ctx& c) {
     double md2 = 0.0;
 #pragma omp parallel for schedule(static) reduction(max : umax, md2)
     for (int64_t i = 0; i < n; ++i) {
-        const Kind k = c.S.kind[i];
+        const Kind k = ghost(c, (size_t)i) ? Kind::Boundary : c.S.kind[i];  // ghosts move by halo only
         if (k == Kind::Fluid) {
             const V3 uh = c.S.vel[i] + hdt * c.S.acc[i];
             const V3 ua = c.P.tvf ? uh + hdt * c.S.acc_bg[i] : uh;
@@ -740,6 +745,7 @@ bool stage_final_kick(Ctx& c) {
     const int64_t n = (int64_t)c.S.size();
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
+        if (ghost(c, (size_t)i)) continue;
         if (c.S.kind[i] == Kind::Fluid) {
             c.S.vel[i] = c.S.vel[i] + hdt * c.S.acc[i];
         } else if (c.S.kind[i] == Kind::Rigid) {
@@ -1037,7 +1043,15 @@ int orc_upload(orc_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t nb
     copy3(S.wall_velocity, s->wall_velocity, n);
     copy1(S.dirichlet_T, s->dirichlet_T, n, (uint8_t)0xff);
     S.dirichlet_C.assign(n, 0xff);
-    S.owner.assign(n, 0);
+    if (s->owner) copy1(S.owner, s->owner, n, 0u);
+    else S.owner.assign(n, (uint32_t)c.P.rank);
+    c.halo.assign(SPHG_MAX_HALO_SLOTS, {});
+    bool any_ghost = false;
+    for (size_t i = 0; i < n; ++i) any_ghost |= ghost(c, i);
+    if (any_ghost && c.P.transitions) {
+        c.err = "phase transitions are single-rank only (ghost particles present)";
+        return SPHG_ERR_CONFIG;
+    }
     resize_aux(c);
     if (s->force) copy3(c.force, s->force, n);
     c.bodies.assign(bodies, bodies + nb);
@@ -1089,6 +1103,8 @@ int orc_download(orc_ctx* h, sphg_soa* o, sphg_body* bodies, size_t* nb) {
     out3(o->wall_velocity, S.wall_velocity);
     out1(o->dirichlet_T, S.dirichlet_T);
     out3(o->force, c.force);
+    if (o->owner)
+        for (size_t i = 0; i < S.size(); ++i) o->owner[i] = ghost(c, i) ? 0xffffffffu : (uint32_t)c.P.rank;
     if (nb) {
         if (bodies) {
             const size_t m = std::min(*nb, c.bodies.size());
@@ -1156,6 +1172,142 @@ int orc_stats(orc_ctx* h, sphg_stats_t* s) {
     s->time = c.t;
     s->max_displacement = c.max_disp;
     s->u_max = c.u_max;
+    return SPHG_OK;
+}
+
+// ---------------- decomposition primitives (sphg.h): oracle records, host buffers
+int orc_halo_doubles(int phase) {
+    return phase == SPHG_HALO_STATE ? 13 : phase == SPHG_HALO_DENSITY ? 4 : phase == SPHG_HALO_WALL ? 6 : -1;
+}
+
+int orc_halo_set(orc_ctx* h, int slot, const uint32_t* ids, size_t n) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (slot < 0 || slot >= SPHG_MAX_HALO_SLOTS) return SPHG_ERR_CONFIG;
+    for (size_t k = 0; k < n; ++k)
+        if (ids[k] >= c.S.size()) return SPHG_ERR_CONFIG;
+    c.halo[slot].assign(ids, ids + n);
+    return SPHG_OK;
+}
+
+int orc_halo_pack(orc_ctx* h, int phase, int slot, double* buf) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    const auto& ids = c.halo[slot];
+    const int d = orc_halo_doubles(phase);
+    if (d < 0) return SPHG_ERR_CONFIG;
+    for (size_t s = 0; s < ids.size(); ++s) {
+        const size_t i = ids[s];
+        double* o = buf + s * d;
+        if (phase == SPHG_HALO_STATE) {
+            put3(o, c.S.pos[i]);
+            put3(o + 3, c.S.vel[i]);
+            put3(o + 6, c.S.vel_adv[i]);
+            put3(o + 9, c.S.wall_velocity[i]);
+            o[12] = c.S.temperature[i];
+        } else if (phase == SPHG_HALO_DENSITY) {
+            o[0] = c.S.density[i];
+            o[1] = c.S.pressure[i];
+            o[2] = o[3] = 0.0;
+        } else {
+            o[0] = c.V_w[i];
+            put3(o + 1, c.S.wall_velocity[i]);
+            o[4] = c.rho_w[i];
+            o[5] = c.S.wall_pressure[i];
+        }
+    }
+    return SPHG_OK;
+}
+
+int orc_halo_unpack(orc_ctx* h, int phase, int slot, const double* buf) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    const auto& ids = c.halo[slot];
+    const int d = orc_halo_doubles(phase);
+    if (d < 0) return SPHG_ERR_CONFIG;
+    for (size_t s = 0; s < ids.size(); ++s) {
+        const size_t i = ids[s];
+        const double* o = buf + s * d;
+        if (phase == SPHG_HALO_STATE) {
+            c.S.pos[i] = v3(o);
+            c.S.vel[i] = v3(o + 3);
+            c.S.vel_adv[i] = v3(o + 6);
+            c.S.wall_velocity[i] = v3(o + 9);
+            c.S.temperature[i] = o[12];
+        } else if (phase == SPHG_HALO_DENSITY) {
+            c.S.density[i] = o[0];
+            c.S.pressure[i] = o[1];
+        } else {
+            c.V_w[i] = o[0];
+            c.S.wall_velocity[i] = v3(o + 1);
+            c.rho_w[i] = o[4];
+            c.S.wall_pressure[i] = o[5];
+            if (c.S.kind[i] == Kind::Boundary) c.S.density[i] = o[4];
+        }
+    }
+    return SPHG_OK;
+}
+
+// per-body Neumaier partials over owned members, in local gid order: nb x 12 x (sum, comp)
+int orc_body_partials(orc_ctx* h, double* out) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    const size_t nb = c.bodies.size();
+    if (c.members.size() != nb) rebuild_members(c);
+    for (size_t k = 0; k < nb; ++k) {
+        const sphg_body& b = c.bodies[k];
+        sphfsi::KahanSum acc[12];
+        if (b.alive) {
+            const sphfsi::Quaternion q = qof(b);
+            for (uint32_t r : c.members[k]) {
+                const V3 rk = sphfsi::rotate(q, c.S.body_frame_pos[r]);
+                const V3& f = c.force[r];
+                const V3 tq = sphfsi::moment(rk, f);
+                const double m = c.S.mass[r];
+                const double Ir = particle_inertia(m, c.P.dx);
+                const double d2 = r2of(rk);
+                for (int a = 0; a < 3; ++a) {
+                    acc[a].add(f[a]);
+                    acc[3 + a].add(tq[a]);
+                }
+                acc[6].add(Ir + m * (d2 - rk[0] * rk[0]));
+                acc[7].add(Ir + m * (d2 - rk[1] * rk[1]));
+                acc[8].add(Ir + m * (d2 - rk[2] * rk[2]));
+                acc[9].add(-m * rk[0] * rk[1]);
+                acc[10].add(-m * rk[0] * rk[2]);
+                acc[11].add(-m * rk[1] * rk[2]);
+            }
+        }
+        for (int q6 = 0; q6 < 12; ++q6) {
+            out[k * 24 + 2 * q6] = acc[q6].sum;
+            out[k * 24 + 2 * q6 + 1] = acc[q6].comp;
+        }
+    }
+    return SPHG_OK;
+}
+
+int orc_body_apply_totals(orc_ctx* h, const double* tot) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    for (size_t k = 0; k < c.bodies.size(); ++k) {
+        sphg_body& b = c.bodies[k];
+        if (!b.alive) continue;
+        const double* v = tot + k * 12;
+        const V3 f{v[0], v[1], v[2]}, t{v[3], v[4], v[5]};
+        put3(b.force, f);
+        put3(b.torque, t);
+        for (int q6 = 0; q6 < 6; ++q6) b.inertia[q6] = v[6 + q6];
+        if (b.mobile && b.mass > 0.0) {
+            put3(b.acc, f / b.mass + v3(c.P.mat[b.material].body_force));
+            V3 al;
+            bool sing;
+            inverse_apply(b.inertia, t, al, sing);
+            put3(b.alpha, al);
+        } else {
+            put3(b.acc, V3::zero());
+            put3(b.alpha, V3::zero());
+        }
+    }
+    return SPHG_OK;
+}
+
+int orc_max_displacement(orc_ctx* h, double* out) {
+    *out = reinterpret_cast<Ctx*>(h)->max_disp;
     return SPHG_OK;
 }
 

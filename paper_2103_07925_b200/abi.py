@@ -26,6 +26,9 @@ STAGE_FINAL_KICK = 7
 STAGE_TRANSITIONS = 8
 STAGE_MASS = 9
 
+HALO_STATE, HALO_DENSITY, HALO_WALL = 0, 1, 2
+MAX_HALO_SLOTS = 64
+
 STAGE_NAMES = ["rebuild", "density", "heat", "extrapolate", "forces", "bodies",
                "kick_drift", "final_kick", "transitions", "mass", "forces_fluid", "forces_rigid",
                "", "", "", ""]
@@ -72,7 +75,8 @@ class SoA(C.Structure):
                 ("kind", C.POINTER(C.c_uint8)), ("group", C.POINTER(C.c_uint32)),
                 ("material", C.POINTER(C.c_uint16)),
                 ("body_frame_pos", _dp), ("wall_pressure", _dp), ("wall_velocity", _dp),
-                ("dirichlet_T", C.POINTER(C.c_uint8)), ("force", _dp)]
+                ("dirichlet_T", C.POINTER(C.c_uint8)), ("force", _dp),
+                ("owner", C.POINTER(C.c_uint32))]
 
 
 class Body(C.Structure):
@@ -118,6 +122,13 @@ def declare(lib, prefix):
         "compute_dt": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "dt_limits": (C.c_int, [C.POINTER(Params), C.c_double, C.c_double, C.POINTER(C.c_double)]),
         "count_pairs": (C.c_int, [vp, C.POINTER(C.c_int64)]),
+        "halo_set": (C.c_int, [vp, C.c_int, C.POINTER(C.c_uint32), C.c_size_t]),
+        "halo_pack": (C.c_int, [vp, C.c_int, C.c_int, C.c_void_p]),
+        "halo_unpack": (C.c_int, [vp, C.c_int, C.c_int, C.c_void_p]),
+        "body_partials": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "body_apply_totals": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "max_displacement": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "halo_doubles": (C.c_int, [C.c_int]),
     }
     for name, (res, args) in list(sig.items()) + list(optional.items()):
         fn = getattr(lib, prefix + name, None)

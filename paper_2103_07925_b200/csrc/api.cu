@@ -301,6 +301,9 @@ int do_stage(sphg_ctx* h, int stage) {
 
 int one_step(sphg_ctx* h) {
   Ctx& c = h->c;
+  if (c.nghost)
+    return fail(h, SPHG_ERR_RUNTIME,
+                "ghost particles present: drive multi-rank steps through the decomposition layer (parallel.py)");
   reset_step_flags(c);
   timed(c, SPHG_STAGE_KICK_DRIFT, kick_all);
   c.t += c.P.dt;
@@ -412,7 +415,8 @@ void stage_upload(Ctx& c, const sphg_soa* s, Particles& dst) {
       S.H2[q] = make_double2(s1(s->temperature, i), Vh);
       S.dT[q] = s1(s->dT_dt, i);
       S.ps[q] = p;
-      S.kmd[q] = make_kmd(kind, mat, dir);
+      const bool ghost = s->owner && s->owner[i] != (uint32_t)c.params.rank;
+      S.kmd[q] = make_kmd(kind, mat, dir) | (ghost ? kGhostBit : 0u);
       S.grp[q] = s->group ? s->group[i] : 0;
     }
     cudaStream_t st = c.stream;
@@ -472,6 +476,7 @@ void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
       if (o->group) o->group[g] = S.grp[q];
       if (o->material) o->material[g] = (uint16_t)mat;
       if (o->dirichlet_T) o->dirichlet_T[g] = (uint8_t)dir_of(kmd);
+      if (o->owner) o->owner[g] = is_ghost(kmd) ? 0xffffffffu : (uint32_t)c.params.rank;
     }
   };
   for (size_t k0 = 0; k0 < n; k0 += kChunk, slot ^= 1) {
@@ -555,6 +560,12 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
       if (kind == SPHG_RIGID && (s->group ? s->group[i] : 0) >= nb)
         return fail(h, SPHG_ERR_CONFIG, "rigid particle " + std::to_string(i) + " refers to a missing body");
     }
+    size_t ng = 0;
+    if (s->owner)
+      for (size_t i = 0; i < n; ++i) ng += s->owner[i] != (uint32_t)c.params.rank ? 1 : 0;
+    if (ng && c.params.transitions)
+      return fail(h, SPHG_ERR_CONFIG, "phase transitions are single-rank only (ghost particles present)");
+    c.nghost = ng;
     // warm upload: same store size and a valid Verlet list -> keep the device order and the list,
     // scatter the host (gid-ordered) data through the gid permutation
     const bool warm = c.built && c.have_state && n == c.n && n > 0;
@@ -586,6 +597,7 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
       if (displacement_exceeds(c)) c.built = false;
     } else {
       iota_gid(c);
+      build_idx_of_gid(c);
       SPHG_CUDA_CHECK(cudaMemcpyAsync(c.cur.R4.p, c.cur.G0.p, n * sizeof(double4), cudaMemcpyDeviceToDevice, c.stream));
       c.built = false;
     }
@@ -810,6 +822,80 @@ int sphg_count_pairs(sphg_ctx* h, int64_t out[4]) {
   });
 }
 
+int sphg_halo_doubles(int phase) {
+  return phase == SPHG_HALO_STATE ? 13 : phase == SPHG_HALO_DENSITY ? 4 : phase == SPHG_HALO_WALL ? 6 : -1;
+}
+
+int sphg_halo_set(sphg_ctx* h, int slot, const uint32_t* ids, size_t n) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (slot < 0 || slot >= SPHG_MAX_HALO_SLOTS) return fail(h, SPHG_ERR_CONFIG, "halo slot out of range");
+    for (size_t k = 0; k < n; ++k)
+      if (ids[k] >= c.n) return fail(h, SPHG_ERR_CONFIG, "halo index out of range");
+    c.halo_ids[slot].alloc(std::max<size_t>(n, 1));
+    h2d(c.halo_ids[slot].p, ids, n, c.stream);
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    c.halo_n[slot] = n;
+    return SPHG_OK;
+  });
+}
+
+int sphg_halo_pack(sphg_ctx* h, int phase, int slot, double* buf) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (slot < 0 || slot >= SPHG_MAX_HALO_SLOTS || sphg_halo_doubles(phase) < 0)
+      return fail(h, SPHG_ERR_CONFIG, "bad halo slot/phase");
+    halo_pack(c, phase, slot, buf);
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    return SPHG_OK;
+  });
+}
+
+int sphg_halo_unpack(sphg_ctx* h, int phase, int slot, const double* buf) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (slot < 0 || slot >= SPHG_MAX_HALO_SLOTS || sphg_halo_doubles(phase) < 0)
+      return fail(h, SPHG_ERR_CONFIG, "bad halo slot/phase");
+    halo_unpack(c, phase, slot, buf);
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    return SPHG_OK;
+  });
+}
+
+int sphg_body_partials(sphg_ctx* h, double* out) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (c.nb == 0) return SPHG_OK;
+    if (!c.built) {
+      const int rc = do_stage(h, SPHG_STAGE_REBUILD);
+      if (rc) return rc;
+    }
+    c.body_buf.alloc(c.nb * 24);
+    SPHG_CUDA_CHECK(cudaMemsetAsync(c.body_buf.p, 0, c.nb * 24 * sizeof(double), c.stream));
+    body_partials(c, c.body_buf.p);
+    d2h(out, c.body_buf.p, c.nb * 24, c.stream);
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    return SPHG_OK;
+  });
+}
+
+int sphg_body_apply_totals(sphg_ctx* h, const double* tot) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (c.nb == 0) return SPHG_OK;
+    c.body_buf.alloc(c.nb * 24);
+    h2d(c.body_buf.p, tot, c.nb * 12, c.stream);
+    body_apply_totals(c, c.body_buf.p);
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    return SPHG_OK;
+  });
+}
+
+int sphg_max_displacement(sphg_ctx* h, double* out) {
+  *out = h->c.max_disp;
+  return SPHG_OK;
+}
+
 const char* sphg_last_error(const sphg_ctx* h) { return h ? h->c.err.c_str() : "null context"; }
 
 void sphg_destroy(sphg_ctx* h) {
@@ -821,6 +907,8 @@ void sphg_destroy(sphg_ctx* h) {
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
   c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();
   c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();
+  c.fidx.free(); c.widx.free(); c.idx_of_gid.free(); c.body_buf.free();
+  for (auto& b : c.halo_ids) b.free();
   if (c.dflags) cudaFree(c.dflags);
   if (c.hflags) cudaFreeHost(c.hflags);
   if (c.hbodies) cudaFreeHost(c.hbodies);

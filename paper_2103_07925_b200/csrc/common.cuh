@@ -59,6 +59,9 @@ __host__ __device__ __forceinline__ uint32_t dir_of(uint32_t kmd) { return (kmd 
 __host__ __device__ __forceinline__ uint32_t make_kmd(uint32_t kind, uint32_t mat, uint32_t dir) {
   return (kind & 3u) | ((mat & 63u) << 2) | ((dir & 255u) << 8);
 }
+// bit 16: ghost copy of a particle owned by another rank (read-only here, refreshed by halos)
+constexpr uint32_t kGhostBit = 1u << 16;
+__host__ __device__ __forceinline__ bool is_ghost(uint32_t kmd) { return (kmd & kGhostBit) != 0u; }
 
 // ------------------------------------------------- pinned (no-FMA) helpers
 // minimum image along one axis [P2]

@@ -117,6 +117,12 @@ struct Ctx {
   unsigned long long* dcount = nullptr;  // pair counters
   cudaEvent_t step_ev[2] = {nullptr, nullptr};
   double last_step_ms = 0.0;
+  // domain decomposition: halo index lists (local ids) and gid -> device index
+  DBuf<uint32_t> idx_of_gid;
+  DBuf<uint32_t> halo_ids[SPHG_MAX_HALO_SLOTS];
+  size_t halo_n[SPHG_MAX_HALO_SLOTS] = {0};
+  size_t nghost = 0;
+  DBuf<double> body_buf;
 };
 
 // ------------------------------------------------------------ launchers
@@ -149,6 +155,11 @@ void gather_by_gid(Ctx& c);          // cur[k] <- alt[gid[k]] for every field bu
 bool displacement_exceeds(Ctx& c);   // max |r - r_ref| > half skin (syncs)
 void iota_gid(Ctx& c);
 void count_pairs(Ctx& c, int64_t out[4]);
+void build_idx_of_gid(Ctx& c);
+void halo_pack(Ctx& c, int phase, int slot, double* buf);
+void halo_unpack(Ctx& c, int phase, int slot, const double* buf);
+void body_partials(Ctx& c, double* dev_out);
+void body_apply_totals(Ctx& c, const double* dev_tot);
 
 // kernels_transition.cu
 int launch_transitions(Ctx& c);  // 0 ok, else error code

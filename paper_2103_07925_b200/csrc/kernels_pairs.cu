@@ -508,12 +508,12 @@ __global__ void __launch_bounds__(kBlock) k_count_pairs(const __grid_constant__ 
   }
 }
 
-__global__ void k_copy_boundary_T(Particles D, const uint32_t* __restrict__ list, size_t nlist,
-                                  double2* __restrict__ Hout) {
-  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= nlist) return;
-  const uint32_t i = list[g];
-  if (kind_of(D.kmd.p[i]) == SPHG_BOUNDARY) Hout[i] = D.H2.p[i];
+// particles the heat kernels do not update (walls, ghosts) keep their T in the new buffer
+__global__ void k_copy_boundary_T(Particles D, size_t n, double2* __restrict__ Hout) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t kmd = D.kmd.p[i];
+  if (kind_of(kmd) == SPHG_BOUNDARY || is_ghost(kmd)) Hout[i] = D.H2.p[i];
 }
 
 __device__ __forceinline__ double sched_value(const DevSchedule& s, double t) {  // Schedule::value_at
@@ -522,11 +522,9 @@ __device__ __forceinline__ double sched_value(const DevSchedule& s, double t) { 
   return s.value[s.n - 1];
 }
 
-__global__ void k_dirichlet(const __grid_constant__ DevParams P, Particles D, const uint32_t* __restrict__ list,
-                            size_t nlist, double t_new) {
-  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= nlist) return;
-  const uint32_t i = list[g];
+__global__ void k_dirichlet(const __grid_constant__ DevParams P, Particles D, size_t n, double t_new) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
   const uint32_t kmd = D.kmd.p[i];
   if (kind_of(kmd) != SPHG_BOUNDARY) return;
   const uint32_t gr = dir_of(kmd);
@@ -573,14 +571,14 @@ void launch_heat(Ctx& c) {
   if (c.n == 0) return;
   const double t_new = c.t + c.P.dt;
   constexpr int G = kGOther;
-  if (c.nw) k_dirichlet<<<grid_for(c.nw, 256), 256, 0, c.stream>>>(c.P, c.cur, c.widx.p, c.nw, t_new);
+  k_dirichlet<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new);
   if (c.nf)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.H2new.p, c.dflags)));
   if (c.nrigid)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.H2new.p, c.dflags)));
-  if (c.nw) k_copy_boundary_T<<<grid_for(c.nw, 256), 256, 0, c.stream>>>(c.cur, c.widx.p, c.nw, c.H2new.p);
+  k_copy_boundary_T<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.cur, c.n, c.H2new.p);
   std::swap(c.cur.H2, c.H2new);
   c.launches += 4;
 }

@@ -94,6 +94,10 @@ __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ Dev
   const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= n) return;  // warp-uniform
+  if (is_ghost(kmd[i])) {  // ghosts keep no row: they are read, never evaluated here
+    if (lane == 0) cnt[i] = 0;
+    return;
+  }
   const double4 pi = G0[i];
   const bool bi = kind_of(kmd[i]) == SPHG_BOUNDARY;
   const int64_t c = cell_key[i];
@@ -156,14 +160,14 @@ __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ Dev
 // ------------------------------------------------------- rigid index
 __global__ void k_rigid_flags(const uint32_t* __restrict__ kmd, size_t n, uint32_t* __restrict__ flag) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) flag[k] = kind_of(kmd[k]) == SPHG_RIGID ? 1u : 0u;
+  if (k < n) flag[k] = (kind_of(kmd[k]) == SPHG_RIGID && !is_ghost(kmd[k])) ? 1u : 0u;
 }
 
 __global__ void k_rigid_compact(const uint32_t* __restrict__ kmd, const uint32_t* __restrict__ group,
                                 const uint32_t* __restrict__ gid, const uint32_t* __restrict__ pos, size_t n,
                                 int gbits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n || kind_of(kmd[k]) != SPHG_RIGID) return;
+  if (k >= n || kind_of(kmd[k]) != SPHG_RIGID || is_ghost(kmd[k])) return;
   const uint32_t s = pos[k];
   keys[s] = ((unsigned long long)group[k] << gbits) | gid[k];
   vals[s] = (uint32_t)k;
@@ -188,16 +192,17 @@ __global__ void k_kind_flags(const uint32_t* __restrict__ kmd, size_t n, uint32_
                              uint32_t* __restrict__ wf) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
+  const bool gh = is_ghost(kmd[k]);
   const bool fl = kind_of(kmd[k]) == SPHG_FLUID;
-  ff[k] = fl ? 1u : 0u;
-  wf[k] = fl ? 0u : 1u;
+  ff[k] = (fl && !gh) ? 1u : 0u;
+  wf[k] = (!fl && !gh) ? 1u : 0u;
 }
 
 __global__ void k_kind_scatter(const uint32_t* __restrict__ kmd, const uint32_t* __restrict__ fpos,
                                const uint32_t* __restrict__ wpos, size_t n, uint32_t* __restrict__ fidx,
                                uint32_t* __restrict__ widx) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
+  if (k >= n || is_ghost(kmd[k])) return;
   if (kind_of(kmd[k]) == SPHG_FLUID) fidx[fpos[k]] = (uint32_t)k;
   else widx[wpos[k]] = (uint32_t)k;
 }
@@ -222,8 +227,12 @@ static void launch_kind_lists(Ctx& c) {
   SPHG_CUDA_CHECK(cudaMemcpyAsync(&lastf, ff + n - 1, 4, cudaMemcpyDeviceToHost, s));
   k_kind_scatter<<<grid_for(n, 256), 256, 0, s>>>(c.cur.kmd.p, fpos, wpos, n, c.fidx.p, c.widx.p);
   SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+  uint32_t lastw = 0, lastwf = 0;
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&lastw, wpos + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&lastwf, wf + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
   c.nf = (size_t)lastp + lastf;
-  c.nw = n - c.nf;
+  c.nw = (size_t)lastw + lastwf;
   c.launches += 2;
 }
 
@@ -277,6 +286,7 @@ void launch_rebuild(Ctx& c) {
   // 3. reorder into the alternate buffer set, swap
   k_reorder<<<grid_for(n, 256), 256, 0, s>>>(perm, skeys, n, c.cur, c.alt, c.cell_key.p);
   std::swap(c.cur, c.alt);
+  build_idx_of_gid(c);
   // 4. cell ranges
   SPHG_CUDA_CHECK(cudaMemsetAsync(c.cell_start.p, 0, c.ncells * sizeof(uint32_t), s));
   SPHG_CUDA_CHECK(cudaMemsetAsync(c.cell_end.p, 0, c.ncells * sizeof(uint32_t), s));

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevP
   double disp2 = 0.0, u2 = 0.0;
   if (k < n) {
     const uint32_t kmd = D.kmd.p[k];
-    const uint32_t kind = kind_of(kmd);
+    const uint32_t kind = is_ghost(kmd) ? 3u : kind_of(kmd);  // ghosts are integrated by their owner
     double3 pn;
     bool moved = true;
     if (kind == SPHG_FLUID) {
@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(256) k_final_kick(const __grid_constant__ DevP
                                                      const sphg_body* __restrict__ B, size_t n) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const uint32_t kind = kind_of(D.kmd.p[k]);
+  const uint32_t kmd = D.kmd.p[k];
+  if (is_ghost(kmd)) return;
+  const uint32_t kind = kind_of(kmd);
   if (kind == SPHG_FLUID) {
     const double3 uh = ldpos(&D.G1.p[k]);
     const double4 a = D.A4.p[k];
@@ -323,7 +325,164 @@ __global__ void k_iota(uint32_t* __restrict__ a, size_t n) {
   if (k < n) a[k] = (uint32_t)k;
 }
 
+// ------------------------------------------------ decomposition primitives
+__global__ void k_idx_of_gid(const uint32_t* __restrict__ gid, size_t n, uint32_t* __restrict__ idx) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) idx[gid[k]] = (uint32_t)k;
+}
+
+// halo record layouts (sphg.h SPHG_HALO_*)
+__global__ void k_halo_pack(Particles D, int phase, const uint32_t* __restrict__ ids, size_t m,
+                            const uint32_t* __restrict__ idx, double* __restrict__ buf) {
+  const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  const uint32_t k = idx[ids[s]];
+  if (phase == SPHG_HALO_STATE) {
+    const double4 g0 = D.G0.p[k], g1 = D.G1.p[k], g2 = D.G2.p[k], v = D.V4.p[k];
+    double* o = buf + s * 13;
+    o[0] = g0.x; o[1] = g0.y; o[2] = g0.z;
+    o[3] = g1.x; o[4] = g1.y; o[5] = g1.z;
+    o[6] = g2.x; o[7] = g2.y; o[8] = g2.z;
+    o[9] = v.x; o[10] = v.y; o[11] = v.z;
+    o[12] = D.H2.p[k].x;
+  } else if (phase == SPHG_HALO_DENSITY) {
+    double* o = buf + s * 4;
+    o[0] = D.G0.p[k].w; o[1] = D.G1.p[k].w; o[2] = D.G2.p[k].w; o[3] = D.H2.p[k].y;
+  } else {
+    const double4 g1 = D.G1.p[k];
+    double* o = buf + s * 6;
+    o[0] = D.G0.p[k].w; o[1] = g1.x; o[2] = g1.y; o[3] = g1.z; o[4] = g1.w; o[5] = D.G2.p[k].w;
+  }
+}
+
+__global__ void k_halo_unpack(Particles D, int phase, const uint32_t* __restrict__ ids, size_t m,
+                              const uint32_t* __restrict__ idx, const double* __restrict__ buf) {
+  const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  const uint32_t k = idx[ids[s]];
+  double* g0 = reinterpret_cast<double*>(&D.G0.p[k]);
+  double* g1 = reinterpret_cast<double*>(&D.G1.p[k]);
+  double* g2 = reinterpret_cast<double*>(&D.G2.p[k]);
+  if (phase == SPHG_HALO_STATE) {
+    const double* o = buf + s * 13;
+    g0[0] = o[0]; g0[1] = o[1]; g0[2] = o[2];
+    g1[0] = o[3]; g1[1] = o[4]; g1[2] = o[5];
+    g2[0] = o[6]; g2[1] = o[7]; g2[2] = o[8];
+    double* v = reinterpret_cast<double*>(&D.V4.p[k]);
+    v[0] = o[9]; v[1] = o[10]; v[2] = o[11];
+    reinterpret_cast<double*>(&D.H2.p[k])[0] = o[12];
+  } else if (phase == SPHG_HALO_DENSITY) {
+    const double* o = buf + s * 4;
+    g0[3] = o[0]; g1[3] = o[1]; g2[3] = o[2];
+    reinterpret_cast<double*>(&D.H2.p[k])[1] = o[3];
+  } else {
+    const double* o = buf + s * 6;
+    g0[3] = o[0]; g1[0] = o[1]; g1[1] = o[2]; g1[2] = o[3]; g1[3] = o[4]; g2[3] = o[5];
+  }
+}
+
+// per-body compensated partials over owned members: out[k*24 + 2c] = sum, +1 = compensation
+__global__ void __launch_bounds__(128) k_body_partials(const __grid_constant__ DevParams P, Particles D,
+                                                        const sphg_body* __restrict__ B, size_t nb,
+                                                        const uint32_t* __restrict__ ridx,
+                                                        const uint32_t* __restrict__ bstart,
+                                                        const uint32_t* __restrict__ bend, double* __restrict__ out) {
+  const size_t k = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= nb) return;
+  const sphg_body& b = B[k];
+  const Quat q = body_q(b);
+  KSum acc[12];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) acc[c] = {0.0, 0.0};
+  if (b.alive) {
+    const uint32_t s0 = bstart[k], s1 = bend[k];
+    for (uint32_t s = s0 + lane; s < s1; s += 32) {
+      const uint32_t r = ridx[s];
+      const double3 rk = qrotate(q, ld3(D.X4.p[r]));
+      const double4 f4 = D.F4.p[r];
+      const double m = D.V4.p[r].w;
+      const double3 t = make_double3(rk.y * f4.z - rk.z * f4.y, rk.z * f4.x - rk.x * f4.z, rk.x * f4.y - rk.y * f4.x);
+      const double Ir = P.Ir_over_m * m;
+      const double d2 = (rk.x * rk.x + rk.y * rk.y) + rk.z * rk.z;
+      acc[0].add(f4.x); acc[1].add(f4.y); acc[2].add(f4.z);
+      acc[3].add(t.x); acc[4].add(t.y); acc[5].add(t.z);
+      acc[6].add(Ir + m * (d2 - rk.x * rk.x));
+      acc[7].add(Ir + m * (d2 - rk.y * rk.y));
+      acc[8].add(Ir + m * (d2 - rk.z * rk.z));
+      acc[9].add(-m * rk.x * rk.y);
+      acc[10].add(-m * rk.x * rk.z);
+      acc[11].add(-m * rk.y * rk.z);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    const KSum v = warp_merge(acc[c]);
+    if (lane == 0) {
+      out[k * 24 + 2 * c] = v.s;
+      out[k * 24 + 2 * c + 1] = v.c;
+    }
+  }
+}
+
+__global__ void k_apply_totals(const __grid_constant__ DevParams P, sphg_body* __restrict__ B, size_t nb,
+                               const double* __restrict__ tot) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb) return;
+  sphg_body& b = B[k];
+  if (!b.alive) return;
+  const double* v = tot + k * 12;
+  for (int a = 0; a < 3; ++a) {
+    b.force[a] = v[a];
+    b.torque[a] = v[3 + a];
+  }
+  for (int a = 0; a < 6; ++a) b.inertia[a] = v[6 + a];
+  if (b.mobile && b.mass > 0.0) {
+    const DevMat& M = P.mat[b.material];
+    for (int a = 0; a < 3; ++a) b.acc[a] = v[a] / b.mass + M.g[a];
+    double3 al;
+    inverse_apply(b.inertia, make_double3(v[3], v[4], v[5]), al);
+    b.alpha[0] = al.x; b.alpha[1] = al.y; b.alpha[2] = al.z;
+  } else {
+    for (int a = 0; a < 3; ++a) b.acc[a] = b.alpha[a] = 0.0;
+  }
+}
+
 }  // namespace
+
+void build_idx_of_gid(Ctx& c) {
+  if (c.n == 0) return;
+  c.idx_of_gid.alloc(c.n);
+  k_idx_of_gid<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.cur.gid.p, c.n, c.idx_of_gid.p);
+  c.launches++;
+}
+
+void halo_pack(Ctx& c, int phase, int slot, double* buf) {
+  const size_t m = c.halo_n[slot];
+  if (m == 0) return;
+  k_halo_pack<<<grid_for(m, 256), 256, 0, c.stream>>>(c.cur, phase, c.halo_ids[slot].p, m, c.idx_of_gid.p, buf);
+  c.launches++;
+}
+
+void halo_unpack(Ctx& c, int phase, int slot, const double* buf) {
+  const size_t m = c.halo_n[slot];
+  if (m == 0) return;
+  k_halo_unpack<<<grid_for(m, 256), 256, 0, c.stream>>>(c.cur, phase, c.halo_ids[slot].p, m, c.idx_of_gid.p, buf);
+  c.launches++;
+}
+
+void body_partials(Ctx& c, double* dev_out) {
+  if (c.nb == 0) return;
+  k_body_partials<<<grid_for(c.nb * 32, 128), 128, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.nb, c.ridx.p,
+                                                                   c.body_start.p, c.body_start.p + c.nb, dev_out);
+  c.launches++;
+}
+
+void body_apply_totals(Ctx& c, const double* dev_tot) {
+  if (c.nb == 0) return;
+  k_apply_totals<<<grid_for(c.nb, 128), 128, 0, c.stream>>>(c.P, c.bodies.p, c.nb, dev_tot);
+  c.launches++;
+}
 
 void gather_by_gid(Ctx& c) {
   if (c.n == 0) return;

@@ -54,7 +54,7 @@ __global__ void k_melt(const __grid_constant__ DevParams P, Particles D, size_t 
   const int tgt = P.mat[mat_of(kmd)].melt;
   const double m = D.V4.p[k].w;
   const double rho0 = P.mat[tgt].rho0;
-  D.kmd.p[k] = make_kmd(SPHG_FLUID, (uint32_t)tgt, dir_of(kmd));
+  D.kmd.p[k] = (kmd & kGhostBit) | make_kmd(SPHG_FLUID, (uint32_t)tgt, dir_of(kmd));
   D.group.p[k] = 0;
   D.V4.p[k] = make_double4(u.x, u.y, u.z, m);
   const double V = m / rho0;
@@ -144,7 +144,7 @@ __global__ void k_solid_apply(const __grid_constant__ DevParams P, Particles D, 
   }
   bmask[body] = 1;
   const double rho0 = P.mat[tgt].rho0;
-  D.kmd.p[i] = make_kmd(SPHG_RIGID, (uint32_t)tgt, dir_of(kmd));
+  D.kmd.p[i] = (kmd & kGhostBit) | make_kmd(SPHG_RIGID, (uint32_t)tgt, dir_of(kmd));
   D.group.p[i] = body;
   D.A4.p[i] = make_double4(0, 0, 0, 0);
   D.B4.p[i] = make_double4(0, 0, 0, 0);

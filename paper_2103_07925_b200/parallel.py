@@ -1,0 +1,329 @@
+"""Spatial domain decomposition over ranks (one process per GPU) — the paper's
+parallel concept with torch.distributed plumbing.
+
+Ownership and ghosts
+  The domain is split into px*py*pz equal boxes (2 -> 2x1x1, 4 -> 2x2x1, 8 -> 2x2x2,
+  longest axes first).  A rank owns the particles whose position lies in its box
+  (`owner`, store.hpp:46) and holds read-only ghost copies of every particle within
+  an L-infinity distance w = r_c + 0.1h + margin of the box (periodic images
+  included).  The margin keeps Verlet rebuilds rank-local: particles are
+  re-partitioned only when the accumulated displacement bound exceeds margin/2.
+
+Per step (bulk-synchronous; the same stage sequence as sphg_step):
+  KICK_DRIFT -> allreduce(max displacement) -> halo STATE -> [REBUILD on all ranks]
+  -> DENSITY -> halo DENSITY -> [HEAT] -> EXTRAPOLATE -> halo WALL -> FORCES
+  -> body partials: all_gather + merge in rank order (compensated, identical on
+     every rank; PAPER:303-373 host->owner->host collapsed into a replicated reduce)
+  -> FINAL_KICK.
+Halo records are packed/unpacked by the engine (device kernels for the GPU
+engine, host loops for the oracle) into tensors exchanged with point-to-point
+send/recv (NCCL on GPUs, gloo in the CPU tests).  Phase transitions are
+single-rank only (the engine refuses ghosts with transitions enabled).
+"""
+import ctypes as C
+import math
+import os
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import abi
+from .store import ParticleStore, VEC_FIELDS, SCALAR_FIELDS, TAG_FIELDS, BODY_DTYPE
+
+
+def factor_dims(nranks, extent):
+    """Rank grid: repeatedly halve the currently longest per-rank extent (powers of 2),
+    falling back to a 1D split along the longest axis otherwise."""
+    dims = [1, 1, 1]
+    n = nranks
+    ext = list(extent)
+    while n > 1 and n % 2 == 0:
+        a = int(np.argmax([ext[k] / dims[k] for k in range(3)]))
+        dims[a] *= 2
+        n //= 2
+    if n > 1:
+        a = int(np.argmax(ext))
+        dims[a] *= n
+    return dims
+
+
+class Grid:
+    def __init__(self, params, nranks):
+        self.lo = np.array([params.lo[a] for a in range(3)])
+        self.hi = np.array([params.hi[a] for a in range(3)])
+        self.L = self.hi - self.lo
+        self.periodic = np.array([bool(params.periodic[a]) for a in range(3)])
+        self.dims = factor_dims(nranks, self.L)
+        self.nranks = nranks
+
+    def coords(self, r):
+        return np.array([r // (self.dims[1] * self.dims[2]), (r // self.dims[2]) % self.dims[1], r % self.dims[2]])
+
+    def box(self, r):
+        c = self.coords(r)
+        w = self.L / np.array(self.dims)
+        lo = self.lo + c * w
+        hi = self.lo + (c + 1) * w
+        return lo, hi
+
+    def owner_of(self, pos):
+        w = self.L / np.array(self.dims)
+        c = np.floor((pos - self.lo) / w).astype(np.int64)
+        for a in range(3):
+            c[:, a] = np.clip(c[:, a], 0, self.dims[a] - 1)
+        return (c[:, 0] * self.dims[1] + c[:, 1]) * self.dims[2] + c[:, 2]
+
+    def near_box(self, pos, r, width):
+        """Particles within L-infinity distance `width` of rank r's box (periodic images)."""
+        lo, hi = self.box(r)
+        ok = np.ones(len(pos), bool)
+        for a in range(3):
+            x = pos[:, a]
+            inside = (x >= lo[a] - width) & (x <= hi[a] + width)
+            if self.periodic[a]:
+                inside |= (x + self.L[a] >= lo[a] - width) & (x + self.L[a] <= hi[a] + width)
+                inside |= (x - self.L[a] >= lo[a] - width) & (x - self.L[a] <= hi[a] + width)
+            ok &= inside
+        return ok
+
+
+def _merge_partials(parts):
+    """Merge per-rank (sum, comp) partials in rank order with TwoSum (numpy: IEEE, no FMA)."""
+    s = parts[0][..., 0].copy()
+    c = parts[0][..., 1].copy()
+    for p in parts[1:]:
+        s2, c2 = p[..., 0], p[..., 1]
+        t = s + s2
+        bp = t - s
+        e = (s - (t - bp)) + (s2 - bp)
+        c = (c + c2) + e
+        s = t
+    return s + c
+
+
+class DistributedSimulation:
+    """One rank of a decomposed run.  `make_engine(params)` returns a Simulation
+    (GPU) or the oracle's engine (CPU tests); `tensor_device` is where halo
+    buffers live (the engine's device)."""
+
+    def __init__(self, params, make_engine, tensor_device="cpu", margin_h=2.0, group=None, engine_device=None):
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.params = params
+        self.params.rank = self.rank
+        self.params.nranks = self.world
+        self.make_engine = make_engine
+        self.dev = torch.device(tensor_device)  # where the exchanged tensors live (the backend's device)
+        # where the engine packs/unpacks (its own memory: cuda for the GPU engine, cpu for the oracle)
+        self.edev = torch.device(engine_device) if engine_device is not None else self.dev
+        self.grid = Grid(params, self.world)
+        h = params.h if params.h > 0 else params.dx
+        self.h = h
+        self.rv = 3.0 * h + 0.1 * h
+        self.half_skin = 0.05 * h
+        self.margin = margin_h * h
+        self.width = self.rv + self.margin
+        self.engine = None
+        self.disp_since_partition = 0.0
+        self.repartitions = 0
+        self.rebuilds = 0
+        self.steps = 0
+        self.comm_s = 0.0
+
+    # ------------------------------------------------------------ layout
+    def distribute(self, store, bodies):
+        """Every rank holds the same global store (seeded generation is deterministic)."""
+        pos = store.pos
+        owner = self.grid.owner_of(pos)
+        self.global_n = store.n
+        r = self.rank
+        own = np.nonzero(owner == r)[0]
+        ghost = np.nonzero((owner != r) & self.grid.near_box(pos, r, self.width))[0]
+        ghost = ghost[np.lexsort((ghost, owner[ghost]))]  # by (owner rank, gid)
+        gids = np.concatenate([own, ghost])
+        self.gids = gids
+        self.n_own = len(own)
+        local = ParticleStore(len(gids))
+        for f in VEC_FIELDS + SCALAR_FIELDS + tuple(TAG_FIELDS):
+            getattr(local, f)[:] = getattr(store, f)[gids]
+        local.owner[:] = owner[gids].astype(np.uint32)
+        lid = np.full(store.n, -1, np.int64)
+        lid[gids] = np.arange(len(gids))
+        # halo lists: send = my owned particles that are ghosts on q; recv = my ghosts owned by q;
+        # both ordered by global gid, so the two sides agree without a handshake
+        self.peers = []
+        for q in range(self.world):
+            if q == r:
+                continue
+            send_g = own[self.grid.near_box(pos[own], q, self.width)]
+            recv_g = ghost[owner[ghost] == q]
+            if len(send_g) == 0 and len(recv_g) == 0:
+                continue
+            self.peers.append((q, lid[send_g].astype(np.uint32), lid[recv_g].astype(np.uint32)))
+        if self.engine is None:
+            self.engine = self.make_engine(self.params)
+        self.engine.upload(local, bodies)
+        for k, (q, s, rcv) in enumerate(self.peers):
+            self._halo_set(2 * k, s)
+            self._halo_set(2 * k + 1, rcv)
+        self.disp_since_partition = 0.0
+        self._bufs = {}
+
+    def _halo_set(self, slot, ids):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        e = self.engine
+        e._check(e._fn("halo_set")(e._h, slot, ids.ctypes.data_as(C.POINTER(C.c_uint32)), len(ids)), "halo_set")
+
+    # ------------------------------------------------------------ exchanges
+    def _halo(self, phase):
+        t0 = time.perf_counter()
+        e = self.engine
+        d = getattr(e.lib, e.prefix + "halo_doubles")(phase)
+        ops, recv = [], []
+        for k, (q, s, rcv) in enumerate(self.peers):
+            key = (phase, k)
+            if key not in self._bufs:
+                mk = lambda m, dev: torch.empty(max(m, 1) * d, dtype=torch.float64, device=dev)
+                staged = self.edev != self.dev
+                self._bufs[key] = (mk(len(s), self.edev), mk(len(rcv), self.edev),
+                                   mk(len(s), self.dev) if staged else None, mk(len(rcv), self.dev) if staged else None)
+            sb, rb, sbx, rbx = self._bufs[key]
+            if len(s):
+                e._check(e._fn("halo_pack")(e._h, phase, 2 * k, sb.data_ptr()), "halo_pack")
+                if sbx is not None:
+                    sbx.copy_(sb)
+                ops.append(dist.P2POp(dist.isend, (sb if sbx is None else sbx)[: len(s) * d], q, group=self.group))
+            if len(rcv):
+                ops.append(dist.P2POp(dist.irecv, (rb if rbx is None else rbx)[: len(rcv) * d], q, group=self.group))
+                recv.append((k, rb, rbx))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for k, rb, rbx in recv:
+            if rbx is not None:
+                rb.copy_(rbx)
+            e._check(e._fn("halo_unpack")(e._h, phase, 2 * k + 1, rb.data_ptr()), "halo_unpack")
+        self.comm_s += time.perf_counter() - t0
+
+    def _bodies(self):
+        e = self.engine
+        nb = e.num_bodies()
+        if nb == 0:
+            return
+        part = np.zeros((nb, 12, 2))
+        e._check(e._fn("body_partials")(e._h, part.ctypes.data_as(C.POINTER(C.c_double))), "body_partials")
+        t0 = time.perf_counter()
+        mine = torch.from_numpy(part).to(self.dev)
+        gathered = [torch.empty_like(mine) for _ in range(self.world)]
+        dist.all_gather(gathered, mine, group=self.group)
+        parts = [g.cpu().numpy() for g in gathered]
+        self.comm_s += time.perf_counter() - t0
+        tot = np.ascontiguousarray(_merge_partials(parts))
+        e._check(e._fn("body_apply_totals")(e._h, tot.ctypes.data_as(C.POINTER(C.c_double))), "body_apply_totals")
+
+    def _allmax(self, x):
+        t = torch.tensor([x], dtype=torch.float64, device=self.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    # ------------------------------------------------------------ stepping
+    def _evaluate(self, thermal):
+        e = self.engine
+        e.run_stage(abi.STAGE_DENSITY)
+        self._halo(abi.HALO_DENSITY)
+        if thermal:
+            e.run_stage(abi.STAGE_HEAT)
+        e.run_stage(abi.STAGE_EXTRAPOLATE)
+        self._halo(abi.HALO_WALL)
+        e.run_stage(abi.STAGE_FORCES)
+        self._bodies()
+
+    def initialize(self):
+        self.engine.run_stage(abi.STAGE_REBUILD)
+        self._evaluate(thermal=False)
+
+    def step(self, nsteps=1):
+        e = self.engine
+        thermal = bool(self.params.thermal)
+        for _ in range(nsteps):
+            e.run_stage(abi.STAGE_KICK_DRIFT)
+            d = C.c_double(0.0)
+            e._check(e._fn("max_displacement")(e._h, C.byref(d)), "max_displacement")
+            disp = self._allmax(d.value)
+            self._halo(abi.HALO_STATE)
+            if disp > self.half_skin:  # SPEC:212, all ranks together
+                self.disp_since_partition += disp
+                if self.disp_since_partition > 0.5 * self.margin:
+                    self.repartition()
+                e.run_stage(abi.STAGE_REBUILD)
+                self.rebuilds += 1
+            self._evaluate(thermal)
+            e.run_stage(abi.STAGE_FINAL_KICK)
+            self.steps += 1
+
+    # ------------------------------------------------------------ global views
+    def gather(self):
+        """Owned particles of every rank -> global store (gid order) and the replicated bodies."""
+        local, bodies = self.engine.download()
+        own = slice(0, self.n_own)
+        payload = {f: getattr(local, f)[own] for f in VEC_FIELDS + SCALAR_FIELDS + tuple(TAG_FIELDS)}
+        payload["gid"] = self.gids[: self.n_own]
+        allp = [None] * self.world
+        dist.all_gather_object(allp, payload, group=self.group)
+        g = ParticleStore(self.global_n)
+        for p in allp:
+            for f in VEC_FIELDS + SCALAR_FIELDS + tuple(TAG_FIELDS):
+                getattr(g, f)[p["gid"]] = p[f]
+        return g, bodies
+
+    def repartition(self):
+        """Re-own and re-ghost from the gathered global state (rare: margin/2 of motion)."""
+        g, bodies = self.gather()
+        g.owner[:] = 0
+        self.repartitions += 1
+        self.distribute(g, bodies)
+
+
+# ---------------------------------------------------------------- bench N>1
+def bench_multi(args):
+    """Strong scaling on the C5 config: every rank generates the seeded global store,
+    keeps its box + ghost shell, runs K steps; value = all particles x K / max rank time."""
+    import json
+    from . import scenarios
+    from .sim import Simulation
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    sc = scenarios.config5(nside=args.nside, n_spheres=args.spheres)
+    ds = DistributedSimulation(sc.params, lambda p: Simulation(p, device=local), tensor_device=f"cuda:{local}")
+    ds.distribute(sc.store, sc.bodies)
+    ds.initialize()
+    ds.step(args.warmup)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    ds.step(args.steps)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    dist.barrier()
+    tmax = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dt = float(tmax.item())
+    n = sc.store.n
+    if rank == 0:
+        line = {"metric": "particle-steps/sec (full SPH step, fp64)", "value": n * args.steps / dt,
+                "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64 lattice + jitter)",
+                "config": {"workload": f"C5 {args.nside}^3 periodic, {sc.info['n_bodies']} spheres",
+                           "particles": n, "parallelism": f"domain decomposition {ds.grid.dims}, NCCL halo",
+                           "ghost_width_h": ds.width / ds.h},
+                "timing": "host wall clock between barriers + cuda synchronize, max over ranks "
+                          "(the per-rank step mixes kernels and NCCL exchanges)",
+                "comm_s_rank0": ds.comm_s, "rebuilds": ds.rebuilds, "repartitions": ds.repartitions}
+        print(json.dumps(line))
+    dist.destroy_process_group()

@@ -14,7 +14,8 @@ from . import abi
 
 VEC_FIELDS = ("pos", "vel", "vel_adv", "acc", "acc_bg", "body_frame_pos", "wall_velocity", "force")
 SCALAR_FIELDS = ("density", "pressure", "mass", "temperature", "dT_dt", "wall_pressure")
-TAG_FIELDS = {"kind": np.uint8, "group": np.uint32, "material": np.uint16, "dirichlet_T": np.uint8}
+TAG_FIELDS = {"kind": np.uint8, "group": np.uint32, "material": np.uint16, "dirichlet_T": np.uint8,
+              "owner": np.uint32}
 
 BODY_DTYPE = np.dtype([
     ("mass", "f8"), ("com", "f8", 3), ("inertia", "f8", 6), ("q", "f8", 4),
