@@ -134,35 +134,44 @@ class DistributedSimulation:
         self.comm_s = 0.0
 
     # ------------------------------------------------------------ layout
-    def distribute(self, store, bodies):
-        """Every rank holds the same global store (seeded generation is deterministic)."""
-        pos = store.pos
-        owner = self.grid.owner_of(pos)
-        self.global_n = store.n
-        r = self.rank
+    def local_gids(self, pos, owner, r):
+        """Owned particles of rank r, then its ghosts ordered by (owner rank, gid)."""
         own = np.nonzero(owner == r)[0]
         ghost = np.nonzero((owner != r) & self.grid.near_box(pos, r, self.width))[0]
-        ghost = ghost[np.lexsort((ghost, owner[ghost]))]  # by (owner rank, gid)
-        gids = np.concatenate([own, ghost])
-        self.gids = gids
-        self.n_own = len(own)
+        ghost = ghost[np.lexsort((ghost, owner[ghost]))]
+        return np.concatenate([own, ghost]), len(own)
+
+    def distribute(self, store, bodies):
+        """Every rank holds the same global store (seeded generation is deterministic)."""
+        owner = self.grid.owner_of(store.pos)
+        gids, n_own = self.local_gids(store.pos, owner, self.rank)
         local = ParticleStore(len(gids))
         for f in VEC_FIELDS + SCALAR_FIELDS + tuple(TAG_FIELDS):
             getattr(local, f)[:] = getattr(store, f)[gids]
         local.owner[:] = owner[gids].astype(np.uint32)
-        lid = np.full(store.n, -1, np.int64)
-        lid[gids] = np.arange(len(gids))
+        self.distribute_local(local, gids, n_own, store.n, bodies)
+
+    def distribute_local(self, local, gids, n_own, global_n, bodies):
+        """Takes this rank's owned + ghost particles (owner field set, global gids)."""
+        self.global_n = global_n
+        self.gids = np.asarray(gids)
+        self.n_own = n_own
+        r = self.rank
+        owner = local.owner.astype(np.int64)
+        ghost_local = np.arange(n_own, local.n)
         # halo lists: send = my owned particles that are ghosts on q; recv = my ghosts owned by q;
         # both ordered by global gid, so the two sides agree without a handshake
         self.peers = []
         for q in range(self.world):
             if q == r:
                 continue
-            send_g = own[self.grid.near_box(pos[own], q, self.width)]
-            recv_g = ghost[owner[ghost] == q]
-            if len(send_g) == 0 and len(recv_g) == 0:
+            near = np.nonzero(self.grid.near_box(local.pos[:n_own], q, self.width))[0]
+            send_l = near[np.argsort(self.gids[near], kind="stable")]
+            recv_l = ghost_local[owner[ghost_local] == q]
+            recv_l = recv_l[np.argsort(self.gids[recv_l], kind="stable")]
+            if len(send_l) == 0 and len(recv_l) == 0:
                 continue
-            self.peers.append((q, lid[send_g].astype(np.uint32), lid[recv_g].astype(np.uint32)))
+            self.peers.append((q, send_l.astype(np.uint32), recv_l.astype(np.uint32)))
         if self.engine is None:
             self.engine = self.make_engine(self.params)
         self.engine.upload(local, bodies)
@@ -289,18 +298,74 @@ class DistributedSimulation:
 
 # ---------------------------------------------------------------- bench N>1
 def bench_multi(args):
-    """Strong scaling on the C5 config: every rank generates the seeded global store,
-    keeps its box + ghost shell, runs K steps; value = all particles x K / max rank time."""
+    """Strong scaling on the C5 config: rank 0 generates the seeded global store and
+    ships each rank its box + ghost shell; K steps; value = all particles x K / max rank time."""
     import json
     from . import scenarios
     from .sim import Simulation
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    gpu = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(gpu)
+    # NCCL over NVLink on a real multi-GPU node; SPHG_DIST_BACKEND=gloo runs the same code with
+    # host-staged buffers (used to smoke-test this path with several ranks sharing one GPU)
+    backend = os.environ.get("SPHG_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+    else:
+        dist.init_process_group(backend)
     rank, world = dist.get_rank(), dist.get_world_size()
-    sc = scenarios.config5(nside=args.nside, n_spheres=args.spheres)
-    ds = DistributedSimulation(sc.params, lambda p: Simulation(p, device=local), tensor_device=f"cuda:{local}")
-    ds.distribute(sc.store, sc.bodies)
+    comm = torch.device("cuda", gpu) if backend == "nccl" else torch.device("cpu")
+    # rank 0 generates the seeded global store once and sends every rank only its
+    # owned + ghost subset (host memory stays O(N) overall instead of O(N x ranks))
+    dev = comm
+    if rank == 0:
+        sc = scenarios.config5(nside=args.nside, n_spheres=args.spheres)
+        meta = [sc.params, sc.bodies, sc.info, sc.store.n]
+    else:
+        meta = [None, None, None, None]
+    dist.broadcast_object_list(meta, src=0)
+    params, bodies, info, n_total = meta
+    ds = DistributedSimulation(params, lambda p: Simulation(p, device=gpu), tensor_device=str(comm),
+                               engine_device=f"cuda:{gpu}")
+    fields = VEC_FIELDS + SCALAR_FIELDS + tuple(TAG_FIELDS)
+    if rank == 0:
+        owner = ds.grid.owner_of(sc.store.pos)
+        for r in range(world - 1, -1, -1):
+            gids, n_own = ds.local_gids(sc.store.pos, owner, r)
+            if r == 0:
+                my = (gids, n_own)
+                continue
+            hdr = torch.tensor([len(gids), n_own], dtype=torch.int64, device=dev)
+            dist.send(hdr, r)
+            dist.send(torch.from_numpy(gids.astype(np.int64)).to(dev), r)
+            for f in fields:  # raw bytes: every dtype travels as uint8
+                a = np.ascontiguousarray(getattr(sc.store, f)[gids])
+                dist.send(torch.from_numpy(a.reshape(-1).view(np.uint8)).to(dev), r)
+            dist.send(torch.from_numpy(owner[gids].astype(np.int64)).to(dev), r)
+        gids, n_own = my
+        loc = ParticleStore(len(gids))
+        for f in fields:
+            getattr(loc, f)[:] = getattr(sc.store, f)[gids]
+        loc.owner[:] = owner[gids].astype(np.uint32)
+        del sc
+    else:
+        hdr = torch.empty(2, dtype=torch.int64, device=dev)
+        dist.recv(hdr, 0)
+        m, n_own = int(hdr[0]), int(hdr[1])
+        g = torch.empty(m, dtype=torch.int64, device=dev)
+        dist.recv(g, 0)
+        gids = g.cpu().numpy()
+        loc = ParticleStore(m)
+        for f in fields:
+            a = getattr(loc, f)
+            t = torch.empty(a.nbytes, dtype=torch.uint8, device=dev)
+            dist.recv(t, 0)
+            a.reshape(-1).view(np.uint8)[:] = t.cpu().numpy()
+        t = torch.empty(m, dtype=torch.int64, device=dev)
+        dist.recv(t, 0)
+        loc.owner[:] = t.cpu().numpy().astype(np.uint32)
+    ds.distribute_local(loc, gids, n_own, n_total, bodies)
+    del loc
     ds.initialize()
     ds.step(args.warmup)
     torch.cuda.synchronize()
@@ -310,17 +375,17 @@ def bench_multi(args):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     dist.barrier()
-    tmax = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+    tmax = torch.tensor([dt], dtype=torch.float64, device=dev)
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     dt = float(tmax.item())
-    n = sc.store.n
+    n = n_total
     if rank == 0:
         line = {"metric": "particle-steps/sec (full SPH step, fp64)", "value": n * args.steps / dt,
                 "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64 lattice + jitter)",
-                "config": {"workload": f"C5 {args.nside}^3 periodic, {sc.info['n_bodies']} spheres",
-                           "particles": n, "parallelism": f"domain decomposition {ds.grid.dims}, NCCL halo",
+                "config": {"workload": f"C5 {args.nside}^3 periodic, {info['n_bodies']} spheres",
+                           "particles": n, "parallelism": f"domain decomposition {ds.grid.dims}, {backend} halo",
                            "ghost_width_h": ds.width / ds.h},
                 "timing": "host wall clock between barriers + cuda synchronize, max over ranks "
                           "(the per-rank step mixes kernels and NCCL exchanges)",
