@@ -78,17 +78,20 @@ __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevP
     const double3 pi = ldpos(&D.G0.p[i]);
     const Row R = row_of(L, i);
     int k = lane;
-    for (; k + G < R.n; k += 2 * G) {  // two independent gathers in flight
-      const uint32_t e0 = __ldg(R.e + k), e1 = __ldg(R.e + k + G);
+    // two independent gathers in flight; the next pair of row entries is prefetched
+    uint32_t e0 = k < R.n ? __ldg(R.e + k) : 0u;
+    uint32_t e1 = k + G < R.n ? __ldg(R.e + k + G) : 0u;
+    for (; k + G < R.n; k += 2 * G) {
+      const uint32_t f0 = k + 2 * G < R.n ? __ldg(R.e + k + 2 * G) : 0u;
+      const uint32_t f1 = k + 3 * G < R.n ? __ldg(R.e + k + 3 * G) : 0u;
       const double3 p0 = ldpos(&D.G0.p[nb_index<M>(e0)]);
       const double3 p1 = ldpos(&D.G0.p[nb_index<M>(e1)]);
       s += density_term<M>(P, pi, p0, e0);
       s += density_term<M>(P, pi, p1, e1);
+      e0 = f0;
+      e1 = f1;
     }
-    if (k < R.n) {
-      const uint32_t e = __ldg(R.e + k);
-      s += density_term<M>(P, pi, ldpos(&D.G0.p[nb_index<M>(e)]), e);
-    }
+    if (k < R.n) s += density_term<M>(P, pi, ldpos(&D.G0.p[nb_index<M>(e0)]), e0);
   }
   s = gsum<G>(s);
   if (!active || lane != 0) return;
@@ -125,8 +128,10 @@ __global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevPara
     hi = D.H2.p[i];
     const double3 pi = ldpos(&D.G0.p[i]);
     const Row R = row_of(L, i);
+    uint32_t en = lane < R.n ? __ldg(R.e + lane) : 0u;
     for (int k = lane; k < R.n; k += G) {
-      const uint32_t e = __ldg(R.e + k);
+      const uint32_t e = en;
+      en = k + G < R.n ? __ldg(R.e + k + G) : 0u;
       const uint32_t j = nb_index<M>(e);
       const double2 hj = D.H2.p[j];
       if (hj.y == 0.0) continue;  // non-Dirichlet wall: no conduction
@@ -198,8 +203,10 @@ __global__ void __launch_bounds__(kBlock) k_extrapolate(const __grid_constant__ 
     }
     const double3 pw = ldpos(&D.G0.p[w]);
     const Row R = row_of(L, w);
+    uint32_t en = lane < R.n ? __ldg(R.e + lane) : 0u;
     for (int k = lane; k < R.n; k += G) {
-      const uint32_t e = __ldg(R.e + k);
+      const uint32_t e = en;
+      en = k + G < R.n ? __ldg(R.e + k + G) : 0u;  // row entries stream from HBM: prefetch
       const uint32_t f = nb_index<M>(e);
       const uint32_t kf = D.kmd.p[f];
       if (kind_of(kf) != SPHG_FLUID) continue;
@@ -326,13 +333,40 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
 // kUnroll = 2: two neighbours per iteration, all six 32-byte records requested
 // before any arithmetic (memory-level parallelism against the gather latency).
 template <int G, int M, bool kTvf, bool kSingleEta, int kUnroll>
+__device__ __forceinline__ void forces_fluid_group(const DevParams& P, const Particles& D, const NbrList& L,
+                                                   const uint32_t* __restrict__ list, size_t nlist, size_t g,
+                                                   int lane, DevFlags* __restrict__ fl);
+
+// default mapping: one group of G lanes per list entry, blocks in list order
+template <int G, int M, bool kTvf, bool kSingleEta, int kUnroll>
 __global__ void __launch_bounds__(kBlock, SPHG_FORCES_MINB) k_forces_fluid(const __grid_constant__ DevParams P,
                                                                             Particles D, NbrList L,
                                                                             const uint32_t* __restrict__ list,
                                                                             size_t nlist, DevFlags* __restrict__ fl) {
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
-  const size_t g = t / G;
-  const int lane = (int)(t % G);
+  forces_fluid_group<G, M, kTvf, kSingleEta, kUnroll>(P, D, L, list, nlist, t / G, (int)(t % G), fl);
+}
+
+// persistent mapping: block b sweeps the contiguous list range [b*chunk, (b+1)*chunk), so the
+// warps resident on one SM work on one compact neighbourhood (neighbour records reused in L1)
+template <int G, int M, bool kTvf, bool kSingleEta, int kUnroll, int kBlk>
+__global__ void __launch_bounds__(kBlk, 1) k_forces_fluid_chunked(
+    const __grid_constant__ DevParams P, Particles D, NbrList L, const uint32_t* __restrict__ list, size_t nlist,
+    size_t chunk, DevFlags* __restrict__ fl) {
+  constexpr int kGroups = kBlk / G;
+  const size_t begin = (size_t)blockIdx.x * chunk;
+  const size_t end = min(nlist, begin + chunk);
+  const int lane = threadIdx.x % G;
+  for (size_t base = begin; base < end; base += kGroups) {
+    const size_t g = base + threadIdx.x / G;
+    forces_fluid_group<G, M, kTvf, kSingleEta, kUnroll>(P, D, L, list, g < end ? nlist : 0, g, lane, fl);
+  }
+}
+
+template <int G, int M, bool kTvf, bool kSingleEta, int kUnroll>
+__device__ __forceinline__ void forces_fluid_group(const DevParams& P, const Particles& D, const NbrList& L,
+                                                   const uint32_t* __restrict__ list, size_t nlist, size_t g,
+                                                   int lane, DevFlags* __restrict__ fl) {
   const bool active = g < nlist;
   const uint32_t i = active ? list[g] : 0u;
   double3 acc = make_double3(0, 0, 0), bg = make_double3(0, 0, 0);
@@ -363,11 +397,31 @@ __global__ void __launch_bounds__(kBlock, SPHG_FORCES_MINB) k_forces_fluid(const
         fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e1, b0, b1, b2, acc, bg, coincident);
       }
     }
-    for (; k < R.n; k += G) {
-      const uint32_t e = __ldg(R.e + k);
-      const uint32_t j = nb_index<M>(e);
-      const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
-      fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
+    if (kUnroll == 3) {
+      // software pipeline: row entry two iterations ahead, neighbour position record one ahead
+      uint32_t e = k < R.n ? __ldg(R.e + k) : 0u;
+      uint32_t e1 = k + G < R.n ? __ldg(R.e + k + G) : 0u;
+      double4 h0 = k < R.n ? ldg4(&D.G0.p[nb_index<M>(e)]) : make_double4(0, 0, 0, 0);
+      for (; k < R.n; k += G) {
+        const uint32_t j = nb_index<M>(e);
+        const double4 h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
+        const uint32_t e2 = k + 2 * G < R.n ? __ldg(R.e + k + 2 * G) : 0u;
+        const double4 h0n = k + G < R.n ? ldg4(&D.G0.p[nb_index<M>(e1)]) : h0;
+        fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
+        e = e1;
+        e1 = e2;
+        h0 = h0n;
+      }
+    } else {
+      // row entry prefetched one iteration ahead (rows stream from HBM: hide the index latency)
+      uint32_t e = k < R.n ? __ldg(R.e + k) : 0u;
+      for (; k < R.n; k += G) {
+        const uint32_t en = k + G < R.n ? __ldg(R.e + k + G) : 0u;
+        const uint32_t j = nb_index<M>(e);
+        const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
+        fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
+        e = en;
+      }
     }
   }
   acc.x = gsum<G>(acc.x);
@@ -414,8 +468,10 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
     R.V2 = g0.w;
     const double3 pr = ld3(g0);
     const Row Rw = row_of(L, r);
+    uint32_t en = lane < Rw.n ? __ldg(Rw.e + lane) : 0u;
     for (int k = lane; k < Rw.n; k += G) {
-      const uint32_t e = __ldg(Rw.e + k);
+      const uint32_t e = en;
+      en = k + G < Rw.n ? __ldg(Rw.e + k + G) : 0u;
       const uint32_t j = nb_index<M>(e);
       const uint32_t kj = D.kmd.p[j];
       const uint32_t kindj = kind_of(kj);
@@ -597,12 +653,30 @@ void launch_extrapolate(Ctx& c) {
 
 template <bool kTvf, bool kSingleEta>
 static void launch_forces_fluid_t(Ctx& c) {
-  if (c.nf && c.unroll_forces == 2)
+  if (c.nf && c.unroll_forces == 3)
+    SPHG_G_DISPATCH(c.group_forces,
+                    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 3>
+                                                     <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
+  else if (c.nf && c.unroll_forces == 2)
     SPHG_G_DISPATCH(c.group_forces,
                     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 2>
                                                      <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
-  else if (c.nf)
+  else if (c.nf && c.persist_blocks > 0) {
+    const size_t nblk = (size_t)c.persist_blocks;
+    const size_t chunk = (c.nf + nblk - 1) / nblk;
+    if (c.persist_threads == 640)
+      SPHG_G_DISPATCH(c.group_forces,
+                      SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid_chunked<G, M, kTvf, kSingleEta, 1, 640>
+                                                       <<<(int)nblk, 640, 0, c.stream>>>(
+                                                           c.P, c.cur, c.nl(), c.fidx.p, c.nf, chunk, c.dflags))));
+    else
+      SPHG_G_DISPATCH(c.group_forces,
+                      SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid_chunked<G, M, kTvf, kSingleEta, 1, 128>
+                                                       <<<(int)nblk, 128, 0, c.stream>>>(
+                                                           c.P, c.cur, c.nl(), c.fidx.p, c.nf, chunk, c.dflags))));
+  } else if (c.nf)
     SPHG_G_DISPATCH(c.group_forces,
                     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 1>
                                                      <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
