@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(256) k_final_kick(const __grid_constant__ DevP
   if (kind == SPHG_FLUID) {
     const double3 uh = ldpos(&D.G1.p[k]);
     const double4 a = D.A4.p[k];
-    stpos(&D.V4.p[k], make_double3(axpy_rn(uh.x, P.hdt, a.x), axpy_rn(uh.y, P.hdt, a.y), axpy_rn(uh.z, P.hdt, a.z)));
+    const double m = D.V4.p[k].w;
+    D.V4.p[k] = make_double4(axpy_rn(uh.x, P.hdt, a.x), axpy_rn(uh.y, P.hdt, a.y), axpy_rn(uh.z, P.hdt, a.z), m);
   } else if (kind == SPHG_RIGID) {
     const sphg_body& b = B[D.group.p[k]];
     const double3 rk = qrotate(body_q(b), ld3(D.X4.p[k]));
