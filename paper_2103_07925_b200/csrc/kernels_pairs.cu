@@ -274,8 +274,10 @@ struct PairSide {
 template <bool kTvf, bool kSingleEta>
 __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, double3 d, double r2,
                                           const DevParams& P, double3& acc, double3& bg) {
-  const double rinv = rsqrt_fast(r2);  // ~1e-11 relative; pair terms enter linearly
-  const double dW = P.sig_h * shape_deriv_q(r2 * rinv * P.inv_h);
+  // accurate q: dW ~ (3-q)^4 amplifies errors of q near the cut-off, and a rigid particle whose
+  // only fluid neighbour sits there sees that single term (coupling force)
+  double rinv;
+  const double dW = P.sig_h * shape_deriv_q(sqrt_and_rinv(r2, rinv) * P.inv_h);
   const double fac = dW * rinv;  // gradW = fac * d
   const double3 gW = make_double3(fac * d.x, fac * d.y, fac * d.z);
   const double V2 = I.V2 + J.V2;
