@@ -60,10 +60,10 @@ __device__ __forceinline__ double density_term(const DevParams& P, double3 pi, d
   const double3 d = pair_delta<M>(P, pi, pj, e);
   const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
   if (r2 > P.rc2) return 0.0;
-  // r = r2 * rsqrt (~1e-11): W errors near the cut-off are tiny in absolute terms against the
-  // self term (66), so the density sum stays far inside 1e-10; + tiny: coincident -> W(0)
-  const double x = r2 + 1e-300;
-  return shape_q(x * rsqrt_fast(x) * P.inv_h);
+  // accurate r: p = c^2 (rho - rho0) cancels, so the pressure (and every force term built on it)
+  // needs rho to ~1e-15, not just 1e-10; + tiny: coincident -> W(0)
+  double ri;
+  return shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);
 }
 
 // rho_i = m_i sigma (66 + sum_j shape(r_ij/h)); p_i = c^2 (rho_i - rho0); V_i = m_i/rho_i
