@@ -530,6 +530,7 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
   if (const char* e = std::getenv("SPHG_UNROLL_FORCES")) c.unroll_forces = std::atoi(e);
   if (const char* e = std::getenv("SPHG_PERSIST_BLOCKS")) c.persist_blocks = std::atoi(e);
   if (const char* e = std::getenv("SPHG_PERSIST_THREADS")) c.persist_threads = std::atoi(e);
+  if (const char* e = std::getenv("SPHG_CELL_BUILD")) c.cell_build = std::atoi(e) != 0;
   try {
     SPHG_CUDA_CHECK(cudaSetDevice(device));
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));

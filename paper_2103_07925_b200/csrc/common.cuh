@@ -261,6 +261,8 @@ struct DevFlags {
   uint32_t n_events;                  // transition events
   uint32_t changed;                   // label propagation
   uint32_t pad[2];
+  uint32_t build_overflow;            // cell-cooperative build could not take a cell
+  uint32_t pad2[3];
 };
 
 __device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, double v) {

@@ -95,6 +95,7 @@ struct Ctx {
   int unroll_forces = 1;
   int persist_blocks = 0;  // > 0: chunked persistent mapping of the fluid force kernel
   int persist_threads = 128;
+  bool cell_build = true;  // cell-cooperative Verlet build (falls back per particle on overflow)
   // transitions scratch
   DBuf<uint32_t> ev_idx, ev_flag, label, tscratch;
   // flags

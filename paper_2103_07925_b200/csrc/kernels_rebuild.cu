@@ -157,6 +157,166 @@ __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ Dev
   }
 }
 
+// Cell-cooperative build: one warp per home cell.  The 27 neighbour cells are
+// staged once in shared memory as fp32 positions relative to the home cell (in
+// units of h); lanes run over the home cell's particles and test every staged
+// candidate in fp32.  Pairs inside a 1e-4 guard band around r_v^2 (fp32 error
+// is ~1e-6 relative here) fall back to the exact fp64 test of [P2] on the
+// original positions, so the list is bit-identical to the pinned rule.
+constexpr int kStage = 512;     // staged candidates per batch (10 KB)
+constexpr int kHomeMax = 256;   // particles per home cell handled here; denser cells -> per-particle kernel
+
+struct BuildCtx {
+  const DevParams* P;
+  const double4* G0;
+  const uint32_t* kmd;
+  uint32_t* nbr;
+  int cap;
+};
+
+// test the staged batch against every home particle, appending hits to their rows
+__device__ __forceinline__ void build_batch(const DevParams& P, const double4* __restrict__ G0,
+                                            const uint32_t* __restrict__ kmd, uint32_t* __restrict__ nbr, int cap,
+                                            uint32_t h0, uint32_t h1, double ox0, double oy0, double oz0,
+                                            const float4* sp, const uint32_t* se, int ns, uint32_t* hc,
+                                            uint32_t emask) {
+  const int lane = threadIdx.x;
+  const float rv2 = (float)(P.rv2 * P.inv_h * P.inv_h);
+  const float lo_band = rv2 * (1.0f - 1e-4f), hi_band = rv2 * (1.0f + 1e-4f);
+  for (uint32_t ib = h0; ib < h1; ib += 32) {
+    const uint32_t i = ib + lane;
+    const bool act = i < h1 && !is_ghost(kmd[i]);
+    double4 pi = make_double4(0, 0, 0, 0);
+    float xi = 0.f, yi = 0.f, zi = 0.f;
+    bool bi = false;
+    uint32_t count = 0;
+    if (act) {
+      pi = G0[i];
+      xi = (float)((pi.x - ox0) * P.inv_h);
+      yi = (float)((pi.y - oy0) * P.inv_h);
+      zi = (float)((pi.z - oz0) * P.inv_h);
+      bi = kind_of(kmd[i]) == SPHG_BOUNDARY;
+      count = hc[i - h0];
+    }
+    uint32_t* row = nbr + (size_t)i * cap;
+    for (int t = 0; t < ns; ++t) {
+      const float4 q = sp[t];
+      const float dx = xi - q.x, dy = yi - q.y, dz = zi - q.z;
+      const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      if (!act || r2 > hi_band) continue;
+      const uint32_t e = se[t];
+      const uint32_t j = e & emask;
+      if (j == i || (bi && q.w != 0.f)) continue;
+      bool hit = r2 < lo_band;
+      if (!hit) {  // guard band: the pinned exact test
+        const double4 pj = G0[j];
+        hit = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) <= P.rv2;
+      }
+      if (hit) {
+        if ((int)count < cap) row[count] = e;
+        ++count;
+      }
+    }
+    if (act) hc[i - h0] = count;
+  }
+}
+
+__global__ void __launch_bounds__(32) k_build_nlist_cells(const __grid_constant__ DevParams P,
+                                                           const double4* __restrict__ G0,
+                                                           const uint32_t* __restrict__ kmd,
+                                                           const uint32_t* __restrict__ cstart,
+                                                           const uint32_t* __restrict__ cend,
+                                                           uint32_t* __restrict__ nbr, uint32_t* __restrict__ cnt,
+                                                           int cap, DevFlags* __restrict__ fl) {
+  __shared__ float4 sp[kStage];     // x, y, z (relative to the home cell, units of h), boundary flag
+  __shared__ uint32_t se[kStage];   // neighbour index | image code
+  __shared__ uint32_t hc[kHomeMax]; // running row length per home particle
+  const int64_t c = blockIdx.x;
+  const int lane = threadIdx.x;
+  const uint32_t h0 = cstart[c], h1 = cend[c];
+  if (h1 <= h0) return;
+  if (h1 - h0 > (uint32_t)kHomeMax) {
+    if (lane == 0) atomicOr(&fl->build_overflow, 1u);
+    return;
+  }
+  for (uint32_t k = lane; k < h1 - h0; k += 32) hc[k] = 0;
+  const int64_t nz = P.ncell[2], ny = P.ncell[1], nx = P.ncell[0];
+  const int64_t cz = c % nz, cy = (c / nz) % ny, cx = c / (nz * ny);
+  const double ox0 = P.lo[0] + (double)cx / P.inv_edge[0];  // any fixed origin near the cell works
+  const double oy0 = P.lo[1] + (double)cy / P.inv_edge[1];
+  const double oz0 = P.lo[2] + (double)cz / P.inv_edge[2];
+  const bool code = P.img_mode == kImgCode;
+  const uint32_t emask = code ? kIdxMask : 0xffffffffu;
+  int ns = 0;
+  for (int ox = -1; ox <= 1; ++ox) {
+    int64_t qx = cx + ox;
+    uint32_t ix = 0;
+    double sx = 0.0;
+    if (qx < 0 || qx >= nx) {
+      if (!P.periodic[0]) continue;
+      ix = qx < 0 ? 1u : 2u;
+      sx = qx < 0 ? -P.L[0] : P.L[0];
+      qx = (qx + nx) % nx;
+    }
+    for (int oy = -1; oy <= 1; ++oy) {
+      int64_t qy = cy + oy;
+      uint32_t iy = 0;
+      double sy = 0.0;
+      if (qy < 0 || qy >= ny) {
+        if (!P.periodic[1]) continue;
+        iy = qy < 0 ? 1u : 2u;
+        sy = qy < 0 ? -P.L[1] : P.L[1];
+        qy = (qy + ny) % ny;
+      }
+      for (int oz = -1; oz <= 1; ++oz) {
+        int64_t qz = cz + oz;
+        uint32_t iz = 0;
+        double sz = 0.0;
+        if (qz < 0 || qz >= nz) {
+          if (!P.periodic[2]) continue;
+          iz = qz < 0 ? 1u : 2u;
+          sz = qz < 0 ? -P.L[2] : P.L[2];
+          qz = (qz + nz) % nz;
+        }
+        const uint32_t tag = code ? ((ix << 26) | (iy << 28) | (iz << 30)) : 0u;
+        const int64_t cj = (qx * ny + qy) * nz + qz;
+        const uint32_t j0 = cstart[cj], j1 = cend[cj];
+        for (uint32_t jb = j0; jb < j1;) {
+          const int take = (int)min((uint32_t)(kStage - ns), j1 - jb);
+          for (int t = lane; t < take; t += 32) {
+            const uint32_t j = jb + t;
+            const double4 pj = G0[j];
+            // the periodic image of the cell: x_j + s sits next to the home cell
+            sp[ns + t] = make_float4((float)((pj.x + sx - ox0) * P.inv_h), (float)((pj.y + sy - oy0) * P.inv_h),
+                                     (float)((pj.z + sz - oz0) * P.inv_h),
+                                     kind_of(kmd[j]) == SPHG_BOUNDARY ? 1.f : 0.f);
+            se[ns + t] = j | tag;
+          }
+          ns += take;
+          jb += take;
+          if (ns == kStage) {
+            __syncwarp();
+            build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, sp, se, ns, hc, emask);
+            __syncwarp();
+            ns = 0;
+          }
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (ns) build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, sp, se, ns, hc, emask);
+  __syncwarp();
+  uint32_t mx = 0;
+  for (uint32_t k = lane; k < h1 - h0; k += 32) {
+    const uint32_t i = h0 + k;
+    const uint32_t v = is_ghost(kmd[i]) ? 0u : hc[k];
+    cnt[i] = v;
+    mx = max(mx, v);
+  }
+  if (mx) atomicMax(&fl->max_count, mx);
+}
+
 // ------------------------------------------------------- rigid index
 __global__ void k_rigid_flags(const uint32_t* __restrict__ kmd, size_t n, uint32_t* __restrict__ flag) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -297,10 +457,21 @@ void launch_rebuild(Ctx& c) {
     if (c.cap <= 0) c.cap = c.params.nlist_capacity > 0 ? c.params.nlist_capacity : 144;
     c.nbr.alloc((size_t)c.cap * n);
     SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->max_count, 0, sizeof(uint32_t), s));
-    k_build_nlist<<<grid_for(n * 32, 128), 128, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_key.p, c.cell_start.p,
-                                                        c.cell_end.p, c.nbr.p, c.cnt.p, c.cap, n, c.dflags);
-    c.launches += 2;
-    uint32_t mc = 0;
+    uint32_t mc = 0, err = 0;
+    if (c.cell_build) {
+      SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->build_overflow, 0, sizeof(uint32_t), s));
+      k_build_nlist_cells<<<(unsigned)c.ncells, 32, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_start.p,
+                                                            c.cell_end.p, c.nbr.p, c.cnt.p, c.cap, c.dflags);
+      SPHG_CUDA_CHECK(cudaMemcpyAsync(&err, &c.dflags->build_overflow, 4, cudaMemcpyDeviceToHost, s));
+      SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+      c.launches += 2;
+    }
+    if (!c.cell_build || err) {  // per-particle build (also the fallback for over-dense cells)
+      k_build_nlist<<<grid_for(n * 32, 128), 128, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_key.p, c.cell_start.p,
+                                                          c.cell_end.p, c.nbr.p, c.cnt.p, c.cap, n, c.dflags);
+      c.launches++;
+    }
+    c.launches++;
     SPHG_CUDA_CHECK(cudaMemcpyAsync(&mc, &c.dflags->max_count, 4, cudaMemcpyDeviceToHost, s));
     SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
     c.max_count = (int)mc;

@@ -189,3 +189,26 @@ def test_cpp_dropin_on_device():
     assert os.path.exists(exe), "build() compiles tests/cpp/test_dropin"
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("cell_build", ["0", "1"])
+def test_nlist_both_builders_bitexact(cell_build, Oracle, monkeypatch):
+    """Per-particle and cell-cooperative Verlet builders give the pinned list."""
+    monkeypatch.setenv("SPHG_CELL_BUILD", cell_build)
+    for sc in (CASES["c1_small"](), CASES["c2_small"]()):
+        sim, orc = run_pair(sc, sim_factory, Oracle, init=False)
+        sim.build_pairs()
+        orc.build_pairs()
+        assert np.array_equal(sim.get_nlist()[1], orc.get_nlist()[1])
+
+
+def test_nlist_dense_cells_fallback(Oracle):
+    """Cells denser than the cooperative builder takes (cell edge override 8.5 dx, ~600 particles
+    per cell) fall back to the per-particle builder; the list is unchanged."""
+    sc = scenarios.config1(nside=32, n_spheres=2, r_range=(3.0, 3.0), seed=5)
+    sc.params.cell_edge_override = 8.5e-3
+    sim, orc = run_pair(sc, sim_factory, Oracle, init=False)
+    sim.build_pairs()
+    orc.build_pairs()
+    assert np.array_equal(sim.get_cells()[0], orc.get_cells()[0])
+    assert np.array_equal(sim.get_nlist()[1], orc.get_nlist()[1])
