@@ -527,9 +527,6 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
   c.ncells = (int64_t)c.P.ncell[0] * c.P.ncell[1] * c.P.ncell[2];
   if (const char* e = std::getenv("SPHG_GROUP_DENSITY")) c.group_density = std::atoi(e);
   if (const char* e = std::getenv("SPHG_GROUP_FORCES")) c.group_forces = std::atoi(e);
-  if (const char* e = std::getenv("SPHG_UNROLL_FORCES")) c.unroll_forces = std::atoi(e);
-  if (const char* e = std::getenv("SPHG_PERSIST_BLOCKS")) c.persist_blocks = std::atoi(e);
-  if (const char* e = std::getenv("SPHG_PERSIST_THREADS")) c.persist_threads = std::atoi(e);
   if (const char* e = std::getenv("SPHG_CELL_BUILD")) c.cell_build = std::atoi(e) != 0;
   try {
     SPHG_CUDA_CHECK(cudaSetDevice(device));
@@ -715,7 +712,7 @@ int sphg_get_nlist(sphg_ctx* h, int64_t* offsets, uint32_t* nbr_gid) {
     d2h(gid.data(), c.cur.gid.p, n, c.stream);
     SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     std::vector<int64_t> cnt_g(n);
-    for (size_t k = 0; k < n; ++k) cnt_g[gid[k]] = cnt[k];
+    for (size_t k = 0; k < n; ++k) cnt_g[gid[k]] = cnt_total(cnt[k]);
     int64_t o = 0;
     for (size_t g = 0; g < n; ++g) {
       if (offsets) offsets[g] = o;
@@ -729,8 +726,11 @@ int sphg_get_nlist(sphg_ctx* h, int64_t* offsets, uint32_t* nbr_gid) {
     const uint32_t mask = c.P.img_mode == kImgCode ? kIdxMask : 0xffffffffu;
     for (size_t k = 0; k < n; ++k) {
       const int64_t base = offsets[gid[k]];
-      for (uint32_t q = 0; q < cnt[k]; ++q) nbr_gid[base + q] = gid[rows[k * (size_t)c.cap + q] & mask];
-      std::sort(nbr_gid + base, nbr_gid + base + cnt[k]);
+      const uint32_t* row = rows.data() + k * (size_t)c.cap;
+      const uint32_t nf = cnt_fluid(cnt[k]), no = cnt_other(cnt[k]);
+      for (uint32_t q = 0; q < nf; ++q) nbr_gid[base + q] = gid[row[q] & mask];
+      for (uint32_t q = 0; q < no; ++q) nbr_gid[base + nf + q] = gid[row[c.cap - 1 - q] & mask];
+      std::sort(nbr_gid + base, nbr_gid + base + nf + no);
     }
     return SPHG_OK;
   });
@@ -757,7 +757,9 @@ int sphg_stats(sphg_ctx* h, sphg_stats_t* s) {
       std::vector<uint32_t> cnt(c.n);
       d2h(cnt.data(), c.cnt.p, c.n, c.stream);
       SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-      s->n_pairs_candidate = std::accumulate(cnt.begin(), cnt.end(), (int64_t)0);
+      int64_t tot = 0;
+      for (uint32_t v : cnt) tot += cnt_total(v);
+      s->n_pairs_candidate = tot;
     }
     if (c.nb) {
       std::vector<sphg_body> b(c.nb);

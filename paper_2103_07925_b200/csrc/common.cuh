@@ -169,6 +169,15 @@ __device__ __forceinline__ double3 pair_delta(const DevParams& P, double3 a, dou
   return d;
 }
 
+// Kind-partitioned rows: fluid neighbours fill row i from the front, rigid and boundary
+// neighbours from the back; cnt[i] packs both counts (fluid | non-fluid << 16).
+__host__ __device__ __forceinline__ uint32_t cnt_fluid(uint32_t c) { return c & 0xffffu; }
+__host__ __device__ __forceinline__ uint32_t cnt_other(uint32_t c) { return c >> 16; }
+__host__ __device__ __forceinline__ uint32_t cnt_total(uint32_t c) { return (c & 0xffffu) + (c >> 16); }
+__host__ __device__ __forceinline__ uint32_t pack_cnt(uint32_t nf, uint32_t no) {
+  return (nf > 0xffffu ? 0xffffu : nf) | ((no > 0xffffu ? 0xffffu : no) << 16);
+}
+
 // sum over a group of G consecutive lanes (every lane of the warp must call it)
 template <int G>
 __device__ __forceinline__ double gsum(double v) {

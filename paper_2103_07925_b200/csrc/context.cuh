@@ -92,9 +92,6 @@ struct Ctx {
   DBuf<uint32_t> fidx, widx, ridx, body_start;
   size_t nf = 0, nw = 0, nrigid = 0;
   int group_density = 4, group_forces = 4;  // lanes per particle in the pair kernels
-  int unroll_forces = 1;
-  int persist_blocks = 0;  // > 0: chunked persistent mapping of the fluid force kernel
-  int persist_threads = 128;
   bool cell_build = true;  // cell-cooperative Verlet build (falls back per particle on overflow)
   // transitions scratch
   DBuf<uint32_t> ev_idx, ev_flag, label, tscratch;

@@ -23,9 +23,7 @@ namespace sphg {
 namespace {
 
 constexpr int kBlock = 128;
-#ifndef SPHG_FORCES_MINB
-#define SPHG_FORCES_MINB 1
-#endif
+
 
 __device__ __forceinline__ double3 ld3(const double4& v) { return make_double3(v.x, v.y, v.z); }
 // One 32-byte load per particle record (sm_100 LDG.E.ENL2.256): a record is one
@@ -46,12 +44,24 @@ __device__ __forceinline__ double3 ldpos(const double4* p) { return ld3(ld4(p));
 __device__ __forceinline__ Quat body_q(const sphg_body& b) { return {b.q[0], b.q[1], b.q[2], b.q[3]}; }
 __device__ __forceinline__ double3 bv(const double* p) { return make_double3(p[0], p[1], p[2]); }
 
+// A Verlet row: fluid neighbours at f[0..nf), rigid/boundary neighbours at b[0], b[-1], ... (no).
 struct Row {
-  const uint32_t* e;
-  int n;
+  const uint32_t* f;
+  const uint32_t* b;
+  int nf, no, n;
+  // unified index over both parts (kernels that treat every neighbour alike)
+  __device__ __forceinline__ uint32_t at(int k) const { return k < nf ? __ldg(f + k) : __ldg(b - (k - nf)); }
 };
 __device__ __forceinline__ Row row_of(const NbrList& L, uint32_t i) {
-  return {L.nbr + (size_t)i * L.cap, (int)L.cnt[i]};
+  const uint32_t c = L.cnt[i];
+  const uint32_t* r = L.nbr + (size_t)i * L.cap;
+  Row R;
+  R.f = r;
+  R.b = r + L.cap - 1;
+  R.nf = (int)cnt_fluid(c);
+  R.no = (int)cnt_other(c);
+  R.n = R.nf + R.no;
+  return R;
 }
 
 // ---------------------------------------------------------------- density
@@ -67,6 +77,7 @@ __device__ __forceinline__ double density_term(const DevParams& P, double3 pi, d
 }
 
 // rho_i = m_i sigma (66 + sum_j shape(r_ij/h)); p_i = c^2 (rho_i - rho0); V_i = m_i/rho_i
+// (j over neighbours of any kind)
 template <int G, int M>
 __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                      const uint32_t* __restrict__ list, size_t nlist) {
@@ -81,11 +92,11 @@ __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevP
     const Row R = row_of(L, i);
     int k = lane;
     // two independent gathers in flight; the next pair of row entries is prefetched
-    uint32_t e0 = k < R.n ? __ldg(R.e + k) : 0u;
-    uint32_t e1 = k + G < R.n ? __ldg(R.e + k + G) : 0u;
+    uint32_t e0 = k < R.n ? R.at(k) : 0u;
+    uint32_t e1 = k + G < R.n ? R.at(k + G) : 0u;
     for (; k + G < R.n; k += 2 * G) {
-      const uint32_t f0 = k + 2 * G < R.n ? __ldg(R.e + k + 2 * G) : 0u;
-      const uint32_t f1 = k + 3 * G < R.n ? __ldg(R.e + k + 3 * G) : 0u;
+      const uint32_t f0 = k + 2 * G < R.n ? R.at(k + 2 * G) : 0u;
+      const uint32_t f1 = k + 3 * G < R.n ? R.at(k + 3 * G) : 0u;
       const double3 p0 = ldpos(&D.G0.p[nb_index<M>(e0)]);
       const double3 p1 = ldpos(&D.G0.p[nb_index<M>(e1)]);
       s += density_term<M>(P, pi, p0, e0);
@@ -130,10 +141,10 @@ __global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevPara
     hi = D.H2.p[i];
     const double3 pi = ldpos(&D.G0.p[i]);
     const Row R = row_of(L, i);
-    uint32_t en = lane < R.n ? __ldg(R.e + lane) : 0u;
+    uint32_t en = lane < R.n ? R.at(lane) : 0u;
     for (int k = lane; k < R.n; k += G) {
       const uint32_t e = en;
-      en = k + G < R.n ? __ldg(R.e + k + G) : 0u;
+      en = k + G < R.n ? R.at(k + G) : 0u;
       const uint32_t j = nb_index<M>(e);
       const double2 hj = D.H2.p[j];
       if (hj.y == 0.0) continue;  // non-Dirichlet wall: no conduction
@@ -177,6 +188,7 @@ __global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevPara
 // ---------------------------------------------------------- extrapolation
 // p_w = sum_f W (p_f + rho_f (g_f - a_w).(r_w - r_f)) / sum_f W;  u~_w = 2 u_w - sum_f W u_f / sum_f W;
 // rho_w = max(rho0, rho0 + p_w/c^2) of the dominant fluid material; V_w = rho0 dx^3 / rho_w  [P6][P7]
+// Only the fluid part of the row is visited.
 template <int G, int M, bool kMultiEos>
 __global__ void __launch_bounds__(kBlock) k_extrapolate(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                          const sphg_body* __restrict__ B,
@@ -205,28 +217,28 @@ __global__ void __launch_bounds__(kBlock) k_extrapolate(const __grid_constant__ 
     }
     const double3 pw = ldpos(&D.G0.p[w]);
     const Row R = row_of(L, w);
-    uint32_t en = lane < R.n ? __ldg(R.e + lane) : 0u;
-    for (int k = lane; k < R.n; k += G) {
+    uint32_t en = lane < R.nf ? __ldg(R.f + lane) : 0u;
+    for (int k = lane; k < R.nf; k += G) {
       const uint32_t e = en;
-      en = k + G < R.n ? __ldg(R.e + k + G) : 0u;  // row entries stream from HBM: prefetch
+      en = k + G < R.nf ? __ldg(R.f + k + G) : 0u;  // row entries stream from HBM: prefetch
       const uint32_t f = nb_index<M>(e);
-      const uint32_t kf = D.kmd.p[f];
-      if (kind_of(kf) != SPHG_FLUID) continue;
-      const double3 d = pair_delta<M>(P, pw, ldpos(&D.G0.p[f]), e);
+      const double4 g0 = ld4(&D.G0.p[f]);
+      const double3 d = pair_delta<M>(P, pw, ld3(g0), e);
       const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
       if (r2 > P.rc2) continue;
       double ri;
       const double W = shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);  // sigma cancels in the ratios
       const double4 g1 = D.G1.p[f];
       const double pf = D.G2.p[f].w;
-      const DevMat& Mf = P.mat[mat_of(kf)];
+      const uint32_t mf = kMultiEos || P.n_mat > 1 ? mat_of(D.kmd.p[f]) : 0u;
+      const DevMat& Mf = P.mat[mf];
       const double ga = (Mf.g[0] - aw.x) * d.x + (Mf.g[1] - aw.y) * d.y + (Mf.g[2] - aw.z) * d.z;
       sw += W;
       sp += W * (pf + g1.w * ga);
       su.x += W * g1.x;
       su.y += W * g1.y;
       su.z += W * g1.z;
-      if (kMultiEos) smat[mat_of(kf)] += W;
+      if (kMultiEos) smat[mf] += W;
     }
   }
   sw = gsum<G>(sw);
@@ -271,7 +283,8 @@ struct PairSide {
   double rho, p, V2, eta, hrho;  // hrho = rho/2 (TVF)
 };
 
-template <bool kTvf, bool kSingleEta>
+// kJFluid = false: j is a wall/rigid particle: A_j = 0 and eta_j = eta_i [P5][P7]
+template <bool kTvf, bool kSingleEta, bool kJFluid>
 __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, double3 d, double r2,
                                           const DevParams& P, double3& acc, double3& bg) {
   // accurate q: dW ~ (3-q)^4 amplifies errors of q near the cut-off, and a rigid particle whose
@@ -283,7 +296,7 @@ __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, 
   const double V2 = I.V2 + J.V2;
   const double pt = fma(J.rho, I.p, I.rho * J.p) * rcp_fast(I.rho + J.rho);
   double et;
-  if (kSingleEta) {
+  if (kSingleEta || !kJFluid) {
     et = I.eta;  // 2 eta eta / (eta + eta)
   } else {
     const double es = I.eta + J.eta;
@@ -294,10 +307,15 @@ __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, 
                            fma(vf, I.u.z - J.u.z, -pt * gW.z));
   if (kTvf) {
     const double ai = I.hrho * (I.du.x * gW.x + I.du.y * gW.y + I.du.z * gW.z);
-    const double aj = J.hrho * (J.du.x * gW.x + J.du.y * gW.y + J.du.z * gW.z);
-    t.x += ai * I.u.x + aj * J.u.x;
-    t.y += ai * I.u.y + aj * J.u.y;
-    t.z += ai * I.u.z + aj * J.u.z;
+    t.x += ai * I.u.x;
+    t.y += ai * I.u.y;
+    t.z += ai * I.u.z;
+    if (kJFluid) {
+      const double aj = J.hrho * (J.du.x * gW.x + J.du.y * gW.y + J.du.z * gW.z);
+      t.x += aj * J.u.x;
+      t.y += aj * J.u.y;
+      t.z += aj * J.u.z;
+    }
   }
   acc.x = fma(V2, t.x, acc.x);
   acc.y = fma(V2, t.y, acc.y);
@@ -307,7 +325,7 @@ __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, 
   bg.z = fma(V2, gW.z, bg.z);
 }
 
-template <int M, bool kTvf, bool kSingleEta>
+template <int M, bool kTvf, bool kSingleEta, bool kJFluid>
 __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
                                            uint32_t e, double4 h0, double4 h1, double4 h2, double3& acc,
                                            double3& bg, bool& coincident) {
@@ -325,52 +343,38 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
   J.hrho = 0.5 * h1.w;
   J.p = h2.w;
   J.V2 = h0.w;
-  if (kSingleEta) {
+  if (kSingleEta || !kJFluid) {
     J.eta = I.eta;
   } else {
-    const uint32_t kj = __ldg(&D.kmd.p[nb_index<M>(e)]);
-    J.eta = kind_of(kj) == SPHG_FLUID ? P.mat[mat_of(kj)].eta : I.eta;  // eta_w := eta_i [P7]
+    J.eta = P.mat[mat_of(__ldg(&D.kmd.p[nb_index<M>(e)]))].eta;
   }
-  pair_term<kTvf, kSingleEta>(I, J, d, r2, P, acc, bg);
+  pair_term<kTvf, kSingleEta, kJFluid>(I, J, d, r2, P, acc, bg);
 }
 
-// kUnroll = 2: two neighbours per iteration, all six 32-byte records requested
-// before any arithmetic (memory-level parallelism against the gather latency).
-template <int G, int M, bool kTvf, bool kSingleEta, int kUnroll>
-__device__ __forceinline__ void forces_fluid_group(const DevParams& P, const Particles& D, const NbrList& L,
-                                                   const uint32_t* __restrict__ list, size_t nlist, size_t g,
-                                                   int lane, DevFlags* __restrict__ fl);
+// one part of a row (fluid: stride +1 from f; non-fluid: stride -1 from b), row entries prefetched
+// one iteration ahead (rows stream from HBM), all three 32-byte neighbour records requested together
+template <int G, int M, bool kTvf, bool kSingleEta, bool kJFluid>
+__device__ __forceinline__ void fluid_part(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
+                                           const uint32_t* base, int stride, int n, int lane, double3& acc,
+                                           double3& bg, bool& coincident) {
+  int k = lane;
+  uint32_t e = k < n ? __ldg(base + stride * k) : 0u;
+  for (; k < n; k += G) {
+    const uint32_t en = k + G < n ? __ldg(base + stride * (k + G)) : 0u;
+    const uint32_t j = nb_index<M>(e);
+    const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
+    fluid_pair<M, kTvf, kSingleEta, kJFluid>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
+    e = en;
+  }
+}
 
-// default mapping: one group of G lanes per list entry, blocks in list order
-template <int G, int M, bool kTvf, bool kSingleEta, int kUnroll>
-__global__ void __launch_bounds__(kBlock, SPHG_FORCES_MINB) k_forces_fluid(const __grid_constant__ DevParams P,
-                                                                            Particles D, NbrList L,
-                                                                            const uint32_t* __restrict__ list,
-                                                                            size_t nlist, DevFlags* __restrict__ fl) {
+template <int G, int M, bool kTvf, bool kSingleEta>
+__global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                          const uint32_t* __restrict__ list, size_t nlist,
+                                                          DevFlags* __restrict__ fl) {
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
-  forces_fluid_group<G, M, kTvf, kSingleEta, kUnroll>(P, D, L, list, nlist, t / G, (int)(t % G), fl);
-}
-
-// persistent mapping: block b sweeps the contiguous list range [b*chunk, (b+1)*chunk), so the
-// warps resident on one SM work on one compact neighbourhood (neighbour records reused in L1)
-template <int G, int M, bool kTvf, bool kSingleEta, int kUnroll, int kBlk>
-__global__ void __launch_bounds__(kBlk, 1) k_forces_fluid_chunked(
-    const __grid_constant__ DevParams P, Particles D, NbrList L, const uint32_t* __restrict__ list, size_t nlist,
-    size_t chunk, DevFlags* __restrict__ fl) {
-  constexpr int kGroups = kBlk / G;
-  const size_t begin = (size_t)blockIdx.x * chunk;
-  const size_t end = min(nlist, begin + chunk);
-  const int lane = threadIdx.x % G;
-  for (size_t base = begin; base < end; base += kGroups) {
-    const size_t g = base + threadIdx.x / G;
-    forces_fluid_group<G, M, kTvf, kSingleEta, kUnroll>(P, D, L, list, g < end ? nlist : 0, g, lane, fl);
-  }
-}
-
-template <int G, int M, bool kTvf, bool kSingleEta, int kUnroll>
-__device__ __forceinline__ void forces_fluid_group(const DevParams& P, const Particles& D, const NbrList& L,
-                                                   const uint32_t* __restrict__ list, size_t nlist, size_t g,
-                                                   int lane, DevFlags* __restrict__ fl) {
+  const size_t g = t / G;
+  const int lane = (int)(t % G);
   const bool active = g < nlist;
   const uint32_t i = active ? list[g] : 0u;
   double3 acc = make_double3(0, 0, 0), bg = make_double3(0, 0, 0);
@@ -389,59 +393,8 @@ __device__ __forceinline__ void forces_fluid_group(const DevParams& P, const Par
     I.eta = P.mat[mat_of(kmd)].eta;
     const double3 pi = ld3(g0);
     const Row R = row_of(L, i);
-    int k = lane;
-    if (kUnroll == 2) {
-      for (; k + G < R.n; k += 2 * G) {
-        const uint32_t e0 = __ldg(R.e + k), e1 = __ldg(R.e + k + G);
-        const uint32_t j0 = nb_index<M>(e0), j1 = nb_index<M>(e1);
-        const double4 a0 = ldg4(&D.G0.p[j0]), b0 = ldg4(&D.G0.p[j1]);
-        const double4 a1 = ldg4(&D.G1.p[j0]), b1 = ldg4(&D.G1.p[j1]);
-        const double4 a2 = ldg4(&D.G2.p[j0]), b2 = ldg4(&D.G2.p[j1]);
-        fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e0, a0, a1, a2, acc, bg, coincident);
-        fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e1, b0, b1, b2, acc, bg, coincident);
-      }
-    }
-    if (kUnroll == 3) {
-      // software pipeline: row entry two iterations ahead, neighbour position record one ahead
-      uint32_t e = k < R.n ? __ldg(R.e + k) : 0u;
-      uint32_t e1 = k + G < R.n ? __ldg(R.e + k + G) : 0u;
-      double4 h0 = k < R.n ? ldg4(&D.G0.p[nb_index<M>(e)]) : make_double4(0, 0, 0, 0);
-      for (; k < R.n; k += G) {
-        const uint32_t j = nb_index<M>(e);
-        const double4 h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
-        const uint32_t e2 = k + 2 * G < R.n ? __ldg(R.e + k + 2 * G) : 0u;
-        const double4 h0n = k + G < R.n ? ldg4(&D.G0.p[nb_index<M>(e1)]) : h0;
-        fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
-        e = e1;
-        e1 = e2;
-        h0 = h0n;
-      }
-    } else if (kUnroll == 4) {
-      // G1/G2 gathered only for pairs inside r_c (saves ~13% of the record wavefronts)
-      uint32_t e = k < R.n ? __ldg(R.e + k) : 0u;
-      for (; k < R.n; k += G) {
-        const uint32_t en = k + G < R.n ? __ldg(R.e + k + G) : 0u;
-        const uint32_t j = nb_index<M>(e);
-        const double4 h0 = ldg4(&D.G0.p[j]);
-        const double3 d = pair_delta<M>(P, pi, ld3(h0), e);
-        const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
-        if (r2 <= P.rc2) {
-          const double4 h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
-          fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
-        }
-        e = en;
-      }
-    } else {
-      // row entry prefetched one iteration ahead (rows stream from HBM: hide the index latency)
-      uint32_t e = k < R.n ? __ldg(R.e + k) : 0u;
-      for (; k < R.n; k += G) {
-        const uint32_t en = k + G < R.n ? __ldg(R.e + k + G) : 0u;
-        const uint32_t j = nb_index<M>(e);
-        const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
-        fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
-        e = en;
-      }
-    }
+    fluid_part<G, M, kTvf, kSingleEta, true>(P, D, I, pi, R.f, 1, R.nf, lane, acc, bg, coincident);
+    fluid_part<G, M, kTvf, kSingleEta, false>(P, D, I, pi, R.b, -1, R.no, lane, acc, bg, coincident);
   }
   acc.x = gsum<G>(acc.x);
   acc.y = gsum<G>(acc.y);
@@ -462,7 +415,8 @@ __device__ __forceinline__ void forces_fluid_group(const DevParams& P, const Par
   D.B4.p[i] = make_double4(f * bg.x, f * bg.y, f * bg.z, 0.0);
 }
 
-// f_r = sum_i -m_i a_ir (fluid neighbours, a_ir from the fluid's view) + contact
+// f_r = sum_i -m_i a_ir over the fluid part of the row (a_ir from the fluid's view)
+//     + contact over the rigid/boundary part
 template <int G, int M, bool kTvf, bool kSingleEta>
 __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                           const uint32_t* __restrict__ list, size_t nlist,
@@ -487,58 +441,60 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
     R.V2 = g0.w;
     const double3 pr = ld3(g0);
     const Row Rw = row_of(L, r);
-    uint32_t en = lane < Rw.n ? __ldg(Rw.e + lane) : 0u;
-    for (int k = lane; k < Rw.n; k += G) {
+    // coupling: fluid part
+    uint32_t en = lane < Rw.nf ? __ldg(Rw.f + lane) : 0u;
+    for (int k = lane; k < Rw.nf; k += G) {
       const uint32_t e = en;
-      en = k + G < Rw.n ? __ldg(Rw.e + k + G) : 0u;
+      en = k + G < Rw.nf ? __ldg(Rw.f + k + G) : 0u;
       const uint32_t j = nb_index<M>(e);
-      const uint32_t kj = D.kmd.p[j];
-      const uint32_t kindj = kind_of(kj);
-      const double4 h0 = ldg4(&D.G0.p[j]);
-      if (kindj == SPHG_FLUID) {
-        // from the fluid's view: d = r_j - r_r (the entry's image is defined for r - j: negate)
-        const double3 dd = pair_delta<M>(P, pr, ld3(h0), e);
-        const double3 d = make_double3(-dd.x, -dd.y, -dd.z);
-        const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
-        if (r2 > P.rc2) continue;
-        if (r2 == 0.0) {
-          coincident = true;
-          continue;
-        }
-        const double4 h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
-        PairSide J;
-        J.u = ld3(h1);
-        J.du = ld3(h2);
-        J.rho = h1.w;
-        J.hrho = 0.5 * h1.w;
-        J.p = h2.w;
-        J.V2 = h0.w;
-        J.eta = P.mat[mat_of(kj)].eta;
-        R.eta = J.eta;  // eta_w := eta_i
-        double3 a = make_double3(0, 0, 0), bgd = make_double3(0, 0, 0);
-        pair_term<kTvf, true>(J, R, d, r2, P, a, bgd);
-        // f_ri = -m_i a_ir = -(V2 term): pair_term accumulates V2*term (a_ir = V2/m_i * term)
-        f.x -= a.x;
-        f.y -= a.y;
-        f.z -= a.z;
-      } else if (kindj == SPHG_BOUNDARY || D.group.p[j] != body) {
-        const double3 d = pair_delta<M>(P, pr, ld3(h0), e);  // r_r - r_j
-        const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
-        if (!(r2 < P.dx * P.dx)) continue;
-        if (r2 == 0.0) {
-          coincident = true;
-          continue;
-        }
-        const double rr = sqrt(r2);
-        const double ri = 1.0 / rr;
-        const double3 e3 = make_double3(d.x * ri, d.y * ri, d.z * ri);
-        const double3 vj = ldpos(&D.V4.p[j]);
-        const double s = P.kc * (rr - P.dx) + P.dc * (e3.x * (vr.x - vj.x) + e3.y * (vr.y - vj.y) + e3.z * (vr.z - vj.z));
-        const double fm = -fmin(0.0, s);
-        f.x += fm * e3.x;
-        f.y += fm * e3.y;
-        f.z += fm * e3.z;
+      const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
+      // from the fluid's view: d = r_j - r_r (the entry's image is defined for r - j: negate)
+      const double3 dd = pair_delta<M>(P, pr, ld3(h0), e);
+      const double3 d = make_double3(-dd.x, -dd.y, -dd.z);
+      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+      if (r2 > P.rc2) continue;
+      if (r2 == 0.0) {
+        coincident = true;
+        continue;
       }
+      PairSide J;
+      J.u = ld3(h1);
+      J.du = ld3(h2);
+      J.rho = h1.w;
+      J.hrho = 0.5 * h1.w;
+      J.p = h2.w;
+      J.V2 = h0.w;
+      J.eta = kSingleEta ? P.mat[P.default_fluid_mat].eta : P.mat[mat_of(__ldg(&D.kmd.p[j]))].eta;
+      R.eta = J.eta;  // eta_w := eta_i
+      double3 a = make_double3(0, 0, 0), bgd = make_double3(0, 0, 0);
+      pair_term<kTvf, true, false>(J, R, d, r2, P, a, bgd);  // j plays i; the rigid side has A = 0
+      // f_ri = -m_i a_ir = -(V2 term): pair_term accumulates V2*term (a_ir = V2/m_i * term)
+      f.x -= a.x;
+      f.y -= a.y;
+      f.z -= a.z;
+    }
+    // contact: rigid particles of other bodies and walls
+    for (int k = lane; k < Rw.no; k += G) {
+      const uint32_t e = __ldg(Rw.b - k);
+      const uint32_t j = nb_index<M>(e);
+      const uint32_t kindj = kind_of(D.kmd.p[j]);
+      if (kindj != SPHG_BOUNDARY && D.group.p[j] == body) continue;
+      const double3 d = pair_delta<M>(P, pr, ldpos(&D.G0.p[j]), e);  // r_r - r_j
+      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+      if (!(r2 < P.dx * P.dx)) continue;
+      if (r2 == 0.0) {
+        coincident = true;
+        continue;
+      }
+      const double rr = sqrt(r2);
+      const double ri = 1.0 / rr;
+      const double3 e3 = make_double3(d.x * ri, d.y * ri, d.z * ri);
+      const double3 vj = ldpos(&D.V4.p[j]);
+      const double s = P.kc * (rr - P.dx) + P.dc * (e3.x * (vr.x - vj.x) + e3.y * (vr.y - vj.y) + e3.z * (vr.z - vj.z));
+      const double fm = -fmin(0.0, s);
+      f.x += fm * e3.x;
+      f.y += fm * e3.y;
+      f.z += fm * e3.z;
     }
   }
   f.x = gsum<G>(f.x);
@@ -566,7 +522,7 @@ __global__ void __launch_bounds__(kBlock) k_count_pairs(const __grid_constant__ 
     const double3 pi = ldpos(&D.G0.p[i]);
     const Row R = row_of(L, (uint32_t)i);
     for (int k = lane; k < R.n; k += G) {
-      const uint32_t e = R.e[k];
+      const uint32_t e = R.at(k);
       const double3 pj = ldpos(&D.G0.p[nb_index<M>(e)]);
       const double3 d = M == kImgNone ? make_double3(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z)
                                       : mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z);
@@ -672,37 +628,9 @@ void launch_extrapolate(Ctx& c) {
 
 template <bool kTvf, bool kSingleEta>
 static void launch_forces_fluid_t(Ctx& c) {
-  if (c.nf && c.unroll_forces == 4)
+  if (c.nf)
     SPHG_G_DISPATCH(c.group_forces,
-                    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 4>
-                                                     <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
-                                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
-  else if (c.nf && c.unroll_forces == 3)
-    SPHG_G_DISPATCH(c.group_forces,
-                    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 3>
-                                                     <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
-                                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
-  else if (c.nf && c.unroll_forces == 2)
-    SPHG_G_DISPATCH(c.group_forces,
-                    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 2>
-                                                     <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
-                                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
-  else if (c.nf && c.persist_blocks > 0) {
-    const size_t nblk = (size_t)c.persist_blocks;
-    const size_t chunk = (c.nf + nblk - 1) / nblk;
-    if (c.persist_threads == 640)
-      SPHG_G_DISPATCH(c.group_forces,
-                      SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid_chunked<G, M, kTvf, kSingleEta, 1, 640>
-                                                       <<<(int)nblk, 640, 0, c.stream>>>(
-                                                           c.P, c.cur, c.nl(), c.fidx.p, c.nf, chunk, c.dflags))));
-    else
-      SPHG_G_DISPATCH(c.group_forces,
-                      SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid_chunked<G, M, kTvf, kSingleEta, 1, 128>
-                                                       <<<(int)nblk, 128, 0, c.stream>>>(
-                                                           c.P, c.cur, c.nl(), c.fidx.p, c.nf, chunk, c.dflags))));
-  } else if (c.nf)
-    SPHG_G_DISPATCH(c.group_forces,
-                    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, 1>
+                    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta>
                                                      <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
   c.launches++;
@@ -710,8 +638,11 @@ static void launch_forces_fluid_t(Ctx& c) {
 
 template <bool kTvf>
 static void launch_forces_rigid_t(Ctx& c) {
-  if (c.nrigid)
+  if (c.nrigid && c.P.single_eta)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGOther, M, kTvf, true><<<blocks_for<kGOther>(c.nrigid), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.dflags)));
+  else if (c.nrigid)
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGOther, M, kTvf, false><<<blocks_for<kGOther>(c.nrigid), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.dflags)));
   c.launches++;
 }

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ Dev
   const bool code = P.img_mode == kImgCode;
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t* row = nbr + i * (size_t)cap;
-  uint32_t count = 0;
+  uint32_t nf = 0, no = 0;
   for (int ox = -1; ox <= 1; ++ox) {
     int64_t qx = cx + ox;
     uint32_t ix = 0;
@@ -136,24 +136,33 @@ __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ Dev
         const uint32_t j0 = cstart[cj], j1 = cend[cj];
         for (uint32_t jb = j0; jb < j1; jb += 32) {
           const uint32_t j = jb + lane;
-          bool hit = false;
-          if (j < j1 && j != i && !(bi && kind_of(kmd[j]) == SPHG_BOUNDARY)) {
-            const double4 pj = G0[j];
-            hit = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) <= P.rv2;  // bit-exact test [P2]
+          bool hit = false, fj = false;
+          if (j < j1 && j != i) {
+            const uint32_t kj = kind_of(kmd[j]);
+            fj = kj == SPHG_FLUID;
+            if (!(bi && kj == SPHG_BOUNDARY)) {
+              const double4 pj = G0[j];
+              hit = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) <= P.rv2;  // bit-exact test [P2]
+            }
           }
-          const uint32_t m = __ballot_sync(0xffffffffu, hit);
-          if (hit) {
-            const uint32_t pos = count + __popc(m & lt);
+          const uint32_t mf = __ballot_sync(0xffffffffu, hit && fj);
+          const uint32_t mo = __ballot_sync(0xffffffffu, hit && !fj);
+          if (hit && fj) {
+            const uint32_t pos = nf + __popc(mf & lt);
             if ((int)pos < cap) row[pos] = j | tag;
+          } else if (hit) {
+            const uint32_t pos = no + __popc(mo & lt);
+            if ((int)pos < cap) row[cap - 1 - pos] = j | tag;
           }
-          count += __popc(m);
+          nf += __popc(mf);
+          no += __popc(mo);
         }
       }
     }
   }
   if (lane == 0) {
-    cnt[i] = count;
-    atomicMax(&fl->max_count, count);
+    cnt[i] = pack_cnt(nf, no);
+    atomicMax(&fl->max_count, nf + no);
   }
 }
 
@@ -198,6 +207,7 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
       bi = kind_of(kmd[i]) == SPHG_BOUNDARY;
       count = hc[i - h0];
     }
+    uint32_t nf = cnt_fluid(count), no = cnt_other(count);
     uint32_t* row = nbr + (size_t)i * cap;
     for (int t = 0; t < ns; ++t) {
       const float4 q = sp[t];
@@ -206,18 +216,23 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
       if (!act || r2 > hi_band) continue;
       const uint32_t e = se[t];
       const uint32_t j = e & emask;
-      if (j == i || (bi && q.w != 0.f)) continue;
+      if (j == i || (bi && q.w == 2.f)) continue;
       bool hit = r2 < lo_band;
       if (!hit) {  // guard band: the pinned exact test
         const double4 pj = G0[j];
         hit = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) <= P.rv2;
       }
       if (hit) {
-        if ((int)count < cap) row[count] = e;
-        ++count;
+        if (q.w == 0.f) {  // fluid neighbours from the front, others from the back
+          if ((int)nf < cap) row[nf] = e;
+          ++nf;
+        } else {
+          if ((int)no < cap) row[cap - 1 - no] = e;
+          ++no;
+        }
       }
     }
-    if (act) hc[i - h0] = count;
+    if (act) hc[i - h0] = pack_cnt(nf, no);
   }
 }
 
@@ -289,7 +304,7 @@ __global__ void __launch_bounds__(32) k_build_nlist_cells(const __grid_constant_
             // the periodic image of the cell: x_j + s sits next to the home cell
             sp[ns + t] = make_float4((float)((pj.x + sx - ox0) * P.inv_h), (float)((pj.y + sy - oy0) * P.inv_h),
                                      (float)((pj.z + sz - oz0) * P.inv_h),
-                                     kind_of(kmd[j]) == SPHG_BOUNDARY ? 1.f : 0.f);
+                                     (float)kind_of(kmd[j]));  // 0 fluid, 1 rigid, 2 boundary
             se[ns + t] = j | tag;
           }
           ns += take;
@@ -312,7 +327,7 @@ __global__ void __launch_bounds__(32) k_build_nlist_cells(const __grid_constant_
     const uint32_t i = h0 + k;
     const uint32_t v = is_ghost(kmd[i]) ? 0u : hc[k];
     cnt[i] = v;
-    mx = max(mx, v);
+    mx = max(mx, cnt_total(v));
   }
   if (mx) atomicMax(&fl->max_count, mx);
 }

@@ -115,11 +115,24 @@ __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevP
       disp2 = r2_exact(mimg3(P, pn.x, pn.y, pn.z, r0.x, r0.y, r0.z));
     }
   }
+  // block-level max, one atomic per block (per-warp atomics on one address serialise in L2)
+  __shared__ double s_d[8], s_u[8];
   disp2 = warp_max(disp2);
   u2 = warp_max(u2);
+  const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
-    atomic_max_pos_double(&fl->max_disp2_bits, disp2);
-    atomic_max_pos_double(&fl->umax2_bits, u2);
+    s_d[w] = disp2;
+    s_u[w] = u2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double d = s_d[0], u = s_u[0];
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      d = fmax(d, s_d[k]);
+      u = fmax(u, s_u[k]);
+    }
+    atomic_max_pos_double(&fl->max_disp2_bits, d);
+    atomic_max_pos_double(&fl->umax2_bits, u);
   }
 }
 

@@ -99,8 +99,10 @@ __global__ void k_solid_target(const __grid_constant__ DevParams P, Particles D,
   double best = 1e300;
   uint32_t bg = 0xffffffffu;
   int tb = -1;
-  for (uint32_t k = 0; k < L.cnt[i]; ++k) {
-    const uint32_t j = entry_index(P, L.nbr[(size_t)i * L.cap + k]);
+  const uint32_t no = cnt_other(L.cnt[i]);  // rigid neighbours live in the non-fluid part of the row
+  const uint32_t* back = L.nbr + (size_t)i * L.cap + L.cap - 1;
+  for (uint32_t k = 0; k < no; ++k) {
+    const uint32_t j = entry_index(P, back[-(int64_t)k]);
     if (kind_of(D.kmd.p[j]) != SPHG_RIGID) continue;
     const double4 pj = D.G0.p[j];
     const double r2 = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z));
@@ -176,8 +178,10 @@ __global__ void k_label_iter(const __grid_constant__ DevParams P, Particles D, s
   const uint32_t body = D.group.p[i];
   const double4 pi = D.G0.p[i];
   uint32_t best = l;
-  for (uint32_t k = 0; k < L.cnt[i]; ++k) {
-    const uint32_t j = entry_index(P, L.nbr[i * L.cap + k]);
+  const uint32_t no = cnt_other(L.cnt[i]);
+  const uint32_t* back = L.nbr + i * L.cap + L.cap - 1;
+  for (uint32_t k = 0; k < no; ++k) {
+    const uint32_t j = entry_index(P, back[-(int64_t)k]);
     if (kind_of(D.kmd.p[j]) != SPHG_RIGID || D.group.p[j] != body) continue;
     const double4 pj = D.G0.p[j];
     if (r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) > adj2) continue;
