@@ -728,8 +728,7 @@ int sphg_get_nlist(sphg_ctx* h, int64_t* offsets, uint32_t* nbr_gid) {
       const int64_t base = offsets[gid[k]];
       const uint32_t* row = rows.data() + k * (size_t)c.cap;
       const uint32_t nf = cnt_fluid(cnt[k]), no = cnt_other(cnt[k]);
-      for (uint32_t q = 0; q < nf; ++q) nbr_gid[base + q] = gid[row[q] & mask];
-      for (uint32_t q = 0; q < no; ++q) nbr_gid[base + nf + q] = gid[row[c.cap - 1 - q] & mask];
+      for (uint32_t q = 0; q < nf + no; ++q) nbr_gid[base + q] = gid[row[q] & mask];
       std::sort(nbr_gid + base, nbr_gid + base + nf + no);
     }
     return SPHG_OK;

@@ -169,8 +169,17 @@ __device__ __forceinline__ double3 pair_delta(const DevParams& P, double3 a, dou
   return d;
 }
 
-// Kind-partitioned rows: fluid neighbours fill row i from the front, rigid and boundary
-// neighbours from the back; cnt[i] packs both counts (fluid | non-fluid << 16).
+// Kind-partitioned rows: while building, fluid neighbours fill row i from the front and rigid /
+// boundary neighbours from the back; the back segment is then moved next to the front one, so a
+// row is [fluid (nf) | non-fluid (no)] contiguous.  cnt[i] packs both counts (nf | no << 16).
+// Move: with lo = max(nf + no, cap - no), entries [lo, cap) go to [nf, nf + cap - lo); source and
+// destination are disjoint, entries already inside [nf, nf + no) stay.  Order within the non-fluid
+// segment is not preserved (rows are sets).
+__device__ __forceinline__ void compact_row(uint32_t* row, uint32_t nf, uint32_t no, int cap, int lane, int width) {
+  if ((int)(nf + no) > cap) return;  // overflow: the caller rebuilds with a larger cap
+  const uint32_t lo = max(nf + no, (uint32_t)cap - no);
+  for (uint32_t m = lane; m < (uint32_t)cap - lo; m += width) row[nf + m] = row[lo + m];
+}
 __host__ __device__ __forceinline__ uint32_t cnt_fluid(uint32_t c) { return c & 0xffffu; }
 __host__ __device__ __forceinline__ uint32_t cnt_other(uint32_t c) { return c >> 16; }
 __host__ __device__ __forceinline__ uint32_t cnt_total(uint32_t c) { return (c & 0xffffu) + (c >> 16); }

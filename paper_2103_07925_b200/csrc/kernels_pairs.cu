@@ -44,20 +44,19 @@ __device__ __forceinline__ double3 ldpos(const double4* p) { return ld3(ld4(p));
 __device__ __forceinline__ Quat body_q(const sphg_body& b) { return {b.q[0], b.q[1], b.q[2], b.q[3]}; }
 __device__ __forceinline__ double3 bv(const double* p) { return make_double3(p[0], p[1], p[2]); }
 
-// A Verlet row: fluid neighbours at f[0..nf), rigid/boundary neighbours at b[0], b[-1], ... (no).
+// A Verlet row: fluid neighbours f[0..nf), rigid/boundary neighbours b[0..no) with b = f + nf.
 struct Row {
   const uint32_t* f;
   const uint32_t* b;
   int nf, no, n;
-  // unified index over both parts (kernels that treat every neighbour alike)
-  __device__ __forceinline__ uint32_t at(int k) const { return k < nf ? __ldg(f + k) : __ldg(b - (k - nf)); }
+  __device__ __forceinline__ uint32_t at(int k) const { return __ldg(f + k); }
 };
 __device__ __forceinline__ Row row_of(const NbrList& L, uint32_t i) {
   const uint32_t c = L.cnt[i];
   const uint32_t* r = L.nbr + (size_t)i * L.cap;
   Row R;
   R.f = r;
-  R.b = r + L.cap - 1;
+  R.b = r + cnt_fluid(c);
   R.nf = (int)cnt_fluid(c);
   R.no = (int)cnt_other(c);
   R.n = R.nf + R.no;
@@ -346,7 +345,8 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
   if (kSingleEta || !kJFluid) {
     J.eta = I.eta;
   } else {
-    J.eta = P.mat[mat_of(__ldg(&D.kmd.p[nb_index<M>(e)]))].eta;
+    const uint32_t kj = __ldg(&D.kmd.p[nb_index<M>(e)]);
+    J.eta = kind_of(kj) == SPHG_FLUID ? P.mat[mat_of(kj)].eta : I.eta;  // eta_w := eta_i [P7]
   }
   pair_term<kTvf, kSingleEta, kJFluid>(I, J, d, r2, P, acc, bg);
 }
@@ -393,8 +393,9 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
     I.eta = P.mat[mat_of(kmd)].eta;
     const double3 pi = ld3(g0);
     const Row R = row_of(L, i);
-    fluid_part<G, M, kTvf, kSingleEta, true>(P, D, I, pi, R.f, 1, R.nf, lane, acc, bg, coincident);
-    fluid_part<G, M, kTvf, kSingleEta, false>(P, D, I, pi, R.b, -1, R.no, lane, acc, bg, coincident);
+    // one pass over the whole contiguous row: wall/rigid records carry du = 0 (A_w = 0) and, with
+    // several viscosities, fluid_pair looks up eta_j by kind (eta_w := eta_i)
+    fluid_part<G, M, kTvf, kSingleEta, true>(P, D, I, pi, R.f, 1, R.n, lane, acc, bg, coincident);
   }
   acc.x = gsum<G>(acc.x);
   acc.y = gsum<G>(acc.y);
@@ -475,7 +476,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
     }
     // contact: rigid particles of other bodies and walls
     for (int k = lane; k < Rw.no; k += G) {
-      const uint32_t e = __ldg(Rw.b - k);
+      const uint32_t e = __ldg(Rw.b + k);
       const uint32_t j = nb_index<M>(e);
       const uint32_t kindj = kind_of(D.kmd.p[j]);
       if (kindj != SPHG_BOUNDARY && D.group.p[j] == body) continue;

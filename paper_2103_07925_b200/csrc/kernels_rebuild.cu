@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ Dev
       }
     }
   }
+  __syncwarp();
+  compact_row(row, nf, no, cap, lane, 32);
   if (lane == 0) {
     cnt[i] = pack_cnt(nf, no);
     atomicMax(&fl->max_count, nf + no);
@@ -326,6 +328,7 @@ __global__ void __launch_bounds__(32) k_build_nlist_cells(const __grid_constant_
   for (uint32_t k = lane; k < h1 - h0; k += 32) {
     const uint32_t i = h0 + k;
     const uint32_t v = is_ghost(kmd[i]) ? 0u : hc[k];
+    if (v) compact_row(nbr + (size_t)i * cap, cnt_fluid(v), cnt_other(v), cap, 0, 1);
     cnt[i] = v;
     mx = max(mx, cnt_total(v));
   }

@@ -100,9 +100,9 @@ __global__ void k_solid_target(const __grid_constant__ DevParams P, Particles D,
   uint32_t bg = 0xffffffffu;
   int tb = -1;
   const uint32_t no = cnt_other(L.cnt[i]);  // rigid neighbours live in the non-fluid part of the row
-  const uint32_t* back = L.nbr + (size_t)i * L.cap + L.cap - 1;
+  const uint32_t* back = L.nbr + (size_t)i * L.cap + cnt_fluid(L.cnt[i]);
   for (uint32_t k = 0; k < no; ++k) {
-    const uint32_t j = entry_index(P, back[-(int64_t)k]);
+    const uint32_t j = entry_index(P, back[k]);
     if (kind_of(D.kmd.p[j]) != SPHG_RIGID) continue;
     const double4 pj = D.G0.p[j];
     const double r2 = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z));
@@ -179,9 +179,9 @@ __global__ void k_label_iter(const __grid_constant__ DevParams P, Particles D, s
   const double4 pi = D.G0.p[i];
   uint32_t best = l;
   const uint32_t no = cnt_other(L.cnt[i]);
-  const uint32_t* back = L.nbr + i * L.cap + L.cap - 1;
+  const uint32_t* back = L.nbr + i * L.cap + cnt_fluid(L.cnt[i]);
   for (uint32_t k = 0; k < no; ++k) {
-    const uint32_t j = entry_index(P, back[-(int64_t)k]);
+    const uint32_t j = entry_index(P, back[k]);
     if (kind_of(D.kmd.p[j]) != SPHG_RIGID || D.group.p[j] != body) continue;
     const double4 pj = D.G0.p[j];
     if (r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) > adj2) continue;
@@ -393,6 +393,8 @@ int launch_transitions(Ctx& c) {
   old.free();
   c.n_melt += nmelt;
   c.n_solid += nsolid;
+  // kinds changed: the rows' fluid / non-fluid partition is stale -> rebuild before the next evaluation
+  c.built = false;
   return 0;
 }
 
