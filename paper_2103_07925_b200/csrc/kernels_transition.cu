@@ -99,10 +99,11 @@ __global__ void k_solid_target(const __grid_constant__ DevParams P, Particles D,
   double best = 1e300;
   uint32_t bg = 0xffffffffu;
   int tb = -1;
-  const uint32_t no = cnt_other(L.cnt[i]);  // rigid neighbours live in the non-fluid part of the row
-  const uint32_t* back = L.nbr + (size_t)i * L.cap + cnt_fluid(L.cnt[i]);
-  for (uint32_t k = 0; k < no; ++k) {
-    const uint32_t j = entry_index(P, back[k]);
+  // whole row: mid-batch the kinds no longer match the rows' fluid / non-fluid partition
+  const uint32_t nn = cnt_total(L.cnt[i]);
+  const uint32_t* row = L.nbr + (size_t)i * L.cap;
+  for (uint32_t k = 0; k < nn; ++k) {
+    const uint32_t j = entry_index(P, row[k]);
     if (kind_of(D.kmd.p[j]) != SPHG_RIGID) continue;
     const double4 pj = D.G0.p[j];
     const double r2 = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z));
@@ -178,10 +179,10 @@ __global__ void k_label_iter(const __grid_constant__ DevParams P, Particles D, s
   const uint32_t body = D.group.p[i];
   const double4 pi = D.G0.p[i];
   uint32_t best = l;
-  const uint32_t no = cnt_other(L.cnt[i]);
-  const uint32_t* back = L.nbr + i * L.cap + cnt_fluid(L.cnt[i]);
-  for (uint32_t k = 0; k < no; ++k) {
-    const uint32_t j = entry_index(P, back[k]);
+  const uint32_t nn = cnt_total(L.cnt[i]);  // whole row (see k_solid_target)
+  const uint32_t* row = L.nbr + i * L.cap;
+  for (uint32_t k = 0; k < nn; ++k) {
+    const uint32_t j = entry_index(P, row[k]);
     if (kind_of(D.kmd.p[j]) != SPHG_RIGID || D.group.p[j] != body) continue;
     const double4 pj = D.G0.p[j];
     if (r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) > adj2) continue;
