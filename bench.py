@@ -225,10 +225,19 @@ def run_sph(args):
     achieved_tf = flops / t_ff / 1e12
     fp64_peak = peaks.get("fp64_tflops")
     hbm_achieved = FORCES_BYTES_PER_FLUID * nf / t_ff / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r01_ncu_full_64m.json")
+    if os.path.exists(tp) and n == 64000000:
+        for k in json.load(open(tp)):
+            if "k_forces_fluid" in k["kernel"]:
+                rd = float(k["dram__bytes_read.sum"].split()[0]) * 1e9
+                wr = float(k["dram__bytes_write.sum"].split()[0]) * 1e9
+                traffic = {"bytes_per_launch": rd + wr, "source": "profiles/r01_ncu_full_64m.json (ncu --set full)",
+                           "note": "rows (~28 GB) + neighbour records re-read past L2; the CSM bytes model is 8.8 GB"}
     roofline = {"bound": "fp64", "kernel": "k_forces_fluid (momentum_rhs + TVF)",
                 "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": (achieved_tf / fp64_peak) if fp64_peak else None,
-                "traffic": None, "launch_ms": stage_ms["forces_fluid"],
+                "traffic": traffic, "launch_ms": stage_ms["forces_fluid"],
                 "flops_per_launch": flops, "flops_model": "91 flop per interacting fluid pair (SURVEY 8(d))",
                 "peak_source": "profiles/fp64_peak.json (DFMA microbenchmark, tools/fp64_peak.cu)",
                 "hbm": {"achieved": hbm_achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -251,22 +260,30 @@ def run_sph(args):
             "wall_s_timed": wall, "gpu_launches": int(launches),
             "rebuilds_in_timed_region": int(st1.rebuilds - st0.rebuilds),
             "clocks": clk.summary(), "gen_s": t_gen}
-    # e2e: through the public API with host buffers each step (upload -> step -> download)
+    # e2e: through the public API with host buffers, every step: H2D of the step's kinematic input
+    # (positions + velocities from pinned host memory, Simulation.upload_state) -> step(1) ->
+    # D2H of the step's fields (positions, velocities, density, pressure) into the ParticleStore
     if not args.no_e2e and args.e2e_steps > 0:
         store = sc.store
-        fields = None
-        sim.download(store)
-        nbytes = store_bytes(store)
+        fields = ("pos", "vel", "density", "pressure")
+        sim.download(store, fields=fields + ("kind", "material", "owner", "group"))
+        pin_pos = torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy()
+        pin_vel = torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy()
+        pin_pos[:] = store.pos
+        pin_vel[:] = store.vel
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            sim.upload(store, sc.bodies)
+            sim.upload_state(pin_pos, pin_vel)
             sim.step(1)
-            store, _ = sim.download(store)
+            sim.download(store, fields=fields)
         e2e_s = time.perf_counter() - t0
-        line["e2e"] = {"value": n * args.e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(nbytes),
-                       "d2h_bytes_per_step": int(nbytes), "steps": args.e2e_steps,
-                       "path": "Simulation.upload(ParticleStore) -> step(1) -> download(ParticleStore), pinned staging"}
+        # device arrays behind the requested fields: G0, V4, G1, G2 records (32 B each) + kmd + gid
+        d2h = n * (4 * 32 + 4 + 4)
+        line["e2e"] = {"value": n * args.e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(48 * n),
+                       "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
+                       "path": "Simulation.upload_state(pos, vel from pinned host) -> step(1) -> "
+                               "download(pos, vel, density, pressure); host wall clock"}
     if not args.no_cpu_baseline and rank == 0:
         line["cpu_baseline"] = cpu_baseline(args.cpu_nside, args.spheres, args.nside)
     sim.close()

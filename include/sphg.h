@@ -174,7 +174,12 @@ int sphg_initialize(sphg_ctx* ctx);
 int sphg_step(sphg_ctx* ctx, int nsteps);
 /* One stage (parity hook; also the per-op evaluator API of SPEC:243-363). */
 int sphg_run_stage(sphg_ctx* ctx, int stage);
-/* Copies the state back in gid order into caller-allocated buffers (NULL fields skipped). */
+/* Warm kinematic update between steps (same store, gid order): positions and velocities only,
+ * e.g. a host-side coupling that moves particles.  Keeps the device order and the Verlet rows
+ * (rebuilt automatically if the update moved a particle beyond the skin). */
+int sphg_upload_state(sphg_ctx* ctx, const double* pos, const double* vel, size_t n);
+/* Copies the state back in gid order into caller-allocated buffers (NULL fields skipped; only the
+ * device arrays behind the requested fields cross PCIe). */
 int sphg_download(sphg_ctx* ctx, sphg_soa* out, sphg_body* bodies_out, size_t* n_bodies_inout);
 /* Cell of every particle (by gid) and the canonical (cell, gid) order. */
 int sphg_get_cells(sphg_ctx* ctx, int64_t* cell_of_gid, uint32_t* sorted_gid);

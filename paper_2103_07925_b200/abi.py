@@ -129,6 +129,7 @@ def declare(lib, prefix):
         "body_apply_totals": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "max_displacement": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "halo_doubles": (C.c_int, [C.c_int]),
+        "upload_state": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_size_t]),
     }
     for name, (res, args) in list(sig.items()) + list(optional.items()):
         fn = getattr(lib, prefix + name, None)

@@ -429,8 +429,18 @@ void stage_upload(Ctx& c, const sphg_soa* s, Particles& dst) {
   }
 }
 
+struct Need {
+  bool G0, G1, G2, V4;
+};
+
 void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
   ensure_staging(c);
+  Need need;
+  need.G0 = o->pos != nullptr;
+  need.V4 = o->vel || o->vel_adv || o->mass;
+  need.G1 = (o->vel && mid_step) || o->vel_adv || o->wall_velocity || o->density;
+  need.G2 = o->vel_adv || o->pressure || o->wall_pressure;
+  size_t bytes_d2h = 0;
   const size_t n = c.n;
   const size_t slot_bytes = kChunk * (kPackBytes + 4);
   cudaStream_t st = c.stream;
@@ -453,17 +463,19 @@ void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
       const uint32_t kmd = S.kmd[q];
       const uint32_t kind = kind_of(kmd), mat = mat_of(kmd);
       const bool fl = kind == SPHG_FLUID;
-      const double4 G0 = S.G0[q], G1 = S.G1[q], G2 = S.G2[q], V4 = S.V4[q];
+      const double4 z4 = make_double4(0, 0, 0, 0);
+      const double4 G0 = need.G0 ? S.G0[q] : z4, G1 = need.G1 ? S.G1[q] : z4, G2 = need.G2 ? S.G2[q] : z4,
+                    V4 = need.V4 ? S.V4[q] : z4;
       put(o->pos, g, G0.x, G0.y, G0.z);
       if (fl && mid_step) put(o->vel, g, G1.x, G1.y, G1.z);
       else put(o->vel, g, V4.x, V4.y, V4.z);
       if (fl) put(o->vel_adv, g, G1.x + G2.x, G1.y + G2.y, G1.z + G2.z);
       else if (kind == SPHG_RIGID) put(o->vel_adv, g, V4.x, V4.y, V4.z);
       else put(o->vel_adv, g, 0, 0, 0);
-      put(o->acc, g, S.A4[q].x, S.A4[q].y, S.A4[q].z);
-      put(o->acc_bg, g, S.B4[q].x, S.B4[q].y, S.B4[q].z);
-      put(o->force, g, S.F4[q].x, S.F4[q].y, S.F4[q].z);
-      put(o->body_frame_pos, g, S.X4[q].x, S.X4[q].y, S.X4[q].z);
+      if (o->acc) put(o->acc, g, S.A4[q].x, S.A4[q].y, S.A4[q].z);
+      if (o->acc_bg) put(o->acc_bg, g, S.B4[q].x, S.B4[q].y, S.B4[q].z);
+      if (o->force) put(o->force, g, S.F4[q].x, S.F4[q].y, S.F4[q].z);
+      if (o->body_frame_pos) put(o->body_frame_pos, g, S.X4[q].x, S.X4[q].y, S.X4[q].z);
       if (fl) put(o->wall_velocity, g, 0, 0, 0);
       else put(o->wall_velocity, g, G1.x, G1.y, G1.z);
       if (o->density) o->density[g] = kind == SPHG_RIGID ? c.P.mat[mat].rho0 : G1.w;
@@ -483,11 +495,23 @@ void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
     const size_t m = std::min(kChunk, n - k0);
     Slot S = slot_view(static_cast<char*>(c.hstage) + slot * slot_bytes);
     SPHG_CUDA_CHECK(cudaEventSynchronize(c.slot_ev[slot]));
-    d2h(S.G0, c.cur.G0.p + k0, m, st); d2h(S.G1, c.cur.G1.p + k0, m, st); d2h(S.G2, c.cur.G2.p + k0, m, st);
-    d2h(S.V4, c.cur.V4.p + k0, m, st); d2h(S.A4, c.cur.A4.p + k0, m, st); d2h(S.B4, c.cur.B4.p + k0, m, st);
-    d2h(S.F4, c.cur.F4.p + k0, m, st); d2h(S.X4, c.cur.X4.p + k0, m, st); d2h(S.H2, c.cur.H2.p + k0, m, st);
-    d2h(S.dT, c.cur.dTdt.p + k0, m, st); d2h(S.ps, c.cur.p_static.p + k0, m, st);
-    d2h(S.kmd, c.cur.kmd.p + k0, m, st); d2h(S.grp, c.cur.group.p + k0, m, st); d2h(S.gid, c.cur.gid.p + k0, m, st);
+    if (need.G0) d2h(S.G0, c.cur.G0.p + k0, m, st);
+    if (need.G1) d2h(S.G1, c.cur.G1.p + k0, m, st);
+    if (need.G2) d2h(S.G2, c.cur.G2.p + k0, m, st);
+    if (need.V4) d2h(S.V4, c.cur.V4.p + k0, m, st);
+    if (o->acc) d2h(S.A4, c.cur.A4.p + k0, m, st);
+    if (o->acc_bg) d2h(S.B4, c.cur.B4.p + k0, m, st);
+    if (o->force) d2h(S.F4, c.cur.F4.p + k0, m, st);
+    if (o->body_frame_pos) d2h(S.X4, c.cur.X4.p + k0, m, st);
+    if (o->temperature) d2h(S.H2, c.cur.H2.p + k0, m, st);
+    if (o->dT_dt) d2h(S.dT, c.cur.dTdt.p + k0, m, st);
+    if (o->pressure) d2h(S.ps, c.cur.p_static.p + k0, m, st);
+    d2h(S.kmd, c.cur.kmd.p + k0, m, st);
+    if (o->group) d2h(S.grp, c.cur.group.p + k0, m, st);
+    d2h(S.gid, c.cur.gid.p + k0, m, st);
+    bytes_d2h += m * (4 + 4 + (need.G0 + need.G1 + need.G2 + need.V4 + !!o->acc + !!o->acc_bg + !!o->force +
+                               !!o->body_frame_pos) * 32 + !!o->temperature * 16 + (!!o->dT_dt + !!o->pressure) * 8 +
+                      !!o->group * 4);
     SPHG_CUDA_CHECK(cudaEventRecord(c.slot_ev[slot], st));
     if (prev_slot >= 0) unpack(prev_slot, prev_k0, prev_m);  // overlaps with the copy just issued
     prev_slot = slot;
@@ -496,6 +520,7 @@ void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
   }
   if (prev_slot >= 0) unpack(prev_slot, prev_k0, prev_m);
   SPHG_CUDA_CHECK(cudaStreamSynchronize(st));
+  c.last_d2h_bytes = bytes_d2h;
 }
 
 }  // namespace
@@ -609,6 +634,27 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     if (c.built) launch_rigid_index(c);  // kinds / bodies may have changed
     SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     c.have_state = true;
+    h->mid_step = false;
+    return SPHG_OK;
+  });
+}
+
+int sphg_upload_state(sphg_ctx* h, const double* pos, const double* vel, size_t n) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    SPHG_CUDA_CHECK(cudaSetDevice(c.device));
+    if (!c.have_state || n != c.n) return fail(h, SPHG_ERR_RUNTIME, "upload_state: store size mismatch (upload first)");
+    if (n == 0) return SPHG_OK;
+    if (!c.built) {  // device order is gid order until the first rebuild
+      build_idx_of_gid(c);
+    }
+    c.state_buf.alloc(6 * n);
+    if (pos) h2d(c.state_buf.p, pos, 3 * n, c.stream);
+    if (vel) h2d(c.state_buf.p + 3 * n, vel, 3 * n, c.stream);
+    scatter_state(c, pos ? c.state_buf.p : nullptr, vel ? c.state_buf.p + 3 * n : nullptr);
+    c.last_h2d_bytes = (pos ? 24 : 0) * n + (vel ? 24 : 0) * n;
+    if (c.built && pos && displacement_exceeds(c)) c.built = false;
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     h->mid_step = false;
     return SPHG_OK;
   });

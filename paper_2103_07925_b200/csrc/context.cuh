@@ -123,6 +123,8 @@ struct Ctx {
   size_t halo_n[SPHG_MAX_HALO_SLOTS] = {0};
   size_t nghost = 0;
   DBuf<double> body_buf;
+  DBuf<double> state_buf;  // upload_state staging (device)
+  size_t last_h2d_bytes = 0, last_d2h_bytes = 0;
 };
 
 // ------------------------------------------------------------ launchers
@@ -154,6 +156,7 @@ void launch_mass(Ctx& c, const uint32_t* body_mask);
 void gather_by_gid(Ctx& c);          // cur[k] <- alt[gid[k]] for every field but gid/R4
 bool displacement_exceeds(Ctx& c);   // max |r - r_ref| > half skin (syncs)
 void iota_gid(Ctx& c);
+void scatter_state(Ctx& c, const double* pos, const double* vel);  // gid-ordered xyz -> G0.xyz / V4.xyz
 void count_pairs(Ctx& c, int64_t out[4]);
 void build_idx_of_gid(Ctx& c);
 void halo_pack(Ctx& c, int phase, int slot, double* buf);

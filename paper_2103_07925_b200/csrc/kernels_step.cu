@@ -462,7 +462,21 @@ __global__ void k_apply_totals(const __grid_constant__ DevParams P, sphg_body* _
   }
 }
 
+__global__ void k_scatter_state(Particles D, size_t n, const uint32_t* __restrict__ idx, const double* __restrict__ pos,
+                                const double* __restrict__ vel) {
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  const uint32_t k = idx[g];
+  if (pos) stpos(&D.G0.p[k], make_double3(pos[3 * g], pos[3 * g + 1], pos[3 * g + 2]));
+  if (vel) stpos(&D.V4.p[k], make_double3(vel[3 * g], vel[3 * g + 1], vel[3 * g + 2]));
+}
+
 }  // namespace
+
+void scatter_state(Ctx& c, const double* pos, const double* vel) {
+  k_scatter_state<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.cur, c.n, c.idx_of_gid.p, pos, vel);
+  c.launches++;
+}
 
 void build_idx_of_gid(Ctx& c) {
   if (c.n == 0) return;

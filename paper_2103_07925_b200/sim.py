@@ -91,6 +91,15 @@ class Simulation:
         self._check(self._fn("upload")(self._h, C.byref(soa), bodies_ptr(bodies), nb), "upload")
         self.n = store.n
 
+    def upload_state(self, pos, vel):
+        """Warm kinematic update (positions, velocities; gid order, (n,3) float64). Either may be None."""
+        dp = C.POINTER(C.c_double)
+        pp = None if pos is None else np.ascontiguousarray(pos, np.float64)
+        vv = None if vel is None else np.ascontiguousarray(vel, np.float64)
+        self._check(self._fn("upload_state")(self._h, pp.ctypes.data_as(dp) if pp is not None else None,
+                                             vv.ctypes.data_as(dp) if vv is not None else None, self.n),
+                    "upload_state")
+
     def num_bodies(self):
         nb = C.c_size_t(0)
         self._check(self._fn("num_bodies")(self._h, C.byref(nb)), "num_bodies")

@@ -212,3 +212,24 @@ def test_nlist_dense_cells_fallback(Oracle):
     orc.build_pairs()
     assert np.array_equal(sim.get_cells()[0], orc.get_cells()[0])
     assert np.array_equal(sim.get_nlist()[1], orc.get_nlist()[1])
+
+
+def test_upload_state_warm_update(Oracle):
+    """sphg_upload_state (kinematic host update between steps) == a full upload of the same state."""
+    sc = CASES["c1_small"]()
+    a = Simulation(sc.params)
+    a.upload(sc.store, sc.bodies)
+    a.initialize()
+    a.step(2)
+    s, b = a.download()
+    s.vel[:] *= 0.5  # host-side intervention on the velocities
+    a.upload_state(s.pos, s.vel)
+    a.step(1)
+    ref = Simulation(sc.params)
+    ref.upload(s, b)
+    ref.step(1)  # cold path: full upload of the same state (a^n carried in the store)
+    ga, _ = a.download()
+    gr, _ = ref.download()
+    from tests.helpers import vec_err
+    assert vec_err(ga.pos, gr.pos, 0.016, 1e-14) <= 1
+    assert vec_err(ga.vel, gr.vel, 1e-3, 1e-9) <= 1
