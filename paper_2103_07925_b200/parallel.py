@@ -201,6 +201,7 @@ class DistributedSimulation:
                                    mk(len(s), self.dev) if staged else None, mk(len(rcv), self.dev) if staged else None)
             sb, rb, sbx, rbx = self._bufs[key]
             if len(s):
+                # halo_pack is synchronous on the engine's stream: the send below sees the packed data
                 e._check(e._fn("halo_pack")(e._h, phase, 2 * k, sb.data_ptr()), "halo_pack")
                 if sbx is not None:
                     sbx.copy_(sb)
@@ -211,6 +212,10 @@ class DistributedSimulation:
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+            if self.dev.type == "cuda":
+                # NCCL's wait() only orders torch's current stream; the engine unpacks on its own
+                # stream, so the host waits for the receives to land first
+                torch.cuda.current_stream(self.dev).synchronize()
         for k, rb, rbx in recv:
             if rbx is not None:
                 rb.copy_(rbx)
