@@ -211,25 +211,41 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
     }
     uint32_t nf = cnt_fluid(count), no = cnt_other(count);
     uint32_t* row = nbr + (size_t)i * cap;
-    for (int t = 0; t < ns; ++t) {
-      const float4 q = sp[t];
-      const float dx = xi - q.x, dy = yi - q.y, dz = zi - q.z;
-      const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      if (!act || r2 > hi_band) continue;
-      const uint32_t e = se[t];
-      const uint32_t j = e & emask;
-      if (j == i || (bi && q.w == 2.f)) continue;
-      bool hit = r2 < lo_band;
-      if (!hit) {  // guard band: the pinned exact test
-        const double4 pj = G0[j];
-        hit = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) <= P.rv2;
+    uint32_t* back = row + cap - 1;
+    // two phases per chunk of 32 staged candidates: (1) fp32 tests into a per-lane bit mask
+    // (fully unrolled; the stage is padded with far-away dummies), (2) each lane walks only its
+    // own set bits.  Hits are ~15% of candidates, so phase 2 runs ~5 times per 32 per lane.
+    for (int tb = 0; tb < ns; tb += 32) {
+      uint32_t m = 0;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const float4 q = sp[tb + u];
+        const float dx = xi - q.x, dy = yi - q.y, dz = zi - q.z;
+        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        m |= (r2 <= hi_band) ? (1u << u) : 0u;
       }
-      if (hit) {
+      if (!act) m = 0;
+      while (m) {
+        const int u = __ffs(m) - 1;
+        m &= m - 1;
+        const int t = tb + u;
+        const uint32_t e = se[t];
+        const float4 q = sp[t];
+        const uint32_t j = e & emask;
+        if (j == i || (bi && q.w == 2.f)) continue;
+        const float dx = xi - q.x, dy = yi - q.y, dz = zi - q.z;
+        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        bool hit = r2 < lo_band;
+        if (!hit) {  // guard band: the pinned exact test
+          const double4 pj = G0[j];
+          hit = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) <= P.rv2;
+        }
+        if (!hit) continue;
         if (q.w == 0.f) {  // fluid neighbours from the front, others from the back
           if ((int)nf < cap) row[nf] = e;
           ++nf;
         } else {
-          if ((int)no < cap) row[cap - 1 - no] = e;
+          if ((int)no < cap) back[-(int)no] = e;
           ++no;
         }
       }
@@ -322,7 +338,15 @@ __global__ void __launch_bounds__(32) k_build_nlist_cells(const __grid_constant_
     }
   }
   __syncwarp();
-  if (ns) build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, sp, se, ns, hc, emask);
+  if (ns) {
+    const int padded = (ns + 31) & ~31;  // far-away dummies fail every test
+    for (int t = ns + lane; t < padded; t += 32) {
+      sp[t] = make_float4(1e30f, 1e30f, 1e30f, 0.f);
+      se[t] = 0u;
+    }
+    __syncwarp();
+    build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, sp, se, padded, hc, emask);
+  }
   __syncwarp();
   uint32_t mx = 0;
   for (uint32_t k = lane; k < h1 - h0; k += 32) {
