@@ -384,10 +384,87 @@ def closed_box_melting(nside=64, dx=1e-3, dt=5e-6, seed=2107, n_grid=3, r_range=
     return Scenario(name, params, s, bodies, steps, info)
 
 
+def two_phase_with_bodies(nside=128, dx=1e-3, dt=None, seed=2111, n_bodies=200, r_range=(2.0, 4.0),
+                          liquid_frac=0.6, rho_l=1000.0, rho_g=1.0, eta_l=1e-3, eta_g=1e-5, c=20.0,
+                          rho_s=1200.0, g=-9.81, kc=10.0, zeta=0.1, jitter=0.05, name="c3", steps=200):
+    """BASELINE configs[2] (C3): closed box, lower liquid_frac liquid (rho 1000, eta 1e-3), upper gas
+    (rho 1, eta 1e-5), shared background pressure, rigid cubes and spheres (50/50 by seed, edge or
+    diameter 4-8 dx -> half-size r_range) of density 1200 placed in the liquid, gravity, isothermal.
+    Pinned: equal reference pressures p0 = rho c^2 in both phases (c_liquid = c,
+    c_gas = c sqrt(rho_l / rho_g)), shared p_b = p0, dt = 0.2 h / c_gas, 3-layer walls, k_c = 10.
+    Exercises the multi-viscosity (eta~ harmonic mean) and multi-EOS (dominant wall material) paths."""
+    c_g = c * math.sqrt(rho_l / rho_g)
+    if dt is None:
+        dt = 0.2 * dx / c_g
+    L = nside * dx
+    nl = 3
+    lo = (-nl * dx,) * 3
+    hi = (L + nl * dx,) * 3
+    pb = rho_l * c * c
+    grav = (0.0, 0.0, g)
+    mats = [material(rho_l, nu=eta_l / rho_l, c=c, pb=pb, g=grav),   # 0 liquid
+            material(rho_g, nu=eta_g / rho_g, c=c_g, pb=pb, g=grav), # 1 gas
+            material(rho_s, c=0.0, g=grav),                            # 2 solid
+            material(rho_l, c=c)]                                       # 3 wall
+    m_r = rho_s * dx ** 3
+    params = _params(dx, dt, lo, hi, (0, 0, 0), mats, kc=kc, dc=damping_from_ratio(zeta, kc, m_r))
+    fl = lattice_box((0.0,) * 3, (L,) * 3, dx)
+    wl = lattice_box(lo, hi, dx)
+    wl = wl[np.any((wl < 0.0) | (wl > L), axis=1)]
+    nf, nw = len(fl), len(wl)
+    # bodies: centres in the liquid, non-overlapping; even ids spheres, odd ids cubes
+    zmax = liquid_frac * L
+    centers, radii = place_spheres(seed, n_bodies, (0.0, 0.0, 0.0), (L, L, zmax), r_range[0], r_range[1], dx,
+                                   periodic=False)
+    owner = np.full(nf, -1, np.int64)
+    n1 = nside
+    for k, (cc, R) in enumerate(zip(centers, radii)):
+        d = fl - cc
+        if k % 2 == 0:
+            inside = ((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]) <= R * R
+        else:
+            inside = np.all(np.abs(d) <= R, axis=1)  # axis-aligned cube (box_region, lattice.hpp:22-25)
+        owner[inside & (owner < 0)] = k
+    n = nf + nw
+    s = ParticleStore(n)
+    u = splitmix_u01(seed, 0, np.arange(3 * nf, dtype=np.uint64)).reshape(nf, 3)
+    s.pos[:nf] = fl + (2.0 * u - 1.0) * (jitter * dx)
+    s.pos[nf:] = wl
+    rig = np.zeros(n, bool)
+    rig[:nf] = owner >= 0
+    gas = np.zeros(n, bool)
+    gas[:nf] = fl[:, 2] >= zmax
+    s.kind[:nf] = abi.FLUID
+    s.kind[nf:] = abi.BOUNDARY
+    s.kind[rig] = abi.RIGID
+    s.group[rig] = owner[owner >= 0].astype(np.uint32)
+    s.material[:nf] = 0
+    s.material[gas & ~rig] = 1
+    s.material[rig] = 2
+    s.material[nf:] = 3
+    rho = np.where(gas, rho_g, rho_l)
+    rho[rig] = rho_s
+    rho[nf:] = rho_l
+    s.mass[:] = rho * dx ** 3
+    s.density[:] = rho
+    bodies = empty_bodies(len(centers))
+    bodies["material"] = 2
+    body_quantities(s, bodies, params)
+    _finish(s, bodies)
+    info = dict(n=n, n_fluid=int((s.kind == abi.FLUID).sum()), n_rigid=int(rig.sum()), n_boundary=nw,
+                n_bodies=len(centers), rigid_fraction=float(rig.mean()), n_gas=int((gas & ~rig).sum()))
+    return Scenario(name, params, s, bodies, steps, info)
+
+
+def config3(**kw):
+    """BASELINE configs[2]: 128^3 two-phase liquid/gas with 200 rigid cubes and spheres."""
+    return two_phase_with_bodies(**kw)
+
+
 def config2(**kw):
     """BASELINE configs[1]: 64^3 + walls, 27 spheres, bottom wall 1800 K, 500 steps of 5e-6 s."""
     return closed_box_melting(**kw)
 
 
 def by_name(name, **kw):
-    return {"c1": config1, "c2": config2, "c5": config5}[name](**kw)
+    return {"c1": config1, "c2": config2, "c3": config3, "c5": config5}[name](**kw)

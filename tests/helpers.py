@@ -44,7 +44,11 @@ def compare_state(sim, orc, params, tol=TOL, what=""):
     """Compares every hot-path field of the two engines; returns the error table."""
     g, gb = sim.download()
     o, ob = orc.download()
-    s = orc.scales()
+    return compare_fields(g, gb, o, ob, orc.scales(), params, tol, what)
+
+
+def compare_fields(g, gb, o, ob, s, params, tol=TOL, what=""):
+    """g/o: stores (or anything with the store's field attributes); s: the oracle's scales()."""
     out = {}
     fl = o.kind == 0
     rg = o.kind == 1
@@ -54,7 +58,6 @@ def compare_state(sim, orc, params, tol=TOL, what=""):
     assert np.array_equal(g.group[rg], o.group[rg]), f"{what}: body ids differ"
     rho0 = np.array([params.mat[m].rho0 for m in range(params.n_mat)])
     c2 = np.array([params.mat[m].c ** 2 for m in range(params.n_mat)])
-    p0 = (rho0 * c2)[o.material]
     out["density"] = assert_close(f"{what} density", g.density[fl], o.density[fl], 0.0, tol)
     out["pressure"] = assert_close(f"{what} pressure", g.pressure[fl], o.pressure[fl],
                                    (c2[o.material] * o.density)[fl], tol)

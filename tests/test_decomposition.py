@@ -79,7 +79,7 @@ def _worker(rank, world, port, case, out):
     dist.destroy_process_group()
 
 
-NSTEPS = {"c1": 6, "c2": 6, "c1fast": 16}
+NSTEPS = {"c1": 6, "c2": 6, "c1fast": 16, "c3": 6}
 
 
 def _case(case):
@@ -87,15 +87,17 @@ def _case(case):
         return scenarios.config1(nside=20, n_spheres=3, r_range=(3.0, 4.0), seed=11)
     if case == "c1fast":  # u ~ U(+-1 m/s): Verlet rebuilds every few steps and repartitions
         return scenarios.config1(nside=20, n_spheres=3, r_range=(3.0, 4.0), seed=13, u0=1.0)
+    if case == "c3":  # two phases, cubes and spheres
+        return scenarios.config3(nside=20, n_bodies=4, r_range=(2.0, 3.0), seed=7)
     sc = scenarios.config2(nside=16, n_grid=2, r_range=(2.0, 3.0), seed=5)
     sc.params.transitions = 0  # transitions are single-rank only
     return sc
 
 
-@pytest.mark.parametrize("case", ["c1", "c2", "c1fast"])
-def test_two_ranks_match_one_rank(case, tmp_path, oracle_mod):
+@pytest.mark.parametrize("case,world", [("c1", 2), ("c2", 2), ("c1fast", 2), ("c3", 2), ("c1", 4)])
+def test_ranks_match_one_rank(case, world, tmp_path, oracle_mod):
     out = str(tmp_path / "ds.npz")
-    mp.spawn(_worker, args=(2, _free_port(), case, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
     d = np.load(out)
     sc = _case(case)
     o = oracle_mod.Oracle(sc.params)

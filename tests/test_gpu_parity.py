@@ -17,6 +17,8 @@ CASES = {
     "c1": lambda: scenarios.config1(),
     "c2_small": lambda: scenarios.config2(nside=18, n_grid=2, r_range=(2.0, 3.0), seed=5),
     "c2_melt": lambda: scenarios.config2(nside=18, n_grid=2, r_range=(2.0, 3.0), seed=5, melt_forcing=True),
+    # two phases (multi-EOS / harmonic-mean viscosity / dominant-material wall state), cubes + spheres
+    "c3_small": lambda: scenarios.config3(nside=20, n_bodies=4, r_range=(2.0, 3.0), seed=7),
 }
 
 
@@ -89,6 +91,33 @@ def test_multistep_c1_small(Oracle):
     # chaotic growth of round-off over 10 steps: 1e-7 of the pair-sum scale
     compare_state(sim, orc, sc.params, tol=1e-7, what="c1_small 10 steps")
     assert sim.stats().rebuilds == orc.stats().rebuilds
+
+
+def test_multistep_transitions(Oracle):
+    """Melting and solidification over several steps: flags bit-exact every step, fields within
+    the multistep tolerance, rebuild count equal (transitions force a rebuild)."""
+    sc = CASES["c2_melt"]()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    for k in range(6):
+        sim.step(1)
+        orc.step(1)
+        g, gb = sim.download()
+        o, ob = orc.download()
+        assert np.array_equal(g.kind, o.kind), f"kind differs after step {k + 1}"
+        assert np.array_equal(g.group, o.group), f"group differs after step {k + 1}"
+        assert np.array_equal(gb["alive"], ob["alive"])
+    assert sim.stats().transitions_melt == orc.stats().transitions_melt
+    assert sim.stats().transitions_solidify == orc.stats().transitions_solidify
+    assert sim.stats().rebuilds == orc.stats().rebuilds
+    compare_state(sim, orc, sc.params, tol=1e-7, what="c2_melt 6 steps")
+
+
+def test_multistep_c3_small(Oracle):
+    sc = CASES["c3_small"]()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    sim.step(8)
+    orc.step(8)
+    compare_state(sim, orc, sc.params, tol=1e-7, what="c3_small 8 steps")
 
 
 def test_stage_by_stage(Oracle):
