@@ -166,6 +166,7 @@ void body_apply_totals(Ctx& c, const double* dev_tot);
 
 // kernels_transition.cu
 int launch_transitions(Ctx& c);  // 0 ok, else error code
+void launch_repartition_rows(Ctx& c);
 
 inline int grid_for(size_t n, int block) { return (int)((n + block - 1) / block); }
 

@@ -299,7 +299,67 @@ void grow_bodies(Ctx& c, size_t need) {
   c.bodies_cap = cap;
 }
 
+
+// Re-partitions every Verlet row into [fluid | non-fluid] after kinds changed, keeping the
+// neighbour SET (and therefore the rebuild schedule) unchanged — the oracle does not
+// rebuild on transitions either.  Warp per row; rows whose partition is still valid are skipped.
+constexpr int kRepartWarps = 8;
+constexpr int kRepartMaxCap = 1024;
+template <int M>
+__global__ void __launch_bounds__(32 * kRepartWarps) k_repartition_rows(const uint32_t* __restrict__ kmd,
+                                                                         uint32_t* __restrict__ nbr,
+                                                                         uint32_t* __restrict__ cnt, int cap,
+                                                                         size_t n) {
+  __shared__ uint32_t buf[kRepartWarps][kRepartMaxCap];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const size_t i = (size_t)blockIdx.x * kRepartWarps + wib;
+  if (i >= n) return;  // warp-uniform
+  const uint32_t c = cnt[i];
+  const uint32_t tot = cnt_total(c), nf_old = cnt_fluid(c);
+  uint32_t* row = nbr + i * (size_t)cap;
+  uint32_t nf = 0;
+  bool bad = false;
+  for (uint32_t base = 0; base < tot; base += 32) {
+    const uint32_t k = base + lane;
+    const bool in = k < tot;
+    const bool isf = in && kind_of(kmd[nb_index<M>(row[k])]) == SPHG_FLUID;
+    nf += __popc(__ballot_sync(0xffffffffu, isf));
+    bad |= in && (isf != (k < nf_old));
+  }
+  if (!__any_sync(0xffffffffu, bad)) return;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t fo = 0, oo = 0;
+  for (uint32_t base = 0; base < tot; base += 32) {
+    const uint32_t k = base + lane;
+    const bool in = k < tot;
+    const uint32_t e = in ? row[k] : 0u;
+    const bool isf = in && kind_of(kmd[nb_index<M>(e)]) == SPHG_FLUID;
+    const uint32_t bf = __ballot_sync(0xffffffffu, isf), bo = __ballot_sync(0xffffffffu, in && !isf);
+    if (in) buf[wib][isf ? fo + __popc(bf & lt) : nf + oo + __popc(bo & lt)] = e;
+    fo += __popc(bf);
+    oo += __popc(bo);
+  }
+  __syncwarp();
+  for (uint32_t k = lane; k < tot; k += 32) row[k] = buf[wib][k];
+  if (lane == 0) cnt[i] = pack_cnt(nf, tot - nf);
+}
+
 }  // namespace
+
+void launch_repartition_rows(Ctx& c) {
+  if (c.n == 0) return;
+  if (c.cap > kRepartMaxCap) {  // very wide rows: rebuild instead
+    c.built = false;
+    return;
+  }
+  const unsigned blocks = (unsigned)((c.n + kRepartWarps - 1) / kRepartWarps);
+  switch (c.P.img_mode) {
+    case kImgNone: k_repartition_rows<kImgNone><<<blocks, 32 * kRepartWarps, 0, c.stream>>>(c.cur.kmd.p, c.nbr.p, c.cnt.p, c.cap, c.n); break;
+    case kImgCode: k_repartition_rows<kImgCode><<<blocks, 32 * kRepartWarps, 0, c.stream>>>(c.cur.kmd.p, c.nbr.p, c.cnt.p, c.cap, c.n); break;
+    default: k_repartition_rows<kImgMin><<<blocks, 32 * kRepartWarps, 0, c.stream>>>(c.cur.kmd.p, c.nbr.p, c.cnt.p, c.cap, c.n); break;
+  }
+  c.launches++;
+}
 
 int launch_transitions(Ctx& c) {
   const size_t n = c.n;
@@ -394,8 +454,8 @@ int launch_transitions(Ctx& c) {
   old.free();
   c.n_melt += nmelt;
   c.n_solid += nsolid;
-  // kinds changed: the rows' fluid / non-fluid partition is stale -> rebuild before the next evaluation
-  c.built = false;
+  // kinds changed: the rows' fluid / non-fluid partition is stale
+  launch_repartition_rows(c);
   return 0;
 }
 
