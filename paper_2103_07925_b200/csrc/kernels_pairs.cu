@@ -324,7 +324,11 @@ __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, 
   bg.z = fma(V2, gW.z, bg.z);
 }
 
-template <int M, bool kTvf, bool kSingleEta, bool kJFluid>
+// Fluid-side pair, with the pair weight w = (V_i^2 + V_j^2) (dW/dr) / r factored out of every term:
+//   acc += -p~ w d + eta~ w (u_i - u_j) + w (rho_j/2) (du_j . d) u_j,   bg += w d.
+// The i-side TVF term (1/2) A_i gradW summed over j equals (rho_i/2) u_i (du_i . bg): it is applied
+// once per particle from bg (k_forces_fluid), not per pair.
+template <int M, bool kTvf, bool kSingleEta>
 __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
                                            uint32_t e, double4 h0, double4 h1, double4 h2, double3& acc,
                                            double3& bg, bool& coincident) {
@@ -335,35 +339,48 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
     coincident = true;
     return;
   }
-  PairSide J;
-  J.u = ld3(h1);
-  J.du = ld3(h2);
-  J.rho = h1.w;
-  J.hrho = 0.5 * h1.w;
-  J.p = h2.w;
-  J.V2 = h0.w;
-  if (kSingleEta || !kJFluid) {
-    J.eta = I.eta;
+  double rinv;
+  const double dW = P.sig_h * shape_deriv_q(sqrt_and_rinv(r2, rinv) * P.inv_h);
+  const double w = (I.V2 + h0.w) * (dW * rinv);
+  bg.x = fma(w, d.x, bg.x);
+  bg.y = fma(w, d.y, bg.y);
+  bg.z = fma(w, d.z, bg.z);
+  const double rho_j = h1.w, p_j = h2.w;
+  const double pw = -fma(rho_j, I.p, I.rho * p_j) * rcp_fast(I.rho + rho_j) * w;
+  double et;
+  if (kSingleEta) {
+    et = I.eta;  // 2 eta eta / (eta + eta)
   } else {
     const uint32_t kj = __ldg(&D.kmd.p[nb_index<M>(e)]);
-    J.eta = kind_of(kj) == SPHG_FLUID ? P.mat[mat_of(kj)].eta : I.eta;  // eta_w := eta_i [P7]
+    const double eta_j = kind_of(kj) == SPHG_FLUID ? P.mat[mat_of(kj)].eta : I.eta;  // eta_w := eta_i [P7]
+    const double es = I.eta + eta_j;
+    et = es > 0.0 ? 2.0 * I.eta * eta_j * rcp_fast(es) : 0.0;
   }
-  pair_term<kTvf, kSingleEta, kJFluid>(I, J, d, r2, P, acc, bg);
+  const double vf = et * w;
+  acc.x = fma(pw, d.x, fma(vf, I.u.x - h1.x, acc.x));
+  acc.y = fma(pw, d.y, fma(vf, I.u.y - h1.y, acc.y));
+  acc.z = fma(pw, d.z, fma(vf, I.u.z - h1.z, acc.z));
+  if (kTvf) {  // wall / rigid records carry du = 0 (A_j = 0)
+    const double cj = w * (0.5 * rho_j) * (h2.x * d.x + h2.y * d.y + h2.z * d.z);
+    acc.x = fma(cj, h1.x, acc.x);
+    acc.y = fma(cj, h1.y, acc.y);
+    acc.z = fma(cj, h1.z, acc.z);
+  }
 }
 
-// one part of a row (fluid: stride +1 from f; non-fluid: stride -1 from b), row entries prefetched
-// one iteration ahead (rows stream from HBM), all three 32-byte neighbour records requested together
-template <int G, int M, bool kTvf, bool kSingleEta, bool kJFluid>
-__device__ __forceinline__ void fluid_part(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
-                                           const uint32_t* base, int stride, int n, int lane, double3& acc,
-                                           double3& bg, bool& coincident) {
+// the fluid particle's row (contiguous, fluid then non-fluid), row entries prefetched one
+// iteration ahead (rows stream from HBM), all three 32-byte neighbour records requested together
+template <int G, int M, bool kTvf, bool kSingleEta>
+__device__ __forceinline__ void fluid_row(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
+                                          const uint32_t* base, int n, int lane, double3& acc, double3& bg,
+                                          bool& coincident) {
   int k = lane;
-  uint32_t e = k < n ? __ldg(base + stride * k) : 0u;
+  uint32_t e = k < n ? __ldg(base + k) : 0u;
   for (; k < n; k += G) {
-    const uint32_t en = k + G < n ? __ldg(base + stride * (k + G)) : 0u;
+    const uint32_t en = k + G < n ? __ldg(base + k + G) : 0u;
     const uint32_t j = nb_index<M>(e);
     const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
-    fluid_pair<M, kTvf, kSingleEta, kJFluid>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
+    fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
     e = en;
   }
 }
@@ -395,7 +412,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
     const Row R = row_of(L, i);
     // one pass over the whole contiguous row: wall/rigid records carry du = 0 (A_w = 0) and, with
     // several viscosities, fluid_pair looks up eta_j by kind (eta_w := eta_i)
-    fluid_part<G, M, kTvf, kSingleEta, true>(P, D, I, pi, R.f, 1, R.n, lane, acc, bg, coincident);
+    fluid_row<G, M, kTvf, kSingleEta>(P, D, I, pi, R.f, R.n, lane, acc, bg, coincident);
   }
   acc.x = gsum<G>(acc.x);
   acc.y = gsum<G>(acc.y);
@@ -409,6 +426,13 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
     atomicMin(&fl->err_gid, D.gid.p[i]);
   }
   if (lane != 0) return;
+  if (kTvf) {  // i-side TVF term: (rho_i/2) u_i (du_i . sum_j (V_i^2+V_j^2) gradW)
+    const double4 g1 = ldg4(&D.G1.p[i]), g2 = ldg4(&D.G2.p[i]);
+    const double ai = 0.5 * g1.w * (g2.x * bg.x + g2.y * bg.y + g2.z * bg.z);
+    acc.x = fma(ai, g1.x, acc.x);
+    acc.y = fma(ai, g1.y, acc.y);
+    acc.z = fma(ai, g1.z, acc.z);
+  }
   const DevMat& Mt = P.mat[mat_of(kmd)];
   const double im = 1.0 / D.V4.p[i].w;
   D.A4.p[i] = make_double4(acc.x * im + Mt.g[0], acc.y * im + Mt.g[1], acc.z * im + Mt.g[2], 0.0);
