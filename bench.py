@@ -271,6 +271,9 @@ def run_sph(args):
         pin_vel = torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy()
         pin_pos[:] = store.pos
         pin_vel[:] = store.vel
+        # the step's results land in pinned host arrays of the store (the download DMAs into them)
+        for f, shape in (("pos", (n, 3)), ("vel", (n, 3)), ("density", (n,)), ("pressure", (n,))):
+            setattr(store, f, torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy())
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
@@ -278,12 +281,12 @@ def run_sph(args):
             sim.step(1)
             sim.download(store, fields=fields)
         e2e_s = time.perf_counter() - t0
-        # device arrays behind the requested fields: G0, V4, G1, G2 records (32 B each) + kmd + gid
-        d2h = n * (4 * 32 + 4 + 4)
+        # the requested fields, packed into gid order on the device: pos, vel (24 B), density, pressure (8 B)
+        d2h = n * (24 + 24 + 8 + 8)
         line["e2e"] = {"value": n * args.e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(48 * n),
                        "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
                        "path": "Simulation.upload_state(pos, vel from pinned host) -> step(1) -> "
-                               "download(pos, vel, density, pressure); host wall clock"}
+                               "download(pos, vel, density, pressure into pinned host arrays); host wall clock"}
     if not args.no_cpu_baseline and rank == 0:
         line["cpu_baseline"] = cpu_baseline(args.cpu_nside, args.spheres, args.nside)
     sim.close()

@@ -1074,6 +1074,24 @@ int orc_initialize(orc_ctx* h) {
     return SPHG_OK;
 }
 
+// sphg_upload_state: new positions / velocities (gid order) into the resident state; the Verlet
+// list survives unless a particle moved more than half the skin from its reference position.
+int orc_upload_state(orc_ctx* h, const double* pos, const double* vel, size_t n) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (n != c.S.size()) {
+        c.err = "upload_state: store size mismatch (upload first)";
+        return SPHG_ERR_RUNTIME;
+    }
+    double md2 = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        if (pos) c.S.pos[i] = V3{pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+        if (vel) c.S.vel[i] = V3{vel[3 * i], vel[3 * i + 1], vel[3 * i + 2]};
+        if (c.built && pos) md2 = std::max(md2, r2of(mi3(c, c.S.pos[i], c.pos_ref[i])));
+    }
+    if (c.built && pos && std::sqrt(md2) > 0.5 * (c.rv - c.rc)) c.built = false;
+    return SPHG_OK;
+}
+
 int orc_step(orc_ctx* h, int nsteps) {
     Ctx& c = *reinterpret_cast<Ctx*>(h);
     for (int k = 0; k < nsteps; ++k)

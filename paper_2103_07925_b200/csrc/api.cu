@@ -429,21 +429,28 @@ void stage_upload(Ctx& c, const sphg_soa* s, Particles& dst) {
   }
 }
 
-struct Need {
-  bool G0, G1, G2, V4;
+// Download: one kernel computes every requested store field from the device records and scatters
+// it into gid order in a device buffer (the reference's SoA layout, interleaved xyz); each field is
+// then one contiguous D2H copy — straight into the caller's array when it is pinned, else through
+// the two pinned staging slots with the host memcpy of one chunk overlapping the copy of the next.
+struct OutPtrs {
+  double *pos, *vel, *vel_adv, *acc, *acc_bg, *body_frame_pos, *wall_velocity, *force;
+  double *density, *pressure, *mass, *temperature, *dT_dt, *wall_pressure;
+  uint8_t* kind;
+  uint32_t* group;
+  uint16_t* material;
+  uint8_t* dirichlet_T;
+  uint32_t* owner;
 };
 
-void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
-  ensure_staging(c);
-  Need need;
-  need.G0 = o->pos != nullptr;
-  need.V4 = o->vel || o->vel_adv || o->mass;
-  need.G1 = (o->vel && mid_step) || o->vel_adv || o->wall_velocity || o->density;
-  need.G2 = o->vel_adv || o->pressure || o->wall_pressure;
-  size_t bytes_d2h = 0;
-  const size_t n = c.n;
-  const size_t slot_bytes = kChunk * (kPackBytes + 4);
-  cudaStream_t st = c.stream;
+__global__ void k_pack_store(const __grid_constant__ DevParams P, Particles D, size_t n, int mid_step,
+                             uint32_t rank, OutPtrs o) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const size_t g = D.gid.p[k];
+  const uint32_t kmd = D.kmd.p[k];
+  const uint32_t kind = kind_of(kmd), mat = mat_of(kmd);
+  const bool fl = kind == SPHG_FLUID;
   auto put = [](double* p, size_t g, double x, double y, double z) {
     if (p) {
       p[3 * g] = x;
@@ -451,76 +458,126 @@ void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
       p[3 * g + 2] = z;
     }
   };
-  int slot = 0;
-  size_t prev_k0 = 0, prev_m = 0;
-  int prev_slot = -1;
-  auto unpack = [&](int sl, size_t k0, size_t m) {
+  if (o.pos) {
+    const double4 G0 = D.G0.p[k];
+    put(o.pos, g, G0.x, G0.y, G0.z);
+  }
+  const bool needG1 = o.vel || o.vel_adv || o.wall_velocity || o.density;
+  const bool needG2 = o.vel_adv || o.pressure || o.wall_pressure;
+  const bool needV4 = o.vel || o.vel_adv || o.mass;
+  const double4 z4 = make_double4(0, 0, 0, 0);
+  const double4 G1 = needG1 ? D.G1.p[k] : z4, G2 = needG2 ? D.G2.p[k] : z4, V4 = needV4 ? D.V4.p[k] : z4;
+  if (fl && mid_step) put(o.vel, g, G1.x, G1.y, G1.z);
+  else put(o.vel, g, V4.x, V4.y, V4.z);
+  if (fl) put(o.vel_adv, g, G1.x + G2.x, G1.y + G2.y, G1.z + G2.z);
+  else if (kind == SPHG_RIGID) put(o.vel_adv, g, V4.x, V4.y, V4.z);
+  else put(o.vel_adv, g, 0, 0, 0);
+  if (o.acc) { const double4 a = D.A4.p[k]; put(o.acc, g, a.x, a.y, a.z); }
+  if (o.acc_bg) { const double4 a = D.B4.p[k]; put(o.acc_bg, g, a.x, a.y, a.z); }
+  if (o.force) { const double4 a = D.F4.p[k]; put(o.force, g, a.x, a.y, a.z); }
+  if (o.body_frame_pos) { const double4 a = D.X4.p[k]; put(o.body_frame_pos, g, a.x, a.y, a.z); }
+  if (fl) put(o.wall_velocity, g, 0, 0, 0);
+  else put(o.wall_velocity, g, G1.x, G1.y, G1.z);
+  if (o.density) o.density[g] = kind == SPHG_RIGID ? P.mat[mat].rho0 : G1.w;
+  if (o.pressure) o.pressure[g] = fl ? G2.w : D.p_static.p[k];
+  if (o.wall_pressure) o.wall_pressure[g] = fl ? 0.0 : G2.w;
+  if (o.mass) o.mass[g] = V4.w;
+  if (o.temperature) o.temperature[g] = D.H2.p[k].x;
+  if (o.dT_dt) o.dT_dt[g] = D.dTdt.p[k];
+  if (o.kind) o.kind[g] = (uint8_t)kind;
+  if (o.group) o.group[g] = D.group.p[k];
+  if (o.material) o.material[g] = (uint16_t)mat;
+  if (o.dirichlet_T) o.dirichlet_T[g] = (uint8_t)dir_of(kmd);
+  if (o.owner) o.owner[g] = is_ghost(kmd) ? 0xffffffffu : rank;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// contiguous device -> host copy of `bytes` (queued on the stream; returns after completion)
+void copy_out(Ctx& c, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  cudaStream_t st = c.stream;
+  if (is_pinned(dst)) {
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    return;
+  }
+  ensure_staging(c);
+  const size_t slot_bytes = kChunk * (kPackBytes + 4);
+  char* hs = static_cast<char*>(c.hstage);
+  int prev = -1;
+  size_t prev_off = 0, prev_len = 0;
+  auto drain = [&](int sl, size_t off, size_t len) {
     SPHG_CUDA_CHECK(cudaEventSynchronize(c.slot_ev[sl]));
-    Slot S = slot_view(static_cast<char*>(c.hstage) + sl * slot_bytes);
+    const char* from = hs + sl * slot_bytes;
+    char* to = static_cast<char*>(dst) + off;
+    const int64_t parts = (int64_t)std::min<size_t>(64, (len + 65535) / 65536);
 #pragma omp parallel for schedule(static)
-    for (int64_t q = 0; q < (int64_t)m; ++q) {
-      const size_t g = S.gid[q];
-      const uint32_t kmd = S.kmd[q];
-      const uint32_t kind = kind_of(kmd), mat = mat_of(kmd);
-      const bool fl = kind == SPHG_FLUID;
-      const double4 z4 = make_double4(0, 0, 0, 0);
-      const double4 G0 = need.G0 ? S.G0[q] : z4, G1 = need.G1 ? S.G1[q] : z4, G2 = need.G2 ? S.G2[q] : z4,
-                    V4 = need.V4 ? S.V4[q] : z4;
-      put(o->pos, g, G0.x, G0.y, G0.z);
-      if (fl && mid_step) put(o->vel, g, G1.x, G1.y, G1.z);
-      else put(o->vel, g, V4.x, V4.y, V4.z);
-      if (fl) put(o->vel_adv, g, G1.x + G2.x, G1.y + G2.y, G1.z + G2.z);
-      else if (kind == SPHG_RIGID) put(o->vel_adv, g, V4.x, V4.y, V4.z);
-      else put(o->vel_adv, g, 0, 0, 0);
-      if (o->acc) put(o->acc, g, S.A4[q].x, S.A4[q].y, S.A4[q].z);
-      if (o->acc_bg) put(o->acc_bg, g, S.B4[q].x, S.B4[q].y, S.B4[q].z);
-      if (o->force) put(o->force, g, S.F4[q].x, S.F4[q].y, S.F4[q].z);
-      if (o->body_frame_pos) put(o->body_frame_pos, g, S.X4[q].x, S.X4[q].y, S.X4[q].z);
-      if (fl) put(o->wall_velocity, g, 0, 0, 0);
-      else put(o->wall_velocity, g, G1.x, G1.y, G1.z);
-      if (o->density) o->density[g] = kind == SPHG_RIGID ? c.P.mat[mat].rho0 : G1.w;
-      if (o->pressure) o->pressure[g] = fl ? G2.w : S.ps[q];
-      if (o->wall_pressure) o->wall_pressure[g] = fl ? 0.0 : G2.w;
-      if (o->mass) o->mass[g] = V4.w;
-      if (o->temperature) o->temperature[g] = S.H2[q].x;
-      if (o->dT_dt) o->dT_dt[g] = S.dT[q];
-      if (o->kind) o->kind[g] = (uint8_t)kind;
-      if (o->group) o->group[g] = S.grp[q];
-      if (o->material) o->material[g] = (uint16_t)mat;
-      if (o->dirichlet_T) o->dirichlet_T[g] = (uint8_t)dir_of(kmd);
-      if (o->owner) o->owner[g] = is_ghost(kmd) ? 0xffffffffu : (uint32_t)c.params.rank;
+    for (int64_t q = 0; q < parts; ++q) {
+      const size_t b0 = len * q / parts, b1 = len * (q + 1) / parts;
+      std::memcpy(to + b0, from + b0, b1 - b0);
     }
   };
-  for (size_t k0 = 0; k0 < n; k0 += kChunk, slot ^= 1) {
-    const size_t m = std::min(kChunk, n - k0);
-    Slot S = slot_view(static_cast<char*>(c.hstage) + slot * slot_bytes);
+  int slot = 0;
+  for (size_t off = 0; off < bytes; off += slot_bytes, slot ^= 1) {
+    const size_t len = std::min(slot_bytes, bytes - off);
     SPHG_CUDA_CHECK(cudaEventSynchronize(c.slot_ev[slot]));
-    if (need.G0) d2h(S.G0, c.cur.G0.p + k0, m, st);
-    if (need.G1) d2h(S.G1, c.cur.G1.p + k0, m, st);
-    if (need.G2) d2h(S.G2, c.cur.G2.p + k0, m, st);
-    if (need.V4) d2h(S.V4, c.cur.V4.p + k0, m, st);
-    if (o->acc) d2h(S.A4, c.cur.A4.p + k0, m, st);
-    if (o->acc_bg) d2h(S.B4, c.cur.B4.p + k0, m, st);
-    if (o->force) d2h(S.F4, c.cur.F4.p + k0, m, st);
-    if (o->body_frame_pos) d2h(S.X4, c.cur.X4.p + k0, m, st);
-    if (o->temperature) d2h(S.H2, c.cur.H2.p + k0, m, st);
-    if (o->dT_dt) d2h(S.dT, c.cur.dTdt.p + k0, m, st);
-    if (o->pressure) d2h(S.ps, c.cur.p_static.p + k0, m, st);
-    d2h(S.kmd, c.cur.kmd.p + k0, m, st);
-    if (o->group) d2h(S.grp, c.cur.group.p + k0, m, st);
-    d2h(S.gid, c.cur.gid.p + k0, m, st);
-    bytes_d2h += m * (4 + 4 + (need.G0 + need.G1 + need.G2 + need.V4 + !!o->acc + !!o->acc_bg + !!o->force +
-                               !!o->body_frame_pos) * 32 + !!o->temperature * 16 + (!!o->dT_dt + !!o->pressure) * 8 +
-                      !!o->group * 4);
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(hs + slot * slot_bytes, static_cast<const char*>(src) + off, len,
+                                    cudaMemcpyDeviceToHost, st));
     SPHG_CUDA_CHECK(cudaEventRecord(c.slot_ev[slot], st));
-    if (prev_slot >= 0) unpack(prev_slot, prev_k0, prev_m);  // overlaps with the copy just issued
-    prev_slot = slot;
-    prev_k0 = k0;
-    prev_m = m;
+    if (prev >= 0) drain(prev, prev_off, prev_len);
+    prev = slot;
+    prev_off = off;
+    prev_len = len;
   }
-  if (prev_slot >= 0) unpack(prev_slot, prev_k0, prev_m);
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(st));
-  c.last_d2h_bytes = bytes_d2h;
+  if (prev >= 0) drain(prev, prev_off, prev_len);
+}
+
+void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
+  const size_t n = c.n;
+  if (n == 0) return;
+  struct F {
+    void* host;
+    size_t elem;
+    void** dev;
+  };
+  OutPtrs d{};
+  const F fields[] = {
+      {o->pos, 24, (void**)&d.pos}, {o->vel, 24, (void**)&d.vel}, {o->vel_adv, 24, (void**)&d.vel_adv},
+      {o->acc, 24, (void**)&d.acc}, {o->acc_bg, 24, (void**)&d.acc_bg},
+      {o->body_frame_pos, 24, (void**)&d.body_frame_pos}, {o->wall_velocity, 24, (void**)&d.wall_velocity},
+      {o->force, 24, (void**)&d.force}, {o->density, 8, (void**)&d.density}, {o->pressure, 8, (void**)&d.pressure},
+      {o->mass, 8, (void**)&d.mass}, {o->temperature, 8, (void**)&d.temperature}, {o->dT_dt, 8, (void**)&d.dT_dt},
+      {o->wall_pressure, 8, (void**)&d.wall_pressure}, {o->kind, 1, (void**)&d.kind}, {o->group, 4, (void**)&d.group},
+      {o->material, 2, (void**)&d.material}, {o->dirichlet_T, 1, (void**)&d.dirichlet_T},
+      {o->owner, 4, (void**)&d.owner}};
+  size_t total = 0;
+  for (const F& f : fields)
+    if (f.host) total += (n * f.elem + 255) / 256 * 256;
+  if (total == 0) return;
+  c.dl_buf.alloc(total);
+  size_t off = 0;
+  for (const F& f : fields)
+    if (f.host) {
+      *f.dev = c.dl_buf.p + off;
+      off += (n * f.elem + 255) / 256 * 256;
+    }
+  k_pack_store<<<grid_for(n, 256), 256, 0, c.stream>>>(c.P, c.cur, n, mid_step ? 1 : 0, (uint32_t)c.params.rank, d);
+  c.launches++;
+  size_t bytes = 0;
+  for (const F& f : fields)
+    if (f.host) {
+      copy_out(c, f.host, *f.dev, n * f.elem);
+      bytes += n * f.elem;
+    }
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  c.last_d2h_bytes = bytes;
 }
 
 }  // namespace
@@ -957,7 +1014,7 @@ void sphg_destroy(sphg_ctx* h) {
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
   c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();
   c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();
-  c.fidx.free(); c.widx.free(); c.idx_of_gid.free(); c.body_buf.free();
+  c.fidx.free(); c.widx.free(); c.brick_buf.free(); c.scan_cells.free(); c.dl_buf.free(); c.idx_of_gid.free(); c.body_buf.free();
   for (auto& b : c.halo_ids) b.free();
   if (c.dflags) cudaFree(c.dflags);
   if (c.hflags) cudaFreeHost(c.hflags);

@@ -51,6 +51,30 @@ struct DevParams {
   int32_t img_mode;     // neighbour-entry image mode (kImgNone / kImgCode / kImgMin)
 };
 
+// ------------------------------------------------------ brick traversal
+// Work order of the cell-structured kernels (Verlet build, pair kernels): cells are visited brick
+// by brick (kBrick^3 cells, bricks and cells inside a brick z-fastest).  Storage stays in the pinned
+// z-fastest (cell, gid) order [P1]; only the order in which cells / particles are PROCESSED
+// changes, so the neighbourhood of the cells in flight (~(kBrick+2)^3 cells) stays in L2 instead
+// of three whole x-planes of the grid.
+constexpr int kBrick = 8;
+__host__ __device__ __forceinline__ int64_t brick_positions(const int32_t* nc) {
+  const int64_t bx = (nc[0] + kBrick - 1) / kBrick, by = (nc[1] + kBrick - 1) / kBrick,
+                bz = (nc[2] + kBrick - 1) / kBrick;
+  return bx * by * bz * (int64_t)(kBrick * kBrick * kBrick);
+}
+// linear cell id of brick position b, or -1 for padding positions past the grid edge
+__host__ __device__ __forceinline__ int64_t brick_to_cell(const int32_t* nc, int64_t b) {
+  constexpr int64_t B3 = kBrick * kBrick * kBrick;
+  const int64_t nby = (nc[1] + kBrick - 1) / kBrick, nbz = (nc[2] + kBrick - 1) / kBrick;
+  const int64_t brick = b / B3, loc = b % B3;
+  const int64_t bz = brick % nbz, by = (brick / nbz) % nby, bx = brick / (nbz * nby);
+  const int64_t lz = loc % kBrick, ly = (loc / kBrick) % kBrick, lx = loc / (kBrick * kBrick);
+  const int64_t cx = bx * kBrick + lx, cy = by * kBrick + ly, cz = bz * kBrick + lz;
+  if (cx >= nc[0] || cy >= nc[1] || cz >= nc[2]) return -1;
+  return (cx * nc[1] + cy) * nc[2] + cz;
+}
+
 // ---------------------------------------------------------------- tags
 // kmd word: bits 0-1 kind, 2-7 material, 8-15 dirichlet group (0xff none)
 __host__ __device__ __forceinline__ uint32_t kind_of(uint32_t kmd) { return kmd & 3u; }

@@ -90,6 +90,8 @@ struct Ctx {
   NbrList nl() const { return {nbr.p, cnt.p, (size_t)cap}; }
   // per-kind index lists: fluid, non-fluid (rigid + boundary), rigid body-major
   DBuf<uint32_t> fidx, widx, ridx, body_start;
+  DBuf<uint32_t> brick_buf, scan_cells;
+  DBuf<uint8_t> dl_buf;  // download: requested store fields in gid order  // kind-list construction in brick order
   size_t nf = 0, nw = 0, nrigid = 0;
   int group_density = 4, group_forces = 4;  // lanes per particle in the pair kernels
   bool cell_build = true;  // cell-cooperative Verlet build (falls back per particle on overflow)

@@ -264,7 +264,8 @@ __global__ void __launch_bounds__(32) k_build_nlist_cells(const __grid_constant_
   __shared__ float4 sp[kStage];     // x, y, z (relative to the home cell, units of h), boundary flag
   __shared__ uint32_t se[kStage];   // neighbour index | image code
   __shared__ uint32_t hc[kHomeMax]; // running row length per home particle
-  const int64_t c = blockIdx.x;
+  const int64_t c = brick_to_cell(P.ncell, blockIdx.x);
+  if (c < 0) return;
   const int lane = threadIdx.x;
   const uint32_t h0 = cstart[c], h1 = cend[c];
   if (h1 <= h0) return;
@@ -390,23 +391,41 @@ int bits_for(uint64_t maxval) {  // bits needed to represent values in [0, maxva
   return b;
 }
 
-__global__ void k_kind_flags(const uint32_t* __restrict__ kmd, size_t n, uint32_t* __restrict__ ff,
-                             uint32_t* __restrict__ wf) {
-  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const bool gh = is_ghost(kmd[k]);
-  const bool fl = kind_of(kmd[k]) == SPHG_FLUID;
-  ff[k] = (fl && !gh) ? 1u : 0u;
-  wf[k] = (!fl && !gh) ? 1u : 0u;
+// per brick position: fluid / non-fluid (non-ghost) particle counts of that cell
+__global__ void k_cell_kind_counts(const __grid_constant__ DevParams P, const uint32_t* __restrict__ kmd,
+                                   const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
+                                   int64_t npos, uint32_t* __restrict__ fc, uint32_t* __restrict__ wc) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= npos) return;
+  const int64_t c = brick_to_cell(P.ncell, b);
+  uint32_t nf = 0, nw = 0;
+  if (c >= 0) {
+    for (uint32_t k = cstart[c]; k < cend[c]; ++k) {
+      const uint32_t m = kmd[k];
+      if (is_ghost(m)) continue;
+      if (kind_of(m) == SPHG_FLUID) ++nf;
+      else ++nw;
+    }
+  }
+  fc[b] = nf;
+  wc[b] = nw;
 }
 
-__global__ void k_kind_scatter(const uint32_t* __restrict__ kmd, const uint32_t* __restrict__ fpos,
-                               const uint32_t* __restrict__ wpos, size_t n, uint32_t* __restrict__ fidx,
-                               uint32_t* __restrict__ widx) {
-  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n || is_ghost(kmd[k])) return;
-  if (kind_of(kmd[k]) == SPHG_FLUID) fidx[fpos[k]] = (uint32_t)k;
-  else widx[wpos[k]] = (uint32_t)k;
+__global__ void k_cell_kind_scatter(const __grid_constant__ DevParams P, const uint32_t* __restrict__ kmd,
+                                    const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
+                                    int64_t npos, const uint32_t* __restrict__ fo, const uint32_t* __restrict__ wo,
+                                    uint32_t* __restrict__ fidx, uint32_t* __restrict__ widx) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= npos) return;
+  const int64_t c = brick_to_cell(P.ncell, b);
+  if (c < 0) return;
+  uint32_t f = fo[b], w = wo[b];
+  for (uint32_t k = cstart[c]; k < cend[c]; ++k) {
+    const uint32_t m = kmd[k];
+    if (is_ghost(m)) continue;
+    if (kind_of(m) == SPHG_FLUID) fidx[f++] = k;
+    else widx[w++] = k;
+  }
 }
 
 }  // namespace
@@ -417,24 +436,27 @@ static void launch_kind_lists(Ctx& c) {
   cudaStream_t s = c.stream;
   c.fidx.alloc(std::max<size_t>(n, 1));
   c.widx.alloc(std::max<size_t>(n, 1));
-  uint32_t* ff = c.vals.p;
-  uint32_t* wf = c.vals_alt.p;
-  uint32_t* fpos = reinterpret_cast<uint32_t*>(c.keys.p);
-  uint32_t* wpos = reinterpret_cast<uint32_t*>(c.keys_alt.p);
-  k_kind_flags<<<grid_for(n, 256), 256, 0, s>>>(c.cur.kmd.p, n, ff, wf);
-  exclusive_scan_u32(ff, fpos, n, c.scan_tmp.p, s, &c.launches);
-  exclusive_scan_u32(wf, wpos, n, c.scan_tmp.p, s, &c.launches);
-  uint32_t lastp = 0, lastf = 0;
-  SPHG_CUDA_CHECK(cudaMemcpyAsync(&lastp, fpos + n - 1, 4, cudaMemcpyDeviceToHost, s));
-  SPHG_CUDA_CHECK(cudaMemcpyAsync(&lastf, ff + n - 1, 4, cudaMemcpyDeviceToHost, s));
-  k_kind_scatter<<<grid_for(n, 256), 256, 0, s>>>(c.cur.kmd.p, fpos, wpos, n, c.fidx.p, c.widx.p);
+  const int64_t npos = brick_positions(c.P.ncell);
+  c.brick_buf.alloc(4 * (size_t)npos + 64);
+  uint32_t* fc = c.brick_buf.p;
+  uint32_t* wc = fc + npos;
+  uint32_t* fo = wc + npos;
+  uint32_t* wo = fo + npos;
+  const unsigned g = (unsigned)((npos + 255) / 256);
+  k_cell_kind_counts<<<g, 256, 0, s>>>(c.P, c.cur.kmd.p, c.cell_start.p, c.cell_end.p, npos, fc, wc);
+  c.scan_cells.alloc(2 * ((size_t)npos / 256 + 2) + 64);
+  exclusive_scan_u32(fc, fo, (size_t)npos, c.scan_cells.p, s, &c.launches);
+  exclusive_scan_u32(wc, wo, (size_t)npos, c.scan_cells.p, s, &c.launches);
+  k_cell_kind_scatter<<<g, 256, 0, s>>>(c.P, c.cur.kmd.p, c.cell_start.p, c.cell_end.p, npos, fo, wo, c.fidx.p,
+                                        c.widx.p);
+  uint32_t tail[4] = {0, 0, 0, 0};
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&tail[0], fo + npos - 1, 4, cudaMemcpyDeviceToHost, s));
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&tail[1], fc + npos - 1, 4, cudaMemcpyDeviceToHost, s));
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&tail[2], wo + npos - 1, 4, cudaMemcpyDeviceToHost, s));
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&tail[3], wc + npos - 1, 4, cudaMemcpyDeviceToHost, s));
   SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
-  uint32_t lastw = 0, lastwf = 0;
-  SPHG_CUDA_CHECK(cudaMemcpyAsync(&lastw, wpos + n - 1, 4, cudaMemcpyDeviceToHost, s));
-  SPHG_CUDA_CHECK(cudaMemcpyAsync(&lastwf, wf + n - 1, 4, cudaMemcpyDeviceToHost, s));
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
-  c.nf = (size_t)lastp + lastf;
-  c.nw = (size_t)lastw + lastwf;
+  c.nf = (size_t)tail[0] + tail[1];
+  c.nw = (size_t)tail[2] + tail[3];
   c.launches += 2;
 }
 
@@ -502,7 +524,7 @@ void launch_rebuild(Ctx& c) {
     uint32_t mc = 0, err = 0;
     if (c.cell_build) {
       SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->build_overflow, 0, sizeof(uint32_t), s));
-      k_build_nlist_cells<<<(unsigned)c.ncells, 32, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_start.p,
+      k_build_nlist_cells<<<(unsigned)brick_positions(c.P.ncell), 32, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_start.p,
                                                             c.cell_end.p, c.nbr.p, c.cnt.p, c.cap, c.dflags);
       SPHG_CUDA_CHECK(cudaMemcpyAsync(&err, &c.dflags->build_overflow, 4, cudaMemcpyDeviceToHost, s));
       SPHG_CUDA_CHECK(cudaStreamSynchronize(s));

@@ -262,3 +262,39 @@ def test_upload_state_warm_update(Oracle):
     from tests.helpers import vec_err
     assert vec_err(ga.pos, gr.pos, 0.016, 1e-14) <= 1
     assert vec_err(ga.vel, gr.vel, 1e-3, 1e-9) <= 1
+
+
+def test_upload_state_matches_oracle(Oracle):
+    """sphg_upload_state on both engines (kinematic update, one particle pushed past half the skin
+    so both drop their Verlet lists), then two steps: fields within the multistep bar."""
+    sc = CASES["c1_small"]()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    sim.step(2)
+    orc.step(2)
+    s, _ = orc.download()
+    s.vel[:] *= 0.5
+    s.pos[0] += 0.2 * sc.params.h
+    for e in (sim, orc):
+        e.upload_state(s.pos, s.vel)
+        e.step(2)
+    compare_state(sim, orc, sc.params, tol=1e-8, what="upload_state + 2 steps")
+    assert sim.stats().rebuilds == orc.stats().rebuilds
+
+
+def test_download_into_pinned_and_pageable(Oracle):
+    """The gid-order device pack lands identically in pinned and pageable host arrays."""
+    import torch
+    sc = CASES["c2_small"]()
+    sim = sim_factory(sc.params)
+    sim.upload(sc.store, sc.bodies)
+    sim.initialize()
+    sim.step(1)
+    a, _ = sim.download()
+    b = a.copy()
+    for f in ("pos", "vel", "density", "pressure", "temperature"):
+        arr = getattr(b, f)
+        pinned = torch.empty(arr.shape, dtype=torch.float64, pin_memory=True).numpy()
+        setattr(b, f, pinned)
+    sim.download(b, fields=("pos", "vel", "density", "pressure", "temperature"))
+    for f in ("pos", "vel", "density", "pressure", "temperature"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
