@@ -209,9 +209,16 @@ def run_sph(args):
     sa = sim.stats()
     sim.step(max(2, args.steps // 2))
     sb = sim.stats()
-    sim.set_timing(False)
     kk = max(2, args.steps // 2)
     stage_ms = {abi.STAGE_NAMES[k]: (sb.stage_ms[k] - sa.stage_ms[k]) / kk for k in range(12)}
+    # one Verlet rebuild (binning + radix sort + reorder + list build + index lists), forced twice
+    sim.run_stage(abi.STAGE_REBUILD)
+    sc0 = sim.stats()
+    sim.run_stage(abi.STAGE_REBUILD)
+    sim.run_stage(abi.STAGE_REBUILD)
+    sc1 = sim.stats()
+    sim.set_timing(False)
+    rebuild_ms = (sc1.stage_ms[abi.STAGE_REBUILD] - sc0.stage_ms[abi.STAGE_REBUILD]) / 2
     launches = (st1.kernel_launches - st0.kernel_launches)
     value = n / (ms_step * 1e-3)
     peaks = load_peaks()
@@ -254,7 +261,7 @@ def run_sph(args):
                        "particles": n, "fluid": nf, "rigid": info["n_rigid"],
                        "rigid_fraction": round(info["rigid_fraction"], 4), "parallelism": "1 GPU",
                        "l2": "inputs larger than L2 (state ~%.1f GB)" % (store_bytes(sc.store) / 1e9)},
-            "roofline": roofline, "fp64": fp64, "stage_ms": stage_ms,
+            "roofline": roofline, "fp64": fp64, "stage_ms": stage_ms, "rebuild_ms": rebuild_ms,
             "step_roofline": {"bytes_per_particle": STEP_BYTES_PER_PARTICLE,
                               "achieved_gbs": STEP_BYTES_PER_PARTICLE * n / (ms_step * 1e-3) / 1e9},
             "wall_s_timed": wall, "gpu_launches": int(launches),

@@ -174,7 +174,17 @@ __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ Dev
 // candidate in fp32.  Pairs inside a 1e-4 guard band around r_v^2 (fp32 error
 // is ~1e-6 relative here) fall back to the exact fp64 test of [P2] on the
 // original positions, so the list is bit-identical to the pinned rule.
-constexpr int kStage = 512;     // staged candidates per batch (10 KB)
+#ifndef SPHG_BUILD_STAGE
+#define SPHG_BUILD_STAGE 512
+#endif
+#ifndef SPHG_BUILD_WARPS
+#define SPHG_BUILD_WARPS 1
+#endif
+#ifndef SPHG_BUILD_MINB
+#define SPHG_BUILD_MINB 1
+#endif
+constexpr int kStage = SPHG_BUILD_STAGE;  // staged candidates per batch (20 B each)
+constexpr int kBuildWarps = SPHG_BUILD_WARPS;  // independent home cells per block (one per warp)
 constexpr int kHomeMax = 256;   // particles per home cell handled here; denser cells -> per-particle kernel
 
 struct BuildCtx {
@@ -191,7 +201,7 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
                                             uint32_t h0, uint32_t h1, double ox0, double oy0, double oz0,
                                             const float4* sp, const uint32_t* se, int ns, uint32_t* hc,
                                             uint32_t emask) {
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const float rv2 = (float)(P.rv2 * P.inv_h * P.inv_h);
   const float lo_band = rv2 * (1.0f - 1e-4f), hi_band = rv2 * (1.0f + 1e-4f);
   for (uint32_t ib = h0; ib < h1; ib += 32) {
@@ -254,19 +264,23 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
   }
 }
 
-__global__ void __launch_bounds__(32) k_build_nlist_cells(const __grid_constant__ DevParams P,
+__global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nlist_cells(const __grid_constant__ DevParams P,
                                                            const double4* __restrict__ G0,
                                                            const uint32_t* __restrict__ kmd,
                                                            const uint32_t* __restrict__ cstart,
                                                            const uint32_t* __restrict__ cend,
                                                            uint32_t* __restrict__ nbr, uint32_t* __restrict__ cnt,
                                                            int cap, DevFlags* __restrict__ fl) {
-  __shared__ float4 sp[kStage];     // x, y, z (relative to the home cell, units of h), boundary flag
-  __shared__ uint32_t se[kStage];   // neighbour index | image code
-  __shared__ uint32_t hc[kHomeMax]; // running row length per home particle
-  const int64_t c = brick_to_cell(P.ncell, blockIdx.x);
+  __shared__ float4 sp_all[kBuildWarps][kStage];     // x, y, z (relative to the home cell, units of h), kind
+  __shared__ uint32_t se_all[kBuildWarps][kStage];   // neighbour index | image code
+  __shared__ uint32_t hc_all[kBuildWarps][kHomeMax]; // running row length per home particle
+  const int wib = threadIdx.x >> 5;
+  float4* sp = sp_all[wib];
+  uint32_t* se = se_all[wib];
+  uint32_t* hc = hc_all[wib];
+  const int64_t c = brick_to_cell(P.ncell, (int64_t)blockIdx.x * kBuildWarps + wib);
   if (c < 0) return;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const uint32_t h0 = cstart[c], h1 = cend[c];
   if (h1 <= h0) return;
   if (h1 - h0 > (uint32_t)kHomeMax) {
@@ -524,7 +538,8 @@ void launch_rebuild(Ctx& c) {
     uint32_t mc = 0, err = 0;
     if (c.cell_build) {
       SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->build_overflow, 0, sizeof(uint32_t), s));
-      k_build_nlist_cells<<<(unsigned)brick_positions(c.P.ncell), 32, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_start.p,
+      k_build_nlist_cells<<<(unsigned)((brick_positions(c.P.ncell) + kBuildWarps - 1) / kBuildWarps),
+                            32 * kBuildWarps, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_start.p,
                                                             c.cell_end.p, c.nbr.p, c.cnt.p, c.cap, c.dflags);
       SPHG_CUDA_CHECK(cudaMemcpyAsync(&err, &c.dflags->build_overflow, 4, cudaMemcpyDeviceToHost, s));
       SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
