@@ -3,7 +3,7 @@
 The reference publishes no dataset: BASELINE.json's configs *are* the inputs.
 Positions follow the lattice convention of the reference's seed_lattice /
 for_each_lattice_point (lattice.hpp:38-82: points at lo + (k + 1/2) dx, last
-axis fastest, mass rho0 dx^3); tests/test_oracle_pins.py checks the generator
+axis fastest, mass rho0 dx^3); tests/test_oracle_kat.py checks the generator
 against the reference's own seed_lattice bit for bit.  Random numbers come from
 a counter-based SplitMix64 (53-bit mantissa mapping), so the same arrays are
 produced on any host and are uploaded identically to the GPU and the oracle
