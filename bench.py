@@ -17,6 +17,7 @@ the SPEC restatement, OpenMP on all host cores) on a bounded sample of the
 same workload.
 """
 import argparse
+import glob
 import json
 import math
 import os
@@ -43,7 +44,7 @@ STEP_BYTES_PER_PARTICLE = 480.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)  # C5: 100 steps (Verlet rebuilds included as they occur)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sph", choices=["sph", "reference"])
     ap.add_argument("--nside", type=int, default=400)
@@ -207,9 +208,9 @@ def run_sph(args):
     # per-stage breakdown (separate pass; per-stage events on the same stream)
     sim.set_timing(True)
     sa = sim.stats()
-    sim.step(max(2, args.steps // 2))
+    kk = max(2, min(20, args.steps // 2))
+    sim.step(kk)
     sb = sim.stats()
-    kk = max(2, args.steps // 2)
     stage_ms = {abi.STAGE_NAMES[k]: (sb.stage_ms[k] - sa.stage_ms[k]) / kk for k in range(12)}
     # one Verlet rebuild (binning + radix sort + reorder + list build + index lists), forced twice
     sim.run_stage(abi.STAGE_REBUILD)
@@ -232,19 +233,27 @@ def run_sph(args):
     achieved_tf = flops / t_ff / 1e12
     fp64_peak = peaks.get("fp64_tflops")
     hbm_achieved = FORCES_BYTES_PER_FLUID * nf / t_ff / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_ncu_full_64m.json")
-    if os.path.exists(tp) and n == 64000000:
+    traffic, l1 = None, None
+    profs = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_64m.json")))
+    if profs and n == 64000000:
+        tp = profs[-1]
         for k in json.load(open(tp)):
-            if "k_forces_fluid" in k["kernel"]:
+            if "k_forces_fluid" in k["kernel"] and "nan" not in k["dram__bytes_read.sum"]:
                 rd = float(k["dram__bytes_read.sum"].split()[0]) * 1e9
                 wr = float(k["dram__bytes_write.sum"].split()[0]) * 1e9
-                traffic = {"bytes_per_launch": rd + wr, "source": "profiles/r01_ncu_full_64m.json (ncu --set full)",
-                           "note": "rows (~28 GB) + neighbour records re-read past L2; the CSM bytes model is 8.8 GB"}
+                src = os.path.relpath(tp, ROOT) + " (ncu --set full, one launch)"
+                traffic = {"bytes_per_launch": rd + wr, "source": src,
+                           "note": "Verlet rows (~29 GB) + neighbour records re-read past L2; the CSM bytes model is 8.8 GB"}
+                wf = k.get("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed")
+                fp = k.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active")
+                if wf:
+                    l1 = {"lsu_wavefronts_pct": float(wf.split()[0]), "fp64_pipe_pct": float(fp.split()[0]) if fp else None,
+                          "source": src, "note": "the binding unit: L1 data-pipe wavefronts (one per distinct 32 B "
+                                                 "sector of a gather), see DESIGN.md section 4"}
     roofline = {"bound": "fp64", "kernel": "k_forces_fluid (momentum_rhs + TVF)",
                 "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": (achieved_tf / fp64_peak) if fp64_peak else None,
-                "traffic": traffic, "launch_ms": stage_ms["forces_fluid"],
+                "traffic": traffic, "l1": l1, "launch_ms": stage_ms["forces_fluid"],
                 "flops_per_launch": flops, "flops_model": "91 flop per interacting fluid pair (SURVEY 8(d))",
                 "peak_source": "profiles/fp64_peak.json (DFMA microbenchmark, tools/fp64_peak.cu)",
                 "hbm": {"achieved": hbm_achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
