@@ -31,8 +31,10 @@ class Error : public std::runtime_error {
 };
 
 /// sphfsi::ScenarioConfig<3> (config.hpp:68-106) -> flat POD of the C ABI.
+/// transitions < 0 takes cfg.transition_mode (config.hpp:61); diffusion switches on the
+/// concentration equation.
 inline sphg_params to_params(const sphfsi::ScenarioConfig<3>& cfg, double dt, int thermal, int transitions,
-                             double contact_damping_override = -1.0) {
+                             double contact_damping_override = -1.0, int diffusion = 0) {
   sphg_params p;
   std::memset(&p, 0, sizeof(p));
   p.dx = cfg.dx;
@@ -56,6 +58,8 @@ inline sphg_params to_params(const sphfsi::ScenarioConfig<3>& cfg, double dt, in
     d.c = s.speed_of_sound;
     d.pb = s.background_pressure;
     d.T_t = s.transition_temperature;
+    d.D = s.diffusivity;
+    d.C_t = s.transition_concentration;
     d.melt_target = s.melt_target == sphfsi::kNoMaterial ? SPHG_NO_MATERIAL : s.melt_target;
     d.solidify_target = s.solidify_target == sphfsi::kNoMaterial ? SPHG_NO_MATERIAL : s.solidify_target;
     const sphfsi::Vec<3> b = cfg.body_force_of(m);
@@ -65,7 +69,8 @@ inline sphg_params to_params(const sphfsi::ScenarioConfig<3>& cfg, double dt, in
   p.dc = contact_damping_override >= 0.0 ? contact_damping_override : cfg.contact_damping;
   p.tvf = cfg.transport_velocity ? 1 : 0;
   p.thermal = thermal;
-  p.transitions = transitions;
+  p.transitions = transitions >= 0 ? transitions : (int32_t)cfg.transition_mode;
+  p.diffusion = diffusion;
   p.n_dirichlet = (int32_t)cfg.dirichlet_temperature.size();
   for (int g = 0; g < p.n_dirichlet && g < SPHG_MAX_DIRICHLET; ++g) {
     const auto& pcs = cfg.dirichlet_temperature[g].pieces;
@@ -73,6 +78,15 @@ inline sphg_params to_params(const sphfsi::ScenarioConfig<3>& cfg, double dt, in
     for (size_t k = 0; k < pcs.size() && k < SPHG_MAX_PIECES; ++k) {
       p.dirichlet_T[g].t_end[k] = pcs[k].t_end;
       p.dirichlet_T[g].value[k] = pcs[k].value;
+    }
+  }
+  p.n_dirichlet_c = (int32_t)cfg.dirichlet_concentration.size();
+  for (int g = 0; g < p.n_dirichlet_c && g < SPHG_MAX_DIRICHLET; ++g) {
+    const auto& pcs = cfg.dirichlet_concentration[g].pieces;
+    p.dirichlet_C[g].n = (int32_t)pcs.size();
+    for (size_t k = 0; k < pcs.size() && k < SPHG_MAX_PIECES; ++k) {
+      p.dirichlet_C[g].t_end[k] = pcs[k].t_end;
+      p.dirichlet_C[g].value[k] = pcs[k].value;
     }
   }
   p.rank = 0;
@@ -103,6 +117,9 @@ inline sphg_soa views(sphfsi::ParticleStore<3>& s, std::vector<sphfsi::Vec<3>>* 
   v.wall_pressure = s.wall_pressure.data();
   v.wall_velocity = d3(s.wall_velocity);
   v.dirichlet_T = s.dirichlet_T.data();
+  v.concentration = s.concentration.data();
+  v.dC_dt = s.dC_dt.data();
+  v.dirichlet_C = s.dirichlet_C.data();
   if (force) {
     force->resize(s.size());
     v.force = d3(*force);

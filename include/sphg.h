@@ -58,6 +58,8 @@ typedef struct {
   int32_t melt_target;      /* SPHG_NO_MATERIAL = none */
   int32_t solidify_target;  /* SPHG_NO_MATERIAL = none */
   double body_force[3];
+  double D;          /* diffusivity (concentration, Remark 2.3 / SPEC:407-411) */
+  double C_t;        /* transition_concentration, NaN = none */
 } sphg_material;
 
 /* sphfsi::Schedule (config.hpp:20-33): value of the first piece with t <= t_end. */
@@ -82,12 +84,15 @@ typedef struct {
   double kc, dc;             /* contact stiffness / damping (config.hpp:81-82) */
   int32_t tvf;               /* transport_velocity (config.hpp:90) */
   int32_t thermal;           /* solve the heat equation */
-  int32_t transitions;       /* 0 none, 1 temperature (config.hpp:61) */
+  int32_t transitions;       /* TransitionMode (config.hpp:61): 0 none, 1 temperature, 2 concentration */
   int32_t n_dirichlet;
   sphg_schedule dirichlet_T[SPHG_MAX_DIRICHLET]; /* config.hpp:94 */
   int32_t default_fluid_mat; /* EOS used for wall density when a wall has no fluid support */
   int32_t nlist_capacity;    /* 0 = auto; grown on overflow */
   int32_t rank, nranks;      /* domain decomposition (1 rank: 0,1) */
+  int32_t diffusion;         /* solve the concentration diffusion equation */
+  int32_t n_dirichlet_c;
+  sphg_schedule dirichlet_C[SPHG_MAX_DIRICHLET]; /* config.hpp:95, indexed by dirichlet_C group */
 } sphg_params;
 
 /* Host SoA views in gid order — the ParticleStore<3> layout (store.hpp:26-46).
@@ -106,6 +111,8 @@ typedef struct {
   uint8_t *dirichlet_T;
   double *force;
   uint32_t *owner;   /* owning rank (store.hpp:46); != params.rank marks a ghost copy; NULL = all owned */
+  double *concentration, *dC_dt; /* store.hpp:36-37 */
+  uint8_t *dirichlet_C;          /* store.hpp:45: concentration schedule group or SPHG_NO_DIRICHLET */
 } sphg_soa;
 
 /* RigidBody.  inertia = world frame about com: xx yy zz xy xz yz. */
@@ -132,7 +139,8 @@ typedef struct {
 enum {
   SPHG_STAGE_REBUILD = 0,     /* cell keys + radix sort + reorder + neighbour list */
   SPHG_STAGE_DENSITY = 1,     /* density_summation + eos_pressure */
-  SPHG_STAGE_HEAT = 2,        /* apply_thermal_dirichlet + conduction_rhs + T update */
+  SPHG_STAGE_HEAT = 2,        /* apply_thermal_dirichlet + conduction_rhs + T update;
+                                 with params.diffusion also diffusion_rhs + C update */
   SPHG_STAGE_EXTRAPOLATE = 3, /* extrapolate_wall_quantities */
   SPHG_STAGE_FORCES = 4,      /* momentum_rhs + coupling_force_on_rigid + contact_force */
   SPHG_STAGE_BODIES = 5,      /* reduce_force_torque -> a_k, alpha_k */
@@ -205,7 +213,7 @@ int sphg_count_pairs(sphg_ctx* ctx, int64_t counts[4]);
  * read by the pair kernels, never integrated, and refreshed by halo unpacks.  Index lists are local ids
  * (positions in the uploaded store); buffers are device pointers for sphg_ (host pointers for orc_). */
 #define SPHG_MAX_HALO_SLOTS 64
-enum { SPHG_HALO_STATE = 0,    /* after the drift: pos, u_int, du, vel, T           (13 doubles) */
+enum { SPHG_HALO_STATE = 0,    /* after the drift: pos, u_int, du, vel, T, C        (14 doubles) */
        SPHG_HALO_DENSITY = 1,  /* after density: V^2, rho, p, V_heat                (4 doubles)  */
        SPHG_HALO_WALL = 2 };   /* after extrapolation: V_w^2, u~_w, rho_w, p_w      (6 doubles)  */
 int sphg_halo_doubles(int phase);

@@ -26,6 +26,8 @@ def load():
         dp = C.POINTER(C.c_double)
         lib.orc_get_scales.argtypes = [C.c_void_p] + [dp] * 7
         lib.orc_get_scales.restype = C.c_int
+        lib.orc_get_scale_dC.argtypes = [C.c_void_p, dp]
+        lib.orc_get_scale_dC.restype = C.c_int
         for f in ("orc_kernel_w", "orc_kernel_dw"):
             getattr(lib, f).argtypes = [C.c_double, C.c_double]
             getattr(lib, f).restype = C.c_double
@@ -71,6 +73,9 @@ class Oracle(Simulation):
                                                        ("acc", "acc_bg", "dT_dt", "force", "density")],
                                             bf.ctypes.data_as(dp), bt.ctypes.data_as(dp)), "scales")
         out["body_force"], out["body_torque"] = bf[:nb], bt[:nb]
+        out["dC_dt"] = np.zeros(n)
+        if n:
+            self._check(self.lib.orc_get_scale_dC(self._h, out["dC_dt"].ctypes.data_as(dp)), "scales")
         return out
 
 

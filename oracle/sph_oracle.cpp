@@ -70,7 +70,7 @@ struct Ctx {
     std::vector<int64_t> cell_of;
     std::vector<uint32_t> sorted;
     // tolerance scales (sum of |pair contributions|)
-    std::vector<double> acc_scale, accbg_scale, dT_scale, force_scale, rho_scale;
+    std::vector<double> acc_scale, accbg_scale, dT_scale, force_scale, rho_scale, dC_scale;
     std::vector<double> body_fscale, body_tscale;
     double t = 0.0;
     int64_t steps = 0, rebuilds = 0, n_melt = 0, n_solid = 0;
@@ -131,6 +131,8 @@ sphfsi::ScenarioConfig<3> to_config(const sphg_params& P) {
         mt.speed_of_sound = P.mat[m].c;
         mt.background_pressure = P.mat[m].pb;
         mt.transition_temperature = P.mat[m].T_t;
+        mt.diffusivity = P.mat[m].D;
+        mt.transition_concentration = P.mat[m].C_t;
         mt.melt_target = P.mat[m].melt_target < 0 ? sphfsi::kNoMaterial : (sphfsi::MaterialId)P.mat[m].melt_target;
         mt.solidify_target =
             P.mat[m].solidify_target < 0 ? sphfsi::kNoMaterial : (sphfsi::MaterialId)P.mat[m].solidify_target;
@@ -148,6 +150,15 @@ sphfsi::ScenarioConfig<3> to_config(const sphg_params& P) {
             s.pieces.push_back({P.dirichlet_T[g].t_end[k], P.dirichlet_T[g].value[k]});
         cfg.dirichlet_temperature.push_back(s);
     }
+    for (int g = 0; g < P.n_dirichlet_c && g < SPHG_MAX_DIRICHLET; ++g) {
+        sphfsi::Schedule s;
+        for (int k = 0; k < P.dirichlet_C[g].n && k < SPHG_MAX_PIECES; ++k)
+            s.pieces.push_back({P.dirichlet_C[g].t_end[k], P.dirichlet_C[g].value[k]});
+        cfg.dirichlet_concentration.push_back(s);
+    }
+    cfg.transition_mode = P.transitions == 2   ? sphfsi::TransitionMode::Concentration
+                          : P.transitions == 1 ? sphfsi::TransitionMode::Temperature
+                                               : sphfsi::TransitionMode::None;
     return cfg;
 }
 
@@ -168,6 +179,10 @@ std::vector<std::string> validate(const sphg_params& P) {
             v.push_back("periodic axis " + std::to_string(a) + " has fewer than 3 cells");
     }
     if (P.n_dirichlet < 0 || P.n_dirichlet > SPHG_MAX_DIRICHLET) v.push_back("dirichlet group count out of range");
+    if (P.n_dirichlet_c < 0 || P.n_dirichlet_c > SPHG_MAX_DIRICHLET)
+        v.push_back("concentration dirichlet group count out of range");
+    if (P.transitions < 0 || P.transitions > 2) v.push_back("unknown transition mode");
+    if (P.transitions == 2 && !P.diffusion) v.push_back("concentration transitions need the diffusion equation");
     if (P.default_fluid_mat < 0 || P.default_fluid_mat >= P.n_mat) v.push_back("default fluid material missing");
     return v;
 }
@@ -343,6 +358,68 @@ bool stage_heat(Ctx& c) {
         c.S.dT_dt[a] = rate;
         c.S.temperature[a] = Tn[a] + c.dt * rate;
         c.dT_scale[a] = scale;
+    }
+    if (coincident)
+        return fail(c, "coincident particles " + std::to_string(bad_i) + " and " + std::to_string(bad_j) +
+                           " at step " + std::to_string(c.steps));
+    return true;
+}
+
+// ------------------------------------------------------------- diffusion
+// Concentration analogue of the heat stage (Remark 2.3 PAPER:141):
+// dC_a/dt = (1/rho_a) sum_b V_b 4 D_a D_b/(D_a+D_b) (C_ab/r_ab) dW/dr, no capacity factor.
+// [P18] Dirichlet concentration groups (config.hpp:95) apply to every particle carrying a
+// group (the paper's fixed-concentration gastric juice is a fluid), set at t^{n+1}
+// before the rates; such particles keep C = C^ (their rate is still reported).  Boundary walls
+// take part only with a group (as for heat); V_b = m/rho (fluid), m/rho0 otherwise.
+bool stage_diffusion(Ctx& c) {
+    const size_t n = c.S.size();
+    const double t_new = c.t + c.dt;
+    auto dir_group = [&](size_t i) -> int {
+        const int g = c.S.dirichlet_C[i];
+        return (g != sphfsi::kNoDirichlet && g < c.P.n_dirichlet_c && c.P.dirichlet_C[g].n > 0) ? g : -1;
+    };
+    for (size_t i = 0; i < n; ++i) {
+        const int g = dir_group(i);
+        if (g >= 0) c.S.concentration[i] = sched_value(c.P.dirichlet_C[g], t_new);
+    }
+    const std::vector<double> Cn = c.S.concentration;  // double buffer
+    const sphfsi::QuinticKernel<3> K(c.h);
+    const double rc2 = c.rc * c.rc;
+    bool coincident = false;
+    size_t bad_i = 0, bad_j = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t ii = 0; ii < (int64_t)n; ++ii) {
+        const size_t a = (size_t)ii;
+        if (c.S.kind[a] == Kind::Boundary || ghost(c, a)) continue;
+        const sphfsi::Material& ma = c.mats[c.S.material[a]];
+        double s = 0.0, sc = 0.0;
+        for (uint32_t b : c.nl[a]) {
+            const bool bd = c.S.kind[b] == Kind::Boundary;
+            if (bd && c.S.dirichlet_C[b] == sphfsi::kNoDirichlet) continue;
+            const V3 d = mi3(c, c.S.pos[a], c.S.pos[b]);
+            const double r2 = r2of(d);
+            if (r2 > rc2) continue;
+            const double r = std::sqrt(r2);
+            if (r == 0.0) {
+#pragma omp critical
+                { coincident = true; bad_i = a; bad_j = b; }
+                continue;
+            }
+            const sphfsi::Material& mb = c.mats[c.S.material[b]];
+            const double dsum = ma.diffusivity + mb.diffusivity;
+            if (dsum == 0.0) continue;
+            const double dt_ = 4.0 * ma.diffusivity * mb.diffusivity / dsum;
+            const double rho_b = bd ? mb.reference_density : c.S.density[b];
+            const double Vb = c.S.mass[b] / rho_b;
+            const double term = Vb * dt_ * ((Cn[a] - Cn[b]) / r) * K.dw_dr(r);
+            s += term;
+            sc += std::abs(term);
+        }
+        const double rate = s / c.S.density[a];
+        c.S.dC_dt[a] = rate;
+        if (dir_group(a) < 0) c.S.concentration[a] = Cn[a] + c.dt * rate;
+        c.dC_scale[a] = sc / c.S.density[a];
     }
     if (coincident)
         return fail(c, "coincident particles " + std::to_string(bad_i) + " and " + std::to_string(bad_j) +
@@ -762,14 +839,17 @@ bool stage_final_kick(Ctx& c) {
 // detect_transitions / apply_transitions / post_transition_body_velocity /
 // split_disconnected_bodies [P12]
 bool stage_transitions(Ctx& c) {
-    if (c.P.transitions != 1) return true;
+    if (c.P.transitions != 1 && c.P.transitions != 2) return true;
+    const bool conc = c.P.transitions == 2;  // TransitionMode::Concentration (config.hpp:61) [P19]
     const size_t n = c.S.size();
     std::vector<uint32_t> melt, solid;
     for (size_t i = 0; i < n; ++i) {
         const sphg_material& m = c.P.mat[c.S.material[i]];
-        if (std::isnan(m.T_t)) continue;
-        if (c.S.kind[i] == Kind::Rigid && m.melt_target >= 0 && c.S.temperature[i] > m.T_t) melt.push_back((uint32_t)i);
-        else if (c.S.kind[i] == Kind::Fluid && m.solidify_target >= 0 && c.S.temperature[i] < m.T_t)
+        const double thr = conc ? m.C_t : m.T_t;
+        const double x = conc ? c.S.concentration[i] : c.S.temperature[i];
+        if (std::isnan(thr)) continue;
+        if (c.S.kind[i] == Kind::Rigid && m.melt_target >= 0 && x > thr) melt.push_back((uint32_t)i);
+        else if (c.S.kind[i] == Kind::Fluid && m.solidify_target >= 0 && x < thr)
             solid.push_back((uint32_t)i);
     }
     if (melt.empty() && solid.empty()) return true;
@@ -928,6 +1008,7 @@ void resize_aux(Ctx& c) {
     c.acc_scale.assign(n, 0.0);
     c.accbg_scale.assign(n, 0.0);
     c.dT_scale.assign(n, 0.0);
+    c.dC_scale.assign(n, 0.0);
     c.force_scale.assign(n, 0.0);
     c.rho_scale.assign(n, 0.0);
 }
@@ -938,7 +1019,7 @@ bool run_stage(Ctx& c, int s) {
     switch (s) {
         case SPHG_STAGE_REBUILD: return stage_rebuild(c);
         case SPHG_STAGE_DENSITY: return stage_density(c);
-        case SPHG_STAGE_HEAT: return c.P.thermal ? stage_heat(c) : true;
+        case SPHG_STAGE_HEAT: return (!c.P.thermal || stage_heat(c)) && (!c.P.diffusion || stage_diffusion(c));
         case SPHG_STAGE_EXTRAPOLATE: return stage_extrapolate(c);
         case SPHG_STAGE_FORCES: return stage_forces(c);
         case SPHG_STAGE_BODIES: return stage_bodies(c);
@@ -957,11 +1038,12 @@ bool one_step(Ctx& c) {
         if (!stage_rebuild(c)) return false;
     if (!stage_density(c)) return false;
     if (c.P.thermal && !stage_heat(c)) return false;
+    if (c.P.diffusion && !stage_diffusion(c)) return false;
     if (!stage_extrapolate(c)) return false;
     if (!stage_forces(c)) return false;
     if (!stage_bodies(c)) return false;
     if (!stage_final_kick(c)) return false;
-    if (c.P.transitions == 1 && !stage_transitions(c)) return false;
+    if (c.P.transitions != 0 && !stage_transitions(c)) return false;
     c.steps++;
     return true;
 }
@@ -1032,8 +1114,8 @@ int orc_upload(orc_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t nb
     copy1(S.mass, s->mass, n, 0.0);
     copy1(S.temperature, s->temperature, n, 0.0);
     copy1(S.dT_dt, s->dT_dt, n, 0.0);
-    S.concentration.assign(n, 0.0);
-    S.dC_dt.assign(n, 0.0);
+    copy1(S.concentration, s->concentration, n, 0.0);
+    copy1(S.dC_dt, s->dC_dt, n, 0.0);
     S.kind.resize(n);
     for (size_t i = 0; i < n; ++i) S.kind[i] = static_cast<Kind>(s->kind[i]);
     copy1(S.group, s->group, n, 0u);
@@ -1042,7 +1124,7 @@ int orc_upload(orc_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t nb
     copy1(S.wall_pressure, s->wall_pressure, n, 0.0);
     copy3(S.wall_velocity, s->wall_velocity, n);
     copy1(S.dirichlet_T, s->dirichlet_T, n, (uint8_t)0xff);
-    S.dirichlet_C.assign(n, 0xff);
+    copy1(S.dirichlet_C, s->dirichlet_C, n, (uint8_t)0xff);
     if (s->owner) copy1(S.owner, s->owner, n, 0u);
     else S.owner.assign(n, (uint32_t)c.P.rank);
     c.halo.assign(SPHG_MAX_HALO_SLOTS, {});
@@ -1120,6 +1202,9 @@ int orc_download(orc_ctx* h, sphg_soa* o, sphg_body* bodies, size_t* nb) {
     out1(o->wall_pressure, S.wall_pressure);
     out3(o->wall_velocity, S.wall_velocity);
     out1(o->dirichlet_T, S.dirichlet_T);
+    out1(o->concentration, S.concentration);
+    out1(o->dC_dt, S.dC_dt);
+    out1(o->dirichlet_C, S.dirichlet_C);
     out3(o->force, c.force);
     if (o->owner)
         for (size_t i = 0; i < S.size(); ++i) o->owner[i] = ghost(c, i) ? 0xffffffffu : (uint32_t)c.P.rank;
@@ -1160,6 +1245,12 @@ int orc_get_nlist(orc_ctx* h, int64_t* offsets, uint32_t* nbr) {
 }
 
 // tolerance scales, gid order
+int orc_get_scale_dC(orc_ctx* h, double* dC) {
+    const Ctx& c = *reinterpret_cast<Ctx*>(h);
+    std::copy(c.dC_scale.begin(), c.dC_scale.end(), dC);
+    return SPHG_OK;
+}
+
 int orc_get_scales(orc_ctx* h, double* acc, double* accbg, double* dT, double* force, double* rho, double* body_f,
                    double* body_t) {
     Ctx& c = *reinterpret_cast<Ctx*>(h);
@@ -1195,7 +1286,7 @@ int orc_stats(orc_ctx* h, sphg_stats_t* s) {
 
 // ---------------- decomposition primitives (sphg.h): oracle records, host buffers
 int orc_halo_doubles(int phase) {
-    return phase == SPHG_HALO_STATE ? 13 : phase == SPHG_HALO_DENSITY ? 4 : phase == SPHG_HALO_WALL ? 6 : -1;
+    return phase == SPHG_HALO_STATE ? 14 : phase == SPHG_HALO_DENSITY ? 4 : phase == SPHG_HALO_WALL ? 6 : -1;
 }
 
 int orc_halo_set(orc_ctx* h, int slot, const uint32_t* ids, size_t n) {
@@ -1221,6 +1312,7 @@ int orc_halo_pack(orc_ctx* h, int phase, int slot, double* buf) {
             put3(o + 6, c.S.vel_adv[i]);
             put3(o + 9, c.S.wall_velocity[i]);
             o[12] = c.S.temperature[i];
+            o[13] = c.S.concentration[i];
         } else if (phase == SPHG_HALO_DENSITY) {
             o[0] = c.S.density[i];
             o[1] = c.S.pressure[i];
@@ -1249,6 +1341,7 @@ int orc_halo_unpack(orc_ctx* h, int phase, int slot, const double* buf) {
             c.S.vel_adv[i] = v3(o + 6);
             c.S.wall_velocity[i] = v3(o + 9);
             c.S.temperature[i] = o[12];
+            c.S.concentration[i] = o[13];
         } else if (phase == SPHG_HALO_DENSITY) {
             c.S.density[i] = o[0];
             c.S.pressure[i] = o[1];

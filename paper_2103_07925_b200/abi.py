@@ -27,6 +27,7 @@ STAGE_TRANSITIONS = 8
 STAGE_MASS = 9
 
 HALO_STATE, HALO_DENSITY, HALO_WALL = 0, 1, 2
+TRANSITIONS_NONE, TRANSITIONS_TEMPERATURE, TRANSITIONS_CONCENTRATION = 0, 1, 2  # config.hpp:61
 MAX_HALO_SLOTS = 64
 
 STAGE_NAMES = ["rebuild", "density", "heat", "extrapolate", "forces", "bodies",
@@ -39,7 +40,8 @@ class Material(C.Structure):
     _fields_ = [("rho0", C.c_double), ("nu", C.c_double), ("cp", C.c_double),
                 ("kappa", C.c_double), ("c", C.c_double), ("pb", C.c_double),
                 ("T_t", C.c_double), ("melt_target", C.c_int32),
-                ("solidify_target", C.c_int32), ("body_force", C.c_double * 3)]
+                ("solidify_target", C.c_int32), ("body_force", C.c_double * 3),
+                ("D", C.c_double), ("C_t", C.c_double)]
 
 
 class Schedule(C.Structure):
@@ -60,7 +62,9 @@ class Params(C.Structure):
                 ("n_dirichlet", C.c_int32),
                 ("dirichlet_T", Schedule * MAX_DIRICHLET),
                 ("default_fluid_mat", C.c_int32), ("nlist_capacity", C.c_int32),
-                ("rank", C.c_int32), ("nranks", C.c_int32)]
+                ("rank", C.c_int32), ("nranks", C.c_int32),
+                ("diffusion", C.c_int32), ("n_dirichlet_c", C.c_int32),
+                ("dirichlet_C", Schedule * MAX_DIRICHLET)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -76,7 +80,8 @@ class SoA(C.Structure):
                 ("material", C.POINTER(C.c_uint16)),
                 ("body_frame_pos", _dp), ("wall_pressure", _dp), ("wall_velocity", _dp),
                 ("dirichlet_T", C.POINTER(C.c_uint8)), ("force", _dp),
-                ("owner", C.POINTER(C.c_uint32))]
+                ("owner", C.POINTER(C.c_uint32)),
+                ("concentration", _dp), ("dC_dt", _dp), ("dirichlet_C", C.POINTER(C.c_uint8))]
 
 
 class Body(C.Structure):

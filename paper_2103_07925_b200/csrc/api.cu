@@ -72,6 +72,10 @@ std::vector<std::string> validate(const sphg_params& P) {  // restates config.hp
   for (int g = 0; g < P.n_dirichlet && g < SPHG_MAX_DIRICHLET; ++g)
     for (int i = 1; i < P.dirichlet_T[g].n && i < SPHG_MAX_PIECES; ++i)
       if (P.dirichlet_T[g].t_end[i] < P.dirichlet_T[g].t_end[i - 1]) fail("temperature schedule pieces out of order");
+  for (int g = 0; g < P.n_dirichlet_c && g < SPHG_MAX_DIRICHLET; ++g)
+    for (int i = 1; i < P.dirichlet_C[g].n && i < SPHG_MAX_PIECES; ++i)
+      if (P.dirichlet_C[g].t_end[i] < P.dirichlet_C[g].t_end[i - 1])
+        fail("concentration schedule pieces out of order");
   // extras (oracle/sph_oracle.cpp validate)
   if (!(P.dt > 0.0)) fail("time step dt must be positive");
   const double rv = kSupport * h + kSkin * h;
@@ -82,6 +86,10 @@ std::vector<std::string> validate(const sphg_params& P) {  // restates config.hp
       fail("periodic axis " + std::to_string(a) + " has fewer than 3 cells");
   }
   if (P.n_dirichlet < 0 || P.n_dirichlet > SPHG_MAX_DIRICHLET) fail("dirichlet group count out of range");
+  if (P.n_dirichlet_c < 0 || P.n_dirichlet_c > SPHG_MAX_DIRICHLET)
+    fail("concentration dirichlet group count out of range");
+  if (P.transitions < 0 || P.transitions > 2) fail("unknown transition mode");
+  if (P.transitions == 2 && !P.diffusion) fail("concentration transitions need the diffusion equation");
   if (P.default_fluid_mat < 0 || P.default_fluid_mat >= P.n_mat) fail("default fluid material missing");
   return v;
 }
@@ -106,6 +114,9 @@ DevParams make_dev_params(const sphg_params& p) {
     d.pb = s.pb;
     d.T_t = s.T_t;
     d.has_Tt = std::isnan(s.T_t) ? 0 : 1;
+    d.D = s.D;
+    d.C_t = s.C_t;
+    d.has_Ct = std::isnan(s.C_t) ? 0 : 1;
     for (int a = 0; a < 3; ++a) d.g[a] = s.body_force[a];
     d.p0 = s.rho0 * s.c * s.c;
     d.inv_c2 = s.c != 0.0 ? 1.0 / (s.c * s.c) : 0.0;
@@ -137,6 +148,15 @@ DevParams make_dev_params(const sphg_params& p) {
       P.sched[g].value[k] = p.dirichlet_T[g].value[k];
     }
   }
+  P.n_schedC = p.n_dirichlet_c;
+  for (int g = 0; g < p.n_dirichlet_c && g < SPHG_MAX_DIRICHLET; ++g) {
+    P.schedC[g].n = p.dirichlet_C[g].n;
+    for (int k = 0; k < SPHG_MAX_PIECES; ++k) {
+      P.schedC[g].t_end[k] = p.dirichlet_C[g].t_end[k];
+      P.schedC[g].value[k] = p.dirichlet_C[g].value[k];
+    }
+  }
+  P.diffusion = p.diffusion;
   P.h = p.h > 0.0 ? p.h : p.dx;
   P.inv_h = 1.0 / P.h;  // kernel.hpp:20 inv_h_
   P.rc = kSupport * P.h;
@@ -270,6 +290,7 @@ int do_stage(sphg_ctx* h, int stage) {
     case SPHG_STAGE_DENSITY: timed(c, stage, launch_density); break;
     case SPHG_STAGE_HEAT:
       if (c.P.thermal) timed(c, stage, launch_heat);
+      if (c.P.diffusion) timed(c, stage, launch_diffusion);
       break;
     case SPHG_STAGE_EXTRAPOLATE: timed(c, stage, launch_extrapolate); break;
     case SPHG_STAGE_FORCES: timed_forces(c); break;
@@ -285,7 +306,7 @@ int do_stage(sphg_ctx* h, int stage) {
       h->mid_step = false;
       break;
     case SPHG_STAGE_TRANSITIONS:
-      if (c.P.transitions == 1) {
+      if (c.P.transitions != 0) {
         const int rc = launch_transitions(c);
         if (rc) return fail(h, rc, c.err);
       }
@@ -313,12 +334,13 @@ int one_step(sphg_ctx* h) {
   if (!c.built || c.max_disp > c.P.half_skin) timed(c, SPHG_STAGE_REBUILD, launch_rebuild);
   timed(c, SPHG_STAGE_DENSITY, launch_density);
   if (c.P.thermal) timed(c, SPHG_STAGE_HEAT, launch_heat);
+  if (c.P.diffusion) timed(c, SPHG_STAGE_HEAT, launch_diffusion);
   timed(c, SPHG_STAGE_EXTRAPOLATE, launch_extrapolate);
   timed_forces(c);
   timed(c, SPHG_STAGE_BODIES, launch_bodies);
   timed(c, SPHG_STAGE_FINAL_KICK, launch_final_kick);
   h->mid_step = false;
-  if (c.P.transitions == 1) {
+  if (c.P.transitions != 0) {
     rc = launch_transitions(c);
     if (rc) return fail(h, rc, c.err);
   }
@@ -341,12 +363,13 @@ void h2d(T* dst, const T* src, size_t n, cudaStream_t s) {
 // chunk.  Device order == gid order on a cold upload; a warm upload lands in
 // the alternate buffers and is gathered through the gid permutation.
 constexpr size_t kChunk = 1u << 18;  // particles per staging chunk
-constexpr size_t kPackBytes = 8 * sizeof(double4) + sizeof(double2) + 2 * sizeof(double) + 2 * sizeof(uint32_t);
+constexpr size_t kPackBytes =
+    8 * sizeof(double4) + 2 * sizeof(double2) + 3 * sizeof(double) + 2 * sizeof(uint32_t);
 
 struct Slot {
   double4 *G0, *G1, *G2, *V4, *A4, *B4, *F4, *X4;
-  double2* H2;
-  double *dT, *ps;
+  double2 *H2, *C2;
+  double *dT, *ps, *dC;
   uint32_t *kmd, *grp, *gid;
 };
 
@@ -359,7 +382,8 @@ Slot slot_view(char* base) {
   };
   take(s.G0, kChunk * 32); take(s.G1, kChunk * 32); take(s.G2, kChunk * 32); take(s.V4, kChunk * 32);
   take(s.A4, kChunk * 32); take(s.B4, kChunk * 32); take(s.F4, kChunk * 32); take(s.X4, kChunk * 32);
-  take(s.H2, kChunk * 16); take(s.dT, kChunk * 8); take(s.ps, kChunk * 8);
+  take(s.H2, kChunk * 16); take(s.C2, kChunk * 16); take(s.dT, kChunk * 8); take(s.ps, kChunk * 8);
+  take(s.dC, kChunk * 8);
   take(s.kmd, kChunk * 4); take(s.grp, kChunk * 4); take(s.gid, kChunk * 4);
   return s;
 }
@@ -372,6 +396,7 @@ void ensure_staging(Ctx& c) {
 
 void stage_upload(Ctx& c, const sphg_soa* s, Particles& dst) {
   ensure_staging(c);
+  const bool conc = c.P.diffusion != 0;
   const size_t n = s->n;
   const size_t slot_bytes = kChunk * (kPackBytes + 4);
   auto v3 = [](const double* p, size_t i) {
@@ -415,8 +440,16 @@ void stage_upload(Ctx& c, const sphg_soa* s, Particles& dst) {
       S.H2[q] = make_double2(s1(s->temperature, i), Vh);
       S.dT[q] = s1(s->dT_dt, i);
       S.ps[q] = p;
+      const uint32_t dirc = s->dirichlet_C ? s->dirichlet_C[i] : SPHG_NO_DIRICHLET;
+      if (conc) {  // diffusion volume: fluid m/rho, rigid and Dirichlet-C walls m/rho0, other walls 0
+        double Vc = 0.0;
+        if (kind == SPHG_FLUID) Vc = V;
+        else if (kind == SPHG_RIGID || dirc != SPHG_NO_DIRICHLET) Vc = mass / M.rho0;
+        S.C2[q] = make_double2(s1(s->concentration, i), Vc);
+        S.dC[q] = s1(s->dC_dt, i);
+      }
       const bool ghost = s->owner && s->owner[i] != (uint32_t)c.params.rank;
-      S.kmd[q] = make_kmd(kind, mat, dir) | (ghost ? kGhostBit : 0u);
+      S.kmd[q] = make_kmd(kind, mat, dir, dirc) | (ghost ? kGhostBit : 0u);
       S.grp[q] = s->group ? s->group[i] : 0;
     }
     cudaStream_t st = c.stream;
@@ -425,6 +458,10 @@ void stage_upload(Ctx& c, const sphg_soa* s, Particles& dst) {
     h2d(dst.F4.p + k0, S.F4, m, st); h2d(dst.X4.p + k0, S.X4, m, st); h2d(dst.H2.p + k0, S.H2, m, st);
     h2d(dst.dTdt.p + k0, S.dT, m, st); h2d(dst.p_static.p + k0, S.ps, m, st);
     h2d(dst.kmd.p + k0, S.kmd, m, st); h2d(dst.group.p + k0, S.grp, m, st);
+    if (conc) {
+      h2d(dst.C2.p + k0, S.C2, m, st);
+      h2d(dst.dCdt.p + k0, S.dC, m, st);
+    }
     SPHG_CUDA_CHECK(cudaEventRecord(c.slot_ev[slot], st));
   }
 }
@@ -441,6 +478,8 @@ struct OutPtrs {
   uint16_t* material;
   uint8_t* dirichlet_T;
   uint32_t* owner;
+  double *concentration, *dC_dt;
+  uint8_t* dirichlet_C;
 };
 
 __global__ void k_pack_store(const __grid_constant__ DevParams P, Particles D, size_t n, int mid_step,
@@ -489,6 +528,9 @@ __global__ void k_pack_store(const __grid_constant__ DevParams P, Particles D, s
   if (o.material) o.material[g] = (uint16_t)mat;
   if (o.dirichlet_T) o.dirichlet_T[g] = (uint8_t)dir_of(kmd);
   if (o.owner) o.owner[g] = is_ghost(kmd) ? 0xffffffffu : rank;
+  if (o.concentration) o.concentration[g] = D.C2.p ? D.C2.p[k].x : 0.0;
+  if (o.dC_dt) o.dC_dt[g] = D.dCdt.p ? D.dCdt.p[k] : 0.0;
+  if (o.dirichlet_C) o.dirichlet_C[g] = (uint8_t)dirc_of(kmd);
 }
 
 bool is_pinned(const void* p) {
@@ -556,7 +598,8 @@ void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
       {o->mass, 8, (void**)&d.mass}, {o->temperature, 8, (void**)&d.temperature}, {o->dT_dt, 8, (void**)&d.dT_dt},
       {o->wall_pressure, 8, (void**)&d.wall_pressure}, {o->kind, 1, (void**)&d.kind}, {o->group, 4, (void**)&d.group},
       {o->material, 2, (void**)&d.material}, {o->dirichlet_T, 1, (void**)&d.dirichlet_T},
-      {o->owner, 4, (void**)&d.owner}};
+      {o->owner, 4, (void**)&d.owner}, {o->concentration, 8, (void**)&d.concentration},
+      {o->dC_dt, 8, (void**)&d.dC_dt}, {o->dirichlet_C, 1, (void**)&d.dirichlet_C}};
   size_t total = 0;
   for (const F& f : fields)
     if (f.host) total += (n * f.elem + 255) / 256 * 256;
@@ -653,9 +696,10 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     const bool warm = c.built && c.have_state && n == c.n && n > 0;
     c.n = n;
     const size_t na = std::max<size_t>(n, 1);
-    c.cur.alloc(na);
-    c.alt.alloc(na);
+    c.cur.alloc(na, c.P.diffusion != 0);
+    c.alt.alloc(na, c.P.diffusion != 0);
     c.H2new.alloc(na);
+    if (c.P.diffusion) c.C2new.alloc(na);
     c.keys.alloc(na);
     c.keys_alt.alloc(na);
     c.vals.alloc(na);
@@ -930,7 +974,7 @@ int sphg_count_pairs(sphg_ctx* h, int64_t out[4]) {
 }
 
 int sphg_halo_doubles(int phase) {
-  return phase == SPHG_HALO_STATE ? 13 : phase == SPHG_HALO_DENSITY ? 4 : phase == SPHG_HALO_WALL ? 6 : -1;
+  return phase == SPHG_HALO_STATE ? 14 : phase == SPHG_HALO_DENSITY ? 4 : phase == SPHG_HALO_WALL ? 6 : -1;
 }
 
 int sphg_halo_set(sphg_ctx* h, int slot, const uint32_t* ids, size_t n) {
@@ -1010,7 +1054,7 @@ void sphg_destroy(sphg_ctx* h) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
-  c.cur.free(); c.alt.free(); c.H2new.free(); c.bodies.free();
+  c.cur.free(); c.alt.free(); c.H2new.free(); c.C2new.free(); c.bodies.free();
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
   c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();
   c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();

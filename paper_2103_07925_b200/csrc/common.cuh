@@ -21,9 +21,9 @@ struct DevMat {
   double g[3];
   double p0;           // rho0 c^2
   double inv_c2;       // 1/c^2 (0 when c == 0)
+  double D, C_t;       // diffusivity, transition concentration
   int32_t melt, solid;
-  int32_t has_Tt;
-  int32_t pad;
+  int32_t has_Tt, has_Ct;
 };
 
 struct DevSchedule {
@@ -35,10 +35,11 @@ struct DevSchedule {
 struct DevParams {
   DevMat mat[kMaxMat];
   DevSchedule sched[SPHG_MAX_DIRICHLET];
+  DevSchedule schedC[SPHG_MAX_DIRICHLET];  // concentration Dirichlet groups (config.hpp:95)
   double lo[3], hi[3], L[3], halfL[3], inv_edge[3];
   int32_t ncell[3];
   int32_t periodic[3];
-  int32_t n_mat, n_sched;
+  int32_t n_mat, n_sched, n_schedC, diffusion;
   double h, inv_h, rc, rc2, rv, rv2, sigma, sig_h, w0;
   double dx, dx3, dt, hdt;
   double kc, dc;
@@ -76,12 +77,15 @@ __host__ __device__ __forceinline__ int64_t brick_to_cell(const int32_t* nc, int
 }
 
 // ---------------------------------------------------------------- tags
-// kmd word: bits 0-1 kind, 2-7 material, 8-15 dirichlet group (0xff none)
+// kmd word: bits 0-1 kind, 2-7 material, 8-15 temperature Dirichlet group, 16 ghost,
+// 24-31 concentration Dirichlet group (0xff none for both groups)
 __host__ __device__ __forceinline__ uint32_t kind_of(uint32_t kmd) { return kmd & 3u; }
 __host__ __device__ __forceinline__ uint32_t mat_of(uint32_t kmd) { return (kmd >> 2) & 63u; }
 __host__ __device__ __forceinline__ uint32_t dir_of(uint32_t kmd) { return (kmd >> 8) & 255u; }
-__host__ __device__ __forceinline__ uint32_t make_kmd(uint32_t kind, uint32_t mat, uint32_t dir) {
-  return (kind & 3u) | ((mat & 63u) << 2) | ((dir & 255u) << 8);
+__host__ __device__ __forceinline__ uint32_t dirc_of(uint32_t kmd) { return kmd >> 24; }
+__host__ __device__ __forceinline__ uint32_t make_kmd(uint32_t kind, uint32_t mat, uint32_t dir,
+                                                      uint32_t dirc = 0xffu) {
+  return (kind & 3u) | ((mat & 63u) << 2) | ((dir & 255u) << 8) | ((dirc & 255u) << 24);
 }
 // bit 16: ghost copy of a particle owned by another rank (read-only here, refreshed by halos)
 constexpr uint32_t kGhostBit = 1u << 16;

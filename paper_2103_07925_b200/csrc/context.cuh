@@ -57,14 +57,20 @@ struct Particles {  // one buffer set (double-buffered for the rebuild reorder)
   DBuf<double2> H2;
   DBuf<double> dTdt, p_static;
   DBuf<uint32_t> kmd, group, gid;
-  void alloc(size_t n) {
+  DBuf<double2> C2;  // concentration, diffusion volume (allocated only with params.diffusion)
+  DBuf<double> dCdt;
+  void alloc(size_t n, bool conc) {
     G0.alloc(n); G1.alloc(n); G2.alloc(n); V4.alloc(n); A4.alloc(n); B4.alloc(n); F4.alloc(n);
     X4.alloc(n); R4.alloc(n); H2.alloc(n); dTdt.alloc(n); p_static.alloc(n);
     kmd.alloc(n); group.alloc(n); gid.alloc(n);
+    if (conc) {
+      C2.alloc(n);
+      dCdt.alloc(n);
+    }
   }
   void free() {
     G0.free(); G1.free(); G2.free(); V4.free(); A4.free(); B4.free(); F4.free(); X4.free(); R4.free();
-    H2.free(); dTdt.free(); p_static.free(); kmd.free(); group.free(); gid.free();
+    H2.free(); dTdt.free(); p_static.free(); kmd.free(); group.free(); gid.free(); C2.free(); dCdt.free();
   }
 };
 
@@ -77,6 +83,7 @@ struct Ctx {
   size_t nb = 0;           // bodies (live or dead)
   Particles cur, alt;      // alt = reorder target / scratch
   DBuf<double2> H2new;     // heat double buffer
+  DBuf<double2> C2new;     // concentration double buffer
   DBuf<sphg_body> bodies;
   size_t bodies_cap = 0;
   // rebuild scratch
@@ -148,6 +155,7 @@ void launch_body_kick(Ctx& c);
 void launch_kick_drift(Ctx& c);
 void launch_density(Ctx& c);
 void launch_heat(Ctx& c);
+void launch_diffusion(Ctx& c);
 void launch_extrapolate(Ctx& c);
 void launch_forces(Ctx& c);
 void launch_forces_fluid(Ctx& c);

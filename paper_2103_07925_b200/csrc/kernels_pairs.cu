@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevP
   reinterpret_cast<double*>(&D.G1.p[i])[3] = rho;
   reinterpret_cast<double*>(&D.G2.p[i])[3] = Mt.c2 * (rho - Mt.rho0);
   if (P.thermal) reinterpret_cast<double*>(&D.H2.p[i])[1] = V;
+  if (P.diffusion) reinterpret_cast<double*>(&D.C2.p[i])[1] = V;
 }
 
 // ------------------------------------------------------------------- heat
@@ -182,6 +183,68 @@ __global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevPara
   if (Ma.cp > 0.0) rate = s / (rho_a * Ma.cp);
   Hout[i] = make_double2(hi.x + P.dt * rate, hi.y);
   D.dTdt.p[i] = rate;
+}
+
+// --------------------------------------------------------------- diffusion
+// dC_a/dt = (1/rho_a) sum_b V_b 4 D_a D_b/(D_a+D_b) (C_ab/r_ab) dW/dr (Remark 2.3),
+// b over fluid, rigid and Dirichlet-C boundary particles (V_diff == 0 marks the others).  Particles
+// in a Dirichlet-C group keep C^ (already set at t^{n+1}) [P18].
+template <int G, int M>
+__global__ void __launch_bounds__(kBlock) k_diffusion(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                       const uint32_t* __restrict__ list, size_t nlist,
+                                                       double2* __restrict__ Cout, DevFlags* __restrict__ fl) {
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  const size_t g = t / G;
+  const int lane = (int)(t % G);
+  const bool active = g < nlist;
+  const uint32_t i = active ? list[g] : 0u;
+  double s = 0.0;
+  bool coincident = false;
+  uint32_t kmd = 0;
+  double2 ci = make_double2(0, 0);
+  if (active) {
+    kmd = D.kmd.p[i];
+    const double Da = P.mat[mat_of(kmd)].D;
+    ci = D.C2.p[i];
+    const double3 pi = ldpos(&D.G0.p[i]);
+    const Row R = row_of(L, i);
+    uint32_t en = lane < R.n ? R.at(lane) : 0u;
+    for (int k = lane; k < R.n; k += G) {
+      const uint32_t e = en;
+      en = k + G < R.n ? R.at(k + G) : 0u;
+      const uint32_t j = nb_index<M>(e);
+      const double2 cj = D.C2.p[j];
+      if (cj.y == 0.0) continue;  // boundary without a concentration group
+      const double3 d = pair_delta<M>(P, pi, ldpos(&D.G0.p[j]), e);
+      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+      if (r2 > P.rc2) continue;
+      if (r2 == 0.0) {
+        coincident = true;
+        continue;
+      }
+      const double Db = P.mat[mat_of(D.kmd.p[j])].D;
+      const double ds = Da + Db;
+      if (ds == 0.0) continue;
+      const double dt_ = 4.0 * Da * Db / ds;
+      double rinv;
+      const double dW = P.sig_h * shape_deriv_q(sqrt_and_rinv(r2, rinv) * P.inv_h);
+      s += cj.y * dt_ * ((ci.x - cj.x) * rinv) * dW;
+    }
+  }
+  s = gsum<G>(s);
+  if (!active) return;
+  if (coincident) {
+    atomicOr(&fl->err, kErrCoincident);
+    atomicMin(&fl->err_gid, D.gid.p[i]);
+  }
+  if (lane != 0) return;
+  const DevMat& Ma = P.mat[mat_of(kmd)];
+  const double rho_a = kind_of(kmd) == SPHG_FLUID ? D.G1.p[i].w : Ma.rho0;
+  const double rate = s / rho_a;
+  const bool fixed = dirc_of(kmd) != SPHG_NO_DIRICHLET && (int)dirc_of(kmd) < P.n_schedC &&
+                     P.schedC[dirc_of(kmd)].n > 0;
+  Cout[i] = make_double2(fixed ? ci.x : ci.x + P.dt * rate, ci.y);
+  D.dCdt.p[i] = rate;
 }
 
 // ---------------------------------------------------------- extrapolation
@@ -588,6 +651,21 @@ __global__ void k_dirichlet(const __grid_constant__ DevParams P, Particles D, si
   reinterpret_cast<double*>(&D.H2.p[i])[0] = sched_value(P.sched[gr], t_new);
 }
 
+__global__ void k_dirichlet_c(const __grid_constant__ DevParams P, Particles D, size_t n, double t_new) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t gr = dirc_of(D.kmd.p[i]);
+  if (gr == SPHG_NO_DIRICHLET || (int)gr >= P.n_schedC || P.schedC[gr].n <= 0) return;
+  reinterpret_cast<double*>(&D.C2.p[i])[0] = sched_value(P.schedC[gr], t_new);
+}
+
+__global__ void k_copy_boundary_C(Particles D, size_t n, double2* __restrict__ Cout) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t kmd = D.kmd.p[i];
+  if (kind_of(kmd) == SPHG_BOUNDARY || is_ghost(kmd)) Cout[i] = D.C2.p[i];
+}
+
 template <int G>
 int blocks_for(size_t groups) {
   return grid_for(groups * G, kBlock);
@@ -636,6 +714,22 @@ void launch_heat(Ctx& c) {
                                          c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.H2new.p, c.dflags)));
   k_copy_boundary_T<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.cur, c.n, c.H2new.p);
   std::swap(c.cur.H2, c.H2new);
+  c.launches += 4;
+}
+
+void launch_diffusion(Ctx& c) {
+  if (c.n == 0) return;
+  const double t_new = c.t + c.P.dt;
+  constexpr int G = kGOther;
+  k_dirichlet_c<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new);
+  if (c.nf)
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_diffusion<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.C2new.p, c.dflags)));
+  if (c.nrigid)
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_diffusion<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.C2new.p, c.dflags)));
+  k_copy_boundary_C<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.cur, c.n, c.C2new.p);
+  std::swap(c.cur.C2, c.C2new);
   c.launches += 4;
 }
 

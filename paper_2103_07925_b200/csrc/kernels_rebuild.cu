@@ -68,6 +68,10 @@ __global__ void k_reorder(const uint32_t* __restrict__ perm, const unsigned long
   dst.kmd.p[k] = src.kmd.p[o];
   dst.group.p[k] = src.group.p[o];
   dst.gid.p[k] = src.gid.p[o];
+  if (src.C2.p) {
+    dst.C2.p[k] = src.C2.p[o];
+    dst.dCdt.p[k] = src.dCdt.p[o];
+  }
   cell_key[k] = (uint32_t)skeys[k];
 }
 

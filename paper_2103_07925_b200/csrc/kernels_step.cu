@@ -321,6 +321,10 @@ __global__ void k_gather_by_gid(Particles cur, Particles src, size_t n) {
   cur.p_static.p[k] = src.p_static.p[g];
   cur.kmd.p[k] = src.kmd.p[g];
   cur.group.p[k] = src.group.p[g];
+  if (cur.C2.p) {
+    cur.C2.p[k] = src.C2.p[g];
+    cur.dCdt.p[k] = src.dCdt.p[g];
+  }
 }
 
 __global__ void k_disp(const __grid_constant__ DevParams P, Particles D, size_t n, DevFlags* __restrict__ fl) {
@@ -353,12 +357,13 @@ __global__ void k_halo_pack(Particles D, int phase, const uint32_t* __restrict__
   const uint32_t k = idx[ids[s]];
   if (phase == SPHG_HALO_STATE) {
     const double4 g0 = D.G0.p[k], g1 = D.G1.p[k], g2 = D.G2.p[k], v = D.V4.p[k];
-    double* o = buf + s * 13;
+    double* o = buf + s * 14;
     o[0] = g0.x; o[1] = g0.y; o[2] = g0.z;
     o[3] = g1.x; o[4] = g1.y; o[5] = g1.z;
     o[6] = g2.x; o[7] = g2.y; o[8] = g2.z;
     o[9] = v.x; o[10] = v.y; o[11] = v.z;
     o[12] = D.H2.p[k].x;
+    o[13] = D.C2.p ? D.C2.p[k].x : 0.0;
   } else if (phase == SPHG_HALO_DENSITY) {
     double* o = buf + s * 4;
     o[0] = D.G0.p[k].w; o[1] = D.G1.p[k].w; o[2] = D.G2.p[k].w; o[3] = D.H2.p[k].y;
@@ -378,17 +383,20 @@ __global__ void k_halo_unpack(Particles D, int phase, const uint32_t* __restrict
   double* g1 = reinterpret_cast<double*>(&D.G1.p[k]);
   double* g2 = reinterpret_cast<double*>(&D.G2.p[k]);
   if (phase == SPHG_HALO_STATE) {
-    const double* o = buf + s * 13;
+    const double* o = buf + s * 14;
     g0[0] = o[0]; g0[1] = o[1]; g0[2] = o[2];
     g1[0] = o[3]; g1[1] = o[4]; g1[2] = o[5];
     g2[0] = o[6]; g2[1] = o[7]; g2[2] = o[8];
     double* v = reinterpret_cast<double*>(&D.V4.p[k]);
     v[0] = o[9]; v[1] = o[10]; v[2] = o[11];
     reinterpret_cast<double*>(&D.H2.p[k])[0] = o[12];
+    if (D.C2.p) reinterpret_cast<double*>(&D.C2.p[k])[0] = o[13];
   } else if (phase == SPHG_HALO_DENSITY) {
     const double* o = buf + s * 4;
     g0[3] = o[0]; g1[3] = o[1]; g2[3] = o[2];
     reinterpret_cast<double*>(&D.H2.p[k])[1] = o[3];
+    // fluid diffusion volume m/rho, the same division the owner did (k_density)
+    if (D.C2.p && kind_of(D.kmd.p[k]) == SPHG_FLUID) reinterpret_cast<double*>(&D.C2.p[k])[1] = D.V4.p[k].w / o[1];
   } else {
     const double* o = buf + s * 6;
     g0[3] = o[0]; g1[0] = o[1]; g1[1] = o[2]; g1[2] = o[3]; g1[3] = o[4]; g2[3] = o[5];

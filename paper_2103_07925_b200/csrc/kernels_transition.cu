@@ -30,10 +30,13 @@ __global__ void k_detect(const __grid_constant__ DevParams P, Particles D, size_
   const uint32_t kind = kind_of(kmd);
   const DevMat& M = P.mat[mat_of(kmd)];
   uint32_t e = 0;
-  if (M.has_Tt) {
-    const double T = D.H2.p[k].x;
-    if (kind == SPHG_RIGID && M.melt >= 0 && T > M.T_t) e = 1;
-    else if (kind == SPHG_FLUID && M.solid >= 0 && T < M.T_t) e = 2;
+  // trigger field by TransitionMode (config.hpp:61): 1 temperature, 2 concentration [P19]
+  const bool conc = P.transitions == 2;
+  if (conc ? M.has_Ct : M.has_Tt) {
+    const double x = conc ? D.C2.p[k].x : D.H2.p[k].x;
+    const double thr = conc ? M.C_t : M.T_t;
+    if (kind == SPHG_RIGID && M.melt >= 0 && x > thr) e = 1;
+    else if (kind == SPHG_FLUID && M.solid >= 0 && x < thr) e = 2;
   }
   ev[k] = e;
   if (e == 1) atomicAdd(&fl->n_events, 1u);
@@ -54,7 +57,7 @@ __global__ void k_melt(const __grid_constant__ DevParams P, Particles D, size_t 
   const int tgt = P.mat[mat_of(kmd)].melt;
   const double m = D.V4.p[k].w;
   const double rho0 = P.mat[tgt].rho0;
-  D.kmd.p[k] = (kmd & kGhostBit) | make_kmd(SPHG_FLUID, (uint32_t)tgt, dir_of(kmd));
+  D.kmd.p[k] = (kmd & kGhostBit) | make_kmd(SPHG_FLUID, (uint32_t)tgt, dir_of(kmd), dirc_of(kmd));
   D.group.p[k] = 0;
   D.V4.p[k] = make_double4(u.x, u.y, u.z, m);
   const double V = m / rho0;
@@ -67,6 +70,7 @@ __global__ void k_melt(const __grid_constant__ DevParams P, Particles D, size_t 
   D.X4.p[k] = make_double4(0, 0, 0, 0);
   D.p_static.p[k] = 0.0;
   reinterpret_cast<double*>(&D.H2.p[k])[1] = V;
+  if (D.C2.p) reinterpret_cast<double*>(&D.C2.p[k])[1] = V;
   bmask[body] = 1;
   blost[body] = 1;
 }
@@ -147,7 +151,7 @@ __global__ void k_solid_apply(const __grid_constant__ DevParams P, Particles D, 
   }
   bmask[body] = 1;
   const double rho0 = P.mat[tgt].rho0;
-  D.kmd.p[i] = (kmd & kGhostBit) | make_kmd(SPHG_RIGID, (uint32_t)tgt, dir_of(kmd));
+  D.kmd.p[i] = (kmd & kGhostBit) | make_kmd(SPHG_RIGID, (uint32_t)tgt, dir_of(kmd), dirc_of(kmd));
   D.group.p[i] = body;
   D.A4.p[i] = make_double4(0, 0, 0, 0);
   D.B4.p[i] = make_double4(0, 0, 0, 0);
@@ -156,6 +160,7 @@ __global__ void k_solid_apply(const __grid_constant__ DevParams P, Particles D, 
   D.G1.p[i] = make_double4(0, 0, 0, rho0);
   D.G2.p[i] = make_double4(0, 0, 0, 0);
   reinterpret_cast<double*>(&D.H2.p[i])[1] = v.w / rho0;
+  if (D.C2.p) reinterpret_cast<double*>(&D.C2.p[i])[1] = v.w / rho0;
 }
 
 __global__ void k_iota(uint32_t* __restrict__ a, size_t n, size_t from) {

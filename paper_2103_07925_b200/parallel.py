@@ -261,7 +261,7 @@ class DistributedSimulation:
 
     def step(self, nsteps=1):
         e = self.engine
-        thermal = bool(self.params.thermal)
+        thermal = bool(self.params.thermal) or bool(self.params.diffusion)  # one stage for T and C
         for _ in range(nsteps):
             e.run_stage(abi.STAGE_KICK_DRIFT)
             d = C.c_double(0.0)

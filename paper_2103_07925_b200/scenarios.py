@@ -64,9 +64,10 @@ def lattice_box(lo, hi, dx):
 
 
 def material(rho0, nu=0.0, cp=0.0, kappa=0.0, c=0.0, pb=0.0, T_t=float("nan"),
-             melt=-1, solidify=-1, g=(0.0, 0.0, 0.0)):
+             melt=-1, solidify=-1, g=(0.0, 0.0, 0.0), D=0.0, C_t=float("nan")):
     m = abi.Material()
     m.rho0, m.nu, m.cp, m.kappa, m.c, m.pb, m.T_t = rho0, nu, cp, kappa, c, pb, T_t
+    m.D, m.C_t = D, C_t
     m.melt_target, m.solidify_target = melt, solidify
     for a in range(3):
         m.body_force[a] = g[a]
@@ -456,6 +457,71 @@ def two_phase_with_bodies(nside=128, dx=1e-3, dt=None, seed=2111, n_bodies=200, 
     return Scenario(name, params, s, bodies, steps, info)
 
 
+def dissolving_bodies(nside=32, dx=1e-3, dt=1e-5, seed=2113, n_bodies=4, r_range=(3.0, 5.0), rho=1000.0,
+                      c=10.0, nu_g=1e-5, nu_c=2e-5, D_g=8e-3, D_s=2e-3, D_c=2e-3, C_t=0.8, kc=10.0, zeta=0.1,
+                      jitter=0.05, forcing=False, name="dissolve", steps=200):
+    """Concentration-driven dissolution (PAPER:936 gastric example in 3D SI units):
+    closed box of "gastric juice" held at C = 1 by a Dirichlet concentration group on every juice
+    particle (PAPER: "fixed to C^ = 1.0 at all times"), rigid boluses with C0 = 0 and diffusivity
+    D_s that dissolve into "chyme" (fluid, D_c) when C > C_t = 0.8; juice diffusivity D_g = 4 D_s
+    (the paper's 1.0 : 0.25), equal densities, no gravity, isothermal; concentration transitions
+    (TransitionMode::Concentration).  forcing=True: body concentrations ~ U[C_t - 0.05, C_t + 0.05]
+    so dissolution starts at step 1 (the parity variant)."""
+    L = nside * dx
+    nl = 3
+    lo = (-nl * dx,) * 3
+    hi = (L + nl * dx,) * 3
+    p0 = rho * c * c
+    mats = [material(rho, nu=nu_g, c=c, pb=p0, D=D_g),                 # 0 gastric juice
+            material(rho, c=c, D=D_s, C_t=C_t, melt=2),                 # 1 bolus (solid)
+            material(rho, nu=nu_c, c=c, pb=p0, D=D_c),                  # 2 chyme
+            material(rho, c=c)]                                          # 3 wall (no diffusion)
+    m_r = rho * dx ** 3
+    params = _params(dx, dt, lo, hi, (0, 0, 0), mats, kc=kc, dc=damping_from_ratio(zeta, kc, m_r),
+                     transitions=abi.TRANSITIONS_CONCENTRATION)
+    params.diffusion = 1
+    params.n_dirichlet_c = 1
+    params.dirichlet_C[0].n = 1
+    params.dirichlet_C[0].t_end[0] = 1e30
+    params.dirichlet_C[0].value[0] = 1.0
+    fl = lattice_box((0.0,) * 3, (L,) * 3, dx)
+    wl = lattice_box(lo, hi, dx)
+    wl = wl[np.any((wl < 0.0) | (wl > L), axis=1)]
+    nf, nw = len(fl), len(wl)
+    centers, radii = place_spheres(seed, n_bodies, (0.0,) * 3, (L,) * 3, r_range[0], r_range[1], dx,
+                                   periodic=False)
+    owner = mark_spheres((nside,) * 3, (0.0,) * 3, dx, (L,) * 3, centers, radii, (False,) * 3)
+    n = nf + nw
+    st = ParticleStore(n)
+    u = splitmix_u01(seed, 0, np.arange(3 * nf, dtype=np.uint64)).reshape(nf, 3)
+    st.pos[:nf] = fl + (2.0 * u - 1.0) * (jitter * dx)
+    st.pos[nf:] = wl
+    rig = np.zeros(n, bool)
+    rig[:nf] = owner >= 0
+    st.kind[:nf] = abi.FLUID
+    st.kind[nf:] = abi.BOUNDARY
+    st.kind[rig] = abi.RIGID
+    st.group[rig] = owner[owner >= 0].astype(np.uint32)
+    st.material[:nf] = 0
+    st.material[rig] = 1
+    st.material[nf:] = 3
+    st.mass[:] = m_r
+    st.density[:] = rho
+    juice = st.kind == abi.FLUID
+    st.concentration[juice] = 1.0
+    st.dirichlet_C[juice] = 0
+    if forcing:
+        cu = splitmix_u01(seed, 3, np.arange(n, dtype=np.uint64))
+        st.concentration[rig] = (C_t - 0.05) + 0.1 * cu[rig]
+    bodies = empty_bodies(len(centers))
+    bodies["material"] = 1
+    body_quantities(st, bodies, params)
+    _finish(st, bodies)
+    info = dict(n=n, n_fluid=int(juice.sum()), n_rigid=int(rig.sum()), n_boundary=nw, n_bodies=len(centers),
+                rigid_fraction=float(rig.mean()))
+    return Scenario(name, params, st, bodies, steps, info)
+
+
 def config3(**kw):
     """BASELINE configs[2]: 128^3 two-phase liquid/gas with 200 rigid cubes and spheres."""
     return two_phase_with_bodies(**kw)
@@ -467,4 +533,4 @@ def config2(**kw):
 
 
 def by_name(name, **kw):
-    return {"c1": config1, "c2": config2, "c3": config3, "c5": config5}[name](**kw)
+    return {"c1": config1, "c2": config2, "c3": config3, "c5": config5, "dissolve": dissolving_bodies}[name](**kw)

@@ -136,7 +136,13 @@ class Simulation:
         self.run_stage(abi.STAGE_DENSITY)
 
     def conduction_rhs(self):
-        """apply_thermal_dirichlet + conduction_rhs + explicit T update."""
+        """apply_thermal_dirichlet + conduction_rhs + explicit T update; with
+        params.diffusion also the concentration analogue (one stage)."""
+        self.run_stage(abi.STAGE_HEAT)
+
+    def diffusion_rhs(self):
+        """Dirichlet concentration + diffusion_rhs + explicit C update; shares the
+        stage with conduction_rhs (both run when enabled)."""
         self.run_stage(abi.STAGE_HEAT)
 
     def extrapolate_wall_quantities(self):

@@ -3,8 +3,8 @@
 The fields, their order, dtypes and the interleaved-xyz layout of Vec<3>
 fields are those of the reference container, so a C++ caller can hand its
 ParticleStore vectors to the C ABI unchanged.  The
-concentration fields (store.hpp:36-37,45) are not on the hot path (SURVEY §8(f)
-f2) and are not carried.
+concentration fields (store.hpp:36-37,45) carry the diffusion extension (SURVEY
+§8(f) f2).
 """
 import ctypes as C
 
@@ -13,9 +13,9 @@ import numpy as np
 from . import abi
 
 VEC_FIELDS = ("pos", "vel", "vel_adv", "acc", "acc_bg", "body_frame_pos", "wall_velocity", "force")
-SCALAR_FIELDS = ("density", "pressure", "mass", "temperature", "dT_dt", "wall_pressure")
+SCALAR_FIELDS = ("density", "pressure", "mass", "temperature", "dT_dt", "wall_pressure", "concentration", "dC_dt")
 TAG_FIELDS = {"kind": np.uint8, "group": np.uint32, "material": np.uint16, "dirichlet_T": np.uint8,
-              "owner": np.uint32}
+              "owner": np.uint32, "dirichlet_C": np.uint8}
 
 BODY_DTYPE = np.dtype([
     ("mass", "f8"), ("com", "f8", 3), ("inertia", "f8", 6), ("q", "f8", 4),
@@ -37,6 +37,7 @@ class ParticleStore:
         for f, dt in TAG_FIELDS.items():
             setattr(self, f, np.zeros(self.n, dt))
         self.dirichlet_T[:] = abi.NO_DIRICHLET
+        self.dirichlet_C[:] = abi.NO_DIRICHLET
 
     def __len__(self):
         return self.n

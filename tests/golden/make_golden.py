@@ -24,13 +24,15 @@ from paper_2103_07925_b200.store import VEC_FIELDS, SCALAR_FIELDS, TAG_FIELDS  #
 
 STEPS = 2
 OUT_FIELDS = ("pos", "vel", "density", "pressure", "acc", "acc_bg", "force", "temperature", "dT_dt",
-              "wall_pressure", "wall_velocity", "kind", "group", "material")
-SCALE_KEYS = ("acc", "acc_bg", "dT_dt", "force", "density", "body_force", "body_torque")
+              "wall_pressure", "wall_velocity", "kind", "group", "material", "concentration", "dC_dt",
+              "dirichlet_C")
+SCALE_KEYS = ("acc", "acc_bg", "dT_dt", "force", "density", "body_force", "body_torque", "dC_dt")
 
 CASES = {
     "c1": lambda: scenarios.config1(nside=10, n_spheres=2, r_range=(1.5, 2.5), seed=3),
     "c2m": lambda: scenarios.config2(nside=10, n_grid=2, r_range=(1.5, 2.0), seed=5, melt_forcing=True),
     "c3": lambda: scenarios.config3(nside=10, n_bodies=2, r_range=(1.5, 2.0), seed=9),
+    "dissolve": lambda: scenarios.dissolving_bodies(nside=10, n_bodies=2, r_range=(1.5, 2.0), seed=21, forcing=True),
 }
 
 

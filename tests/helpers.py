@@ -73,6 +73,10 @@ def compare_fields(g, gb, o, ob, s, params, tol=TOL, what=""):
     out["force"] = assert_close(f"{what} force", g.force[rg], o.force[rg], s["force"][rg], tol)
     out["dT_dt"] = assert_close(f"{what} dT_dt", g.dT_dt, o.dT_dt, s["dT_dt"], tol)
     out["temperature"] = assert_close(f"{what} T", g.temperature, o.temperature, 0.0, tol)
+    if params.diffusion:
+        out["dC_dt"] = assert_close(f"{what} dC_dt", g.dC_dt, o.dC_dt, s["dC_dt"], tol)
+        out["concentration"] = assert_close(f"{what} C", g.concentration, o.concentration, 1.0, tol)
+        assert np.array_equal(g.dirichlet_C, o.dirichlet_C), f"{what}: concentration groups differ"
     L = np.array([params.hi[a] - params.lo[a] for a in range(3)])
     out["pos"] = assert_close(f"{what} pos", g.pos, o.pos, float(np.max(L)), 1e-14)
     out["vel"] = assert_close(f"{what} vel", g.vel, o.vel, uscale, 1e-9)

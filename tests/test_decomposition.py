@@ -73,13 +73,13 @@ def _worker(rank, world, port, case, out):
     g, b = ds.gather()
     if rank == 0:
         np.savez(out, pos=g.pos, vel=g.vel, acc=g.acc, acc_bg=g.acc_bg, density=g.density, pressure=g.pressure,
-                 force=g.force, T=g.temperature, dT=g.dT_dt, kind=g.kind,
+                 force=g.force, T=g.temperature, dT=g.dT_dt, kind=g.kind, C=g.concentration,
                  bforce=b["force"], btorque=b["torque"], binertia=b["inertia"], bvel=b["vel"], bcom=b["com"],
                  rebuilds=ds.rebuilds, repart=ds.repartitions)
     dist.destroy_process_group()
 
 
-NSTEPS = {"c1": 6, "c2": 6, "c1fast": 16, "c3": 6}
+NSTEPS = {"c1": 6, "c2": 6, "c1fast": 16, "c3": 6, "diff": 6}
 
 
 def _case(case):
@@ -87,6 +87,10 @@ def _case(case):
         return scenarios.config1(nside=20, n_spheres=3, r_range=(3.0, 4.0), seed=11)
     if case == "c1fast":  # u ~ U(+-1 m/s): Verlet rebuilds every few steps and repartitions
         return scenarios.config1(nside=20, n_spheres=3, r_range=(3.0, 4.0), seed=13, u0=1.0)
+    if case == "diff":  # concentration diffusion with a Dirichlet-C bath (C crosses the halo)
+        sc = scenarios.dissolving_bodies(nside=16, n_bodies=2, r_range=(2.0, 3.0), seed=13)
+        sc.params.transitions = 0
+        return sc
     if case == "c3":  # two phases, cubes and spheres
         return scenarios.config3(nside=20, n_bodies=4, r_range=(2.0, 3.0), seed=7)
     sc = scenarios.config2(nside=16, n_grid=2, r_range=(2.0, 3.0), seed=5)
@@ -94,7 +98,7 @@ def _case(case):
     return sc
 
 
-@pytest.mark.parametrize("case,world", [("c1", 2), ("c2", 2), ("c1fast", 2), ("c3", 2), ("c1", 4)])
+@pytest.mark.parametrize("case,world", [("c1", 2), ("c2", 2), ("c1fast", 2), ("c3", 2), ("diff", 2), ("c1", 4)])
 def test_ranks_match_one_rank(case, world, tmp_path, oracle_mod):
     out = str(tmp_path / "ds.npz")
     mp.spawn(_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
@@ -116,6 +120,7 @@ def test_ranks_match_one_rank(case, world, tmp_path, oracle_mod):
     assert vec_err(d["acc"][fl], g.acc[fl], s["acc"][fl], 1e-8) <= 1
     assert vec_err(d["force"][rg], g.force[rg], s["force"][rg], 1e-8) <= 1
     assert vec_err(d["T"], g.temperature, 0.0, 1e-12) <= 1
+    assert vec_err(d["C"], g.concentration, 1.0, 1e-12) <= 1
     al = b["alive"] == 1
     assert vec_err(d["bforce"][al], b["force"][al], s["body_force"][al], 1e-8) <= 1
     assert vec_err(d["binertia"][al], b["inertia"][al], np.abs(b["inertia"][al][:, :3]).max(1), 1e-12) <= 1

@@ -59,7 +59,7 @@ def check_engine(eng, name, tol_init, tol_step):
 
 
 def test_fixtures_present():
-    assert set(NAMES) >= {"c1", "c2m", "c3"}
+    assert set(NAMES) >= {"c1", "c2m", "c3", "dissolve"}
 
 
 @pytest.mark.parametrize("name", NAMES)

@@ -19,6 +19,8 @@ CASES = {
     "c2_melt": lambda: scenarios.config2(nside=18, n_grid=2, r_range=(2.0, 3.0), seed=5, melt_forcing=True),
     # two phases (multi-EOS / harmonic-mean viscosity / dominant-material wall state), cubes + spheres
     "c3_small": lambda: scenarios.config3(nside=20, n_bodies=4, r_range=(2.0, 3.0), seed=7),
+    # concentration diffusion + Dirichlet-C fluid bath + concentration-mode dissolution at step 1
+    "dissolve": lambda: scenarios.dissolving_bodies(nside=16, n_bodies=3, r_range=(2.0, 3.0), seed=13, forcing=True),
 }
 
 
@@ -110,6 +112,21 @@ def test_multistep_transitions(Oracle):
     assert sim.stats().transitions_solidify == orc.stats().transitions_solidify
     assert sim.stats().rebuilds == orc.stats().rebuilds
     compare_state(sim, orc, sc.params, tol=1e-7, what="c2_melt 6 steps")
+
+
+def test_multistep_dissolve(Oracle):
+    """Diffusion + concentration transitions over several steps: flags exact, fields at the
+    multistep bar."""
+    sc = CASES["dissolve"]()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    for k in range(5):
+        sim.step(1)
+        orc.step(1)
+        g, _ = sim.download()
+        o, _ = orc.download()
+        assert np.array_equal(g.kind, o.kind), f"kind differs after step {k + 1}"
+    assert sim.stats().transitions_melt == orc.stats().transitions_melt > 0
+    compare_state(sim, orc, sc.params, tol=1e-7, what="dissolve 5 steps")
 
 
 def test_multistep_c3_small(Oracle):

@@ -391,6 +391,88 @@ def test_dirichlet_schedule(O):
         assert np.all(g.temperature[bottom] == want)
 
 
+# --------------------------------------------------------------- diffusion
+def _dissolve(**kw):
+    kw.setdefault("nside", 12)
+    kw.setdefault("n_bodies", 1)
+    kw.setdefault("r_range", (3.0, 3.0))
+    return scenarios.dissolving_bodies(**kw)
+
+
+def test_uniform_concentration_no_rate(O):
+    sc = _dissolve()
+    sc.store.concentration[:] = 1.0
+    o = O.Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.initialize()
+    o.diffusion_rhs()
+    g, _ = o.download()
+    assert np.all(g.dC_dt == 0.0)
+    assert np.all(g.concentration == 1.0)
+
+
+def test_two_particle_diffusion_conserves_mC(O):  # sum m_a C_a conserved to round-off
+    sc = _dissolve()
+    p = sc.params
+    p.transitions = 0
+    st = ParticleStore(2)
+    c0 = np.array([0.5 * (p.lo[a] + p.hi[a]) for a in range(3)])
+    st.pos[0] = c0
+    st.pos[1] = c0 + [1.5 * p.dx, 0.0, 0.0]
+    st.kind[:] = abi.FLUID
+    st.material[0], st.material[1] = 0, 2  # different diffusivities (harmonic mean)
+    st.mass[:] = 1000.0 * p.dx ** 3
+    st.density[:] = 1000.0
+    st.concentration[:] = (0.0, 1.0)
+    o = O.Oracle(p)
+    o.upload(st, empty_bodies(0))
+    o.initialize()
+    o.diffusion_rhs()
+    g, _ = o.download()
+    assert g.dC_dt[0] > 0.0 > g.dC_dt[1]
+    mC = g.mass * g.dC_dt
+    assert abs(mC.sum()) <= 1e-14 * np.abs(mC).max()
+
+
+def test_bath_maximum_principle(O):  # body C non-decreasing and bounded by the bath's 1
+    sc = _dissolve()
+    o = O.Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.initialize()
+    rig = sc.store.kind == abi.RIGID
+    prev = sc.store.concentration[rig].copy()
+    for _ in range(5):
+        o.step(2)
+        g, _ = o.download()
+        cur = g.concentration[rig]
+        assert np.all(cur >= prev) and np.all(cur <= 1.0)
+        prev = cur
+    juice = sc.store.dirichlet_C == 0
+    assert np.all(g.concentration[juice] == 1.0)  # [P18] Dirichlet fluid keeps C^
+
+
+def _bolus_at(O, C):
+    sc = _dissolve()
+    rig = sc.store.kind == abi.RIGID
+    sc.store.concentration[rig] = C
+    o = O.Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.initialize()
+    o.apply_transitions()
+    return sc, o
+
+
+def test_concentration_transition_strict_inequality(O):  # SPEC:461-463 in concentration mode
+    sc, o = _bolus_at(O, 0.8)
+    assert o.stats().transitions_melt == 0
+    sc, o = _bolus_at(O, 0.81)  # C_r = 0.81, C_t = 0.8 -> melt
+    g, b = o.download()
+    rig = sc.store.kind == abi.RIGID
+    assert o.stats().transitions_melt == int(rig.sum())
+    assert np.all(g.kind[rig] == abi.FLUID) and np.all(g.material[rig] == 2)  # dissolved into chyme
+    assert b["alive"][0] == 0
+
+
 # -------------------------------------------------------------- transitions
 def _one_body_melt(O, T, u=(0.01, 0.0, 0.0)):
     sc = scenarios.config2(nside=10, n_grid=1, r_range=(2.0, 2.0), T_hot=300.0)
