@@ -199,15 +199,31 @@ struct BuildCtx {
   int cap;
 };
 
-// test the staged batch against every home particle, appending hits to their rows
+// test the staged batch against every home particle, appending hits to their rows.
+// Per chunk of 32 staged candidates each lane (home particle) builds bit masks: (1) fp32 tests,
+// fully unrolled: "inside" (r^2 < r_v^2 (1 - 1e-4)) and "maybe" (r^2 <= r_v^2 (1 + 1e-4)); (2) the
+// rare guard-band bits get the pinned exact fp64 test [P2]; (3) self and boundary-boundary bits are
+// cleared with per-chunk masks built at staging; (4) the lane appends its fluid hits to the front
+// of its row and the others to the back, one short loop iteration per hit.
 __device__ __forceinline__ void build_batch(const DevParams& P, const double4* __restrict__ G0,
                                             const uint32_t* __restrict__ kmd, uint32_t* __restrict__ nbr, int cap,
                                             uint32_t h0, uint32_t h1, double ox0, double oy0, double oz0,
                                             const float4* sp, const uint32_t* se, int ns, uint32_t* hc,
+                                            const uint32_t* hs, uint32_t batch, uint32_t* fmask, uint32_t* bmask,
                                             uint32_t emask) {
   const int lane = threadIdx.x & 31;
   const float rv2 = (float)(P.rv2 * P.inv_h * P.inv_h);
   const float lo_band = rv2 * (1.0f - 1e-4f), hi_band = rv2 * (1.0f + 1e-4f);
+  // per-chunk kind masks of the staged candidates (padding dummies count as fluid; they never hit)
+  for (int tb = 0; tb < ns; tb += 32) {
+    const float w = sp[tb + lane].w;
+    const uint32_t f = __ballot_sync(0xffffffffu, w == 0.f), bd = __ballot_sync(0xffffffffu, w == 2.f);
+    if (lane == 0) {
+      fmask[tb >> 5] = f;
+      bmask[tb >> 5] = bd;
+    }
+  }
+  __syncwarp();
   for (uint32_t ib = h0; ib < h1; ib += 32) {
     const uint32_t i = ib + lane;
     const bool act = i < h1 && !is_ghost(kmd[i]);
@@ -215,6 +231,7 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
     float xi = 0.f, yi = 0.f, zi = 0.f;
     bool bi = false;
     uint32_t count = 0;
+    int self = -1;  // this batch's stage index of particle i itself
     if (act) {
       pi = G0[i];
       xi = (float)((pi.x - ox0) * P.inv_h);
@@ -222,46 +239,45 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
       zi = (float)((pi.z - oz0) * P.inv_h);
       bi = kind_of(kmd[i]) == SPHG_BOUNDARY;
       count = hc[i - h0];
+      const uint32_t h = hs[i - h0];
+      if ((h >> 16) == batch) self = (int)(h & 0xffffu);
     }
     uint32_t nf = cnt_fluid(count), no = cnt_other(count);
     uint32_t* row = nbr + (size_t)i * cap;
     uint32_t* back = row + cap - 1;
-    // two phases per chunk of 32 staged candidates: (1) fp32 tests into a per-lane bit mask
-    // (fully unrolled; the stage is padded with far-away dummies), (2) each lane walks only its
-    // own set bits.  Hits are ~15% of candidates, so phase 2 runs ~5 times per 32 per lane.
     for (int tb = 0; tb < ns; tb += 32) {
-      uint32_t m = 0;
+      uint32_t in = 0, maybe = 0;
 #pragma unroll
       for (int u = 0; u < 32; ++u) {
         const float4 q = sp[tb + u];
         const float dx = xi - q.x, dy = yi - q.y, dz = zi - q.z;
         const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        m |= (r2 <= hi_band) ? (1u << u) : 0u;
+        maybe |= (r2 <= hi_band) ? (1u << u) : 0u;
+        in |= (r2 < lo_band) ? (1u << u) : 0u;
       }
-      if (!act) m = 0;
-      while (m) {
-        const int u = __ffs(m) - 1;
-        m &= m - 1;
-        const int t = tb + u;
-        const uint32_t e = se[t];
-        const float4 q = sp[t];
-        const uint32_t j = e & emask;
-        if (j == i || (bi && q.w == 2.f)) continue;
-        const float dx = xi - q.x, dy = yi - q.y, dz = zi - q.z;
-        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        bool hit = r2 < lo_band;
-        if (!hit) {  // guard band: the pinned exact test
-          const double4 pj = G0[j];
-          hit = r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) <= P.rv2;
-        }
-        if (!hit) continue;
-        if (q.w == 0.f) {  // fluid neighbours from the front, others from the back
-          if ((int)nf < cap) row[nf] = e;
-          ++nf;
-        } else {
-          if ((int)no < cap) back[-(int)no] = e;
-          ++no;
-        }
+      if (!act) maybe = in = 0;
+      uint32_t band = maybe & ~in;
+      while (band) {  // guard band: the pinned exact test (rare)
+        const int u = __ffs(band) - 1;
+        band &= band - 1;
+        const double4 pj = G0[se[tb + u] & emask];
+        if (r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) <= P.rv2) in |= 1u << u;
+      }
+      if (self >= tb && self < tb + 32) in &= ~(1u << (self - tb));
+      if (bi) in &= ~bmask[tb >> 5];
+      const uint32_t fm = fmask[tb >> 5];
+      uint32_t hf = in & fm, ho = in & ~fm;
+      while (hf) {  // fluid neighbours from the front
+        const int u = __ffs(hf) - 1;
+        hf &= hf - 1;
+        if ((int)nf < cap) row[nf] = se[tb + u];
+        ++nf;
+      }
+      while (ho) {  // rigid / boundary neighbours from the back
+        const int u = __ffs(ho) - 1;
+        ho &= ho - 1;
+        if ((int)no < cap) back[-(int)no] = se[tb + u];
+        ++no;
       }
     }
     if (act) hc[i - h0] = pack_cnt(nf, no);
@@ -278,10 +294,13 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
   __shared__ float4 sp_all[kBuildWarps][kStage];     // x, y, z (relative to the home cell, units of h), kind
   __shared__ uint32_t se_all[kBuildWarps][kStage];   // neighbour index | image code
   __shared__ uint32_t hc_all[kBuildWarps][kHomeMax]; // running row length per home particle
+  __shared__ uint32_t hs_all[kBuildWarps][kHomeMax]; // (batch << 16 | stage index) of each home particle
+  __shared__ uint32_t fm_all[kBuildWarps][kStage / 32], bm_all[kBuildWarps][kStage / 32];
   const int wib = threadIdx.x >> 5;
   float4* sp = sp_all[wib];
   uint32_t* se = se_all[wib];
   uint32_t* hc = hc_all[wib];
+  uint32_t* hs = hs_all[wib];
   const int64_t c = brick_to_cell(P.ncell, (int64_t)blockIdx.x * kBuildWarps + wib);
   if (c < 0) return;
   const int lane = threadIdx.x & 31;
@@ -291,7 +310,10 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
     if (lane == 0) atomicOr(&fl->build_overflow, 1u);
     return;
   }
-  for (uint32_t k = lane; k < h1 - h0; k += 32) hc[k] = 0;
+  for (uint32_t k = lane; k < h1 - h0; k += 32) {
+    hc[k] = 0;
+    hs[k] = 0xffffffffu;
+  }
   const int64_t nz = P.ncell[2], ny = P.ncell[1], nx = P.ncell[0];
   const int64_t cz = c % nz, cy = (c / nz) % ny, cx = c / (nz * ny);
   const double ox0 = P.lo[0] + (double)cx / P.inv_edge[0];  // any fixed origin near the cell works
@@ -300,6 +322,7 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
   const bool code = P.img_mode == kImgCode;
   const uint32_t emask = code ? kIdxMask : 0xffffffffu;
   int ns = 0;
+  uint32_t batch = 0;
   for (int ox = -1; ox <= 1; ++ox) {
     int64_t qx = cx + ox;
     uint32_t ix = 0;
@@ -332,6 +355,7 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
         }
         const uint32_t tag = code ? ((ix << 26) | (iy << 28) | (iz << 30)) : 0u;
         const int64_t cj = (qx * ny + qy) * nz + qz;
+        const bool home = ox == 0 && oy == 0 && oz == 0;
         const uint32_t j0 = cstart[cj], j1 = cend[cj];
         for (uint32_t jb = j0; jb < j1;) {
           const int take = (int)min((uint32_t)(kStage - ns), j1 - jb);
@@ -343,14 +367,17 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
                                      (float)((pj.z + sz - oz0) * P.inv_h),
                                      (float)kind_of(kmd[j]));  // 0 fluid, 1 rigid, 2 boundary
             se[ns + t] = j | tag;
+            if (home) hs[j - h0] = (batch << 16) | (uint32_t)(ns + t);
           }
           ns += take;
           jb += take;
           if (ns == kStage) {
             __syncwarp();
-            build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, sp, se, ns, hc, emask);
+            build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, sp, se, ns, hc, hs, batch, fm_all[wib],
+                        bm_all[wib], emask);
             __syncwarp();
             ns = 0;
+            ++batch;
           }
         }
       }
@@ -364,7 +391,8 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
       se[t] = 0u;
     }
     __syncwarp();
-    build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, sp, se, padded, hc, emask);
+    build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, sp, se, padded, hc, hs, batch, fm_all[wib],
+                bm_all[wib], emask);
   }
   __syncwarp();
   uint32_t mx = 0;
