@@ -1024,7 +1024,8 @@ int sphg_body_partials(sphg_ctx* h, double* out) {
     c.body_buf.alloc(c.nb * 24);
     SPHG_CUDA_CHECK(cudaMemsetAsync(c.body_buf.p, 0, c.nb * 24 * sizeof(double), c.stream));
     body_partials(c, c.body_buf.p);
-    d2h(out, c.body_buf.p, c.nb * 24, c.stream);
+    // host or device destination (the multi-rank driver gathers device tensors over NCCL)
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(out, c.body_buf.p, c.nb * 24 * sizeof(double), cudaMemcpyDefault, c.stream));
     SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     return SPHG_OK;
   });
@@ -1035,7 +1036,7 @@ int sphg_body_apply_totals(sphg_ctx* h, const double* tot) {
     Ctx& c = h->c;
     if (c.nb == 0) return SPHG_OK;
     c.body_buf.alloc(c.nb * 24);
-    h2d(c.body_buf.p, tot, c.nb * 12, c.stream);
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(c.body_buf.p, tot, c.nb * 12 * sizeof(double), cudaMemcpyDefault, c.stream));
     body_apply_totals(c, c.body_buf.p);
     SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     return SPHG_OK;

@@ -90,9 +90,10 @@ class Grid:
 
 
 def _merge_partials(parts):
-    """Merge per-rank (sum, comp) partials in rank order with TwoSum (numpy: IEEE, no FMA)."""
-    s = parts[0][..., 0].copy()
-    c = parts[0][..., 1].copy()
+    """Merge per-rank (sum, comp) partials in rank order with TwoSum.  Works on numpy arrays
+    (host) and torch tensors (device): single IEEE adds/subs, no FMA, so both give the same bits."""
+    s = parts[0][..., 0].clone() if torch.is_tensor(parts[0]) else parts[0][..., 0].copy()
+    c = parts[0][..., 1].clone() if torch.is_tensor(parts[0]) else parts[0][..., 1].copy()
     for p in parts[1:]:
         s2, c2 = p[..., 0], p[..., 1]
         t = s + s2
@@ -227,8 +228,21 @@ class DistributedSimulation:
         nb = e.num_bodies()
         if nb == 0:
             return
+        dp = C.POINTER(C.c_double)
+        if self.dev.type == "cuda" and self.edev.type == "cuda":
+            # device path: partials -> NCCL all_gather -> TwoSum merge in rank order on the GPU -> totals
+            mine = torch.empty((nb, 12, 2), dtype=torch.float64, device=self.dev)
+            e._check(e._fn("body_partials")(e._h, C.cast(mine.data_ptr(), dp)), "body_partials")
+            t0 = time.perf_counter()
+            gathered = [torch.empty_like(mine) for _ in range(self.world)]
+            dist.all_gather(gathered, mine, group=self.group)
+            tot = _merge_partials(gathered).contiguous()
+            torch.cuda.current_stream(self.dev).synchronize()  # the engine reads tot on its own stream
+            self.comm_s += time.perf_counter() - t0
+            e._check(e._fn("body_apply_totals")(e._h, C.cast(tot.data_ptr(), dp)), "body_apply_totals")
+            return
         part = np.zeros((nb, 12, 2))
-        e._check(e._fn("body_partials")(e._h, part.ctypes.data_as(C.POINTER(C.c_double))), "body_partials")
+        e._check(e._fn("body_partials")(e._h, part.ctypes.data_as(dp)), "body_partials")
         t0 = time.perf_counter()
         mine = torch.from_numpy(part).to(self.dev)
         gathered = [torch.empty_like(mine) for _ in range(self.world)]
@@ -236,7 +250,7 @@ class DistributedSimulation:
         parts = [g.cpu().numpy() for g in gathered]
         self.comm_s += time.perf_counter() - t0
         tot = np.ascontiguousarray(_merge_partials(parts))
-        e._check(e._fn("body_apply_totals")(e._h, tot.ctypes.data_as(C.POINTER(C.c_double))), "body_apply_totals")
+        e._check(e._fn("body_apply_totals")(e._h, tot.ctypes.data_as(dp)), "body_apply_totals")
 
     def _allmax(self, x):
         t = torch.tensor([x], dtype=torch.float64, device=self.dev)

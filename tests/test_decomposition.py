@@ -124,3 +124,13 @@ def test_ranks_match_one_rank(case, world, tmp_path, oracle_mod):
     al = b["alive"] == 1
     assert vec_err(d["bforce"][al], b["force"][al], s["body_force"][al], 1e-8) <= 1
     assert vec_err(d["binertia"][al], b["inertia"][al], np.abs(b["inertia"][al][:, :3]).max(1), 1e-12) <= 1
+
+
+def test_merge_partials_torch_matches_numpy():
+    """The device merge (torch ops) and the host merge (numpy) give identical bits."""
+    import torch
+    rng = np.random.default_rng(5)
+    parts = [rng.standard_normal((7, 12, 2)) * 10.0 ** rng.integers(-8, 8, (7, 12, 2)) for _ in range(4)]
+    a = _merge_partials(parts)
+    b = _merge_partials([torch.from_numpy(p) for p in parts]).numpy()
+    assert np.array_equal(a, b)

@@ -62,3 +62,36 @@ def test_gpu_two_ranks_match_single_rank(case, tmp_path):
     assert vec_err(d["force"][rg], g.force[rg], s["force"][rg], 1e-8) <= 1
     al = b["alive"] == 1
     assert vec_err(d["bforce"][al], b["force"][al], s["body_force"][al], 1e-8) <= 1
+
+
+def test_body_partials_device_pointers():
+    """sphg_body_partials / sphg_body_apply_totals accept device pointers (the NCCL path of
+    DistributedSimulation._bodies) and give the same result as host pointers."""
+    import ctypes as C
+    import torch
+    from paper_2103_07925_b200 import scenarios, Simulation
+    sc = scenarios.config1(nside=20, n_spheres=3, r_range=(3.0, 4.0), seed=11)
+    dp = C.POINTER(C.c_double)
+    out = []
+    for dev in ("host", "cuda"):
+        sim = Simulation(sc.params, device=0)
+        sim.upload(sc.store, sc.bodies)
+        sim.initialize()
+        nb = sim.num_bodies()
+        if dev == "host":
+            part = np.zeros((nb, 12, 2))
+            sim._check(sim._fn("body_partials")(sim._h, part.ctypes.data_as(dp)), "partials")
+            tot = np.ascontiguousarray(part[..., 0] + part[..., 1])
+            sim._check(sim._fn("body_apply_totals")(sim._h, tot.ctypes.data_as(dp)), "apply")
+        else:
+            part = torch.zeros((nb, 12, 2), dtype=torch.float64, device="cuda")
+            sim._check(sim._fn("body_partials")(sim._h, C.cast(part.data_ptr(), dp)), "partials")
+            tot = (part[..., 0] + part[..., 1]).contiguous()
+            torch.cuda.synchronize()
+            sim._check(sim._fn("body_apply_totals")(sim._h, C.cast(tot.data_ptr(), dp)), "apply")
+            part = part.cpu().numpy()
+        _, b = sim.download()
+        out.append((part, b))
+    assert np.array_equal(out[0][0], out[1][0])
+    for f in ("force", "torque", "acc", "alpha"):
+        assert np.array_equal(out[0][1][f], out[1][1][f]), f
