@@ -183,7 +183,10 @@ def run_sph(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         from paper_2103_07925_b200 import parallel
-        return parallel.bench_multi(args)
+        line = parallel.bench_multi(args, clock_factory=ClockSampler)
+        if line is not None:
+            print(json.dumps(line))
+        return
     torch.cuda.set_device(local)
     t_gen = time.perf_counter()
     sc = scenarios.config5(nside=args.nside, n_spheres=args.spheres)

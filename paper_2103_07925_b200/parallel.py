@@ -316,9 +316,10 @@ class DistributedSimulation:
 
 
 # ---------------------------------------------------------------- bench N>1
-def bench_multi(args):
+def bench_multi(args, clock_factory=None):
     """Strong scaling on the C5 config: rank 0 generates the seeded global store and
-    ships each rank its box + ghost shell; K steps; value = all particles x K / max rank time."""
+    ships each rank its box + ghost shell; K steps; value = all particles x K / max rank time.
+    Returns rank 0's JSON line (dict), None on the other ranks."""
     import json
     from . import scenarios
     from .sim import Simulation
@@ -389,14 +390,56 @@ def bench_multi(args):
     ds.step(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
-    t0 = time.perf_counter()
-    ds.step(args.steps)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    st0 = ds.engine.stats()
+    import contextlib
+    clk = clock_factory(gpu) if clock_factory is not None else contextlib.nullcontext()
+    with clk:
+        t0 = time.perf_counter()
+        ds.step(args.steps)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    launches = ds.engine.stats().kernel_launches - st0.kernel_launches
     dist.barrier()
     tmax = torch.tensor([dt], dtype=torch.float64, device=dev)
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     dt = float(tmax.item())
+    tl = torch.tensor([float(launches)], dtype=torch.float64, device=dev)
+    dist.all_reduce(tl, op=dist.ReduceOp.SUM)
+    # e2e through the public API on every rank: pinned host positions / velocities of the rank's
+    # particles -> upload_state -> one decomposed step -> download of pos, vel, density, pressure
+    e2e = None
+    if not getattr(args, "no_e2e", False) and getattr(args, "e2e_steps", 0) > 0:
+        eng = ds.engine
+        m = eng.n
+        loc, _ = eng.download(fields=("pos", "vel"))
+        pin = {f: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+               for f, shape in (("pos", (m, 3)), ("vel", (m, 3)), ("density", (m,)), ("pressure", (m,)))}
+        pin["pos"][:] = loc.pos
+        pin["vel"][:] = loc.vel
+        out = ParticleStore(0)
+        out.n = m
+        for f in VEC_FIELDS + SCALAR_FIELDS:
+            setattr(out, f, pin.get(f, np.zeros((m, 3) if f in VEC_FIELDS else m)))
+        for f, dt_ in TAG_FIELDS.items():
+            setattr(out, f, np.zeros(m, dt_))
+        torch.cuda.synchronize()
+        dist.barrier()
+        t1 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            eng.upload_state(pin["pos"], pin["vel"])
+            ds.step(1)
+            eng.download(out, fields=("pos", "vel", "density", "pressure"))
+        te = time.perf_counter() - t1
+        te_t = torch.tensor([te], dtype=torch.float64, device=dev)
+        dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
+        hb = torch.tensor([48.0 * m, 64.0 * m], dtype=torch.float64, device=dev)
+        dist.all_reduce(hb, op=dist.ReduceOp.SUM)
+        e2e = {"value": n_total * args.e2e_steps / float(te_t.item()), "unit": "particle-steps/s",
+               "h2d_bytes_per_step": int(hb[0].item()), "d2h_bytes_per_step": int(hb[1].item()),
+               "steps": args.e2e_steps,
+               "path": "per rank: upload_state(pos, vel of owned + ghost particles from pinned host) -> "
+                       "DistributedSimulation.step(1) -> download(pos, vel, density, pressure into pinned host); "
+                       "host wall clock, max over ranks"}
     n = n_total
     if rank == 0:
         line = {"metric": "particle-steps/sec (full SPH step, fp64)", "value": n * args.steps / dt,
@@ -408,6 +451,10 @@ def bench_multi(args):
                            "ghost_width_h": ds.width / ds.h},
                 "timing": "host wall clock between barriers + cuda synchronize, max over ranks "
                           "(the per-rank step mixes kernels and NCCL exchanges)",
-                "comm_s_rank0": ds.comm_s, "rebuilds": ds.rebuilds, "repartitions": ds.repartitions}
-        print(json.dumps(line))
+                "comm_s_rank0": ds.comm_s, "rebuilds": ds.rebuilds, "repartitions": ds.repartitions,
+                "gpu_launches": int(tl.item()), "e2e": e2e, "roofline": None,
+                "roofline_note": "per-kernel roofline is reported by the N=1 line; N>1 adds halo/body exchanges"}
+        if clock_factory is not None:
+            line["clocks"] = clk.summary()
     dist.destroy_process_group()
+    return line if rank == 0 else None
