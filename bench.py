@@ -41,19 +41,36 @@ FLOPS_PER_PAIR_DENSITY = 17.0
 STEP_BYTES_PER_PARTICLE = 480.0
 
 
+DEFAULT_NSIDE = {"c5": 400, "c1": 32, "c2": 64, "c3": 128, "dissolve": 64}
+
+
+def make_scenario(args):
+    from paper_2103_07925_b200 import scenarios
+    if args.config == "c5":
+        return scenarios.config5(nside=args.nside, n_spheres=args.spheres)
+    if args.config == "c1":
+        return scenarios.config1(nside=args.nside)
+    return scenarios.by_name(args.config, nside=args.nside)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)  # C5: 100 steps (Verlet rebuilds included as they occur)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sph", choices=["sph", "reference"])
-    ap.add_argument("--nside", type=int, default=400)
+    ap.add_argument("--config", default="c5", choices=["c5", "c1", "c2", "c3", "dissolve"],
+                    help="c5 = the headline workload (BASELINE metric); the others are secondary measurements")
+    ap.add_argument("--nside", type=int, default=None, help="lattice side (default: the config's BASELINE size)")
     ap.add_argument("--spheres", type=int, default=20000)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-nside", type=int, default=96)
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.nside is None:
+        args.nside = DEFAULT_NSIDE[args.config]
+    return args
 
 
 def load_peaks():
@@ -189,7 +206,7 @@ def run_sph(args):
         return
     torch.cuda.set_device(local)
     t_gen = time.perf_counter()
-    sc = scenarios.config5(nside=args.nside, n_spheres=args.spheres)
+    sc = make_scenario(args)
     t_gen = time.perf_counter() - t_gen
     n = sc.store.n
     sim = Simulation(sc.params, device=local)
@@ -269,8 +286,12 @@ def run_sph(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64 lattice + jitter)",
-            "config": {"workload": f"C5 {args.nside}^3 periodic, {info['n_bodies']} rigid spheres R~U[3,6]dx",
+            "config": {"workload": (f"C5 {args.nside}^3 periodic, {info['n_bodies']} rigid spheres R~U[3,6]dx"
+                                    if args.config == "c5" else
+                                    f"{args.config} nside {args.nside}, {info['n_bodies']} bodies, "
+                                    f"{info.get('n_boundary', 0)} wall particles (secondary measurement)"),
                        "particles": n, "fluid": nf, "rigid": info["n_rigid"],
+                       "fluid_rigid_rate": (nf + info["n_rigid"]) / (ms_step * 1e-3),
                        "rigid_fraction": round(info["rigid_fraction"], 4), "parallelism": "1 GPU",
                        "l2": "inputs larger than L2 (state ~%.1f GB)" % (store_bytes(sc.store) / 1e9)},
             "roofline": roofline, "fp64": fp64, "stage_ms": stage_ms, "rebuild_ms": rebuild_ms,
@@ -306,7 +327,7 @@ def run_sph(args):
                        "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
                        "path": "Simulation.upload_state(pos, vel from pinned host) -> step(1) -> "
                                "download(pos, vel, density, pressure into pinned host arrays); host wall clock"}
-    if not args.no_cpu_baseline and rank == 0:
+    if not args.no_cpu_baseline and rank == 0 and args.config == "c5":
         line["cpu_baseline"] = cpu_baseline(args.cpu_nside, args.spheres, args.nside)
     sim.close()
     print(json.dumps(line))
