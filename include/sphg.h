@@ -207,6 +207,24 @@ int sphg_dt_limits(const sphg_params* params, double u_max, double m_r, double l
 /* Pair counts of the current Verlet list: [0] candidates, [1] within r_c (interacting),
  * [2] interacting with a fluid particle i (the fluid force kernel's pairs), [3] with a non-fluid i. */
 int sphg_count_pairs(sphg_ctx* ctx, int64_t counts[4]);
+
+/* shepard_interpolate (the Shepard filter used for every field
+ * figure) on a regular grid, the post-processing gather behind OutputPlan::shepard_grid
+ * (config.hpp:53-59):
+ *   f^(x) = sum_j V_j f_j W(|x - r_j|, h) / sum_j V_j W(|x - r_j|, h),  V_j = m_j / rho_j
+ * over the particles whose kind bit is set in kind_mask (1 << SPHG_FLUID | ...), minimum image on
+ * periodic axes.  Grid point (a, b, c) = origin + (a, b, c) * spacing, stored z fastest:
+ * out[((a * dims[1] + b) * dims[2] + c) * ncomp + comp].  A point with no particle within r_c
+ * gets NaN and support = 0 ("no support" signal); support may be NULL. */
+enum {
+  SPHG_FIELD_VELOCITY = 0,      /* 3 components */
+  SPHG_FIELD_TEMPERATURE = 1,
+  SPHG_FIELD_CONCENTRATION = 2,
+  SPHG_FIELD_PRESSURE = 3,
+  SPHG_FIELD_DENSITY = 4
+};
+int sphg_shepard_grid(sphg_ctx* ctx, const double origin[3], const double spacing[3], const int32_t dims[3],
+                      int32_t field, uint32_t kind_mask, double* out, uint8_t* support);
 /* ---- domain decomposition primitives (one context per rank).
  * The host layer (paper_2103_07925_b200/parallel.py) owns the exchange; these move data between the
  * context and contiguous halo records.  Ghosts are the uploaded particles with owner != rank: they are

@@ -1245,6 +1245,50 @@ int orc_get_nlist(orc_ctx* h, int64_t* offsets, uint32_t* nbr) {
 }
 
 // tolerance scales, gid order
+// shepard_interpolate on a grid: brute force over all particles in gid order.
+int orc_shepard_grid(orc_ctx* h, const double* origin, const double* spacing, const int32_t* dims, int32_t field,
+                     uint32_t kind_mask, double* out, uint8_t* support) {
+    const Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (dims[0] < 0 || dims[1] < 0 || dims[2] < 0 || field < 0 || field > SPHG_FIELD_DENSITY) return SPHG_ERR_CONFIG;
+    const int nc = field == SPHG_FIELD_VELOCITY ? 3 : 1;
+    const sphfsi::QuinticKernel<3> K(c.P.h > 0.0 ? c.P.h : c.P.dx);
+    const double rc = sphfsi::kKernelSupportScale * (c.P.h > 0.0 ? c.P.h : c.P.dx);
+    const double rc2 = rc * rc;
+    const size_t n = c.S.size();
+    const int64_t np = (int64_t)dims[0] * dims[1] * dims[2];
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < np; ++q) {
+        const int64_t a = q / ((int64_t)dims[1] * dims[2]), b = (q / dims[2]) % dims[1], cc = q % dims[2];
+        const V3 x{origin[0] + (double)a * spacing[0], origin[1] + (double)b * spacing[1],
+                   origin[2] + (double)cc * spacing[2]};
+        double num[3] = {0, 0, 0}, den = 0.0;
+        for (size_t j = 0; j < n; ++j) {
+            if (!((kind_mask >> static_cast<uint32_t>(c.S.kind[j])) & 1u) || ghost(c, j)) continue;
+            const double r2 = r2of(mi3(c, x, c.S.pos[j]));
+            if (r2 > rc2) continue;
+            const sphfsi::Material& m = c.mats[c.S.material[j]];
+            const double rho = c.S.kind[j] == Kind::Fluid ? c.S.density[j] : m.reference_density;
+            const double w = (c.S.mass[j] / rho) * K.w(std::sqrt(r2));
+            den += w;
+            switch (field) {
+                case SPHG_FIELD_VELOCITY:
+                    for (int k = 0; k < 3; ++k) num[k] += w * c.S.vel[j][k];
+                    break;
+                case SPHG_FIELD_TEMPERATURE: num[0] += w * c.S.temperature[j]; break;
+                case SPHG_FIELD_CONCENTRATION: num[0] += w * c.S.concentration[j]; break;
+                case SPHG_FIELD_PRESSURE:
+                    num[0] += w * (c.S.kind[j] == Kind::Fluid ? c.S.pressure[j] : c.S.wall_pressure[j]);
+                    break;
+                default: num[0] += w * rho; break;
+            }
+        }
+        const bool ok = den > 0.0;
+        for (int k = 0; k < nc; ++k) out[q * nc + k] = ok ? num[k] / den : kNaN;
+        if (support) support[q] = ok ? 1 : 0;
+    }
+    return SPHG_OK;
+}
+
 int orc_get_scale_dC(orc_ctx* h, double* dC) {
     const Ctx& c = *reinterpret_cast<Ctx*>(h);
     std::copy(c.dC_scale.begin(), c.dC_scale.end(), dC);

@@ -28,6 +28,7 @@ STAGE_MASS = 9
 
 HALO_STATE, HALO_DENSITY, HALO_WALL = 0, 1, 2
 TRANSITIONS_NONE, TRANSITIONS_TEMPERATURE, TRANSITIONS_CONCENTRATION = 0, 1, 2  # config.hpp:61
+FIELD_VELOCITY, FIELD_TEMPERATURE, FIELD_CONCENTRATION, FIELD_PRESSURE, FIELD_DENSITY = 0, 1, 2, 3, 4
 MAX_HALO_SLOTS = 64
 
 STAGE_NAMES = ["rebuild", "density", "heat", "extrapolate", "forces", "bodies",
@@ -135,6 +136,8 @@ def declare(lib, prefix):
         "max_displacement": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "halo_doubles": (C.c_int, [C.c_int]),
         "upload_state": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_size_t]),
+        "shepard_grid": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32),
+                                   C.c_int32, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint8)]),
     }
     for name, (res, args) in list(sig.items()) + list(optional.items()):
         fn = getattr(lib, prefix + name, None)

@@ -7,7 +7,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsphg.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["radix_sort.cu", "kernels_rebuild.cu", "kernels_step.cu", "kernels_pairs.cu", "kernels_transition.cu", "api.cu"]
+SOURCES = ["radix_sort.cu", "kernels_rebuild.cu", "kernels_step.cu", "kernels_pairs.cu", "kernels_transition.cu",
+           "kernels_post.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fopenmp",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-ccbin", "/usr/bin/g++"]

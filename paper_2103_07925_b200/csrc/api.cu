@@ -973,6 +973,40 @@ int sphg_count_pairs(sphg_ctx* h, int64_t out[4]) {
   });
 }
 
+int sphg_shepard_grid(sphg_ctx* h, const double origin[3], const double spacing[3], const int32_t dims[3],
+                      int32_t field, uint32_t kind_mask, double* out, uint8_t* support) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    SPHG_CUDA_CHECK(cudaSetDevice(c.device));
+    if (dims[0] < 0 || dims[1] < 0 || dims[2] < 0 || field < 0 || field > SPHG_FIELD_DENSITY)
+      return fail(h, SPHG_ERR_CONFIG, "shepard_grid: bad dims or field");
+    if (!c.have_state) return fail(h, SPHG_ERR_RUNTIME, "no particle state uploaded");
+    const int64_t np = (int64_t)dims[0] * dims[1] * dims[2];
+    const int nc = field == SPHG_FIELD_VELOCITY ? 3 : 1;
+    if (np == 0) return SPHG_OK;
+    if (c.n == 0) {  // nothing supports any point
+      for (int64_t q = 0; q < np * nc; ++q) out[q] = std::numeric_limits<double>::quiet_NaN();
+      if (support) std::memset(support, 0, (size_t)np);
+      return SPHG_OK;
+    }
+    if (!c.built) {
+      const int rc = do_stage(h, SPHG_STAGE_REBUILD);
+      if (rc) return rc;
+    }
+    DBuf<double> dout;
+    DBuf<uint8_t> dsup;
+    dout.alloc((size_t)np * nc);
+    if (support) dsup.alloc((size_t)np);
+    shepard_grid(c, origin, spacing, dims, field, kind_mask, dout.p, support ? dsup.p : nullptr);
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(out, dout.p, (size_t)np * nc * sizeof(double), cudaMemcpyDefault, c.stream));
+    if (support) SPHG_CUDA_CHECK(cudaMemcpyAsync(support, dsup.p, (size_t)np, cudaMemcpyDefault, c.stream));
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    dout.free();
+    dsup.free();
+    return SPHG_OK;
+  });
+}
+
 int sphg_halo_doubles(int phase) {
   return phase == SPHG_HALO_STATE ? 14 : phase == SPHG_HALO_DENSITY ? 4 : phase == SPHG_HALO_WALL ? 6 : -1;
 }

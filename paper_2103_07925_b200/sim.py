@@ -186,6 +186,25 @@ class Simulation:
     def set_timing(self, enabled=True):
         self._check(self._fn("set_timing")(self._h, int(bool(enabled))), "set_timing")
 
+    def shepard_grid(self, origin, spacing, dims, field=abi.FIELD_VELOCITY, kinds=(abi.FLUID,)):
+        """shepard_interpolate (SPEC:123-131) on a regular grid (OutputPlan::shepard_grid,
+        config.hpp:53-59).  Returns (values[dims..., ncomp] with NaN where unsupported, support)."""
+        o = np.ascontiguousarray(origin, np.float64)
+        sp = np.ascontiguousarray(spacing, np.float64)
+        d = np.ascontiguousarray(dims, np.int32)
+        nc = 3 if field == abi.FIELD_VELOCITY else 1
+        out = np.zeros(int(np.prod(d)) * nc)
+        sup = np.zeros(int(np.prod(d)), np.uint8)
+        mask = 0
+        for k in kinds:
+            mask |= 1 << int(k)
+        dp = C.POINTER(C.c_double)
+        self._check(self._fn("shepard_grid")(self._h, o.ctypes.data_as(dp), sp.ctypes.data_as(dp),
+                                             d.ctypes.data_as(C.POINTER(C.c_int32)), int(field), mask,
+                                             out.ctypes.data_as(dp), sup.ctypes.data_as(C.POINTER(C.c_uint8))),
+                    "shepard_grid")
+        return out.reshape(tuple(d) + (nc,)), sup.reshape(tuple(d)).astype(bool)
+
     def count_pairs(self):
         """(candidates, interacting, interacting with fluid i, interacting with non-fluid i)."""
         out = (C.c_int64 * 4)()

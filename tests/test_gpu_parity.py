@@ -315,3 +315,30 @@ def test_download_into_pinned_and_pageable(Oracle):
     sim.download(b, fields=("pos", "vel", "density", "pressure", "temperature"))
     for f in ("pos", "vel", "density", "pressure", "temperature"):
         assert np.array_equal(getattr(a, f), getattr(b, f)), f
+
+
+@pytest.mark.parametrize("case", ["c1_small", "c2_small", "dissolve"])
+def test_shepard_grid_parity(case, Oracle):
+    """shepard_interpolate on a grid, device vs oracle, every field, after two steps
+    (particles off their rebuild positions); points outside the domain have no support on both."""
+    sc = CASES[case]()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    sim.step(2)
+    orc.step(2)
+    p = sc.params
+    lo = np.array([p.lo[a] for a in range(3)])
+    hi = np.array([p.hi[a] for a in range(3)])
+    dims = (9, 7, 8)
+    sp = (hi - lo) / (np.array(dims) - 1) * 1.15  # the last points fall outside the domain
+    org = lo - 0.05 * (hi - lo)
+    kinds = (abi.FLUID,) if case != "c2_small" else (abi.FLUID, abi.RIGID)
+    fields = [abi.FIELD_VELOCITY, abi.FIELD_TEMPERATURE, abi.FIELD_PRESSURE, abi.FIELD_DENSITY]
+    if p.diffusion:
+        fields.append(abi.FIELD_CONCENTRATION)
+    for f in fields:
+        g, gs = sim.shepard_grid(org, sp, dims, f, kinds)
+        o, os_ = orc.shepard_grid(org, sp, dims, f, kinds)
+        assert np.array_equal(gs, os_), f"support differs (field {f})"
+        scale = max(float(np.nanmax(np.abs(o))), 1e-30)
+        assert np.allclose(g[gs], o[os_], rtol=1e-12, atol=1e-12 * scale), f"field {f}"
+        assert np.all(np.isnan(g[~gs]))

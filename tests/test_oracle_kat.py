@@ -571,3 +571,57 @@ def test_conservation_periodic_c1(O):  # SPEC:290, 636(a)(b)
     P1, S1, M1 = momentum()
     assert M1 == M0
     assert np.all(np.abs(P1 - P0) <= 1e-10 * S0)
+
+
+# ----------------------------------------------------------- Shepard grid
+def _grid_over(sc, n=6):
+    p = sc.params
+    lo = np.array([p.lo[a] for a in range(3)])
+    hi = np.array([p.hi[a] for a in range(3)])
+    sp = (hi - lo) / (n + 1)
+    return lo + sp, sp, (n, n, n)
+
+
+def test_shepard_constant_field(O):  # constant field -> the constant (to summation round-off:
+    # "exactly" holds in exact arithmetic; the two ~100-term fp64 sums round independently)
+    sc = scenarios.config1(nside=12, n_spheres=1, r_range=(2.0, 2.0), seed=3)
+    sc.store.temperature[:] = 7.0
+    o = O.Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.initialize()
+    org, sp, dims = _grid_over(sc)
+    v, sup = o.shepard_grid(org, sp, dims, abi.FIELD_TEMPERATURE, kinds=(abi.FLUID, abi.RIGID))
+    assert sup.all()
+    assert np.max(np.abs(v - 7.0)) <= 7.0 * 1e-13
+
+
+def test_shepard_single_neighbour_and_no_support(O):
+    sc = scenarios.config1(nside=12, n_spheres=1, r_range=(2.0, 2.0), seed=3)
+    p = sc.params
+    st = ParticleStore(1)
+    c0 = np.array([0.5 * (p.lo[a] + p.hi[a]) for a in range(3)])
+    st.pos[0] = c0
+    st.kind[0] = abi.FLUID
+    st.mass[0] = 1000.0 * p.dx ** 3
+    st.density[0] = 1000.0
+    st.temperature[0] = 321.5
+    o = O.Oracle(p)
+    o.upload(st, empty_bodies(0))
+    v, sup = o.shepard_grid(c0 + [0.7 * p.dx, 0.0, 0.0], [5 * p.dx] * 3, (2, 1, 1), abi.FIELD_TEMPERATURE)
+    assert sup[0, 0, 0] and abs(v[0, 0, 0, 0] - 321.5) <= 321.5 * 2e-16
+    assert not sup[1, 0, 0] and np.isnan(v[1, 0, 0, 0])  # 5 dx away: no particle within r_c
+
+
+def test_shepard_linear_field_interior(O):  # linear field, interior point, within 1 %
+    sc = scenarios.config1(nside=16, n_spheres=1, r_range=(2.0, 2.0), seed=3)
+    s = sc.store
+    s.kind[:] = abi.FLUID
+    s.pos[:] = scenarios.lattice_box((0.0,) * 3, (16 * sc.params.dx,) * 3, sc.params.dx)  # no jitter
+    s.temperature[:] = 300.0 + 1e4 * s.pos[:, 0]
+    o = O.Oracle(sc.params)
+    o.upload(s, empty_bodies(0))
+    o.initialize()
+    x = np.array([7.3, 8.1, 6.6]) * sc.params.dx
+    v, sup = o.shepard_grid(x, [sc.params.dx] * 3, (1, 1, 1), abi.FIELD_TEMPERATURE)
+    exact = 300.0 + 1e4 * x[0]
+    assert abs(v[0, 0, 0, 0] - exact) <= 0.01 * abs(exact)
