@@ -162,6 +162,14 @@ class DeviceSimulation {
   void reduce_force_torque() { stage(SPHG_STAGE_BODIES); }
   void reduce_mass_quantities() { stage(SPHG_STAGE_MASS); }
   void apply_transitions() { stage(SPHG_STAGE_TRANSITIONS); }
+  void diffusion_rhs() { stage(SPHG_STAGE_HEAT); }
+  /// ScenarioConfig::wall_groups (config.hpp:35-51, 93): WallGroup<3>::velocity_at and
+  /// acceleration_at are evaluated on the host every step (the groups must outlive this object).
+  void set_wall_groups(const std::vector<sphfsi::WallGroup<3>>* groups) {
+    walls_ = groups;
+    const int32_t ng = groups ? (int32_t)groups->size() : 0;
+    check(sphg_set_wall_motion(ctx_, ng, ng ? &DeviceSimulation::wall_thunk : nullptr, this), "set_wall_motion");
+  }
   void initialize() { check(sphg_initialize(ctx_), "initialize"); }
   void step(int n = 1) { check(sphg_step(ctx_, n), "step"); }
   sphg_stats_t stats() {
@@ -175,7 +183,16 @@ class DeviceSimulation {
   void check(int rc, const char* what) {
     if (rc != SPHG_OK) throw Error(rc, std::string(what) + ": " + sphg_last_error(ctx_));
   }
+  static void wall_thunk(int32_t g, double t, double vel[3], double acc[3], void* user) {
+    const auto& w = (*static_cast<DeviceSimulation*>(user)->walls_)[(size_t)g];
+    const sphfsi::Vec<3> v = w.velocity_at(t), a = w.acceleration_at(t);
+    for (int k = 0; k < 3; ++k) {
+      vel[k] = v[k];
+      acc[k] = a[k];
+    }
+  }
   sphg_ctx* ctx_ = nullptr;
+  const std::vector<sphfsi::WallGroup<3>>* walls_ = nullptr;
 };
 
 }  // namespace sphfsi_gpu

@@ -208,6 +208,17 @@ int sphg_dt_limits(const sphg_params* params, double u_max, double m_r, double l
  * [2] interacting with a fluid particle i (the fluid force kernel's pairs), [3] with a non-fluid i. */
 int sphg_count_pairs(sphg_ctx* ctx, int64_t counts[4]);
 
+/* Moving wall groups: WallGroup<3>::velocity_at / acceleration_at (config.hpp:35-51), SPEC:237,
+ * 273, 278.  Boundary particles whose `group` is g < n_groups belong to wall group g.  Each step
+ * the library calls fn(g, t^{n+1/2}, vel, acc, user) for the drift (r += dt vel; acc unused) and
+ * fn(g, t^{n+1}, vel, acc, user) for the wall state the pair sums see at t^{n+1} (boundary
+ * velocity u_w = vel, wall acceleration a_w = acc in the pressure extrapolation).  `acc` is
+ * pre-filled with the reference's default, the central difference (v(t+1e-6) - v(t-1e-6))/2e-6;
+ * the callee may overwrite it.  fn = NULL (default) = fixed walls.  n_groups <= SPHG_MAX_WALL_GROUPS. */
+#define SPHG_MAX_WALL_GROUPS 8
+typedef void (*sphg_wall_motion_fn)(int32_t group, double t, double vel[3], double acc[3], void* user);
+int sphg_set_wall_motion(sphg_ctx* ctx, int32_t n_groups, sphg_wall_motion_fn fn, void* user);
+
 /* shepard_interpolate (the Shepard filter used for every field
  * figure) on a regular grid, the post-processing gather behind OutputPlan::shepard_grid
  * (config.hpp:53-59):

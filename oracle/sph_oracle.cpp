@@ -79,11 +79,37 @@ struct Ctx {
     double h = 0, rc = 0, rv = 0, dt = 0;
     double max_disp = 0, u_max = 0;
     bool built = false;
+    // moving wall groups (sphg_set_wall_motion): callback + per-step values
+    int n_walls = 0;
+    sphg_wall_motion_fn wall_fn = nullptr;
+    void* wall_user = nullptr;
+    double wall_vh[SPHG_MAX_WALL_GROUPS][3] = {}, wall_v[SPHG_MAX_WALL_GROUPS][3] = {},
+           wall_a[SPHG_MAX_WALL_GROUPS][3] = {};
     std::string err;
     int threads = 0;
 };
 
 inline bool ghost(const Ctx& c, size_t i) { return c.S.owner[i] != (uint32_t)c.P.rank; }
+
+// WallGroup::velocity_at / acceleration_at (config.hpp:42-50) through the host callback [P20]
+void eval_walls(Ctx& c, double t, double (*vel)[3], double (*acc)[3]) {
+    for (int g = 0; g < c.n_walls; ++g) {
+        double v[3] = {0, 0, 0}, vp[3] = {0, 0, 0}, vm[3] = {0, 0, 0}, a[3], dummy[3];
+        const double e = 1e-6;
+        c.wall_fn(g, t + e, vp, dummy, c.wall_user);
+        c.wall_fn(g, t - e, vm, dummy, c.wall_user);
+        for (int k = 0; k < 3; ++k) a[k] = (vp[k] - vm[k]) / (2.0 * e);
+        c.wall_fn(g, t, v, a, c.wall_user);
+        for (int k = 0; k < 3; ++k) {
+            vel[g][k] = v[k];
+            if (acc) acc[g][k] = a[k];
+        }
+    }
+}
+inline bool wall_member(const Ctx& c, size_t i) {
+    return c.n_walls > 0 && c.S.kind[i] == Kind::Boundary && c.S.group[i] < (uint32_t)c.n_walls;
+}
+
 
 inline double mi(const Ctx& c, double d, int a) {  // minimum image [P2]
     if (c.P.periodic[a]) {
@@ -443,6 +469,10 @@ bool stage_extrapolate(Ctx& c) {
     for (int64_t w = 0; w < n; ++w) {
         if (c.S.kind[w] == Kind::Fluid || ghost(c, (size_t)w)) continue;
         V3 uw = V3::zero(), aw = V3::zero();
+        if (wall_member(c, (size_t)w)) {  // prescribed wall velocity / acceleration at t^{n+1} [P20]
+            uw = v3(c.wall_v[c.S.group[w]]);
+            aw = v3(c.wall_a[c.S.group[w]]);
+        }
         if (c.S.kind[w] == Kind::Rigid) {
             const sphg_body& b = c.bodies[c.S.group[w]];
             const V3 rk = rigid_rk(c, (size_t)w);
@@ -763,6 +793,10 @@ bool stage_mass(Ctx& c) {
 // step(): half kick, drift, orientation, slave [P14]
 bool stage_kick_drift(Ctx& c) {
     const double hdt = 0.5 * c.dt, dt = c.dt;
+    if (c.n_walls > 0) {
+        eval_walls(c, c.t + hdt, c.wall_vh, nullptr);
+        eval_walls(c, c.t + dt, c.wall_v, c.wall_a);
+    }
     const int64_t n = (int64_t)c.S.size();
     double umax = 0.0;
     for (auto& b : c.bodies) {
@@ -795,6 +829,10 @@ bool stage_kick_drift(Ctx& c) {
             const V3 u = v3(b.vel) + sphfsi::cross(v3(b.omega), rk);
             c.S.vel[i] = u;
             c.S.vel_adv[i] = u;
+        } else if (wall_member(c, (size_t)i)) {  // prescribed wall motion [P20]
+            const uint32_t g = c.S.group[i];
+            c.S.pos[i] = wrap3(c, c.S.pos[i] + dt * v3(c.wall_vh[g]));
+            c.S.vel[i] = v3(c.wall_v[g]);
         } else {
             continue;
         }
@@ -1149,8 +1187,19 @@ int orc_run_stage(orc_ctx* h, int stage) {
     return run_stage(c, stage) ? SPHG_OK : SPHG_ERR_RUNTIME;
 }
 
+int orc_set_wall_motion(orc_ctx* h, int32_t n_groups, sphg_wall_motion_fn fn, void* user) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (n_groups < 0 || n_groups > SPHG_MAX_WALL_GROUPS) return SPHG_ERR_CONFIG;
+    c.n_walls = fn ? n_groups : 0;
+    c.wall_fn = fn;
+    c.wall_user = user;
+    if (c.n_walls) eval_walls(c, c.t, c.wall_v, c.wall_a);  // state at the current time (a^0)
+    return SPHG_OK;
+}
+
 int orc_initialize(orc_ctx* h) {
     Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (c.n_walls) eval_walls(c, c.t, c.wall_v, c.wall_a);
     for (int s : {SPHG_STAGE_REBUILD, SPHG_STAGE_DENSITY, SPHG_STAGE_EXTRAPOLATE, SPHG_STAGE_FORCES, SPHG_STAGE_BODIES})
         if (!run_stage(c, s)) return SPHG_ERR_RUNTIME;
     return SPHG_OK;

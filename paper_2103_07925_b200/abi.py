@@ -105,6 +105,12 @@ class Stats(C.Structure):
                 ("last_step_call_ms", C.c_double)]
 
 
+# void fn(int32 group, double t, double vel[3], double acc[3], void* user)  (sphg_set_wall_motion)
+WALL_MOTION_FN = C.CFUNCTYPE(None, C.c_int32, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                             C.c_void_p)
+MAX_WALL_GROUPS = 8
+
+
 def declare(lib, prefix):
     """Attach argtypes/restypes for the sphg_* (or orc_*) entry points."""
     vp = C.c_void_p
@@ -136,6 +142,7 @@ def declare(lib, prefix):
         "max_displacement": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "halo_doubles": (C.c_int, [C.c_int]),
         "upload_state": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_size_t]),
+        "set_wall_motion": (C.c_int, [vp, C.c_int32, WALL_MOTION_FN, C.c_void_p]),
         "shepard_grid": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                    C.c_int32, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint8)]),
     }

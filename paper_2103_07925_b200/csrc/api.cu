@@ -271,7 +271,28 @@ void timed_forces(Ctx& c) {  // stage 4 = 10 (fluid kernel) + 11 (rigid kernel)
   c.stage_ms[SPHG_STAGE_FORCES] += (c.stage_ms[10] - before10) + (c.stage_ms[11] - before11);
 }
 
+// WallGroup::velocity_at / acceleration_at (config.hpp:42-50) through the host callback, into the
+// launch parameters: acc pre-filled with the reference's central difference [P20]
+void eval_walls(Ctx& c, double t, double (*vel)[3], double (*acc)[3]) {
+  for (int g = 0; g < c.P.n_walls; ++g) {
+    double v[3] = {0, 0, 0}, vp[3] = {0, 0, 0}, vm[3] = {0, 0, 0}, a[3], dummy[3];
+    const double e = 1e-6;
+    c.wall_fn(g, t + e, vp, dummy, c.wall_user);
+    c.wall_fn(g, t - e, vm, dummy, c.wall_user);
+    for (int k = 0; k < 3; ++k) a[k] = (vp[k] - vm[k]) / (2.0 * e);
+    c.wall_fn(g, t, v, a, c.wall_user);
+    for (int k = 0; k < 3; ++k) {
+      vel[g][k] = v[k];
+      if (acc) acc[g][k] = a[k];
+    }
+  }
+}
+
 void kick_all(Ctx& c) {
+  if (c.P.n_walls > 0) {
+    eval_walls(c, c.t + 0.5 * c.P.dt, c.P.wall_vh, nullptr);
+    eval_walls(c, c.t + c.P.dt, c.P.wall_v, c.P.wall_a);
+  }
   launch_body_kick(c);
   launch_kick_drift(c);
 }
@@ -761,8 +782,21 @@ int sphg_upload_state(sphg_ctx* h, const double* pos, const double* vel, size_t 
   });
 }
 
+int sphg_set_wall_motion(sphg_ctx* h, int32_t n_groups, sphg_wall_motion_fn fn, void* user) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (n_groups < 0 || n_groups > SPHG_MAX_WALL_GROUPS) return fail(h, SPHG_ERR_CONFIG, "wall group count out of range");
+    c.wall_fn = fn;
+    c.wall_user = user;
+    c.P.n_walls = fn ? n_groups : 0;
+    if (c.P.n_walls) eval_walls(c, c.t, c.P.wall_v, c.P.wall_a);  // state at the current time (a^0)
+    return SPHG_OK;
+  });
+}
+
 int sphg_initialize(sphg_ctx* h) {
   return guarded(h, [&]() -> int {
+    if (h->c.P.n_walls) eval_walls(h->c, h->c.t, h->c.P.wall_v, h->c.P.wall_a);
     for (int s : {SPHG_STAGE_REBUILD, SPHG_STAGE_DENSITY, SPHG_STAGE_EXTRAPOLATE, SPHG_STAGE_FORCES, SPHG_STAGE_BODIES}) {
       const int rc = do_stage(h, s);
       if (rc) return rc;

@@ -102,6 +102,8 @@ struct Ctx {
   size_t nf = 0, nw = 0, nrigid = 0;
   int group_density = 4, group_forces = 4;  // lanes per particle in the pair kernels
   bool cell_build = true;  // cell-cooperative Verlet build (falls back per particle on overflow)
+  sphg_wall_motion_fn wall_fn = nullptr;  // moving wall groups (sphg_set_wall_motion)
+  void* wall_user = nullptr;
   // transitions scratch
   DBuf<uint32_t> ev_idx, ev_flag, label, tscratch;
   // flags

@@ -268,6 +268,13 @@ __global__ void __launch_bounds__(kBlock) k_extrapolate(const __grid_constant__ 
   for (int m = 0; m < (kMultiEos ? kMaxMat : 1); ++m) smat[m] = 0.0;
   if (active) {
     const uint32_t kmd = D.kmd.p[w];
+    if (kind_of(kmd) == SPHG_BOUNDARY && P.n_walls > 0) {  // prescribed wall motion [P20]
+      const uint32_t gr = D.group.p[w];
+      if (gr < (uint32_t)P.n_walls) {
+        uw = make_double3(P.wall_v[gr][0], P.wall_v[gr][1], P.wall_v[gr][2]);
+        aw = make_double3(P.wall_a[gr][0], P.wall_a[gr][1], P.wall_a[gr][2]);
+      }
+    }
     if (kind_of(kmd) == SPHG_RIGID) {
       const sphg_body& b = B[D.group.p[w]];
       const double3 rk = qrotate(body_q(b), ld3(D.X4.p[w]));

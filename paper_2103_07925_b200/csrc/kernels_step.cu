@@ -99,6 +99,14 @@ __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevP
       stpos(&D.G0.p[k], pn);
       const double3 wxr = cross3(bv(b.omega), rk);
       stpos(&D.V4.p[k], make_double3(b.vel[0] + wxr.x, b.vel[1] + wxr.y, b.vel[2] + wxr.z));
+    } else if (kind == SPHG_BOUNDARY && D.group.p[k] < (uint32_t)P.n_walls) {  // prescribed motion [P20]
+      const uint32_t gr = D.group.p[k];
+      const double3 p = ldpos(&D.G0.p[k]);
+      pn = make_double3(wrap1(P, axpy_rn(p.x, P.dt, P.wall_vh[gr][0]), 0),
+                        wrap1(P, axpy_rn(p.y, P.dt, P.wall_vh[gr][1]), 1),
+                        wrap1(P, axpy_rn(p.z, P.dt, P.wall_vh[gr][2]), 2));
+      stpos(&D.G0.p[k], pn);
+      stpos(&D.V4.p[k], make_double3(P.wall_v[gr][0], P.wall_v[gr][1], P.wall_v[gr][2]));
     } else {
       moved = false;
     }

@@ -522,6 +522,54 @@ def dissolving_bodies(nside=32, dx=1e-3, dt=1e-5, seed=2113, n_bodies=4, r_range
     return Scenario(name, params, st, bodies, steps, info)
 
 
+def couette_channel(nside=16, nz=None, dx=1e-3, dt=1e-5, seed=2117, rho=1000.0, c=10.0, nu=1e-5, u_wall=0.01,
+                    jitter=0.05, name="couette", steps=200):
+    """Moving wall groups (PAPER §4.2): channel periodic in x and y,
+    3-layer walls below z = 0 (wall group 0, fixed) and above z = H (wall group 1, moving along x
+    with u_wall; see `wall_velocity`).  Fluid at rest initially, no gravity, no bodies."""
+    nz = nz or nside
+    L = nside * dx
+    H = nz * dx
+    nl = 3
+    lo = (0.0, 0.0, -nl * dx)
+    hi = (L, L, H + nl * dx)
+    p0 = rho * c * c
+    mats = [material(rho, nu=nu, c=c, pb=p0), material(rho, c=c)]  # 0 fluid, 1 wall
+    params = _params(dx, dt, lo, hi, (1, 1, 0), mats)
+    fl = lattice_box((0.0, 0.0, 0.0), (L, L, H), dx)
+    wl = lattice_box(lo, hi, dx)
+    wl = wl[(wl[:, 2] < 0.0) | (wl[:, 2] > H)]
+    nf, nw = len(fl), len(wl)
+    n = nf + nw
+    st = ParticleStore(n)
+    u = splitmix_u01(seed, 0, np.arange(3 * nf, dtype=np.uint64)).reshape(nf, 3)
+    pos = fl + (2.0 * u - 1.0) * (jitter * dx)
+    for a in range(2):  # periodic axes: wrap the jitter
+        pos[:, a] = np.mod(pos[:, a], L)
+    st.pos[:nf] = pos
+    st.pos[nf:] = wl
+    st.kind[:nf] = abi.FLUID
+    st.kind[nf:] = abi.BOUNDARY
+    st.material[nf:] = 1
+    st.group[nf:] = (wl[:, 2] > H).astype(np.uint32)  # wall group: 0 bottom, 1 top
+    st.mass[:] = rho * dx ** 3
+    st.density[:] = rho
+    bodies = empty_bodies(0)
+    _finish(st, bodies)
+    info = dict(n=n, n_fluid=nf, n_rigid=0, n_boundary=nw, n_bodies=0, rigid_fraction=0.0, u_wall=u_wall)
+    return Scenario(name, params, st, bodies, steps, info)
+
+
+def wall_velocity(u_wall, omega=0.0):
+    """velocity(g, t) of couette_channel's wall groups: group 1 moves along x with
+    u_wall (omega = 0) or u_wall sin(omega t); group 0 is fixed."""
+    def v(g, t):
+        if g != 1:
+            return (0.0, 0.0, 0.0)
+        return (u_wall * (math.sin(omega * t) if omega else 1.0), 0.0, 0.0)
+    return v
+
+
 def config3(**kw):
     """BASELINE configs[2]: 128^3 two-phase liquid/gas with 200 rigid cubes and spheres."""
     return two_phase_with_bodies(**kw)
@@ -533,4 +581,5 @@ def config2(**kw):
 
 
 def by_name(name, **kw):
-    return {"c1": config1, "c2": config2, "c3": config3, "c5": config5, "dissolve": dissolving_bodies}[name](**kw)
+    return {"c1": config1, "c2": config2, "c3": config3, "c5": config5, "dissolve": dissolving_bodies,
+            "couette": couette_channel}[name](**kw)

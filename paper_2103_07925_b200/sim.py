@@ -186,6 +186,27 @@ class Simulation:
     def set_timing(self, enabled=True):
         self._check(self._fn("set_timing")(self._h, int(bool(enabled))), "set_timing")
 
+    def set_wall_motion(self, n_groups, velocity, acceleration=None):
+        """Moving wall groups (WallGroup<3>, config.hpp:35-51): boundary particles with group g <
+        n_groups move with velocity(g, t) -> 3 floats; acceleration(g, t) defaults to the
+        reference's central difference.  velocity=None fixes the walls again."""
+        if velocity is None:
+            self._wall_cb = None
+            self._check(self._fn("set_wall_motion")(self._h, 0, abi.WALL_MOTION_FN(), None), "set_wall_motion")
+            return
+
+        def cb(g, t, vel, acc, user):
+            v = velocity(int(g), float(t))
+            for k in range(3):
+                vel[k] = float(v[k])
+            if acceleration is not None:
+                a = acceleration(int(g), float(t))
+                for k in range(3):
+                    acc[k] = float(a[k])
+
+        self._wall_cb = abi.WALL_MOTION_FN(cb)  # keep the thunk alive as long as the context uses it
+        self._check(self._fn("set_wall_motion")(self._h, int(n_groups), self._wall_cb, None), "set_wall_motion")
+
     def shepard_grid(self, origin, spacing, dims, field=abi.FIELD_VELOCITY, kinds=(abi.FLUID,)):
         """shepard_interpolate (SPEC:123-131) on a regular grid (OutputPlan::shepard_grid,
         config.hpp:53-59).  Returns (values[dims..., ncomp] with NaN where unsupported, support)."""

@@ -342,3 +342,26 @@ def test_shepard_grid_parity(case, Oracle):
         scale = max(float(np.nanmax(np.abs(o))), 1e-30)
         assert np.allclose(g[gs], o[os_], rtol=1e-12, atol=1e-12 * scale), f"field {f}"
         assert np.all(np.isnan(g[~gs]))
+
+
+@pytest.mark.parametrize("omega", [0.0, 3000.0])
+def test_moving_walls_parity(omega, Oracle):
+    """Prescribed wall motion (WallGroup, config.hpp:35-51): drift with u_w(t^{n+1/2}), wall state
+    u_w, a_w (central difference) at t^{n+1}; device vs oracle after 1 and 6 steps."""
+    sc = scenarios.couette_channel(nside=16, nz=12)
+    sim, orc = sim_factory(sc.params), Oracle(sc.params)
+    for e in (sim, orc):
+        e.upload(sc.store, sc.bodies)
+        e.set_wall_motion(2, scenarios.wall_velocity(0.01, omega=omega))
+        e.initialize()
+    compare_state(sim, orc, sc.params, what=f"couette omega={omega} init")
+    sim.step(1)
+    orc.step(1)
+    compare_state(sim, orc, sc.params, what=f"couette omega={omega} step1")
+    sim.step(5)
+    orc.step(5)
+    compare_state(sim, orc, sc.params, tol=1e-7, what=f"couette omega={omega} 6 steps")
+    g, _ = sim.download()
+    o, _ = orc.download()
+    w = g.kind == abi.BOUNDARY
+    assert np.array_equal(g.pos[w], o.pos[w]) and np.array_equal(g.vel[w], o.vel[w])

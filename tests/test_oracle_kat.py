@@ -625,3 +625,43 @@ def test_shepard_linear_field_interior(O):  # linear field, interior p
     v, sup = o.shepard_grid(x, [sc.params.dx] * 3, (1, 1, 1), abi.FIELD_TEMPERATURE)
     exact = 300.0 + 1e4 * x[0]
     assert abs(v[0, 0, 0, 0] - exact) <= 0.01 * abs(exact)
+
+
+# ------------------------------------------------------------- moving walls
+def test_moving_wall_pulls_fluid(O):  # u_wall = (0.01, 0), fluid at rest -> pulled along
+    sc = scenarios.couette_channel(nside=12, nz=10, jitter=0.0)
+    o = O.Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.set_wall_motion(2, scenarios.wall_velocity(0.01))
+    o.initialize()
+    g, _ = o.download()
+    fl = g.kind == abi.FLUID
+    H = 10 * sc.params.dx
+    near_top = fl & (g.pos[:, 2] > H - 2 * sc.params.dx)
+    near_bottom = fl & (g.pos[:, 2] < 2 * sc.params.dx)
+    assert np.all(g.acc[near_top, 0] > 0.0)
+    assert np.max(np.abs(g.acc[near_bottom, 0])) < 1e-8  # the fixed wall exerts no x force on fluid at rest
+    top = g.kind == abi.BOUNDARY
+    top &= g.group == 1
+    wv = g.wall_velocity[top, 0]  # u~_w = 2 u_w - <u_f>_W = 0.02 with fluid support, u_w without
+    assert np.all((wv == 0.02) | (wv == 0.01)) and np.any(wv == 0.02)
+
+
+def test_moving_wall_drift_and_central_difference(O):  # config.hpp:42-50
+    sc = scenarios.couette_channel(nside=12, nz=10, jitter=0.0)
+    o = O.Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    om = 2000.0
+    o.set_wall_motion(2, scenarios.wall_velocity(0.01, omega=om))
+    o.initialize()
+    o.step(3)
+    g, _ = o.download()
+    top = (sc.store.kind == abi.BOUNDARY) & (sc.store.group == 1)
+    dt = sc.params.dt
+    want = sum(dt * 0.01 * np.sin(om * (k + 0.5) * dt) for k in range(3))  # drift with u(t^{n+1/2})
+    L = sc.params.hi[0] - sc.params.lo[0]
+    dxs = np.mod(g.pos[top, 0] - sc.store.pos[top, 0] + 0.5 * L, L) - 0.5 * L
+    assert np.allclose(dxs, want, rtol=0.0, atol=2e-17)  # a few ulps of |x| ~ 1e-2
+    assert np.allclose(g.vel[top, 0], 0.01 * np.sin(om * 3 * dt), rtol=1e-14)  # u_w(t^{n+1})
+    bottom = (sc.store.kind == abi.BOUNDARY) & (sc.store.group == 0)
+    assert np.array_equal(g.pos[bottom], sc.store.pos[bottom])
