@@ -63,6 +63,8 @@ def parse():
                     help="c5 = the headline workload (BASELINE metric); the others are secondary measurements")
     ap.add_argument("--nside", type=int, default=None, help="lattice side (default: the config's BASELINE size)")
     ap.add_argument("--spheres", type=int, default=20000)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1: strong = the 64M C5 box split over N GPUs; weak = 8M particles per GPU")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -339,7 +339,13 @@ def bench_multi(args, clock_factory=None):
     # owned + ghost subset (host memory stays O(N) overall instead of O(N x ranks))
     dev = comm
     if rank == 0:
-        sc = scenarios.config5(nside=args.nside, n_spheres=args.spheres)
+        if getattr(args, "scaling", "strong") == "weak":
+            # BASELINE C5 weak scaling: 8M particles (200^3) per GPU, sphere density of C5
+            nside = int(round(200 * world ** (1.0 / 3.0)))
+            nsph = int(round(args.spheres * (nside / 400.0) ** 3))
+            sc = scenarios.config5(nside=nside, n_spheres=nsph)
+        else:
+            sc = scenarios.config5(nside=args.nside, n_spheres=args.spheres)
         meta = [sc.params, sc.bodies, sc.info, sc.store.n]
     else:
         meta = [None, None, None, None]
@@ -442,11 +448,14 @@ def bench_multi(args, clock_factory=None):
                        "host wall clock, max over ranks"}
     n = n_total
     if rank == 0:
+        weak = getattr(args, "scaling", "strong") == "weak"
         line = {"metric": "particle-steps/sec (full SPH step, fp64)", "value": n * args.steps / dt,
                 "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
+                "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+                "scaling": "weak" if weak else "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64 lattice + jitter)",
-                "config": {"workload": f"C5 {args.nside}^3 periodic, {info['n_bodies']} spheres",
+                "config": {"workload": f"C5 {round(n ** (1 / 3))}^3 periodic, {info['n_bodies']} spheres"
+                                       + (" (8M per GPU)" if weak else ""),
                            "particles": n, "parallelism": f"domain decomposition {ds.grid.dims}, {backend} halo",
                            "ghost_width_h": ds.width / ds.h},
                 "timing": "host wall clock between barriers + cuda synchronize, max over ranks "
