@@ -307,12 +307,90 @@ class DistributedSimulation:
                 getattr(g, f)[p["gid"]] = p[f]
         return g, bodies
 
+    # ------------------------------------------------------------ migration
+    _FIELDS = VEC_FIELDS + SCALAR_FIELDS + tuple(TAG_FIELDS)
+
+    def _record_dtype(self):
+        st = ParticleStore(1)
+        spec = [("gid", np.int64)]
+        for f in self._FIELDS:
+            a = getattr(st, f)
+            spec.append((f, a.dtype, a.shape[1:]))
+        return np.dtype(spec)
+
+    def _pack(self, local, idx, gids):
+        rec = np.zeros(len(idx), self._record_dtype())
+        rec["gid"] = gids
+        for f in self._FIELDS:
+            rec[f] = getattr(local, f)[idx]
+        return rec
+
+    def _exchange(self, outgoing):
+        """outgoing[q] = record array for rank q -> list of record arrays received from every rank
+        (point-to-point: counts first, then payload bytes; NCCL or gloo)."""
+        rd = self._record_dtype()
+        counts_out = {q: torch.tensor([len(outgoing.get(q, ()))], dtype=torch.int64, device=self.dev)
+                      for q in range(self.world) if q != self.rank}
+        counts_in = {q: torch.zeros(1, dtype=torch.int64, device=self.dev)
+                     for q in range(self.world) if q != self.rank}
+        ops = []
+        for q in counts_out:
+            ops.append(dist.P2POp(dist.isend, counts_out[q], q, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, counts_in[q], q, group=self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        ops, bufs = [], {}
+        for q in counts_out:
+            m_out = int(counts_out[q].item())
+            m_in = int(counts_in[q].item())
+            if m_out:
+                data = torch.from_numpy(np.ascontiguousarray(outgoing[q]).view(np.uint8)).to(self.dev)
+                ops.append(dist.P2POp(dist.isend, data, q, group=self.group))
+                bufs[("s", q)] = data
+            if m_in:
+                bufs[("r", q)] = torch.empty(m_in * rd.itemsize, dtype=torch.uint8, device=self.dev)
+                ops.append(dist.P2POp(dist.irecv, bufs[("r", q)], q, group=self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        if self.dev.type == "cuda":
+            torch.cuda.current_stream(self.dev).synchronize()
+        got = {q: bufs[("r", q)].cpu().numpy().view(rd) for q in counts_in if ("r", q) in bufs}
+        return got
+
     def repartition(self):
-        """Re-own and re-ghost from the gathered global state (rare: margin/2 of motion)."""
-        g, bodies = self.gather()
-        g.owner[:] = 0
+        """Particle migration: every rank sends the owned particles that left its box
+        to their new owner, then ships each peer the owned particles inside that peer's ghost shell;
+        no rank ever holds more than its own owned + ghost set.  Rare: after margin/2 of motion."""
+        local, bodies = self.engine.download()
+        n_own = self.n_own
+        pos = local.pos[:n_own]
+        gids = self.gids[:n_own].astype(np.int64)
+        new_owner = self.grid.owner_of(pos)
+        keep = np.nonzero(new_owner == self.rank)[0]
+        outgoing = {q: self._pack(local, np.nonzero(new_owner == q)[0], gids[new_owner == q])
+                    for q in range(self.world) if q != self.rank}
+        got = self._exchange(outgoing)
+        owned = np.concatenate([self._pack(local, keep, gids[keep])] + [got[q] for q in sorted(got)])
+        owned = owned[np.argsort(owned["gid"], kind="stable")]
+        # ghosts: each peer gets my (new) owned particles within its shell
+        opos = owned["pos"]
+        shells = {q: owned[self.grid.near_box(opos, q, self.width)] for q in range(self.world) if q != self.rank}
+        got = self._exchange(shells)
+        ghosts = [got[q] for q in sorted(got)]  # (owner rank, gid) order, as local_gids
+        ghost_owner = np.concatenate([np.full(len(got[q]), q, np.uint32) for q in sorted(got)]) \
+            if ghosts else np.zeros(0, np.uint32)
+        for k, q in enumerate(sorted(got)):
+            ghosts[k] = ghosts[k][np.argsort(ghosts[k]["gid"], kind="stable")]
+        allrec = np.concatenate([owned] + ghosts) if ghosts else owned
+        new = ParticleStore(len(allrec))
+        for f in self._FIELDS:
+            getattr(new, f)[:] = allrec[f]
+        new.owner[: len(owned)] = self.rank
+        new.owner[len(owned):] = ghost_owner
         self.repartitions += 1
-        self.distribute(g, bodies)
+        self.distribute_local(new, allrec["gid"], len(owned), self.global_n, bodies)
 
 
 # ---------------------------------------------------------------- bench N>1
