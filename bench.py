@@ -301,7 +301,8 @@ def run_sph(args):
                               "achieved_gbs": STEP_BYTES_PER_PARTICLE * n / (ms_step * 1e-3) / 1e9},
             "wall_s_timed": wall, "gpu_launches": int(launches),
             "rebuilds_in_timed_region": int(st1.rebuilds - st0.rebuilds),
-            "clocks": clk.summary(), "gen_s": t_gen}
+            "clocks": clk.summary(), "gen_s": t_gen,
+            "device_memory_gb": round((torch.cuda.mem_get_info(local)[1] - torch.cuda.mem_get_info(local)[0]) / 1e9, 1)}
     # e2e: through the public API with host buffers, every step: H2D of the step's kinematic input
     # (positions + velocities from pinned host memory, Simulation.upload_state) -> step(1) ->
     # D2H of the step's fields (positions, velocities, density, pressure) into the ParticleStore
