@@ -392,3 +392,25 @@ def test_full_size_c5_momentum_conservation():
     assert sim.stats().rebuilds > r0  # the run crossed at least one Verlet rebuild
     assert np.all(np.abs(p1 - p0) <= 1e-12 * np.maximum(s0, s1)), (p1 - p0) / s0
     assert m1 == m0
+
+
+def test_minimum_image_entry_mode(Oracle):
+    """Stores with >= 2^26 particles keep plain indices in the rows and take the minimum image in
+    the pair kernels (kImgMin); forced here at a small size: lists and step-1 fields unchanged."""
+    import subprocess, sys, os
+    code = (
+        "import numpy as np\n"
+        "from paper_2103_07925_b200 import scenarios, Simulation\n"
+        "from oracle.oracle import Oracle\n"
+        "from tests.helpers import compare_state, run_pair\n"
+        "sc = scenarios.config1(nside=20, n_spheres=3, r_range=(3.0, 4.0), seed=11)\n"
+        "sim, orc = run_pair(sc, lambda p: Simulation(p, device=0), Oracle, init=False)\n"
+        "sim.build_pairs(); orc.build_pairs()\n"
+        "assert np.array_equal(sim.get_nlist()[1], orc.get_nlist()[1])\n"
+        "sim.initialize(); orc.initialize(); sim.step(2); orc.step(2)\n"
+        "compare_state(sim, orc, sc.params, tol=1e-9, what='imgmin')\n"
+        "print('ok')\n")
+    env = dict(os.environ, SPHG_IMG_MIN="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
