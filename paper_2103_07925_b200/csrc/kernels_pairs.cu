@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(kBlock) k_count_pairs(const __grid_constant__ 
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t i = t / G;
   const int lane = (int)(t % G);
-  double c = 0, in = 0;
+  uint32_t c = 0, in = 0;
   bool fluid = false;
   if (i < n) {
     fluid = kind_of(D.kmd.p[i]) == SPHG_FLUID;
@@ -621,16 +621,30 @@ __global__ void __launch_bounds__(kBlock) k_count_pairs(const __grid_constant__ 
       const double3 pj = ldpos(&D.G0.p[nb_index<M>(e)]);
       const double3 d = M == kImgNone ? make_double3(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z)
                                       : mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z);
-      c += 1.0;
-      if (r2_exact(d) <= P.rc2) in += 1.0;
+      c += 1u;
+      if (r2_exact(d) <= P.rc2) in += 1u;
     }
   }
-  c = gsum<G>(c);
-  in = gsum<G>(in);
-  if (i < n && lane == 0) {
-    atomicAdd(out, (unsigned long long)c);
-    atomicAdd(out + 1, (unsigned long long)in);
-    atomicAdd(out + (fluid ? 2 : 3), (unsigned long long)in);
+  // per-block totals, one atomic per counter per block (same-address atomics serialise in L2)
+  unsigned long long v[4] = {0, 0, 0, 0};
+  if (i < n) {
+    v[0] = (unsigned long long)c;
+    v[1] = (unsigned long long)in;
+    v[fluid ? 2 : 3] = (unsigned long long)in;
+  }
+  __shared__ unsigned long long sv[kBlock / 32][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    unsigned long long x = v[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5][q] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    unsigned long long x = 0;
+    for (int w = 0; w < kBlock / 32; ++w) x += sv[w][threadIdx.x];
+    if (x) atomicAdd(out + threadIdx.x, x);
   }
 }
 

@@ -414,3 +414,28 @@ def test_minimum_image_entry_mode(Oracle):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_count_pairs(Oracle):
+    """sphg_count_pairs (the bench's flop model input) against the oracle's lists and positions."""
+    sc = CASES["c2_small"]()
+    sim, orc = run_pair(sc, sim_factory, Oracle, init=False)
+    sim.build_pairs()
+    orc.build_pairs()
+    cand, inter, inter_f, inter_o = sim.count_pairs()
+    off, nbr = orc.get_nlist()
+    o, _ = orc.download()
+    p = sc.params
+    L = np.array([p.hi[a] - p.lo[a] for a in range(3)])
+    i = np.repeat(np.arange(len(off) - 1), np.diff(off))
+    d = o.pos[i] - o.pos[nbr]
+    for a in range(3):
+        if p.periodic[a]:
+            d[:, a] = np.where(d[:, a] > 0.5 * L[a], d[:, a] - L[a], np.where(d[:, a] < -0.5 * L[a], d[:, a] + L[a], d[:, a]))
+    r2 = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+    rc = 3.0 * (p.h if p.h > 0 else p.dx)
+    hit = r2 <= rc * rc
+    assert cand == len(nbr)
+    assert inter == int(hit.sum())
+    assert inter_f == int(hit[o.kind[i] == abi.FLUID].sum())
+    assert inter_o == inter - inter_f
