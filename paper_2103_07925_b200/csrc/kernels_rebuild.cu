@@ -321,6 +321,10 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
   const double oz0 = P.lo[2] + (double)cz / P.inv_edge[2];
   const bool code = P.img_mode == kImgCode;
   const uint32_t emask = code ? kIdxMask : 0xffffffffu;
+  // home cell box in staged units (h), and the squared staging radius r_v (1 + 1e-3)
+  const float ex = (float)(1.0 / (P.inv_edge[0] * P.h)), ey = (float)(1.0 / (P.inv_edge[1] * P.h)),
+              ez = (float)(1.0 / (P.inv_edge[2] * P.h));
+  const float box_lim = (float)(P.rv2 * P.inv_h * P.inv_h) * 1.001f;
   int ns = 0;
   uint32_t batch = 0;
   for (int ox = -1; ox <= 1; ++ox) {
@@ -357,28 +361,42 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
         const int64_t cj = (qx * ny + qy) * nz + qz;
         const bool home = ox == 0 && oy == 0 && oz == 0;
         const uint32_t j0 = cstart[cj], j1 = cend[cj];
-        for (uint32_t jb = j0; jb < j1;) {
-          const int take = (int)min((uint32_t)(kStage - ns), j1 - jb);
-          for (int t = lane; t < take; t += 32) {
-            const uint32_t j = jb + t;
-            const double4 pj = G0[j];
-            // the periodic image of the cell: x_j + s sits next to the home cell
-            sp[ns + t] = make_float4((float)((pj.x + sx - ox0) * P.inv_h), (float)((pj.y + sy - oy0) * P.inv_h),
-                                     (float)((pj.z + sz - oz0) * P.inv_h),
-                                     (float)kind_of(kmd[j]));  // 0 fluid, 1 rigid, 2 boundary
-            se[ns + t] = j | tag;
-            if (home) hs[j - h0] = (batch << 16) | (uint32_t)(ns + t);
-          }
-          ns += take;
-          jb += take;
-          if (ns == kStage) {
+        for (uint32_t jb = j0; jb < j1; jb += 32) {
+          if (ns > kStage - 32) {  // room for a full round: flush the batch (padded to whole chunks)
+            const int padded = (ns + 31) & ~31;
+            for (int t = ns + lane; t < padded; t += 32) {
+              sp[t] = make_float4(1e30f, 1e30f, 1e30f, 0.f);
+              se[t] = 0u;
+            }
             __syncwarp();
-            build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, sp, se, ns, hc, hs, batch, fm_all[wib],
+            build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, sp, se, padded, hc, hs, batch, fm_all[wib],
                         bm_all[wib], emask);
             __syncwarp();
             ns = 0;
             ++batch;
           }
+          // one candidate per lane: stage it only if it can be within r_v of the home cell's box
+          // (conservative fp32 box distance with a 1e-3 margin; the exact rule decides later)
+          const uint32_t j = jb + lane;
+          bool keep = j < j1;
+          float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (keep) {
+            const double4 pj = G0[j];
+            // the periodic image of the cell: x_j + s sits next to the home cell
+            q = make_float4((float)((pj.x + sx - ox0) * P.inv_h), (float)((pj.y + sy - oy0) * P.inv_h),
+                            (float)((pj.z + sz - oz0) * P.inv_h), (float)kind_of(kmd[j]));  // 0 fluid 1 rigid 2 wall
+            const float dx = fmaxf(0.f, fmaxf(-q.x, q.x - ex)), dy = fmaxf(0.f, fmaxf(-q.y, q.y - ey)),
+                        dz = fmaxf(0.f, fmaxf(-q.z, q.z - ez));
+            keep = home || (dx * dx + dy * dy + dz * dz <= box_lim);
+          }
+          const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+          if (keep) {
+            const int at = ns + __popc(bal & ((1u << lane) - 1u));
+            sp[at] = q;
+            se[at] = j | tag;
+            if (home) hs[j - h0] = (batch << 16) | (uint32_t)at;
+          }
+          ns += __popc(bal);
         }
       }
     }
