@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevPara
       const uint32_t j = nb_index<M>(e);
       const double2 hj = D.H2.p[j];
       if (hj.y == 0.0) continue;  // non-Dirichlet wall: no conduction
-      const double3 d = pair_delta<M>(P, pi, ldpos(&D.G0.p[j]), e);
+      const double3 d = pair_delta<M>(P, pi, ld3(ldg4(&D.G0.p[j])), e);  // G0 is read-only here
       const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
       if (r2 > P.rc2) continue;
       if (r2 == 0.0) {
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kBlock) k_diffusion(const __grid_constant__ De
       const uint32_t j = nb_index<M>(e);
       const double2 cj = D.C2.p[j];
       if (cj.y == 0.0) continue;  // boundary without a concentration group
-      const double3 d = pair_delta<M>(P, pi, ldpos(&D.G0.p[j]), e);
+      const double3 d = pair_delta<M>(P, pi, ld3(ldg4(&D.G0.p[j])), e);  // G0 is read-only here
       const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
       if (r2 > P.rc2) continue;
       if (r2 == 0.0) {
