@@ -704,6 +704,14 @@ int blocks_for(size_t groups) {
     else { constexpr int G = 4; CALL; }                  \
   } while (0)
 constexpr int kGOther = 4;
+#ifndef SPHG_G_RIGID
+#define SPHG_G_RIGID 4
+#endif
+#ifndef SPHG_G_EXTRAP
+#define SPHG_G_EXTRAP 4
+#endif
+constexpr int kGRigid = SPHG_G_RIGID;   // lanes per rigid particle in k_forces_rigid (swept)
+constexpr int kGExtrap = SPHG_G_EXTRAP; // lanes per wall/rigid particle in k_extrapolate (swept)
 
 #define SPHG_IMG_DISPATCH(MODE, CALL)                             \
   do {                                                            \
@@ -756,7 +764,7 @@ void launch_diffusion(Ctx& c) {
 
 void launch_extrapolate(Ctx& c) {
   if (c.nw == 0) return;
-  constexpr int G = kGOther;
+  constexpr int G = kGExtrap;
   if (c.P.single_eos)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_extrapolate<G, M, false><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw)));
@@ -779,10 +787,10 @@ static void launch_forces_fluid_t(Ctx& c) {
 template <bool kTvf>
 static void launch_forces_rigid_t(Ctx& c) {
   if (c.nrigid && c.P.single_eta)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGOther, M, kTvf, true><<<blocks_for<kGOther>(c.nrigid), kBlock, 0, c.stream>>>(
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGRigid, M, kTvf, true><<<blocks_for<kGRigid>(c.nrigid), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.dflags)));
   else if (c.nrigid)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGOther, M, kTvf, false><<<blocks_for<kGOther>(c.nrigid), kBlock, 0, c.stream>>>(
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGRigid, M, kTvf, false><<<blocks_for<kGRigid>(c.nrigid), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.dflags)));
   c.launches++;
 }
