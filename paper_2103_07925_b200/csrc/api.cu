@@ -756,7 +756,10 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     c.nb = nb;
     h2d(c.bodies.p, bodies, nb, c.stream);
     SPHG_CUDA_CHECK(cudaMemsetAsync(c.dflags, 0, sizeof(DevFlags), c.stream));
-    if (c.built) launch_rigid_index(c);  // kinds / bodies may have changed
+    if (c.built) {  // kinds / bodies may have changed
+      launch_rigid_index(c);
+      launch_contact_order(c);
+    }
     SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     c.have_state = true;
     h->mid_step = false;
@@ -1130,7 +1133,7 @@ void sphg_destroy(sphg_ctx* h) {
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
   c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();
   c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();
-  c.fidx.free(); c.widx.free(); c.brick_buf.free(); c.scan_cells.free(); c.dl_buf.free(); c.idx_of_gid.free(); c.body_buf.free();
+  c.fidx.free(); c.widx.free(); c.ncon.free(); c.brick_buf.free(); c.scan_cells.free(); c.dl_buf.free(); c.idx_of_gid.free(); c.body_buf.free();
   for (auto& b : c.halo_ids) b.free();
   if (c.dflags) cudaFree(c.dflags);
   if (c.hflags) cudaFreeHost(c.hflags);

@@ -97,6 +97,7 @@ struct Ctx {
   NbrList nl() const { return {nbr.p, cnt.p, (size_t)cap}; }
   // per-kind index lists: fluid, non-fluid (rigid + boundary), rigid body-major
   DBuf<uint32_t> fidx, widx, ridx, body_start;
+  DBuf<uint32_t> ncon;  // per rigid particle: contact candidates at the front of its non-fluid row part
   DBuf<uint32_t> brick_buf, scan_cells;
   DBuf<uint8_t> dl_buf;  // download: requested store fields in gid order  // kind-list construction in brick order
   size_t nf = 0, nw = 0, nrigid = 0;
@@ -181,6 +182,7 @@ void body_apply_totals(Ctx& c, const double* dev_tot);
 // kernels_transition.cu
 int launch_transitions(Ctx& c);  // 0 ok, else error code
 void launch_repartition_rows(Ctx& c);
+void launch_contact_order(Ctx& c);
 
 inline int grid_for(size_t n, int block) { return (int)((n + block - 1) / block); }
 

@@ -515,6 +515,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
 template <int G, int M, bool kTvf, bool kSingleEta>
 __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                           const uint32_t* __restrict__ list, size_t nlist,
+                                                          const uint32_t* __restrict__ ncon,
                                                           DevFlags* __restrict__ fl) {
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
@@ -568,8 +569,10 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
       f.y -= a.y;
       f.z -= a.z;
     }
-    // contact: rigid particles of other bodies and walls
-    for (int k = lane; k < Rw.no; k += G) {
+    // contact: rigid particles of other bodies and walls, ordered first in the
+    // non-fluid part by k_contact_order (ncon of them)
+    const int ncand = (int)ncon[r];
+    for (int k = lane; k < ncand; k += G) {
       const uint32_t e = __ldg(Rw.b + k);
       const uint32_t j = nb_index<M>(e);
       const uint32_t kindj = kind_of(D.kmd.p[j]);
@@ -788,10 +791,10 @@ template <bool kTvf>
 static void launch_forces_rigid_t(Ctx& c) {
   if (c.nrigid && c.P.single_eta)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGRigid, M, kTvf, true><<<blocks_for<kGRigid>(c.nrigid), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.dflags)));
+                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags)));
   else if (c.nrigid)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGRigid, M, kTvf, false><<<blocks_for<kGRigid>(c.nrigid), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.dflags)));
+                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags)));
   c.launches++;
 }
 

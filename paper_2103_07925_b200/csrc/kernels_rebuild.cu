@@ -424,6 +424,90 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
   if (mx) atomicMax(&fl->max_count, mx);
 }
 
+// ------------------------------------------------------ contact order
+// Contact only acts between different bodies or a body and a wall.  For every
+// rigid particle the non-fluid part of its row is reordered (a set: order is free) so that those
+// candidates come first, and their number is kept in ncon: k_forces_rigid then scans ncon entries
+// instead of the whole non-fluid part, which for a body's interior is all its own particles.
+// Redone at every rebuild and after transitions (group ids change).  Warp per rigid particle.
+constexpr int kConWarps = 8;
+constexpr int kConMaxRow = 1024;
+template <int M>
+__global__ void __launch_bounds__(32 * kConWarps) k_contact_order(const uint32_t* __restrict__ kmd,
+                                                                   const uint32_t* __restrict__ group,
+                                                                   uint32_t* __restrict__ nbr,
+                                                                   const uint32_t* __restrict__ cnt, int cap,
+                                                                   const uint32_t* __restrict__ ridx, size_t nrigid,
+                                                                   uint32_t* __restrict__ ncon) {
+  __shared__ uint32_t buf[kConWarps][kConMaxRow];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const size_t g = (size_t)blockIdx.x * kConWarps + wib;
+  if (g >= nrigid) return;  // warp-uniform
+  const uint32_t r = ridx[g];
+  const uint32_t c = cnt[r];
+  const uint32_t nf = cnt_fluid(c), no = cnt_other(c);
+  uint32_t* seg = nbr + (size_t)r * cap + nf;
+  if (no > (uint32_t)kConMaxRow) {  // not reordered: scan the whole part
+    if (lane == 0) ncon[r] = no;
+    return;
+  }
+  const uint32_t body = group[r];
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t nc = 0;
+  for (uint32_t base = 0; base < no; base += 32) {
+    const uint32_t k = base + lane;
+    bool cand = false;
+    if (k < no) {
+      const uint32_t j = nb_index<M>(seg[k]);
+      cand = kind_of(kmd[j]) == SPHG_BOUNDARY || group[j] != body;
+    }
+    nc += __popc(__ballot_sync(0xffffffffu, cand));
+  }
+  uint32_t fo = 0, oo = 0;
+  for (uint32_t base = 0; base < no; base += 32) {
+    const uint32_t k = base + lane;
+    const bool in = k < no;
+    const uint32_t e = in ? seg[k] : 0u;
+    bool cand = false;
+    if (in) {
+      const uint32_t j = nb_index<M>(e);
+      cand = kind_of(kmd[j]) == SPHG_BOUNDARY || group[j] != body;
+    }
+    const uint32_t bc = __ballot_sync(0xffffffffu, in && cand), bo = __ballot_sync(0xffffffffu, in && !cand);
+    if (in) buf[wib][cand ? fo + __popc(bc & lt) : nc + oo + __popc(bo & lt)] = e;
+    fo += __popc(bc);
+    oo += __popc(bo);
+  }
+  __syncwarp();
+  for (uint32_t k = lane; k < no; k += 32) seg[k] = buf[wib][k];
+  if (lane == 0) ncon[r] = nc;
+}
+
+}  // namespace
+
+void launch_contact_order(Ctx& c) {
+  if (c.nrigid == 0) return;
+  c.ncon.alloc(std::max<size_t>(c.n, 1));
+  const unsigned blocks = (unsigned)((c.nrigid + kConWarps - 1) / kConWarps);
+  switch (c.P.img_mode) {
+    case kImgNone:
+      k_contact_order<kImgNone><<<blocks, 32 * kConWarps, 0, c.stream>>>(c.cur.kmd.p, c.cur.group.p, c.nbr.p, c.cnt.p,
+                                                                          c.cap, c.ridx.p, c.nrigid, c.ncon.p);
+      break;
+    case kImgCode:
+      k_contact_order<kImgCode><<<blocks, 32 * kConWarps, 0, c.stream>>>(c.cur.kmd.p, c.cur.group.p, c.nbr.p, c.cnt.p,
+                                                                          c.cap, c.ridx.p, c.nrigid, c.ncon.p);
+      break;
+    default:
+      k_contact_order<kImgMin><<<blocks, 32 * kConWarps, 0, c.stream>>>(c.cur.kmd.p, c.cur.group.p, c.nbr.p, c.cnt.p,
+                                                                         c.cap, c.ridx.p, c.nrigid, c.ncon.p);
+      break;
+  }
+  c.launches++;
+}
+
+namespace {
+
 // ------------------------------------------------------- rigid index
 __global__ void k_rigid_flags(const uint32_t* __restrict__ kmd, size_t n, uint32_t* __restrict__ flag) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -609,6 +693,7 @@ void launch_rebuild(Ctx& c) {
     c.nbr.free();
   }
   launch_rigid_index(c);
+  launch_contact_order(c);
   c.built = true;
   c.rebuilds++;
 }

@@ -459,8 +459,9 @@ int launch_transitions(Ctx& c) {
   old.free();
   c.n_melt += nmelt;
   c.n_solid += nsolid;
-  // kinds changed: the rows' fluid / non-fluid partition is stale
+  // kinds changed: the rows' fluid / non-fluid partition is stale; body ids changed: contact order
   launch_repartition_rows(c);
+  if (c.built) launch_contact_order(c);
   return 0;
 }
 

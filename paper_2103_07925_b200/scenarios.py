@@ -241,7 +241,7 @@ def _finish(store, bodies):
 
 def periodic_spheres(nside=32, n_spheres=4, r_range=(4.0, 4.0), dx=1e-3, dt=1e-5, seed=2103,
                      rho_f=1000.0, c=10.0, eta=1e-3, rho_s=2000.0, kc=1e3, zeta=0.1, u0=0.01,
-                     jitter=0.05, name="c1", steps=100):
+                     jitter=0.05, name="c1", steps=100, centers=None, radii=None):
     """BASELINE configs[0] (C1: 32^3, 4 spheres R=4dx) and configs[4] (C5: 400^3, ~20k spheres R~U[3,6]dx).
 
     Periodic cube, lattice + uniform jitter, fluid u ~ U(-u0, u0), spheres
@@ -257,7 +257,9 @@ def periodic_spheres(nside=32, n_spheres=4, r_range=(4.0, 4.0), dx=1e-3, dt=1e-5
     params = _params(dx, dt, lo, hi, (1, 1, 1), mats, kc=kc, dc=damping_from_ratio(zeta, kc, m_r))
     pos = lattice_box(lo, hi, dx)
     n = len(pos)
-    centers, radii = place_spheres(seed, n_spheres, lo, (L, L, L), r_range[0], r_range[1], dx, True)
+    if centers is None:
+        centers, radii = place_spheres(seed, n_spheres, lo, (L, L, L), r_range[0], r_range[1], dx, True)
+    centers, radii = np.asarray(centers, np.float64), np.asarray(radii, np.float64)
     owner = mark_spheres((nside,) * 3, lo, dx, (L, L, L), centers, radii, (True, True, True))
     s = ParticleStore(n)
     u = splitmix_u01(seed, 0, np.arange(3 * n, dtype=np.uint64)).reshape(n, 3)
@@ -282,6 +284,23 @@ def periodic_spheres(nside=32, n_spheres=4, r_range=(4.0, 4.0), dx=1e-3, dt=1e-5
     info = dict(n=n, n_fluid=int((~rig).sum()), n_rigid=int(rig.sum()), n_boundary=0,
                 n_bodies=len(centers), rigid_fraction=float(rig.mean()))
     return Scenario(name, params, s, bodies, steps, info)
+
+
+def colliding_spheres(nside=20, R=3.0, gap=-0.3, u=0.05, dx=1e-3, **kw):
+    """Two spheres of radius R dx, centres 2R + gap + 1 dx apart along x (the default puts three
+    particle pairs of the two bodies within the contact range dx), approaching each other
+    at +-u: spring-dashpot contact is active from the first force evaluation."""
+    L = nside * dx
+    c0 = 0.5 * L
+    off = (R + 0.5 * gap + 0.5) * dx  # +0.5: lattice points sit at half spacings
+    centers = [(c0 - off, c0, c0), (c0 + off, c0, c0)]
+    sc = periodic_spheres(nside=nside, dx=dx, centers=centers, radii=[R * dx, R * dx], name="collide", **kw)
+    s, b = sc.store, sc.bodies
+    for k, sgn in ((0, 1.0), (1, -1.0)):
+        b["vel"][k] = (sgn * u, 0.0, 0.0)
+        s.vel[(s.kind == abi.RIGID) & (s.group == k)] = (sgn * u, 0.0, 0.0)
+    s.vel_adv[:] = s.vel
+    return sc
 
 
 def config1(**kw):

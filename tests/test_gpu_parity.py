@@ -439,3 +439,23 @@ def test_count_pairs(Oracle):
     assert inter == int(hit.sum())
     assert inter_f == int(hit[o.kind[i] == abi.FLUID].sum())
     assert inter_o == inter - inter_f
+
+
+def test_contact_parity(Oracle):
+    """Two bodies inside each other's contact range, approaching: spring-dashpot contact
+     on the device vs the oracle, initial forces and 5 steps (the contact candidates
+    are ordered first in each rigid row by k_contact_order)."""
+    sc = scenarios.colliding_spheres()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    _, ob = orc.download()
+    p0 = scenarios.colliding_spheres().params
+    p0.kc = p0.dc = 0.0
+    nocontact = Oracle(p0)
+    nocontact.upload(sc.store, sc.bodies)
+    nocontact.initialize()
+    _, nb = nocontact.download()
+    assert np.all(np.abs(ob["force"][:, 0] - nb["force"][:, 0]) > 1e-3 * np.abs(nb["force"][:, 0]))  # contact acts
+    compare_state(sim, orc, sc.params, what="contact init")
+    sim.step(5)
+    orc.step(5)
+    compare_state(sim, orc, sc.params, tol=1e-7, what="contact 5 steps")
