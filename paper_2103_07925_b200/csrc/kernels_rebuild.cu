@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
 // instead of the whole non-fluid part, which for a body's interior is all its own particles.
 // Redone at every rebuild and after transitions (group ids change).  Warp per rigid particle.
 constexpr int kConWarps = 8;
-constexpr int kConMaxRow = 1024;
+constexpr int kConMaxRow = 512;
 template <int M>
 __global__ void __launch_bounds__(32 * kConWarps) k_contact_order(const uint32_t* __restrict__ kmd,
                                                                    const uint32_t* __restrict__ group,
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(32 * kConWarps) k_contact_order(const uint32_t
                                                                    const uint32_t* __restrict__ cnt, int cap,
                                                                    const uint32_t* __restrict__ ridx, size_t nrigid,
                                                                    uint32_t* __restrict__ ncon) {
-  __shared__ uint32_t buf[kConWarps][kConMaxRow];
+  __shared__ uint32_t buf[kConWarps][kConMaxRow], rest[kConWarps][kConMaxRow];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const size_t g = (size_t)blockIdx.x * kConWarps + wib;
   if (g >= nrigid) return;  // warp-uniform
@@ -453,16 +453,7 @@ __global__ void __launch_bounds__(32 * kConWarps) k_contact_order(const uint32_t
   }
   const uint32_t body = group[r];
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t nc = 0;
-  for (uint32_t base = 0; base < no; base += 32) {
-    const uint32_t k = base + lane;
-    bool cand = false;
-    if (k < no) {
-      const uint32_t j = nb_index<M>(seg[k]);
-      cand = kind_of(kmd[j]) == SPHG_BOUNDARY || group[j] != body;
-    }
-    nc += __popc(__ballot_sync(0xffffffffu, cand));
-  }
+  // one pass: candidates and the rest into two staging buffers, then both back in order
   uint32_t fo = 0, oo = 0;
   for (uint32_t base = 0; base < no; base += 32) {
     const uint32_t k = base + lane;
@@ -474,13 +465,19 @@ __global__ void __launch_bounds__(32 * kConWarps) k_contact_order(const uint32_t
       cand = kind_of(kmd[j]) == SPHG_BOUNDARY || group[j] != body;
     }
     const uint32_t bc = __ballot_sync(0xffffffffu, in && cand), bo = __ballot_sync(0xffffffffu, in && !cand);
-    if (in) buf[wib][cand ? fo + __popc(bc & lt) : nc + oo + __popc(bo & lt)] = e;
+    if (in) {
+      if (cand) buf[wib][fo + __popc(bc & lt)] = e;
+      else rest[wib][oo + __popc(bo & lt)] = e;
+    }
     fo += __popc(bc);
     oo += __popc(bo);
   }
   __syncwarp();
-  for (uint32_t k = lane; k < no; k += 32) seg[k] = buf[wib][k];
-  if (lane == 0) ncon[r] = nc;
+  if (fo != 0 && oo != 0) {  // nothing to move when the part is all one class
+    for (uint32_t k = lane; k < fo; k += 32) seg[k] = buf[wib][k];
+    for (uint32_t k = lane; k < oo; k += 32) seg[fo + k] = rest[wib][k];
+  }
+  if (lane == 0) ncon[r] = fo;
 }
 
 }  // namespace
