@@ -809,8 +809,8 @@ bool stage_kick_drift(Ctx& c) {
         const sphfsi::Quaternion q = sphfsi::orientation_step<3>(qof(b), w, dt);
         b.q[0] = q.w; b.q[1] = q.x; b.q[2] = q.y; b.q[3] = q.z;
     }
-    bool escaped = false;
-    int64_t bad = 0;
+    bool escaped = false, nonfinite = false;
+    int64_t bad = std::numeric_limits<int64_t>::max(), bad_nf = std::numeric_limits<int64_t>::max();
     double md2 = 0.0;
 #pragma omp parallel for schedule(static) reduction(max : umax, md2)
     for (int64_t i = 0; i < n; ++i) {
@@ -836,17 +836,23 @@ bool stage_kick_drift(Ctx& c) {
         } else {
             continue;
         }
-        for (int a = 0; a < 3; ++a)
-            if (!c.P.periodic[a] && (c.S.pos[i][a] < c.P.lo[a] || c.S.pos[i][a] > c.P.hi[a])) {
+        for (int a = 0; a < 3; ++a) {
+            if (!std::isfinite(c.S.pos[i][a])) {  // a blown-up state: SPEC:625 runtime assertion
 #pragma omp critical
-                { escaped = true; bad = i; }
+                { nonfinite = true; bad_nf = std::min(bad_nf, i); }
+            } else if (!c.P.periodic[a] && (c.S.pos[i][a] < c.P.lo[a] || c.S.pos[i][a] > c.P.hi[a])) {
+#pragma omp critical
+                { escaped = true; bad = std::min(bad, i); }
             }
+        }
         if (c.built) md2 = std::max(md2, r2of(mi3(c, c.S.pos[i], c.pos_ref[i])));
     }
     c.u_max = std::sqrt(umax);
     c.max_disp = std::sqrt(md2);
     c.t += c.dt;
     if (escaped) return fail(c, "escaped particle " + std::to_string(bad) + " at step " + std::to_string(c.steps + 1));
+    if (nonfinite)
+        return fail(c, "non-finite state of particle " + std::to_string(bad_nf) + " at step " + std::to_string(c.steps + 1));
     return true;
 }
 

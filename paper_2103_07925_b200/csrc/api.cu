@@ -240,8 +240,11 @@ int check_flags(sphg_ctx* h, bool sync) {
   c.max_disp = std::sqrt(bits_to_double(f.max_disp2_bits));
   c.u_max = std::sqrt(bits_to_double(f.umax2_bits));
   if (f.err) {
+    const std::string step = " at step " + std::to_string(c.steps + (h->mid_step ? 1 : 0));
+    if (!(f.err & (kErrEscape | kErrCoincident)) && (f.err & kErrNaN))
+      return fail(h, SPHG_ERR_RUNTIME, "non-finite state of particle " + std::to_string(f.err_gid2) + step);
     std::string what = (f.err & kErrEscape) ? "escaped particle " : (f.err & kErrCoincident) ? "coincident particles at particle " : "runtime assertion at particle ";
-    return fail(h, SPHG_ERR_RUNTIME, what + std::to_string(f.err_gid) + " at step " + std::to_string(c.steps + (h->mid_step ? 1 : 0)));
+    return fail(h, SPHG_ERR_RUNTIME, what + std::to_string(f.err_gid) + step);
   }
   return SPHG_OK;
 }
@@ -679,6 +682,8 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     SPHG_CUDA_CHECK(cudaMalloc(&c.dflags, sizeof(DevFlags)));
     SPHG_CUDA_CHECK(cudaMemset(c.dflags, 0, sizeof(DevFlags)));
+    // the offending gids are reduced with atomicMin: start them at "none"
+    SPHG_CUDA_CHECK(cudaMemset(&c.dflags->err_gid, 0xff, 2 * sizeof(uint32_t)));
     SPHG_CUDA_CHECK(cudaMallocHost(&c.hflags, sizeof(DevFlags)));
     std::memset(c.hflags, 0, sizeof(DevFlags));
     SPHG_CUDA_CHECK(cudaEventCreate(&c.ev[0]));
@@ -756,6 +761,7 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     c.nb = nb;
     h2d(c.bodies.p, bodies, nb, c.stream);
     SPHG_CUDA_CHECK(cudaMemsetAsync(c.dflags, 0, sizeof(DevFlags), c.stream));
+    SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->err_gid, 0xff, 2 * sizeof(uint32_t), c.stream));
     if (c.built) {  // kinds / bodies may have changed
       launch_rigid_index(c);
       launch_contact_order(c);

@@ -114,7 +114,10 @@ __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevP
       const double xs[3] = {pn.x, pn.y, pn.z};
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        if (!P.periodic[a] && (xs[a] < P.lo[a] || xs[a] > P.hi[a])) {
+        if (!isfinite(xs[a])) {  // a blown-up state (SPEC:625 runtime assertion)
+          atomicOr(&fl->err, kErrNaN);
+          atomicMin(&fl->err_gid2, D.gid.p[k]);
+        } else if (!P.periodic[a] && (xs[a] < P.lo[a] || xs[a] > P.hi[a])) {
           atomicOr(&fl->err, kErrEscape);
           atomicMin(&fl->err_gid, D.gid.p[k]);
         }

@@ -178,24 +178,40 @@ def test_empty_store():
     assert sim.stats().steps == 3
 
 
-def test_coincident_particles_fail():
+def test_coincident_particles_fail():  # fatal, names the particle
     sc = scenarios.config1(nside=16, n_spheres=0)
     sc.store.pos[5] = sc.store.pos[6]
     sim = Simulation(sc.params)
     sim.upload(sc.store, sc.bodies)
     with pytest.raises(SPHError) as e:
         sim.initialize()
-    assert e.value.code == 3 and "coincident" in str(e.value)
+    assert e.value.code == 3 and "coincident particles at particle 5 " in str(e.value)
 
 
-def test_escaped_particle_fail():
+def test_escaped_particle_fail():  # fatal, names the particle and the step
     sc = scenarios.config2(nside=12, n_grid=1, r_range=(2.0, 2.0))
-    sc.store.pos[0, 2] = sc.params.hi[2] + 1e-3
+    sc.store.pos[7, 2] = sc.params.hi[2] + 1e-3
     sim = Simulation(sc.params)
     sim.upload(sc.store, sc.bodies)
     with pytest.raises(SPHError) as e:
         sim.initialize()
-    assert e.value.code == 3 and "escaped" in str(e.value)
+    assert e.value.code == 3 and "escaped particle 7 " in str(e.value)
+
+
+def test_non_finite_state_fail(Oracle):  # SPEC:625 runtime assertion on a blown-up state
+    """A NaN velocity spreads through the initial forces to the particle's neighbours; both engines
+    stop at step 1 naming the same (smallest) gid of the non-finite set."""
+    sc = scenarios.config1(nside=16, n_spheres=1, r_range=(3.0, 3.0))
+    sc.store.vel[9] = np.nan
+    msgs = []
+    for eng in (Simulation(sc.params), Oracle(sc.params)):
+        eng.upload(sc.store, sc.bodies)
+        eng.initialize()
+        with pytest.raises(SPHError) as e:
+            eng.step(1)
+        assert e.value.code == 3 and "non-finite state of particle" in str(e.value), str(e.value)
+        msgs.append(str(e.value).split("non-finite")[1])
+    assert msgs[0] == msgs[1]
 
 
 def test_nlist_capacity_growth(Oracle):
