@@ -475,3 +475,28 @@ def test_contact_parity(Oracle):
     sim.step(5)
     orc.step(5)
     compare_state(sim, orc, sc.params, tol=1e-7, what="contact 5 steps")
+
+
+@pytest.mark.parametrize("case", ["c1_small", "c2_small"])
+def test_without_transport_velocity(case, Oracle):
+    """transport_velocity = false (config.hpp:90): the kTvf = false kernel variants (no A-tensor,
+    no background pressure, drift with u)."""
+    sc = CASES[case]()
+    sc.params.tvf = 0
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    sim.step(2)
+    orc.step(2)
+    compare_state(sim, orc, sc.params, tol=1e-9, what=f"{case} tvf=0")
+
+
+def test_heat_with_distinct_conductivities(Oracle):
+    """Materials with different conductivities: the harmonic-mean kappa~ path of k_heat (the
+    single-kappa shortcut is off), with melting at step 1."""
+    sc = CASES["c2_melt"]()
+    p = sc.params
+    p.mat[1].kappa = 35.0   # solid conducts better than the liquids
+    p.mat[3].kappa = 5.0    # walls
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    sim.step(2)
+    orc.step(2)
+    compare_state(sim, orc, p, tol=1e-9, what="multi-kappa heat")
