@@ -500,3 +500,18 @@ def test_heat_with_distinct_conductivities(Oracle):
     sim.step(2)
     orc.step(2)
     compare_state(sim, orc, p, tol=1e-9, what="multi-kappa heat")
+
+
+def test_compute_dt_uses_device_u_max(Oracle):
+    """compute_dt on the device: the CFL term from the kick's u_max (max |u^{n+1/2}|
+    of the fluid) agrees with the oracle's; the other terms are the host formula."""
+    from paper_2103_07925_b200.sim import dt_limits
+    sc = CASES["c1_small"]()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    sim.step(3)
+    orc.step(3)
+    assert abs(sim.stats().u_max - orc.stats().u_max) <= 1e-9 * orc.stats().u_max
+    lim = sim.compute_dt()
+    m_r = sc.params.mat[1].rho0 * sc.params.dx ** 3
+    want = dt_limits(sc.params, orc.stats().u_max, m_r)
+    assert np.allclose(lim, want, rtol=1e-9, atol=0.0, equal_nan=True)
