@@ -148,6 +148,14 @@ DevParams make_dev_params(const sphg_params& p) {
       P.sched[g].value[k] = p.dirichlet_T[g].value[k];
     }
   }
+  P.single_g = 1;
+  if (p.n_mat > 0) {
+    const sphg_material& dm = p.mat[p.default_fluid_mat >= 0 && p.default_fluid_mat < p.n_mat ? p.default_fluid_mat : 0];
+    for (int m = 0; m < p.n_mat; ++m)
+      if (p.mat[m].c > 0.0 && p.mat[m].nu >= 0.0)  // a fluid-capable material
+        for (int a = 0; a < 3; ++a)
+          if (p.mat[m].body_force[a] != dm.body_force[a]) P.single_g = 0;
+  }
   P.n_schedC = p.n_dirichlet_c;
   for (int g = 0; g < p.n_dirichlet_c && g < SPHG_MAX_DIRICHLET; ++g) {
     P.schedC[g].n = p.dirichlet_C[g].n;

@@ -50,6 +50,7 @@ struct DevParams {
   int32_t single_kappa; // all materials share kappa       -> kappa~ = 2 kappa
   int32_t single_eos;   // all fluid materials share rho0,c -> wall EOS material fixed
   int32_t img_mode;     // neighbour-entry image mode (kImgNone / kImgCode / kImgMin)
+  int32_t single_g;     // every fluid-capable material has default_fluid_mat's body force
   // moving wall groups (sphg_set_wall_motion), refreshed by the host before every kick [P20]:
   // velocity at t^{n+1/2} (drift), velocity and acceleration at t^{n+1} (wall state)
   int32_t n_walls, pad_w;

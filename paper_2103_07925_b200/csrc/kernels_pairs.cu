@@ -291,15 +291,16 @@ __global__ void __launch_bounds__(kBlock) k_extrapolate(const __grid_constant__ 
       const uint32_t e = en;
       en = k + G < R.nf ? __ldg(R.f + k + G) : 0u;  // row entries stream from HBM: prefetch
       const uint32_t f = nb_index<M>(e);
-      const double4 g0 = ld4(&D.G0.p[f]);
+      // fluid records are only read here (the kernel writes wall/rigid records): read-only path
+      const double4 g0 = ldg4(&D.G0.p[f]);
       const double3 d = pair_delta<M>(P, pw, ld3(g0), e);
       const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
       if (r2 > P.rc2) continue;
       double ri;
       const double W = shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);  // sigma cancels in the ratios
-      const double4 g1 = D.G1.p[f];
-      const double pf = D.G2.p[f].w;
-      const uint32_t mf = kMultiEos || P.n_mat > 1 ? mat_of(D.kmd.p[f]) : 0u;
+      const double4 g1 = ldg4(&D.G1.p[f]);
+      const double pf = __ldg(reinterpret_cast<const double*>(&D.G2.p[f]) + 3);
+      const uint32_t mf = kMultiEos || !P.single_g ? mat_of(__ldg(&D.kmd.p[f])) : (uint32_t)P.default_fluid_mat;
       const DevMat& Mf = P.mat[mf];
       const double ga = (Mf.g[0] - aw.x) * d.x + (Mf.g[1] - aw.y) * d.y + (Mf.g[2] - aw.z) * d.z;
       sw += W;
