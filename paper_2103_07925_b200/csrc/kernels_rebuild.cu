@@ -267,18 +267,35 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
       if (bi) in &= ~bmask[tb >> 5];
       const uint32_t fm = fmask[tb >> 5];
       uint32_t hf = in & fm, ho = in & ~fm;
-      while (hf) {  // fluid neighbours from the front
-        const int u = __ffs(hf) - 1;
-        hf &= hf - 1;
-        if ((int)nf < cap) row[nf] = se[tb + u];
-        ++nf;
+      const uint32_t cf = __popc(hf), co = __popc(ho);
+      const uint32_t* seb = se + tb;
+      if (nf + cf <= (uint32_t)cap && no + co <= (uint32_t)cap) {  // common case: no bound checks
+        uint32_t* wp = row + nf;
+        while (hf) {  // fluid neighbours from the front
+          const int u = __ffs(hf) - 1;
+          hf &= hf - 1;
+          *wp++ = seb[u];
+        }
+        uint32_t* bp = back - no;
+        while (ho) {  // rigid / boundary neighbours from the back
+          const int u = __ffs(ho) - 1;
+          ho &= ho - 1;
+          *bp-- = seb[u];
+        }
+      } else {  // overflowing row: count only what fits (the caller rebuilds with a larger cap)
+        for (uint32_t k = nf; hf; ++k) {
+          const int u = __ffs(hf) - 1;
+          hf &= hf - 1;
+          if ((int)k < cap) row[k] = seb[u];
+        }
+        for (uint32_t k = no; ho; ++k) {
+          const int u = __ffs(ho) - 1;
+          ho &= ho - 1;
+          if ((int)k < cap) back[-(int)k] = seb[u];
+        }
       }
-      while (ho) {  // rigid / boundary neighbours from the back
-        const int u = __ffs(ho) - 1;
-        ho &= ho - 1;
-        if ((int)no < cap) back[-(int)no] = se[tb + u];
-        ++no;
-      }
+      nf += cf;
+      no += co;
     }
     if (act) hc[i - h0] = pack_cnt(nf, no);
   }
