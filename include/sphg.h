@@ -250,7 +250,8 @@ int sphg_halo_set(sphg_ctx* ctx, int slot, const uint32_t* local_ids, size_t n);
 int sphg_halo_pack(sphg_ctx* ctx, int phase, int slot, double* buf);
 int sphg_halo_unpack(sphg_ctx* ctx, int phase, int slot, const double* buf);
 /* Per-body compensated partial sums over owned rigid particles: nb x 24 doubles (12 x (sum, comp):
- * f xyz, torque xyz, inertia xx yy zz xy xz yz), written to host memory. */
+ * f xyz, torque xyz, inertia xx yy zz xy xz yz).  `out` / `totals` may be host or device pointers
+ * (unified addressing), so an NCCL driver gathers and merges them without host staging. */
 int sphg_body_partials(sphg_ctx* ctx, double* out);
 /* Global per-body sums (nb x 12, merged by the caller in rank order) -> f, tau, I, a_k, alpha_k. */
 int sphg_body_apply_totals(sphg_ctx* ctx, const double* totals);
