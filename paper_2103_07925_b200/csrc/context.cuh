@@ -163,6 +163,7 @@ void launch_extrapolate(Ctx& c);
 void launch_forces(Ctx& c);
 void launch_forces_fluid(Ctx& c);
 void launch_forces_rigid(Ctx& c);
+void launch_forces_diag(Ctx& c);  // diagnostic builds only (stage 12)
 void launch_bodies(Ctx& c);
 void launch_final_kick(Ctx& c);
 void launch_mass(Ctx& c, const uint32_t* body_mask);

@@ -511,6 +511,39 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
   D.B4.p[i] = make_double4(f * bg.x, f * bg.y, f * bg.z, 0.0);
 }
 
+#ifdef SPHG_DIAG_LOADS_ONLY
+// Diagnostic twin of k_forces_fluid (built only with -DSPHG_DIAG_LOADS_ONLY): the same row walk,
+// the same three 256-bit neighbour loads and r^2 test, almost no arithmetic; results go to a
+// scratch array.  Timed as stage 12 to separate the gather cost from the pair arithmetic.
+template <int G, int M>
+__global__ void __launch_bounds__(kBlock) k_forces_loads_only(const __grid_constant__ DevParams P, Particles D,
+                                                               NbrList L, const uint32_t* __restrict__ list,
+                                                               size_t nlist, double* __restrict__ scratch) {
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  const size_t g = t / G;
+  const int lane = (int)(t % G);
+  const bool active = g < nlist;
+  const uint32_t i = active ? list[g] : 0u;
+  double s = 0.0;
+  if (active) {
+    const double3 pi = ld3(ldg4(&D.G0.p[i]));
+    const Row R = row_of(L, i);
+    uint32_t e = lane < R.n ? __ldg(R.f + lane) : 0u;
+    for (int k = lane; k < R.n; k += G) {
+      const uint32_t en = k + G < R.n ? __ldg(R.f + k + G) : 0u;
+      const uint32_t j = nb_index<M>(e);
+      const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
+      const double3 d = pair_delta<M>(P, pi, ld3(h0), e);
+      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+      if (r2 <= P.rc2) s += h0.w + h1.x + h1.y + h1.z + h1.w + h2.x + h2.y + h2.z + h2.w;
+      e = en;
+    }
+  }
+  s = gsum<G>(s);
+  if (active && lane == 0) scratch[i] = s;
+}
+#endif
+
 // f_r = sum_i -m_i a_ir over the fluid part of the row (a_ir from the fluid's view)
 //     + contact over the rigid/boundary part
 template <int G, int M, bool kTvf, bool kSingleEta>
@@ -806,6 +839,18 @@ void launch_forces_fluid(Ctx& c) {
   else if (tvf) launch_forces_fluid_t<true, false>(c);
   else if (single) launch_forces_fluid_t<false, true>(c);
   else launch_forces_fluid_t<false, false>(c);
+}
+
+void launch_forces_diag(Ctx& c) {
+#ifdef SPHG_DIAG_LOADS_ONLY
+  if (c.nf == 0) return;
+  static DBuf<double> scratch;
+  scratch.alloc(c.n);
+  SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_loads_only<4, M><<<blocks_for<4>(c.nf), kBlock, 0, c.stream>>>(
+                                       c.P, c.cur, c.nl(), c.fidx.p, c.nf, scratch.p)));
+#else
+  (void)c;
+#endif
 }
 
 void launch_forces_rigid(Ctx& c) {
