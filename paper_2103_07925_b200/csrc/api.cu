@@ -748,10 +748,10 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     c.cell_key.alloc(na);
     c.cnt.alloc(na);
     const bool any_periodic = c.P.periodic[0] || c.P.periodic[1] || c.P.periodic[2];
-    // image-coded entries need the index in 26 bits; larger stores use the minimum image
+    // image-coded entries need the index in 27 bits; larger stores use the minimum image
     // (SPHG_IMG_MIN=1 forces that path for testing at small sizes)
     static const bool force_min = std::getenv("SPHG_IMG_MIN") && std::atoi(std::getenv("SPHG_IMG_MIN")) != 0;
-    const int mode = !any_periodic ? kImgNone : ((n < (size_t(1) << 26) && !force_min) ? kImgCode : kImgMin);
+    const int mode = !any_periodic ? kImgNone : ((n < (size_t(1) << kIdxBits) && !force_min) ? kImgCode : kImgMin);
     if (mode != c.P.img_mode) {
       c.P.img_mode = mode;
       c.built = false;

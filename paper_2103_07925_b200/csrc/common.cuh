@@ -175,12 +175,17 @@ __device__ __forceinline__ double sqrt_and_rinv(double x, double& rinv) {
 
 // ------------------------------------------------- neighbour-list entries
 // Row-major Verlet list: nbr[i * cap + k], k < cnt[i].  With periodic axes and
-// N < 2^26 an entry packs the neighbour index (26 bits) with the periodic image
-// of its cell (2 bits per axis: 0 none, 1 +L, 2 -L), fixed at build time.  For
-// any pair inside r_v + skin < L/2 this reproduces the minimum image of the
-// oracle; the pair kernels then need 3 adds instead of 6 compares + selects.
+// N < 2^27 an entry packs the neighbour index (27 bits) with the periodic image
+// of its cell (per axis 0 none, 1 +L, 2 -L, packed base 3 into 5 bits), fixed at
+// build time.  For any pair inside r_v + skin < L/2 this reproduces the minimum
+// image of the oracle; the pair kernels then need 3 adds (on the rare wrapped
+// entries) instead of 6 compares + selects.  Larger stores keep plain indices.
 enum { kImgNone = 0, kImgCode = 1, kImgMin = 2 };
-constexpr uint32_t kIdxMask = 0x03FFFFFFu;
+constexpr int kIdxBits = 27;
+constexpr uint32_t kIdxMask = (1u << kIdxBits) - 1u;
+__host__ __device__ __forceinline__ uint32_t img_tag(uint32_t ix, uint32_t iy, uint32_t iz) {
+  return (ix + 3u * iy + 9u * iz) << kIdxBits;
+}
 
 template <int M>
 __device__ __forceinline__ uint32_t nb_index(uint32_t e) {
@@ -194,10 +199,11 @@ template <int M>
 __device__ __forceinline__ double3 pair_delta(const DevParams& P, double3 a, double3 b, uint32_t e) {
   if (M == kImgMin) return make_double3(mimg(P, a.x - b.x, 0), mimg(P, a.y - b.y, 1), mimg(P, a.z - b.z, 2));
   double3 d = make_double3(a.x - b.x, a.y - b.y, a.z - b.z);
-  if (M == kImgCode && (e >> 26) != 0u) {  // only entries in wrapped cells (rare, mostly warp-uniform)
-    d.x += img_shift((e >> 26) & 3u, P.L[0]);
-    d.y += img_shift((e >> 28) & 3u, P.L[1]);
-    d.z += img_shift(e >> 30, P.L[2]);
+  if (M == kImgCode && (e >> kIdxBits) != 0u) {  // only entries in wrapped cells (rare, mostly warp-uniform)
+    const uint32_t c = e >> kIdxBits;
+    d.x += img_shift(c % 3u, P.L[0]);
+    d.y += img_shift((c / 3u) % 3u, P.L[1]);
+    d.z += img_shift(c / 9u, P.L[2]);
   }
   return d;
 }

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ Dev
           iz = qz < 0 ? 1u : 2u;
           qz = (qz + nz) % nz;
         }
-        const uint32_t tag = code ? ((ix << 26) | (iy << 28) | (iz << 30)) : 0u;
+        const uint32_t tag = code ? img_tag(ix, iy, iz) : 0u;
         const int64_t cj = (qx * ny + qy) * nz + qz;
         const uint32_t j0 = cstart[cj], j1 = cend[cj];
         for (uint32_t jb = j0; jb < j1; jb += 32) {
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
           sz = qz < 0 ? -P.L[2] : P.L[2];
           qz = (qz + nz) % nz;
         }
-        const uint32_t tag = code ? ((ix << 26) | (iy << 28) | (iz << 30)) : 0u;
+        const uint32_t tag = code ? img_tag(ix, iy, iz) : 0u;
         const int64_t cj = (qx * ny + qy) * nz + qz;
         const bool home = ox == 0 && oy == 0 && oz == 0;
         const uint32_t j0 = cstart[cj], j1 = cend[cj];
