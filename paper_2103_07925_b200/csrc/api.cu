@@ -844,9 +844,15 @@ int sphg_step(sphg_ctx* h, int nsteps) {
     }
     SPHG_CUDA_CHECK(cudaEventRecord(c.step_ev[0], c.stream));
     for (int k = 0; k < nsteps; ++k) {
+      c.defer_final = k + 1 < nsteps && c.P.transitions == 0 && !c.timing;
       const int rc = one_step(h);
-      if (rc) return rc;
+      if (rc) {
+        c.defer_final = false;
+        if (c.final_pending) launch_final_kick_particles(c);  // leave a complete state behind
+        return rc;
+      }
     }
+    c.defer_final = false;
     SPHG_CUDA_CHECK(cudaEventRecord(c.step_ev[1], c.stream));
     const int rc = check_flags(h, true);
     float ms = 0.f;

@@ -111,6 +111,9 @@ struct Ctx {
   DevFlags* dflags = nullptr;   // device
   DevFlags* hflags = nullptr;   // pinned host mirror
   bool built = false;
+  // kick fusion inside one sphg_step(K) call: the particle final kick of step n is deferred into the
+  // kick-drift pass of step n+1 (never across API calls, with transitions, or with stage timing)
+  bool defer_final = false, final_pending = false;
   bool have_state = false;
   double t = 0.0;
   int64_t steps = 0, rebuilds = 0, n_melt = 0, n_solid = 0, launches = 0;
@@ -166,6 +169,7 @@ void launch_forces_rigid(Ctx& c);
 void launch_forces_diag(Ctx& c);  // diagnostic builds only (stage 12)
 void launch_bodies(Ctx& c);
 void launch_final_kick(Ctx& c);
+void launch_final_kick_particles(Ctx& c);
 void launch_mass(Ctx& c, const uint32_t* body_mask);
 void gather_by_gid(Ctx& c);          // cur[k] <- alt[gid[k]] for every field but gid/R4
 bool displacement_exceeds(Ctx& c);   // max |r - r_ref| > half skin (syncs)

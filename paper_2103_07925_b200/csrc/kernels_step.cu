@@ -65,6 +65,9 @@ __global__ void k_body_kick(const __grid_constant__ DevParams P, sphg_body* __re
 
 // fluid: u^{n+1/2} = u + dt/2 a; u~ = u^{n+1/2} + dt/2 a_bg; r += dt u~ (wrapped).
 // rigid: r_r = r_k + R(q) chi, u_r = u_k + w x r_rk.  Verlet displacement + u_max.
+// kFinal: the previous step's final fluid kick (u^n = u^{n-1/2} + dt/2 a^n, k_final_kick) is folded
+// in, with the same two roundings as the separate kernels, so the fused pass is bit-identical.
+template <bool kFinal>
 __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevParams P, Particles D,
                                                      const sphg_body* __restrict__ B, size_t n,
                                                      DevFlags* __restrict__ fl) {
@@ -76,8 +79,15 @@ __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevP
     double3 pn;
     bool moved = true;
     if (kind == SPHG_FLUID) {
-      const double4 v = D.V4.p[k];
       const double4 a = D.A4.p[k];
+      double3 v;
+      if (kFinal) {
+        const double3 uprev = ldpos(&D.G1.p[k]);
+        v = make_double3(axpy_rn(uprev.x, P.hdt, a.x), axpy_rn(uprev.y, P.hdt, a.y), axpy_rn(uprev.z, P.hdt, a.z));
+        stpos(&D.V4.p[k], v);
+      } else {
+        v = ldpos(&D.V4.p[k]);
+      }
       const double3 uh = make_double3(axpy_rn(v.x, P.hdt, a.x), axpy_rn(v.y, P.hdt, a.y), axpy_rn(v.z, P.hdt, a.z));
       double3 ua = uh;
       if (P.tvf) {
@@ -565,7 +575,11 @@ void launch_body_kick(Ctx& c) {
 
 void launch_kick_drift(Ctx& c) {
   if (c.n == 0) return;
-  k_kick_drift<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.n, c.dflags);
+  if (c.final_pending)  // the previous step deferred its particle final kick into this pass
+    k_kick_drift<true><<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.n, c.dflags);
+  else
+    k_kick_drift<false><<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.n, c.dflags);
+  c.final_pending = false;
   c.launches++;
 }
 
@@ -579,8 +593,20 @@ void launch_bodies(Ctx& c) {
 void launch_final_kick(Ctx& c) {
   if (c.n == 0) return;
   if (c.nb) k_body_final<<<grid_for(c.nb, 128), 128, 0, c.stream>>>(c.P, c.bodies.p, c.nb);
+  if (c.defer_final) {  // next step's kick-drift applies it (fluid); rigid end velocities are overwritten there
+    c.final_pending = true;
+    c.launches += c.nb ? 1 : 0;
+    return;
+  }
   k_final_kick<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.n);
   c.launches += c.nb ? 2 : 1;
+}
+
+void launch_final_kick_particles(Ctx& c) {  // the deferred particle part alone
+  if (c.n == 0) return;
+  k_final_kick<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.n);
+  c.final_pending = false;
+  c.launches++;
 }
 
 void launch_mass(Ctx& c, const uint32_t* mask) {
