@@ -368,10 +368,15 @@ int one_step(sphg_ctx* h) {
   if (rc) return rc;
   if (!c.built || c.max_disp > c.P.half_skin) timed(c, SPHG_STAGE_REBUILD, launch_rebuild);
   timed(c, SPHG_STAGE_DENSITY, launch_density);
-  if (c.P.thermal) timed(c, SPHG_STAGE_HEAT, launch_heat);
+  // fold fluid conduction into the forces pass (same terms, same order; heat does not feed the
+  // extrapolation or the forces, so moving it after them changes nothing)
+  c.fuse_heat = c.P.thermal && !c.timing;
+  if (c.P.thermal) timed(c, SPHG_STAGE_HEAT, c.fuse_heat ? launch_heat_begin : launch_heat);
   if (c.P.diffusion) timed(c, SPHG_STAGE_HEAT, launch_diffusion);
   timed(c, SPHG_STAGE_EXTRAPOLATE, launch_extrapolate);
   timed_forces(c);
+  if (c.fuse_heat) launch_heat_end(c);
+  c.fuse_heat = false;
   timed(c, SPHG_STAGE_BODIES, launch_bodies);
   timed(c, SPHG_STAGE_FINAL_KICK, launch_final_kick);
   h->mid_step = false;

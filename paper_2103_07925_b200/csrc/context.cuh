@@ -114,6 +114,8 @@ struct Ctx {
   // kick fusion inside one sphg_step(K) call: the particle final kick of step n is deferred into the
   // kick-drift pass of step n+1 (never across API calls, with transitions, or with stage timing)
   bool defer_final = false, final_pending = false;
+  // conduction of fluid particles folded into k_forces_fluid inside sphg_step (not for stage calls)
+  bool fuse_heat = false;
   bool have_state = false;
   double t = 0.0;
   int64_t steps = 0, rebuilds = 0, n_melt = 0, n_solid = 0, launches = 0;
@@ -161,6 +163,8 @@ void launch_body_kick(Ctx& c);
 void launch_kick_drift(Ctx& c);
 void launch_density(Ctx& c);
 void launch_heat(Ctx& c);
+void launch_heat_begin(Ctx& c);
+void launch_heat_end(Ctx& c);
 void launch_diffusion(Ctx& c);
 void launch_extrapolate(Ctx& c);
 void launch_forces(Ctx& c);

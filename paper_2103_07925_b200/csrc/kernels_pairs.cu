@@ -399,10 +399,17 @@ __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, 
 //   acc += -p~ w d + eta~ w (u_i - u_j) + w (rho_j/2) (du_j . d) u_j,   bg += w d.
 // The i-side TVF term (1/2) A_i gradW summed over j equals (rho_i/2) u_i (du_i . bg): it is applied
 // once per particle from bg (k_forces_fluid), not per pair.
-template <int M, bool kTvf, bool kSingleEta>
+// conduction folded into the fluid forces pass (one row walk; see launch_heat_begin): T_i, kappa_i
+// of the fluid particle and the running sum of k_heat
+struct HeatSide {
+  double T, kappa, s;
+};
+
+template <int M, bool kTvf, bool kSingleEta, bool kHeat = false>
 __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
                                            uint32_t e, double4 h0, double4 h1, double4 h2, double3& acc,
-                                           double3& bg, bool& coincident) {
+                                           double3& bg, bool& coincident, HeatSide* heat = nullptr,
+                                           double2 hj = double2{0.0, 0.0}) {
   const double3 d = pair_delta<M>(P, pi, ld3(h0), e);
   const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
   if (r2 > P.rc2) return;
@@ -412,6 +419,19 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
   }
   double rinv;
   const double dW = P.sig_h * shape_deriv_q(sqrt_and_rinv(r2, rinv) * P.inv_h);
+  if (kHeat && hj.y != 0.0) {  // same term, same order as k_heat (non-Dirichlet walls: V_heat = 0)
+    double kt;
+    bool conduct = true;
+    if (P.single_kappa) {
+      kt = 2.0 * heat->kappa;
+    } else {
+      const double kb = P.mat[mat_of(__ldg(&D.kmd.p[nb_index<M>(e)]))].kappa;
+      const double ks = heat->kappa + kb;
+      conduct = ks != 0.0;
+      kt = conduct ? 4.0 * heat->kappa * kb / ks : 0.0;
+    }
+    if (conduct) heat->s += hj.y * kt * ((heat->T - hj.x) * rinv) * dW;
+  }
   const double w = (I.V2 + h0.w) * (dW * rinv);
   bg.x = fma(w, d.x, bg.x);
   bg.y = fma(w, d.y, bg.y);
@@ -441,25 +461,28 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
 
 // the fluid particle's row (contiguous, fluid then non-fluid), row entries prefetched one
 // iteration ahead (rows stream from HBM), all three 32-byte neighbour records requested together
-template <int G, int M, bool kTvf, bool kSingleEta>
+template <int G, int M, bool kTvf, bool kSingleEta, bool kHeat = false>
 __device__ __forceinline__ void fluid_row(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
                                           const uint32_t* base, int n, int lane, double3& acc, double3& bg,
-                                          bool& coincident) {
+                                          bool& coincident, HeatSide* heat = nullptr) {
   int k = lane;
   uint32_t e = k < n ? __ldg(base + k) : 0u;
   for (; k < n; k += G) {
     const uint32_t en = k + G < n ? __ldg(base + k + G) : 0u;
     const uint32_t j = nb_index<M>(e);
     const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
-    fluid_pair<M, kTvf, kSingleEta>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident);
+    double2 hj = double2{0.0, 0.0};
+    if (kHeat) hj = __ldg(&D.H2.p[j]);
+    fluid_pair<M, kTvf, kSingleEta, kHeat>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident, heat, hj);
     e = en;
   }
 }
 
-template <int G, int M, bool kTvf, bool kSingleEta>
+template <int G, int M, bool kTvf, bool kSingleEta, bool kHeat = false>
 __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                           const uint32_t* __restrict__ list, size_t nlist,
-                                                          DevFlags* __restrict__ fl) {
+                                                          DevFlags* __restrict__ fl,
+                                                          double2* __restrict__ Hout = nullptr) {
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
@@ -468,8 +491,15 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
   double3 acc = make_double3(0, 0, 0), bg = make_double3(0, 0, 0);
   bool coincident = false;
   uint32_t kmd = 0;
+  HeatSide heat{0.0, 0.0, 0.0};
+  double2 hi = double2{0.0, 0.0};
   if (active) {
     kmd = D.kmd.p[i];
+    if (kHeat) {
+      hi = D.H2.p[i];
+      heat.T = hi.x;
+      heat.kappa = P.mat[mat_of(kmd)].kappa;
+    }
     const double4 g0 = ldg4(&D.G0.p[i]), g1 = ldg4(&D.G1.p[i]), g2 = ldg4(&D.G2.p[i]);
     PairSide I;
     I.u = ld3(g1);
@@ -483,8 +513,9 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
     const Row R = row_of(L, i);
     // one pass over the whole contiguous row: wall/rigid records carry du = 0 (A_w = 0) and, with
     // several viscosities, fluid_pair looks up eta_j by kind (eta_w := eta_i)
-    fluid_row<G, M, kTvf, kSingleEta>(P, D, I, pi, R.f, R.n, lane, acc, bg, coincident);
+    fluid_row<G, M, kTvf, kSingleEta, kHeat>(P, D, I, pi, R.f, R.n, lane, acc, bg, coincident, &heat);
   }
+  if (kHeat) heat.s = gsum<G>(heat.s);
   acc.x = gsum<G>(acc.x);
   acc.y = gsum<G>(acc.y);
   acc.z = gsum<G>(acc.z);
@@ -509,6 +540,12 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
   D.A4.p[i] = make_double4(acc.x * im + Mt.g[0], acc.y * im + Mt.g[1], acc.z * im + Mt.g[2], 0.0);
   const double f = kTvf ? -Mt.pb * im : 0.0;
   D.B4.p[i] = make_double4(f * bg.x, f * bg.y, f * bg.z, 0.0);
+  if (kHeat) {  // the k_heat epilogue for a fluid particle (rho_a = rho_i)
+    double rate = 0.0;
+    if (Mt.cp > 0.0) rate = heat.s / (D.G1.p[i].w * Mt.cp);
+    Hout[i] = make_double2(hi.x + P.dt * rate, hi.y);
+    D.dTdt.p[i] = rate;
+  }
 }
 
 #ifdef SPHG_DIAG_LOADS_ONLY
@@ -767,20 +804,36 @@ void launch_density(Ctx& c) {
   c.launches++;
 }
 
-void launch_heat(Ctx& c) {
+// Heat in two halves so one_step can fold the fluid part into the forces pass (c.fuse_heat):
+// begin = Dirichlet values at t^{n+1} + rigid conduction (+ fluid conduction when not fused);
+// end = walls / ghosts keep T, swap the double buffer.
+void launch_heat_begin(Ctx& c) {
   if (c.n == 0) return;
   const double t_new = c.t + c.P.dt;
   constexpr int G = kGOther;
   k_dirichlet<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new);
-  if (c.nf)
+  if (c.nf && !c.fuse_heat)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.H2new.p, c.dflags)));
   if (c.nrigid)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.H2new.p, c.dflags)));
+  c.launches += 3;
+}
+
+void launch_heat_end(Ctx& c) {
+  if (c.n == 0) return;
   k_copy_boundary_T<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.cur, c.n, c.H2new.p);
   std::swap(c.cur.H2, c.H2new);
-  c.launches += 4;
+  c.launches++;
+}
+
+void launch_heat(Ctx& c) {
+  const bool f = c.fuse_heat;
+  c.fuse_heat = false;
+  launch_heat_begin(c);
+  launch_heat_end(c);
+  c.fuse_heat = f;
 }
 
 void launch_diffusion(Ctx& c) {
@@ -813,6 +866,13 @@ void launch_extrapolate(Ctx& c) {
 
 template <bool kTvf, bool kSingleEta>
 static void launch_forces_fluid_t(Ctx& c) {
+  if (c.nf && c.fuse_heat) {  // conduction of the fluid particles in the same row walk (G = 4)
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<4, M, kTvf, kSingleEta, true>
+                                     <<<blocks_for<4>(c.nf), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, c.H2new.p)));
+    c.launches++;
+    return;
+  }
   if (c.nf)
     SPHG_G_DISPATCH(c.group_forces,
                     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta>

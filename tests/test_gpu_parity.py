@@ -533,3 +533,21 @@ def test_fused_kick_is_bit_identical():
     for f in ("pos", "vel", "vel_adv", "acc", "acc_bg", "density", "pressure", "force"):
         assert np.array_equal(getattr(ga, f), getattr(gb, f)), f
     assert np.array_equal(ba, bb)
+
+
+def test_fused_heat_is_bit_identical():
+    """sphg_step folds fluid conduction into the forces pass; with stage timing on it runs the
+    separate heat kernel.  Both give bit-identical temperatures and rates (C2 with melting)."""
+    sc = CASES["c2_melt"]()
+    a, b = sim_factory(sc.params), sim_factory(sc.params)
+    for e in (a, b):
+        e.upload(sc.store, sc.bodies)
+        e.initialize()
+    b.set_timing(True)
+    a.step(3)
+    b.step(3)
+    ga, _ = a.download()
+    gb, _ = b.download()
+    for f in ("temperature", "dT_dt", "pos", "vel", "acc", "density"):
+        assert np.array_equal(getattr(ga, f), getattr(gb, f)), f
+    assert np.array_equal(ga.kind, gb.kind)
