@@ -280,7 +280,7 @@ void timed_forces(Ctx& c) {  // stage 4 = 10 (fluid kernel) + 11 (rigid kernel)
   timed(c, 10, launch_forces_fluid);
   timed(c, 11, launch_forces_rigid);
 #ifdef SPHG_DIAG_LOADS_ONLY
-  timed(c, 12, launch_forces_diag);
+  launch_forces_diag(c);  // times its own variants into stage_ms[12..15]
 #endif
   c.stage_ms[SPHG_STAGE_FORCES] += (c.stage_ms[10] - before10) + (c.stage_ms[11] - before11);
 }

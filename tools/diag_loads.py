@@ -15,4 +15,10 @@ sim.step(5)
 b = sim.stats()
 f = (b.stage_ms[10] - a.stage_ms[10]) / 5
 d = (b.stage_ms[12] - a.stage_ms[12]) / 5
-print(f"nside {n}: forces_fluid {f:.3f} ms, loads-only twin {d:.3f} ms, ratio {d / f:.2f}")
+v = [(b.stage_ms[k] - a.stage_ms[k]) / 5 for k in (13, 14, 15)]
+if os.environ.get("SPHG_DIAG_MODE", "").startswith("G"):
+    print(f"nside {n}: forces_fluid {f:.3f} ms; loads-only twin G=4 {d:.3f}, G=2 {v[0]:.3f}, G=8 {v[1]:.3f}, "
+          f"G=16 {v[2]:.3f} ms")
+else:
+    print(f"nside {n}: forces_fluid {f:.3f} ms, loads-only twin (3 SoA records) {d:.3f} ms, "
+          f"3 loads from one 128 B AoS record {v[0]:.3f} ms, G0 record only {v[1]:.3f} ms")
