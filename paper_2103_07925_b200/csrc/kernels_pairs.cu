@@ -2,9 +2,12 @@
 //
 //   k_density       density_summation + eos_pressure
 //   k_heat          conduction_rhs + explicit T update
+//   k_diffusion     diffusion_rhs + explicit C update
 //   k_extrapolate   extrapolate_wall_quantities                 (Adami 2012)
 //   k_forces_fluid  momentum_rhs with transport velocity
+//                   (+ the fluid conduction sums inside sphg_step, kHeat)
 //   k_forces_rigid  coupling_force_on_rigid + contact_force
+//   k_count_pairs   Verlet candidates / pairs within r_c (bench flop model)
 //
 // Parallelisation: a group of G consecutive lanes owns one particle i and
 // strides over its Verlet row (nbr[i*cap + k]); the rows list neighbours in
@@ -12,7 +15,9 @@
 // few cache lines per warp load instead of one line per lane.  Partial sums
 // are combined with warp shuffles (gsum); lane 0 of the group writes.  Every
 // sum is a gather (no fp64 atomics), hence deterministic.  Groups iterate over
-// compact per-kind index lists (fluid / non-fluid / rigid) built at rebuild.
+// compact per-kind index lists (fluid / non-fluid in brick order, rigid body-major) built at
+// rebuild.  These kernels are gather-bound, not FP64-bound (a loads-only twin of
+// k_forces_fluid takes 97 % of its time).
 #include <cmath>
 #include <cstring>
 

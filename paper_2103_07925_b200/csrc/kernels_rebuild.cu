@@ -8,6 +8,10 @@
 // same on any GPU count and identical to the oracle's (bit-exact test).
 // Candidates: j != i, not both boundary, r^2 <= (r_c + 0.1 h)^2 evaluated as
 // (dx*dx + dy*dy) + dz*dz in round-to-nearest without contraction [P2].
+// Lists: k_build_nlist_cells (warp per home cell, cells visited brick by brick, fp32 staging with
+// an exact fp64 guard band) or k_build_nlist (warp per particle, fallback for dense cells); rows
+// are kind-partitioned [fluid | non-fluid] and, for rigid particles, the non-fluid part starts
+// with the contact candidates (k_contact_order).  Kind lists are emitted in brick order.
 #include <algorithm>
 
 #include "context.cuh"

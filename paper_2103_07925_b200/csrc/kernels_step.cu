@@ -6,9 +6,11 @@
 //   k_mass                       reduce_mass_quantities
 //   k_body_final / k_final_kick  final half kick + slave velocities
 //
-// All pair kernels are gather-only (one thread per particle, Verlet ELL list,
-// no fp64 atomics), so every sum is deterministic.  The pair arithmetic is
-// FMA-contracted fp64; see DESIGN.md §4 for the per-kernel roofline.
+// Also here: the decomposition hooks (halo pack/unpack, per-body partials and totals), the
+// warm-upload gather by gid and the Verlet displacement check.  Every body sum is a fixed-order
+// compensated reduction (no fp64 atomics), so results are deterministic; the kick / drift
+// arithmetic uses round-to-nearest intrinsics to match the oracle bit for bit [P17].  Inside one
+// sphg_step(K) call the particle final kick is folded into the next kick-drift (k_kick_drift<true>).
 #include <cmath>
 #include <cstring>
 
