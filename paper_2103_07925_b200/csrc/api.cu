@@ -7,7 +7,8 @@
 //   sphg_step       step(state, dt)
 //   sphg_run_stage  build_pairs / density_summation / conduction_rhs / extrapolate_wall_quantities /
 //                   momentum_rhs+coupling+contact / reduce_force_torque / transitions / reduce_mass_quantities
-//   sphg_download   device SoA -> ParticleStore<3>
+//   sphg_download   device SoA -> ParticleStore<3> (device-side pack into gid order, then DMA)
+//   sphg_set_wall_motion / sphg_shepard_grid / sphg_halo_* / sphg_body_*: see include/sphg.h
 #include <algorithm>
 #include <cmath>
 #include <cstdio>

@@ -5,13 +5,15 @@
 //   G0 = (x, y, z, V^2)        interaction volume squared (fluid: (m/rho)^2, wall/rigid: V_w^2)
 //   G1 = (u, rho)              interaction velocity/density (fluid: u^{n+1/2}, rho; wall/rigid: u~_w, rho_w)
 //   G2 = (du, p)               du = u_adv - u (TVF A term; 0 for wall/rigid), pressure (wall/rigid: p_w)
-//   V4 = (vel, mass)           true velocity (fluid u^n between steps, rigid u_r, boundary 0)
+//   V4 = (vel, mass)           true velocity (fluid u^n between steps, rigid u_r, boundary: wall
+//                              group velocity or 0)
 //   A4 = (acc, -)  B4 = (acc_bg, -)  F4 = (f_r, -)  X4 = (chi, -)  R4 = (pos at last rebuild, -)
 //   H2 = (T, V_heat)           temperature and the conduction volume V_b (0 for non-Dirichlet walls)
-//   kmd (kind|mat|dirichlet), group, gid : uint32
-// Verlet candidates are row-major: nbr[i * cap + k] for k < cnt[i]; entries pack
-// the periodic image code (common.cuh kImgCode).  Per-kind index lists (fluid,
-// non-fluid, rigid body-major) drive the pair kernels.
+//   C2 = (C, V_diff), dCdt     concentration (only with params.diffusion)
+//   kmd (kind|mat|Dirichlet-T|ghost|Dirichlet-C), group, gid : uint32
+// Verlet candidates are row-major: nbr[i * cap + k] for k < cnt[i] (cnt = nf | no << 16,
+// [fluid | non-fluid]); entries pack the periodic image code (common.cuh kImgCode).  Per-kind
+// index lists (fluid / non-fluid in brick order, rigid body-major) drive the pair kernels.
 #pragma once
 
 #include <string>
