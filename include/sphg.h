@@ -168,6 +168,8 @@ typedef struct {
                                  10 = fluid forces kernel, 11 = rigid forces kernel (both inside 4) */
   int64_t kernel_launches;
   double last_step_call_ms;   /* device time of the last sphg_step call (CUDA events on the stream) */
+  int64_t graph_captures;     /* CUDA graphs captured for the per-step launch chains (SPHG_GRAPHS=0: none) */
+  int64_t graph_replays;      /* chain launches served by an already captured graph */
 } sphg_stats_t;
 
 typedef struct sphg_ctx sphg_ctx;

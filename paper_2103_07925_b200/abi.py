@@ -102,7 +102,8 @@ class Stats(C.Structure):
                 ("max_neighbours", C.c_int32), ("cells", C.c_int32 * 3), ("pad", C.c_int32),
                 ("time", C.c_double), ("max_displacement", C.c_double), ("u_max", C.c_double),
                 ("stage_ms", C.c_double * 16), ("kernel_launches", C.c_int64),
-                ("last_step_call_ms", C.c_double)]
+                ("last_step_call_ms", C.c_double), ("graph_captures", C.c_int64),
+                ("graph_replays", C.c_int64)]
 
 
 # void fn(int32 group, double t, double vel[3], double acc[3], void* user)  (sphg_set_wall_motion)

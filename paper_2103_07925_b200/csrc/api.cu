@@ -240,9 +240,9 @@ void ensure_bodies(Ctx& c, size_t need) {
 }
 
 // reads the flag block; returns SPHG_OK or a runtime error with a one-line message
-int check_flags(sphg_ctx* h, bool sync) {
+int check_flags(sphg_ctx* h, bool sync, bool copy = true) {  // copy=false: the readback is already enqueued
   Ctx& c = h->c;
-  SPHG_CUDA_CHECK(cudaMemcpyAsync(c.hflags, c.dflags, sizeof(DevFlags), cudaMemcpyDeviceToHost, c.stream));
+  if (copy) SPHG_CUDA_CHECK(cudaMemcpyAsync(c.hflags, c.dflags, sizeof(DevFlags), cudaMemcpyDeviceToHost, c.stream));
   if (sync) SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
   SPHG_CUDA_CHECK(cudaGetLastError());
   const DevFlags& f = *c.hflags;
@@ -356,30 +356,155 @@ int do_stage(sphg_ctx* h, int stage) {
   return check_flags(h, true);
 }
 
-int one_step(sphg_ctx* h) {
-  Ctx& c = h->c;
-  if (c.nghost)
-    return fail(h, SPHG_ERR_RUNTIME,
-                "ghost particles present: drive multi-rank steps through the decomposition layer (parallel.py)");
+// ------------------------------------------------------------------ CUDA graphs
+// The two launch chains of a step — (A) flag reset + kicks + drift + flag readback, (B) density ..
+// final kick — are captured once per distinct launch configuration and replayed: on a 32k-particle
+// store the step is launch-latency bound (13-16 launches of a few microseconds each).  The key holds
+// every pointer, count and parameter a launch in the chain reads (Particles by value, the kind
+// lists, the Verlet rows, the body table, DevParams), so a configuration seen before — e.g. the
+// alternating heat buffers, or the cur/alt buffer sets after a reorder — replays its own graph and
+// a new one is captured.  Host-side effects of the chain (buffer swaps, deferred final kick, launch
+// count) are recorded at capture and re-applied on replay.  Not used with stage timing, moving
+// walls (their launch arguments change every step) or ghosts.
+template <class T>
+void key_put(std::vector<unsigned char>& k, const T& v) {
+  const unsigned char* b = reinterpret_cast<const unsigned char*>(&v);
+  k.insert(k.end(), b, b + sizeof(T));
+}
+
+std::vector<unsigned char> graph_key(const Ctx& c, int chain) {
+  std::vector<unsigned char> k;
+  k.reserve(2048);
+  key_put(k, chain);
+  key_put(k, c.cur); key_put(k, c.alt); key_put(k, c.H2new); key_put(k, c.C2new);
+  key_put(k, c.bodies.p); key_put(k, c.nbr.p); key_put(k, c.cnt.p); key_put(k, c.cap);
+  key_put(k, c.fidx.p); key_put(k, c.widx.p); key_put(k, c.ridx.p); key_put(k, c.body_start.p);
+  key_put(k, c.ncon.p);
+  key_put(k, c.n); key_put(k, c.nb); key_put(k, c.nf); key_put(k, c.nw); key_put(k, c.nrigid);
+  key_put(k, c.group_density); key_put(k, c.group_forces);
+  key_put(k, c.defer_final); key_put(k, c.fuse_heat); key_put(k, c.final_pending);
+  key_put(k, c.P);
+  return k;
+}
+
+bool graphs_allowed(const Ctx& c) {
+#ifdef SPHG_DIAG_LOADS_ONLY
+  return false;  // the diagnostic variants synchronise inside the forces stage
+#else
+  return c.use_graphs && !c.timing && c.P.n_walls == 0 && c.nghost == 0;
+#endif
+}
+
+constexpr size_t kMaxGraphs = 8;
+
+void destroy_graphs(Ctx& c) {
+  for (auto& e : c.graphs)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+  c.graphs.clear();
+}
+
+void run_graph(Ctx& c, int chain, void (*body)(Ctx&)) {
+  std::vector<unsigned char> key = graph_key(c, chain);
+  for (auto& e : c.graphs) {
+    if (e.key != key) continue;
+    SPHG_CUDA_CHECK(cudaGraphLaunch(e.exec, c.stream));
+    c.cur = e.cur_after;
+    c.H2new = e.H2new_after;
+    c.C2new = e.C2new_after;
+    c.final_pending = e.final_pending_after;
+    c.launches += e.launches;
+    e.used = ++c.graph_clock;
+    c.graph_replays++;
+    return;
+  }
+  const int64_t l0 = c.launches;
+  SPHG_CUDA_CHECK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  c.capturing = true;
+  try {
+    body(c);
+  } catch (...) {
+    c.capturing = false;
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(c.stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  c.capturing = false;
+  cudaGraph_t g = nullptr;
+  SPHG_CUDA_CHECK(cudaStreamEndCapture(c.stream, &g));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  SPHG_CUDA_CHECK(ie);
+  SPHG_CUDA_CHECK(cudaGraphLaunch(exec, c.stream));
+  if (c.graphs.size() >= kMaxGraphs) {  // evict the least recently used
+    auto lru = std::min_element(c.graphs.begin(), c.graphs.end(),
+                                [](const Ctx::GraphEntry& a, const Ctx::GraphEntry& b) { return a.used < b.used; });
+    cudaGraphExecDestroy(lru->exec);
+    c.graphs.erase(lru);
+  }
+  Ctx::GraphEntry e;
+  e.key = std::move(key);
+  e.exec = exec;
+  e.launches = c.launches - l0;
+  e.cur_after = c.cur;
+  e.H2new_after = c.H2new;
+  e.C2new_after = c.C2new;
+  e.final_pending_after = c.final_pending;
+  e.used = ++c.graph_clock;
+  c.graphs.push_back(std::move(e));
+  c.graph_captures++;
+}
+
+void chain_kick(Ctx& c) {  // (A): everything up to the per-step flag readback
   reset_step_flags(c);
   timed(c, SPHG_STAGE_KICK_DRIFT, kick_all);
-  c.t += c.P.dt;
-  h->mid_step = true;
-  int rc = check_flags(h, true);  // one 48-byte readback per step: Verlet trigger + escape check
-  if (rc) return rc;
-  if (!c.built || c.max_disp > c.P.half_skin) timed(c, SPHG_STAGE_REBUILD, launch_rebuild);  // SPEC:212
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(c.hflags, c.dflags, sizeof(DevFlags), cudaMemcpyDeviceToHost, c.stream));
+}
+
+void chain_forces(Ctx& c) {  // (B): density .. final kick
+  if (c.capturing && (c.P.thermal || c.P.diffusion))
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(c.dtime, c.htime, sizeof(double), cudaMemcpyHostToDevice, c.stream));
   timed(c, SPHG_STAGE_DENSITY, launch_density);
-  // fold fluid conduction into the forces pass (same terms, same order; heat does not feed the
-  // extrapolation or the forces, so moving it after them changes nothing)
-  c.fuse_heat = c.P.thermal && !c.timing;
   if (c.P.thermal) timed(c, SPHG_STAGE_HEAT, c.fuse_heat ? launch_heat_begin : launch_heat);
   if (c.P.diffusion) timed(c, SPHG_STAGE_HEAT, launch_diffusion);
   timed(c, SPHG_STAGE_EXTRAPOLATE, launch_extrapolate);
   timed_forces(c);
   if (c.fuse_heat) launch_heat_end(c);
-  c.fuse_heat = false;
   timed(c, SPHG_STAGE_BODIES, launch_bodies);
   timed(c, SPHG_STAGE_FINAL_KICK, launch_final_kick);
+}
+
+int one_step(sphg_ctx* h) {
+  Ctx& c = h->c;
+  if (c.nghost)
+    return fail(h, SPHG_ERR_RUNTIME,
+                "ghost particles present: drive multi-rank steps through the decomposition layer (parallel.py)");
+  const bool graphs = graphs_allowed(c);
+  if (graphs) {
+    if (!c.dtime) {
+      SPHG_CUDA_CHECK(cudaMalloc(&c.dtime, sizeof(double)));
+      SPHG_CUDA_CHECK(cudaMallocHost(&c.htime, sizeof(double)));
+    }
+    run_graph(c, 0, chain_kick);
+  } else {
+    chain_kick(c);
+  }
+  c.t += c.P.dt;
+  h->mid_step = true;
+  int rc = check_flags(h, true, false);  // one 48-byte readback per step: Verlet trigger + escape check
+  if (rc) return rc;
+  if (!c.built || c.max_disp > c.P.half_skin) timed(c, SPHG_STAGE_REBUILD, launch_rebuild);  // SPEC:212
+  // fold fluid conduction into the forces pass (same terms, same order; heat does not feed the
+  // extrapolation or the forces, so moving it after them changes nothing)
+  c.fuse_heat = c.P.thermal && !c.timing;
+  if (graphs) {
+    *c.htime = c.t + c.P.dt;  // read by the memcpy node; the previous replay finished (flag sync above)
+    run_graph(c, 1, chain_forces);
+  } else {
+    chain_forces(c);
+  }
+  c.fuse_heat = false;
   h->mid_step = false;
   if (c.P.transitions != 0) {
     rc = launch_transitions(c);
@@ -694,6 +819,7 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
   if (const char* e = std::getenv("SPHG_GROUP_DENSITY")) c.group_density = std::atoi(e);
   if (const char* e = std::getenv("SPHG_GROUP_FORCES")) c.group_forces = std::atoi(e);
   if (const char* e = std::getenv("SPHG_CELL_BUILD")) c.cell_build = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SPHG_GRAPHS")) c.use_graphs = std::atoi(e) != 0;
   try {
     SPHG_CUDA_CHECK(cudaSetDevice(device));
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
@@ -968,6 +1094,8 @@ int sphg_stats(sphg_ctx* h, sphg_stats_t* s) {
     for (int k = 0; k < 16; ++k) s->stage_ms[k] = c.stage_ms[k];
     s->kernel_launches = c.launches;
     s->last_step_call_ms = c.last_step_ms;
+    s->graph_captures = c.graph_captures;
+    s->graph_replays = c.graph_replays;
     if (c.built && c.n) {
       std::vector<uint32_t> cnt(c.n);
       d2h(cnt.data(), c.cnt.p, c.n, c.stream);
@@ -1158,6 +1286,9 @@ void sphg_destroy(sphg_ctx* h) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
+  destroy_graphs(c);
+  if (c.dtime) cudaFree(c.dtime);
+  if (c.htime) cudaFreeHost(c.htime);
   c.cur.free(); c.alt.free(); c.H2new.free(); c.C2new.free(); c.bodies.free();
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
   c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();

@@ -144,6 +144,25 @@ struct Ctx {
   DBuf<double> body_buf;
   DBuf<double> state_buf;  // upload_state staging (device)
   size_t last_h2d_bytes = 0, last_d2h_bytes = 0;
+  // CUDA graphs of the two per-step launch chains (api.cu run_graph): keyed by every pointer, count
+  // and parameter the chain's launches read, so a rebuild / transition / upload selects (or captures)
+  // another graph instead of replaying stale arguments.  The Dirichlet schedules read t^{n+1} from
+  // dtime (a memcpy node from the pinned htime) when captured.
+  struct GraphEntry {
+    std::vector<unsigned char> key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+    Particles cur_after;
+    DBuf<double2> H2new_after, C2new_after;
+    bool final_pending_after = false;
+    uint64_t used = 0;
+  };
+  std::vector<GraphEntry> graphs;
+  uint64_t graph_clock = 0;
+  int64_t graph_captures = 0, graph_replays = 0;
+  bool use_graphs = true, capturing = false;
+  double* dtime = nullptr;  // device t^{n+1} for captured Dirichlet kernels
+  double* htime = nullptr;  // pinned host source of dtime
 };
 
 // ------------------------------------------------------------ launchers

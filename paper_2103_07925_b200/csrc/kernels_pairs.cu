@@ -789,9 +789,12 @@ __device__ __forceinline__ double sched_value(const DevSchedule& s, double t) { 
   return s.value[s.n - 1];
 }
 
-__global__ void k_dirichlet(const __grid_constant__ DevParams P, Particles D, size_t n, double t_new) {
+// t_dev (graph replay): t^{n+1} from device memory, refreshed by a memcpy node every replay
+__global__ void k_dirichlet(const __grid_constant__ DevParams P, Particles D, size_t n, double t_new,
+                            const double* __restrict__ t_dev) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (t_dev) t_new = *t_dev;
   const uint32_t kmd = D.kmd.p[i];
   if (kind_of(kmd) != SPHG_BOUNDARY) return;
   const uint32_t gr = dir_of(kmd);
@@ -799,9 +802,11 @@ __global__ void k_dirichlet(const __grid_constant__ DevParams P, Particles D, si
   reinterpret_cast<double*>(&D.H2.p[i])[0] = sched_value(P.sched[gr], t_new);
 }
 
-__global__ void k_dirichlet_c(const __grid_constant__ DevParams P, Particles D, size_t n, double t_new) {
+__global__ void k_dirichlet_c(const __grid_constant__ DevParams P, Particles D, size_t n, double t_new,
+                              const double* __restrict__ t_dev) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (t_dev) t_new = *t_dev;
   const uint32_t gr = dirc_of(D.kmd.p[i]);
   if (gr == SPHG_NO_DIRICHLET || (int)gr >= P.n_schedC || P.schedC[gr].n <= 0) return;
   reinterpret_cast<double*>(&D.C2.p[i])[0] = sched_value(P.schedC[gr], t_new);
@@ -864,7 +869,7 @@ void launch_heat_begin(Ctx& c) {
   if (c.n == 0) return;
   const double t_new = c.t + c.P.dt;
   constexpr int G = kGOther;
-  k_dirichlet<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new);
+  k_dirichlet<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new, c.capturing ? c.dtime : nullptr);
   if (c.nf && !c.fuse_heat)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.H2new.p, c.dflags)));
@@ -893,7 +898,7 @@ void launch_diffusion(Ctx& c) {
   if (c.n == 0) return;
   const double t_new = c.t + c.P.dt;
   constexpr int G = kGOther;
-  k_dirichlet_c<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new);
+  k_dirichlet_c<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new, c.capturing ? c.dtime : nullptr);
   if (c.nf)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_diffusion<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.C2new.p, c.dflags)));
