@@ -41,7 +41,7 @@ FLOPS_PER_PAIR_DENSITY = 17.0
 STEP_BYTES_PER_PARTICLE = 480.0
 
 
-DEFAULT_NSIDE = {"c5": 400, "c1": 32, "c2": 64, "c3": 128, "dissolve": 64}
+DEFAULT_NSIDE = {"c5": 400, "c1": 32, "c2": 64, "c3": 128, "c4": 200, "dissolve": 64}
 
 
 def make_scenario(args):
@@ -50,6 +50,9 @@ def make_scenario(args):
         return scenarios.config5(nside=args.nside, n_spheres=args.spheres)
     if args.config == "c1":
         return scenarios.config1(nside=args.nside)
+    if args.config == "c4":  # 400 x 200 x 200 (with walls) = 16M; --nside scales y and z (x = 2 nside)
+        return scenarios.config4(nx=2 * args.nside, ny=args.nside, nz=args.nside - 6,
+                                 n_grains=int(round(5000 * (args.nside / 200.0) ** 2)))
     return scenarios.by_name(args.config, nside=args.nside)
 
 
@@ -59,7 +62,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)  # C5: 100 steps (Verlet rebuilds included as they occur)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sph", choices=["sph", "reference"])
-    ap.add_argument("--config", default="c5", choices=["c5", "c1", "c2", "c3", "dissolve"],
+    ap.add_argument("--config", default="c5", choices=["c5", "c1", "c2", "c3", "c4", "dissolve"],
                     help="c5 = the headline workload (BASELINE metric); the others are secondary measurements")
     ap.add_argument("--nside", type=int, default=None, help="lattice side (default: the config's BASELINE size)")
     ap.add_argument("--spheres", type=int, default=20000)

@@ -93,6 +93,20 @@ typedef struct {
   int32_t diffusion;         /* solve the concentration diffusion equation */
   int32_t n_dirichlet_c;
   sphg_schedule dirichlet_C[SPHG_MAX_DIRICHLET]; /* config.hpp:95, indexed by dirichlet_C group */
+  /* Moving Gaussian surface heat flux (BASELINE configs[3], C4).  An extension: the reference has no
+   * heat sources, so this term is pinned here, not by the reference [P21]:
+   *   q(x, y, t) = 2 P / (pi r0^2) exp(-2 rho^2 / r0^2),  rho^2 = (x - c_x(t))^2 + (y - c_y(t))^2,
+   *   c(t) = hs_origin + hs_velocity t (wrapped, minimum image on periodic axes), q = 0 for rho > 4 r0,
+   * absorbed at t^{n+1} by every exposed non-boundary particle a of a material in hs_material_mask:
+   *   dT_a/dt += q(x_a, y_a) dx^2 / (m_a c_p,a)   (c_p,a > 0),
+   * where a is exposed unless a Verlet neighbour b of a mask material (any kind) with r_ab <= r_c
+   * lies above it: z_b - z_a > dx/2 and (x_b - x_a)^2 + (y_b - y_a)^2 < (3 dx/4)^2. */
+  int32_t heat_source;          /* 0 = none (requires thermal) */
+  uint32_t hs_material_mask;    /* bit m: material m absorbs / shadows */
+  double hs_power;              /* absorbed power P [W] */
+  double hs_radius;             /* 1/e^2 radius r0 [m] */
+  double hs_origin[3];          /* spot centre at t = 0 (z unused) */
+  double hs_velocity[3];        /* scan velocity (z unused) */
 } sphg_params;
 
 /* Host SoA views in gid order — the ParticleStore<3> layout (store.hpp:26-46).

@@ -210,6 +210,10 @@ std::vector<std::string> validate(const sphg_params& P) {
     if (P.transitions < 0 || P.transitions > 2) v.push_back("unknown transition mode");
     if (P.transitions == 2 && !P.diffusion) v.push_back("concentration transitions need the diffusion equation");
     if (P.default_fluid_mat < 0 || P.default_fluid_mat >= P.n_mat) v.push_back("default fluid material missing");
+    if (P.heat_source) {  // [P21]
+        if (!P.thermal) v.push_back("heat source needs the heat equation");
+        if (!(P.hs_radius > 0.0)) v.push_back("heat source radius must be positive");
+    }
     return v;
 }
 
@@ -331,8 +335,39 @@ double sched_value(const sphg_schedule& s, double t) {  // Schedule::value_at (c
     return sc.value_at(t);
 }
 
+// Moving Gaussian surface heat flux [P21] (BASELINE C4; not in the reference, which has no heat
+// sources: PAPER:118).  Source rate q(x_a, y_a, t) dx^2 / (m_a c_p,a) of particle a at
+// time t (sphg.h documents the exposure rule); 0 when a does not absorb.
+inline bool hs_absorbs(const Ctx& c, size_t i) {
+    return (c.P.hs_material_mask >> c.S.material[i]) & 1u;
+}
+double heat_source_rate(const Ctx& c, size_t a, double t) {
+    if (!c.P.heat_source || c.S.kind[a] == Kind::Boundary || !hs_absorbs(c, a)) return 0.0;
+    const sphfsi::Material& ma = c.mats[c.S.material[a]];
+    if (!(ma.heat_capacity > 0.0)) return 0.0;
+    double rho2 = 0.0;
+    for (int ax = 0; ax < 2; ++ax) {
+        double cx = c.P.hs_origin[ax] + c.P.hs_velocity[ax] * t;
+        cx = c.P.periodic[ax] ? c.P.lo[ax] + (cx - c.P.lo[ax]) - c.L[ax] * std::floor((cx - c.P.lo[ax]) / c.L[ax]) : cx;
+        const double d = mi(c, c.S.pos[a][ax] - cx, ax);
+        rho2 += d * d;
+    }
+    const double r0 = c.P.hs_radius;
+    if (rho2 > 16.0 * r0 * r0) return 0.0;  // truncated at 4 r0
+    const double rc2 = c.rc * c.rc, dz = 0.5 * c.P.dx, lat2 = 0.5625 * c.P.dx * c.P.dx;
+    for (uint32_t b : c.nl[a]) {  // shadowed by a mask particle above a (any kind)
+        if (!hs_absorbs(c, b)) continue;
+        const V3 d = mi3(c, c.S.pos[a], c.S.pos[b]);  // r_a - r_b
+        if (r2of(d) > rc2) continue;
+        if (-d[2] > dz && d[0] * d[0] + d[1] * d[1] < lat2) return 0.0;
+    }
+    const double q = 2.0 * c.P.hs_power / (M_PI * r0 * r0) * std::exp(-2.0 * rho2 / (r0 * r0));
+    return q * (c.P.dx * c.P.dx) / (c.S.mass[a] * ma.heat_capacity);
+}
+
 // apply_thermal_dirichlet at t^{n+1} [P9]; conduction_rhs (SPEC:398-406,
-// PAPER:399-405) with T^n, r^{n+1}, rho^{n+1}; T^{n+1} = T^n + dt rate.
+// PAPER:399-405) with T^n, r^{n+1}, rho^{n+1}; T^{n+1} = T^n + dt rate;
+// + the surface heat flux at t^{n+1} [P21].
 bool stage_heat(Ctx& c) {
     const size_t n = c.S.size();
     const double t_new = c.t + c.dt;
@@ -380,6 +415,11 @@ bool stage_heat(Ctx& c) {
             const double den = c.S.density[a] * ma.heat_capacity;
             rate = s / den;
             scale = sc / den;
+            if (c.P.heat_source) {
+                const double q = heat_source_rate(c, a, t_new);
+                rate += q;
+                scale += std::abs(q);
+            }
         }
         c.S.dT_dt[a] = rate;
         c.S.temperature[a] = Tn[a] + c.dt * rate;

@@ -65,7 +65,11 @@ class Params(C.Structure):
                 ("default_fluid_mat", C.c_int32), ("nlist_capacity", C.c_int32),
                 ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("diffusion", C.c_int32), ("n_dirichlet_c", C.c_int32),
-                ("dirichlet_C", Schedule * MAX_DIRICHLET)]
+                ("dirichlet_C", Schedule * MAX_DIRICHLET),
+                # moving Gaussian surface heat flux (C4, [P21]; not in the reference)
+                ("heat_source", C.c_int32), ("hs_material_mask", C.c_uint32),
+                ("hs_power", C.c_double), ("hs_radius", C.c_double),
+                ("hs_origin", C.c_double * 3), ("hs_velocity", C.c_double * 3)]
 
 
 _dp = C.POINTER(C.c_double)

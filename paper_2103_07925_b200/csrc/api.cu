@@ -92,6 +92,10 @@ std::vector<std::string> validate(const sphg_params& P) {  // restates config.hp
   if (P.transitions < 0 || P.transitions > 2) fail("unknown transition mode");
   if (P.transitions == 2 && !P.diffusion) fail("concentration transitions need the diffusion equation");
   if (P.default_fluid_mat < 0 || P.default_fluid_mat >= P.n_mat) fail("default fluid material missing");
+  if (P.heat_source) {  // [P21]
+    if (!P.thermal) fail("heat source needs the heat equation");
+    if (!(P.hs_radius > 0.0)) fail("heat source radius must be positive");
+  }
   return v;
 }
 
@@ -186,6 +190,17 @@ DevParams make_dev_params(const sphg_params& p) {
   P.Ir_over_m = 0.4 * reff * reff;
   P.tvf = p.tvf;
   P.thermal = p.thermal;
+  P.heat_source = p.thermal && p.heat_source;  // [P21]; constants as the oracle forms them
+  P.hs_mask = p.hs_material_mask;
+  P.hs_q0 = 2.0 * p.hs_power / (M_PI * p.hs_radius * p.hs_radius);
+  P.hs_r0sq = p.hs_radius * p.hs_radius;
+  P.hs_cut2 = 16.0 * p.hs_radius * p.hs_radius;
+  for (int a = 0; a < 2; ++a) {
+    P.hs_origin[a] = p.hs_origin[a];
+    P.hs_vel[a] = p.hs_velocity[a];
+  }
+  P.hs_dz = 0.5 * p.dx;
+  P.hs_lat2 = 0.5625 * p.dx * p.dx;
   P.transitions = p.transitions;
   P.default_fluid_mat = p.default_fluid_mat;
   for (int a = 0; a < 3; ++a) {
@@ -869,6 +884,10 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     c.alt.alloc(na, c.P.diffusion != 0);
     c.H2new.alloc(na);
     if (c.P.diffusion) c.C2new.alloc(na);
+    if (c.P.heat_source) {
+      c.hsrc.alloc(na);
+      c.P.hsrc = c.hsrc.p;
+    }
     c.keys.alloc(na);
     c.keys_alt.alloc(na);
     c.vals.alloc(na);
@@ -1289,7 +1308,7 @@ void sphg_destroy(sphg_ctx* h) {
   destroy_graphs(c);
   if (c.dtime) cudaFree(c.dtime);
   if (c.htime) cudaFreeHost(c.htime);
-  c.cur.free(); c.alt.free(); c.H2new.free(); c.C2new.free(); c.bodies.free();
+  c.cur.free(); c.alt.free(); c.H2new.free(); c.C2new.free(); c.hsrc.free(); c.bodies.free();
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
   c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();
   c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();

@@ -55,6 +55,15 @@ struct DevParams {
   // velocity at t^{n+1/2} (drift), velocity and acceleration at t^{n+1} (wall state)
   int32_t n_walls, pad_w;
   double wall_vh[SPHG_MAX_WALL_GROUPS][3], wall_v[SPHG_MAX_WALL_GROUPS][3], wall_a[SPHG_MAX_WALL_GROUPS][3];
+  // moving Gaussian surface heat flux [P21] (sphg.h): source rate per particle (storage order) in hsrc,
+  // written by k_heat_source before the conduction kernels read it in their epilogues
+  int32_t heat_source;
+  uint32_t hs_mask;
+  double hs_q0;                    // 2 P / (pi r0^2)
+  double hs_r0sq, hs_cut2;         // r0^2, (4 r0)^2
+  double hs_origin[2], hs_vel[2];
+  double hs_dz, hs_lat2;           // dx/2, (3 dx/4)^2
+  double* hsrc;
 };
 
 // ------------------------------------------------------ brick traversal

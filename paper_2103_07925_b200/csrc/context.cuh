@@ -86,6 +86,7 @@ struct Ctx {
   Particles cur, alt;      // alt = reorder target / scratch
   DBuf<double2> H2new;     // heat double buffer
   DBuf<double2> C2new;     // concentration double buffer
+  DBuf<double> hsrc;       // surface heat flux source rate per particle [P21] (params.heat_source)
   DBuf<sphg_body> bodies;
   size_t bodies_cap = 0;
   // rebuild scratch

@@ -187,9 +187,71 @@ __global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevPara
   const uint32_t kind = kind_of(kmd);
   const double rho_a = kind == SPHG_FLUID ? D.G1.p[i].w : Ma.rho0;
   double rate = 0.0;
-  if (Ma.cp > 0.0) rate = s / (rho_a * Ma.cp);
+  if (Ma.cp > 0.0) {
+    rate = s / (rho_a * Ma.cp);
+    if (P.heat_source) rate += P.hsrc[i];  // [P21]
+  }
   Hout[i] = make_double2(hi.x + P.dt * rate, hi.y);
   D.dTdt.p[i] = rate;
+}
+
+// ------------------------------------------------------- surface heat flux
+// Moving Gaussian surface heat flux [P21] (BASELINE C4; the reference has no heat sources): source
+// rate q(x_i, y_i, t^{n+1}) dx^2 / (m_i c_p,i) of an exposed absorbing particle into P.hsrc[i], 0
+// otherwise.  Exposure: no mask-material neighbour within r_c above i (sphg.h); a discrete decision,
+// so the geometry uses the pinned no-FMA arithmetic of the oracle.  Groups outside 4 r0 of the spot
+// skip their row.  t_dev (graph replay): t^{n+1} from device memory.
+template <int G>
+__global__ void __launch_bounds__(kBlock) k_heat_source(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                         const uint32_t* __restrict__ list, size_t nlist,
+                                                         double t_new, const double* __restrict__ t_dev) {
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  const size_t g = t / G;
+  const int lane = (int)(t % G);
+  const bool active = g < nlist;
+  const uint32_t i = active ? list[g] : 0u;
+  if (t_dev) t_new = *t_dev;
+  bool absorbs = false;
+  double rho2 = 0.0, blocked = 0.0;
+  uint32_t kmd = 0;
+  if (active) {
+    kmd = D.kmd.p[i];
+    absorbs = ((P.hs_mask >> mat_of(kmd)) & 1u) && kind_of(kmd) != SPHG_BOUNDARY && P.mat[mat_of(kmd)].cp > 0.0;
+  }
+  double3 pi = make_double3(0, 0, 0);
+  if (absorbs) {
+    pi = ldpos(&D.G0.p[i]);
+    const double pxy[2] = {pi.x, pi.y};
+    for (int a = 0; a < 2; ++a) {
+      double c = __dadd_rn(P.hs_origin[a], __dmul_rn(P.hs_vel[a], t_new));
+      if (P.periodic[a]) {
+        const double u = __dsub_rn(c, P.lo[a]);
+        c = __dsub_rn(__dadd_rn(P.lo[a], u), __dmul_rn(P.L[a], floor(__ddiv_rn(u, P.L[a]))));
+      }
+      const double d = mimg(P, __dsub_rn(pxy[a], c), a);
+      rho2 = __dadd_rn(rho2, __dmul_rn(d, d));
+    }
+    absorbs = !(rho2 > P.hs_cut2);
+  }
+  if (absorbs) {
+    const Row R = row_of(L, i);
+    for (int k = lane; k < R.n && blocked == 0.0; k += G) {
+      const uint32_t j = R.at(k) & (P.img_mode == kImgCode ? kIdxMask : 0xffffffffu);
+      if (!((P.hs_mask >> mat_of(D.kmd.p[j])) & 1u)) continue;
+      const double3 pj = ldpos(&D.G0.p[j]);
+      const double3 d = mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z);  // r_i - r_j
+      if (r2_exact(d) > P.rc2) continue;
+      if (-d.z > P.hs_dz && __dadd_rn(__dmul_rn(d.x, d.x), __dmul_rn(d.y, d.y)) < P.hs_lat2) blocked = 1.0;
+    }
+  }
+  blocked = gsum<G>(blocked);
+  if (!active || lane != 0) return;
+  double q = 0.0;
+  if (absorbs && blocked == 0.0) {
+    const double e = exp(-2.0 * rho2 / P.hs_r0sq);
+    q = P.hs_q0 * e * (P.dx * P.dx) / (D.V4.p[i].w * P.mat[mat_of(kmd)].cp);
+  }
+  P.hsrc[i] = q;
 }
 
 // --------------------------------------------------------------- diffusion
@@ -549,7 +611,10 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
   D.B4.p[i] = make_double4(f * bg.x, f * bg.y, f * bg.z, 0.0);
   if (kHeat) {  // the k_heat epilogue for a fluid particle (rho_a = rho_i)
     double rate = 0.0;
-    if (Mt.cp > 0.0) rate = heat.s / (D.G1.p[i].w * Mt.cp);
+    if (Mt.cp > 0.0) {
+      rate = heat.s / (D.G1.p[i].w * Mt.cp);
+      if (P.heat_source) rate += P.hsrc[i];  // [P21]
+    }
     Hout[i] = make_double2(hi.x + P.dt * rate, hi.y);
     D.dTdt.p[i] = rate;
   }
@@ -870,6 +935,15 @@ void launch_heat_begin(Ctx& c) {
   const double t_new = c.t + c.P.dt;
   constexpr int G = kGOther;
   k_dirichlet<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new, c.capturing ? c.dtime : nullptr);
+  if (c.P.heat_source) {  // [P21] source rates before the conduction epilogues read them
+    if (c.nf)
+      k_heat_source<G><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, t_new,
+                                                                      c.capturing ? c.dtime : nullptr);
+    if (c.nrigid)
+      k_heat_source<G><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(c.P, c.cur, c.nl(), c.ridx.p, c.nrigid,
+                                                                          t_new, c.capturing ? c.dtime : nullptr);
+    c.launches += 2;
+  }
   if (c.nf && !c.fuse_heat)
     SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.H2new.p, c.dflags)));

@@ -477,11 +477,16 @@ def bench_multi(args, clock_factory=None):
     st0 = ds.engine.stats()
     import contextlib
     clk = clock_factory(gpu) if clock_factory is not None else contextlib.nullcontext()
+    # device clock: CUDA events on this rank's current stream bracket the K steps (each decomposed
+    # step ends host-synchronised, so the end event fires when the last kernel / exchange is done)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with clk:
-        t0 = time.perf_counter()
+        ev0.record()
         ds.step(args.steps)
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
+        ev1.record()
+        ev1.synchronize()
+        dt = ev0.elapsed_time(ev1) * 1e-3
     launches = ds.engine.stats().kernel_launches - st0.kernel_launches
     dist.barrier()
     tmax = torch.tensor([dt], dtype=torch.float64, device=dev)
@@ -536,8 +541,8 @@ def bench_multi(args, clock_factory=None):
                                        + (" (8M per GPU)" if weak else ""),
                            "particles": n, "parallelism": f"domain decomposition {ds.grid.dims}, {backend} halo",
                            "ghost_width_h": ds.width / ds.h},
-                "timing": "host wall clock between barriers + cuda synchronize, max over ranks "
-                          "(the per-rank step mixes kernels and NCCL exchanges)",
+                "timing": "CUDA events on each rank's stream between barriers + cuda synchronize, "
+                          "max over ranks (the per-rank step mixes kernels and NCCL exchanges)",
                 "comm_s_rank0": ds.comm_s, "rebuilds": ds.rebuilds, "repartitions": ds.repartitions,
                 "gpu_launches": int(tl.item()), "e2e": e2e, "roofline": None,
                 "roofline_note": "per-kernel roofline is reported by the N=1 line; N>1 adds halo/body exchanges"}

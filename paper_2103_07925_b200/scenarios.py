@@ -589,6 +589,134 @@ def wall_velocity(u_wall, omega=0.0):
     return v
 
 
+def deposit_grains(seed, n_grains, Lx, Ly, z0, dx, median=4.0, sigma=0.3, r_clip=(2.0, 8.0), gap=1.0, trials=32):
+    """Seeded sequential deposition of log-normal spheres onto a plane (C4 powder layer).
+
+    Radii R = median exp(sigma N(0,1)) dx (Box-Muller on stream 4), clipped to r_clip.  Grain k is
+    dropped vertically at `trials` positions (x, y) ~ U(periodic footprint) (stream 2); at each it
+    rests at the first contact, with the substrate at z0 (centre z0 + R + gap dx) or with an earlier
+    grain j (centre distance R + R_j + gap dx, minimum image in x and y), and it is placed at the
+    lowest of these rests (first on ties).  The lowest-of-several drops stands in for the settling of
+    a DEM random close packing, which is not run.  Returns centres (n, 3)
+    and radii (n,)."""
+    u = splitmix_u01(seed, 4, np.arange(2 * n_grains, dtype=np.uint64)).reshape(n_grains, 2)
+    z = np.sqrt(-2.0 * np.log1p(-u[:, 0])) * np.cos(2.0 * math.pi * u[:, 1])
+    radii = np.clip(median * np.exp(sigma * z), r_clip[0], r_clip[1]) * dx
+    xy_all = splitmix_u01(seed, 2, np.arange(2 * trials * n_grains, dtype=np.uint64)).reshape(n_grains, trials, 2)
+    xy_all = xy_all * (Lx, Ly)
+    xy = np.zeros((n_grains, 2))
+    cz = np.zeros(n_grains)
+    g = gap * dx
+    for k in range(n_grains):
+        R = radii[k]
+        t = xy_all[k]                                  # (trials, 2)
+        zk = np.full(trials, z0 + R + g)
+        if k:
+            d = xy[None, :k, :] - t[:, None, :]        # (trials, k, 2)
+            d[..., 0] -= Lx * np.round(d[..., 0] / Lx)
+            d[..., 1] -= Ly * np.round(d[..., 1] / Ly)
+            rho2 = d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1]
+            s2 = (R + radii[:k] + g) ** 2
+            zc = np.where(rho2 < s2, cz[:k] + np.sqrt(np.maximum(s2 - rho2, 0.0)), -np.inf)
+            zk = np.maximum(zk, zc.max(axis=1))
+        b = int(np.argmin(zk))
+        xy[k] = t[b]
+        cz[k] = zk[b]
+    return np.column_stack([xy, cz]), radii
+
+
+def powder_bed(nx=400, ny=200, nz=194, dx=5e-6, dt=None, seed=2119, n_grains=5000, median=4.0, sigma=0.3,
+               T0=1550.0, T_t=1700.0, rho=7900.0, c=20.0, nu=1e-6, cp=700.0, kappa=20.0,
+               rho_gas=1.6, eta_gas=2.2e-5, cp_gas=520.0, kappa_gas=0.018, power=200.0, r0_dx=20.0,
+               scan_speed=1.0, g=-9.81, kc=1e3, zeta=0.1, jitter=0.05, name="c4", steps=1000):
+    """BASELINE configs[3] (C4): powder-bed-fusion-like melt, ~16M particles at dx = 5e-6 m.
+
+    Periodic in x and y; a 3-layer substrate slab (boundary particles, Dirichlet at T0) at the bottom
+    and a 3-layer lid on top; n_grains rigid metal grains (log-normal radii, median 4 dx, sigma 0.3)
+    deposited on the substrate by deposit_grains; argon-like gas everywhere else (rho 1.6).  Metal as
+    C2 (rho 7900, c 20, c_p 700, kappa 20, T_t 1700: solid 1 melts into liquid 2, which solidifies
+    into 1).  A Gaussian surface heat flux of `power` W, 1/e^2 radius r0_dx dx, scans along x at
+    `scan_speed` m/s from x = L_x/4 on the centre line [P21] (an extension: the reference has no heat
+    sources).  Pinned: gas c = c sqrt(rho / rho_gas) with one shared
+    p_b = rho c^2 (as C3), dt = 0.2 h / c_gas, bed preheated to T0 = 1550 K so the exposed grain
+    surface reaches T_t within the run (the flux heats it by ~330 K over 1000 steps).
+    nz counts the interior lattice layers (200 with the two 3-layer walls)."""
+    c_g = c * math.sqrt(rho / rho_gas)
+    if dt is None:
+        dt = 0.2 * dx / c_g
+    Lx, Ly, Lz = nx * dx, ny * dx, nz * dx
+    nl = 3
+    lo = (0.0, 0.0, -nl * dx)
+    hi = (Lx, Ly, Lz + nl * dx)
+    pb = rho * c * c
+    grav = (0.0, 0.0, g)
+    mats = [material(rho_gas, nu=eta_gas / rho_gas, cp=cp_gas, kappa=kappa_gas, c=c_g, pb=pb, g=grav),  # 0 gas
+            material(rho, cp=cp, kappa=kappa, c=c, T_t=T_t, melt=2, g=grav),                          # 1 solid
+            material(rho, nu=nu, cp=cp, kappa=kappa, c=c, pb=pb, T_t=T_t, solidify=1, g=grav),       # 2 melt
+            material(rho, cp=cp, kappa=kappa, c=c),                                                    # 3 substrate
+            material(rho_gas, c=c_g)]                                                                  # 4 lid
+    m_r = rho * dx ** 3
+    params = _params(dx, dt, lo, hi, (1, 1, 0), mats, kc=kc, dc=damping_from_ratio(zeta, kc, m_r),
+                     thermal=1, transitions=1)
+    params.n_dirichlet = 1
+    params.dirichlet_T[0].n = 1
+    params.dirichlet_T[0].t_end[0] = 1e30
+    params.dirichlet_T[0].value[0] = T0
+    params.heat_source = 1
+    params.hs_material_mask = (1 << 1) | (1 << 2) | (1 << 3)
+    params.hs_power = power
+    params.hs_radius = r0_dx * dx
+    params.hs_origin[0], params.hs_origin[1] = 0.25 * Lx, 0.5 * Ly
+    params.hs_velocity[0] = scan_speed
+    fl = lattice_box((0.0, 0.0, 0.0), (Lx, Ly, Lz), dx)
+    wl = lattice_box(lo, hi, dx)
+    wl = wl[(wl[:, 2] < 0.0) | (wl[:, 2] > Lz)]
+    nf, nw = len(fl), len(wl)
+    centers, radii = deposit_grains(seed, n_grains, Lx, Ly, 0.0, dx, median, sigma)
+    keep = centers[:, 2] + radii < Lz - 3.0 * dx  # grains must fit under the lid
+    centers, radii = centers[keep], radii[keep]
+    owner = mark_spheres((nx, ny, nz), (0.0, 0.0, 0.0), dx, (Lx, Ly, Lz), centers, radii, (True, True, False))
+    n = nf + nw
+    st = ParticleStore(n)
+    u = splitmix_u01(seed, 0, np.arange(3 * nf, dtype=np.uint64)).reshape(nf, 3)
+    p = fl + (2.0 * u - 1.0) * (jitter * dx)
+    for a, L in ((0, Lx), (1, Ly)):  # periodic wrap of the jittered lattice
+        p[:, a] = np.where(p[:, a] < 0.0, p[:, a] + L, np.where(p[:, a] >= L, p[:, a] - L, p[:, a]))
+    st.pos[:nf] = p
+    st.pos[nf:] = wl
+    rig = np.zeros(n, bool)
+    rig[:nf] = owner >= 0
+    st.kind[:nf] = abi.FLUID
+    st.kind[nf:] = abi.BOUNDARY
+    st.kind[rig] = abi.RIGID
+    st.group[rig] = owner[owner >= 0].astype(np.uint32)
+    st.material[:nf] = 0
+    st.material[rig] = 1
+    sub = np.zeros(n, bool)
+    sub[nf:] = wl[:, 2] < 0.0
+    st.material[nf:] = 4
+    st.material[sub] = 3
+    st.dirichlet_T[sub] = 0
+    dens = np.full(n, rho_gas)
+    dens[rig | sub] = rho
+    st.mass[:] = dens * dx ** 3
+    st.density[:] = dens
+    st.temperature[:] = T0
+    bodies = empty_bodies(len(centers))
+    bodies["material"] = 1
+    body_quantities(st, bodies, params)
+    _finish(st, bodies)
+    info = dict(n=n, n_fluid=int((st.kind == abi.FLUID).sum()), n_rigid=int(rig.sum()), n_boundary=nw,
+                n_bodies=len(centers), rigid_fraction=float(rig.mean()),
+                bed_height_dx=float(np.max(centers[:, 2] + radii) / dx) if len(centers) else 0.0)
+    return Scenario(name, params, st, bodies, steps, info)
+
+
+def config4(**kw):
+    """BASELINE configs[3] (C4): powder bed under a moving Gaussian heat flux (powder_bed)."""
+    return powder_bed(**kw)
+
+
 def config3(**kw):
     """BASELINE configs[2]: 128^3 two-phase liquid/gas with 200 rigid cubes and spheres."""
     return two_phase_with_bodies(**kw)
@@ -600,5 +728,5 @@ def config2(**kw):
 
 
 def by_name(name, **kw):
-    return {"c1": config1, "c2": config2, "c3": config3, "c5": config5, "dissolve": dissolving_bodies,
+    return {"c1": config1, "c2": config2, "c3": config3, "c4": config4, "c5": config5, "dissolve": dissolving_bodies,
             "couette": couette_channel}[name](**kw)

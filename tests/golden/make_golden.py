@@ -33,6 +33,8 @@ CASES = {
     "c2m": lambda: scenarios.config2(nside=10, n_grid=2, r_range=(1.5, 2.0), seed=5, melt_forcing=True),
     "c3": lambda: scenarios.config3(nside=10, n_bodies=2, r_range=(1.5, 2.0), seed=9),
     "dissolve": lambda: scenarios.dissolving_bodies(nside=10, n_bodies=2, r_range=(1.5, 2.0), seed=21, forcing=True),
+    # powder bed under the moving surface heat flux [P21]: exposed grain surfaces melt at step 1
+    "c4": lambda: scenarios.config4(nx=12, ny=12, nz=24, n_grains=4, median=2.5, r0_dx=4.0, T0=1699.0, seed=3),
 }
 
 

@@ -665,3 +665,93 @@ def test_moving_wall_drift_and_central_difference(O):  # config.hpp:42-50
     assert np.allclose(g.vel[top, 0], 0.01 * np.sin(om * 3 * dt), rtol=1e-14)  # u_w(t^{n+1})
     bottom = (sc.store.kind == abi.BOUNDARY) & (sc.store.group == 0)
     assert np.array_equal(g.pos[bottom], sc.store.pos[bottom])
+
+
+# ---------------------------------------------------- surface heat flux [P21]
+# The moving Gaussian surface flux of BASELINE C4 is an extension (the reference has no heat
+# sources); these known answers pin the oracle to the formula in sphg.h.
+def _flux_params(P=200.0, r0=5e-3, origin=(0.006, 0.006), vel=(0.0, 0.0), t0=0.0):
+    p = _single_material_params(periodic=True)
+    p.n_mat = 2
+    p.mat[0] = scenarios.material(1.6, nu=1e-5, cp=520.0, kappa=0.0, c=10.0)   # gas: not in the mask
+    p.mat[1] = scenarios.material(7900.0, nu=1e-6, cp=700.0, kappa=0.0, c=10.0)  # metal
+    p.thermal = 1
+    p.t0 = t0
+    p.heat_source = 1
+    p.hs_material_mask = 1 << 1
+    p.hs_power, p.hs_radius = P, r0
+    p.hs_origin[0], p.hs_origin[1] = origin
+    p.hs_velocity[0], p.hs_velocity[1] = vel
+    return p
+
+
+def _flux_rates(O, p, pos, mats):
+    s = ParticleStore(len(pos))
+    s.pos[:] = pos
+    s.material[:] = mats
+    s.mass[:] = np.where(np.asarray(mats) == 1, 7900.0, 1.6) * p.dx ** 3
+    s.density[:] = np.where(np.asarray(mats) == 1, 7900.0, 1.6)
+    s.temperature[:] = 300.0
+    o = O.Oracle(p)
+    o.upload(s, None)
+    o.initialize()
+    o.conduction_rhs()
+    g, _ = o.download()
+    return g.dT_dt
+
+
+def _peak_rate(p):
+    q0 = 2.0 * p.hs_power / (math.pi * p.hs_radius ** 2)
+    return q0 * p.dx ** 2 / (7900.0 * p.dx ** 3 * 700.0)
+
+
+def test_heat_flux_isolated_particle_at_spot_centre(O):
+    p = _flux_params()
+    r = _flux_rates(O, p, [[0.006, 0.006, 0.006]], [1])
+    assert r[0] == pytest.approx(_peak_rate(p), rel=1e-15)
+
+
+def test_heat_flux_gaussian_profile_and_truncation(O):
+    p = _flux_params(r0=1e-3)
+    x = 0.006 + np.array([0.0, 1e-3, 2e-3, 3.99e-3, 4.01e-3])  # 0, r0, 2 r0, just inside / outside 4 r0
+    # one particle per run, so none shadows another
+    got = [_flux_rates(O, p, [[xi, 0.006, 0.006]], [1])[0] for xi in x]
+    want = [_peak_rate(p) * math.exp(-2.0 * ((xi - 0.006) / 1e-3) ** 2) for xi in x[:4]] + [0.0]
+    assert got[:4] == pytest.approx(want[:4], rel=1e-14)
+    assert got[4] == 0.0
+
+
+def test_heat_flux_shadowing(O):
+    p = _flux_params()
+    c = [0.006, 0.006, 0.006]
+    above = [0.006, 0.006, 0.007]              # dz = dx, lateral 0: shadows the lower particle
+    beside = [0.006 + 8e-4, 0.006, 0.007]      # lateral 0.8 dx > 3/4 dx: does not shadow
+    half = [0.006, 0.006, 0.006 + 4e-4]        # dz = 0.4 dx <= dx/2: does not shadow
+    r = _flux_rates(O, p, [c, above], [1, 1])
+    assert r[0] == 0.0 and r[1] > 0.0
+    assert _flux_rates(O, p, [c, beside], [1, 1])[0] == pytest.approx(_peak_rate(p), rel=1e-15)
+    assert _flux_rates(O, p, [c, half], [1, 1])[0] == pytest.approx(_peak_rate(p), rel=1e-15)
+    # a gas particle (material not in the mask) neither absorbs nor shadows
+    r = _flux_rates(O, p, [c, above], [1, 0])
+    assert r[0] == pytest.approx(_peak_rate(p), rel=1e-15) and r[1] == 0.0
+
+
+def test_heat_flux_spot_moves_and_wraps(O):
+    # spot centre at t^{n+1} = t0 + dt: origin + v t^{n+1}, wrapped on the periodic x axis (L = 12 mm)
+    v = 100.0
+    t1 = 1.0e-4
+    p = _flux_params(r0=1e-3, origin=(0.011, 0.006), vel=(v, 0.0), t0=t1 - 1e-5)
+    xc = 0.011 + v * t1 - 0.012  # 0.009 after the wrap
+    r = _flux_rates(O, p, [[xc, 0.006, 0.006]], [1])
+    assert r[0] == pytest.approx(_peak_rate(p), rel=1e-12)
+
+
+def test_heat_flux_config_refused_without_heat_equation():
+    from paper_2103_07925_b200 import _lib
+    import ctypes as C
+    lib = _lib.load()
+    p = _flux_params()
+    p.thermal = 0
+    buf = C.create_string_buffer(4096)
+    assert lib.sphg_validate(C.byref(p), buf, 4096) == abi.ERR_CONFIG
+    assert b"heat source needs the heat equation" in buf.value
