@@ -2,6 +2,7 @@
 //
 //   k_density       density_summation + eos_pressure
 //   k_heat          conduction_rhs + explicit T update
+//   k_heat_source   moving Gaussian surface heat flux (C4)      ([P21]; an extension, no reference counterpart)
 //   k_diffusion     diffusion_rhs + explicit C update
 //   k_extrapolate   extrapolate_wall_quantities                 (Adami 2012)
 //   k_forces_fluid  momentum_rhs with transport velocity
