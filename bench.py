@@ -68,7 +68,7 @@ def parse():
     ap.add_argument("--spheres", type=int, default=20000)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="N>1: strong = the 64M C5 box split over N GPUs; weak = 8M particles per GPU")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-nside", type=int, default=96)
@@ -320,19 +320,21 @@ def run_sph(args):
         # the step's results land in pinned host arrays of the store (the download DMAs into them)
         for f, shape in (("pos", (n, 3)), ("vel", (n, 3)), ("density", (n,)), ("pressure", (n,))):
             setattr(store, f, torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy())
+        sim.upload_state(pin_pos, pin_vel)  # untimed: first use of the copy stream and staging
+        sim.step_download(1, store=store, fields=fields)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             sim.upload_state(pin_pos, pin_vel)
-            sim.step(1)
-            sim.download(store, fields=fields)
+            sim.step_download(1, store=store, fields=fields)  # pos / density / pressure leave during the forces
         e2e_s = time.perf_counter() - t0
         # the requested fields, packed into gid order on the device: pos, vel (24 B), density, pressure (8 B)
         d2h = n * (24 + 24 + 8 + 8)
         line["e2e"] = {"value": n * args.e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(48 * n),
                        "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
-                       "path": "Simulation.upload_state(pos, vel from pinned host) -> step(1) -> "
-                               "download(pos, vel, density, pressure into pinned host arrays); host wall clock"}
+                       "path": "Simulation.upload_state(pos, vel from pinned host) -> step_download(1: pos, vel, "
+                               "density, pressure into pinned host arrays; pos/density/pressure copied while the "
+                               "step's force kernels run); host wall clock"}
     if not args.no_cpu_baseline and rank == 0 and args.config == "c5":
         line["cpu_baseline"] = cpu_baseline(args.cpu_nside, args.spheres, args.nside)
     sim.close()

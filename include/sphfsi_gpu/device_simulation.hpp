@@ -153,6 +153,16 @@ class DeviceSimulation {
     bodies.resize(nb);
     check(sphg_download(ctx_, &v, bodies.data(), &nb), "download");
   }
+  /// nsteps steps, then download(): the snapshot step of the run loop; positions,
+  /// density, pressure and tags cross PCIe while the last step's forces run (transitions off).
+  void step_download(int nsteps, sphfsi::ParticleStore<3>& s, std::vector<sphg_body>& bodies) {
+    sphg_soa v = views(s);
+    size_t nb = 0;
+    check(sphg_num_bodies(ctx_, &nb), "num_bodies");
+    bodies.resize(nb);
+    check(sphg_step_download(ctx_, nsteps, &v, bodies.data(), &nb), "step_download");
+    if (nb != bodies.size()) download(s, bodies);  // bodies spawned during the steps
+  }
   // SPEC operations, bulk over the store
   void build_pairs() { stage(SPHG_STAGE_REBUILD); }
   void density_summation() { stage(SPHG_STAGE_DENSITY); }

@@ -196,6 +196,12 @@ int sphg_upload(sphg_ctx* ctx, const sphg_soa* soa, const sphg_body* bodies, siz
 int sphg_initialize(sphg_ctx* ctx);
 /* nsteps full KDK steps, stream-ordered. */
 int sphg_step(sphg_ctx* ctx, int nsteps);
+/* nsteps steps, then the requested store fields (and, with nb_io, the body table) in gid order, as
+ * sphg_step followed by sphg_download — the snapshot step of the reference's run loop.
+ * With transitions off, the fields that are final after the last step's wall extrapolation
+ * (pos, density, pressure, wall_pressure, wall_velocity, mass, body_frame_pos and the tags) cross
+ * PCIe on a second stream while that step's force kernels run; the rest after the final kick. */
+int sphg_step_download(sphg_ctx* ctx, int nsteps, sphg_soa* out, sphg_body* bodies_out, size_t* n_bodies_inout);
 /* One stage (parity hook; also the per-op evaluator API of SPEC:243-363). */
 int sphg_run_stage(sphg_ctx* ctx, int stage);
 /* Warm kinematic update between steps (same store, gid order): positions and velocities only,

@@ -1313,6 +1313,11 @@ int orc_download(orc_ctx* h, sphg_soa* o, sphg_body* bodies, size_t* nb) {
     return SPHG_OK;
 }
 
+int orc_step_download(orc_ctx* h, int nsteps, sphg_soa* o, sphg_body* bodies, size_t* nb) {
+    const int rc = orc_step(h, nsteps);
+    return rc ? rc : orc_download(h, o, bodies, nb);
+}
+
 int orc_num_bodies(orc_ctx* h, size_t* nb) {
     *nb = reinterpret_cast<Ctx*>(h)->bodies.size();
     return SPHG_OK;

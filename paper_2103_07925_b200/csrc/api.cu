@@ -484,6 +484,7 @@ void chain_forces(Ctx& c) {  // (B): density .. final kick
   if (c.P.thermal) timed(c, SPHG_STAGE_HEAT, c.fuse_heat ? launch_heat_begin : launch_heat);
   if (c.P.diffusion) timed(c, SPHG_STAGE_HEAT, launch_diffusion);
   timed(c, SPHG_STAGE_EXTRAPOLATE, launch_extrapolate);
+  if (c.pre_forces) c.pre_forces(c);
   timed_forces(c);
   if (c.fuse_heat) launch_heat_end(c);
   timed(c, SPHG_STAGE_BODIES, launch_bodies);
@@ -513,7 +514,7 @@ int one_step(sphg_ctx* h) {
   // fold fluid conduction into the forces pass (same terms, same order; heat does not feed the
   // extrapolation or the forces, so moving it after them changes nothing)
   c.fuse_heat = c.P.thermal && !c.timing;
-  if (graphs) {
+  if (graphs && !c.pre_forces) {
     *c.htime = c.t + c.P.dt;  // read by the memcpy node; the previous replay finished (flag sync above)
     run_graph(c, 1, chain_forces);
   } else {
@@ -724,9 +725,9 @@ bool is_pinned(const void* p) {
 }
 
 // contiguous device -> host copy of `bytes` (queued on the stream; returns after completion)
-void copy_out(Ctx& c, void* dst, const void* src, size_t bytes) {
+void copy_out(Ctx& c, void* dst, const void* src, size_t bytes, cudaStream_t st = nullptr) {
   if (!bytes) return;
-  cudaStream_t st = c.stream;
+  if (!st) st = c.stream;
   if (is_pinned(dst)) {
     SPHG_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
     return;
@@ -762,46 +763,83 @@ void copy_out(Ctx& c, void* dst, const void* src, size_t bytes) {
   if (prev >= 0) drain(prev, prev_off, prev_len);
 }
 
-void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
+// The requested store fields, carved out of dl_buf.  early = final once the wall extrapolation has run
+// (positions, density, pressure, wall state, mass, body-frame offsets, tags): the final kick only
+// writes V4.xyz, so with transitions off these can leave the device while the forces run.
+struct DlPlan {
+  OutPtrs early{}, late{};
+  struct Item {
+    void* host;
+    const void* dev;
+    size_t bytes;
+    bool early;
+  };
+  std::vector<Item> items;
+  size_t bytes = 0;
+};
+
+DlPlan plan_download(Ctx& c, sphg_soa* o) {
+  DlPlan pl;
   const size_t n = c.n;
-  if (n == 0) return;
   struct F {
     void* host;
     size_t elem;
-    void** dev;
+    bool early;
+    void** e;
+    void** l;
   };
-  OutPtrs d{};
-  const F fields[] = {
-      {o->pos, 24, (void**)&d.pos}, {o->vel, 24, (void**)&d.vel}, {o->vel_adv, 24, (void**)&d.vel_adv},
-      {o->acc, 24, (void**)&d.acc}, {o->acc_bg, 24, (void**)&d.acc_bg},
-      {o->body_frame_pos, 24, (void**)&d.body_frame_pos}, {o->wall_velocity, 24, (void**)&d.wall_velocity},
-      {o->force, 24, (void**)&d.force}, {o->density, 8, (void**)&d.density}, {o->pressure, 8, (void**)&d.pressure},
-      {o->mass, 8, (void**)&d.mass}, {o->temperature, 8, (void**)&d.temperature}, {o->dT_dt, 8, (void**)&d.dT_dt},
-      {o->wall_pressure, 8, (void**)&d.wall_pressure}, {o->kind, 1, (void**)&d.kind}, {o->group, 4, (void**)&d.group},
-      {o->material, 2, (void**)&d.material}, {o->dirichlet_T, 1, (void**)&d.dirichlet_T},
-      {o->owner, 4, (void**)&d.owner}, {o->concentration, 8, (void**)&d.concentration},
-      {o->dC_dt, 8, (void**)&d.dC_dt}, {o->dirichlet_C, 1, (void**)&d.dirichlet_C}};
+  OutPtrs& E = pl.early;
+  OutPtrs& L = pl.late;
+#define SPHG_DL(name, elem, early) {o->name, elem, early, (void**)&E.name, (void**)&L.name}
+  const F fields[] = {SPHG_DL(pos, 24, true), SPHG_DL(vel, 24, false), SPHG_DL(vel_adv, 24, false),
+                      SPHG_DL(acc, 24, false), SPHG_DL(acc_bg, 24, false), SPHG_DL(body_frame_pos, 24, true),
+                      SPHG_DL(wall_velocity, 24, true), SPHG_DL(force, 24, false), SPHG_DL(density, 8, true),
+                      SPHG_DL(pressure, 8, true), SPHG_DL(mass, 8, true), SPHG_DL(temperature, 8, false),
+                      SPHG_DL(dT_dt, 8, false), SPHG_DL(wall_pressure, 8, true), SPHG_DL(kind, 1, true),
+                      SPHG_DL(group, 4, true), SPHG_DL(material, 2, true), SPHG_DL(dirichlet_T, 1, true),
+                      SPHG_DL(owner, 4, true), SPHG_DL(concentration, 8, false), SPHG_DL(dC_dt, 8, false),
+                      SPHG_DL(dirichlet_C, 1, true)};
+#undef SPHG_DL
   size_t total = 0;
   for (const F& f : fields)
     if (f.host) total += (n * f.elem + 255) / 256 * 256;
-  if (total == 0) return;
+  if (total == 0 || n == 0) return pl;
   c.dl_buf.alloc(total);
   size_t off = 0;
   for (const F& f : fields)
     if (f.host) {
-      *f.dev = c.dl_buf.p + off;
+      void* dev = c.dl_buf.p + off;
+      *(f.early ? f.e : f.l) = dev;
+      pl.items.push_back({f.host, dev, n * f.elem, f.early});
+      pl.bytes += n * f.elem;
       off += (n * f.elem + 255) / 256 * 256;
     }
-  k_pack_store<<<grid_for(n, 256), 256, 0, c.stream>>>(c.P, c.cur, n, mid_step ? 1 : 0, (uint32_t)c.params.rank, d);
+  return pl;
+}
+
+void pack(Ctx& c, const OutPtrs& d, bool mid_step) {
+  k_pack_store<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, mid_step ? 1 : 0,
+                                                         (uint32_t)c.params.rank, d);
   c.launches++;
-  size_t bytes = 0;
-  for (const F& f : fields)
-    if (f.host) {
-      copy_out(c, f.host, *f.dev, n * f.elem);
-      bytes += n * f.elem;
-    }
+}
+
+OutPtrs merged(const DlPlan& pl) {  // every requested field in one pack
+  OutPtrs d = pl.early;
+  const void* const* l = reinterpret_cast<const void* const*>(&pl.late);
+  void** m = reinterpret_cast<void**>(&d);
+  for (size_t k = 0; k < sizeof(OutPtrs) / sizeof(void*); ++k)
+    if (l[k]) m[k] = const_cast<void*>(l[k]);
+  return d;
+}
+
+void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
+  if (c.n == 0) return;
+  DlPlan pl = plan_download(c, o);
+  if (pl.items.empty()) return;
+  pack(c, merged(pl), mid_step);
+  for (const auto& it : pl.items) copy_out(c, it.host, it.dev, it.bytes);
   SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-  c.last_d2h_bytes = bytes;
+  c.last_d2h_bytes = pl.bytes;
 }
 
 }  // namespace
@@ -979,37 +1017,98 @@ int sphg_initialize(sphg_ctx* h) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+// nsteps full steps; with `out`, the requested store fields are downloaded at the end.  With
+// transitions off, the fields that are final after the last step's wall extrapolation (DlPlan::early)
+// are packed there and copied on copy_stream while the force kernels run; the rest after the final
+// kick.  Same values as sphg_step followed by sphg_download.
+int run_steps(sphg_ctx* h, int nsteps, sphg_soa* out) {
+  Ctx& c = h->c;
+  if (!c.have_state) return fail(h, SPHG_ERR_RUNTIME, "no particle state uploaded");
+  if (out && out->n != c.n) return fail(h, SPHG_ERR_RUNTIME, "download: store size mismatch");
+  SPHG_CUDA_CHECK(cudaSetDevice(c.device));
+  if (c.n == 0) {
+    c.steps += nsteps;
+    c.t += nsteps * c.P.dt;
+    return SPHG_OK;
+  }
+  if (!c.step_ev[0]) {
+    SPHG_CUDA_CHECK(cudaEventCreate(&c.step_ev[0]));
+    SPHG_CUDA_CHECK(cudaEventCreate(&c.step_ev[1]));
+  }
+  const bool overlap = out && nsteps > 0 && c.P.transitions == 0 && !c.timing;
+  DlPlan pl;
+  if (overlap) {
+    pl = plan_download(c, out);
+    if (!c.copy_stream) {
+      SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+      SPHG_CUDA_CHECK(cudaEventCreateWithFlags(&c.dl_ev, cudaEventDisableTiming));
+    }
+  }
+  SPHG_CUDA_CHECK(cudaEventRecord(c.step_ev[0], c.stream));
+  for (int k = 0; k < nsteps; ++k) {
+    c.defer_final = k + 1 < nsteps && c.P.transitions == 0 && !c.timing;
+    if (overlap && k + 1 == nsteps)
+      c.pre_forces = [&pl](Ctx& cc) {
+        pack(cc, pl.early, false);
+        SPHG_CUDA_CHECK(cudaEventRecord(cc.dl_ev, cc.stream));
+      };
+    const int rc = one_step(h);
+    c.pre_forces = nullptr;
+    if (rc) {
+      c.defer_final = false;
+      if (c.final_pending) launch_final_kick_particles(c);  // leave a complete state behind
+      return rc;
+    }
+  }
+  c.defer_final = false;
+  size_t bytes = 0;
+  if (overlap) {  // the forces of the last step are queued on c.stream: copy the early fields meanwhile
+    SPHG_CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, c.dl_ev, 0));
+    for (const auto& it : pl.items)
+      if (it.early) copy_out(c, it.host, it.dev, it.bytes, c.copy_stream);
+    pack(c, pl.late, false);
+  }
+  SPHG_CUDA_CHECK(cudaEventRecord(c.step_ev[1], c.stream));
+  const int rc = check_flags(h, true);
+  float ms = 0.f;
+  SPHG_CUDA_CHECK(cudaEventElapsedTime(&ms, c.step_ev[0], c.step_ev[1]));
+  c.last_step_ms = ms;
+  if (overlap) SPHG_CUDA_CHECK(cudaStreamSynchronize(c.copy_stream));  // never leave copies in flight
+  if (rc || !out) return rc;
+  if (overlap) {
+    for (const auto& it : pl.items)
+      if (!it.early) copy_out(c, it.host, it.dev, it.bytes);
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.copy_stream));
+    for (const auto& it : pl.items) bytes += it.bytes;
+    c.last_d2h_bytes = bytes;
+  } else {
+    stage_download(c, out, false);
+  }
+  return SPHG_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int sphg_step(sphg_ctx* h, int nsteps) {
+  return guarded(h, [&]() -> int { return run_steps(h, nsteps, nullptr); });
+}
+
+int sphg_step_download(sphg_ctx* h, int nsteps, sphg_soa* out, sphg_body* bodies, size_t* nb_io) {
   return guarded(h, [&]() -> int {
+    const int rc = run_steps(h, nsteps, out);
+    if (rc) return rc;
     Ctx& c = h->c;
-    if (!c.have_state) return fail(h, SPHG_ERR_RUNTIME, "no particle state uploaded");
-    SPHG_CUDA_CHECK(cudaSetDevice(c.device));
-    if (c.n == 0) {
-      c.steps += nsteps;
-      c.t += nsteps * c.P.dt;
-      return SPHG_OK;
+    if (nb_io) {
+      if (bodies) d2h(bodies, c.bodies.p, std::min(*nb_io, c.nb), c.stream);
+      SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      *nb_io = c.nb;
     }
-    if (!c.step_ev[0]) {
-      SPHG_CUDA_CHECK(cudaEventCreate(&c.step_ev[0]));
-      SPHG_CUDA_CHECK(cudaEventCreate(&c.step_ev[1]));
-    }
-    SPHG_CUDA_CHECK(cudaEventRecord(c.step_ev[0], c.stream));
-    for (int k = 0; k < nsteps; ++k) {
-      c.defer_final = k + 1 < nsteps && c.P.transitions == 0 && !c.timing;
-      const int rc = one_step(h);
-      if (rc) {
-        c.defer_final = false;
-        if (c.final_pending) launch_final_kick_particles(c);  // leave a complete state behind
-        return rc;
-      }
-    }
-    c.defer_final = false;
-    SPHG_CUDA_CHECK(cudaEventRecord(c.step_ev[1], c.stream));
-    const int rc = check_flags(h, true);
-    float ms = 0.f;
-    SPHG_CUDA_CHECK(cudaEventElapsedTime(&ms, c.step_ev[0], c.step_ev[1]));
-    c.last_step_ms = ms;
-    return rc;
+    return SPHG_OK;
   });
 }
 
@@ -1309,6 +1408,8 @@ void sphg_destroy(sphg_ctx* h) {
   if (c.dtime) cudaFree(c.dtime);
   if (c.htime) cudaFreeHost(c.htime);
   c.cur.free(); c.alt.free(); c.H2new.free(); c.C2new.free(); c.hsrc.free(); c.bodies.free();
+  if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+  if (c.dl_ev) cudaEventDestroy(c.dl_ev);
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
   c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();
   c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();

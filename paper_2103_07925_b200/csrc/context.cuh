@@ -16,6 +16,7 @@
 // index lists (fluid / non-fluid in brick order, rigid body-major) drive the pair kernels.
 #pragma once
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -164,6 +165,11 @@ struct Ctx {
   bool use_graphs = true, capturing = false;
   double* dtime = nullptr;  // device t^{n+1} for captured Dirichlet kernels
   double* htime = nullptr;  // pinned host source of dtime
+  // sphg_step_download: enqueued after the wall extrapolation of the last step (eager chain), packs the
+  // fields that are final by then so their D2H copies on copy_stream overlap the force kernels
+  std::function<void(Ctx&)> pre_forces;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t dl_ev = nullptr;
 };
 
 // ------------------------------------------------------------ launchers

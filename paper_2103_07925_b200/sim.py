@@ -123,6 +123,23 @@ class Simulation:
         """step(state, dt), nsteps times."""
         self._check(self._fn("step")(self._h, int(nsteps)), "step")
 
+    def step_download(self, nsteps=1, store=None, fields=None):
+        """nsteps steps, then download() of `fields` — one call, so the fields that are final before
+        the last step's force pass (positions, density, pressure, wall state, mass, tags) are copied
+        to the host while the forces run.  Returns (ParticleStore, bodies) like download()."""
+        if store is None:
+            store = ParticleStore(self.n)
+        soa = store.soa(fields)
+        nb = C.c_size_t(self.num_bodies())
+        bodies = np.zeros(nb.value, BODY_DTYPE)
+        rc = self._fn("step_download")(self._h, int(nsteps), C.byref(soa), bodies_ptr(bodies), C.byref(nb))
+        self._check(rc, "step_download")
+        if nb.value != len(bodies):  # bodies spawned during the steps
+            bodies = np.zeros(nb.value, BODY_DTYPE)
+            self._check(self._fn("download")(self._h, C.byref(store.soa(())), bodies_ptr(bodies), C.byref(nb)),
+                        "download")
+        return store, bodies
+
     def run_stage(self, stage):
         self._check(self._fn("run_stage")(self._h, int(stage)), abi.STAGE_NAMES[stage])
 

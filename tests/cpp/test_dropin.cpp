@@ -36,9 +36,9 @@ int main() {
   sphfsi_gpu::DeviceSimulation sim(p, 0);
   sim.upload(store, {});
   sim.initialize();
-  sim.step(5);
+  sim.step(4);
   std::vector<sphg_body> bodies;
-  sim.download(store, bodies);
+  sim.step_download(1, store, bodies);  // the snapshot step: step + download in one call
   double lo = 1e300, hi = -1e300;
   for (double r : store.density) { lo = std::min(lo, r); hi = std::max(hi, r); }
   if (!(lo > 950.0 && hi < 1050.0)) { std::printf("density out of range %g %g\n", lo, hi); return 3; }

@@ -357,6 +357,34 @@ def test_upload_state_matches_oracle(Oracle):
     assert sim.stats().rebuilds == orc.stats().rebuilds
 
 
+@pytest.mark.parametrize("name", ["c1_small", "c2_melt", "c4_small"])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_step_download_equals_step_then_download(name, pinned):
+    """sphg_step_download (early fields copied during the last step's forces when transitions are
+    off; c2_melt / c4_small take the plain path) returns exactly what sphg_step + sphg_download do."""
+    import torch
+    from paper_2103_07925_b200.store import ParticleStore, SCALAR_FIELDS, TAG_FIELDS, VEC_FIELDS
+    sc = CASES[name]()
+    a, b = sim_factory(sc.params), sim_factory(sc.params)
+    for e in (a, b):
+        e.upload(sc.store, sc.bodies)
+        e.initialize()
+    fields = VEC_FIELDS + SCALAR_FIELDS + tuple(TAG_FIELDS)
+    out = ParticleStore(sc.store.n)
+    if pinned:
+        for f in fields:
+            arr = getattr(out, f)
+            t = torch.empty(arr.shape, dtype=getattr(torch, str(arr.dtype)), pin_memory=True)
+            setattr(out, f, t.numpy())
+    for k in (1, 3):
+        ga, ba = a.step_download(k, store=out, fields=fields)
+        b.step(k)
+        gb, bb = b.download()
+        for f in fields:
+            assert np.array_equal(getattr(ga, f), getattr(gb, f)), f"{f} after {k} steps"
+        assert np.array_equal(ba, bb)
+
+
 def test_download_into_pinned_and_pageable(Oracle):
     """The gid-order device pack lands identically in pinned and pageable host arrays."""
     import torch
