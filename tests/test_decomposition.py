@@ -71,6 +71,22 @@ def _worker(rank, world, port, case, out):
     ds.initialize()
     ds.step(NSTEPS[case])
     g, b = ds.gather()
+    # topology of the owned particles by gid: cell id and the gid-sorted Verlet candidate list
+    cells, _ = ds.engine.get_cells()
+    off, nbr = ds.engine.get_nlist()
+    own = ds.n_own
+    topo = {"gid": ds.gids[:own].astype(np.int64), "cell": np.asarray(cells)[:own].astype(np.int64),
+            "rows": [np.sort(ds.gids[nbr[off[i]:off[i + 1]]]).astype(np.int64) for i in range(own)]}
+    allt = [None] * world
+    dist.all_gather_object(allt, topo)
+    if rank == 0:
+        gid = np.concatenate([t["gid"] for t in allt])
+        cell = np.concatenate([t["cell"] for t in allt])
+        rows = [r for t in allt for r in t["rows"]]
+        order = np.argsort(gid)
+        lens = np.array([len(rows[k]) for k in order], np.int64)
+        flat = np.concatenate([rows[k] for k in order]) if len(order) else np.zeros(0, np.int64)
+        np.savez(out + ".topo.npz", gid=gid[order], cell=cell[order], lens=lens, flat=flat)
     if rank == 0:
         np.savez(out, pos=g.pos, vel=g.vel, acc=g.acc, acc_bg=g.acc_bg, density=g.density, pressure=g.pressure,
                  force=g.force, T=g.temperature, dT=g.dT_dt, kind=g.kind, C=g.concentration,
@@ -121,6 +137,17 @@ def test_ranks_match_one_rank(case, world, tmp_path, oracle_mod):
     assert vec_err(d["force"][rg], g.force[rg], s["force"][rg], 1e-8) <= 1
     assert vec_err(d["T"], g.temperature, 0.0, 1e-12) <= 1
     assert vec_err(d["C"], g.concentration, 1.0, 1e-12) <= 1
+    # cells, Verlet lists and flags match the one-rank run bit-exactly by gid (lists are
+    # compared where both runs last rebuilt at the same step, i.e. without a repartition)
+    assert np.array_equal(d["kind"], g.kind)
+    t = np.load(out + ".topo.npz")
+    assert np.array_equal(t["gid"], np.arange(sc.store.n))
+    cells_1, _ = o.get_cells()
+    assert np.array_equal(t["cell"], cells_1)
+    if int(d["repart"]) == 0:
+        off1, nbr1 = o.get_nlist()
+        assert np.array_equal(t["lens"], np.diff(off1))
+        assert np.array_equal(t["flat"], nbr1.astype(np.int64))
     al = b["alive"] == 1
     assert vec_err(d["bforce"][al], b["force"][al], s["body_force"][al], 1e-8) <= 1
     assert vec_err(d["binertia"][al], b["inertia"][al], np.abs(b["inertia"][al][:, :3]).max(1), 1e-12) <= 1
