@@ -33,8 +33,11 @@ launch = {"source": "ncu --metrics gpu__time_duration.sum --clock-control none, 
           "kernels": [{"kernel": k, "launches": cnt[k], "ms_total": round(v, 3), "ms_per_launch": round(v / cnt[k], 3),
                        "share": round(v / tot, 4)} for k, v in sorted(agg.items(), key=lambda x: -x[1])]}
 json.dump(launch, open(os.path.join(out, f"{tag}_launches_64m.json"), "w"), indent=1)
-rep = os.path.join(ROOT, "gpurun_out", f"prof_{tag}.ncu-rep")
-if os.path.exists(rep):
+full = []
+for rep in (os.path.join(ROOT, "gpurun_out", f"prof_{tag}.ncu-rep"),
+            os.path.join(ROOT, "gpurun_out", f"prof_{tag}_build.ncu-rep")):  # pair kernels; the Verlet builder
+    if not os.path.exists(rep):
+        continue
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(raw.splitlines()))
     hdr, units = rr[0], rr[1]
@@ -47,8 +50,9 @@ if os.path.exists(rep):
             "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "launch__grid_size", "smsp__inst_executed.sum"]
-    full = []
     for r in rr[2:]:
+        if "nan" in r[hdr.index("dram__bytes_read.sum")].lower():
+            continue  # a capture whose metric passes failed (repeated kernel); the other capture is kept
         e = {"kernel": short(r[hdr.index("Kernel Name")])}
         for k in keys:
             if k in hdr:
@@ -63,5 +67,6 @@ if os.path.exists(rep):
         s = sum(st.values()) or 1.0
         e["stalls_pct"] = {k: round(100 * v / s, 1) for k, v in sorted(st.items(), key=lambda x: -x[1])[:6]}
         full.append(e)
+if full:
     json.dump(full, open(os.path.join(out, f"{tag}_ncu_full_64m.json"), "w"), indent=1)
 print("ok", tag)
