@@ -41,7 +41,7 @@ FLOPS_PER_PAIR_DENSITY = 17.0
 STEP_BYTES_PER_PARTICLE = 480.0
 
 
-DEFAULT_NSIDE = {"c5": 400, "c1": 32, "c2": 64, "c3": 128, "c4": 200, "dissolve": 64}
+DEFAULT_NSIDE = {"c5": 400, "c1": 32, "c2": 64, "c3": 128, "c4": 200, "dissolve": 64, "paper46": 150}
 
 
 def make_scenario(args):
@@ -62,8 +62,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)  # C5: 100 steps (Verlet rebuilds included as they occur)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sph", choices=["sph", "reference"])
-    ap.add_argument("--config", default="c5", choices=["c5", "c1", "c2", "c3", "c4", "dissolve"],
-                    help="c5 = the headline workload (BASELINE metric); the others are secondary measurements")
+    ap.add_argument("--config", default="c5", choices=["c5", "c1", "c2", "c3", "c4", "dissolve", "paper46"],
+                    help="c5 = the headline workload (BASELINE metric); the others are secondary measurements "
+                         "(paper46 = the paper's own strong-scaling case, PAPER:1011-1014)")
     ap.add_argument("--nside", type=int, default=None, help="lattice side (default: the config's BASELINE size)")
     ap.add_argument("--spheres", type=int, default=20000)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
@@ -160,6 +161,26 @@ def cpu_baseline(nside, spheres_total, nside_total, steps_max=20, budget_s=15.0)
     return {"value": sc.store.n * k / dt, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"C5 physics, {nside}^3={sc.store.n} particles periodic, {ns} spheres, {k} steps "
                       f"(oracle: SPEC restatement on the reference headers, OpenMP)"}
+
+
+def cpu_baseline_scenario(sc, what, steps_max=10, budget_s=20.0):
+    """The oracle on the full scenario (bounded step count): the paper46 case is small enough."""
+    from oracle.oracle import Oracle
+    o = Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.initialize()
+    o.step(1)  # warm-up
+    t0 = time.perf_counter()
+    k = 0
+    while k < steps_max:
+        o.step(1)
+        k += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": sc.store.n * k / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{what}: {sc.store.n} particles, {k} steps (oracle, OpenMP)"}
 
 
 def run_reference(args):
@@ -337,6 +358,8 @@ def run_sph(args):
                                "step's force kernels run); host wall clock"}
     if not args.no_cpu_baseline and rank == 0 and args.config == "c5":
         line["cpu_baseline"] = cpu_baseline(args.cpu_nside, args.spheres, args.nside)
+    if not args.no_cpu_baseline and rank == 0 and args.config == "paper46":
+        line["cpu_baseline"] = cpu_baseline_scenario(make_scenario(args), "the paper's strong-scaling case itself")
     sim.close()
     print(json.dumps(line))
 

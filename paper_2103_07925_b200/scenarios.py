@@ -712,6 +712,67 @@ def powder_bed(nx=400, ny=200, nz=194, dx=5e-6, dt=None, seed=2119, n_grains=500
     return Scenario(name, params, st, bodies, steps, info)
 
 
+def paper_strong_scaling(nside=150, n_grid=6, dx=0.2, D=2.5, rho_f=1.0, nu=1.0, rho_s=10.0, g=1.0, c=50.0,
+                         dt=1e-3, kc=1e3, zeta=0.1, jitter=0.0, seed=2123, name="paper46", steps=100):
+    """The paper's own strong-scaling case: a cubic box of edge L = 30
+    (150^3 lattice at dx = 0.2) inside 3-layer boundary walls (156^3 - 150^3 = 421,416), 216 = 6^3
+    rigid spheres of diameter 2.5 and density 10 on a regular grid, fluid rho 1, nu 1, c 50
+    (p0 = p_b = 2500), gravity 1 downward on fluid and bodies, 48^3 cells of edge 0.65
+    (cell_edge_override), dt = 1e-3: 3,796,416 particles, as the paper's 3.79e6 (3.15e6 fluid,
+    2.20e5 rigid, 4.21e5 boundary).  Pinned (the paper does not state them for this case): k_c = 1e3
+    with damping ratio 0.1 (contact limit 0.22 sqrt(m_r/k_c) = 2.0e-3 >= dt), no jitter (the paper
+    starts from the lattice at rest).  nside / n_grid shrink it for the parity tests (same dx, box
+    edge nside dx, sphere centres at (k + 1/2) L / n_grid)."""
+    L = nside * dx
+    nl = 3
+    lo = (-nl * dx,) * 3
+    hi = (L + nl * dx,) * 3
+    p0 = rho_f * c * c
+    grav = (0.0, 0.0, -g)
+    mats = [material(rho_f, nu=nu, c=c, pb=p0, g=grav),  # 0 fluid
+            material(rho_s, c=0.0, g=grav),              # 1 solid
+            material(rho_f, c=c)]                        # 2 wall
+    m_r = rho_s * dx ** 3
+    params = _params(dx, dt, lo, hi, (0, 0, 0), mats, kc=kc, dc=damping_from_ratio(zeta, kc, m_r))
+    if nside == 150:
+        params.cell_edge_override = 0.65  # 48^3 cells over the 31.2 box (PAPER:1014)
+    fl = lattice_box((0.0,) * 3, (L,) * 3, dx)
+    wl = lattice_box(lo, hi, dx)
+    wl = wl[np.any((wl < 0.0) | (wl > L), axis=1)]
+    nf, nw = len(fl), len(wl)
+    sp = L / n_grid
+    ax = (np.arange(n_grid) + 0.5) * sp
+    centers = np.stack(np.meshgrid(ax, ax, ax, indexing="ij"), -1).reshape(-1, 3)
+    radii = np.full(len(centers), 0.5 * D)
+    owner = mark_spheres((nside,) * 3, (0.0,) * 3, dx, (L,) * 3, centers, radii, (False,) * 3)
+    n = nf + nw
+    st = ParticleStore(n)
+    if jitter > 0.0:
+        u = splitmix_u01(seed, 0, np.arange(3 * nf, dtype=np.uint64)).reshape(nf, 3)
+        fl = fl + (2.0 * u - 1.0) * (jitter * dx)
+    st.pos[:nf] = fl
+    st.pos[nf:] = wl
+    rig = np.zeros(n, bool)
+    rig[:nf] = owner >= 0
+    st.kind[:nf] = abi.FLUID
+    st.kind[nf:] = abi.BOUNDARY
+    st.kind[rig] = abi.RIGID
+    st.group[rig] = owner[owner >= 0].astype(np.uint32)
+    st.material[rig] = 1
+    st.material[nf:] = 2
+    dens = np.full(n, rho_f)
+    dens[rig] = rho_s
+    st.mass[:] = dens * dx ** 3
+    st.density[:] = dens
+    bodies = empty_bodies(len(centers))
+    bodies["material"] = 1
+    body_quantities(st, bodies, params)
+    _finish(st, bodies)
+    info = dict(n=n, n_fluid=int((st.kind == abi.FLUID).sum()), n_rigid=int(rig.sum()), n_boundary=nw,
+                n_bodies=len(centers), rigid_fraction=float(rig.mean()))
+    return Scenario(name, params, st, bodies, steps, info)
+
+
 def config4(**kw):
     """BASELINE configs[3] (C4): powder bed under a moving Gaussian heat flux (powder_bed)."""
     return powder_bed(**kw)
@@ -729,4 +790,5 @@ def config2(**kw):
 
 def by_name(name, **kw):
     return {"c1": config1, "c2": config2, "c3": config3, "c4": config4, "c5": config5, "dissolve": dissolving_bodies,
+            "paper46": paper_strong_scaling,
             "couette": couette_channel}[name](**kw)

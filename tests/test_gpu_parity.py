@@ -23,6 +23,9 @@ CASES = {
     "dissolve": lambda: scenarios.dissolving_bodies(nside=16, n_bodies=3, r_range=(2.0, 3.0), seed=13, forcing=True),
     # powder bed (periodic x, y; substrate + lid walls; gas; log-normal grains) under the moving
     # Gaussian surface heat flux [P21]: exposed grain surfaces melt at step 1
+    # the paper's strong-scaling case at a small size (closed box, 8 spheres D = 2.5 on a grid, lattice
+    # without jitter: many pairs exactly at r_c / r_v)
+    "paper46_small": lambda: scenarios.paper_strong_scaling(nside=30, n_grid=2),
     "c4_small": lambda: scenarios.config4(nx=24, ny=24, nz=40, n_grains=12, r0_dx=6.0, T0=1698.0, seed=3),
 }
 

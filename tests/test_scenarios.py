@@ -51,3 +51,29 @@ def test_spheres_do_not_overlap():
 def test_splitmix_uniform_range():
     u = scenarios.splitmix_u01(123, 0, np.arange(100000, dtype=np.uint64))
     assert u.min() >= 0.0 and u.max() < 1.0 and abs(u.mean() - 0.5) < 0.01
+
+
+def test_paper_strong_scaling_counts():  # 3.79e6 = 3.15e6 fluid + 2.20e5 rigid + 4.21e5 boundary
+    sc = scenarios.paper_strong_scaling()
+    assert sc.store.n == 3796416
+    assert sc.info["n_boundary"] == 156 ** 3 - 150 ** 3
+    assert round(sc.info["n_fluid"] / 1e6, 2) == 3.15
+    assert round(sc.info["n_rigid"] / 1e5, 1) == 2.2
+    assert sc.info["n_bodies"] == 216
+    ext = sc.params.hi[0] - sc.params.lo[0]
+    assert int(ext // sc.params.cell_edge_override) == 48  # 48^3 cells of edge 0.65
+
+
+def test_powder_bed_shape():  # BASELINE configs[3]: ~16M particles, ~5000 grains, log-normal radii
+    sc = scenarios.config4(nx=80, ny=40, nz=80, n_grains=100)
+    assert sc.store.n == 80 * 40 * 86
+    assert sc.info["n_bodies"] == 100  # every grain fits under the lid
+    r = []
+    for k in range(sc.info["n_bodies"]):
+        m = sc.store.group[sc.store.kind == 1] == k
+        r.append(m.sum())
+    assert min(r) > 0
+    _, radii = scenarios.deposit_grains(2119, 2000, 1.0, 1.0, 0.0, 1e-3)
+    med = np.median(radii / 1e-3)
+    assert 3.8 < med < 4.2  # median 4 dx
+    assert 0.25 < np.std(np.log(radii)) < 0.32  # sigma 0.3 (clipped tails)
