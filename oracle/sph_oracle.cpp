@@ -586,8 +586,13 @@ inline Side side_of(const Ctx& c, size_t j, const sphfsi::Material* eta_from) {
 
 // pair acceleration a_ij of fluid i due to j (momentum_rhs, PAPER:240-246 + TVF [P5]);
 // returns a_ij and adds V2*gradW to bg.
+// mag (tolerance scale): the summed magnitudes of the elementary products of the pair
+// term — both halves of p~, the viscous and the two TVF terms — so a cancellation inside p~ (a fluid
+// just below rho0 against a hydrostatic wall pressure) does not shrink the scale below the rounding of
+// its parts.  It bounds |returned value| from above.
+inline double norm3(const V3& v);
 inline V3 pair_acc(const Ctx& c, const sphfsi::QuinticKernel<3>& K, const Side& I, double mi_, const Side& J,
-                   const V3& d, double r, V3& bgsum) {
+                   const V3& d, double r, V3& bgsum, double* mag = nullptr) {
     const double dW = K.dw_dr(r);
     const V3 e = d / r;
     const V3 gW = dW * e;
@@ -603,6 +608,14 @@ inline V3 pair_acc(const Ctx& c, const sphfsi::QuinticKernel<3>& K, const Side& 
         term += 0.5 * (Ai + Aj);
     }
     bgsum += V2 * gW;
+    if (mag) {
+        double m = (std::abs(J.rho * I.p) + std::abs(I.rho * J.p)) / (I.rho + J.rho) * std::abs(dW) +
+                   std::abs(et * dW / r) * norm3(I.u - J.u);
+        if (c.P.tvf)
+            m += 0.5 * (std::abs(I.rho * sphfsi::dot(I.du, gW)) * norm3(I.u) +
+                        std::abs(J.rho * sphfsi::dot(J.du, gW)) * norm3(J.u));
+        *mag = std::abs(V2 / mi_) * m;
+    }
     return (V2 / mi_) * term;
 }
 
@@ -635,10 +648,11 @@ bool stage_forces(Ctx& c) {
                 }
                 const Side J = side_of(c, j, &mi_);
                 V3 bgp = V3::zero();
-                const V3 a = pair_acc(c, K, I, c.S.mass[i], J, d, r, bgp);
+                double mag = 0.0;
+                const V3 a = pair_acc(c, K, I, c.S.mass[i], J, d, r, bgp, &mag);
                 sum += a;
                 bg += bgp;
-                sc += norm3(a);
+                sc += mag;
                 bgsc += norm3(bgp);
             }
             const V3 b = v3(c.P.mat[c.S.material[i]].body_force);
@@ -668,10 +682,11 @@ bool stage_forces(Ctx& c) {
                     const Side Jf = side_of(c, j, nullptr);
                     const Side R = side_of(c, (size_t)i, &mj);
                     V3 bgp = V3::zero();
-                    const V3 a = pair_acc(c, K, Jf, c.S.mass[j], R, d, r, bgp);
+                    double mag = 0.0;
+                    const V3 a = pair_acc(c, K, Jf, c.S.mass[j], R, d, r, bgp, &mag);
                     const V3 fr = (-c.S.mass[j]) * a;
                     f += fr;
-                    sc += norm3(fr);
+                    sc += c.S.mass[j] * mag;
                 } else if (kj == Kind::Boundary || c.S.group[j] != body) {
                     const V3 d = mi3(c, c.S.pos[i], c.S.pos[j]);
                     const double r2 = r2of(d);

@@ -174,6 +174,8 @@ DevParams make_dev_params(const sphg_params& p) {
   P.inv_h = 1.0 / P.h;  // kernel.hpp:20 inv_h_
   P.rc = kSupport * P.h;
   P.rc2 = P.rc * P.rc;
+  P.rc2_lo = P.rc2 * (1.0 - 2e-4);
+  P.rc2_hi = P.rc2 * (1.0 + 1e-12);
   P.rv = P.rc + kSkin * P.h;
   P.rv2 = P.rv * P.rv;
   P.sigma = 1.0 / (120.0 * M_PI * P.h * P.h * P.h);  // kernel.hpp:44

@@ -41,6 +41,7 @@ struct DevParams {
   int32_t periodic[3];
   int32_t n_mat, n_sched, n_schedC, diffusion;
   double h, inv_h, rc, rc2, rv, rv2, sigma, sig_h, w0;
+  double rc2_lo, rc2_hi;  // rc^2 (1 - 2e-4), rc^2 (1 + 1e-12): the band where pair_q takes the pinned arithmetic
   double dx, dx3, dt, hdt;
   double kc, dc;
   double half_skin;
@@ -180,6 +181,33 @@ __device__ __forceinline__ double sqrt_and_rinv(double x, double& rinv) {
   const double e = fma(-r0, r0, x);
   rinv = y;
   return fma(0.5 * y, e, r0);
+}
+
+// q = r/h and 1/r of a pair with r^2 <= rc2_hi (r^2 as computed by the caller, FMA allowed).  dW ~ (3-q)^4
+// and W ~ (3-q)^5 turn a last-bit difference of q into a relative error ~12/(3-q) times larger, which
+// decides the result where a particle's only support sits near r_c (a rigid particle three layers deep,
+// a wall behind an exact lattice; a lone Shepard weight that is tiny instead of 0).  So within a
+// relative 2e-4 of r_c^2 the pair takes the oracle's arithmetic: no-FMA r^2, correctly rounded root,
+// q = r * (1/h) (kernel.hpp:30, 36); q = 3 is returned for pairs the exact r^2 puts outside r_c.
+// Callers treat q >= 3 as a zero kernel (kernel.hpp:49, 63).  Elsewhere the fast accurate root.
+template <class DP>
+__device__ __forceinline__ double pair_q(const DP& P, double3 d, double r2, double& rinv) {
+  if (r2 >= P.rc2_lo) {
+    const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(d.x, d.x), __dmul_rn(d.y, d.y)), __dmul_rn(d.z, d.z));
+    const double r = __dsqrt_rn(r2e);
+    rinv = 1.0 / r;
+    return r2e > P.rc2 ? 3.0 : __dmul_rn(r, P.inv_h);
+  }
+  return sqrt_and_rinv(r2 + 1e-300, rinv) * P.inv_h;
+}
+// Shepard weight shape W/sigma of a pair at offset d, or false outside r_c (see pair_q)
+template <class DP>
+__device__ __forceinline__ bool shepard_shape(const DP& P, double3 d, double r2, double& W) {
+  if (r2 > P.rc2_hi) return false;
+  double ri;
+  const double q = pair_q(P, d, r2, ri);
+  W = q >= 3.0 ? 0.0 : shape_q(q);
+  return true;
 }
 
 // ------------------------------------------------- neighbour-list entries

@@ -363,11 +363,9 @@ __global__ void __launch_bounds__(kBlock) k_extrapolate(const __grid_constant__ 
       const uint32_t f = nb_index<M>(e);
       // fluid records are only read here (the kernel writes wall/rigid records): read-only path
       const double4 g0 = ldg4(&D.G0.p[f]);
-      const double3 d = pair_delta<M>(P, pw, ld3(g0), e);
-      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
-      if (r2 > P.rc2) continue;
-      double ri;
-      const double W = shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);  // sigma cancels in the ratios
+      const double3 d = pair_delta<M>(P, pw, ld3(g0), e);  // = the oracle's minimum-image r_w - r_f
+      double W;  // sigma cancels in the ratios; pinned arithmetic within ulps of r_c (empty support)
+      if (!shepard_shape(P, d, d.x * d.x + d.y * d.y + d.z * d.z, W)) continue;
       const double4 g1 = ldg4(&D.G1.p[f]);
       const double pf = __ldg(reinterpret_cast<const double*>(&D.G2.p[f]) + 3);
       const uint32_t mf = kMultiEos || !P.single_g ? mat_of(__ldg(&D.kmd.p[f])) : (uint32_t)P.default_fluid_mat;
@@ -427,10 +425,11 @@ struct PairSide {
 template <bool kTvf, bool kSingleEta, bool kJFluid>
 __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, double3 d, double r2,
                                           const DevParams& P, double3& acc, double3& bg) {
-  // accurate q: dW ~ (3-q)^4 amplifies errors of q near the cut-off, and a rigid particle whose
-  // only fluid neighbour sits there sees that single term (coupling force)
+  // pinned q near the cut-off: dW ~ (3-q)^4 amplifies errors of q there, and a rigid particle whose
+  // only fluid neighbours sit there sees only those terms (coupling force)
   double rinv;
-  const double dW = P.sig_h * shape_deriv_q(sqrt_and_rinv(r2, rinv) * P.inv_h);
+  const double q = pair_q(P, d, r2, rinv);
+  const double dW = q >= 3.0 ? 0.0 : P.sig_h * shape_deriv_q(q);
   const double fac = dW * rinv;  // gradW = fac * d
   const double3 gW = make_double3(fac * d.x, fac * d.y, fac * d.z);
   const double V2 = I.V2 + J.V2;
@@ -738,7 +737,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
       const double3 dd = pair_delta<M>(P, pr, ld3(h0), e);
       const double3 d = make_double3(-dd.x, -dd.y, -dd.z);
       const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
-      if (r2 > P.rc2) continue;
+      if (r2 > P.rc2_hi) continue;  // pair_term settles the band around r_c with the exact r^2
       if (r2 == 0.0) {
         coincident = true;
         continue;
@@ -768,13 +767,13 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
       const uint32_t kindj = kind_of(D.kmd.p[j]);
       if (kindj != SPHG_BOUNDARY && D.group.p[j] == body) continue;
       const double3 d = pair_delta<M>(P, pr, ldpos(&D.G0.p[j]), e);  // r_r - r_j
-      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
-      if (!(r2 < P.dx * P.dx)) continue;
-      if (r2 == 0.0) {
+      // the contact decision r < dx is discrete: the oracle's no-FMA r^2 and correctly rounded root
+      const double rr = __dsqrt_rn(r2_exact(d));
+      if (!(rr < P.dx)) continue;
+      if (rr == 0.0) {
         coincident = true;
         continue;
       }
-      const double rr = sqrt(r2);
       const double ri = 1.0 / rr;
       const double3 e3 = make_double3(d.x * ri, d.y * ri, d.z * ri);
       const double3 vj = ldpos(&D.V4.p[j]);

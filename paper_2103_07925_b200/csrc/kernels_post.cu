@@ -42,27 +42,21 @@ __global__ void __launch_bounds__(128) k_shepard_grid(const __grid_constant__ De
   double num0 = 0.0, num1 = 0.0, num2 = 0.0, den = 0.0;
   for (int dx = -1; dx <= 1; ++dx) {
     int qx = ci[0] + dx;
-    double shx = 0.0;
     if (qx < 0 || qx >= P.ncell[0]) {
       if (!P.periodic[0]) continue;
-      shx = qx < 0 ? -P.L[0] : P.L[0];
       qx = (qx + P.ncell[0]) % P.ncell[0];
     }
     for (int dy = -1; dy <= 1; ++dy) {
       int qy = ci[1] + dy;
-      double shy = 0.0;
-      if (qy < 0 || qy >= P.ncell[1]) {
+        if (qy < 0 || qy >= P.ncell[1]) {
         if (!P.periodic[1]) continue;
-        shy = qy < 0 ? -P.L[1] : P.L[1];
-        qy = (qy + P.ncell[1]) % P.ncell[1];
+          qy = (qy + P.ncell[1]) % P.ncell[1];
       }
       for (int dz = -1; dz <= 1; ++dz) {
         int qz = ci[2] + dz;
-        double shz = 0.0;
-        if (qz < 0 || qz >= P.ncell[2]) {
+            if (qz < 0 || qz >= P.ncell[2]) {
           if (!P.periodic[2]) continue;
-          shz = qz < 0 ? -P.L[2] : P.L[2];
-          qz = (qz + P.ncell[2]) % P.ncell[2];
+              qz = (qz + P.ncell[2]) % P.ncell[2];
         }
         const int64_t cell = ((int64_t)qx * P.ncell[1] + qy) * P.ncell[2] + qz;
         const uint32_t j0 = cstart[cell], j1 = cend[cell];
@@ -70,13 +64,13 @@ __global__ void __launch_bounds__(128) k_shepard_grid(const __grid_constant__ De
           const uint32_t kmd = D.kmd.p[j];
           if (!((kind_mask >> kind_of(kmd)) & 1u) || is_ghost(kmd)) continue;
           const double4 g0 = D.G0.p[j];
-          const double ddx = x[0] - (g0.x + shx), ddy = x[1] - (g0.y + shy), ddz = x[2] - (g0.z + shz);
-          const double r2 = ddx * ddx + ddy * ddy + ddz * ddz;
-          if (r2 > P.rc2) continue;
+          // the oracle's minimum image x - r_j (the cell's image shift picks the same image inside r_c)
+          const double3 d = mimg3(P, x[0], x[1], x[2], g0.x, g0.y, g0.z);
+          double W;  // pinned arithmetic within ulps of r_c, where a lone weight decides "no support"
+          if (!shepard_shape(P, d, d.x * d.x + d.y * d.y + d.z * d.z, W)) continue;
           const bool fl = kind_of(kmd) == SPHG_FLUID;
           const double rho = fl ? D.G1.p[j].w : P.mat[mat_of(kmd)].rho0;
-          double ri;
-          const double w = (D.V4.p[j].w / rho) * (P.sigma * shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h));
+          const double w = (D.V4.p[j].w / rho) * (P.sigma * W);
           den += w;
           switch (field) {
             case SPHG_FIELD_VELOCITY: {

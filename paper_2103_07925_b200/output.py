@@ -166,14 +166,22 @@ class OutputPlan:
     prefix: str = "sph"
 
 
-def _write_outputs(sim, plan, step, traj, store):
+def _wants(plan, step, traj):
+    snap = bool(plan.snapshot_interval) and step % plan.snapshot_interval == 0
+    tr = traj is not None and bool(plan.trajectory_interval) and step % plan.trajectory_interval == 0
+    return snap, tr, (SNAPSHOT_FIELDS if snap else ("kind",)) if (snap or tr) else None
+
+
+def _write_outputs(sim, plan, step, traj, store, downloaded=None):
     st = sim.stats()
     t = st.time
-    snap = plan.snapshot_interval and step % plan.snapshot_interval == 0
-    tr = traj is not None and plan.trajectory_interval and step % plan.trajectory_interval == 0
+    snap, tr, fields = _wants(plan, step, traj)
     gr = plan.grid is not None and plan.grid_interval and step % plan.grid_interval == 0
     if snap or tr:
-        store, bodies = sim.download(store, fields=SNAPSHOT_FIELDS if snap else ("kind",))
+        if downloaded is not None:
+            store, bodies = downloaded
+        else:
+            store, bodies = sim.download(store, fields=fields)
         if snap:
             write_snapshot(store, t, os.path.join(plan.out_dir, "%s_%08d.txt" % (plan.prefix, step)), step)
         if tr:
@@ -190,7 +198,8 @@ def _write_outputs(sim, plan, step, traj, store):
 def run(sim, nsteps, plan, log=None):
     """run(config, overrides) -> exit status + artifacts for an already uploaded and
     initialised simulation: steps it `nsteps` times, writing the plan's outputs at step 0 and every
-    interval.  Between output points the steps go to the device in one sphg_step(K) call.  Returns
+    interval.  Between output points the steps go to the device in one sphg_step(K) call (one
+    sphg_step_download(K) when the point writes a snapshot or trajectory).  Returns
     (status, message): 0 ok, 2 config violation, 3 runtime assertion (escaped / coincident
     particle, non-finite state), 4 device failure — the SPEC's exit codes."""
     os.makedirs(plan.out_dir, exist_ok=True)
@@ -203,9 +212,14 @@ def run(sim, nsteps, plan, log=None):
         store = _write_outputs(sim, plan, 0, traj, store)
         while step < nsteps:
             nxt = min([nsteps] + [(step // i + 1) * i for i in intervals])
-            sim.step(nxt - step)
+            fields = _wants(plan, nxt, traj)[2]
+            if fields is not None:  # snapshot step: the download overlaps the last step's forces
+                got = sim.step_download(nxt - step, store=store, fields=fields)
+            else:
+                sim.step(nxt - step)
+                got = None
             step = nxt
-            store = _write_outputs(sim, plan, step, traj, store)
+            store = _write_outputs(sim, plan, step, traj, store, got)
             if log:
                 log("step %d t=%s" % (step, _g(sim.stats().time)))
     except SPHError as e:
