@@ -95,10 +95,12 @@ def _worker(rank, world, port, case, out):
     dist.destroy_process_group()
 
 
-NSTEPS = {"c1": 6, "c2": 6, "c1fast": 16, "c3": 6, "diff": 6}
+NSTEPS = {"c1": 6, "c2": 6, "c1fast": 16, "c3": 6, "diff": 6, "bigbody": 0}
 
 
 def _case(case):
+    if case == "bigbody":  # one body of ~1e4 particles in a periodic fluid box (SPEC acceptance 5)
+        return scenarios.config1(nside=36, n_spheres=1, r_range=(13.0, 13.0), seed=17)
     if case == "c1":
         return scenarios.config1(nside=20, n_spheres=3, r_range=(3.0, 4.0), seed=11)
     if case == "c1fast":  # u ~ U(+-1 m/s): Verlet rebuilds every few steps and repartitions
@@ -151,6 +153,26 @@ def test_ranks_match_one_rank(case, world, tmp_path, oracle_mod):
     al = b["alive"] == 1
     assert vec_err(d["bforce"][al], b["force"][al], s["body_force"][al], 1e-8) <= 1
     assert vec_err(d["binertia"][al], b["inertia"][al], np.abs(b["inertia"][al][:, :3]).max(1), 1e-12) <= 1
+
+
+def test_body_reductions_partition_invariant_8_workers(tmp_path, oracle_mod):
+    """SPEC acceptance 5: for a 3D body of ~1e4 particles, the world inertia, force and torque of 1
+    worker and 8 workers (2x2x2 boxes; body partials merged in rank order with TwoSum) agree to 1e-12."""
+    out = str(tmp_path / "ds.npz")
+    mp.spawn(_worker, args=(8, _free_port(), "bigbody", out), nprocs=8, join=True)
+    d = np.load(out)
+    sc = _case("bigbody")
+    assert 9000 < int((sc.store.kind == abi.RIGID).sum()) < 11000
+    o = oracle_mod.Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.initialize()
+    _, b = o.download()
+    s = o.scales()
+    from tests.helpers import vec_err
+    assert vec_err(d["binertia"], b["inertia"], np.abs(b["inertia"][:, :3]).max(1), 1e-12) <= 1
+    assert vec_err(d["bforce"], b["force"], s["body_force"], 1e-12) <= 1
+    assert vec_err(d["btorque"], b["torque"], s["body_torque"], 1e-12) <= 1
+    assert np.array_equal(d["bcom"], b["com"])
 
 
 def test_merge_partials_torch_matches_numpy():
