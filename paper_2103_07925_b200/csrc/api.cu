@@ -877,6 +877,9 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
   if (const char* e = std::getenv("SPHG_GRAPHS")) c.use_graphs = std::atoi(e) != 0;
   try {
     SPHG_CUDA_CHECK(cudaSetDevice(device));
+    int sms = 148;
+    SPHG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    c.fill_groups = (size_t)sms * 2048 / 4 / 2;
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     SPHG_CUDA_CHECK(cudaMalloc(&c.dflags, sizeof(DevFlags)));
     SPHG_CUDA_CHECK(cudaMemset(c.dflags, 0, sizeof(DevFlags)));

@@ -105,7 +105,8 @@ struct Ctx {
   DBuf<uint32_t> brick_buf, scan_cells;
   DBuf<uint8_t> dl_buf;  // download: requested store fields in gid order  // kind-list construction in brick order
   size_t nf = 0, nw = 0, nrigid = 0;
-  int group_density = 4, group_forces = 4;  // lanes per particle in the pair kernels
+  int group_density = 0, group_forces = 0;  // lanes per particle in the pair kernels (0 = lanes_for)
+  size_t fill_groups = 37888;  // particles that fill the GPU at 4 lanes: SMs x 2048 threads / 4 / 2
   bool cell_build = true;  // cell-cooperative Verlet build (falls back per particle on overflow)
   sphg_wall_motion_fn wall_fn = nullptr;  // moving wall groups (sphg_set_wall_motion)
   void* wall_user = nullptr;

@@ -892,23 +892,26 @@ int blocks_for(size_t groups) {
 }  // namespace
 
 // ============================================================= launchers
-// Lanes per particle (G): 8, 16 or 32, per kernel family (Ctx::group_*; default
-// from measurements; SPHG_GROUP_* environment overrides for tuning).
-#define SPHG_G_DISPATCH(GV, CALL)                       \
-  do {                                                  \
-    if ((GV) == 8) { constexpr int G = 8; CALL; }        \
-    else if ((GV) == 2) { constexpr int G = 2; CALL; }   \
-    else { constexpr int G = 4; CALL; }                  \
+// Lanes per particle (G).  4 is the measured optimum for lists that fill the GPU (DESIGN.md §4:
+// 2 / 8 / 16 lose at 64M).  A list below a quarter of a GPU's worth of 4-lane groups (the rigid and
+// wall subsets of small stores: ~1e3-1e4 particles) gets a warp per particle instead: there each
+// kernel is one latency chain per row walk, and 4 lanes per particle leave most SMs idle (C1: rigid
+// forces 21.6 -> 7.5 us, extrapolation 31 -> 10 us; its 31k-particle fluid list stays faster at 4).  The choice depends only on the list
+// length, so fused and unfused variants of a sum take the same summation order.
+// SPHG_GROUP_DENSITY / SPHG_GROUP_FORCES (2, 4, 8) fix the width for tuning sweeps.
+inline int lanes_for(const Ctx& c, size_t nlist) { return 2 * nlist < c.fill_groups ? 32 : 4; }
+#define SPHG_L_DISPATCH(C, NLIST, CALL)                              \
+  do {                                                              \
+    if (lanes_for(C, NLIST) == 32) { constexpr int G = 32; CALL; }  \
+    else { constexpr int G = 4; CALL; }                             \
   } while (0)
-constexpr int kGOther = 4;
-#ifndef SPHG_G_RIGID
-#define SPHG_G_RIGID 4
-#endif
-#ifndef SPHG_G_EXTRAP
-#define SPHG_G_EXTRAP 4
-#endif
-constexpr int kGRigid = SPHG_G_RIGID;   // lanes per rigid particle in k_forces_rigid (swept)
-constexpr int kGExtrap = SPHG_G_EXTRAP; // lanes per wall/rigid particle in k_extrapolate (swept)
+#define SPHG_G_DISPATCH(C, GV, NLIST, CALL)                      \
+  do {                                                          \
+    if ((GV) == 8) { constexpr int G = 8; CALL; }                \
+    else if ((GV) == 2) { constexpr int G = 2; CALL; }           \
+    else if ((GV) == 4) { constexpr int G = 4; CALL; }           \
+    else SPHG_L_DISPATCH(C, NLIST, CALL);                        \
+  } while (0)
 
 #define SPHG_IMG_DISPATCH(MODE, CALL)                             \
   do {                                                            \
@@ -921,7 +924,7 @@ constexpr int kGExtrap = SPHG_G_EXTRAP; // lanes per wall/rigid particle in k_ex
 
 void launch_density(Ctx& c) {
   if (c.nf == 0) return;
-  SPHG_G_DISPATCH(c.group_density,
+  SPHG_G_DISPATCH(c, c.group_density, c.nf,
                   SPHG_IMG_DISPATCH(c.P.img_mode, (k_density<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                                        c.P, c.cur, c.nl(), c.fidx.p, c.nf))));
   c.launches++;
@@ -933,23 +936,22 @@ void launch_density(Ctx& c) {
 void launch_heat_begin(Ctx& c) {
   if (c.n == 0) return;
   const double t_new = c.t + c.P.dt;
-  constexpr int G = kGOther;
   k_dirichlet<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new, c.capturing ? c.dtime : nullptr);
   if (c.P.heat_source) {  // [P21] source rates before the conduction epilogues read them
     if (c.nf)
-      k_heat_source<G><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, t_new,
-                                                                      c.capturing ? c.dtime : nullptr);
+      SPHG_L_DISPATCH(c, c.nf, (k_heat_source<G><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                   c.P, c.cur, c.nl(), c.fidx.p, c.nf, t_new, c.capturing ? c.dtime : nullptr)));
     if (c.nrigid)
-      k_heat_source<G><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(c.P, c.cur, c.nl(), c.ridx.p, c.nrigid,
-                                                                          t_new, c.capturing ? c.dtime : nullptr);
+      SPHG_L_DISPATCH(c, c.nrigid, (k_heat_source<G><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
+                                       c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, t_new, c.capturing ? c.dtime : nullptr)));
     c.launches += 2;
   }
   if (c.nf && !c.fuse_heat)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.H2new.p, c.dflags)));
+    SPHG_L_DISPATCH(c, c.nf, SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.H2new.p, c.dflags))));
   if (c.nrigid)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.H2new.p, c.dflags)));
+    SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.H2new.p, c.dflags))));
   c.launches += 3;
 }
 
@@ -971,14 +973,13 @@ void launch_heat(Ctx& c) {
 void launch_diffusion(Ctx& c) {
   if (c.n == 0) return;
   const double t_new = c.t + c.P.dt;
-  constexpr int G = kGOther;
   k_dirichlet_c<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new, c.capturing ? c.dtime : nullptr);
   if (c.nf)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_diffusion<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.C2new.p, c.dflags)));
+    SPHG_L_DISPATCH(c, c.nf, SPHG_IMG_DISPATCH(c.P.img_mode, (k_diffusion<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.C2new.p, c.dflags))));
   if (c.nrigid)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_diffusion<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.C2new.p, c.dflags)));
+    SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, (k_diffusion<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.C2new.p, c.dflags))));
   k_copy_boundary_C<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.cur, c.n, c.C2new.p);
   std::swap(c.cur.C2, c.C2new);
   c.launches += 4;
@@ -986,27 +987,26 @@ void launch_diffusion(Ctx& c) {
 
 void launch_extrapolate(Ctx& c) {
   if (c.nw == 0) return;
-  constexpr int G = kGExtrap;
   if (c.P.single_eos)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_extrapolate<G, M, false><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw)));
+    SPHG_L_DISPATCH(c, c.nw, SPHG_IMG_DISPATCH(c.P.img_mode, (k_extrapolate<G, M, false><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw))));
   else
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_extrapolate<G, M, true><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw)));
+    SPHG_L_DISPATCH(c, c.nw, SPHG_IMG_DISPATCH(c.P.img_mode, (k_extrapolate<G, M, true><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw))));
   c.launches++;
 }
 
 template <bool kTvf, bool kSingleEta>
 static void launch_forces_fluid_t(Ctx& c) {
-  if (c.nf && c.fuse_heat) {  // conduction of the fluid particles in the same row walk (G = 4)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<4, M, kTvf, kSingleEta, true>
-                                     <<<blocks_for<4>(c.nf), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, c.H2new.p)));
+  if (c.nf && c.fuse_heat) {  // conduction of the fluid particles in the same row walk (k_heat's width)
+    SPHG_L_DISPATCH(c, c.nf, SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, true>
+                                     <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, c.H2new.p))));
     c.launches++;
     return;
   }
   if (c.nf)
-    SPHG_G_DISPATCH(c.group_forces,
+    SPHG_G_DISPATCH(c, c.group_forces, c.nf,
                     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta>
                                                      <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags))));
@@ -1016,11 +1016,11 @@ static void launch_forces_fluid_t(Ctx& c) {
 template <bool kTvf>
 static void launch_forces_rigid_t(Ctx& c) {
   if (c.nrigid && c.P.single_eta)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGRigid, M, kTvf, true><<<blocks_for<kGRigid>(c.nrigid), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags)));
+    SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<G, M, kTvf, true><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags))));
   else if (c.nrigid)
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<kGRigid, M, kTvf, false><<<blocks_for<kGRigid>(c.nrigid), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags)));
+    SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<G, M, kTvf, false><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
+                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags))));
   c.launches++;
 }
 

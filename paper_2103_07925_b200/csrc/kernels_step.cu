@@ -207,13 +207,17 @@ __device__ void inverse_apply(const double I[6], double3 t, double3& out) {
 }
 
 // one warp per body: compensated (f, tau, I) over the body-major rigid index
-__global__ void __launch_bounds__(128) k_body_reduce(const __grid_constant__ DevParams P, Particles D,
+// W = 1: a warp per body (many bodies).  W = 8: a block of 8 warps per body for small body tables
+// (C1: 4 bodies of ~280 particles), whose reduction is otherwise one serial chain per body; the 8
+// warp partials are merged in warp order in shared memory (compensated, deterministic).
+template <int W>
+__global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_body_reduce(const __grid_constant__ DevParams P, Particles D,
                                                       sphg_body* __restrict__ B, size_t nb,
                                                       const uint32_t* __restrict__ ridx,
                                                       const uint32_t* __restrict__ bstart,
                                                       const uint32_t* __restrict__ bend) {
-  const size_t k = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const size_t k = W == 1 ? ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5 : (size_t)blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = W == 1 ? 0 : (int)(threadIdx.x >> 5);
   if (k >= nb) return;
   sphg_body& b = B[k];
   if (!b.alive) return;
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(128) k_body_reduce(const __grid_constant__ Dev
 #pragma unroll
   for (int c = 0; c < 12; ++c) acc[c] = {0.0, 0.0};
   const uint32_t s0 = bstart[k], s1 = bend[k];
-  for (uint32_t s = s0 + lane; s < s1; s += 32) {
+  for (uint32_t s = s0 + warp * 32 + lane; s < s1; s += 32 * W) {
     const uint32_t r = ridx[s];
     const double3 rk = qrotate(q, ld3(D.X4.p[r]));
     const double4 f4 = D.F4.p[r];
@@ -240,9 +244,28 @@ __global__ void __launch_bounds__(128) k_body_reduce(const __grid_constant__ Dev
     acc[11].add(-m * rk.y * rk.z);
   }
   double v[12];
+  if (W == 1) {
 #pragma unroll
-  for (int c = 0; c < 12; ++c) v[c] = warp_merge(acc[c]).value();
-  if (lane != 0) return;
+    for (int c = 0; c < 12; ++c) v[c] = warp_merge(acc[c]).value();
+    if (lane != 0) return;
+  } else {
+    __shared__ double part[W][12][2];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+      const KSum m = warp_merge(acc[c]);
+      if (lane == 0) {
+        part[warp][c][0] = m.s;
+        part[warp][c][1] = m.c;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int c = 0; c < 12; ++c) {
+      KSum m = {part[0][c][0], part[0][c][1]};
+      for (int w = 1; w < W; ++w) m.merge(part[w][c][0], part[w][c][1]);
+      v[c] = m.value();
+    }
+  }
   for (int a = 0; a < 3; ++a) {
     b.force[a] = v[a];
     b.torque[a] = v[3 + a];
@@ -587,8 +610,12 @@ void launch_kick_drift(Ctx& c) {
 
 void launch_bodies(Ctx& c) {
   if (c.nb == 0) return;
-  k_body_reduce<<<grid_for(c.nb * 32, 128), 128, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.nb, c.ridx.p,
-                                                                 c.body_start.p, c.body_start.p + c.nb);
+  if (c.nb < 148)  // fewer bodies than SMs: a block of 8 warps per body
+    k_body_reduce<8><<<(unsigned)c.nb, 256, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.nb, c.ridx.p, c.body_start.p,
+                                                          c.body_start.p + c.nb);
+  else
+    k_body_reduce<1><<<grid_for(c.nb * 32, 128), 128, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.nb, c.ridx.p,
+                                                                    c.body_start.p, c.body_start.p + c.nb);
   c.launches++;
 }
 
