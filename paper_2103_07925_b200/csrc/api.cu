@@ -175,6 +175,8 @@ DevParams make_dev_params(const sphg_params& p) {
   P.rc = kSupport * P.h;
   P.rc2 = P.rc * P.rc;
   P.rc2_lo = P.rc2 * (1.0 - 2e-4);
+  P.rc2_ulp = P.rc2 * (1.0 - 1e-12);
+  P.dx2_hi = p.dx * p.dx * (1.0 + 1e-12);
   P.rc2_hi = P.rc2 * (1.0 + 1e-12);
   P.rv = P.rc + kSkin * P.h;
   P.rv2 = P.rv * P.rv;

@@ -41,7 +41,8 @@ struct DevParams {
   int32_t periodic[3];
   int32_t n_mat, n_sched, n_schedC, diffusion;
   double h, inv_h, rc, rc2, rv, rv2, sigma, sig_h, w0;
-  double rc2_lo, rc2_hi;  // rc^2 (1 - 2e-4), rc^2 (1 + 1e-12): the band where pair_q takes the pinned arithmetic
+  double dx2_hi;  // dx^2 (1 + 1e-12): contact candidates beyond it are apart without the exact test
+  double rc2_lo, rc2_ulp, rc2_hi;  // rc^2 (1 - 2e-4), rc^2 (1 - 1e-12), rc^2 (1 + 1e-12): pair_q's pinned bands
   double dx, dx3, dt, hdt;
   double kc, dc;
   double half_skin;
@@ -183,7 +184,8 @@ __device__ __forceinline__ double sqrt_and_rinv(double x, double& rinv) {
   return fma(0.5 * y, e, r0);
 }
 
-// q = r/h and 1/r of a pair with r^2 <= rc2_hi (r^2 as computed by the caller, FMA allowed).  dW ~ (3-q)^4
+// q = r/h and 1/r of a pair with r^2 <= rc2_hi (r^2 as computed by the caller, FMA allowed); pairs with
+// r^2 >= band_lo take the pinned path.  dW ~ (3-q)^4
 // and W ~ (3-q)^5 turn a last-bit difference of q into a relative error ~12/(3-q) times larger, which
 // decides the result where a particle's only support sits near r_c (a rigid particle three layers deep,
 // a wall behind an exact lattice; a lone Shepard weight that is tiny instead of 0).  So within a
@@ -191,8 +193,8 @@ __device__ __forceinline__ double sqrt_and_rinv(double x, double& rinv) {
 // q = r * (1/h) (kernel.hpp:30, 36); q = 3 is returned for pairs the exact r^2 puts outside r_c.
 // Callers treat q >= 3 as a zero kernel (kernel.hpp:49, 63).  Elsewhere the fast accurate root.
 template <class DP>
-__device__ __forceinline__ double pair_q(const DP& P, double3 d, double r2, double& rinv) {
-  if (r2 >= P.rc2_lo) {
+__device__ __forceinline__ double pair_q(const DP& P, double3 d, double r2, double& rinv, double band_lo) {
+  if (r2 >= band_lo) {
     const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(d.x, d.x), __dmul_rn(d.y, d.y)), __dmul_rn(d.z, d.z));
     const double r = __dsqrt_rn(r2e);
     rinv = 1.0 / r;
@@ -200,12 +202,14 @@ __device__ __forceinline__ double pair_q(const DP& P, double3 d, double r2, doub
   }
   return sqrt_and_rinv(r2 + 1e-300, rinv) * P.inv_h;
 }
-// Shepard weight shape W/sigma of a pair at offset d, or false outside r_c (see pair_q)
+// Shepard weight shape W/sigma of a pair at offset d, or false outside r_c (see pair_q).  A ratio
+// sum W f / sum W does not feel the weights' relative errors, only a lone weight that is 0 on one
+// side and tiny on the other: the pinned band is a few ulps wide here (rc2_ulp).
 template <class DP>
 __device__ __forceinline__ bool shepard_shape(const DP& P, double3 d, double r2, double& W) {
   if (r2 > P.rc2_hi) return false;
   double ri;
-  const double q = pair_q(P, d, r2, ri);
+  const double q = pair_q(P, d, r2, ri, P.rc2_ulp);
   W = q >= 3.0 ? 0.0 : shape_q(q);
   return true;
 }

@@ -38,8 +38,22 @@ __device__ __forceinline__ double3 ld3(const double4& v) { return make_double3(v
 // sector, so a gather costs one sector instead of two 16-byte requests.
 __device__ __forceinline__ double4 ldg4(const double4* p) {  // read-only (non-coherent) path
   double4 v;
+#ifdef SPHG_REC_EVICT_LAST
+  asm("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+#else
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+#endif
   return v;
+}
+// a Verlet row entry (rows stream from HBM once per pass)
+__device__ __forceinline__ uint32_t ldrow(const uint32_t* p) {
+#ifdef SPHG_ROW_EVICT_FIRST
+  uint32_t v;
+  asm("ld.global.nc.L1::evict_first.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
 }
 __device__ __forceinline__ double4 ld4(const double4* p) {  // coherent path (array written in-kernel)
   double4 v;
@@ -57,7 +71,7 @@ struct Row {
   const uint32_t* f;
   const uint32_t* b;
   int nf, no, n;
-  __device__ __forceinline__ uint32_t at(int k) const { return __ldg(f + k); }
+  __device__ __forceinline__ uint32_t at(int k) const { return ldrow(f + k); }
 };
 __device__ __forceinline__ Row row_of(const NbrList& L, uint32_t i) {
   const uint32_t c = L.cnt[i];
@@ -428,7 +442,7 @@ __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, 
   // pinned q near the cut-off: dW ~ (3-q)^4 amplifies errors of q there, and a rigid particle whose
   // only fluid neighbours sit there sees only those terms (coupling force)
   double rinv;
-  const double q = pair_q(P, d, r2, rinv);
+  const double q = pair_q(P, d, r2, rinv, P.rc2_lo);
   const double dW = q >= 3.0 ? 0.0 : P.sig_h * shape_deriv_q(q);
   const double fac = dW * rinv;  // gradW = fac * d
   const double3 gW = make_double3(fac * d.x, fac * d.y, fac * d.z);
@@ -535,9 +549,9 @@ __device__ __forceinline__ void fluid_row(const DevParams& P, const Particles& D
                                           const uint32_t* base, int n, int lane, double3& acc, double3& bg,
                                           bool& coincident, HeatSide* heat = nullptr) {
   int k = lane;
-  uint32_t e = k < n ? __ldg(base + k) : 0u;
+  uint32_t e = k < n ? ldrow(base + k) : 0u;
   for (; k < n; k += G) {
-    const uint32_t en = k + G < n ? __ldg(base + k + G) : 0u;
+    const uint32_t en = k + G < n ? ldrow(base + k + G) : 0u;
     const uint32_t j = nb_index<M>(e);
     const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
     double2 hj = double2{0.0, 0.0};
@@ -767,6 +781,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
       const uint32_t kindj = kind_of(D.kmd.p[j]);
       if (kindj != SPHG_BOUNDARY && D.group.p[j] == body) continue;
       const double3 d = pair_delta<M>(P, pr, ldpos(&D.G0.p[j]), e);  // r_r - r_j
+      if (d.x * d.x + d.y * d.y + d.z * d.z > P.dx2_hi) continue;  // clearly apart (most candidates)
       // the contact decision r < dx is discrete: the oracle's no-FMA r^2 and correctly rounded root
       const double rr = __dsqrt_rn(r2_exact(d));
       if (!(rr < P.dx)) continue;
