@@ -42,7 +42,7 @@ struct DevParams {
   int32_t n_mat, n_sched, n_schedC, diffusion;
   double h, inv_h, rc, rc2, rv, rv2, sigma, sig_h, w0;
   double dx2_hi;  // dx^2 (1 + 1e-12): contact candidates beyond it are apart without the exact test
-  double rc2_lo, rc2_ulp, rc2_hi;  // rc^2 (1 - 2e-4), rc^2 (1 - 1e-12), rc^2 (1 + 1e-12): pair_q's pinned bands
+  double rc2_lo, rc2_ulp, rc2_hi;  // rc^2 (1 - 2e-4), rc^2 (1 - 1e-12), rc^2 (1 + 1e-12): pinned_q's bands
   double dx, dx3, dt, hdt;
   double kc, dc;
   double half_skin;
@@ -184,32 +184,28 @@ __device__ __forceinline__ double sqrt_and_rinv(double x, double& rinv) {
   return fma(0.5 * y, e, r0);
 }
 
-// q = r/h and 1/r of a pair with r^2 <= rc2_hi (r^2 as computed by the caller, FMA allowed); pairs with
-// r^2 >= band_lo take the pinned path.  dW ~ (3-q)^4
-// and W ~ (3-q)^5 turn a last-bit difference of q into a relative error ~12/(3-q) times larger, which
-// decides the result where a particle's only support sits near r_c (a rigid particle three layers deep,
-// a wall behind an exact lattice; a lone Shepard weight that is tiny instead of 0).  So within a
-// relative 2e-4 of r_c^2 the pair takes the oracle's arithmetic: no-FMA r^2, correctly rounded root,
-// q = r * (1/h) (kernel.hpp:30, 36); q = 3 is returned for pairs the exact r^2 puts outside r_c.
-// Callers treat q >= 3 as a zero kernel (kernel.hpp:49, 63).  Elsewhere the fast accurate root.
-template <class DP>
-__device__ __forceinline__ double pair_q(const DP& P, double3 d, double r2, double& rinv, double band_lo) {
-  if (r2 >= band_lo) {
-    const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(d.x, d.x), __dmul_rn(d.y, d.y)), __dmul_rn(d.z, d.z));
-    const double r = __dsqrt_rn(r2e);
-    rinv = 1.0 / r;
-    return r2e > P.rc2 ? 3.0 : __dmul_rn(r, P.inv_h);
-  }
-  return sqrt_and_rinv(r2 + 1e-300, rinv) * P.inv_h;
+// Near the cut-off the kernel is ill-conditioned: dW ~ (3-q)^4 and W ~ (3-q)^5 turn a last-bit
+// difference of q into a relative error ~12/(3-q) larger.  That decides the result only where ALL of a
+// particle's pairs sit in a band just below r_c (one pair further inside dominates every band term
+// by (3-q)^4): a rigid particle three layers deep, a wall behind an exact lattice, a Shepard ratio
+// whose lone weight is tiny instead of 0.  For those particles the sums are redone with the oracle's
+// arithmetic: no-FMA r^2, correctly rounded root, q = r * (1/h) (kernel.hpp:30, 36), zero kernel for
+// q >= 3 (kernel.hpp:49, 63).  The hot kernels take the fast root and flag such particles; a second
+// launch of the same kernel (kPin) redoes only the flagged ones, so the pinned arithmetic costs the
+// hot loop no registers.
+__device__ __forceinline__ double pinned_q(double3 d, double rc2, double inv_h, double& rinv) {
+  const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(d.x, d.x), __dmul_rn(d.y, d.y)), __dmul_rn(d.z, d.z));
+  const double r = __dsqrt_rn(r2e);
+  rinv = 1.0 / r;
+  return r2e > rc2 ? 3.0 : __dmul_rn(r, inv_h);
 }
-// Shepard weight shape W/sigma of a pair at offset d, or false outside r_c (see pair_q).  A ratio
-// sum W f / sum W does not feel the weights' relative errors, only a lone weight that is 0 on one
-// side and tiny on the other: the pinned band is a few ulps wide here (rc2_ulp).
+// Shepard weight shape W/sigma of a pair at offset d, or false outside r_c (grid gather: not hot, so
+// pairs within a few ulps of r_c take pinned_q inline)
 template <class DP>
 __device__ __forceinline__ bool shepard_shape(const DP& P, double3 d, double r2, double& W) {
   if (r2 > P.rc2_hi) return false;
   double ri;
-  const double q = pair_q(P, d, r2, ri, P.rc2_ulp);
+  const double q = r2 >= P.rc2_ulp ? pinned_q(d, P.rc2, P.inv_h, ri) : sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h;
   W = q >= 3.0 ? 0.0 : shape_q(q);
   return true;
 }
@@ -268,6 +264,12 @@ __host__ __device__ __forceinline__ uint32_t pack_cnt(uint32_t nf, uint32_t no) 
 }
 
 // sum over a group of G consecutive lanes (every lane of the warp must call it)
+template <int G>
+__device__ __forceinline__ int gmax(int v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
 template <int G>
 __device__ __forceinline__ double gsum(double v) {
 #pragma unroll

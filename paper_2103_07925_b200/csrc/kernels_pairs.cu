@@ -335,21 +335,27 @@ __global__ void __launch_bounds__(kBlock) k_diffusion(const __grid_constant__ De
 // p_w = sum_f W (p_f + rho_f (g_f - a_w).(r_w - r_f)) / sum_f W;  u~_w = 2 u_w - sum_f W u_f / sum_f W;
 // rho_w = max(rho0, rho0 + p_w/c^2) of the dominant fluid material; V_w = rho0 dx^3 / rho_w  [P6][P7]
 // Only the fluid part of the row is visited.
-template <int G, int M, bool kMultiEos>
-__global__ void __launch_bounds__(kBlock) k_extrapolate(const __grid_constant__ DevParams P, Particles D, NbrList L,
+// kPin = false: the sums with the fast root; a particle whose fluid pairs all sit within a few ulps
+// below r_c^2 is flagged in pin[] and not written.  kPin = true: only the flagged particles, with
+// pinned_q (see common.cuh).
+template <int G, int M, bool kMultiEos, bool kPin>
+// (the fast variant fits 56 registers without spills: 9 blocks of 128 per SM)
+__global__ void __launch_bounds__(kBlock, kPin ? 1 : 9) k_extrapolate(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                          const sphg_body* __restrict__ B,
-                                                         const uint32_t* __restrict__ list, size_t nlist) {
+                                                         const uint32_t* __restrict__ list, size_t nlist,
+                                                         uint8_t* __restrict__ pin) {
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
-  const bool active = g < nlist;
-  const uint32_t w = active ? list[g] : 0u;
+  const uint32_t w = g < nlist ? list[g] : 0u;
+  const bool active = g < nlist && (!kPin || pin[w]);
   double3 uw = make_double3(0, 0, 0), aw = make_double3(0, 0, 0);
   double sw = 0.0, sp = 0.0;
   double3 su = make_double3(0, 0, 0);
   double smat[kMultiEos ? kMaxMat : 1];
 #pragma unroll
   for (int m = 0; m < (kMultiEos ? kMaxMat : 1); ++m) smat[m] = 0.0;
+  int st = 0;  // 2: a fluid pair clearly inside r_c, 1: only pairs within ulps below r_c^2, 0: none
   if (active) {
     const uint32_t kmd = D.kmd.p[w];
     if (kind_of(kmd) == SPHG_BOUNDARY && P.n_walls > 0) {  // prescribed wall motion [P20]
@@ -378,8 +384,18 @@ __global__ void __launch_bounds__(kBlock) k_extrapolate(const __grid_constant__ 
       // fluid records are only read here (the kernel writes wall/rigid records): read-only path
       const double4 g0 = ldg4(&D.G0.p[f]);
       const double3 d = pair_delta<M>(P, pw, ld3(g0), e);  // = the oracle's minimum-image r_w - r_f
-      double W;  // sigma cancels in the ratios; pinned arithmetic within ulps of r_c (empty support)
-      if (!shepard_shape(P, d, d.x * d.x + d.y * d.y + d.z * d.z, W)) continue;
+      const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
+      double W, ri;  // sigma cancels in the ratios
+      if (kPin) {
+        if (r2 > P.rc2_hi) continue;
+        const double q = pinned_q(d, P.rc2, P.inv_h, ri);
+        if (q >= 3.0) continue;
+        W = shape_q(q);
+      } else {
+        st = max(st, r2 < P.rc2_ulp ? 2 : (r2 <= P.rc2_hi ? 1 : 0));
+        if (r2 > P.rc2) continue;
+        W = shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);
+      }
       const double4 g1 = ldg4(&D.G1.p[f]);
       const double pf = __ldg(reinterpret_cast<const double*>(&D.G2.p[f]) + 3);
       const uint32_t mf = kMultiEos || !P.single_g ? mat_of(__ldg(&D.kmd.p[f])) : (uint32_t)P.default_fluid_mat;
@@ -401,6 +417,11 @@ __global__ void __launch_bounds__(kBlock) k_extrapolate(const __grid_constant__ 
   if (kMultiEos) {
 #pragma unroll
     for (int m = 0; m < kMaxMat; ++m) smat[m] = gsum<G>(smat[m]);
+  }
+  if (!kPin) {  // all fluid pairs within ulps below r_c: a lone weight decides "no support" -> pinned redo
+    const bool band = gmax<G>(st) == 1;
+    if (active && lane == 0) pin[w] = band;
+    if (band) return;
   }
   if (!active || lane != 0) return;
   int m = P.default_fluid_mat;
@@ -436,13 +457,10 @@ struct PairSide {
 };
 
 // kJFluid = false: j is a wall/rigid particle: A_j = 0 and eta_j = eta_i [P5][P7]
+// q, rinv: the pair's q = r/h and 1/r (fast root, or pinned_q for flagged particles)
 template <bool kTvf, bool kSingleEta, bool kJFluid>
-__device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, double3 d, double r2,
+__device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, double3 d, double q, double rinv,
                                           const DevParams& P, double3& acc, double3& bg) {
-  // pinned q near the cut-off: dW ~ (3-q)^4 amplifies errors of q there, and a rigid particle whose
-  // only fluid neighbours sit there sees only those terms (coupling force)
-  double rinv;
-  const double q = pair_q(P, d, r2, rinv, P.rc2_lo);
   const double dW = q >= 3.0 ? 0.0 : P.sig_h * shape_deriv_q(q);
   const double fac = dW * rinv;  // gradW = fac * d
   const double3 gW = make_double3(fac * d.x, fac * d.y, fac * d.z);
@@ -715,16 +733,19 @@ __global__ void k_fill_aos(Particles D, size_t n, double4* __restrict__ aos) {
 
 // f_r = sum_i -m_i a_ir over the fluid part of the row (a_ir from the fluid's view)
 //     + contact over the rigid/boundary part
-template <int G, int M, bool kTvf, bool kSingleEta>
+// kPin = false: the fast root; a particle whose fluid pairs all sit within 2e-4 below r_c^2 is flagged
+// in pin[] and not written.  kPin = true: only the flagged particles, coupling with pinned_q.
+template <int G, int M, bool kTvf, bool kSingleEta, bool kPin>
 __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                           const uint32_t* __restrict__ list, size_t nlist,
                                                           const uint32_t* __restrict__ ncon,
-                                                          DevFlags* __restrict__ fl) {
+                                                          DevFlags* __restrict__ fl, uint8_t* __restrict__ pin) {
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
-  const bool active = g < nlist;
-  const uint32_t r = active ? list[g] : 0u;
+  const uint32_t r = g < nlist ? list[g] : 0u;
+  const bool active = g < nlist && (!kPin || pin[r]);
+  int st = 0;  // 2: a fluid pair clearly inside r_c, 1: only pairs in the 2e-4 band below r_c^2, 0: none
   double3 f = make_double3(0, 0, 0);
   bool coincident = false;
   if (active) {
@@ -751,10 +772,19 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
       const double3 dd = pair_delta<M>(P, pr, ld3(h0), e);
       const double3 d = make_double3(-dd.x, -dd.y, -dd.z);
       const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
-      if (r2 > P.rc2_hi) continue;  // pair_term settles the band around r_c with the exact r^2
-      if (r2 == 0.0) {
-        coincident = true;
-        continue;
+      double q, rinv;
+      if (kPin) {
+        if (r2 > P.rc2_hi) continue;
+        q = pinned_q(d, P.rc2, P.inv_h, rinv);
+        if (q >= 3.0) continue;
+      } else {
+        st = max(st, r2 < P.rc2_lo ? 2 : (r2 <= P.rc2_hi ? 1 : 0));
+        if (r2 > P.rc2) continue;
+        if (r2 == 0.0) {
+          coincident = true;
+          continue;
+        }
+        q = sqrt_and_rinv(r2, rinv) * P.inv_h;
       }
       PairSide J;
       J.u = ld3(h1);
@@ -766,7 +796,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
       J.eta = kSingleEta ? P.mat[P.default_fluid_mat].eta : P.mat[mat_of(__ldg(&D.kmd.p[j]))].eta;
       R.eta = J.eta;  // eta_w := eta_i
       double3 a = make_double3(0, 0, 0), bgd = make_double3(0, 0, 0);
-      pair_term<kTvf, true, false>(J, R, d, r2, P, a, bgd);  // j plays i; the rigid side has A = 0
+      pair_term<kTvf, true, false>(J, R, d, q, rinv, P, a, bgd);  // j plays i; the rigid side has A = 0
       // f_ri = -m_i a_ir = -(V2 term): pair_term accumulates V2*term (a_ir = V2/m_i * term)
       f.x -= a.x;
       f.y -= a.y;
@@ -802,6 +832,11 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
   f.x = gsum<G>(f.x);
   f.y = gsum<G>(f.y);
   f.z = gsum<G>(f.z);
+  if (!kPin) {  // every fluid pair in the band below r_c: their last bits decide -> pinned redo
+    const bool band = gmax<G>(st) == 1;
+    if (active && lane == 0) pin[r] = band;
+    if (band) return;
+  }
   if (!active) return;
   if (coincident) {
     atomicOr(&fl->err, kErrCoincident);
@@ -1000,15 +1035,23 @@ void launch_diffusion(Ctx& c) {
   c.launches += 4;
 }
 
+// fast pass over the list, then the pinned redo of the particles it flagged (a launch whose groups
+// exit at once unless pin[] is set; see common.cuh pinned_q)
+template <bool kMultiEos>
+static void launch_extrapolate_t(Ctx& c) {
+  SPHG_L_DISPATCH(c, c.nw, SPHG_IMG_DISPATCH(c.P.img_mode, ({
+    k_extrapolate<G, M, kMultiEos, false><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
+        c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw, c.pin.p);
+    k_extrapolate<G, M, kMultiEos, true><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
+        c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw, c.pin.p);
+  })));
+  c.launches += 2;
+}
+
 void launch_extrapolate(Ctx& c) {
   if (c.nw == 0) return;
-  if (c.P.single_eos)
-    SPHG_L_DISPATCH(c, c.nw, SPHG_IMG_DISPATCH(c.P.img_mode, (k_extrapolate<G, M, false><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw))));
-  else
-    SPHG_L_DISPATCH(c, c.nw, SPHG_IMG_DISPATCH(c.P.img_mode, (k_extrapolate<G, M, true><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw))));
-  c.launches++;
+  if (c.P.single_eos) launch_extrapolate_t<false>(c);
+  else launch_extrapolate_t<true>(c);
 }
 
 template <bool kTvf, bool kSingleEta>
@@ -1030,13 +1073,18 @@ static void launch_forces_fluid_t(Ctx& c) {
 
 template <bool kTvf>
 static void launch_forces_rigid_t(Ctx& c) {
-  if (c.nrigid && c.P.single_eta)
-    SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<G, M, kTvf, true><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags))));
-  else if (c.nrigid)
-    SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_rigid<G, M, kTvf, false><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags))));
-  c.launches++;
+  if (!c.nrigid) return;
+#define SPHG_RIGID_PAIR(SE)                                                                                 \
+  SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, ({                                          \
+    k_forces_rigid<G, M, kTvf, SE, false><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(                \
+        c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags, c.pin.p);                                \
+    k_forces_rigid<G, M, kTvf, SE, true><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(                 \
+        c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags, c.pin.p);                                \
+  })))
+  if (c.P.single_eta) SPHG_RIGID_PAIR(true);
+  else SPHG_RIGID_PAIR(false);
+#undef SPHG_RIGID_PAIR
+  c.launches += 2;
 }
 
 void launch_forces_fluid(Ctx& c) {
