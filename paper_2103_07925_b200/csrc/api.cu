@@ -928,7 +928,8 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     c.cur.alloc(na, c.P.diffusion != 0);
     c.alt.alloc(na, c.P.diffusion != 0);
     c.H2new.alloc(na);
-    c.pin.alloc(na);
+    c.pin_list.alloc(na);
+    if (!c.pin_any) SPHG_CUDA_CHECK(cudaMalloc(&c.pin_any, sizeof(uint32_t)));
     if (c.P.diffusion) c.C2new.alloc(na);
     if (c.P.heat_source) {
       c.hsrc.alloc(na);
@@ -1415,7 +1416,8 @@ void sphg_destroy(sphg_ctx* h) {
   destroy_graphs(c);
   if (c.dtime) cudaFree(c.dtime);
   if (c.htime) cudaFreeHost(c.htime);
-  c.cur.free(); c.alt.free(); c.H2new.free(); c.C2new.free(); c.hsrc.free(); c.pin.free(); c.bodies.free();
+  c.cur.free(); c.alt.free(); c.H2new.free(); c.C2new.free(); c.hsrc.free(); c.pin_list.free();
+  if (c.pin_any) cudaFree(c.pin_any); c.bodies.free();
   if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
   if (c.dl_ev) cudaEventDestroy(c.dl_ev);
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();

@@ -88,7 +88,8 @@ struct Ctx {
   DBuf<double2> H2new;     // heat double buffer
   DBuf<double2> C2new;     // concentration double buffer
   DBuf<double> hsrc;       // surface heat flux source rate per particle [P21] (params.heat_source)
-  DBuf<uint8_t> pin;       // particles whose rigid / wall sums take the pinned redo (common.cuh pinned_q)
+  DBuf<uint32_t> pin_list;  // particles whose rigid / wall sums take the pinned redo (common.cuh pinned_q)
+  uint32_t* pin_any = nullptr;  // device: their count
   DBuf<sphg_body> bodies;
   size_t bodies_cap = 0;
   // rebuild scratch

@@ -336,19 +336,25 @@ __global__ void __launch_bounds__(kBlock) k_diffusion(const __grid_constant__ De
 // rho_w = max(rho0, rho0 + p_w/c^2) of the dominant fluid material; V_w = rho0 dx^3 / rho_w  [P6][P7]
 // Only the fluid part of the row is visited.
 // kPin = false: the sums with the fast root; a particle whose fluid pairs all sit within a few ulps
-// below r_c^2 is flagged in pin[] and not written.  kPin = true: only the flagged particles, with
+// below r_c^2 is appended to pin_list and not written.  kPin = true: only those particles, with
 // pinned_q (see common.cuh).
 template <int G, int M, bool kMultiEos, bool kPin>
 // (the fast variant fits 56 registers without spills: 9 blocks of 128 per SM)
 __global__ void __launch_bounds__(kBlock, kPin ? 1 : 9) k_extrapolate(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                          const sphg_body* __restrict__ B,
                                                          const uint32_t* __restrict__ list, size_t nlist,
-                                                         uint8_t* __restrict__ pin) {
+                                                         uint32_t* __restrict__ pin_list, uint32_t* __restrict__ any) {
+  // kPin: the flagged particles, compacted by the fast pass into pin_list[0 .. *any)
+  if (kPin) {
+    nlist = *any;
+    list = pin_list;
+    if ((size_t)blockIdx.x * (kBlock / G) >= nlist) return;  // the common case: nothing flagged
+  }
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
   const uint32_t w = g < nlist ? list[g] : 0u;
-  const bool active = g < nlist && (!kPin || pin[w]);
+  const bool active = g < nlist;
   double3 uw = make_double3(0, 0, 0), aw = make_double3(0, 0, 0);
   double sw = 0.0, sp = 0.0;
   double3 su = make_double3(0, 0, 0);
@@ -420,7 +426,7 @@ __global__ void __launch_bounds__(kBlock, kPin ? 1 : 9) k_extrapolate(const __gr
   }
   if (!kPin) {  // all fluid pairs within ulps below r_c: a lone weight decides "no support" -> pinned redo
     const bool band = gmax<G>(st) == 1;
-    if (active && lane == 0) pin[w] = band;
+    if (band && active && lane == 0) pin_list[atomicAdd(any, 1u)] = w;
     if (band) return;
   }
   if (!active || lane != 0) return;
@@ -733,18 +739,25 @@ __global__ void k_fill_aos(Particles D, size_t n, double4* __restrict__ aos) {
 
 // f_r = sum_i -m_i a_ir over the fluid part of the row (a_ir from the fluid's view)
 //     + contact over the rigid/boundary part
-// kPin = false: the fast root; a particle whose fluid pairs all sit within 2e-4 below r_c^2 is flagged
-// in pin[] and not written.  kPin = true: only the flagged particles, coupling with pinned_q.
+// kPin = false: the fast root; a particle whose fluid pairs all sit within 2e-4 below r_c^2 is appended
+// to pin_list and not written.  kPin = true: only those particles, coupling with pinned_q.
 template <int G, int M, bool kTvf, bool kSingleEta, bool kPin>
 __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                           const uint32_t* __restrict__ list, size_t nlist,
                                                           const uint32_t* __restrict__ ncon,
-                                                          DevFlags* __restrict__ fl, uint8_t* __restrict__ pin) {
+                                                          DevFlags* __restrict__ fl, uint32_t* __restrict__ pin_list,
+                                                          uint32_t* __restrict__ any) {
+  // kPin: the flagged particles, compacted by the fast pass into pin_list[0 .. *any)
+  if (kPin) {
+    nlist = *any;
+    list = pin_list;
+    if ((size_t)blockIdx.x * (kBlock / G) >= nlist) return;  // the common case: nothing flagged
+  }
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
   const uint32_t r = g < nlist ? list[g] : 0u;
-  const bool active = g < nlist && (!kPin || pin[r]);
+  const bool active = g < nlist;
   int st = 0;  // 2: a fluid pair clearly inside r_c, 1: only pairs in the 2e-4 band below r_c^2, 0: none
   double3 f = make_double3(0, 0, 0);
   bool coincident = false;
@@ -834,7 +847,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
   f.z = gsum<G>(f.z);
   if (!kPin) {  // every fluid pair in the band below r_c: their last bits decide -> pinned redo
     const bool band = gmax<G>(st) == 1;
-    if (active && lane == 0) pin[r] = band;
+    if (band && active && lane == 0) pin_list[atomicAdd(any, 1u)] = r;
     if (band) return;
   }
   if (!active) return;
@@ -1035,15 +1048,16 @@ void launch_diffusion(Ctx& c) {
   c.launches += 4;
 }
 
-// fast pass over the list, then the pinned redo of the particles it flagged (a launch whose groups
-// exit at once unless pin[] is set; see common.cuh pinned_q)
+// fast pass over the list, then the pinned redo of the particles it appended to pin_list (a launch
+// whose blocks past the flagged count exit at once; see common.cuh pinned_q)
 template <bool kMultiEos>
 static void launch_extrapolate_t(Ctx& c) {
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.pin_any, 0, sizeof(uint32_t), c.stream));
   SPHG_L_DISPATCH(c, c.nw, SPHG_IMG_DISPATCH(c.P.img_mode, ({
     k_extrapolate<G, M, kMultiEos, false><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
-        c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw, c.pin.p);
+        c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw, c.pin_list.p, c.pin_any);
     k_extrapolate<G, M, kMultiEos, true><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
-        c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw, c.pin.p);
+        c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw, c.pin_list.p, c.pin_any);
   })));
   c.launches += 2;
 }
@@ -1074,12 +1088,13 @@ static void launch_forces_fluid_t(Ctx& c) {
 template <bool kTvf>
 static void launch_forces_rigid_t(Ctx& c) {
   if (!c.nrigid) return;
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.pin_any, 0, sizeof(uint32_t), c.stream));
 #define SPHG_RIGID_PAIR(SE)                                                                                 \
   SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, ({                                          \
     k_forces_rigid<G, M, kTvf, SE, false><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(                \
-        c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags, c.pin.p);                                \
+        c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags, c.pin_list.p, c.pin_any);                     \
     k_forces_rigid<G, M, kTvf, SE, true><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(                 \
-        c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags, c.pin.p);                                \
+        c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags, c.pin_list.p, c.pin_any);                     \
   })))
   if (c.P.single_eta) SPHG_RIGID_PAIR(true);
   else SPHG_RIGID_PAIR(false);
