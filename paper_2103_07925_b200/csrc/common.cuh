@@ -184,6 +184,18 @@ __device__ __forceinline__ double sqrt_and_rinv(double x, double& rinv) {
   return fma(0.5 * y, e, r0);
 }
 
+// q = r/h and 1/r of a pair with offset d and r^2 = d.d (r2, FMA allowed) inside r_c.  SPHG_EXACT_Q:
+// the oracle's q bit for bit (no-FMA r^2, correctly rounded root, q = r * (1/h)) in every pair kernel.
+__device__ __forceinline__ double pair_qr(double3 d, double r2, double inv_h, double& rinv) {
+#ifdef SPHG_EXACT_Q
+  const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(d.x, d.x), __dmul_rn(d.y, d.y)), __dmul_rn(d.z, d.z));
+  rinv = rsqrt_fast(r2e);
+  return __dmul_rn(__dsqrt_rn(r2e), inv_h);
+#else
+  return sqrt_and_rinv(r2 + 1e-300, rinv) * inv_h;
+#endif
+}
+
 // Near the cut-off the kernel is ill-conditioned: dW ~ (3-q)^4 and W ~ (3-q)^5 turn a last-bit
 // difference of q into a relative error ~12/(3-q) larger.  That decides the result only where ALL of a
 // particle's pairs sit in a band just below r_c (one pair further inside dominates every band term

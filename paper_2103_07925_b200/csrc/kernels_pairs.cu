@@ -94,7 +94,7 @@ __device__ __forceinline__ double density_term(const DevParams& P, double3 pi, d
   // accurate r: p = c^2 (rho - rho0) cancels, so the pressure (and every force term built on it)
   // needs rho to ~1e-15, not just 1e-10; + tiny: coincident -> W(0)
   double ri;
-  return shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);
+  return shape_q(pair_qr(d, r2, P.inv_h, ri));
 }
 
 // rho_i = m_i sigma (66 + sum_j shape(r_ij/h)); p_i = c^2 (rho_i - rho0); V_i = m_i/rho_i
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevPara
         kt = 4.0 * Ma.kappa * kb / ks;
       }
       double rinv;
-      const double dW = P.sig_h * shape_deriv_q(sqrt_and_rinv(r2, rinv) * P.inv_h);
+      const double dW = P.sig_h * shape_deriv_q(pair_qr(d, r2, P.inv_h, rinv));
       s += hj.y * kt * ((hi.x - hj.x) * rinv) * dW;
     }
   }
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kBlock) k_diffusion(const __grid_constant__ De
       if (ds == 0.0) continue;
       const double dt_ = 4.0 * Da * Db / ds;
       double rinv;
-      const double dW = P.sig_h * shape_deriv_q(sqrt_and_rinv(r2, rinv) * P.inv_h);
+      const double dW = P.sig_h * shape_deriv_q(pair_qr(d, r2, P.inv_h, rinv));
       s += cj.y * dt_ * ((ci.x - cj.x) * rinv) * dW;
     }
   }
@@ -335,8 +335,9 @@ __global__ void __launch_bounds__(kBlock) k_diffusion(const __grid_constant__ De
 // p_w = sum_f W (p_f + rho_f (g_f - a_w).(r_w - r_f)) / sum_f W;  u~_w = 2 u_w - sum_f W u_f / sum_f W;
 // rho_w = max(rho0, rho0 + p_w/c^2) of the dominant fluid material; V_w = rho0 dx^3 / rho_w  [P6][P7]
 // Only the fluid part of the row is visited.
-// kPin = false: the sums with the fast root; a particle whose fluid pairs all sit within a few ulps
-// below r_c^2 is appended to pin_list and not written.  kPin = true: only those particles, with
+// kPin = false: the sums with the fast root; a particle whose fluid pairs all sit within 2e-4 below
+// r_c^2 is appended to pin_list and not written (there the weights' relative errors ~15 eps/(3-q)
+// reach the ratios; a lone weight can even be 0 on one side and tiny on the other).  kPin = true: only those particles, with
 // pinned_q (see common.cuh).
 template <int G, int M, bool kMultiEos, bool kPin>
 // (the fast variant fits 56 registers without spills: 9 blocks of 128 per SM)
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(kBlock, kPin ? 1 : 9) k_extrapolate(const __gr
   double smat[kMultiEos ? kMaxMat : 1];
 #pragma unroll
   for (int m = 0; m < (kMultiEos ? kMaxMat : 1); ++m) smat[m] = 0.0;
-  int st = 0;  // 2: a fluid pair clearly inside r_c, 1: only pairs within ulps below r_c^2, 0: none
+  int st = 0;  // 2: a fluid pair clearly inside r_c, 1: only pairs in the 2e-4 band below r_c^2, 0: none
   if (active) {
     const uint32_t kmd = D.kmd.p[w];
     if (kind_of(kmd) == SPHG_BOUNDARY && P.n_walls > 0) {  // prescribed wall motion [P20]
@@ -398,9 +399,9 @@ __global__ void __launch_bounds__(kBlock, kPin ? 1 : 9) k_extrapolate(const __gr
         if (q >= 3.0) continue;
         W = shape_q(q);
       } else {
-        st = max(st, r2 < P.rc2_ulp ? 2 : (r2 <= P.rc2_hi ? 1 : 0));
+        st = max(st, r2 < P.rc2_lo ? 2 : (r2 <= P.rc2_hi ? 1 : 0));
         if (r2 > P.rc2) continue;
-        W = shape_q(sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h);
+        W = shape_q(pair_qr(d, r2, P.inv_h, ri));
       }
       const double4 g1 = ldg4(&D.G1.p[f]);
       const double pf = __ldg(reinterpret_cast<const double*>(&D.G2.p[f]) + 3);
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(kBlock, kPin ? 1 : 9) k_extrapolate(const __gr
 #pragma unroll
     for (int m = 0; m < kMaxMat; ++m) smat[m] = gsum<G>(smat[m]);
   }
-  if (!kPin) {  // all fluid pairs within ulps below r_c: a lone weight decides "no support" -> pinned redo
+  if (!kPin) {  // all fluid pairs in the band below r_c: the weights' last bits decide -> pinned redo
     const bool band = gmax<G>(st) == 1;
     if (band && active && lane == 0) pin_list[atomicAdd(any, 1u)] = w;
     if (band) return;
@@ -525,7 +526,7 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
     return;
   }
   double rinv;
-  const double dW = P.sig_h * shape_deriv_q(sqrt_and_rinv(r2, rinv) * P.inv_h);
+  const double dW = P.sig_h * shape_deriv_q(pair_qr(d, r2, P.inv_h, rinv));
   if (kHeat && hj.y != 0.0) {  // same term, same order as k_heat (non-Dirichlet walls: V_heat = 0)
     double kt;
     bool conduct = true;
@@ -797,7 +798,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
           coincident = true;
           continue;
         }
-        q = sqrt_and_rinv(r2, rinv) * P.inv_h;
+        q = pair_qr(d, r2, P.inv_h, rinv);
       }
       PairSide J;
       J.u = ld3(h1);
