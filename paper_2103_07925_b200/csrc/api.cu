@@ -296,6 +296,24 @@ void timed(Ctx& c, int stage, void (*fn)(Ctx&)) {
 }
 
 void timed_forces(Ctx& c) {  // stage 4 = 10 (fluid kernel) + 11 (rigid kernel)
+  if (!c.timing && c.concurrent_rigid && c.nrigid) {
+    // the rigid coupling / contact pass reads only the state the extrapolation left: it runs on a second
+    // stream beside the fluid force pass (joined before the body reduction)
+    if (!c.side_stream) {
+      SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.side_stream, cudaStreamNonBlocking));
+      SPHG_CUDA_CHECK(cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming));
+      SPHG_CUDA_CHECK(cudaEventCreateWithFlags(&c.join_ev, cudaEventDisableTiming));
+    }
+    SPHG_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
+    SPHG_CUDA_CHECK(cudaStreamWaitEvent(c.side_stream, c.fork_ev, 0));
+    std::swap(c.stream, c.side_stream);
+    launch_forces_rigid(c);
+    std::swap(c.stream, c.side_stream);
+    SPHG_CUDA_CHECK(cudaEventRecord(c.join_ev, c.side_stream));
+    launch_forces_fluid(c);
+    SPHG_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.join_ev, 0));
+    return;
+  }
   const double before10 = c.stage_ms[10], before11 = c.stage_ms[11];
   timed(c, 10, launch_forces_fluid);
   timed(c, 11, launch_forces_rigid);
@@ -877,6 +895,7 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
   if (const char* e = std::getenv("SPHG_GROUP_FORCES")) c.group_forces = std::atoi(e);
   if (const char* e = std::getenv("SPHG_CELL_BUILD")) c.cell_build = std::atoi(e) != 0;
   if (const char* e = std::getenv("SPHG_GRAPHS")) c.use_graphs = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SPHG_CONCURRENT_RIGID")) c.concurrent_rigid = std::atoi(e) != 0;
   try {
     SPHG_CUDA_CHECK(cudaSetDevice(device));
     int sms = 148;
@@ -1419,6 +1438,9 @@ void sphg_destroy(sphg_ctx* h) {
   c.cur.free(); c.alt.free(); c.H2new.free(); c.C2new.free(); c.hsrc.free(); c.pin_list.free();
   if (c.pin_any) cudaFree(c.pin_any); c.bodies.free();
   if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+  if (c.side_stream) cudaStreamDestroy(c.side_stream);
+  if (c.fork_ev) cudaEventDestroy(c.fork_ev);
+  if (c.join_ev) cudaEventDestroy(c.join_ev);
   if (c.dl_ev) cudaEventDestroy(c.dl_ev);
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
   c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();

@@ -171,6 +171,10 @@ struct Ctx {
   // sphg_step_download: enqueued after the wall extrapolation of the last step (eager chain), packs the
   // fields that are final by then so their D2H copies on copy_stream overlap the force kernels
   std::function<void(Ctx&)> pre_forces;
+  // rigid force pass on a second stream beside the fluid one (SPHG_CONCURRENT_RIGID=0 serialises)
+  bool concurrent_rigid = true;
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t dl_ev = nullptr;
 };
