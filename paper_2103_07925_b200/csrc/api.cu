@@ -496,12 +496,11 @@ void run_graph(Ctx& c, int chain, void (*body)(Ctx&)) {
 void chain_kick(Ctx& c) {  // (A): everything up to the per-step flag readback
   reset_step_flags(c);
   timed(c, SPHG_STAGE_KICK_DRIFT, kick_all);
+  launch_step_tail(c);
   SPHG_CUDA_CHECK(cudaMemcpyAsync(c.hflags, c.dflags, sizeof(DevFlags), cudaMemcpyDeviceToHost, c.stream));
 }
 
-void chain_forces(Ctx& c) {  // (B): density .. final kick
-  if (c.capturing && (c.P.thermal || c.P.diffusion))
-    SPHG_CUDA_CHECK(cudaMemcpyAsync(c.dtime, c.htime, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+void chain_forces(Ctx& c) {  // (B): density .. final kick (captured kernels read t^{n+1} from dtime)
   timed(c, SPHG_STAGE_DENSITY, launch_density);
   if (c.P.thermal) timed(c, SPHG_STAGE_HEAT, c.fuse_heat ? launch_heat_begin : launch_heat);
   if (c.P.diffusion) timed(c, SPHG_STAGE_HEAT, launch_diffusion);
@@ -520,29 +519,51 @@ int one_step(sphg_ctx* h) {
                 "ghost particles present: drive multi-rank steps through the decomposition layer (parallel.py)");
   const bool graphs = graphs_allowed(c);
   if (graphs) {
-    if (!c.dtime) {
-      SPHG_CUDA_CHECK(cudaMalloc(&c.dtime, sizeof(double)));
-      SPHG_CUDA_CHECK(cudaMallocHost(&c.htime, sizeof(double)));
+    if (!c.dtime) {  // [0] the force chain's time, [1] the clock (see k_step_tail)
+      SPHG_CUDA_CHECK(cudaMalloc(&c.dtime, 2 * sizeof(double)));
+      SPHG_CUDA_CHECK(cudaMallocHost(&c.htime, 2 * sizeof(double)));
+      c.htime[0] = c.htime[1] = c.t;
+      SPHG_CUDA_CHECK(cudaMemcpyAsync(c.dtime, c.htime, 2 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
     }
     run_graph(c, 0, chain_kick);
   } else {
     chain_kick(c);
   }
+  SPHG_CUDA_CHECK(cudaEventRecord(c.kick_ev, c.stream));
   c.t += c.P.dt;
   h->mid_step = true;
-  int rc = check_flags(h, true, false);  // one 48-byte readback per step: Verlet trigger + escape check
-  if (rc) return rc;
-  if (!c.built || c.max_disp > c.P.half_skin) timed(c, SPHG_STAGE_REBUILD, launch_rebuild);
   // fold fluid conduction into the forces pass (same terms, same order; heat does not feed the
   // extrapolation or the forces, so moving it after them changes nothing)
-  c.fuse_heat = c.P.thermal && !c.timing;
-  if (graphs && !c.pre_forces) {
-    *c.htime = c.t + c.P.dt;  // read by the memcpy node; the previous replay finished (flag sync above)
-    run_graph(c, 1, chain_forces);
-  } else {
-    chain_forces(c);
+  auto forces = [&]() {
+    c.fuse_heat = c.P.thermal && !c.timing;
+    if (graphs && !c.pre_forces) run_graph(c, 1, chain_forces);
+    else chain_forces(c);
+    c.fuse_heat = false;
+  };
+  // speculative: queue the force chain before reading the kick chain's flags, so the GPU never waits
+  // for the host's one 48-byte readback per step; dskip voids the queued chain when the step needs a
+  // rebuild or hit an error, and the host state it changed is restored before the redo
+  const bool spec = c.speculate && c.built && c.P.transitions == 0 && !c.timing && !c.pre_forces;
+  const Particles cur0 = c.cur;
+  const DBuf<double2> h2n0 = c.H2new, c2n0 = c.C2new;
+  const bool fp0 = c.final_pending;
+  const int64_t l0 = c.launches;
+  if (spec) forces();
+  SPHG_CUDA_CHECK(cudaEventSynchronize(c.kick_ev));
+  int rc = check_flags(h, false, false);  // Verlet trigger + escape check
+  const bool rebuild = !c.built || c.max_disp > c.P.half_skin;
+  if (spec && (rc || rebuild)) {  // the queued chain voided itself: restore its host-side state
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    c.cur = cur0;
+    c.H2new = h2n0;
+    c.C2new = c2n0;
+    c.final_pending = fp0;
+    c.launches = l0;
   }
-  c.fuse_heat = false;
+  if (rc || rebuild) SPHG_CUDA_CHECK(cudaMemsetAsync(c.dskip, 0, sizeof(uint32_t), c.stream));
+  if (rc) return rc;
+  if (rebuild) timed(c, SPHG_STAGE_REBUILD, launch_rebuild);
+  if (!spec || rebuild) forces();
   h->mid_step = false;
   if (c.P.transitions != 0) {
     rc = launch_transitions(c);
@@ -896,6 +917,7 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
   if (const char* e = std::getenv("SPHG_CELL_BUILD")) c.cell_build = std::atoi(e) != 0;
   if (const char* e = std::getenv("SPHG_GRAPHS")) c.use_graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("SPHG_CONCURRENT_RIGID")) c.concurrent_rigid = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SPHG_SPECULATE")) c.speculate = std::atoi(e) != 0;
   try {
     SPHG_CUDA_CHECK(cudaSetDevice(device));
     int sms = 148;
@@ -908,6 +930,10 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
     SPHG_CUDA_CHECK(cudaMemset(&c.dflags->err_gid, 0xff, 2 * sizeof(uint32_t)));
     SPHG_CUDA_CHECK(cudaMallocHost(&c.hflags, sizeof(DevFlags)));
     std::memset(c.hflags, 0, sizeof(DevFlags));
+    SPHG_CUDA_CHECK(cudaMalloc(&c.dskip, sizeof(uint32_t)));
+    SPHG_CUDA_CHECK(cudaMemset(c.dskip, 0, sizeof(uint32_t)));
+    c.P.skip = c.dskip;
+    SPHG_CUDA_CHECK(cudaEventCreateWithFlags(&c.kick_ev, cudaEventDisableTiming));
     SPHG_CUDA_CHECK(cudaEventCreate(&c.ev[0]));
     SPHG_CUDA_CHECK(cudaEventCreate(&c.ev[1]));
   } catch (const CudaError& e) {
@@ -1065,6 +1091,10 @@ int run_steps(sphg_ctx* h, int nsteps, sphg_soa* out) {
   if (!c.step_ev[0]) {
     SPHG_CUDA_CHECK(cudaEventCreate(&c.step_ev[0]));
     SPHG_CUDA_CHECK(cudaEventCreate(&c.step_ev[1]));
+  }
+  if (c.dtime) {  // the captured force chain reads its time from the device clock: resync it with c.t
+    c.htime[0] = c.htime[1] = c.t;
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(c.dtime, c.htime, 2 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
   }
   const bool overlap = out && nsteps > 0 && c.P.transitions == 0 && !c.timing;
   DlPlan pl;
@@ -1438,6 +1468,8 @@ void sphg_destroy(sphg_ctx* h) {
   c.cur.free(); c.alt.free(); c.H2new.free(); c.C2new.free(); c.hsrc.free(); c.pin_list.free();
   if (c.pin_any) cudaFree(c.pin_any); c.bodies.free();
   if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+  if (c.dskip) cudaFree(c.dskip);
+  if (c.kick_ev) cudaEventDestroy(c.kick_ev);
   if (c.side_stream) cudaStreamDestroy(c.side_stream);
   if (c.fork_ev) cudaEventDestroy(c.fork_ev);
   if (c.join_ev) cudaEventDestroy(c.join_ev);

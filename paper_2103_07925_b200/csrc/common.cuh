@@ -66,7 +66,15 @@ struct DevParams {
   double hs_origin[2], hs_vel[2];
   double hs_dz, hs_lat2;           // dx/2, (3 dx/4)^2
   double* hsrc;
+  // speculative step (api.cu one_step): set on the device by the tail of the kick chain when the step
+  // needs a Verlet rebuild (or hit an error); every kernel of the force chain then returns at once
+  const uint32_t* skip;
 };
+#define SPHG_SKIP_IF_FLAGGED(P) \
+  do {                          \
+    if ((P).skip && *(P).skip)  \
+      return;                   \
+  } while (0)
 
 // ------------------------------------------------------ brick traversal
 // Work order of the cell-structured kernels (Verlet build, pair kernels): cells are visited brick

@@ -152,7 +152,7 @@ struct Ctx {
   // CUDA graphs of the two per-step launch chains (api.cu run_graph): keyed by every pointer, count
   // and parameter the chain's launches read, so a rebuild / transition / upload selects (or captures)
   // another graph instead of replaying stale arguments.  The Dirichlet schedules read t^{n+1} from
-  // dtime (a memcpy node from the pinned htime) when captured.
+  // dtime[0], a device clock the kick chain's tail advances every step (resynced with c.t per call).
   struct GraphEntry {
     std::vector<unsigned char> key;
     cudaGraphExec_t exec = nullptr;
@@ -166,11 +166,17 @@ struct Ctx {
   uint64_t graph_clock = 0;
   int64_t graph_captures = 0, graph_replays = 0;
   bool use_graphs = true, capturing = false;
-  double* dtime = nullptr;  // device t^{n+1} for captured Dirichlet kernels
-  double* htime = nullptr;  // pinned host source of dtime
+  double* dtime = nullptr;  // device: [0] the force chain's time (c.t + dt), [1] the clock (c.t)
+  double* htime = nullptr;  // pinned host staging for the resync
   // sphg_step_download: enqueued after the wall extrapolation of the last step (eager chain), packs the
   // fields that are final by then so their D2H copies on copy_stream overlap the force kernels
   std::function<void(Ctx&)> pre_forces;
+  // speculative steps (one_step): the force chain is queued before the host has read the kick
+  // chain's flags; dskip (read by every force-chain kernel through DevParams::skip) voids it when the
+  // step needs a Verlet rebuild.  SPHG_SPECULATE=0 turns it off.
+  bool speculate = true;
+  uint32_t* dskip = nullptr;
+  cudaEvent_t kick_ev = nullptr;
   // rigid force pass on a second stream beside the fluid one (SPHG_CONCURRENT_RIGID=0 serialises)
   bool concurrent_rigid = true;
   cudaStream_t side_stream = nullptr;
@@ -196,6 +202,7 @@ void launch_rigid_index(Ctx& c);
 // kernels_step.cu
 void launch_body_kick(Ctx& c);
 void launch_kick_drift(Ctx& c);
+void launch_step_tail(Ctx& c);  // dskip (rebuild or error pending) and the device clock t^{n+1}
 void launch_density(Ctx& c);
 void launch_heat(Ctx& c);
 void launch_heat_begin(Ctx& c);

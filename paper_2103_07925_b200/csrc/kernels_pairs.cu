@@ -102,6 +102,7 @@ __device__ __forceinline__ double density_term(const DevParams& P, double3 pi, d
 template <int G, int M>
 __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                      const uint32_t* __restrict__ list, size_t nlist) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
@@ -148,6 +149,7 @@ template <int G, int M>
 __global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                   const uint32_t* __restrict__ list, size_t nlist,
                                                   double2* __restrict__ Hout, DevFlags* __restrict__ fl) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
@@ -220,6 +222,7 @@ template <int G>
 __global__ void __launch_bounds__(kBlock) k_heat_source(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                          const uint32_t* __restrict__ list, size_t nlist,
                                                          double t_new, const double* __restrict__ t_dev) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
@@ -277,6 +280,7 @@ template <int G, int M>
 __global__ void __launch_bounds__(kBlock) k_diffusion(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                        const uint32_t* __restrict__ list, size_t nlist,
                                                        double2* __restrict__ Cout, DevFlags* __restrict__ fl) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
@@ -345,6 +349,7 @@ __global__ void __launch_bounds__(kBlock, kPin ? 1 : 9) k_extrapolate(const __gr
                                                          const sphg_body* __restrict__ B,
                                                          const uint32_t* __restrict__ list, size_t nlist,
                                                          uint32_t* __restrict__ pin_list, uint32_t* __restrict__ any) {
+  SPHG_SKIP_IF_FLAGGED(P);
   // kPin: the flagged particles, compacted by the fast pass into pin_list[0 .. *any)
   if (kPin) {
     nlist = *any;
@@ -591,6 +596,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
                                                           const uint32_t* __restrict__ list, size_t nlist,
                                                           DevFlags* __restrict__ fl,
                                                           double2* __restrict__ Hout = nullptr) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
   const int lane = (int)(t % G);
@@ -748,6 +754,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
                                                           const uint32_t* __restrict__ ncon,
                                                           DevFlags* __restrict__ fl, uint32_t* __restrict__ pin_list,
                                                           uint32_t* __restrict__ any) {
+  SPHG_SKIP_IF_FLAGGED(P);
   // kPin: the flagged particles, compacted by the fast pass into pin_list[0 .. *any)
   if (kPin) {
     nlist = *any;
@@ -905,7 +912,8 @@ __global__ void __launch_bounds__(kBlock) k_count_pairs(const __grid_constant__ 
 }
 
 // particles the heat kernels do not update (walls, ghosts) keep their T in the new buffer
-__global__ void k_copy_boundary_T(Particles D, size_t n, double2* __restrict__ Hout) {
+__global__ void k_copy_boundary_T(const __grid_constant__ DevParams P, Particles D, size_t n, double2* __restrict__ Hout) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t kmd = D.kmd.p[i];
@@ -921,6 +929,7 @@ __device__ __forceinline__ double sched_value(const DevSchedule& s, double t) { 
 // t_dev (graph replay): t^{n+1} from device memory, refreshed by a memcpy node every replay
 __global__ void k_dirichlet(const __grid_constant__ DevParams P, Particles D, size_t n, double t_new,
                             const double* __restrict__ t_dev) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (t_dev) t_new = *t_dev;
@@ -933,6 +942,7 @@ __global__ void k_dirichlet(const __grid_constant__ DevParams P, Particles D, si
 
 __global__ void k_dirichlet_c(const __grid_constant__ DevParams P, Particles D, size_t n, double t_new,
                               const double* __restrict__ t_dev) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (t_dev) t_new = *t_dev;
@@ -941,7 +951,8 @@ __global__ void k_dirichlet_c(const __grid_constant__ DevParams P, Particles D, 
   reinterpret_cast<double*>(&D.C2.p[i])[0] = sched_value(P.schedC[gr], t_new);
 }
 
-__global__ void k_copy_boundary_C(Particles D, size_t n, double2* __restrict__ Cout) {
+__global__ void k_copy_boundary_C(const __grid_constant__ DevParams P, Particles D, size_t n, double2* __restrict__ Cout) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t kmd = D.kmd.p[i];
@@ -1021,7 +1032,7 @@ void launch_heat_begin(Ctx& c) {
 
 void launch_heat_end(Ctx& c) {
   if (c.n == 0) return;
-  k_copy_boundary_T<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.cur, c.n, c.H2new.p);
+  k_copy_boundary_T<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, c.H2new.p);
   std::swap(c.cur.H2, c.H2new);
   c.launches++;
 }
@@ -1044,7 +1055,7 @@ void launch_diffusion(Ctx& c) {
   if (c.nrigid)
     SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, (k_diffusion<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.C2new.p, c.dflags))));
-  k_copy_boundary_C<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.cur, c.n, c.C2new.p);
+  k_copy_boundary_C<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, c.C2new.p);
   std::swap(c.cur.C2, c.C2new);
   c.launches += 4;
 }

@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevP
 }
 
 __global__ void k_body_final(const __grid_constant__ DevParams P, sphg_body* __restrict__ B, size_t nb) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nb) return;
   sphg_body& b = B[k];
@@ -173,6 +174,7 @@ __global__ void k_body_final(const __grid_constant__ DevParams P, sphg_body* __r
 
 __global__ void __launch_bounds__(256) k_final_kick(const __grid_constant__ DevParams P, Particles D,
                                                      const sphg_body* __restrict__ B, size_t n) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const uint32_t kmd = D.kmd.p[k];
@@ -216,6 +218,7 @@ __global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_body_reduce(const __g
                                                       const uint32_t* __restrict__ ridx,
                                                       const uint32_t* __restrict__ bstart,
                                                       const uint32_t* __restrict__ bend) {
+  SPHG_SKIP_IF_FLAGGED(P);
   const size_t k = W == 1 ? ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5 : (size_t)blockIdx.x;
   const int lane = threadIdx.x & 31, warp = W == 1 ? 0 : (int)(threadIdx.x >> 5);
   if (k >= nb) return;
@@ -595,6 +598,26 @@ void iota_gid(Ctx& c) {
 void launch_body_kick(Ctx& c) {
   if (c.nb == 0) return;
   k_body_kick<<<grid_for(c.nb, 128), 128, 0, c.stream>>>(c.P, c.bodies.p, c.nb);
+  c.launches++;
+}
+
+// end of the kick chain: flag the force chain to void itself when the Verlet trigger fired (max
+// displacement > half skin, compared as the host does: sqrt of the squared maximum) or an error is
+// pending, and advance the device clock: dtime[1] mirrors the host's c.t (c.t += dt), dtime[0] is the
+// time the captured force chain reads (the host's c.t + dt after the increment), same double adds
+__global__ void k_step_tail(const __grid_constant__ DevParams P, const DevFlags* __restrict__ fl,
+                            uint32_t* __restrict__ skip, double* __restrict__ dtime) {
+  const double md = sqrt(__longlong_as_double((long long)fl->max_disp2_bits));
+  *skip = (md > P.half_skin || fl->err != 0u) ? 1u : 0u;
+  if (dtime) {
+    const double t = dtime[1] + P.dt;
+    dtime[1] = t;
+    dtime[0] = t + P.dt;
+  }
+}
+
+void launch_step_tail(Ctx& c) {
+  k_step_tail<<<1, 1, 0, c.stream>>>(c.P, c.dflags, c.dskip, c.dtime);
   c.launches++;
 }
 
