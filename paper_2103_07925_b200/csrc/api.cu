@@ -419,7 +419,7 @@ std::vector<unsigned char> graph_key(const Ctx& c, int chain) {
   key_put(k, c.ncon.p);
   key_put(k, c.n); key_put(k, c.nb); key_put(k, c.nf); key_put(k, c.nw); key_put(k, c.nrigid);
   key_put(k, c.group_density); key_put(k, c.group_forces);
-  key_put(k, c.defer_final); key_put(k, c.fuse_heat); key_put(k, c.final_pending);
+  key_put(k, c.defer_final); key_put(k, c.fuse_heat); key_put(k, c.fuse_diff); key_put(k, c.final_pending);
   key_put(k, c.P);
   return k;
 }
@@ -503,11 +503,12 @@ void chain_kick(Ctx& c) {  // (A): everything up to the per-step flag readback
 void chain_forces(Ctx& c) {  // (B): density .. final kick (captured kernels read t^{n+1} from dtime)
   timed(c, SPHG_STAGE_DENSITY, launch_density);
   if (c.P.thermal) timed(c, SPHG_STAGE_HEAT, c.fuse_heat ? launch_heat_begin : launch_heat);
-  if (c.P.diffusion) timed(c, SPHG_STAGE_HEAT, launch_diffusion);
+  if (c.P.diffusion) timed(c, SPHG_STAGE_HEAT, c.fuse_diff ? launch_diffusion_begin : launch_diffusion);
   timed(c, SPHG_STAGE_EXTRAPOLATE, launch_extrapolate);
   if (c.pre_forces) c.pre_forces(c);
   timed_forces(c);
   if (c.fuse_heat) launch_heat_end(c);
+  if (c.fuse_diff) launch_diffusion_end(c);
   timed(c, SPHG_STAGE_BODIES, launch_bodies);
   timed(c, SPHG_STAGE_FINAL_KICK, launch_final_kick);
 }
@@ -536,9 +537,10 @@ int one_step(sphg_ctx* h) {
   // extrapolation or the forces, so moving it after them changes nothing)
   auto forces = [&]() {
     c.fuse_heat = c.P.thermal && !c.timing;
+    c.fuse_diff = c.P.diffusion && !c.P.thermal && !c.timing;  // one scalar field per row walk
     if (graphs && !c.pre_forces) run_graph(c, 1, chain_forces);
     else chain_forces(c);
-    c.fuse_heat = false;
+    c.fuse_heat = c.fuse_diff = false;
   };
   // speculative: queue the force chain before reading the kick chain's flags, so the GPU never waits
   // for the host's one 48-byte readback per step; dskip voids the queued chain when the step needs a

@@ -123,6 +123,7 @@ struct Ctx {
   bool defer_final = false, final_pending = false;
   // conduction of fluid particles folded into k_forces_fluid inside sphg_step (not for stage calls)
   bool fuse_heat = false;
+  bool fuse_diff = false;  // likewise the concentration sums, when the heat equation is off
   bool have_state = false;
   double t = 0.0;
   int64_t steps = 0, rebuilds = 0, n_melt = 0, n_solid = 0, launches = 0;
@@ -208,6 +209,8 @@ void launch_heat(Ctx& c);
 void launch_heat_begin(Ctx& c);
 void launch_heat_end(Ctx& c);
 void launch_diffusion(Ctx& c);
+void launch_diffusion_begin(Ctx& c);
+void launch_diffusion_end(Ctx& c);
 void launch_extrapolate(Ctx& c);
 void launch_forces(Ctx& c);
 void launch_forces_fluid(Ctx& c);

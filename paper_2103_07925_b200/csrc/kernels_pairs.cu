@@ -514,8 +514,10 @@ __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, 
 // once per particle from bg (k_forces_fluid), not per pair.
 // conduction folded into the fluid forces pass (one row walk; see launch_heat_begin): T_i, kappa_i
 // of the fluid particle and the running sum of k_heat
+// (kHeat with diff = 1: the same fold for the concentration sums of k_diffusion, D for kappa)
 struct HeatSide {
   double T, kappa, s;
+  int diff;
 };
 
 template <int M, bool kTvf, bool kSingleEta, bool kHeat = false>
@@ -532,13 +534,14 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
   }
   double rinv;
   const double dW = P.sig_h * shape_deriv_q(pair_qr(d, r2, P.inv_h, rinv));
-  if (kHeat && hj.y != 0.0) {  // same term, same order as k_heat (non-Dirichlet walls: V_heat = 0)
+  if (kHeat && hj.y != 0.0) {  // same term, same order as k_heat / k_diffusion (V_heat / V_diff = 0: skip)
     double kt;
     bool conduct = true;
-    if (P.single_kappa) {
+    if (!heat->diff && P.single_kappa) {
       kt = 2.0 * heat->kappa;
     } else {
-      const double kb = P.mat[mat_of(__ldg(&D.kmd.p[nb_index<M>(e)]))].kappa;
+      const DevMat& Mb = P.mat[mat_of(__ldg(&D.kmd.p[nb_index<M>(e)]))];
+      const double kb = heat->diff ? Mb.D : Mb.kappa;
       const double ks = heat->kappa + kb;
       conduct = ks != 0.0;
       kt = conduct ? 4.0 * heat->kappa * kb / ks : 0.0;
@@ -577,7 +580,8 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
 template <int G, int M, bool kTvf, bool kSingleEta, bool kHeat = false>
 __device__ __forceinline__ void fluid_row(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
                                           const uint32_t* base, int n, int lane, double3& acc, double3& bg,
-                                          bool& coincident, HeatSide* heat = nullptr) {
+                                          bool& coincident, HeatSide* heat = nullptr,
+                                          const double2* __restrict__ Sin = nullptr) {
   int k = lane;
   uint32_t e = k < n ? ldrow(base + k) : 0u;
   for (; k < n; k += G) {
@@ -585,7 +589,7 @@ __device__ __forceinline__ void fluid_row(const DevParams& P, const Particles& D
     const uint32_t j = nb_index<M>(e);
     const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
     double2 hj = double2{0.0, 0.0};
-    if (kHeat) hj = __ldg(&D.H2.p[j]);
+    if (kHeat) hj = __ldg(&Sin[j]);
     fluid_pair<M, kTvf, kSingleEta, kHeat>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident, heat, hj);
     e = en;
   }
@@ -595,7 +599,8 @@ template <int G, int M, bool kTvf, bool kSingleEta, bool kHeat = false>
 __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                           const uint32_t* __restrict__ list, size_t nlist,
                                                           DevFlags* __restrict__ fl,
-                                                          double2* __restrict__ Hout = nullptr) {
+                                                          double2* __restrict__ Hout = nullptr,
+                                                          const double2* __restrict__ Sin = nullptr, int sdiff = 0) {
   SPHG_SKIP_IF_FLAGGED(P);
   const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
   const size_t g = t / G;
@@ -605,14 +610,14 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
   double3 acc = make_double3(0, 0, 0), bg = make_double3(0, 0, 0);
   bool coincident = false;
   uint32_t kmd = 0;
-  HeatSide heat{0.0, 0.0, 0.0};
+  HeatSide heat{0.0, 0.0, 0.0, sdiff};
   double2 hi = double2{0.0, 0.0};
   if (active) {
     kmd = D.kmd.p[i];
-    if (kHeat) {
-      hi = D.H2.p[i];
+    if (kHeat) {  // Sin: (T, V_heat), or (C, V_diff) with sdiff
+      hi = Sin[i];
       heat.T = hi.x;
-      heat.kappa = P.mat[mat_of(kmd)].kappa;
+      heat.kappa = sdiff ? P.mat[mat_of(kmd)].D : P.mat[mat_of(kmd)].kappa;
     }
     const double4 g0 = ldg4(&D.G0.p[i]), g1 = ldg4(&D.G1.p[i]), g2 = ldg4(&D.G2.p[i]);
     PairSide I;
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
     const Row R = row_of(L, i);
     // one pass over the whole contiguous row: wall/rigid records carry du = 0 (A_w = 0) and, with
     // several viscosities, fluid_pair looks up eta_j by kind (eta_w := eta_i)
-    fluid_row<G, M, kTvf, kSingleEta, kHeat>(P, D, I, pi, R.f, R.n, lane, acc, bg, coincident, &heat);
+    fluid_row<G, M, kTvf, kSingleEta, kHeat>(P, D, I, pi, R.f, R.n, lane, acc, bg, coincident, &heat, Sin);
   }
   if (kHeat) heat.s = gsum<G>(heat.s);
   acc.x = gsum<G>(acc.x);
@@ -654,7 +659,13 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
   D.A4.p[i] = make_double4(acc.x * im + Mt.g[0], acc.y * im + Mt.g[1], acc.z * im + Mt.g[2], 0.0);
   const double f = kTvf ? -Mt.pb * im : 0.0;
   D.B4.p[i] = make_double4(f * bg.x, f * bg.y, f * bg.z, 0.0);
-  if (kHeat) {  // the k_heat epilogue for a fluid particle (rho_a = rho_i)
+  if (kHeat && sdiff) {  // the k_diffusion epilogue for a fluid particle (rho_a = rho_i)
+    const double rate = heat.s / D.G1.p[i].w;
+    const uint32_t gc = dirc_of(kmd);
+    const bool fixed = gc != SPHG_NO_DIRICHLET && (int)gc < P.n_schedC && P.schedC[gc].n > 0;
+    Hout[i] = make_double2(fixed ? hi.x : hi.x + P.dt * rate, hi.y);
+    D.dCdt.p[i] = rate;
+  } else if (kHeat) {  // the k_heat epilogue for a fluid particle (rho_a = rho_i)
     double rate = 0.0;
     if (Mt.cp > 0.0) {
       rate = heat.s / (D.G1.p[i].w * Mt.cp);
@@ -1045,19 +1056,35 @@ void launch_heat(Ctx& c) {
   c.fuse_heat = f;
 }
 
-void launch_diffusion(Ctx& c) {
+// Diffusion in two halves like heat (c.fuse_diff folds the fluid part into the forces pass when the heat
+// equation is off): begin = Dirichlet-C at t^{n+1} + rigid (+ fluid when not fused) sums; end = walls /
+// ghosts keep C, swap the double buffer.
+void launch_diffusion_begin(Ctx& c) {
   if (c.n == 0) return;
   const double t_new = c.t + c.P.dt;
   k_dirichlet_c<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, t_new, c.capturing ? c.dtime : nullptr);
-  if (c.nf)
+  if (c.nf && !c.fuse_diff)
     SPHG_L_DISPATCH(c, c.nf, SPHG_IMG_DISPATCH(c.P.img_mode, (k_diffusion<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.C2new.p, c.dflags))));
   if (c.nrigid)
     SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, (k_diffusion<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.C2new.p, c.dflags))));
+  c.launches += 3;
+}
+
+void launch_diffusion_end(Ctx& c) {
+  if (c.n == 0) return;
   k_copy_boundary_C<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, c.C2new.p);
   std::swap(c.cur.C2, c.C2new);
-  c.launches += 4;
+  c.launches++;
+}
+
+void launch_diffusion(Ctx& c) {
+  const bool f = c.fuse_diff;
+  c.fuse_diff = false;
+  launch_diffusion_begin(c);
+  launch_diffusion_end(c);
+  c.fuse_diff = f;
 }
 
 // fast pass over the list, then the pinned redo of the particles it appended to pin_list (a launch
@@ -1082,10 +1109,14 @@ void launch_extrapolate(Ctx& c) {
 
 template <bool kTvf, bool kSingleEta>
 static void launch_forces_fluid_t(Ctx& c) {
-  if (c.nf && c.fuse_heat) {  // conduction of the fluid particles in the same row walk (k_heat's width)
+  if (c.nf && (c.fuse_heat || c.fuse_diff)) {  // conduction / diffusion of the fluid particles in the same
+                                               // row walk (k_heat's / k_diffusion's width and order)
+    const bool dif = !c.fuse_heat;
+    const double2* sin = dif ? c.cur.C2.p : c.cur.H2.p;
+    double2* out = dif ? c.C2new.p : c.H2new.p;
     SPHG_L_DISPATCH(c, c.nf, SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, true>
                                      <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, c.H2new.p))));
+                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, out, sin, dif ? 1 : 0))));
     c.launches++;
     return;
   }

@@ -627,6 +627,25 @@ def test_fused_heat_is_bit_identical():
     assert np.array_equal(ga.kind, gb.kind)
 
 
+def test_fused_diffusion_is_bit_identical():
+    """Without the heat equation, sphg_step folds the fluid concentration sums into the forces pass
+    (same terms, same order as k_diffusion); with stage timing on they run in k_diffusion.  Same
+    concentrations, rates and transition flags bit for bit (dissolution with concentration-mode
+    transitions)."""
+    sc = CASES["dissolve"]()
+    a, b = sim_factory(sc.params), sim_factory(sc.params)
+    for e in (a, b):
+        e.upload(sc.store, sc.bodies)
+        e.initialize()
+    b.set_timing(True)
+    a.step(4)
+    b.step(4)
+    ga, _ = a.download()
+    gb, _ = b.download()
+    for f in ("concentration", "dC_dt", "pos", "vel", "acc", "density", "kind", "group"):
+        assert np.array_equal(getattr(ga, f), getattr(gb, f)), f
+
+
 @pytest.mark.parametrize("name,steps", [("c1_small", 40), ("c2_melt", 6), ("c3_small", 12), ("dissolve", 6),
                                         ("c4_scan", 6)])
 def test_graph_replay_is_bit_identical(monkeypatch, name, steps):
