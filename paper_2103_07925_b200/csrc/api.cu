@@ -545,7 +545,7 @@ int one_step(sphg_ctx* h) {
   // speculative: queue the force chain before reading the kick chain's flags, so the GPU never waits
   // for the host's one 48-byte readback per step; dskip voids the queued chain when the step needs a
   // rebuild or hit an error, and the host state it changed is restored before the redo
-  const bool spec = c.speculate && c.built && c.P.transitions == 0 && !c.timing && !c.pre_forces;
+  const bool spec = c.speculate && c.built && !c.timing && !c.pre_forces;
   const Particles cur0 = c.cur;
   const DBuf<double2> h2n0 = c.H2new, c2n0 = c.C2new;
   const bool fp0 = c.final_pending;
