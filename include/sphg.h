@@ -107,7 +107,18 @@ typedef struct {
   double hs_radius;             /* 1/e^2 radius r0 [m] */
   double hs_origin[3];          /* spot centre at t = 0 (z unused) */
   double hs_velocity[3];        /* scan velocity (z unused) */
+  /* Runtime time-step assertion: after every step the five compute_dt
+   * limits are evaluated with that step's u_max (max |u^{n+1/2}| of fluid particles, from the kick)
+   * and m_r = the smallest mass a rigid particle can have in the run (rigid particles, plus fluid
+   * particles of a material with a solidify target when transitions are on; fixed at upload) [P22].
+   * dt above the smallest limit: SPHG_DT_REFUSE returns SPHG_ERR_RUNTIME naming the violated
+   * condition (the step itself completes); SPHG_DT_WARN counts it in the stats (SURVEY App. A15:
+   * BASELINE C1/C5 prescribe a dt above the contact limit); SPHG_DT_OFF skips the check. */
+  int32_t dt_check;
+  int32_t pad_dt;
 } sphg_params;
+
+enum { SPHG_DT_REFUSE = 0, SPHG_DT_WARN = 1, SPHG_DT_OFF = 2 };
 
 /* Host SoA views in gid order — the ParticleStore<3> layout (store.hpp:26-46).
  * Vec<3> fields are 3*n doubles, interleaved xyz.  `force` is an optional
@@ -184,6 +195,11 @@ typedef struct {
   double last_step_call_ms;   /* device time of the last sphg_step call (CUDA events on the stream) */
   int64_t graph_captures;     /* CUDA graphs captured for the per-step launch chains (SPHG_GRAPHS=0: none) */
   int64_t graph_replays;      /* chain launches served by an already captured graph */
+  int64_t dt_violations;      /* steps whose dt exceeded a compute_dt limit (runtime assertion, SPHG_DT_WARN) */
+  int32_t dt_term;            /* the most restrictive limit at the last check: 0 cfl, 1 viscous, 2 body force,
+                                 3 contact, 4 conduction (-1: none checked) */
+  int32_t pad3;
+  double dt_limit;            /* its value */
 } sphg_stats_t;
 
 typedef struct sphg_ctx sphg_ctx;

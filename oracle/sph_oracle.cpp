@@ -87,6 +87,11 @@ struct Ctx {
            wall_a[SPHG_MAX_WALL_GROUPS][3] = {};
     std::string err;
     int threads = 0;
+    // runtime time-step assertion [P22]
+    double m_r = 0.0;              // smallest mass a rigid particle can have in this run (0: none)
+    int64_t dt_violations = 0;
+    int dt_term = -1;
+    double dt_limit = std::numeric_limits<double>::infinity();
 };
 
 inline bool ghost(const Ctx& c, size_t i) { return c.S.owner[i] != (uint32_t)c.P.rank; }
@@ -1130,6 +1135,53 @@ bool run_stage(Ctx& c, int s) {
     return fail(c, "unknown stage");
 }
 
+// compute_dt: cfl 0.25 h/(c+|u_max|), viscous 0.125 h^2/nu, body force
+// 0.25 sqrt(h/|b_max|), contact 0.22 sqrt(m_r/k_c), conduction 0.1 rho c_p h^2/kappa, each over the most
+// restrictive material; absent physics -> +inf.
+void dt_terms(const Ctx& c, double u_max, double lim[5]) {
+    const double inf = std::numeric_limits<double>::infinity();
+    for (int k = 0; k < 5; ++k) lim[k] = inf;
+    const double h = c.h;
+    double bmax = 0.0;
+    for (int m = 0; m < c.P.n_mat; ++m) {
+        const sphg_material& M = c.P.mat[m];
+        if (M.c > 0.0) lim[0] = std::min(lim[0], 0.25 * h / (M.c + u_max));
+        if (M.nu > 0.0) lim[1] = std::min(lim[1], 0.125 * h * h / M.nu);
+        bmax = std::max(bmax, std::sqrt(M.body_force[0] * M.body_force[0] + M.body_force[1] * M.body_force[1] +
+                                        M.body_force[2] * M.body_force[2]));
+        if (c.P.thermal && M.kappa > 0.0 && M.cp > 0.0) lim[4] = std::min(lim[4], 0.1 * M.rho0 * M.cp * h * h / M.kappa);
+    }
+    if (bmax > 0.0) lim[2] = 0.25 * std::sqrt(h / bmax);
+    if (c.P.kc > 0.0 && c.m_r > 0.0) lim[3] = 0.22 * std::sqrt(c.m_r / c.P.kc);
+}
+
+// Runtime assertion after a step ("refuse with diagnostic listing the violated condition";
+// SPEC:560-561): u_max of this step's kick.
+bool check_dt(Ctx& c) {
+    if (c.P.dt_check == SPHG_DT_OFF) return true;
+    static const char* names[5] = {"cfl", "viscous", "body force", "contact", "conduction"};
+    double lim[5];
+    dt_terms(c, c.u_max, lim);
+    c.dt_term = -1;
+    c.dt_limit = std::numeric_limits<double>::infinity();
+    std::string bad;
+    for (int k = 0; k < 5; ++k) {
+        if (lim[k] < c.dt_limit) { c.dt_limit = lim[k]; c.dt_term = k; }
+        if (c.dt > lim[k]) {
+            char b[96];
+            std::snprintf(b, sizeof b, "%s%s limit %.6g", bad.empty() ? "" : ", ", names[k], lim[k]);
+            bad += b;
+        }
+    }
+    if (bad.empty()) return true;
+    c.dt_violations++;
+    if (c.P.dt_check == SPHG_DT_WARN) return true;
+    char b[128];
+    std::snprintf(b, sizeof b, "time-step condition violated at step %lld: dt = %.6g exceeds the ",
+                  (long long)c.steps, c.dt);
+    return fail(c, std::string(b) + bad);
+}
+
 bool one_step(Ctx& c) {
     if (!stage_kick_drift(c)) return false;
     const double half_skin = 0.5 * (c.rv - c.rc);
@@ -1144,7 +1196,7 @@ bool one_step(Ctx& c) {
     if (!stage_final_kick(c)) return false;
     if (c.P.transitions != 0 && !stage_transitions(c)) return false;
     c.steps++;
-    return true;
+    return check_dt(c);
 }
 
 void copy3(std::vector<V3>& dst, const double* src, size_t n) {
@@ -1234,6 +1286,13 @@ int orc_upload(orc_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t nb
         return SPHG_ERR_CONFIG;
     }
     resize_aux(c);
+    c.m_r = 0.0;  // [P22]: rigid particles, and fluid particles that may solidify
+    for (size_t i = 0; i < n; ++i) {
+        const bool can_be_rigid = S.kind[i] == Kind::Rigid ||
+                                  (S.kind[i] == Kind::Fluid && c.P.transitions != 0 &&
+                                   c.P.mat[S.material[i]].solidify_target >= 0);
+        if (can_be_rigid && S.mass[i] > 0.0 && (c.m_r == 0.0 || S.mass[i] < c.m_r)) c.m_r = S.mass[i];
+    }
     if (s->force) copy3(c.force, s->force, n);
     c.bodies.assign(bodies, bodies + nb);
     c.body_fscale.assign(nb, 0.0);
@@ -1440,6 +1499,9 @@ int orc_stats(orc_ctx* h, sphg_stats_t* s) {
     s->time = c.t;
     s->max_displacement = c.max_disp;
     s->u_max = c.u_max;
+    s->dt_violations = c.dt_violations;
+    s->dt_term = c.dt_term;
+    s->dt_limit = c.dt_limit;
     return SPHG_OK;
 }
 

@@ -14,6 +14,8 @@ NO_DIRICHLET = 0xFF
 FLUID, RIGID, BOUNDARY = 0, 1, 2  # store.hpp:11 Kind
 
 OK, ERR_CONFIG, ERR_RUNTIME, ERR_CUDA = 0, 2, 3, 4
+DT_REFUSE, DT_WARN, DT_OFF = 0, 1, 2  # sphg_params.dt_check
+DT_TERMS = ("cfl", "viscous", "body force", "contact", "conduction")  # compute_dt order
 
 STAGE_REBUILD = 0
 STAGE_DENSITY = 1
@@ -69,7 +71,9 @@ class Params(C.Structure):
                 # moving Gaussian surface heat flux (C4, [P21]; not in the reference)
                 ("heat_source", C.c_int32), ("hs_material_mask", C.c_uint32),
                 ("hs_power", C.c_double), ("hs_radius", C.c_double),
-                ("hs_origin", C.c_double * 3), ("hs_velocity", C.c_double * 3)]
+                ("hs_origin", C.c_double * 3), ("hs_velocity", C.c_double * 3),
+                # runtime time-step assertion: DT_REFUSE / DT_WARN / DT_OFF
+                ("dt_check", C.c_int32), ("pad_dt", C.c_int32)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -107,7 +111,8 @@ class Stats(C.Structure):
                 ("time", C.c_double), ("max_displacement", C.c_double), ("u_max", C.c_double),
                 ("stage_ms", C.c_double * 16), ("kernel_launches", C.c_int64),
                 ("last_step_call_ms", C.c_double), ("graph_captures", C.c_int64),
-                ("graph_replays", C.c_int64)]
+                ("graph_replays", C.c_int64), ("dt_violations", C.c_int64), ("dt_term", C.c_int32),
+                ("pad3", C.c_int32), ("dt_limit", C.c_double)]
 
 
 # void fn(int32 group, double t, double vel[3], double acc[3], void* user)  (sphg_set_wall_motion)

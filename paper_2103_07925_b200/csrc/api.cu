@@ -416,7 +416,7 @@ std::vector<unsigned char> graph_key(const Ctx& c, int chain) {
   key_put(k, c.cur); key_put(k, c.alt); key_put(k, c.H2new); key_put(k, c.C2new);
   key_put(k, c.bodies.p); key_put(k, c.nbr.p); key_put(k, c.cnt.p); key_put(k, c.cap);
   key_put(k, c.fidx.p); key_put(k, c.widx.p); key_put(k, c.ridx.p); key_put(k, c.body_start.p);
-  key_put(k, c.ncon.p);
+  key_put(k, c.ncon.p); key_put(k, c.pin_list.p); key_put(k, c.hsrc.p);
   key_put(k, c.n); key_put(k, c.nb); key_put(k, c.nf); key_put(k, c.nw); key_put(k, c.nrigid);
   key_put(k, c.group_density); key_put(k, c.group_forces);
   key_put(k, c.defer_final); key_put(k, c.fuse_heat); key_put(k, c.fuse_diff); key_put(k, c.final_pending);
@@ -513,6 +513,37 @@ void chain_forces(Ctx& c) {  // (B): density .. final kick (captured kernels rea
   timed(c, SPHG_STAGE_FINAL_KICK, launch_final_kick);
 }
 
+// Runtime time-step assertion ("refuse with diagnostic listing the violated condition",
+// SPEC:558-561): the compute_dt limits with this step's u_max (read from the kick chain's flags) [P22].
+int check_dt(sphg_ctx* h) {
+  Ctx& c = h->c;
+  if (c.params.dt_check == SPHG_DT_OFF) return SPHG_OK;
+  static const char* names[5] = {"cfl", "viscous", "body force", "contact", "conduction"};
+  double lim[5];
+  sphg_dt_limits(&c.params, c.u_max, c.m_r, lim);
+  c.dt_term = -1;
+  c.dt_limit = std::numeric_limits<double>::infinity();
+  std::string bad;
+  for (int k = 0; k < 5; ++k) {
+    if (lim[k] < c.dt_limit) {
+      c.dt_limit = lim[k];
+      c.dt_term = k;
+    }
+    if (c.P.dt > lim[k]) {
+      char b[96];
+      std::snprintf(b, sizeof b, "%s%s limit %.6g", bad.empty() ? "" : ", ", names[k], lim[k]);
+      bad += b;
+    }
+  }
+  if (bad.empty()) return SPHG_OK;
+  c.dt_violations++;
+  if (c.params.dt_check == SPHG_DT_WARN) return SPHG_OK;
+  char b[128];
+  std::snprintf(b, sizeof b, "time-step condition violated at step %lld: dt = %.6g exceeds the ", (long long)c.steps,
+                c.P.dt);
+  return fail(h, SPHG_ERR_RUNTIME, std::string(b) + bad);
+}
+
 int one_step(sphg_ctx* h) {
   Ctx& c = h->c;
   if (c.nghost)
@@ -572,7 +603,7 @@ int one_step(sphg_ctx* h) {
     if (rc) return fail(h, rc, c.err);
   }
   c.steps++;
-  return SPHG_OK;
+  return check_dt(h);
 }
 
 template <class T>
@@ -953,6 +984,7 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     const size_t n = s->n;
     if (n >= (size_t)UINT32_MAX) return fail(h, SPHG_ERR_CONFIG, "too many particles for 32-bit gids");
     // validate tags first (nothing is modified on failure)
+    double m_r = 0.0;  // [P22]: rigid particles, and fluid particles that may solidify
     for (size_t i = 0; i < n; ++i) {
       const uint32_t kind = s->kind ? s->kind[i] : 0;
       const uint32_t mat = s->material ? s->material[i] : 0;
@@ -960,13 +992,22 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
         return fail(h, SPHG_ERR_CONFIG, "particle " + std::to_string(i) + " has an invalid kind/material");
       if (kind == SPHG_RIGID && (s->group ? s->group[i] : 0) >= nb)
         return fail(h, SPHG_ERR_CONFIG, "rigid particle " + std::to_string(i) + " refers to a missing body");
+      const bool can_be_rigid = kind == SPHG_RIGID || (kind == SPHG_FLUID && c.params.transitions != 0 &&
+                                                       c.params.mat[mat].solidify_target >= 0);
+      const double m = s->mass ? s->mass[i] : 0.0;
+      if (can_be_rigid && m > 0.0 && (m_r == 0.0 || m < m_r)) m_r = m;
     }
+    c.m_r = m_r;
     size_t ng = 0;
     if (s->owner)
       for (size_t i = 0; i < n; ++i) ng += s->owner[i] != (uint32_t)c.params.rank ? 1 : 0;
     if (ng && c.params.transitions)
       return fail(h, SPHG_ERR_CONFIG, "phase transitions are single-rank only (ghost particles present)");
     c.nghost = ng;
+    // buffers below may be reallocated (and a freed address handed out again): no captured graph may
+    // survive an upload (the graph key holds raw pointers)
+    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    destroy_graphs(c);
     // warm upload: same store size and a valid Verlet list -> keep the device order and the list,
     // scatter the host (gid-ordered) data through the gid permutation
     const bool warm = c.built && c.have_state && n == c.n && n > 0;
@@ -1274,6 +1315,9 @@ int sphg_stats(sphg_ctx* h, sphg_stats_t* s) {
     s->last_step_call_ms = c.last_step_ms;
     s->graph_captures = c.graph_captures;
     s->graph_replays = c.graph_replays;
+    s->dt_violations = c.dt_violations;
+    s->dt_term = c.dt_term;
+    s->dt_limit = c.dt_limit;
     if (c.built && c.n) {
       std::vector<uint32_t> cnt(c.n);
       d2h(cnt.data(), c.cnt.p, c.n, c.stream);
@@ -1319,18 +1363,8 @@ int sphg_dt_limits(const sphg_params* p, double u_max, double m_r, double lim[5]
 
 int sphg_compute_dt(sphg_ctx* h, double lim[5]) {
   return guarded(h, [&]() -> int {
-    Ctx& c = h->c;
-    double mr = 0.0;
-    if (c.params.kc > 0.0 && c.nb > 0) {
-      std::vector<sphg_body> b(c.nb);
-      d2h(b.data(), c.bodies.p, c.nb, c.stream);
-      SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-      double best = std::numeric_limits<double>::infinity();
-      for (auto& x : b)
-        if (x.alive) best = std::min(best, c.params.mat[x.material].rho0 * c.P.dx3);
-      if (best < std::numeric_limits<double>::infinity()) mr = best;
-    }
-    return sphg_dt_limits(&c.params, c.u_max, mr, lim);
+    Ctx& c = h->c;  // m_r: the smallest possible rigid particle mass, fixed at upload [P22]
+    return sphg_dt_limits(&c.params, c.u_max, c.m_r, lim);
   });
 }
 

@@ -184,6 +184,11 @@ struct Ctx {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t dl_ev = nullptr;
+  // runtime time-step assertion (api.cu check_dt) [P22]
+  double m_r = 0.0;  // smallest mass a rigid particle can have in this run (set at upload; 0 = none)
+  int64_t dt_violations = 0;
+  int dt_term = -1;
+  double dt_limit = 0.0;
 };
 
 // ------------------------------------------------------------ launchers

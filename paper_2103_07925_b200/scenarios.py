@@ -98,6 +98,29 @@ def _params(dx, dt, lo, hi, periodic, mats, kc=0.0, dc=0.0, tvf=1, thermal=0, tr
     return p
 
 
+def dt_limits_host(params, u_max, m_r):
+    """compute_dt terms in plain Python (scenario setup; the product check runs in the
+    library): cfl, viscous, body force, contact, conduction (+inf = absent)."""
+    inf = float("inf")
+    lim = [inf] * 5
+    h = params.h if params.h > 0 else params.dx
+    bmax = 0.0
+    for m in range(params.n_mat):
+        M = params.mat[m]
+        if M.c > 0:
+            lim[0] = min(lim[0], 0.25 * h / (M.c + u_max))
+        if M.nu > 0:
+            lim[1] = min(lim[1], 0.125 * h * h / M.nu)
+        bmax = max(bmax, math.sqrt(sum(M.body_force[a] ** 2 for a in range(3))))
+        if params.thermal and M.kappa > 0 and M.cp > 0:
+            lim[4] = min(lim[4], 0.1 * M.rho0 * M.cp * h * h / M.kappa)
+    if bmax > 0:
+        lim[2] = 0.25 * math.sqrt(h / bmax)
+    if params.kc > 0 and m_r > 0:
+        lim[3] = 0.22 * math.sqrt(m_r / params.kc)
+    return lim
+
+
 def damping_from_ratio(zeta, kc, m_r):
     """d_c = 2 zeta sqrt(k_c m_eff), m_eff = m_r/2 for equal rigid particles."""
     return 2.0 * zeta * math.sqrt(kc * 0.5 * m_r)
@@ -255,6 +278,9 @@ def periodic_spheres(nside=32, n_spheres=4, r_range=(4.0, 4.0), dx=1e-3, dt=1e-5
             material(rho_s, c=0.0)]                          # 1 solid
     m_r = rho_s * dx ** 3
     params = _params(dx, dt, lo, hi, (1, 1, 1), mats, kc=kc, dc=damping_from_ratio(zeta, kc, m_r))
+    # BASELINE prescribes dt = 1e-5 s, above the contact limit 0.22 sqrt(m_r/k_c) = 9.84e-6 s (SURVEY
+    # App. B1): the runtime assertion warns instead of refusing (App. A15)
+    params.dt_check = abi.DT_WARN if dt > dt_limits_host(params, 0.0, m_r if kc > 0 else 0.0)[3] else abi.DT_REFUSE
     pos = lattice_box(lo, hi, dx)
     n = len(pos)
     if centers is None:
@@ -734,6 +760,9 @@ def paper_strong_scaling(nside=150, n_grid=6, dx=0.2, D=2.5, rho_f=1.0, nu=1.0, 
             material(rho_f, c=c)]                        # 2 wall
     m_r = rho_s * dx ** 3
     params = _params(dx, dt, lo, hi, (0, 0, 0), mats, kc=kc, dc=damping_from_ratio(zeta, kc, m_r))
+    # the paper's dt = 1e-3 is exactly the CFL limit 0.25 h / c at rest, so any flow exceeds it: the
+    # runtime assertion warns instead of refusing the paper's own setting
+    params.dt_check = abi.DT_WARN
     if nside == 150:
         params.cell_edge_override = 0.65  # 48^3 cells over the 31.2 box
     fl = lattice_box((0.0,) * 3, (L,) * 3, dx)
@@ -770,6 +799,112 @@ def paper_strong_scaling(nside=150, n_grid=6, dx=0.2, D=2.5, rho_f=1.0, nu=1.0, 
     _finish(st, bodies)
     info = dict(n=n, n_fluid=int((st.kind == abi.FLUID).sum()), n_rigid=int(rig.sum()), n_boundary=nw,
                 n_bodies=len(centers), rigid_fraction=float(rig.mean()))
+    return Scenario(name, params, st, bodies, steps, info)
+
+
+def hydrostatic_tank(nxy=10, nz=20, dx=1e-3, dt=1e-5, rho=1000.0, c=10.0, nu=1e-6, g=-9.81, pb=0.0,
+                     hydrostatic=True, sphere_radius=0.0, rho_s=1200.0, jitter=0.0, seed=2129,
+                     name="tank", steps=0):
+    """A water column for the reference's hydrostatic KATs: periodic in x and y
+    (nxy dx), fluid 0 <= z <= H = nz dx between 3-layer fixed walls below z = 0 and above z = H
+    (closed, so no free surface), gravity g along z.  hydrostatic=True starts from the analytic
+    field p = rho0 |g| (H - z), rho = rho0 + p / c^2 (the EOS inverse, material.hpp:64-67);
+    otherwise rho = rho0, p = 0.  sphere_radius > 0 relabels a sphere (radius in dx, centred at
+    mid-depth) as a rigid body of density rho_s (SPEC:287 submerged body).  Materials: 0 fluid,
+    1 wall, 2 solid."""
+    L = nxy * dx
+    H = nz * dx
+    nl = 3
+    lo = (0.0, 0.0, -nl * dx)
+    hi = (L, L, H + nl * dx)
+    mats = [material(rho, nu=nu, c=c, pb=pb, g=(0.0, 0.0, g)), material(rho, c=c), material(rho_s, c=0.0)]
+    params = _params(dx, dt, lo, hi, (1, 1, 0), mats, tvf=1 if pb > 0 else 0)
+    fl = lattice_box((0.0, 0.0, 0.0), (L, L, H), dx)
+    wl = lattice_box(lo, hi, dx)
+    wl = wl[(wl[:, 2] < 0.0) | (wl[:, 2] > H)]
+    nf, nw = len(fl), len(wl)
+    n = nf + nw
+    st = ParticleStore(n)
+    pos = fl.copy()
+    if jitter:
+        u = splitmix_u01(seed, 0, np.arange(3 * nf, dtype=np.uint64)).reshape(nf, 3)
+        pos = pos + (2.0 * u - 1.0) * (jitter * dx)
+        for a in range(2):
+            pos[:, a] = np.mod(pos[:, a], L)
+    st.pos[:nf] = pos
+    st.pos[nf:] = wl
+    st.kind[:nf] = abi.FLUID
+    st.kind[nf:] = abi.BOUNDARY
+    st.material[nf:] = 1
+    st.mass[:] = rho * dx ** 3
+    st.density[:] = rho
+    if hydrostatic:
+        p = rho * abs(g) * (H - pos[:, 2])
+        st.pressure[:nf] = p
+        st.density[:nf] = rho + p / (c * c)
+    nb = 0
+    if sphere_radius > 0.0:
+        cen = np.array([0.5 * L, 0.5 * L, 0.5 * H])
+        owner = mark_spheres((nxy, nxy, nz), (0.0, 0.0, 0.0), dx, (L, L, H), [cen], [sphere_radius * dx],
+                             (True, True, False))
+        rig = np.zeros(n, bool)
+        rig[:nf] = owner >= 0
+        st.kind[rig] = abi.RIGID
+        st.material[rig] = 2
+        st.group[rig] = 0
+        st.mass[rig] = rho_s * dx ** 3
+        st.density[rig] = rho_s
+        st.pressure[rig] = 0.0
+        nb = 1
+    bodies = empty_bodies(nb)
+    bodies["material"] = 2
+    body_quantities(st, bodies, params)
+    _finish(st, bodies)
+    info = dict(n=n, n_fluid=int((st.kind == abi.FLUID).sum()), n_rigid=int((st.kind == abi.RIGID).sum()),
+                n_boundary=nw, n_bodies=nb, H=H)
+    return Scenario(name, params, st, bodies, steps, info)
+
+
+def conduction_rod(nx=20, nyz=10, dx=1.0, rho=1.0, cp=1.0, kappa=1.0, T_lo=0.0, T_hi=1.0, name="rod", steps=0):
+    """The reference's steady-conduction KAT in 3D: a bar of particles 0 <= x <= nx dx
+    (periodic in y and z, so the problem is one-dimensional) between 3-layer Dirichlet end walls
+    held at T_lo (x < 0) and T_hi (x > nx dx).  The bar is a fixed (immobile) rigid body, so only
+    conduction acts; dt = 0.5 x the conduction limit 0.1 rho c_p h^2 / kappa."""
+    nl = 3
+    Lx = nx * dx
+    W = nyz * dx
+    lo = (-nl * dx, 0.0, 0.0)
+    hi = (Lx + nl * dx, W, W)
+    dt = 0.5 * 0.1 * rho * cp * dx * dx / kappa
+    mats = [material(rho, c=1.0, cp=cp, kappa=kappa), material(rho, cp=cp, kappa=kappa)]  # 0 fluid (unused), 1 solid
+    params = _params(dx, dt, lo, hi, (0, 1, 1), mats, tvf=0, thermal=1)
+    params.n_dirichlet = 2
+    for gidx, v in ((0, T_lo), (1, T_hi)):
+        params.dirichlet_T[gidx].n = 1
+        params.dirichlet_T[gidx].t_end[0] = 1e30
+        params.dirichlet_T[gidx].value[0] = v
+    pts = lattice_box(lo, hi, dx)
+    n = len(pts)
+    st = ParticleStore(n)
+    st.pos[:] = pts
+    wall = (pts[:, 0] < 0.0) | (pts[:, 0] > Lx)
+    st.kind[:] = abi.RIGID
+    st.kind[wall] = abi.BOUNDARY
+    st.material[:] = 1
+    st.group[~wall] = 0
+    st.mass[:] = rho * dx ** 3
+    st.density[:] = rho
+    st.dirichlet_T[pts[:, 0] < 0.0] = 0
+    st.dirichlet_T[pts[:, 0] > Lx] = 1
+    st.temperature[:] = 0.5 * (T_lo + T_hi)
+    st.temperature[pts[:, 0] < 0.0] = T_lo
+    st.temperature[pts[:, 0] > Lx] = T_hi
+    bodies = empty_bodies(1)
+    bodies["material"] = 1
+    bodies["mobile"] = 0
+    body_quantities(st, bodies, params)
+    _finish(st, bodies)
+    info = dict(n=n, n_fluid=0, n_rigid=int((~wall).sum()), n_boundary=int(wall.sum()), n_bodies=1, Lx=Lx)
     return Scenario(name, params, st, bodies, steps, info)
 
 

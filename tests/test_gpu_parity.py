@@ -497,8 +497,11 @@ def test_minimum_image_entry_mode(Oracle):
         "sim, orc = run_pair(sc, lambda p: Simulation(p, device=0), Oracle, init=False)\n"
         "sim.build_pairs(); orc.build_pairs()\n"
         "assert np.array_equal(sim.get_nlist()[1], orc.get_nlist()[1])\n"
-        "sim.initialize(); orc.initialize(); sim.step(2); orc.step(2)\n"
-        "compare_state(sim, orc, sc.params, tol=1e-9, what='imgmin')\n"
+        "sim.initialize(); orc.initialize(); sim.step(1); orc.step(1)\n"
+        "compare_state(sim, orc, sc.params, what='imgmin step1')\n"
+        "s, b = orc.download(); sim.upload(s, b); o2 = Oracle(sc.params); o2.upload(s, b)\n"
+        "sim.step(1); o2.step(1)\n"
+        "compare_state(sim, o2, sc.params, what='imgmin step2')\n"
         "print('ok')\n")
     env = dict(os.environ, SPHG_IMG_MIN="1")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -558,9 +561,10 @@ def test_without_transport_velocity(case, Oracle):
     sc = CASES[case]()
     sc.params.tvf = 0
     sim, orc = run_pair(sc, sim_factory, Oracle)
-    sim.step(2)
-    orc.step(2)
-    compare_state(sim, orc, sc.params, tol=1e-9, what=f"{case} tvf=0")
+    sim.step(1)
+    orc.step(1)
+    compare_state(sim, orc, sc.params, what=f"{case} tvf=0 step1")
+    step_from_identical_inputs(sim, orc, Oracle, sc.params, f"{case} tvf=0 step2")
 
 
 def test_heat_with_distinct_conductivities(Oracle):
@@ -571,9 +575,10 @@ def test_heat_with_distinct_conductivities(Oracle):
     p.mat[1].kappa = 35.0   # solid conducts better than the liquids
     p.mat[3].kappa = 5.0    # walls
     sim, orc = run_pair(sc, sim_factory, Oracle)
-    sim.step(2)
-    orc.step(2)
-    compare_state(sim, orc, p, tol=1e-9, what="multi-kappa heat")
+    sim.step(1)
+    orc.step(1)
+    compare_state(sim, orc, p, what="multi-kappa heat step1")
+    step_from_identical_inputs(sim, orc, Oracle, p, "multi-kappa heat step2")
 
 
 def test_compute_dt_uses_device_u_max(Oracle):
@@ -675,19 +680,82 @@ def test_graph_replay_is_bit_identical(monkeypatch, name, steps):
     assert np.array_equal(ba, bb)
 
 
+def _fast(sc, u):
+    """Fluid velocities raised to |u_i| ~ u so Verlet rebuilds happen within a few steps."""
+    fl = sc.store.kind == abi.FLUID
+    rng = np.random.default_rng(17)
+    sc.store.vel[fl] = rng.uniform(-u, u, (int(fl.sum()), 3))
+    sc.store.vel_adv[fl] = sc.store.vel[fl]
+    return sc
+
+
+SPEC_CASES = {"c2_melt_fast": lambda: _fast(CASES["c2_melt"](), 2.0),
+              "dissolve_fast": lambda: _fast(CASES["dissolve"](), 1.0)}
+
+
+@pytest.mark.parametrize("name", list(SPEC_CASES))
+def test_speculation_is_bit_identical(monkeypatch, name):
+    """sphg_step queues the force chain before it reads the kick chain's flags (speculation); when the
+    step needs a Verlet rebuild the queued chain voids itself and the host restores the state it
+    changed (buffer swaps, deferred final kick) before rebuilding.  A context created with
+    SPHG_SPECULATE=0 never speculates.  Same state bit for bit across rebuilds and phase transitions
+    (ADVICE r1)."""
+    sc = SPEC_CASES[name]()
+    a = sim_factory(sc.params)
+    monkeypatch.setenv("SPHG_SPECULATE", "0")
+    b = sim_factory(sc.params)
+    monkeypatch.delenv("SPHG_SPECULATE")
+    for e in (a, b):
+        e.upload(sc.store, sc.bodies)
+        e.initialize()
+    for k in (1, 5, 9):
+        a.step(k)
+        b.step(k)
+    sa, sb = a.stats(), b.stats()
+    assert sa.rebuilds == sb.rebuilds and sa.rebuilds >= 3, (sa.rebuilds, sb.rebuilds)
+    assert sa.transitions_melt + sa.transitions_solidify > 0
+    assert (sa.transitions_melt, sa.transitions_solidify) == (sb.transitions_melt, sb.transitions_solidify)
+    ga, ba = a.download()
+    gb, bb = b.download()
+    from paper_2103_07925_b200.store import SCALAR_FIELDS, TAG_FIELDS, VEC_FIELDS
+    for f in VEC_FIELDS + SCALAR_FIELDS + tuple(TAG_FIELDS):
+        assert np.array_equal(getattr(ga, f), getattr(gb, f)), f
+    assert np.array_equal(ba, bb)
+
+
 # BASELINE sizes that the oracle still steps in seconds: C2 (343k, heat + forced melting), C3 (2.41M,
-# two phases, 200 bodies) and the paper's own strong-scaling case (3.80M, 216 spheres, exact lattice)
+# two phases, 200 bodies), the paper's own strong-scaling case (3.80M, 216 spheres, exact lattice) and
+# C5 at one GPU's weak-scaling share (200^3 = 8M particles, 2500 spheres R ~ U[3, 6] dx: the headline
+# sphere density, three radix passes, 4-lane rigid groups)
 FULL = {
     "c2_full_melt": lambda: scenarios.config2(melt_forcing=True),
     "c3_full": lambda: scenarios.config3(),
     "paper46_full": lambda: scenarios.paper_strong_scaling(),
+    "c5_200": lambda: scenarios.config5(nside=200, n_spheres=2500),
 }
+
+
+def step_from_identical_inputs(sim, orc, Oracle, params, what, steps=1, compare_lists=True):
+    """One step of both engines from the SAME state: the oracle's state at t^n (store + body table,
+    bit for bit) is uploaded into the device (a warm upload: device order and Verlet rows kept) and
+    into a fresh oracle context, both step, and every field is compared at the 1e-10 bar.  (Stepping
+    each engine from its own previous step would compare two trajectories that already differ by the
+    1e-10 of the step before.)"""
+    o_state, o_bodies = orc.download()
+    sim.upload(o_state, o_bodies)
+    orc2 = Oracle(params)
+    orc2.upload(o_state, o_bodies)
+    del o_state
+    sim.step(steps)
+    orc2.step(steps)
+    compare_state(sim, orc2, params, what=what)
+    return orc2
 
 
 @pytest.mark.parametrize("case", list(FULL))
 def test_full_size_parity(case, Oracle):
-    """Cells, (cell, gid) order and Verlet lists bit-exact, then initialize() and one full step (flags
-    bit-exact, fields within 1e-10) at the BASELINE size, device vs oracle."""
+    """Cells, (cell, gid) order and Verlet lists bit-exact, then initialize() and one full step from
+    identical inputs (flags bit-exact, fields within 1e-10) at the BASELINE size, device vs oracle."""
     sc = FULL[case]()
     sim, orc = run_pair(sc, sim_factory, Oracle, init=False)
     for e in (sim, orc):
@@ -695,16 +763,12 @@ def test_full_size_parity(case, Oracle):
     cg, og = sim.get_cells()
     co, oo = orc.get_cells()
     assert np.array_equal(cg, co) and np.array_equal(og, oo), "cells / order differ"
+    del cg, og, co, oo
     offg, nbg = sim.get_nlist()
     offo, nbo = orc.get_nlist()
     assert np.array_equal(offg, offo) and np.array_equal(nbg, nbo), "neighbour lists differ"
-    del nbg, nbo
+    del nbg, nbo, offg, offo
     for e in (sim, orc):
         e.initialize()
     compare_state(sim, orc, sc.params, what=f"{case} init")
-    sim.step(1)
-    orc.step(1)
-    # step 1 starts from step 0's results, which agree only to the 1e-10 bar: the body accelerations
-    # enter every rigid particle's wall pressure through rho (g - a_w).(r_w - r_f), and at these sizes
-    # some rigid force sums hinge on that pressure (paper46: 1.4e-10 of p_w -> 1.37e-10 of f_r)
-    compare_state(sim, orc, sc.params, tol=1e-9, what=f"{case} step1")
+    step_from_identical_inputs(sim, orc, Oracle, sc.params, f"{case} step1")
