@@ -26,6 +26,8 @@ def load():
         dp = C.POINTER(C.c_double)
         lib.orc_get_scales.argtypes = [C.c_void_p] + [dp] * 7
         lib.orc_get_scales.restype = C.c_int
+        lib.orc_get_pscales.argtypes = [C.c_void_p, dp, dp]
+        lib.orc_get_pscales.restype = C.c_int
         lib.orc_get_scale_dC.argtypes = [C.c_void_p, dp]
         lib.orc_get_scale_dC.restype = C.c_int
         for f in ("orc_kernel_w", "orc_kernel_dw"):
@@ -63,7 +65,8 @@ class Oracle(Simulation):
         return Simulation.validate(params, lib or load(), "orc_")
 
     def scales(self):
-        """Per-particle sums of |pair contributions| (DESIGN.md §5 tolerance metric)."""
+        """Per-particle sums of |pair contributions| (DESIGN.md §5 tolerance metric), plus acc_p /
+        force_p: the pressure sensitivity sum |d term/d p| c^2 rho (absolute EOS allowance)."""
         n = self.n
         nb = self.num_bodies()
         out = {k: np.zeros(n) for k in ("acc", "acc_bg", "dT_dt", "force", "density")}
@@ -74,8 +77,11 @@ class Oracle(Simulation):
                                             bf.ctypes.data_as(dp), bt.ctypes.data_as(dp)), "scales")
         out["body_force"], out["body_torque"] = bf[:nb], bt[:nb]
         out["dC_dt"] = np.zeros(n)
+        out["acc_p"], out["force_p"] = np.zeros(n), np.zeros(n)
         if n:
             self._check(self.lib.orc_get_scale_dC(self._h, out["dC_dt"].ctypes.data_as(dp)), "scales")
+            self._check(self.lib.orc_get_pscales(self._h, out["acc_p"].ctypes.data_as(dp),
+                                                 out["force_p"].ctypes.data_as(dp)), "scales")
         return out
 
 

@@ -71,6 +71,10 @@ struct Ctx {
     std::vector<uint32_t> sorted;
     // tolerance scales (sum of |pair contributions|)
     std::vector<double> acc_scale, accbg_scale, dT_scale, force_scale, rho_scale, dC_scale;
+    // pressure sensitivity of acc (fluid) / f_r (rigid): sum over pairs of |d term / d p| x c^2 rho, the
+    // EOS-level magnitude behind each pressure (p = c^2 (rho - rho0) cancels): an absolute allowance of a
+    // few ulp of it covers the last-bit density differences any reordered density sum makes
+    std::vector<double> acc_pscale, force_pscale;
     std::vector<double> body_fscale, body_tscale;
     double t = 0.0;
     int64_t steps = 0, rebuilds = 0, n_melt = 0, n_solid = 0;
@@ -597,7 +601,8 @@ inline Side side_of(const Ctx& c, size_t j, const sphfsi::Material* eta_from) {
 // its parts.  It bounds |returned value| from above.
 inline double norm3(const V3& v);
 inline V3 pair_acc(const Ctx& c, const sphfsi::QuinticKernel<3>& K, const Side& I, double mi_, const Side& J,
-                   const V3& d, double r, V3& bgsum, double* mag = nullptr) {
+                   const V3& d, double r, V3& bgsum, double* mag = nullptr, double* psens = nullptr,
+                   double PI = 0.0, double PJ = 0.0) {
     const double dW = K.dw_dr(r);
     const V3 e = d / r;
     const V3 gW = dW * e;
@@ -621,6 +626,7 @@ inline V3 pair_acc(const Ctx& c, const sphfsi::QuinticKernel<3>& K, const Side& 
                         std::abs(J.rho * sphfsi::dot(J.du, gW)) * norm3(J.u));
         *mag = std::abs(V2 / mi_) * m;
     }
+    if (psens) *psens = std::abs(V2 / mi_) * std::abs(dW) * (J.rho * PI + I.rho * PJ) / (I.rho + J.rho);
     return (V2 / mi_) * term;
 }
 
@@ -640,7 +646,8 @@ bool stage_forces(Ctx& c) {
             const sphfsi::Material& mi_ = c.mats[c.S.material[i]];
             const Side I = side_of(c, (size_t)i, nullptr);
             V3 sum = V3::zero(), bg = V3::zero();
-            double sc = 0.0, bgsc = 0.0;
+            double sc = 0.0, bgsc = 0.0, psc = 0.0;
+            const double Pi = mi_.speed_of_sound * mi_.speed_of_sound * I.rho;  // EOS magnitude c^2 rho
             for (uint32_t j : c.nl[i]) {
                 const V3 d = mi3(c, c.S.pos[i], c.S.pos[j]);
                 const double r2 = r2of(d);
@@ -653,11 +660,15 @@ bool stage_forces(Ctx& c) {
                 }
                 const Side J = side_of(c, j, &mi_);
                 V3 bgp = V3::zero();
-                double mag = 0.0;
-                const V3 a = pair_acc(c, K, I, c.S.mass[i], J, d, r, bgp, &mag);
+                double mag = 0.0, ps = 0.0;
+                // a wall / rigid pressure is a Shepard average of fluid pressures: the fluid's EOS magnitude
+                const sphfsi::Material& mj = J.fluid ? c.mats[c.S.material[j]] : mi_;
+                const double Pj = mj.speed_of_sound * mj.speed_of_sound * J.rho;
+                const V3 a = pair_acc(c, K, I, c.S.mass[i], J, d, r, bgp, &mag, &ps, Pi, Pj);
                 sum += a;
                 bg += bgp;
                 sc += mag;
+                psc += ps;
                 bgsc += norm3(bgp);
             }
             const V3 b = v3(c.P.mat[c.S.material[i]].body_force);
@@ -665,11 +676,12 @@ bool stage_forces(Ctx& c) {
             const double f = c.P.tvf ? -mi_.background_pressure / c.S.mass[i] : 0.0;
             c.S.acc_bg[i] = f * bg;
             c.acc_scale[i] = sc + norm3(b);
+            c.acc_pscale[i] = psc;
             c.accbg_scale[i] = std::abs(f) * bgsc;
         } else if (ki == Kind::Rigid) {
             // coupling_force_on_rigid f_ri = -m_i a_ir + contact_force
             V3 f = V3::zero();
-            double sc = 0.0;
+            double sc = 0.0, psc = 0.0;
             const uint32_t body = c.S.group[i];
             for (uint32_t j : c.nl[i]) {
                 const Kind kj = c.S.kind[j];
@@ -687,11 +699,13 @@ bool stage_forces(Ctx& c) {
                     const Side Jf = side_of(c, j, nullptr);
                     const Side R = side_of(c, (size_t)i, &mj);
                     V3 bgp = V3::zero();
-                    double mag = 0.0;
-                    const V3 a = pair_acc(c, K, Jf, c.S.mass[j], R, d, r, bgp, &mag);
+                    double mag = 0.0, ps = 0.0;
+                    const double Pf = mj.speed_of_sound * mj.speed_of_sound * Jf.rho;
+                    const V3 a = pair_acc(c, K, Jf, c.S.mass[j], R, d, r, bgp, &mag, &ps, Pf, Pf);
                     const V3 fr = (-c.S.mass[j]) * a;
                     f += fr;
                     sc += c.S.mass[j] * mag;
+                    psc += c.S.mass[j] * ps;
                 } else if (kj == Kind::Boundary || c.S.group[j] != body) {
                     const V3 d = mi3(c, c.S.pos[i], c.S.pos[j]);
                     const double r2 = r2of(d);
@@ -712,6 +726,7 @@ bool stage_forces(Ctx& c) {
             }
             c.force[i] = f;
             c.force_scale[i] = sc;
+            c.force_pscale[i] = psc;
         }
     }
     if (coincident)
@@ -1114,6 +1129,8 @@ void resize_aux(Ctx& c) {
     c.dT_scale.assign(n, 0.0);
     c.dC_scale.assign(n, 0.0);
     c.force_scale.assign(n, 0.0);
+    c.acc_pscale.assign(n, 0.0);
+    c.force_pscale.assign(n, 0.0);
     c.rho_scale.assign(n, 0.0);
 }
 
@@ -1466,6 +1483,13 @@ int orc_shepard_grid(orc_ctx* h, const double* origin, const double* spacing, co
 int orc_get_scale_dC(orc_ctx* h, double* dC) {
     const Ctx& c = *reinterpret_cast<Ctx*>(h);
     std::copy(c.dC_scale.begin(), c.dC_scale.end(), dC);
+    return SPHG_OK;
+}
+
+int orc_get_pscales(orc_ctx* h, double* acc, double* force) {
+    const Ctx& c = *reinterpret_cast<Ctx*>(h);
+    std::copy(c.acc_pscale.begin(), c.acc_pscale.end(), acc);
+    std::copy(c.force_pscale.begin(), c.force_pscale.end(), force);
     return SPHG_OK;
 }
 

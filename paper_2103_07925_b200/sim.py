@@ -187,9 +187,12 @@ class Simulation:
                                           order.ctypes.data_as(C.POINTER(C.c_uint32))), "get_cells")
         return cell, order
 
-    def get_nlist(self):
+    def get_nlist(self, offsets_only=False):
+        """Verlet candidate lists (CSR by gid, rows gid-sorted); offsets_only: just the n+1 offsets."""
         off = np.zeros(self.n + 1, np.int64)
         self._check(self._fn("get_nlist")(self._h, off.ctypes.data_as(C.POINTER(C.c_int64)), None), "get_nlist")
+        if offsets_only:
+            return off
         nbr = np.zeros(int(off[-1]), np.uint32)
         self._check(self._fn("get_nlist")(self._h, off.ctypes.data_as(C.POINTER(C.c_int64)),
                                           nbr.ctypes.data_as(C.POINTER(C.c_uint32))), "get_nlist")

@@ -26,7 +26,7 @@ STEPS = 2
 OUT_FIELDS = ("pos", "vel", "density", "pressure", "acc", "acc_bg", "force", "temperature", "dT_dt",
               "wall_pressure", "wall_velocity", "kind", "group", "material", "concentration", "dC_dt",
               "dirichlet_C")
-SCALE_KEYS = ("acc", "acc_bg", "dT_dt", "force", "density", "body_force", "body_torque", "dC_dt")
+SCALE_KEYS = ("acc", "acc_bg", "dT_dt", "force", "density", "body_force", "body_torque", "dC_dt", "acc_p", "force_p")
 
 CASES = {
     "c1": lambda: scenarios.config1(nside=10, n_spheres=2, r_range=(1.5, 2.5), seed=3),

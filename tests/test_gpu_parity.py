@@ -4,6 +4,8 @@ Bars (BASELINE north_star): cells, sort order and Verlet lists bit-exact;
 density / acceleration / temperature rate / body force & torque within 1e-10
 (DESIGN.md §5 metric); phase flags bit-exact after step 1.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -742,14 +744,47 @@ def step_from_identical_inputs(sim, orc, Oracle, params, what, steps=1, compare_
     each engine from its own previous step would compare two trajectories that already differ by the
     1e-10 of the step before.)"""
     o_state, o_bodies = orc.download()
+    orc.close()  # at the headline size two oracle contexts would not fit the host's RAM
     sim.upload(o_state, o_bodies)
     orc2 = Oracle(params)
     orc2.upload(o_state, o_bodies)
     del o_state
     sim.step(steps)
     orc2.step(steps)
-    compare_state(sim, orc2, params, what=what)
+    orc2.last_errors = compare_state(sim, orc2, params, what=what)
     return orc2
+
+
+def _host_ram_gb():
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 1e9
+    except (ValueError, OSError):
+        return 0.0
+
+
+def test_headline_c5_parity(Oracle):
+    """The headline workload itself (BASELINE configs[4], C5: 400^3 = 64M particles, 20,000 spheres, one
+    GPU): cell ids and (cell, gid) order bit-exact, every particle's Verlet candidate count equal (the
+    lists themselves are compared entry by entry at 8M, c5_200), initialize() and one step from identical
+    inputs within 1e-10.  Needs ~150 GB of host RAM for the oracle (the B200 box has 196 GB)."""
+    if _host_ram_gb() < 150:
+        pytest.skip(f"host RAM {_host_ram_gb():.0f} GB < 150 GB for the 64M oracle")
+    sc = scenarios.config5()
+    sim, orc = run_pair(sc, sim_factory, Oracle, init=False)
+    sc.store = None
+    for e in (sim, orc):
+        e.build_pairs()
+    cg, og = sim.get_cells()
+    co, oo = orc.get_cells()
+    assert np.array_equal(cg, co) and np.array_equal(og, oo), "cells / order differ"
+    del cg, og, co, oo
+    assert np.array_equal(sim.get_nlist(offsets_only=True), orc.get_nlist(offsets_only=True)), "counts differ"
+    for e in (sim, orc):
+        e.initialize()
+    e0 = compare_state(sim, orc, sc.params, what="c5 64M init")
+    print("c5 64M init: max error / tolerance per field", e0)
+    o2 = step_from_identical_inputs(sim, orc, Oracle, sc.params, "c5 64M step1")
+    print("c5 64M step 1 (identical inputs): max error / tolerance per field", o2.last_errors)
 
 
 @pytest.mark.parametrize("case", list(FULL))
