@@ -2,6 +2,7 @@
 // MEASURED_PEAKS.json carries HBM and bf16 only).  8 independent FMA chains per
 // thread, 148 SMs x 8 blocks x 256 threads, CUDA events, best of 5.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __global__ void k_dfma(double* out, int iters, double a, double b) {
@@ -18,7 +19,8 @@ __global__ void k_dfma(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const double sustain_s = argc > 1 ? atof(argv[1]) : 0.0;  // > 0: also back to back for this long
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* d;
@@ -39,9 +41,21 @@ int main() {
     if (ms < best) best = ms;
   }
   const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
-  int clk = 0;
-  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-  printf("{\"fp64_tflops\": %.3f, \"ms\": %.3f, \"sms\": %d, \"how\": \"DFMA microbenchmark tools/fp64_peak.cu, 8 chains x 256 thr x %d blocks, best of 5\"}\n",
-         flops / (best * 1e-3) / 1e12, best, sms, blocks);
+  double sustained = 0.0;
+  int reps = 0;
+  float total = 0.f;
+  if (sustain_s > 0.0) {  // back-to-back launches for sustain_s seconds (power / clock steady state)
+    cudaEventRecord(e0);
+    reps = (int)(sustain_s * 1e3 / best) + 1;
+    for (int r = 0; r < reps; ++r) k_dfma<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&total, e0, e1);
+    sustained = flops * reps / (total * 1e-3) / 1e12;
+  }
+  printf("{\"fp64_tflops\": %.3f, \"fp64_tflops_sustained\": %.3f, \"ms\": %.3f, \"sustained_s\": %.3f, "
+         "\"sms\": %d, \"how\": \"DFMA microbenchmark tools/fp64_peak.cu, 8 chains x 256 thr x %d blocks: best of 5 "
+         "(burst) and %d launches back to back (sustained)\"}\n",
+         flops / (best * 1e-3) / 1e12, sustained, best, total * 1e-3, sms, blocks, reps);
   return 0;
 }
