@@ -24,31 +24,44 @@ __device__ __forceinline__ uint32_t hash(uint32_t x) {
 }
 
 template <int MODE>
+__device__ __forceinline__ uint32_t index_of(uint32_t seed, int lane, uint32_t window) {
+  const int grp = lane >> 2, sub = lane & 3;
+  if (MODE == 0) return (hash(seed + grp) % (window - 4)) + sub;          // unaligned groups of 4
+  if (MODE == 1) return ((hash(seed + grp) % (window / 4)) * 4) + sub;    // aligned groups (one line each)
+  if (MODE == 2) return hash(seed + lane) % window;                       // random
+  if (MODE == 3) return ((seed % (window / 4)) * 4) + sub;                // every group on the same line
+  return ((seed % (window / 32)) * 32) + lane;                            // 32 consecutive, aligned
+}
+
+// U independent iterations in flight (3 loads each), addresses from a precomputed per-lane table so
+// the loop is load-throughput bound, not latency bound
+template <int MODE>
 __global__ void __launch_bounds__(128) k_gather(const double4* __restrict__ a, const double4* __restrict__ b,
                                                  const double4* __restrict__ c, uint32_t window, int iters,
                                                  double* __restrict__ out) {
-  const int lane = threadIdx.x & 31, grp = lane >> 2, sub = lane & 3;
+  constexpr int U = 4, T = 16;
+  const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t base = (warp * 977u) % (64u * 1024u * 1024u / 2u);  // per-warp window start
+  const uint32_t base = (warp * 977u) % (64u * 1024u * 1024u / 2u);
+  __shared__ uint32_t tab[4][T][32];
+  const int w = threadIdx.x >> 5;
+  for (int t = 0; t < T; ++t) tab[w][t][lane] = base + index_of<MODE>(hash(warp * 131u + t), lane, window);
+  __syncwarp();
   double s = 0.0;
-  uint32_t seed = warp * 0x9E3779B9u;
-  for (int it = 0; it < iters; ++it) {
-    seed = hash(seed + it);
-    uint32_t idx;
-    if (MODE == 0) {         // unaligned groups of 4 consecutive
-      idx = (hash(seed + grp) % (window - 4)) + sub;
-    } else if (MODE == 1) {  // aligned groups (one line each)
-      idx = ((hash(seed + grp) % (window / 4)) * 4) + sub;
-    } else if (MODE == 2) {  // random
-      idx = hash(seed + lane) % window;
-    } else if (MODE == 3) {  // every group on the same line
-      idx = ((seed % (window / 4)) * 4) + sub;
-    } else {                 // 32 consecutive, aligned
-      idx = ((seed % (window / 32)) * 32) + lane;
+  for (int it = 0; it < iters; it += U) {
+    double4 x[U], y[U], z[U];
+    // a data dependence the compiler cannot see through (the records are zeros: dep stays 0), so
+    // every iteration's loads are really issued
+    const uint32_t dep = (uint32_t)__double_as_longlong(s) & 1u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t idx = tab[w][(it + u) & (T - 1)][lane] + dep;
+      x[u] = ldg4(a + idx);
+      y[u] = ldg4(b + idx);
+      z[u] = ldg4(c + idx);
     }
-    idx += base;
-    const double4 x = ldg4(a + idx), y = ldg4(b + idx), z = ldg4(c + idx);
-    s += x.x + y.y + z.z + x.w;
+#pragma unroll
+    for (int u = 0; u < U; ++u) s += x[u].x + y[u].y + z[u].z + x[u].w;
   }
   if (s == 12345.678) out[0] = s;
 }
