@@ -295,6 +295,21 @@ int sphg_body_partials(sphg_ctx* ctx, double* out);
 int sphg_body_apply_totals(sphg_ctx* ctx, const double* totals);
 /* Max displacement since the last rebuild over owned particles (after a KICK_DRIFT stage). */
 int sphg_max_displacement(sphg_ctx* ctx, double* out);
+/* Transition event log ("Event log (CSV): step, particle id, direction, body ids"): when enabled,
+ * every applied transition is recorded as (step, gid, direction 1 melt / 2 solidify, body it left (melt)
+ * or -1, body it ended the batch in (solidify, after splits) or -1), ordered by step then gid.
+ * sphg_transition_events copies up to `cap` of the events recorded since the last call into `out`
+ * (out may be NULL to query), stores the number copied (or pending, with out = NULL) in *n and drops
+ * the copied ones. */
+typedef struct {
+  int64_t step;
+  uint32_t gid;
+  int32_t direction;
+  int32_t body_from;
+  int32_t body_to;
+} sphg_event;
+int sphg_set_event_log(sphg_ctx* ctx, int enabled);
+int sphg_transition_events(sphg_ctx* ctx, sphg_event* out, size_t cap, size_t* n);
 const char* sphg_last_error(const sphg_ctx* ctx);
 void sphg_destroy(sphg_ctx* ctx);
 /* Messages of validate_config for `params` joined by '\n' (empty = valid). */

@@ -94,6 +94,9 @@ struct Ctx {
     // runtime time-step assertion [P22]
     double m_r = 0.0;              // smallest mass a rigid particle can have in this run (0: none)
     int64_t dt_violations = 0;
+    // transition event log (sphg_set_event_log)
+    bool event_log = false;
+    std::vector<sphg_event> events;
     int dt_term = -1;
     double dt_limit = std::numeric_limits<double>::infinity();
 };
@@ -981,8 +984,11 @@ bool stage_transitions(Ctx& c) {
     // 1. melts: rigid -> fluid with the body's rigid-motion velocity
     std::vector<char> melting(n, 0);
     for (uint32_t r : melt) melting[r] = 1;
+    std::vector<sphg_event> batch;
+    const int64_t ev_step = c.steps + 1;
     for (uint32_t r : melt) {
         const uint32_t k = c.S.group[r];
+        if (c.event_log) batch.push_back(sphg_event{ev_step, r, 1, (int32_t)k, -1});
         const sphg_body& b = c.bodies[k];
         const V3 rk = sphfsi::rotate(qof(b), c.S.body_frame_pos[r]);
         const V3 u = v3(b.vel) + sphfsi::cross(v3(b.omega), rk);
@@ -1093,6 +1099,11 @@ bool stage_transitions(Ctx& c) {
         }
     }
     rebuild_members(c);
+    if (c.event_log) {  // solidified particles with the body they ended the batch in; all ordered by gid
+        for (uint32_t i : solid) batch.push_back(sphg_event{ev_step, i, 2, -1, (int32_t)c.S.group[i]});
+        std::sort(batch.begin(), batch.end(), [](const sphg_event& a, const sphg_event& b) { return a.gid < b.gid; });
+        c.events.insert(c.events.end(), batch.begin(), batch.end());
+    }
     // 4. mass quantities + post-transition velocity u_k = u'_k + w x (r_k - r'_k) [P12]
     for (size_t k = 0; k < c.bodies.size(); ++k) {
         if (k >= affected.size() || !affected[k]) continue;
@@ -1483,6 +1494,24 @@ int orc_shepard_grid(orc_ctx* h, const double* origin, const double* spacing, co
 int orc_get_scale_dC(orc_ctx* h, double* dC) {
     const Ctx& c = *reinterpret_cast<Ctx*>(h);
     std::copy(c.dC_scale.begin(), c.dC_scale.end(), dC);
+    return SPHG_OK;
+}
+
+int orc_set_event_log(orc_ctx* h, int enabled) {
+    reinterpret_cast<Ctx*>(h)->event_log = enabled != 0;
+    return SPHG_OK;
+}
+
+int orc_transition_events(orc_ctx* h, sphg_event* out, size_t cap, size_t* n) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (!out) {
+        *n = c.events.size();
+        return SPHG_OK;
+    }
+    const size_t m = std::min(cap, c.events.size());
+    std::copy(c.events.begin(), c.events.begin() + m, out);
+    c.events.erase(c.events.begin(), c.events.begin() + m);
+    *n = m;
     return SPHG_OK;
 }
 

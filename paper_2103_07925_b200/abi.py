@@ -115,6 +115,15 @@ class Stats(C.Structure):
                 ("pad3", C.c_int32), ("dt_limit", C.c_double)]
 
 
+class Event(C.Structure):
+    """sphg_event: one applied transition (SPEC:502 event log)."""
+    _fields_ = [("step", C.c_int64), ("gid", C.c_uint32), ("direction", C.c_int32),
+                ("body_from", C.c_int32), ("body_to", C.c_int32)]
+
+
+MELT, SOLIDIFY = 1, 2  # sphg_event.direction
+
+
 # void fn(int32 group, double t, double vel[3], double acc[3], void* user)  (sphg_set_wall_motion)
 WALL_MOTION_FN = C.CFUNCTYPE(None, C.c_int32, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
                              C.c_void_p)
@@ -153,6 +162,8 @@ def declare(lib, prefix):
         "halo_doubles": (C.c_int, [C.c_int]),
         "upload_state": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_size_t]),
         "set_wall_motion": (C.c_int, [vp, C.c_int32, WALL_MOTION_FN, C.c_void_p]),
+        "set_event_log": (C.c_int, [vp, C.c_int]),
+        "transition_events": (C.c_int, [vp, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t)]),
         "shepard_grid": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                    C.c_int32, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint8)]),
     }

@@ -1491,6 +1491,24 @@ int sphg_max_displacement(sphg_ctx* h, double* out) {
   return SPHG_OK;
 }
 
+int sphg_set_event_log(sphg_ctx* h, int enabled) {
+  h->c.event_log = enabled != 0;
+  return SPHG_OK;
+}
+
+int sphg_transition_events(sphg_ctx* h, sphg_event* out, size_t cap, size_t* n) {
+  Ctx& c = h->c;
+  if (!out) {
+    *n = c.events.size();
+    return SPHG_OK;
+  }
+  const size_t m = std::min(cap, c.events.size());
+  std::copy(c.events.begin(), c.events.begin() + m, out);
+  c.events.erase(c.events.begin(), c.events.begin() + m);
+  *n = m;
+  return SPHG_OK;
+}
+
 const char* sphg_last_error(const sphg_ctx* h) { return h ? h->c.err.c_str() : "null context"; }
 
 void sphg_destroy(sphg_ctx* h) {
@@ -1513,6 +1531,7 @@ void sphg_destroy(sphg_ctx* h) {
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
   c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();
   c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();
+  c.label_list.free(); c.label_flags.free(); c.ev_log.free(); c.ev_count.free();
   c.fidx.free(); c.widx.free(); c.ncon.free(); c.brick_buf.free(); c.scan_cells.free(); c.dl_buf.free(); c.idx_of_gid.free(); c.body_buf.free();
   for (auto& b : c.halo_ids) b.free();
   if (c.dflags) cudaFree(c.dflags);

@@ -114,6 +114,12 @@ struct Ctx {
   void* wall_user = nullptr;
   // transitions scratch
   DBuf<uint32_t> ev_idx, ev_flag, label, tscratch;
+  DBuf<uint32_t> label_list, label_flags;  // compact list of labelled particles; sweep flags + count
+  // transition event log (sphg_set_event_log): device buffer of the current batch, host accumulation
+  bool event_log = false;
+  DBuf<sphg_event> ev_log;
+  DBuf<uint32_t> ev_count;
+  std::vector<sphg_event> events;
   // flags
   DevFlags* dflags = nullptr;   // device
   DevFlags* hflags = nullptr;   // pinned host mirror

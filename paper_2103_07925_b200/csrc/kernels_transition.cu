@@ -14,6 +14,8 @@
 //    members follow the rigid motion, then reduce_force_torque for all bodies.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "context.cuh"
 
 namespace sphg {
@@ -44,11 +46,13 @@ __global__ void k_detect(const __grid_constant__ DevParams P, Particles D, size_
 }
 
 __global__ void k_melt(const __grid_constant__ DevParams P, Particles D, size_t n, const uint32_t* __restrict__ ev,
-                       const sphg_body* __restrict__ B, uint32_t* __restrict__ bmask, uint32_t* __restrict__ blost) {
+                       const sphg_body* __restrict__ B, uint32_t* __restrict__ bmask, uint32_t* __restrict__ blost,
+                       sphg_event* __restrict__ log, uint32_t* __restrict__ nlog, int64_t step) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n || ev[k] != 1) return;
   const uint32_t kmd = D.kmd.p[k];
   const uint32_t body = D.group.p[k];
+  if (log) log[atomicAdd(nlog, 1u)] = sphg_event{step, D.gid.p[k], 1, (int32_t)body, -1};
   const sphg_body& b = B[body];
   const double4 x = D.X4.p[k];
   const double3 rk = qrotate(body_q(b), make_double3(x.x, x.y, x.z));
@@ -163,31 +167,45 @@ __global__ void k_solid_apply(const __grid_constant__ DevParams P, Particles D, 
   if (D.C2.p) reinterpret_cast<double*>(&D.C2.p[i])[1] = v.w / rho0;
 }
 
+// event log: every solidified particle with the body it ended the batch in (after splits)
+__global__ void k_log_solid(Particles D, const uint32_t* __restrict__ list, size_t m, sphg_event* __restrict__ log,
+                            uint32_t* __restrict__ nlog, int64_t step) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const uint32_t i = list[e];
+  log[atomicAdd(nlog, 1u)] = sphg_event{step, D.gid.p[i], 2, -1, (int32_t)D.group.p[i]};
+}
+
 __global__ void k_iota(uint32_t* __restrict__ a, size_t n, size_t from) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) a[from + k] = (uint32_t)(from + k);
 }
 
 // ---------------------------------------------------- connected components
-__global__ void k_label_init(Particles D, size_t n, const uint32_t* __restrict__ blost, uint32_t* __restrict__ label) {
+// Rigid particles of bodies that lost particles get label = gid, the others NONE; the labels then
+// relax to the minimum gid of their component (adjacency r <= 1.5 dx within one body).  The relaxation
+// runs entirely on the device: the labelled particles are compacted into a list and one cooperative
+// kernel iterates over that list with grid-wide barriers until a sweep changes nothing (no host
+// round trip per sweep, no full-store launch per sweep).
+__global__ void k_label_init(Particles D, size_t n, const uint32_t* __restrict__ blost, uint32_t* __restrict__ label,
+                             uint32_t* __restrict__ list, uint32_t* __restrict__ count) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  label[k] = (kind_of(D.kmd.p[k]) == SPHG_RIGID && blost[D.group.p[k]]) ? D.gid.p[k] : 0xffffffffu;
+  const bool on = kind_of(D.kmd.p[k]) == SPHG_RIGID && blost[D.group.p[k]];
+  label[k] = on ? D.gid.p[k] : 0xffffffffu;
+  if (on) list[atomicAdd(count, 1u)] = (uint32_t)k;  // order is irrelevant: the fixpoint is unique
 }
 
-__global__ void k_label_iter(const __grid_constant__ DevParams P, Particles D, size_t n, NbrList L,
-                             uint32_t* __restrict__ label, double adj2, DevFlags* __restrict__ fl) {
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  uint32_t l = label[i];
-  if (l == 0xffffffffu) return;
+__device__ __forceinline__ bool label_relax(const DevParams& P, const Particles& D, const NbrList& L,
+                                            uint32_t* label, double adj2, uint32_t i) {
+  const uint32_t l = label[i];
   const uint32_t body = D.group.p[i];
   const double4 pi = D.G0.p[i];
   uint32_t best = l;
   const uint32_t nn = cnt_total(L.cnt[i]);  // whole row (see k_solid_target)
-  const uint32_t* row = L.nbr + i * L.cap;
+  const uint32_t* row = L.nbr + (size_t)i * L.cap;
   for (uint32_t k = 0; k < nn; ++k) {
-    const uint32_t j = entry_index(P, row[k]);
+    const uint32_t j = P.img_mode == kImgCode ? (row[k] & kIdxMask) : row[k];
     if (kind_of(D.kmd.p[j]) != SPHG_RIGID || D.group.p[j] != body) continue;
     const double4 pj = D.G0.p[j];
     if (r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) > adj2) continue;
@@ -195,7 +213,37 @@ __global__ void k_label_iter(const __grid_constant__ DevParams P, Particles D, s
   }
   if (best < l) {
     atomicMin(&label[i], best);
-    fl->changed = 1;
+    return true;
+  }
+  return false;
+}
+
+// cooperative: grid-stride sweeps over the list, grid barrier, stop when a sweep changed nothing.
+// flags[0..1]: double-buffered "changed" words (cleared one sweep ahead); flags[2]: sweeps done
+__global__ void k_label_coop(const __grid_constant__ DevParams P, Particles D, NbrList L, const uint32_t* __restrict__ list,
+                             const uint32_t* __restrict__ count, uint32_t* __restrict__ label, double adj2,
+                             uint32_t* __restrict__ flags) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t m = *count;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+  for (uint32_t sweep = 0;; ++sweep) {
+    if (sweep >= 1000000u) {  // cannot happen (labels only decrease); never spin forever
+      if (tid == 0) flags[2] = 0xffffffffu;
+      return;
+    }
+    uint32_t* changed = flags + (sweep & 1u);
+    if (tid == 0) flags[(sweep + 1) & 1u] = 0u;  // the next sweep's word; nobody reads it this sweep
+    bool any = false;
+    for (size_t e = tid; e < m; e += stride) any |= label_relax(P, D, L, label, adj2, list[e]);
+    if (any) atomicOr(changed, 1u);
+    grid.sync();
+    const uint32_t c = *reinterpret_cast<volatile uint32_t*>(changed);
+    if (!c) {
+      if (tid == 0) flags[2] = sweep + 1;
+      return;
+    }
+    grid.sync();  // every thread has read `changed` before it is cleared two sweeps later
   }
 }
 
@@ -395,8 +443,20 @@ int launch_transitions(Ctx& c) {
   SPHG_CUDA_CHECK(cudaMemsetAsync(bmask, 0, 2 * cap * sizeof(uint32_t), s));
   k_iota<<<grid_for(cap, 256), 256, 0, s>>>(src, cap, 0);
   if (nb0) SPHG_CUDA_CHECK(cudaMemcpyAsync(old.p, c.bodies.p, nb0 * sizeof(sphg_body), cudaMemcpyDeviceToDevice, s));
+  // event log (sphg_set_event_log): this batch's events, drained to the host at the end of the batch
+  sphg_event* elog = nullptr;
+  uint32_t* nlog = nullptr;
+  if (c.event_log) {
+    c.ev_log.alloc(nmelt + nsolid + 1);
+    c.ev_count.alloc(1);
+    SPHG_CUDA_CHECK(cudaMemsetAsync(c.ev_count.p, 0, sizeof(uint32_t), s));
+    elog = c.ev_log.p;
+    nlog = c.ev_count.p;
+  }
+  const int64_t step = c.steps + 1;
   // 1. melt
-  if (nmelt) k_melt<<<grid_for(n, 256), 256, 0, s>>>(c.P, c.cur, n, c.ev_flag.p, c.bodies.p, bmask, blost);
+  if (nmelt)
+    k_melt<<<grid_for(n, 256), 256, 0, s>>>(c.P, c.cur, n, c.ev_flag.p, c.bodies.p, bmask, blost, elog, nlog, step);
   // 2. solidify: events in gid order, attach or spawn
   size_t nspawn = 0;
   if (nsolid) {
@@ -422,14 +482,30 @@ int launch_transitions(Ctx& c) {
   // 3. split bodies that lost particles
   if (nmelt) {
     c.label.alloc(n);
-    k_label_init<<<grid_for(n, 256), 256, 0, s>>>(c.cur, n, blost, c.label.p);
+    c.label_list.alloc(n);
+    c.label_flags.alloc(4);
+    SPHG_CUDA_CHECK(cudaMemsetAsync(c.label_flags.p, 0, 4 * sizeof(uint32_t), s));
+    k_label_init<<<grid_for(n, 256), 256, 0, s>>>(c.cur, n, blost, c.label.p, c.label_list.p, c.label_flags.p + 3);
     const double adj2 = (1.5 * c.P.dx) * (1.5 * c.P.dx);
-    for (int it = 0; it < 100000; ++it) {
-      SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->changed, 0, sizeof(uint32_t), s));
-      k_label_iter<<<grid_for(n, 128), 128, 0, s>>>(c.P, c.cur, n, c.nl(), c.label.p, adj2, c.dflags);
-      c.launches += 2;
-      if (!read_u32(c, &c.dflags->changed)) break;
+    // one cooperative launch: as many blocks as can be co-resident
+    static int coop_blocks = 0;
+    if (!coop_blocks) {
+      int per_sm = 0, sms = 0;
+      SPHG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_label_coop, 256, 0));
+      SPHG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+      coop_blocks = std::max(1, per_sm) * sms;
     }
+    DevParams Pv = c.P;
+    Particles Dv = c.cur;
+    NbrList Lv = c.nl();
+    const uint32_t* lp = c.label_list.p;
+    const uint32_t* cp = c.label_flags.p + 3;
+    uint32_t* labp = c.label.p;
+    double a2 = adj2;
+    uint32_t* fp = c.label_flags.p;
+    void* args[] = {&Pv, &Dv, &Lv, &lp, &cp, &labp, &a2, &fp};
+    SPHG_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_label_coop, dim3(coop_blocks), dim3(256), args, 0, s));
+    c.launches += 2;
     const int gbits = bits_for(n - 1);
     k_split_roots<<<grid_for(n, 256), 256, 0, s>>>(c.cur, n, c.label.p, c.ridx.p, c.body_start.p, gbits, c.keys.p,
                                                    c.vals.p, c.dflags);
@@ -448,6 +524,10 @@ int launch_transitions(Ctx& c) {
       c.launches += 2;
     }
   }
+  if (elog && nsolid) {
+    k_log_solid<<<grid_for(nsolid, 128), 128, 0, s>>>(c.cur, c.ev_idx.p, nsolid, elog, nlog, step);
+    c.launches++;
+  }
   // 4. mass quantities + post-transition velocity + member velocities
   launch_mass(c, bmask);
   k_post_velocity<<<grid_for(c.nb, 128), 128, 0, s>>>(c.P, c.bodies.p, old.p, bmask, src, c.nb, nb0);
@@ -457,6 +537,13 @@ int launch_transitions(Ctx& c) {
   launch_bodies(c);
   SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
   old.free();
+  if (elog) {  // drain this batch's events to the host, ordered by gid (each particle once per batch)
+    const size_t m = (size_t)nmelt + nsolid;
+    std::vector<sphg_event> ev(m);
+    SPHG_CUDA_CHECK(cudaMemcpy(ev.data(), elog, m * sizeof(sphg_event), cudaMemcpyDeviceToHost));
+    std::sort(ev.begin(), ev.end(), [](const sphg_event& a, const sphg_event& b) { return a.gid < b.gid; });
+    c.events.insert(c.events.end(), ev.begin(), ev.end());
+  }
   c.n_melt += nmelt;
   c.n_solid += nsolid;
   // kinds changed: the rows' fluid / non-fluid partition is stale; body ids changed: contact order

@@ -164,6 +164,7 @@ class OutputPlan:
     grid_interval: int = 0
     grid: GridSpec = None
     prefix: str = "sph"
+    event_log: bool = False  # transition event log CSV: step,particle,direction,body_from,body_to
 
 
 def _wants(plan, step, traj):
@@ -203,6 +204,11 @@ def run(sim, nsteps, plan, log=None):
     (status, message): 0 ok, 2 config violation, 3 runtime assertion (escaped / coincident
     particle, non-finite state), 4 device failure — the SPEC's exit codes."""
     os.makedirs(plan.out_dir, exist_ok=True)
+    events = None
+    if plan.event_log:
+        sim.set_event_log(True)
+        events = open(os.path.join(plan.out_dir, plan.prefix + "_transitions.csv"), "w", newline="\n")
+        events.write("step,particle,direction,body_from,body_to\n")
     traj = TrajectoryWriter(os.path.join(plan.out_dir, plan.prefix + "_bodies.csv")) if plan.trajectory_interval else None
     intervals = [i for i in (plan.snapshot_interval, plan.trajectory_interval,
                              plan.grid_interval if plan.grid is not None else 0) if i]
@@ -220,11 +226,24 @@ def run(sim, nsteps, plan, log=None):
                 got = None
             step = nxt
             store = _write_outputs(sim, plan, step, traj, store, got)
+            if events is not None:
+                _write_events(events, sim.transition_events())
             if log:
                 log("step %d t=%s" % (step, _g(sim.stats().time)))
     except SPHError as e:
+        if events is not None:
+            _write_events(events, sim.transition_events())
         return e.code, str(e)
+    finally:
+        if events is not None:
+            events.close()
     return 0, "ok"
+
+
+def _write_events(fh, ev):
+    names = {1: "melt", 2: "solidify"}
+    for e in ev:
+        fh.write("%d,%d,%s,%d,%d\n" % (e["step"], e["gid"], names[int(e["direction"])], e["body_from"], e["body_to"]))
 
 
 def scaling_report(lines, path):

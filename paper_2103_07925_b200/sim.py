@@ -246,6 +246,21 @@ class Simulation:
                     "shepard_grid")
         return out.reshape(tuple(d) + (nc,)), sup.reshape(tuple(d)).astype(bool)
 
+    def set_event_log(self, enabled=True):
+        """Record every applied transition (SPEC:502 event log); drained by transition_events()."""
+        self._check(self._fn("set_event_log")(self._h, int(bool(enabled))), "set_event_log")
+
+    def transition_events(self):
+        """The transitions recorded since the last call: structured array (step, gid, direction 1 melt /
+        2 solidify, body_from, body_to), ordered by step then gid."""
+        n = C.c_size_t(0)
+        self._check(self._fn("transition_events")(self._h, None, 0, C.byref(n)), "transition_events")
+        buf = (abi.Event * max(n.value, 1))()
+        self._check(self._fn("transition_events")(self._h, buf, n.value, C.byref(n)), "transition_events")
+        dt = np.dtype([("step", "i8"), ("gid", "u4"), ("direction", "i4"), ("body_from", "i4"), ("body_to", "i4")])
+        assert dt.itemsize == C.sizeof(abi.Event)
+        return np.frombuffer(bytes(buf), dt, count=n.value).copy()
+
     def count_pairs(self):
         """(candidates, interacting, interacting with fluid i, interacting with non-fluid i)."""
         out = (C.c_int64 * 4)()

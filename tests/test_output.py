@@ -129,3 +129,55 @@ def test_scaling_report(tmp_path):  # (workers, wall time/step, effici
     assert rows[1] == "1,0.01,100.0" and rows[2] == "2,0.00625,80.0" and rows[3] == "4,0.0025,100.0"
     weak = [{"n_gpus": 1, "ms_per_step": 10.0, "scaling": "weak"}, {"n_gpus": 8, "ms_per_step": 12.5, "scaling": "weak"}]
     assert open(scaling_report(weak, p)).read().splitlines()[2] == "8,0.0125,80.0"
+
+
+def _melt_case():
+    return scenarios.config2(nside=12, n_grid=2, r_range=(2.0, 3.0), seed=5, melt_forcing=True)
+
+
+def test_transition_event_log(tmp_path):  # "Event log (CSV): step, particle id, direction, body ids"
+    from oracle.oracle import Oracle
+    sc = _melt_case()
+    sim = Oracle(sc.params)
+    sim.upload(sc.store, sc.bodies)
+    sim.initialize()
+    sim.set_event_log(True)
+    before, _ = sim.download()
+    sim.step(1)
+    ev = sim.transition_events()
+    after, _ = sim.download()
+    st = sim.stats()
+    melt, solid = ev[ev["direction"] == abi.MELT], ev[ev["direction"] == abi.SOLIDIFY]
+    assert len(melt) == st.transitions_melt > 0 and len(solid) == st.transitions_solidify > 0
+    assert np.all(ev["step"] == 1) and np.all(np.diff(ev["gid"].astype(np.int64)) > 0)
+    assert np.all(before.kind[melt["gid"]] == abi.RIGID) and np.all(after.kind[melt["gid"]] == abi.FLUID)
+    assert np.array_equal(melt["body_from"], before.group[melt["gid"]].astype(np.int32)) and np.all(melt["body_to"] == -1)
+    assert np.all(after.kind[solid["gid"]] == abi.RIGID)
+    assert np.array_equal(solid["body_to"], after.group[solid["gid"]].astype(np.int32)) and np.all(solid["body_from"] == -1)
+    assert len(sim.transition_events()) == 0  # drained
+    # through the run loop: one CSV row per event
+    sim2 = Oracle(sc.params)
+    sim2.upload(sc.store, sc.bodies)
+    sim2.initialize()
+    assert run(sim2, 3, OutputPlan(out_dir=str(tmp_path), trajectory_interval=2, event_log=True)) == (0, "ok")
+    rows = open(tmp_path / "sph_transitions.csv").read().splitlines()
+    st2 = sim2.stats()
+    assert rows[0] == "step,particle,direction,body_from,body_to"
+    assert len(rows) - 1 == st2.transitions_melt + st2.transitions_solidify
+    assert rows[1].split(",")[:3] == ["1", str(int(ev["gid"][0])), "melt" if ev["direction"][0] == 1 else "solidify"]
+
+
+@pytest.mark.gpu
+def test_transition_event_log_device_matches_oracle():
+    from oracle.oracle import Oracle
+    from paper_2103_07925_b200 import Simulation
+    sc = _melt_case()
+    out = []
+    for make in (lambda p: Simulation(p, device=0), Oracle):
+        e = make(sc.params)
+        e.upload(sc.store, sc.bodies)
+        e.initialize()
+        e.set_event_log(True)
+        e.step(3)
+        out.append(e.transition_events())
+    assert len(out[0]) > 0 and np.array_equal(out[0], out[1])
