@@ -70,6 +70,25 @@ typedef struct {
   double value[SPHG_MAX_PIECES];
 } sphg_schedule;
 
+/* Inflow / outflow buffer zone ("a buffer-zone with prescribed parabolic velocity and
+ * particle recycling"; §4.4 inlet/outlet) [P23].  A FLUID particle whose position lies in
+ * the zone box (lo <= x < hi on every axis) is a buffer particle: it is not accelerated by the pair
+ * forces but moves with the prescribed velocity U(x, t) = e_axis u_mean f(xi) for t > t_start (0 before:
+ * the zone is held at rest), f = 6 xi (1 - xi) with xi = (x_p - lo_p) / (hi_p - lo_p) along profile_axis
+ * (parabolic, mean 1), or f = 1 with profile_axis = -1.  It keeps every other fluid role (density
+ * summation, EOS, pair forces on its neighbours, transport velocity = U).  Roles follow the position,
+ * so a particle becomes fluid when it leaves an inflow zone and a buffer particle when it enters an
+ * outflow zone; with the inflow and outflow zones at the two ends of a periodic axis the periodic wrap
+ * recycles outflow particles into the inflow zone (particle count and mass stay exact). */
+#define SPHG_MAX_BUFFERS 4
+typedef struct {
+  int32_t axis;          /* flow axis 0..2 */
+  int32_t profile_axis;  /* transverse axis of the parabolic profile, -1 = uniform */
+  double lo[3], hi[3];   /* zone box */
+  double u_mean;         /* mean velocity along the axis (signed) */
+  double t_start;        /* prescribed for t > t_start; at rest before */
+} sphg_buffer;
+
 /* Flat POD derived from sphfsi::ScenarioConfig<3> (config.hpp:68-106). */
 typedef struct {
   double dx;                 /* initial spacing */
@@ -115,7 +134,8 @@ typedef struct {
    * condition (the step itself completes); SPHG_DT_WARN counts it in the stats (SURVEY App. A15:
    * BASELINE C1/C5 prescribe a dt above the contact limit); SPHG_DT_OFF skips the check. */
   int32_t dt_check;
-  int32_t pad_dt;
+  int32_t n_buffers;             /* inflow / outflow buffer zones (sphg_buffer, [P23]) */
+  sphg_buffer buffers[SPHG_MAX_BUFFERS];
 } sphg_params;
 
 enum { SPHG_DT_REFUSE = 0, SPHG_DT_WARN = 1, SPHG_DT_OFF = 2 };

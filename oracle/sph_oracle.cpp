@@ -222,6 +222,14 @@ std::vector<std::string> validate(const sphg_params& P) {
     if (P.transitions < 0 || P.transitions > 2) v.push_back("unknown transition mode");
     if (P.transitions == 2 && !P.diffusion) v.push_back("concentration transitions need the diffusion equation");
     if (P.default_fluid_mat < 0 || P.default_fluid_mat >= P.n_mat) v.push_back("default fluid material missing");
+    if (P.n_buffers < 0 || P.n_buffers > SPHG_MAX_BUFFERS) v.push_back("buffer zone count out of range");
+    for (int b = 0; b < P.n_buffers && b < SPHG_MAX_BUFFERS; ++b) {  // [P23]
+        const sphg_buffer& B = P.buffers[b];
+        if (B.axis < 0 || B.axis > 2 || B.profile_axis < -1 || B.profile_axis > 2 || B.profile_axis == B.axis)
+            v.push_back("buffer zone axes invalid");
+        for (int a = 0; a < 3; ++a)
+            if (!(B.hi[a] > B.lo[a])) v.push_back("buffer zone box is empty");
+    }
     if (P.heat_source) {  // [P21]
         if (!P.thermal) v.push_back("heat source needs the heat equation");
         if (!(P.hs_radius > 0.0)) v.push_back("heat source radius must be positive");
@@ -869,6 +877,36 @@ bool stage_mass(Ctx& c) {
 
 // ------------------------------------------------------------ integrator
 // step(): half kick, drift, orientation, slave [P14]
+// Inflow / outflow buffer zones [P23] (sphg.h sphg_buffer): the zone of a fluid particle at
+// x (first zone whose box lo <= x < hi holds it) or -1, and the zone's prescribed velocity at x when
+// the zone is active at time t (t > t_start), U = e_axis u_mean 6 xi (1 - xi) along profile_axis.
+int buffer_of(const Ctx& c, const V3& x) {
+    for (int b = 0; b < c.P.n_buffers; ++b) {
+        const sphg_buffer& B = c.P.buffers[b];
+        bool in = true;
+        for (int a = 0; a < 3; ++a) in = in && x[a] >= B.lo[a] && x[a] < B.hi[a];
+        if (in) return b;
+    }
+    return -1;
+}
+
+V3 buffer_velocity(const Ctx& c, int b, const V3& x, double t) {
+    const sphg_buffer& B = c.P.buffers[b];
+    double u = 0.0;
+    if (t > B.t_start) {
+        double f = 1.0;
+        if (B.profile_axis >= 0) {
+            const int a = B.profile_axis;
+            const double xi = (x[a] - B.lo[a]) / (B.hi[a] - B.lo[a]);
+            f = (6.0 * xi) * (1.0 - xi);
+        }
+        u = B.u_mean * f;
+    }
+    V3 v = V3::zero();
+    v[B.axis] = u;
+    return v;
+}
+
 bool stage_kick_drift(Ctx& c) {
     const double hdt = 0.5 * c.dt, dt = c.dt;
     if (c.n_walls > 0) {
@@ -894,8 +932,9 @@ bool stage_kick_drift(Ctx& c) {
     for (int64_t i = 0; i < n; ++i) {
         const Kind k = ghost(c, (size_t)i) ? Kind::Boundary : c.S.kind[i];  // ghosts move by halo only
         if (k == Kind::Fluid) {
-            const V3 uh = c.S.vel[i] + hdt * c.S.acc[i];
-            const V3 ua = c.P.tvf ? uh + hdt * c.S.acc_bg[i] : uh;
+            const int zb = c.P.n_buffers ? buffer_of(c, c.S.pos[i]) : -1;  // [P23], role from x^n
+            const V3 uh = zb >= 0 ? buffer_velocity(c, zb, c.S.pos[i], c.t + hdt) : c.S.vel[i] + hdt * c.S.acc[i];
+            const V3 ua = (c.P.tvf && zb < 0) ? uh + hdt * c.S.acc_bg[i] : uh;
             c.S.vel[i] = uh;
             c.S.vel_adv[i] = ua;
             c.S.pos[i] = wrap3(c, c.S.pos[i] + dt * ua);
@@ -946,7 +985,8 @@ bool stage_final_kick(Ctx& c) {
     for (int64_t i = 0; i < n; ++i) {
         if (ghost(c, (size_t)i)) continue;
         if (c.S.kind[i] == Kind::Fluid) {
-            c.S.vel[i] = c.S.vel[i] + hdt * c.S.acc[i];
+            const int zb = c.P.n_buffers ? buffer_of(c, c.S.pos[i]) : -1;  // [P23], role from x^{n+1}
+            c.S.vel[i] = zb >= 0 ? buffer_velocity(c, zb, c.S.pos[i], c.t) : c.S.vel[i] + hdt * c.S.acc[i];
         } else if (c.S.kind[i] == Kind::Rigid) {
             const sphg_body& b = c.bodies[c.S.group[i]];
             const V3 rk = sphfsi::rotate(qof(b), c.S.body_frame_pos[i]);

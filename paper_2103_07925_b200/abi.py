@@ -53,6 +53,15 @@ class Schedule(C.Structure):
                 ("t_end", C.c_double * MAX_PIECES), ("value", C.c_double * MAX_PIECES)]
 
 
+MAX_BUFFERS = 4
+
+
+class Buffer(C.Structure):
+    """sphg_buffer: inflow / outflow buffer zone with a prescribed (parabolic) velocity [P23]."""
+    _fields_ = [("axis", C.c_int32), ("profile_axis", C.c_int32), ("lo", C.c_double * 3), ("hi", C.c_double * 3),
+                ("u_mean", C.c_double), ("t_start", C.c_double)]
+
+
 class Params(C.Structure):
     """Flat POD of sphfsi::ScenarioConfig<3> (config.hpp:68-106)."""
     _fields_ = [("dx", C.c_double), ("h", C.c_double), ("dt", C.c_double), ("t0", C.c_double),
@@ -73,7 +82,7 @@ class Params(C.Structure):
                 ("hs_power", C.c_double), ("hs_radius", C.c_double),
                 ("hs_origin", C.c_double * 3), ("hs_velocity", C.c_double * 3),
                 # runtime time-step assertion: DT_REFUSE / DT_WARN / DT_OFF
-                ("dt_check", C.c_int32), ("pad_dt", C.c_int32)]
+                ("dt_check", C.c_int32), ("n_buffers", C.c_int32), ("buffers", Buffer * MAX_BUFFERS)]
 
 
 _dp = C.POINTER(C.c_double)

@@ -92,6 +92,14 @@ std::vector<std::string> validate(const sphg_params& P) {  // restates config.hp
   if (P.transitions < 0 || P.transitions > 2) fail("unknown transition mode");
   if (P.transitions == 2 && !P.diffusion) fail("concentration transitions need the diffusion equation");
   if (P.default_fluid_mat < 0 || P.default_fluid_mat >= P.n_mat) fail("default fluid material missing");
+  if (P.n_buffers < 0 || P.n_buffers > SPHG_MAX_BUFFERS) fail("buffer zone count out of range");
+  for (int b = 0; b < P.n_buffers && b < SPHG_MAX_BUFFERS; ++b) {
+    const sphg_buffer& B = P.buffers[b];
+    if (B.axis < 0 || B.axis > 2 || B.profile_axis < -1 || B.profile_axis > 2 || B.profile_axis == B.axis)
+      fail("buffer zone axes invalid");
+    for (int a = 0; a < 3; ++a)
+      if (!(B.hi[a] > B.lo[a])) fail("buffer zone box is empty");
+  }
   if (P.heat_source) {  // [P21]
     if (!P.thermal) fail("heat source needs the heat equation");
     if (!(P.hs_radius > 0.0)) fail("heat source radius must be positive");
@@ -207,6 +215,16 @@ DevParams make_dev_params(const sphg_params& p) {
   P.hs_lat2 = 0.5625 * p.dx * p.dx;
   P.transitions = p.transitions;
   P.default_fluid_mat = p.default_fluid_mat;
+  P.n_buf = p.n_buffers;
+  for (int b = 0; b < p.n_buffers && b < SPHG_MAX_BUFFERS; ++b) {
+    P.buf[b].axis = p.buffers[b].axis;
+    P.buf[b].paxis = p.buffers[b].profile_axis;
+    for (int a = 0; a < 3; ++a) {
+      P.buf[b].lo[a] = p.buffers[b].lo[a];
+      P.buf[b].hi[a] = p.buffers[b].hi[a];
+    }
+    P.buf[b].u_mean = p.buffers[b].u_mean;
+  }
   for (int a = 0; a < 3; ++a) {
     P.lo[a] = p.lo[a];
     P.hi[a] = p.hi[a];
@@ -341,6 +359,15 @@ void eval_walls(Ctx& c, double t, double (*vel)[3], double (*acc)[3]) {
 }
 
 void kick_all(Ctx& c) {
+  if (c.P.n_buf > 0) {  // which buffer zones prescribe their velocity at t^n, t^{n+1/2}, t^{n+1} [P23]
+    c.P.buf_prev = c.P.buf_half = c.P.buf_new = 0u;
+    for (int b = 0; b < c.P.n_buf; ++b) {
+      const double ts = c.params.buffers[b].t_start;
+      if (c.t > ts) c.P.buf_prev |= 1u << b;
+      if (c.t + 0.5 * c.P.dt > ts) c.P.buf_half |= 1u << b;
+      if (c.t + c.P.dt > ts) c.P.buf_new |= 1u << b;
+    }
+  }
   if (c.P.n_walls > 0) {
     eval_walls(c, c.t + 0.5 * c.P.dt, c.P.wall_vh, nullptr);
     eval_walls(c, c.t + c.P.dt, c.P.wall_v, c.P.wall_a);

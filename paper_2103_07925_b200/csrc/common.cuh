@@ -69,6 +69,14 @@ struct DevParams {
   // speculative step (api.cu one_step): set on the device by the tail of the kick chain when the step
   // needs a Verlet rebuild (or hit an error); every kernel of the force chain then returns at once
   const uint32_t* skip;
+  // inflow / outflow buffer zones [P23] (sphg_buffer); bit b of buf_half / buf_new / buf_prev: zone b
+  // prescribes its velocity at t^{n+1/2} / t^{n+1} / t^n (t > t_start), set by the host every kick
+  struct Buf {
+    int32_t axis, paxis;
+    double lo[3], hi[3], u_mean;
+  } buf[SPHG_MAX_BUFFERS];
+  int32_t n_buf;
+  uint32_t buf_half, buf_new, buf_prev;
 };
 #define SPHG_SKIP_IF_FLAGGED(P) \
   do {                          \
@@ -228,6 +236,33 @@ __device__ __forceinline__ bool shepard_shape(const DP& P, double3 d, double r2,
   const double q = r2 >= P.rc2_ulp ? pinned_q(d, P.rc2, P.inv_h, ri) : sqrt_and_rinv(r2 + 1e-300, ri) * P.inv_h;
   W = q >= 3.0 ? 0.0 : shape_q(q);
   return true;
+}
+
+// ------------------------------------------------------- buffer zones [P23]
+// zone of a fluid particle at x (first zone whose box holds it), -1 outside every zone
+__device__ __forceinline__ int buffer_of(const DevParams& P, double x, double y, double z) {
+  for (int b = 0; b < P.n_buf; ++b) {
+    const DevParams::Buf& B = P.buf[b];
+    if (x >= B.lo[0] && x < B.hi[0] && y >= B.lo[1] && y < B.hi[1] && z >= B.lo[2] && z < B.hi[2]) return b;
+  }
+  return -1;
+}
+// prescribed velocity U(x) of zone b (pinned arithmetic: the drift is a bit-exact stage), 0 when the
+// zone is not active at the time the caller's mask describes
+__device__ __forceinline__ double3 buffer_velocity(const DevParams& P, int b, double x, double y, double z,
+                                                   uint32_t active) {
+  const DevParams::Buf& B = P.buf[b];
+  double u = 0.0;
+  if ((active >> b) & 1u) {
+    double f = 1.0;
+    if (B.paxis >= 0) {
+      const double xp = B.paxis == 0 ? x : (B.paxis == 1 ? y : z);
+      const double xi = __ddiv_rn(__dsub_rn(xp, B.lo[B.paxis]), __dsub_rn(B.hi[B.paxis], B.lo[B.paxis]));
+      f = __dmul_rn(__dmul_rn(6.0, xi), __dsub_rn(1.0, xi));
+    }
+    u = __dmul_rn(B.u_mean, f);
+  }
+  return make_double3(B.axis == 0 ? u : 0.0, B.axis == 1 ? u : 0.0, B.axis == 2 ? u : 0.0);
 }
 
 // ------------------------------------------------- neighbour-list entries

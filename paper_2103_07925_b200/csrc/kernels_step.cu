@@ -82,21 +82,32 @@ __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevP
     bool moved = true;
     if (kind == SPHG_FLUID) {
       const double4 a = D.A4.p[k];
+      const double3 p = ldpos(&D.G0.p[k]);
+      // a buffer-zone particle moves with the zone's prescribed velocity [P23] (role from x^n)
+      const int zb = P.n_buf ? buffer_of(P, p.x, p.y, p.z) : -1;
       double3 v;
       if (kFinal) {
-        const double3 uprev = ldpos(&D.G1.p[k]);
-        v = make_double3(axpy_rn(uprev.x, P.hdt, a.x), axpy_rn(uprev.y, P.hdt, a.y), axpy_rn(uprev.z, P.hdt, a.z));
+        if (zb >= 0) {
+          v = buffer_velocity(P, zb, p.x, p.y, p.z, P.buf_prev);
+        } else {
+          const double3 uprev = ldpos(&D.G1.p[k]);
+          v = make_double3(axpy_rn(uprev.x, P.hdt, a.x), axpy_rn(uprev.y, P.hdt, a.y), axpy_rn(uprev.z, P.hdt, a.z));
+        }
         stpos(&D.V4.p[k], v);
       } else {
         v = ldpos(&D.V4.p[k]);
       }
-      const double3 uh = make_double3(axpy_rn(v.x, P.hdt, a.x), axpy_rn(v.y, P.hdt, a.y), axpy_rn(v.z, P.hdt, a.z));
-      double3 ua = uh;
-      if (P.tvf) {
-        const double4 bg = D.B4.p[k];
-        ua = make_double3(axpy_rn(uh.x, P.hdt, bg.x), axpy_rn(uh.y, P.hdt, bg.y), axpy_rn(uh.z, P.hdt, bg.z));
+      double3 uh, ua;
+      if (zb >= 0) {
+        uh = ua = buffer_velocity(P, zb, p.x, p.y, p.z, P.buf_half);
+      } else {
+        uh = make_double3(axpy_rn(v.x, P.hdt, a.x), axpy_rn(v.y, P.hdt, a.y), axpy_rn(v.z, P.hdt, a.z));
+        ua = uh;
+        if (P.tvf) {
+          const double4 bg = D.B4.p[k];
+          ua = make_double3(axpy_rn(uh.x, P.hdt, bg.x), axpy_rn(uh.y, P.hdt, bg.y), axpy_rn(uh.z, P.hdt, bg.z));
+        }
       }
-      const double3 p = ldpos(&D.G0.p[k]);
       pn = make_double3(wrap1(P, axpy_rn(p.x, P.dt, ua.x), 0), wrap1(P, axpy_rn(p.y, P.dt, ua.y), 1),
                         wrap1(P, axpy_rn(p.z, P.dt, ua.z), 2));
       stpos(&D.G0.p[k], pn);
@@ -181,9 +192,18 @@ __global__ void __launch_bounds__(256) k_final_kick(const __grid_constant__ DevP
   if (is_ghost(kmd)) return;
   const uint32_t kind = kind_of(kmd);
   if (kind == SPHG_FLUID) {
+    const double m = D.V4.p[k].w;
+    if (P.n_buf) {  // role from x^{n+1} [P23]
+      const double3 p = ldpos(&D.G0.p[k]);
+      const int zb = buffer_of(P, p.x, p.y, p.z);
+      if (zb >= 0) {
+        const double3 u = buffer_velocity(P, zb, p.x, p.y, p.z, P.buf_new);
+        D.V4.p[k] = make_double4(u.x, u.y, u.z, m);
+        return;
+      }
+    }
     const double3 uh = ldpos(&D.G1.p[k]);
     const double4 a = D.A4.p[k];
-    const double m = D.V4.p[k].w;
     D.V4.p[k] = make_double4(axpy_rn(uh.x, P.hdt, a.x), axpy_rn(uh.y, P.hdt, a.y), axpy_rn(uh.z, P.hdt, a.z), m);
   } else if (kind == SPHG_RIGID) {
     const sphg_body& b = B[D.group.p[k]];

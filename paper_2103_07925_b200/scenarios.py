@@ -908,6 +908,73 @@ def conduction_rod(nx=20, nyz=10, dx=1.0, rho=1.0, cp=1.0, kappa=1.0, T_lo=0.0, 
     return Scenario(name, params, st, bodies, steps, info)
 
 
+def buffer_channel(nx=32, ny=10, nz=16, dx=1e-3, dt=1e-5, rho=1000.0, c=10.0, nu=1e-6, u_mean=0.05,
+                   t_start=0.0, zone=4, jitter=0.05, seed=2131, name="channel", steps=200):
+    """Inflow / outflow buffer zones (§4.4) [P23]: a channel
+    periodic in x and y between 3-layer walls below z = 0 and above z = H.  The first `zone` dx of x are
+    the inflow zone and the last `zone` dx the outflow zone; both prescribe the parabolic profile
+    u_x = u_mean 6 xi (1 - xi), xi = z / H, for t > t_start.  The periodic wrap carries particles
+    leaving the outflow zone into the inflow zone (particle recycling)."""
+    Lx, W, H = nx * dx, ny * dx, nz * dx
+    nl = 3
+    lo = (0.0, 0.0, -nl * dx)
+    hi = (Lx, W, H + nl * dx)
+    mats = [material(rho, nu=nu, c=c, pb=rho * c * c), material(rho, c=c)]  # 0 fluid, 1 wall
+    params = _params(dx, dt, lo, hi, (1, 1, 0), mats)
+    params.n_buffers = 2
+    for b, (x0, x1) in enumerate(((0.0, zone * dx), (Lx - zone * dx, Lx))):
+        B = params.buffers[b]
+        B.axis, B.profile_axis = 0, 2
+        B.lo[0], B.hi[0] = x0, x1
+        B.lo[1], B.hi[1] = 0.0, W
+        B.lo[2], B.hi[2] = 0.0, H
+        B.u_mean, B.t_start = u_mean, t_start
+    fl = lattice_box((0.0, 0.0, 0.0), (Lx, W, H), dx)
+    wl = lattice_box(lo, hi, dx)
+    wl = wl[(wl[:, 2] < 0.0) | (wl[:, 2] > H)]
+    nf, nw = len(fl), len(wl)
+    st = ParticleStore(nf + nw)
+    u = splitmix_u01(seed, 0, np.arange(3 * nf, dtype=np.uint64)).reshape(nf, 3)
+    pos = fl + (2.0 * u - 1.0) * (jitter * dx)
+    for a in range(2):
+        pos[:, a] = np.mod(pos[:, a], (Lx, W)[a])
+    st.pos[:nf] = pos
+    st.pos[nf:] = wl
+    st.kind[nf:] = abi.BOUNDARY
+    st.material[nf:] = 1
+    st.mass[:] = rho * dx ** 3
+    st.density[:] = rho
+    bodies = empty_bodies(0)
+    _finish(st, bodies)
+    info = dict(n=nf + nw, n_fluid=nf, n_rigid=0, n_boundary=nw, n_bodies=0, rigid_fraction=0.0, H=H, Lx=Lx)
+    return Scenario(name, params, st, bodies, steps, info)
+
+
+def buffer_velocity_host(params, pos, t):
+    """The prescribed velocity of every position inside a buffer zone at time t (NaN outside), with the
+    pinned arithmetic of sphg_buffer [P23] (numpy float64, no FMA): a host check for the tests."""
+    out = np.full((len(pos), 3), np.nan)
+    done = np.zeros(len(pos), bool)
+    for b in range(params.n_buffers):
+        B = params.buffers[b]
+        inside = ~done
+        for a in range(3):
+            inside &= (pos[:, a] >= B.lo[a]) & (pos[:, a] < B.hi[a])
+        u = np.zeros(int(inside.sum()))
+        if t > B.t_start:
+            f = np.ones_like(u)
+            if B.profile_axis >= 0:
+                a = B.profile_axis
+                xi = (pos[inside, a] - B.lo[a]) / (B.hi[a] - B.lo[a])
+                f = (6.0 * xi) * (1.0 - xi)
+            u = B.u_mean * f
+        v = np.zeros((len(u), 3))
+        v[:, B.axis] = u
+        out[inside] = v
+        done |= inside
+    return out
+
+
 def config4(**kw):
     """BASELINE configs[3] (C4): powder bed under a moving Gaussian heat flux (powder_bed)."""
     return powder_bed(**kw)
@@ -926,4 +993,4 @@ def config2(**kw):
 def by_name(name, **kw):
     return {"c1": config1, "c2": config2, "c3": config3, "c4": config4, "c5": config5, "dissolve": dissolving_bodies,
             "paper46": paper_strong_scaling,
-            "couette": couette_channel}[name](**kw)
+            "couette": couette_channel, "channel": buffer_channel}[name](**kw)
