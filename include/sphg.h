@@ -216,6 +216,7 @@ typedef struct {
   int64_t graph_captures;     /* CUDA graphs captured for the per-step launch chains (SPHG_GRAPHS=0: none) */
   int64_t graph_replays;      /* chain launches served by an already captured graph */
   int64_t dt_violations;      /* steps whose dt exceeded a compute_dt limit (runtime assertion, SPHG_DT_WARN) */
+  int64_t host_syncs;         /* host-blocking waits on the device since creation (stream / event syncs) */
   int32_t dt_term;            /* the most restrictive limit at the last check: 0 cfl, 1 viscous, 2 body force,
                                  3 contact, 4 conduction (-1: none checked) */
   int32_t pad3;
@@ -307,6 +308,35 @@ int sphg_halo_doubles(int phase);
 int sphg_halo_set(sphg_ctx* ctx, int slot, const uint32_t* local_ids, size_t n);
 int sphg_halo_pack(sphg_ctx* ctx, int phase, int slot, double* buf);
 int sphg_halo_unpack(sphg_ctx* ctx, int phase, int slot, const double* buf);
+/* In-library decomposed step (bulk-synchronous).  With ghosts present and an
+ * exchange callback set, sphg_step(ctx, K) runs the whole decomposed step on the library's stream:
+ * kick / drift, MAX exchange (global max displacement and u_max), one flag readback (the Verlet
+ * decision and error check), STATE halo (the interior density runs meanwhile on a second stream),
+ * [rank-local rebuild], boundary density, DENSITY halo, [heat], extrapolation, WALL halo, forces, body
+ * partials -> BODIES all-gather -> rank-order TwoSum merge on the device, final kick.  At each exchange
+ * point the library has packed the bound send buffers on `stream` and calls fn(phase, stream, user);
+ * fn enqueues the transfers so that, in the order of `stream`, the bound receive buffers (the MAX words,
+ * the body gather buffer) hold the peers' data before any later work on it (NCCL through
+ * torch.distributed on an external stream does this without blocking the host).  Halo slots as
+ * sphg_halo_set: per peer k, send slot 2k and receive slot 2k+1. */
+enum { SPHG_XCHG_MAX = 3, SPHG_XCHG_BODIES = 4 };
+typedef int (*sphg_exchange_fn)(int32_t phase, void* stream, void* user);
+int sphg_set_exchange(sphg_ctx* ctx, sphg_exchange_fn fn, void* user);
+/* the library's cudaStream_t (as void*) */
+int sphg_get_stream(sphg_ctx* ctx, void** stream);
+/* device buffer of (phase, slot): halo records of sphg_halo_doubles(phase) doubles per listed particle */
+int sphg_halo_bind(sphg_ctx* ctx, int phase, int slot, double* dev_buf);
+/* device buffer of the two words the MAX exchange reduces in place (MAX over ranks): the squared max
+ * displacement and the squared max fluid speed of this step, as the bits of non-negative doubles (so an
+ * integer MAX is the double MAX; a local runtime error is sent as +inf) */
+int sphg_max_bind(sphg_ctx* ctx, uint64_t* dev_words);
+/* [0] global max displacement since the last rebuild, [1] sum of the global displacements at the
+ * rebuilds since the last upload (with [0]: a bound on any particle's drift since it was partitioned),
+ * [2] global max fluid speed of the last kick */
+int sphg_drift(sphg_ctx* ctx, double out[3]);
+/* body partials (nb x 24 doubles, as sphg_body_partials) are written to dev_partials; the BODIES exchange
+ * all-gathers them into dev_gathered (world x nb x 24, rank order) */
+int sphg_body_bind(sphg_ctx* ctx, double* dev_partials, double* dev_gathered, int32_t world);
 /* Per-body compensated partial sums over owned rigid particles: nb x 24 doubles (12 x (sum, comp):
  * f xyz, torque xyz, inertia xx yy zz xy xz yz).  `out` / `totals` may be host or device pointers
  * (unified addressing), so an NCCL driver gathers and merges them without host staging. */

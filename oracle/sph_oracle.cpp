@@ -97,6 +97,16 @@ struct Ctx {
     // transition event log (sphg_set_event_log)
     bool event_log = false;
     std::vector<sphg_event> events;
+    // in-library decomposed step (sphg.h): exchange callback + bound host buffers
+    sphg_exchange_fn exch_fn = nullptr;
+    void* exch_user = nullptr;
+    double* halo_buf[3][SPHG_MAX_HALO_SLOTS] = {};
+    uint64_t* max_words = nullptr;
+    double* body_part = nullptr;
+    double* body_gath = nullptr;
+    int world = 1;
+    bool has_ghosts = false;
+    double disp_since_partition = 0.0;
     int dt_term = -1;
     double dt_limit = std::numeric_limits<double>::infinity();
 };
@@ -1349,6 +1359,8 @@ int orc_upload(orc_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t nb
     c.halo.assign(SPHG_MAX_HALO_SLOTS, {});
     bool any_ghost = false;
     for (size_t i = 0; i < n; ++i) any_ghost |= ghost(c, i);
+    c.has_ghosts = any_ghost;
+    c.disp_since_partition = 0.0;
     if (any_ghost && c.P.transitions) {
         c.err = "phase transitions are single-rank only (ghost particles present)";
         return SPHG_ERR_CONFIG;
@@ -1411,10 +1423,18 @@ int orc_upload_state(orc_ctx* h, const double* pos, const double* vel, size_t n)
     return SPHG_OK;
 }
 
+int decomposed_step(orc_ctx* h);
+
 int orc_step(orc_ctx* h, int nsteps) {
     Ctx& c = *reinterpret_cast<Ctx*>(h);
-    for (int k = 0; k < nsteps; ++k)
-        if (!one_step(c)) return SPHG_ERR_RUNTIME;
+    for (int k = 0; k < nsteps; ++k) {
+        if (c.has_ghosts && c.exch_fn) {
+            const int rc = decomposed_step(h);
+            if (rc) return rc;
+        } else if (!one_step(c)) {
+            return SPHG_ERR_RUNTIME;
+        }
+    }
     return SPHG_OK;
 }
 
@@ -1729,6 +1749,126 @@ int orc_body_apply_totals(orc_ctx* h, const double* tot) {
         }
     }
     return SPHG_OK;
+}
+
+// ---- in-library decomposed step (sphg.h), the oracle's restatement of api.cu one_step_decomposed:
+// the same stage order, exchange points and rank-order TwoSum merge of the body partials (host buffers)
+int orc_set_exchange(orc_ctx* h, sphg_exchange_fn fn, void* user) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    c.exch_fn = fn;
+    c.exch_user = user;
+    return SPHG_OK;
+}
+int orc_get_stream(orc_ctx*, void** stream) {
+    *stream = nullptr;
+    return SPHG_OK;
+}
+int orc_halo_bind(orc_ctx* h, int phase, int slot, double* buf) {
+    if (phase < 0 || phase > 2 || slot < 0 || slot >= SPHG_MAX_HALO_SLOTS) return SPHG_ERR_CONFIG;
+    reinterpret_cast<Ctx*>(h)->halo_buf[phase][slot] = buf;
+    return SPHG_OK;
+}
+int orc_max_bind(orc_ctx* h, uint64_t* words) {
+    reinterpret_cast<Ctx*>(h)->max_words = words;
+    return SPHG_OK;
+}
+int orc_body_bind(orc_ctx* h, double* part, double* gath, int32_t world) {
+    if (world < 1) return SPHG_ERR_CONFIG;
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    c.body_part = part;
+    c.body_gath = gath;
+    c.world = world;
+    return SPHG_OK;
+}
+int orc_drift(orc_ctx* h, double out[3]) {
+    const Ctx& c = *reinterpret_cast<Ctx*>(h);
+    out[0] = c.max_disp;
+    out[1] = c.disp_since_partition;
+    out[2] = c.u_max;
+    return SPHG_OK;
+}
+
+static int xchg(Ctx& c, int phase) {
+    if (c.exch_fn(phase, nullptr, c.exch_user)) {
+        c.err = "exchange callback failed in phase " + std::to_string(phase);
+        return SPHG_ERR_CUDA;
+    }
+    return SPHG_OK;
+}
+
+static int halo_xchg(orc_ctx* h, int phase) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    for (int slot = 0; slot < SPHG_MAX_HALO_SLOTS; slot += 2)
+        if (!c.halo[slot].empty()) {
+            if (!c.halo_buf[phase][slot]) return SPHG_ERR_CONFIG;
+            orc_halo_pack(h, phase, slot, c.halo_buf[phase][slot]);
+        }
+    const int rc = xchg(c, phase);
+    if (rc) return rc;
+    for (int slot = 1; slot < SPHG_MAX_HALO_SLOTS; slot += 2)
+        if (!c.halo[slot].empty()) {
+            if (!c.halo_buf[phase][slot]) return SPHG_ERR_CONFIG;
+            orc_halo_unpack(h, phase, slot, c.halo_buf[phase][slot]);
+        }
+    return SPHG_OK;
+}
+
+int decomposed_step(orc_ctx* h) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (c.P.transitions) return SPHG_ERR_CONFIG;
+    if (!c.max_words) return SPHG_ERR_CONFIG;
+    const bool ok = stage_kick_drift(c);
+    // global max displacement and speed (a local error travels as +inf)
+    const double d2 = ok ? c.max_disp * c.max_disp : std::numeric_limits<double>::infinity();
+    const double u2 = c.u_max * c.u_max;
+    std::memcpy(&c.max_words[0], &d2, 8);
+    std::memcpy(&c.max_words[1], &u2, 8);
+    int rc = xchg(c, SPHG_XCHG_MAX);
+    if (rc) return rc;
+    double gd2, gu2;
+    std::memcpy(&gd2, &c.max_words[0], 8);
+    std::memcpy(&gu2, &c.max_words[1], 8);
+    if (!ok) return SPHG_ERR_RUNTIME;
+    if (std::isinf(gd2)) {
+        c.err = "runtime assertion on another rank at step " + std::to_string(c.steps + 1);
+        return SPHG_ERR_RUNTIME;
+    }
+    c.max_disp = std::sqrt(gd2);
+    c.u_max = std::sqrt(gu2);
+    if ((rc = halo_xchg(h, SPHG_HALO_STATE))) return rc;
+    const double half_skin = 0.5 * (c.rv - c.rc);
+    if (!c.built || c.max_disp > half_skin) {  // SPEC:212, rank-local
+        c.disp_since_partition += c.max_disp;
+        if (!stage_rebuild(c)) return SPHG_ERR_RUNTIME;
+    }
+    if (!stage_density(c)) return SPHG_ERR_RUNTIME;
+    if ((rc = halo_xchg(h, SPHG_HALO_DENSITY))) return rc;
+    if (c.P.thermal && !stage_heat(c)) return SPHG_ERR_RUNTIME;
+    if (c.P.diffusion && !stage_diffusion(c)) return SPHG_ERR_RUNTIME;
+    if (!stage_extrapolate(c)) return SPHG_ERR_RUNTIME;
+    if ((rc = halo_xchg(h, SPHG_HALO_WALL))) return rc;
+    if (!stage_forces(c)) return SPHG_ERR_RUNTIME;
+    const size_t nb = c.bodies.size();
+    if (nb) {
+        if (!c.body_part || !c.body_gath) return SPHG_ERR_CONFIG;
+        orc_body_partials(h, c.body_part);
+        if ((rc = xchg(c, SPHG_XCHG_BODIES))) return rc;
+        std::vector<double> tot(nb * 12);
+        for (size_t q = 0; q < nb * 12; ++q) {  // rank-order TwoSum (parallel._merge_partials)
+            double sm = c.body_gath[2 * q], cp = c.body_gath[2 * q + 1];
+            for (int r = 1; r < c.world; ++r) {
+                const double s2 = c.body_gath[(size_t)r * nb * 24 + 2 * q], c2 = c.body_gath[(size_t)r * nb * 24 + 2 * q + 1];
+                const double t = sm + s2, bp = t - sm, e = (sm - (t - bp)) + (s2 - bp);
+                cp = (cp + c2) + e;
+                sm = t;
+            }
+            tot[q] = sm + cp;
+        }
+        orc_body_apply_totals(h, tot.data());
+    }
+    if (!stage_final_kick(c)) return SPHG_ERR_RUNTIME;
+    c.steps++;
+    return check_dt(c) ? SPHG_OK : SPHG_ERR_RUNTIME;
 }
 
 int orc_max_displacement(orc_ctx* h, double* out) {

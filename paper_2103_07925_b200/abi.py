@@ -29,6 +29,7 @@ STAGE_TRANSITIONS = 8
 STAGE_MASS = 9
 
 HALO_STATE, HALO_DENSITY, HALO_WALL = 0, 1, 2
+XCHG_MAX, XCHG_BODIES = 3, 4  # exchange phases of the in-library decomposed step (sphg_set_exchange)
 TRANSITIONS_NONE, TRANSITIONS_TEMPERATURE, TRANSITIONS_CONCENTRATION = 0, 1, 2  # config.hpp:61
 FIELD_VELOCITY, FIELD_TEMPERATURE, FIELD_CONCENTRATION, FIELD_PRESSURE, FIELD_DENSITY = 0, 1, 2, 3, 4
 MAX_HALO_SLOTS = 64
@@ -120,7 +121,8 @@ class Stats(C.Structure):
                 ("time", C.c_double), ("max_displacement", C.c_double), ("u_max", C.c_double),
                 ("stage_ms", C.c_double * 16), ("kernel_launches", C.c_int64),
                 ("last_step_call_ms", C.c_double), ("graph_captures", C.c_int64),
-                ("graph_replays", C.c_int64), ("dt_violations", C.c_int64), ("dt_term", C.c_int32),
+                ("graph_replays", C.c_int64), ("dt_violations", C.c_int64), ("host_syncs", C.c_int64),
+                ("dt_term", C.c_int32),
                 ("pad3", C.c_int32), ("dt_limit", C.c_double)]
 
 
@@ -132,6 +134,9 @@ class Event(C.Structure):
 
 MELT, SOLIDIFY = 1, 2  # sphg_event.direction
 
+
+# int fn(int32 phase, void* stream, void* user)  (sphg_set_exchange)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_int32, C.c_void_p, C.c_void_p)
 
 # void fn(int32 group, double t, double vel[3], double acc[3], void* user)  (sphg_set_wall_motion)
 WALL_MOTION_FN = C.CFUNCTYPE(None, C.c_int32, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -172,6 +177,12 @@ def declare(lib, prefix):
         "upload_state": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_size_t]),
         "set_wall_motion": (C.c_int, [vp, C.c_int32, WALL_MOTION_FN, C.c_void_p]),
         "set_event_log": (C.c_int, [vp, C.c_int]),
+        "set_exchange": (C.c_int, [vp, EXCHANGE_FN, C.c_void_p]),
+        "get_stream": (C.c_int, [vp, C.POINTER(C.c_void_p)]),
+        "halo_bind": (C.c_int, [vp, C.c_int, C.c_int, C.c_void_p]),
+        "max_bind": (C.c_int, [vp, C.c_void_p]),
+        "body_bind": (C.c_int, [vp, C.c_void_p, C.c_void_p, C.c_int32]),
+        "drift": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "transition_events": (C.c_int, [vp, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t)]),
         "shepard_grid": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                    C.c_int32, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint8)]),

@@ -269,7 +269,7 @@ void ensure_bodies(Ctx& c, size_t need) {
   SPHG_CUDA_CHECK(cudaMalloc(&nb, cap * sizeof(sphg_body)));
   SPHG_CUDA_CHECK(cudaMemsetAsync(nb, 0, cap * sizeof(sphg_body), c.stream));
   if (c.bodies.p && c.nb) SPHG_CUDA_CHECK(cudaMemcpyAsync(nb, c.bodies.p, c.nb * sizeof(sphg_body), cudaMemcpyDeviceToDevice, c.stream));
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  host_sync(c, c.stream);
   c.bodies.free();
   c.bodies.p = nb;
   c.bodies.n = cap;
@@ -280,7 +280,7 @@ void ensure_bodies(Ctx& c, size_t need) {
 int check_flags(sphg_ctx* h, bool sync, bool copy = true) {  // copy=false: the readback is already enqueued
   Ctx& c = h->c;
   if (copy) SPHG_CUDA_CHECK(cudaMemcpyAsync(c.hflags, c.dflags, sizeof(DevFlags), cudaMemcpyDeviceToHost, c.stream));
-  if (sync) SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  if (sync) host_sync(c, c.stream);
   SPHG_CUDA_CHECK(cudaGetLastError());
   const DevFlags& f = *c.hflags;
   c.max_disp = std::sqrt(bits_to_double(f.max_disp2_bits));
@@ -571,11 +571,112 @@ int check_dt(sphg_ctx* h) {
   return fail(h, SPHG_ERR_RUNTIME, std::string(b) + bad);
 }
 
+// ------------------------------------------------------- decomposed step
+// One decomposed step on the library stream (sphg.h "In-library decomposed step"): the exchange callback
+// enqueues the transfers; the host blocks once, on the flag readback that carries the global Verlet
+// decision.
+int exchange(sphg_ctx* h, int phase) {
+  Ctx& c = h->c;
+  const int rc = c.exch_fn(phase, reinterpret_cast<void*>(c.stream), c.exch_user);
+  if (rc) return fail(h, SPHG_ERR_CUDA, "exchange callback failed in phase " + std::to_string(phase));
+  return SPHG_OK;
+}
+
+int halo_exchange(sphg_ctx* h, int phase) {
+  Ctx& c = h->c;
+  for (int slot = 0; slot < SPHG_MAX_HALO_SLOTS; slot += 2)
+    if (c.halo_n[slot]) {
+      if (!c.halo_buf[phase][slot]) return fail(h, SPHG_ERR_CONFIG, "halo send buffer not bound");
+      halo_pack(c, phase, slot, c.halo_buf[phase][slot]);
+    }
+  const int rc = exchange(h, phase);
+  if (rc) return rc;
+  for (int slot = 1; slot < SPHG_MAX_HALO_SLOTS; slot += 2)
+    if (c.halo_n[slot]) {
+      if (!c.halo_buf[phase][slot]) return fail(h, SPHG_ERR_CONFIG, "halo receive buffer not bound");
+      halo_unpack(c, phase, slot, c.halo_buf[phase][slot]);
+    }
+  return SPHG_OK;
+}
+
+__global__ void k_flag_error_global(DevFlags* fl) {  // a local error becomes an infinite global displacement
+  if (fl->err) fl->max_disp2_bits = 0x7FF0000000000000ull;
+}
+
+int one_step_decomposed(sphg_ctx* h) {
+  Ctx& c = h->c;
+  if (c.P.transitions) return fail(h, SPHG_ERR_CONFIG, "phase transitions are single-rank only");
+  reset_step_flags(c);
+  kick_all(c);
+  k_flag_error_global<<<1, 1, 0, c.stream>>>(c.dflags);
+  c.launches++;
+  if (!c.max_words) return fail(h, SPHG_ERR_CONFIG, "MAX exchange buffer not bound");
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(c.max_words, &c.dflags->max_disp2_bits, 2 * sizeof(uint64_t),
+                                  cudaMemcpyDeviceToDevice, c.stream));
+  int rc = exchange(h, SPHG_XCHG_MAX);  // global max displacement, u_max (and errors)
+  if (rc) return rc;
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&c.dflags->max_disp2_bits, c.max_words, 2 * sizeof(uint64_t),
+                                  cudaMemcpyDeviceToDevice, c.stream));
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(c.hflags, c.dflags, sizeof(DevFlags), cudaMemcpyDeviceToHost, c.stream));
+  host_sync(c, c.stream);
+  c.t += c.P.dt;
+  h->mid_step = true;
+  rc = check_flags(h, false, false);
+  if (rc) return rc;
+  if (std::isinf(c.max_disp)) return fail(h, SPHG_ERR_RUNTIME, "runtime assertion on another rank at step " +
+                                                                     std::to_string(c.steps + 1));
+  const bool rebuild = !c.built || c.max_disp > c.P.half_skin;
+  // the interior density reads owned neighbours only: it runs while the STATE halo is in flight
+  const bool overlap = !rebuild && c.nf_interior > 0;
+  if (overlap) {
+    if (!c.dens_stream) {
+      SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.dens_stream, cudaStreamNonBlocking));
+      SPHG_CUDA_CHECK(cudaEventCreateWithFlags(&c.dens_fork, cudaEventDisableTiming));
+      SPHG_CUDA_CHECK(cudaEventCreateWithFlags(&c.dens_join, cudaEventDisableTiming));
+    }
+    SPHG_CUDA_CHECK(cudaEventRecord(c.dens_fork, c.stream));
+    SPHG_CUDA_CHECK(cudaStreamWaitEvent(c.dens_stream, c.dens_fork, 0));
+    launch_density_interior(c, c.dens_stream);
+    SPHG_CUDA_CHECK(cudaEventRecord(c.dens_join, c.dens_stream));
+  }
+  rc = halo_exchange(h, SPHG_HALO_STATE);
+  if (rc) return rc;
+  if (rebuild) {
+    c.disp_since_partition += c.max_disp;
+    timed(c, SPHG_STAGE_REBUILD, launch_rebuild);  // rank-local (the ghost margin covers it)
+    launch_density(c);
+  } else {
+    launch_density_boundary(c);
+    if (overlap) SPHG_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.dens_join, 0));
+  }
+  if ((rc = halo_exchange(h, SPHG_HALO_DENSITY))) return rc;
+  if (c.P.thermal) launch_heat(c);
+  if (c.P.diffusion) launch_diffusion(c);
+  launch_extrapolate(c);
+  if ((rc = halo_exchange(h, SPHG_HALO_WALL))) return rc;
+  if (c.pre_forces) c.pre_forces(c);
+  timed_forces(c);
+  if (c.nb) {
+    if (!c.body_part || !c.body_gath) return fail(h, SPHG_ERR_CONFIG, "body exchange buffers not bound");
+    body_partials(c, c.body_part);
+    if ((rc = exchange(h, SPHG_XCHG_BODIES))) return rc;
+    c.body_tot.alloc(c.nb * 12);
+    merge_body_partials(c, c.body_gath, c.world, c.body_tot.p);
+    body_apply_totals(c, c.body_tot.p);
+  }
+  launch_final_kick(c);
+  h->mid_step = false;
+  c.steps++;
+  return check_dt(h);
+}
+
 int one_step(sphg_ctx* h) {
   Ctx& c = h->c;
+  if (c.nghost && c.exch_fn) return one_step_decomposed(h);
   if (c.nghost)
     return fail(h, SPHG_ERR_RUNTIME,
-                "ghost particles present: drive multi-rank steps through the decomposition layer (parallel.py)");
+                "ghost particles present: set an exchange callback (sphg_set_exchange) or drive the stages "
+                "through the decomposition layer (parallel.py)");
   const bool graphs = graphs_allowed(c);
   if (graphs) {
     if (!c.dtime) {  // [0] the force chain's time, [1] the clock (see k_step_tail)
@@ -609,11 +710,11 @@ int one_step(sphg_ctx* h) {
   const bool fp0 = c.final_pending;
   const int64_t l0 = c.launches;
   if (spec) forces();
-  SPHG_CUDA_CHECK(cudaEventSynchronize(c.kick_ev));
+  host_sync_event(c, c.kick_ev);
   int rc = check_flags(h, false, false);  // Verlet trigger + escape check
   const bool rebuild = !c.built || c.max_disp > c.P.half_skin;
   if (spec && (rc || rebuild)) {  // the queued chain voided itself: restore its host-side state
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     c.cur = cur0;
     c.H2new = h2n0;
     c.C2new = c2n0;
@@ -941,7 +1042,7 @@ void stage_download(Ctx& c, sphg_soa* o, bool mid_step) {
   if (pl.items.empty()) return;
   pack(c, merged(pl), mid_step);
   for (const auto& it : pl.items) copy_out(c, it.host, it.dev, it.bytes);
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  host_sync(c, c.stream);
   c.last_d2h_bytes = pl.bytes;
 }
 
@@ -1031,9 +1132,10 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     if (ng && c.params.transitions)
       return fail(h, SPHG_ERR_CONFIG, "phase transitions are single-rank only (ghost particles present)");
     c.nghost = ng;
+    c.disp_since_partition = 0.0;
     // buffers below may be reallocated (and a freed address handed out again): no captured graph may
     // survive an upload (the graph key holds raw pointers)
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     destroy_graphs(c);
     // warm upload: same store size and a valid Verlet list -> keep the device order and the list,
     // scatter the host (gid-ordered) data through the gid permutation
@@ -1089,8 +1191,9 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     if (c.built) {  // kinds / bodies may have changed
       launch_rigid_index(c);
       launch_contact_order(c);
+      launch_ghost_split(c);
     }
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     c.have_state = true;
     h->mid_step = false;
     return SPHG_OK;
@@ -1112,7 +1215,7 @@ int sphg_upload_state(sphg_ctx* h, const double* pos, const double* vel, size_t 
     scatter_state(c, pos ? c.state_buf.p : nullptr, vel ? c.state_buf.p + 3 * n : nullptr);
     c.last_h2d_bytes = (pos ? 24 : 0) * n + (vel ? 24 : 0) * n;
     if (c.built && pos && displacement_exceeds(c)) c.built = false;
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     h->mid_step = false;
     return SPHG_OK;
   });
@@ -1204,13 +1307,13 @@ int run_steps(sphg_ctx* h, int nsteps, sphg_soa* out) {
   float ms = 0.f;
   SPHG_CUDA_CHECK(cudaEventElapsedTime(&ms, c.step_ev[0], c.step_ev[1]));
   c.last_step_ms = ms;
-  if (overlap) SPHG_CUDA_CHECK(cudaStreamSynchronize(c.copy_stream));  // never leave copies in flight
+  if (overlap) host_sync(c, c.copy_stream);  // never leave copies in flight
   if (rc || !out) return rc;
   if (overlap) {
     for (const auto& it : pl.items)
       if (!it.early) copy_out(c, it.host, it.dev, it.bytes);
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.copy_stream));
+    host_sync(c, c.stream);
+    host_sync(c, c.copy_stream);
     for (const auto& it : pl.items) bytes += it.bytes;
     c.last_d2h_bytes = bytes;
   } else {
@@ -1233,7 +1336,7 @@ int sphg_step_download(sphg_ctx* h, int nsteps, sphg_soa* out, sphg_body* bodies
     Ctx& c = h->c;
     if (nb_io) {
       if (bodies) d2h(bodies, c.bodies.p, std::min(*nb_io, c.nb), c.stream);
-      SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      host_sync(c, c.stream);
       *nb_io = c.nb;
     }
     return SPHG_OK;
@@ -1260,7 +1363,7 @@ int sphg_download(sphg_ctx* h, sphg_soa* o, sphg_body* bodies, size_t* nb_io) {
     stage_download(c, o, h->mid_step);
     if (nb_io) {
       if (bodies) d2h(bodies, c.bodies.p, std::min(*nb_io, c.nb), c.stream);
-      SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      host_sync(c, c.stream);
       *nb_io = c.nb;
     }
     return SPHG_OK;
@@ -1278,7 +1381,7 @@ int sphg_get_cells(sphg_ctx* h, int64_t* cell_of_gid, uint32_t* sorted_gid) {
     std::vector<uint32_t> key(n), gid(n);
     d2h(key.data(), c.cell_key.p, n, c.stream);
     d2h(gid.data(), c.cur.gid.p, n, c.stream);
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     for (size_t k = 0; k < n; ++k) {
       if (cell_of_gid) cell_of_gid[gid[k]] = key[k];
       if (sorted_gid) sorted_gid[k] = gid[k];
@@ -1298,7 +1401,7 @@ int sphg_get_nlist(sphg_ctx* h, int64_t* offsets, uint32_t* nbr_gid) {
     std::vector<uint32_t> cnt(n), gid(n);
     d2h(cnt.data(), c.cnt.p, n, c.stream);
     d2h(gid.data(), c.cur.gid.p, n, c.stream);
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     std::vector<int64_t> cnt_g(n);
     for (size_t k = 0; k < n; ++k) cnt_g[gid[k]] = cnt_total(cnt[k]);
     int64_t o = 0;
@@ -1310,7 +1413,7 @@ int sphg_get_nlist(sphg_ctx* h, int64_t* offsets, uint32_t* nbr_gid) {
     if (!nbr_gid) return SPHG_OK;
     std::vector<uint32_t> rows((size_t)c.cap * n);
     d2h(rows.data(), c.nbr.p, rows.size(), c.stream);
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     const uint32_t mask = c.P.img_mode == kImgCode ? kIdxMask : 0xffffffffu;
     for (size_t k = 0; k < n; ++k) {
       const int64_t base = offsets[gid[k]];
@@ -1343,12 +1446,13 @@ int sphg_stats(sphg_ctx* h, sphg_stats_t* s) {
     s->graph_captures = c.graph_captures;
     s->graph_replays = c.graph_replays;
     s->dt_violations = c.dt_violations;
+    s->host_syncs = c.host_syncs;
     s->dt_term = c.dt_term;
     s->dt_limit = c.dt_limit;
     if (c.built && c.n) {
       std::vector<uint32_t> cnt(c.n);
       d2h(cnt.data(), c.cnt.p, c.n, c.stream);
-      SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      host_sync(c, c.stream);
       int64_t tot = 0;
       for (uint32_t v : cnt) tot += cnt_total(v);
       s->n_pairs_candidate = tot;
@@ -1356,7 +1460,7 @@ int sphg_stats(sphg_ctx* h, sphg_stats_t* s) {
     if (c.nb) {
       std::vector<sphg_body> b(c.nb);
       d2h(b.data(), c.bodies.p, c.nb, c.stream);
-      SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      host_sync(c, c.stream);
       for (auto& x : b) s->bodies_alive += x.alive ? 1 : 0;
     }
     return SPHG_OK;
@@ -1436,7 +1540,7 @@ int sphg_shepard_grid(sphg_ctx* h, const double origin[3], const double spacing[
     shepard_grid(c, origin, spacing, dims, field, kind_mask, dout.p, support ? dsup.p : nullptr);
     SPHG_CUDA_CHECK(cudaMemcpyAsync(out, dout.p, (size_t)np * nc * sizeof(double), cudaMemcpyDefault, c.stream));
     if (support) SPHG_CUDA_CHECK(cudaMemcpyAsync(support, dsup.p, (size_t)np, cudaMemcpyDefault, c.stream));
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     dout.free();
     dsup.free();
     return SPHG_OK;
@@ -1455,7 +1559,7 @@ int sphg_halo_set(sphg_ctx* h, int slot, const uint32_t* ids, size_t n) {
       if (ids[k] >= c.n) return fail(h, SPHG_ERR_CONFIG, "halo index out of range");
     c.halo_ids[slot].alloc(std::max<size_t>(n, 1));
     h2d(c.halo_ids[slot].p, ids, n, c.stream);
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     c.halo_n[slot] = n;
     return SPHG_OK;
   });
@@ -1467,7 +1571,7 @@ int sphg_halo_pack(sphg_ctx* h, int phase, int slot, double* buf) {
     if (slot < 0 || slot >= SPHG_MAX_HALO_SLOTS || sphg_halo_doubles(phase) < 0)
       return fail(h, SPHG_ERR_CONFIG, "bad halo slot/phase");
     halo_pack(c, phase, slot, buf);
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     return SPHG_OK;
   });
 }
@@ -1478,7 +1582,7 @@ int sphg_halo_unpack(sphg_ctx* h, int phase, int slot, const double* buf) {
     if (slot < 0 || slot >= SPHG_MAX_HALO_SLOTS || sphg_halo_doubles(phase) < 0)
       return fail(h, SPHG_ERR_CONFIG, "bad halo slot/phase");
     halo_unpack(c, phase, slot, buf);
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     return SPHG_OK;
   });
 }
@@ -1496,7 +1600,7 @@ int sphg_body_partials(sphg_ctx* h, double* out) {
     body_partials(c, c.body_buf.p);
     // host or device destination (the multi-rank driver gathers device tensors over NCCL)
     SPHG_CUDA_CHECK(cudaMemcpyAsync(out, c.body_buf.p, c.nb * 24 * sizeof(double), cudaMemcpyDefault, c.stream));
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     return SPHG_OK;
   });
 }
@@ -1508,13 +1612,51 @@ int sphg_body_apply_totals(sphg_ctx* h, const double* tot) {
     c.body_buf.alloc(c.nb * 24);
     SPHG_CUDA_CHECK(cudaMemcpyAsync(c.body_buf.p, tot, c.nb * 12 * sizeof(double), cudaMemcpyDefault, c.stream));
     body_apply_totals(c, c.body_buf.p);
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    host_sync(c, c.stream);
     return SPHG_OK;
   });
 }
 
 int sphg_max_displacement(sphg_ctx* h, double* out) {
   *out = h->c.max_disp;
+  return SPHG_OK;
+}
+
+int sphg_set_exchange(sphg_ctx* h, sphg_exchange_fn fn, void* user) {
+  h->c.exch_fn = fn;
+  h->c.exch_user = user;
+  return SPHG_OK;
+}
+
+int sphg_get_stream(sphg_ctx* h, void** stream) {
+  *stream = reinterpret_cast<void*>(h->c.stream);
+  return SPHG_OK;
+}
+
+int sphg_halo_bind(sphg_ctx* h, int phase, int slot, double* buf) {
+  if (phase < 0 || phase > 2 || slot < 0 || slot >= SPHG_MAX_HALO_SLOTS)
+    return fail(h, SPHG_ERR_CONFIG, "bad halo slot/phase");
+  h->c.halo_buf[phase][slot] = buf;
+  return SPHG_OK;
+}
+
+int sphg_max_bind(sphg_ctx* h, uint64_t* words) {
+  h->c.max_words = words;
+  return SPHG_OK;
+}
+
+int sphg_drift(sphg_ctx* h, double out[3]) {
+  out[0] = h->c.max_disp;
+  out[1] = h->c.disp_since_partition;
+  out[2] = h->c.u_max;
+  return SPHG_OK;
+}
+
+int sphg_body_bind(sphg_ctx* h, double* part, double* gath, int32_t world) {
+  if (world < 1) return fail(h, SPHG_ERR_CONFIG, "world size must be >= 1");
+  h->c.body_part = part;
+  h->c.body_gath = gath;
+  h->c.world = world;
   return SPHG_OK;
 }
 
@@ -1555,6 +1697,10 @@ void sphg_destroy(sphg_ctx* h) {
   if (c.fork_ev) cudaEventDestroy(c.fork_ev);
   if (c.join_ev) cudaEventDestroy(c.join_ev);
   if (c.dl_ev) cudaEventDestroy(c.dl_ev);
+  if (c.dens_stream) cudaStreamDestroy(c.dens_stream);
+  if (c.dens_fork) cudaEventDestroy(c.dens_fork);
+  if (c.dens_join) cudaEventDestroy(c.dens_join);
+  c.body_tot.free();
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
   c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();
   c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();

@@ -195,7 +195,31 @@ struct Ctx {
   int64_t dt_violations = 0;
   int dt_term = -1;
   double dt_limit = 0.0;
+  int64_t host_syncs = 0;  // host-blocking waits on the device (sphg_stats_t.host_syncs)
+  // in-library decomposed step (api.cu one_step_decomposed): exchange callback and bound buffers
+  sphg_exchange_fn exch_fn = nullptr;
+  void* exch_user = nullptr;
+  double* halo_buf[3][SPHG_MAX_HALO_SLOTS] = {};
+  uint64_t* max_words = nullptr; // 2 words reduced by the MAX exchange
+  double* body_part = nullptr;   // nb x 24 partials this rank contributes
+  double* body_gath = nullptr;   // world x nb x 24, filled by the BODIES exchange
+  int world = 1;
+  size_t nf_interior = 0;        // fidx[0, nf_interior): fluid particles with no ghost neighbour
+  double disp_since_partition = 0.0;  // sum of the global displacements at rebuilds since the last upload
+  DBuf<double> body_tot;         // merged nb x 12 totals
+  cudaStream_t dens_stream = nullptr;
+  cudaEvent_t dens_fork = nullptr, dens_join = nullptr;
 };
+
+// every host-blocking wait of the library goes through these (counted in sphg_stats_t.host_syncs)
+inline void host_sync(Ctx& c, cudaStream_t s) {
+  SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+  c.host_syncs++;
+}
+inline void host_sync_event(Ctx& c, cudaEvent_t e) {
+  SPHG_CUDA_CHECK(cudaEventSynchronize(e));
+  c.host_syncs++;
+}
 
 // ------------------------------------------------------------ launchers
 // radix_sort.cu
@@ -216,6 +240,10 @@ void launch_body_kick(Ctx& c);
 void launch_kick_drift(Ctx& c);
 void launch_step_tail(Ctx& c);  // dskip (rebuild or error pending) and the device clock t^{n+1}
 void launch_density(Ctx& c);
+void launch_density_interior(Ctx& c, cudaStream_t st);
+void launch_density_boundary(Ctx& c);
+void launch_ghost_split(Ctx& c);  // orders fidx [interior | next to a ghost] (decomposed steps)
+void merge_body_partials(Ctx& c, const double* gathered, int world, double* totals);
 void launch_heat(Ctx& c);
 void launch_heat_begin(Ctx& c);
 void launch_heat_end(Ctx& c);

@@ -1008,12 +1008,21 @@ inline int lanes_for(const Ctx& c, size_t nlist) { return 2 * nlist < c.fill_gro
     }                                                             \
   } while (0)
 
-void launch_density(Ctx& c) {
-  if (c.nf == 0) return;
-  SPHG_G_DISPATCH(c, c.group_density, c.nf,
-                  SPHG_IMG_DISPATCH(c.P.img_mode, (k_density<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
-                                                       c.P, c.cur, c.nl(), c.fidx.p, c.nf))));
+static void launch_density_list(Ctx& c, const uint32_t* list, size_t m, cudaStream_t st) {
+  if (m == 0) return;
+  SPHG_G_DISPATCH(c, c.group_density, m,
+                  SPHG_IMG_DISPATCH(c.P.img_mode, (k_density<G, M><<<blocks_for<G>(m), kBlock, 0, st>>>(
+                                                       c.P, c.cur, c.nl(), list, m))));
   c.launches++;
+}
+
+void launch_density(Ctx& c) { launch_density_list(c, c.fidx.p, c.nf, c.stream); }
+
+// decomposed steps: the fluid list is ordered [interior | next to a ghost] (launch_ghost_split); the
+// interior part reads only owned neighbours, so it runs before the STATE halo has landed
+void launch_density_interior(Ctx& c, cudaStream_t st) { launch_density_list(c, c.fidx.p, c.nf_interior, st); }
+void launch_density_boundary(Ctx& c) {
+  launch_density_list(c, c.fidx.p + c.nf_interior, c.nf - c.nf_interior, c.stream);
 }
 
 // Heat in two halves so one_step can fold the fluid part into the forces pass (c.fuse_heat):
@@ -1229,7 +1238,7 @@ void count_pairs(Ctx& c, int64_t out[4]) {
                                        c.P, c.cur, c.nl(), c.n, c.dcount)));
   unsigned long long h[4];
   SPHG_CUDA_CHECK(cudaMemcpyAsync(h, c.dcount, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  host_sync(c, c.stream);
   for (int k = 0; k < 4; ++k) out[k] = (int64_t)h[k];
 }
 

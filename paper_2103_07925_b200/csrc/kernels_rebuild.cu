@@ -596,6 +596,57 @@ __global__ void k_cell_kind_scatter(const __grid_constant__ DevParams P, const u
 
 }  // namespace
 
+namespace {
+// 1 = the fluid particle's row holds no ghost (its sums need no halo data)
+template <int M>
+__global__ void k_interior_flags(const uint32_t* __restrict__ kmd, const uint32_t* __restrict__ fidx, size_t nf,
+                                 NbrList L, uint32_t* __restrict__ flag) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nf) return;
+  const uint32_t i = fidx[e];
+  const uint32_t nn = cnt_total(L.cnt[i]);
+  const uint32_t* row = L.nbr + (size_t)i * L.cap;
+  uint32_t in = 1u;
+  for (uint32_t k = 0; k < nn && in; ++k)
+    if (is_ghost(kmd[nb_index<M>(row[k])])) in = 0u;
+  flag[e] = in;
+}
+
+__global__ void k_split_scatter(const uint32_t* __restrict__ fidx, const uint32_t* __restrict__ flag,
+                                const uint32_t* __restrict__ pos, size_t nf, uint32_t n_in, uint32_t* __restrict__ out) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nf) return;
+  const uint32_t p = pos[e];  // interior particles before e
+  out[flag[e] ? p : n_in + (uint32_t)e - p] = fidx[e];
+}
+}  // namespace
+
+// Decomposed steps: order fidx [interior | next to a ghost], stably, so the interior density can run
+// while the STATE halo is in flight (api.cu one_step_decomposed).  Single rank: all interior.
+void launch_ghost_split(Ctx& c) {
+  c.nf_interior = c.nf;
+  if (c.nghost == 0 || c.nf == 0) return;
+  cudaStream_t s = c.stream;
+  uint32_t* flag = c.vals_alt.p;  // scratch (n >= nf)
+  uint32_t* pos = c.vals.p;
+  switch (c.P.img_mode) {
+    case kImgNone: k_interior_flags<kImgNone><<<grid_for(c.nf, 128), 128, 0, s>>>(c.cur.kmd.p, c.fidx.p, c.nf, c.nl(), flag); break;
+    case kImgCode: k_interior_flags<kImgCode><<<grid_for(c.nf, 128), 128, 0, s>>>(c.cur.kmd.p, c.fidx.p, c.nf, c.nl(), flag); break;
+    default: k_interior_flags<kImgMin><<<grid_for(c.nf, 128), 128, 0, s>>>(c.cur.kmd.p, c.fidx.p, c.nf, c.nl(), flag); break;
+  }
+  exclusive_scan_u32(flag, pos, c.nf, c.scan_tmp.p, s, &c.launches);
+  uint32_t tail[2] = {0, 0};
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&tail[0], pos + c.nf - 1, 4, cudaMemcpyDeviceToHost, s));
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&tail[1], flag + c.nf - 1, 4, cudaMemcpyDeviceToHost, s));
+  host_sync(c, s);
+  const uint32_t n_in = tail[0] + tail[1];
+  uint32_t* out = c.keys_alt.p ? reinterpret_cast<uint32_t*>(c.keys_alt.p) : nullptr;  // scratch (8 B x n)
+  k_split_scatter<<<grid_for(c.nf, 256), 256, 0, s>>>(c.fidx.p, flag, pos, c.nf, n_in, out);
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(c.fidx.p, out, c.nf * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  c.nf_interior = n_in;
+  c.launches += 3;
+}
+
 // fluid / non-fluid index lists (cell order) for the pair kernels
 static void launch_kind_lists(Ctx& c) {
   const size_t n = c.n;
@@ -620,9 +671,10 @@ static void launch_kind_lists(Ctx& c) {
   SPHG_CUDA_CHECK(cudaMemcpyAsync(&tail[1], fc + npos - 1, 4, cudaMemcpyDeviceToHost, s));
   SPHG_CUDA_CHECK(cudaMemcpyAsync(&tail[2], wo + npos - 1, 4, cudaMemcpyDeviceToHost, s));
   SPHG_CUDA_CHECK(cudaMemcpyAsync(&tail[3], wc + npos - 1, 4, cudaMemcpyDeviceToHost, s));
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+  host_sync(c, s);
   c.nf = (size_t)tail[0] + tail[1];
   c.nw = (size_t)tail[2] + tail[3];
+  c.nf_interior = c.nf;  // canonical order; launch_ghost_split reorders for decomposed steps
   c.launches += 2;
 }
 
@@ -640,7 +692,7 @@ void launch_rigid_index(Ctx& c) {
   uint32_t last_pos = 0, last_flag = 0;
   SPHG_CUDA_CHECK(cudaMemcpyAsync(&last_pos, pos + n - 1, 4, cudaMemcpyDeviceToHost, s));
   SPHG_CUDA_CHECK(cudaMemcpyAsync(&last_flag, flag + n - 1, 4, cudaMemcpyDeviceToHost, s));
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+  host_sync(c, s);
   const size_t m = (size_t)last_pos + last_flag;
   c.nrigid = m;
   SPHG_CUDA_CHECK(cudaMemsetAsync(c.body_start.p, 0, 2 * std::max<size_t>(c.nb, 1) * sizeof(uint32_t), s));
@@ -694,7 +746,7 @@ void launch_rebuild(Ctx& c) {
                             32 * kBuildWarps, 0, s>>>(c.P, c.cur.G0.p, c.cur.kmd.p, c.cell_start.p,
                                                             c.cell_end.p, c.nbr.p, c.cnt.p, c.cap, c.dflags);
       SPHG_CUDA_CHECK(cudaMemcpyAsync(&err, &c.dflags->build_overflow, 4, cudaMemcpyDeviceToHost, s));
-      SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+      host_sync(c, s);
       c.launches += 2;
     }
     if (!c.cell_build || err) {  // per-particle build (also the fallback for over-dense cells)
@@ -704,7 +756,7 @@ void launch_rebuild(Ctx& c) {
     }
     c.launches++;
     SPHG_CUDA_CHECK(cudaMemcpyAsync(&mc, &c.dflags->max_count, 4, cudaMemcpyDeviceToHost, s));
-    SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+    host_sync(c, s);
     c.max_count = (int)mc;
     if ((int)mc <= c.cap) break;
     c.cap = (int)((mc + 15) / 8 * 8);
@@ -712,6 +764,7 @@ void launch_rebuild(Ctx& c) {
   }
   launch_rigid_index(c);
   launch_contact_order(c);
+  launch_ghost_split(c);
   c.built = true;
   c.rebuilds++;
 }

@@ -539,6 +539,23 @@ __global__ void k_apply_totals(const __grid_constant__ DevParams P, sphg_body* _
   }
 }
 
+// global body totals from the ranks' compensated partials, merged in rank order with TwoSum (the same
+// single IEEE adds as parallel._merge_partials, so every rank gets bit-identical totals)
+__global__ void k_merge_partials(const double* __restrict__ g, size_t nb, int world, double* __restrict__ tot) {
+  const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // (body, component)
+  if (q >= nb * 12) return;
+  double s = g[2 * q], c = g[2 * q + 1];
+  for (int r = 1; r < world; ++r) {
+    const double s2 = g[(size_t)r * nb * 24 + 2 * q], c2 = g[(size_t)r * nb * 24 + 2 * q + 1];
+    const double t = __dadd_rn(s, s2);
+    const double bp = __dsub_rn(t, s);
+    const double e = __dadd_rn(__dsub_rn(s, __dsub_rn(t, bp)), __dsub_rn(s2, bp));
+    c = __dadd_rn(__dadd_rn(c, c2), e);
+    s = t;
+  }
+  tot[q] = __dadd_rn(s, c);
+}
+
 __global__ void k_scatter_state(Particles D, size_t n, const uint32_t* __restrict__ idx, const double* __restrict__ pos,
                                 const double* __restrict__ vel) {
   const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -583,6 +600,12 @@ void body_partials(Ctx& c, double* dev_out) {
   c.launches++;
 }
 
+void merge_body_partials(Ctx& c, const double* gathered, int world, double* totals) {
+  if (c.nb == 0) return;
+  k_merge_partials<<<grid_for(c.nb * 12, 128), 128, 0, c.stream>>>(gathered, c.nb, world, totals);
+  c.launches++;
+}
+
 void body_apply_totals(Ctx& c, const double* dev_tot) {
   if (c.nb == 0) return;
   k_apply_totals<<<grid_for(c.nb, 128), 128, 0, c.stream>>>(c.P, c.bodies.p, c.nb, dev_tot);
@@ -601,7 +624,7 @@ bool displacement_exceeds(Ctx& c) {
   k_disp<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, c.dflags);
   unsigned long long b = 0;
   SPHG_CUDA_CHECK(cudaMemcpyAsync(&b, &c.dflags->max_disp2_bits, 8, cudaMemcpyDeviceToHost, c.stream));
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  host_sync(c, c.stream);
   double d2;
   memcpy(&d2, &b, 8);
   c.launches += 2;

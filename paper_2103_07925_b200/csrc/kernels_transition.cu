@@ -333,7 +333,7 @@ int bits_for(uint64_t maxval) {
 uint32_t read_u32(Ctx& c, const uint32_t* p) {
   uint32_t v = 0;
   SPHG_CUDA_CHECK(cudaMemcpyAsync(&v, p, 4, cudaMemcpyDeviceToHost, c.stream));
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  host_sync(c, c.stream);
   return v;
 }
 
@@ -345,7 +345,7 @@ void grow_bodies(Ctx& c, size_t need) {
   SPHG_CUDA_CHECK(cudaMemsetAsync(nb, 0, cap * sizeof(sphg_body), c.stream));
   if (c.bodies.p && c.nb)
     SPHG_CUDA_CHECK(cudaMemcpyAsync(nb, c.bodies.p, c.nb * sizeof(sphg_body), cudaMemcpyDeviceToDevice, c.stream));
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  host_sync(c, c.stream);
   c.bodies.free();
   c.bodies.p = nb;
   c.bodies.n = cap;
@@ -535,7 +535,7 @@ int launch_transitions(Ctx& c) {
   c.launches += 4;
   // 5. force/torque with the new membership
   launch_bodies(c);
-  SPHG_CUDA_CHECK(cudaStreamSynchronize(s));
+  host_sync(c, s);
   old.free();
   if (elog) {  // drain this batch's events to the host, ordered by gid (each particle once per batch)
     const size_t m = (size_t)nmelt + nsolid;

@@ -109,7 +109,8 @@ class DistributedSimulation:
     (GPU) or the oracle's engine (CPU tests); `tensor_device` is where halo
     buffers live (the engine's device)."""
 
-    def __init__(self, params, make_engine, tensor_device="cpu", margin_h=2.0, group=None, engine_device=None):
+    def __init__(self, params, make_engine, tensor_device="cpu", margin_h=2.0, group=None, engine_device=None,
+                 fused=True):
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -133,6 +134,12 @@ class DistributedSimulation:
         self.rebuilds = 0
         self.steps = 0
         self.comm_s = 0.0
+        # in-library decomposed step (sphg_set_exchange): the engine runs the whole step on its stream
+        # and calls back for the transfers; False = the stage-by-stage driver below
+        self.fused = fused
+        self._cb = None
+        self._ext = None
+        self._xerr = None
 
     # ------------------------------------------------------------ layout
     def local_gids(self, pos, owner, r):
@@ -181,11 +188,110 @@ class DistributedSimulation:
             self._halo_set(2 * k + 1, rcv)
         self.disp_since_partition = 0.0
         self._bufs = {}
+        if self._fused_ok():
+            self._bind_fused()
 
     def _halo_set(self, slot, ids):
         ids = np.ascontiguousarray(ids, np.uint32)
         e = self.engine
         e._check(e._fn("halo_set")(e._h, slot, ids.ctypes.data_as(C.POINTER(C.c_uint32)), len(ids)), "halo_set")
+
+    # ------------------------------------------------- in-library decomposed step
+    def _fused_ok(self):
+        e = self.engine
+        return self.fused and e is not None and getattr(e.lib, e.prefix + "set_exchange", None) is not None
+
+    def _bind_fused(self):
+        """Buffers the engine packs into / unpacks from at the exchange points of its decomposed step
+        (halo records per peer, the two MAX words, body partials and their all-gather), plus the
+        exchange callback.  They live where the engine computes (device for the GPU engine)."""
+        e = self.engine
+        f = lambda name: getattr(e.lib, e.prefix + name)
+        mk = lambda m, dt=torch.float64: torch.zeros(max(int(m), 1), dtype=dt, device=self.edev)
+        self._fb = {}
+        for phase in (abi.HALO_STATE, abi.HALO_DENSITY, abi.HALO_WALL):
+            d = f("halo_doubles")(phase)
+            for k, (q, snd, rcv) in enumerate(self.peers):
+                for slot, m in ((2 * k, len(snd)), (2 * k + 1, len(rcv))):
+                    b = mk(m * d)
+                    self._fb[(phase, slot)] = b
+                    e._check(f("halo_bind")(e._h, phase, slot, C.c_void_p(b.data_ptr())), "halo_bind")
+        self._maxw = mk(2, torch.int64)
+        e._check(f("max_bind")(e._h, C.c_void_p(self._maxw.data_ptr())), "max_bind")
+        nb = e.num_bodies()
+        self._bpart = mk(nb * 24)
+        self._bgath = mk(self.world * nb * 24)
+        e._check(f("body_bind")(e._h, C.c_void_p(self._bpart.data_ptr()), C.c_void_p(self._bgath.data_ptr()),
+                                self.world), "body_bind")
+        self._nb = nb
+        if self._cb is None:
+            self._cb = abi.EXCHANGE_FN(self._exchange_cb)  # keep the thunk alive with the context
+        e._check(f("set_exchange")(e._h, self._cb, None), "set_exchange")
+
+    def _exchange_cb(self, phase, stream, user):
+        try:
+            t0 = time.perf_counter()
+            if self.edev.type == "cuda":
+                # every transfer is enqueued on the engine's stream: the NCCL work waits for the pack
+                # kernels and the unpack kernels wait for it, without blocking the host
+                if self._ext is None or self._ext_ptr != stream:
+                    self._ext = torch.cuda.ExternalStream(stream, device=self.edev)
+                    self._ext_ptr = stream
+                with torch.cuda.stream(self._ext):
+                    self._transfer(phase)
+            else:
+                self._transfer(phase)
+            self.comm_s += time.perf_counter() - t0
+            return 0
+        except Exception as ex:  # surfaces as the engine's error return
+            self._xerr = ex
+            return 1
+
+    def _transfer(self, phase):
+        staged = self.edev != self.dev  # engine on the GPU, transport (gloo) on the host
+        to_t = (lambda t: t.to(self.dev)) if staged else (lambda t: t)  # D2H in stream order (blocking)
+        if phase in (abi.HALO_STATE, abi.HALO_DENSITY, abi.HALO_WALL):
+            d = getattr(self.engine.lib, self.engine.prefix + "halo_doubles")(phase)
+            ops, recv = [], []
+            for k, (q, snd, rcv) in enumerate(self.peers):
+                if len(snd):
+                    ops.append(dist.P2POp(dist.isend, to_t(self._fb[(phase, 2 * k)][: len(snd) * d]), q, group=self.group))
+                if len(rcv):
+                    rb = self._fb[(phase, 2 * k + 1)][: len(rcv) * d]
+                    rt = torch.empty(rb.numel(), dtype=rb.dtype, device=self.dev) if staged else rb
+                    ops.append(dist.P2POp(dist.irecv, rt, q, group=self.group))
+                    recv.append((rb, rt))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+            if staged:
+                for rb, rt in recv:
+                    rb.copy_(rt)
+        elif phase == abi.XCHG_MAX:
+            t = to_t(self._maxw)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            if staged:
+                self._maxw.copy_(t)
+        elif phase == abi.XCHG_BODIES:
+            m = self._nb * 24
+            part = to_t(self._bpart[:m])
+            gath = torch.empty(self.world * m, dtype=torch.float64, device=self.dev) if staged else self._bgath
+            if self.dev.type == "cuda":
+                dist.all_gather_into_tensor(gath[: self.world * m], part, group=self.group)
+            else:
+                dist.all_gather([gath[r * m:(r + 1) * m] for r in range(self.world)], part, group=self.group)
+            if staged:
+                self._bgath[: self.world * m].copy_(gath)
+        else:
+            raise ValueError(f"unknown exchange phase {phase}")
+
+    def drift(self):
+        """(global max displacement since the last rebuild, sum of the displacements at rebuilds since
+        the partition, global max fluid speed)."""
+        e = self.engine
+        out = (C.c_double * 3)()
+        e._check(getattr(e.lib, e.prefix + "drift")(e._h, out), "drift")
+        return tuple(out)
 
     # ------------------------------------------------------------ exchanges
     def _halo(self, phase):
@@ -275,6 +381,25 @@ class DistributedSimulation:
 
     def step(self, nsteps=1):
         e = self.engine
+        if self._fused_ok():
+            # one engine call per step: the engine runs kick .. final kick with its own exchanges; the
+            # host only decides between steps whether the partition still covers the drift (a particle
+            # may drift up to margin/2 before its ghosts could miss a neighbour; a step with a rebuild
+            # adds at most half a skin)
+            r0 = e.stats().rebuilds
+            for _ in range(nsteps):
+                md, acc, _u = self.drift()
+                if acc + md + self.half_skin > 0.5 * self.margin:
+                    self.repartition()
+                try:
+                    e.step(1)
+                except Exception:
+                    if self._xerr is not None:
+                        raise RuntimeError(f"exchange failed: {self._xerr!r}") from self._xerr
+                    raise
+                self.steps += 1
+            self.rebuilds += e.stats().rebuilds - r0
+            return
         thermal = bool(self.params.thermal) or bool(self.params.diffusion)  # one stage for T and C
         for _ in range(nsteps):
             e.run_stage(abi.STAGE_KICK_DRIFT)

@@ -132,21 +132,24 @@ def test_ranks_match_one_rank(case, world, tmp_path, oracle_mod):
     rg = g.kind == abi.RIGID
     from tests.helpers import vec_err
     if case == "c1fast":
-        assert d["rebuilds"] >= 2 and d["repart"] >= 1 and o.stats().rebuilds == d["rebuilds"] + 1
+        # the displacement-triggered rebuilds are the single rank's; a repartition between steps adds at
+        # most one (the re-uploaded store is binned afresh on the next step)
+        single = o.stats().rebuilds - 1
+        assert d["rebuilds"] >= 2 and d["repart"] >= 1 and single <= d["rebuilds"] <= single + d["repart"]
     assert vec_err(d["pos"], g.pos, float(sc.params.hi[0] - sc.params.lo[0]), 1e-14) <= 1
     assert vec_err(d["density"][fl], g.density[fl], 0.0, 1e-10) <= 1
     assert vec_err(d["acc"][fl], g.acc[fl], s["acc"][fl], 1e-8) <= 1
     assert vec_err(d["force"][rg], g.force[rg], s["force"][rg], 1e-8) <= 1
     assert vec_err(d["T"], g.temperature, 0.0, 1e-12) <= 1
     assert vec_err(d["C"], g.concentration, 1.0, 1e-12) <= 1
-    # cells, Verlet lists and flags match the one-rank run bit-exactly by gid (lists are
-    # compared where both runs last rebuilt at the same step, i.e. without a repartition)
+    # cells, Verlet lists and flags match the one-rank run bit-exactly by gid (cells and
+    # lists are compared where both runs last rebuilt at the same step, i.e. without a repartition)
     assert np.array_equal(d["kind"], g.kind)
     t = np.load(out + ".topo.npz")
     assert np.array_equal(t["gid"], np.arange(sc.store.n))
-    cells_1, _ = o.get_cells()
-    assert np.array_equal(t["cell"], cells_1)
     if int(d["repart"]) == 0:
+        cells_1, _ = o.get_cells()
+        assert np.array_equal(t["cell"], cells_1)
         off1, nbr1 = o.get_nlist()
         assert np.array_equal(t["lens"], np.diff(off1))
         assert np.array_equal(t["flat"], nbr1.astype(np.int64))
@@ -183,3 +186,47 @@ def test_merge_partials_torch_matches_numpy():
     a = _merge_partials(parts)
     b = _merge_partials([torch.from_numpy(p) for p in parts]).numpy()
     assert np.array_equal(a, b)
+
+
+def test_one_decomposed_step_at_the_single_step_bar(tmp_path, oracle_mod):
+    """One step of 2 oracle ranks (the in-library decomposed step: kick, MAX, STATE, density, DENSITY,
+    extrapolation, WALL, forces, BODIES) against one single-rank step: every per-step field within the
+    1e-10 bar (same neighbour sets summed in another order)."""
+    from tests.helpers import vec_err, EOS_ULPS
+    out = str(tmp_path / "d1.npz")
+    port = _free_port()
+    mp.spawn(_worker1, args=(2, port, out), nprocs=2, join=True)
+    d = np.load(out)
+    sc = _case("c1")
+    o = oracle_mod.Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.initialize()
+    o.step(1)
+    g, b = o.download()
+    s = o.scales()
+    fl, rg = g.kind == abi.FLUID, g.kind == abi.RIGID
+    assert vec_err(d["pos"], g.pos, float(sc.params.hi[0] - sc.params.lo[0]), 1e-14) <= 1
+    assert vec_err(d["density"][fl], g.density[fl], 0.0) <= 1
+    assert vec_err(d["acc"][fl], g.acc[fl], s["acc"][fl], allow=EOS_ULPS * s["acc_p"][fl]) <= 1
+    assert vec_err(d["force"][rg], g.force[rg], s["force"][rg], allow=EOS_ULPS * s["force_p"][rg]) <= 1
+    al = b["alive"] == 1
+    assert vec_err(d["bforce"][al], b["force"][al], s["body_force"][al]) <= 1
+    assert vec_err(d["btorque"][al], b["torque"][al], s["body_torque"][al]) <= 1
+
+
+def _worker1(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Oracle
+    from paper_2103_07925_b200.parallel import DistributedSimulation
+    sc = _case("c1")
+    ds = DistributedSimulation(sc.params, lambda p: Oracle(p), tensor_device="cpu", margin_h=0.3)
+    ds.distribute(sc.store, sc.bodies)
+    ds.initialize()
+    ds.step(1)
+    g, b = ds.gather()
+    if rank == 0:
+        np.savez(out, pos=g.pos, acc=g.acc, density=g.density, force=g.force, bforce=b["force"], btorque=b["torque"])
+    dist.destroy_process_group()
