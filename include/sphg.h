@@ -42,7 +42,8 @@ enum {
   SPHG_OK = 0,
   SPHG_ERR_CONFIG = 2,
   SPHG_ERR_RUNTIME = 3,
-  SPHG_ERR_CUDA = 4
+  SPHG_ERR_CUDA = 4,
+  SPHG_NEED_PARTITION = 5 /* not an error: sphg_step stopped before a step its partition may not cover */
 };
 
 /* POD mirror of sphfsi::Material (material.hpp:17-36) plus the per-material
@@ -334,6 +335,11 @@ int sphg_max_bind(sphg_ctx* ctx, uint64_t* dev_words);
  * rebuilds since the last upload (with [0]: a bound on any particle's drift since it was partitioned),
  * [2] global max fluid speed of the last kick */
 int sphg_drift(sphg_ctx* ctx, double out[3]);
+/* decomposed runs: sphg_step returns SPHG_NEED_PARTITION before a step at which [1] + [0] + half a skin
+ * of sphg_drift would exceed `limit` (the caller migrates particles, re-uploads and steps on); 0 = off */
+int sphg_set_partition_limit(sphg_ctx* ctx, double limit);
+/* cheap host counters: [0] steps, [1] Verlet rebuilds, [2] host-blocking syncs, [3] kernel launches */
+int sphg_counters(sphg_ctx* ctx, int64_t out[4]);
 /* body partials (nb x 24 doubles, as sphg_body_partials) are written to dev_partials; the BODIES exchange
  * all-gathers them into dev_gathered (world x nb x 24, rank order) */
 int sphg_body_bind(sphg_ctx* ctx, double* dev_partials, double* dev_gathered, int32_t world);

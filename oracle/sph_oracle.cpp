@@ -107,6 +107,7 @@ struct Ctx {
     int world = 1;
     bool has_ghosts = false;
     double disp_since_partition = 0.0;
+    double partition_limit = 0.0;
     int dt_term = -1;
     double dt_limit = std::numeric_limits<double>::infinity();
 };
@@ -1429,6 +1430,8 @@ int orc_step(orc_ctx* h, int nsteps) {
     Ctx& c = *reinterpret_cast<Ctx*>(h);
     for (int k = 0; k < nsteps; ++k) {
         if (c.has_ghosts && c.exch_fn) {
+            if (c.partition_limit > 0.0 && c.disp_since_partition + c.max_disp + 0.5 * (c.rv - c.rc) > c.partition_limit)
+                return SPHG_NEED_PARTITION;  // sphg.h sphg_set_partition_limit
             const int rc = decomposed_step(h);
             if (rc) return rc;
         } else if (!one_step(c)) {
@@ -1778,6 +1781,18 @@ int orc_body_bind(orc_ctx* h, double* part, double* gath, int32_t world) {
     c.body_part = part;
     c.body_gath = gath;
     c.world = world;
+    return SPHG_OK;
+}
+int orc_set_partition_limit(orc_ctx* h, double limit) {
+    reinterpret_cast<Ctx*>(h)->partition_limit = limit;
+    return SPHG_OK;
+}
+int orc_counters(orc_ctx* h, int64_t out[4]) {
+    const Ctx& c = *reinterpret_cast<Ctx*>(h);
+    out[0] = c.steps;
+    out[1] = c.rebuilds;
+    out[2] = 0;
+    out[3] = 0;
     return SPHG_OK;
 }
 int orc_drift(orc_ctx* h, double out[3]) {

@@ -14,6 +14,7 @@ NO_DIRICHLET = 0xFF
 FLUID, RIGID, BOUNDARY = 0, 1, 2  # store.hpp:11 Kind
 
 OK, ERR_CONFIG, ERR_RUNTIME, ERR_CUDA = 0, 2, 3, 4
+NEED_PARTITION = 5  # sphg_step stopped before a step its partition may not cover (not an error)
 DT_REFUSE, DT_WARN, DT_OFF = 0, 1, 2  # sphg_params.dt_check
 DT_TERMS = ("cfl", "viscous", "body force", "contact", "conduction")  # compute_dt order
 
@@ -183,6 +184,8 @@ def declare(lib, prefix):
         "max_bind": (C.c_int, [vp, C.c_void_p]),
         "body_bind": (C.c_int, [vp, C.c_void_p, C.c_void_p, C.c_int32]),
         "drift": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "set_partition_limit": (C.c_int, [vp, C.c_double]),
+        "counters": (C.c_int, [vp, C.POINTER(C.c_int64)]),
         "transition_events": (C.c_int, [vp, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t)]),
         "shepard_grid": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                    C.c_int32, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint8)]),

@@ -358,16 +358,21 @@ void eval_walls(Ctx& c, double t, double (*vel)[3], double (*acc)[3]) {
   }
 }
 
-void kick_all(Ctx& c) {
-  if (c.P.n_buf > 0) {  // which buffer zones prescribe their velocity at t^n, t^{n+1/2}, t^{n+1} [P23]
-    c.P.buf_prev = c.P.buf_half = c.P.buf_new = 0u;
-    for (int b = 0; b < c.P.n_buf; ++b) {
-      const double ts = c.params.buffers[b].t_start;
-      if (c.t > ts) c.P.buf_prev |= 1u << b;
-      if (c.t + 0.5 * c.P.dt > ts) c.P.buf_half |= 1u << b;
-      if (c.t + c.P.dt > ts) c.P.buf_new |= 1u << b;
-    }
+// which buffer zones prescribe their velocity at t^n, t^{n+1/2}, t^{n+1} [P23]; a launch parameter, so it
+// is set before a step's graph key is formed (one_step) — inside a captured body a replay would skip it
+void update_buffer_flags(Ctx& c) {
+  if (c.P.n_buf <= 0) return;
+  c.P.buf_prev = c.P.buf_half = c.P.buf_new = 0u;
+  for (int b = 0; b < c.P.n_buf; ++b) {
+    const double ts = c.params.buffers[b].t_start;
+    if (c.t > ts) c.P.buf_prev |= 1u << b;
+    if (c.t + 0.5 * c.P.dt > ts) c.P.buf_half |= 1u << b;
+    if (c.t + c.P.dt > ts) c.P.buf_new |= 1u << b;
   }
+}
+
+void kick_all(Ctx& c) {
+  update_buffer_flags(c);
   if (c.P.n_walls > 0) {
     eval_walls(c, c.t + 0.5 * c.P.dt, c.P.wall_vh, nullptr);
     eval_walls(c, c.t + c.P.dt, c.P.wall_v, c.P.wall_a);
@@ -678,6 +683,7 @@ int one_step(sphg_ctx* h) {
                 "ghost particles present: set an exchange callback (sphg_set_exchange) or drive the stages "
                 "through the decomposition layer (parallel.py)");
   const bool graphs = graphs_allowed(c);
+  update_buffer_flags(c);
   if (graphs) {
     if (!c.dtime) {  // [0] the force chain's time, [1] the clock (see k_step_tail)
       SPHG_CUDA_CHECK(cudaMalloc(&c.dtime, 2 * sizeof(double)));
@@ -1280,6 +1286,15 @@ int run_steps(sphg_ctx* h, int nsteps, sphg_soa* out) {
   }
   SPHG_CUDA_CHECK(cudaEventRecord(c.step_ev[0], c.stream));
   for (int k = 0; k < nsteps; ++k) {
+    // decomposed runs: stop before a step the partition might not cover (the caller repartitions and
+    // calls again for the remaining steps): a particle's drift since its partition is bounded by the
+    // displacements at the rebuilds since then plus the current one, and a step adds at most half a skin
+    if (c.nghost && c.partition_limit > 0.0 && c.disp_since_partition + c.max_disp + c.P.half_skin > c.partition_limit) {
+      if (c.final_pending) launch_final_kick_particles(c);
+      c.defer_final = false;
+      host_sync(c, c.stream);
+      return SPHG_NEED_PARTITION;
+    }
     c.defer_final = k + 1 < nsteps && c.P.transitions == 0 && !c.timing;
     if (overlap && k + 1 == nsteps)
       c.pre_forces = [&pl](Ctx& cc) {
@@ -1642,6 +1657,19 @@ int sphg_halo_bind(sphg_ctx* h, int phase, int slot, double* buf) {
 
 int sphg_max_bind(sphg_ctx* h, uint64_t* words) {
   h->c.max_words = words;
+  return SPHG_OK;
+}
+
+int sphg_set_partition_limit(sphg_ctx* h, double limit) {
+  h->c.partition_limit = limit;
+  return SPHG_OK;
+}
+
+int sphg_counters(sphg_ctx* h, int64_t out[4]) {
+  out[0] = h->c.steps;
+  out[1] = h->c.rebuilds;
+  out[2] = h->c.host_syncs;
+  out[3] = h->c.launches;
   return SPHG_OK;
 }
 

@@ -206,6 +206,7 @@ struct Ctx {
   int world = 1;
   size_t nf_interior = 0;        // fidx[0, nf_interior): fluid particles with no ghost neighbour
   double disp_since_partition = 0.0;  // sum of the global displacements at rebuilds since the last upload
+  double partition_limit = 0.0;       // sphg_set_partition_limit (0 = none)
   DBuf<double> body_tot;         // merged nb x 12 totals
   cudaStream_t dens_stream = nullptr;
   cudaEvent_t dens_fork = nullptr, dens_join = nullptr;

@@ -382,23 +382,28 @@ class DistributedSimulation:
     def step(self, nsteps=1):
         e = self.engine
         if self._fused_ok():
-            # one engine call per step: the engine runs kick .. final kick with its own exchanges; the
-            # host only decides between steps whether the partition still covers the drift (a particle
-            # may drift up to margin/2 before its ghosts could miss a neighbour; a step with a rebuild
-            # adds at most half a skin)
-            r0 = e.stats().rebuilds
-            for _ in range(nsteps):
-                md, acc, _u = self.drift()
-                if acc + md + self.half_skin > 0.5 * self.margin:
+            # the engine runs kick .. final kick with its own exchanges, nsteps at a time; it stops with
+            # NEED_PARTITION before a step the partition may not cover (a particle may drift up to
+            # margin/2 before its ghosts could miss a neighbour), the host migrates and steps on
+            f = lambda name: getattr(e.lib, e.prefix + name)
+            e._check(f("set_partition_limit")(e._h, 0.5 * self.margin), "set_partition_limit")
+            s0, r0 = e.counters()[:2]
+            done = 0
+            while done < nsteps:
+                rc = f("step")(e._h, nsteps - done)
+                s1 = e.counters()[0]
+                done += s1 - s0
+                s0 = s1
+                if rc == abi.NEED_PARTITION:
                     self.repartition()
-                try:
-                    e.step(1)
-                except Exception:
+                    continue
+                if rc != 0:
                     if self._xerr is not None:
                         raise RuntimeError(f"exchange failed: {self._xerr!r}") from self._xerr
-                    raise
-                self.steps += 1
-            self.rebuilds += e.stats().rebuilds - r0
+                    e._check(rc, "step")
+            self.steps += nsteps
+            r1 = e.counters()[1]
+            self.rebuilds += r1 - r0
             return
         thermal = bool(self.params.thermal) or bool(self.params.diffusion)  # one stage for T and C
         for _ in range(nsteps):

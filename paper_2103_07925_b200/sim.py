@@ -261,6 +261,12 @@ class Simulation:
         assert dt.itemsize == C.sizeof(abi.Event)
         return np.frombuffer(bytes(buf), dt, count=n.value).copy()
 
+    def counters(self):
+        """Cheap host counters: (steps, rebuilds, host_syncs, kernel_launches)."""
+        out = (C.c_int64 * 4)()
+        self._check(self._fn("counters")(self._h, out), "counters")
+        return tuple(out)
+
     def count_pairs(self):
         """(candidates, interacting, interacting with fluid i, interacting with non-fluid i)."""
         out = (C.c_int64 * 4)()
