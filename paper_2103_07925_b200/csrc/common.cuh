@@ -300,6 +300,40 @@ __device__ __forceinline__ double3 pair_delta(const DevParams& P, double3 a, dou
   return d;
 }
 
+// A particle that crosses a periodic face between rebuilds moves by -/+L: the image codes of its pairs,
+// fixed at build time, are then off by one period.  The drift records it (wrap code: per axis 0 none, 1 the
+// particle jumped by -L, 2 by +L, base 3) and k_wrap_patch_* shift the codes of its row entries and of
+// the entries that reference it, so d = r_i - r_j + shift stays the minimum image until the next rebuild.
+__device__ __forceinline__ uint32_t wrap_code(const DevParams& P, double3 o, double3 n) {
+  uint32_t code = 0, mul = 1;
+  const double xo[3] = {o.x, o.y, o.z}, xn[3] = {n.x, n.y, n.z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (P.periodic[a]) {
+      const double d = xn[a] - xo[a];
+      if (d < -P.halfL[a]) code += 1u * mul;       // crossed hi: jumped by -L
+      else if (d > P.halfL[a]) code += 2u * mul;   // crossed lo: jumped by +L
+    }
+    mul *= 3u;
+  }
+  return code;
+}
+// entry image code + sign * (wrap of one side): per axis value v in {0, +1, -1} (codes 0, 1, 2)
+__device__ __forceinline__ uint32_t shift_code(uint32_t code, uint32_t w, int sign) {
+  uint32_t out = 0, mul = 1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int c = (int)(code % 3u), wa = (int)(w % 3u);
+    int v = c == 1 ? 1 : (c == 2 ? -1 : 0);
+    v += sign * (wa == 1 ? 1 : (wa == 2 ? -1 : 0));  // x_i jumped by -L: d = x_i - x_j + s needs s + L
+    out += (uint32_t)(v == 1 ? 1 : (v == -1 ? 2 : 0)) * mul;
+    code /= 3u;
+    w /= 3u;
+    mul *= 3u;
+  }
+  return out;
+}
+
 // Kind-partitioned rows: while building, fluid neighbours fill row i from the front and rigid /
 // boundary neighbours from the back; the back segment is then moved next to the front one, so a
 // row is [fluid (nf) | non-fluid (no)] contiguous.  cnt[i] packs both counts (nf | no << 16).
@@ -417,8 +451,21 @@ struct DevFlags {
   uint32_t changed;                   // label propagation
   uint32_t pad[2];
   uint32_t build_overflow;            // cell-cooperative build could not take a cell
-  uint32_t pad2[3];
+  uint32_t n_wrapped;                 // particles that crossed a periodic face this step (wrap_list)
+  uint32_t pad2[2];
 };
+
+// drift / upload_state: note a periodic-face crossing for the row patch (kernels_step.cu k_wrap_patch_*)
+__device__ __forceinline__ void record_wrap(const DevParams& P, DevFlags* fl, uint32_t* list, uint32_t k, double3 o,
+                                            double3 n) {
+  if (P.img_mode != kImgCode || !list) return;
+  const uint32_t w = wrap_code(P, o, n);
+  if (w) {
+    const uint32_t s = atomicAdd(&fl->n_wrapped, 1u);
+    list[2 * s] = k;
+    list[2 * s + 1] = w;
+  }
+}
 
 __device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, double v) {
   atomicMax(addr, (unsigned long long)__double_as_longlong(v));

@@ -114,7 +114,8 @@ struct Ctx {
   void* wall_user = nullptr;
   // transitions scratch
   DBuf<uint32_t> ev_idx, ev_flag, label, tscratch;
-  DBuf<uint32_t> label_list, label_flags;  // compact list of labelled particles; sweep flags + count
+  DBuf<uint32_t> label_list, label_flags;
+  DBuf<uint32_t> wrap_list;  // (index, wrap code) of the particles that crossed a periodic face this step  // compact list of labelled particles; sweep flags + count
   // transition event log (sphg_set_event_log): device buffer of the current batch, host accumulation
   bool event_log = false;
   DBuf<sphg_event> ev_log;
@@ -239,6 +240,7 @@ void launch_rigid_index(Ctx& c);
 // kernels_step.cu
 void launch_body_kick(Ctx& c);
 void launch_kick_drift(Ctx& c);
+void launch_wrap_patch(Ctx& c);  // image codes of rows after periodic-face crossings (n_wrapped, wrap_list)
 void launch_step_tail(Ctx& c);  // dskip (rebuild or error pending) and the device clock t^{n+1}
 void launch_density(Ctx& c);
 void launch_density_interior(Ctx& c, cudaStream_t st);
@@ -270,6 +272,7 @@ void shepard_grid(Ctx& c, const double origin[3], const double spacing[3], const
 void build_idx_of_gid(Ctx& c);
 void halo_pack(Ctx& c, int phase, int slot, double* buf);
 void halo_unpack(Ctx& c, int phase, int slot, const double* buf);
+void wrap_ghosts(Ctx& c);
 void body_partials(Ctx& c, double* dev_out);
 void body_apply_totals(Ctx& c, const double* dev_tot);
 

@@ -717,6 +717,7 @@ void launch_rebuild(Ctx& c) {
   const size_t n = c.n;
   cudaStream_t s = c.stream;
   if (n == 0) return;
+  wrap_ghosts(c);
   // 1. keys in gid order
   k_keys_by_gid<<<grid_for(n, 256), 256, 0, s>>>(c.P, c.cur.G0.p, c.cur.gid.p, n, c.keys.p, c.vals.p, c.dflags);
   // 2. stable radix sort by cell

@@ -72,7 +72,7 @@ __global__ void k_body_kick(const __grid_constant__ DevParams P, sphg_body* __re
 template <bool kFinal>
 __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevParams P, Particles D,
                                                      const sphg_body* __restrict__ B, size_t n,
-                                                     DevFlags* __restrict__ fl) {
+                                                     DevFlags* __restrict__ fl, uint32_t* __restrict__ wrap_list) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   double disp2 = 0.0, u2 = 0.0;
   if (k < n) {
@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevP
       }
       pn = make_double3(wrap1(P, axpy_rn(p.x, P.dt, ua.x), 0), wrap1(P, axpy_rn(p.y, P.dt, ua.y), 1),
                         wrap1(P, axpy_rn(p.z, P.dt, ua.z), 2));
+      record_wrap(P, fl, wrap_list, (uint32_t)k, p, pn);
       stpos(&D.G0.p[k], pn);
       stpos(&D.G1.p[k], uh);
       stpos(&D.G2.p[k], make_double3(__dsub_rn(ua.x, uh.x), __dsub_rn(ua.y, uh.y), __dsub_rn(ua.z, uh.z)));
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevP
       const double3 rk = qrotate(body_q(b), ld3(D.X4.p[k]));
       pn = make_double3(wrap1(P, __dadd_rn(b.com[0], rk.x), 0), wrap1(P, __dadd_rn(b.com[1], rk.y), 1),
                         wrap1(P, __dadd_rn(b.com[2], rk.z), 2));
+      record_wrap(P, fl, wrap_list, (uint32_t)k, ldpos(&D.G0.p[k]), pn);
       stpos(&D.G0.p[k], pn);
       const double3 wxr = cross3(bv(b.omega), rk);
       stpos(&D.V4.p[k], make_double3(b.vel[0] + wxr.x, b.vel[1] + wxr.y, b.vel[2] + wxr.z));
@@ -128,6 +130,7 @@ __global__ void __launch_bounds__(256) k_kick_drift(const __grid_constant__ DevP
       pn = make_double3(wrap1(P, axpy_rn(p.x, P.dt, P.wall_vh[gr][0]), 0),
                         wrap1(P, axpy_rn(p.y, P.dt, P.wall_vh[gr][1]), 1),
                         wrap1(P, axpy_rn(p.z, P.dt, P.wall_vh[gr][2]), 2));
+      record_wrap(P, fl, wrap_list, (uint32_t)k, p, pn);
       stpos(&D.G0.p[k], pn);
       stpos(&D.V4.p[k], make_double3(P.wall_v[gr][0], P.wall_v[gr][1], P.wall_v[gr][2]));
     } else {
@@ -443,8 +446,12 @@ __global__ void k_halo_pack(Particles D, int phase, const uint32_t* __restrict__
   }
 }
 
-__global__ void k_halo_unpack(Particles D, int phase, const uint32_t* __restrict__ ids, size_t m,
-                              const uint32_t* __restrict__ idx, const double* __restrict__ buf) {
+// continuous (the Verlet rows are valid): a ghost whose owner moved it across a periodic face keeps
+// coordinates continuous with the ones its image-coded entries were built for (unwrapped by one period);
+// launch_rebuild wraps ghosts back before binning
+__global__ void k_halo_unpack(const __grid_constant__ DevParams P, Particles D, int phase,
+                              const uint32_t* __restrict__ ids, size_t m, const uint32_t* __restrict__ idx,
+                              const double* __restrict__ buf, int continuous) {
   const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= m) return;
   const uint32_t k = idx[ids[s]];
@@ -453,7 +460,17 @@ __global__ void k_halo_unpack(Particles D, int phase, const uint32_t* __restrict
   double* g2 = reinterpret_cast<double*>(&D.G2.p[k]);
   if (phase == SPHG_HALO_STATE) {
     const double* o = buf + s * 14;
-    g0[0] = o[0]; g0[1] = o[1]; g0[2] = o[2];
+    double x[3] = {o[0], o[1], o[2]};
+    if (continuous) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (P.periodic[a]) {
+          const double d = x[a] - g0[a];
+          if (d > P.halfL[a]) x[a] -= P.L[a];
+          else if (d < -P.halfL[a]) x[a] += P.L[a];
+        }
+    }
+    g0[0] = x[0]; g0[1] = x[1]; g0[2] = x[2];
     g1[0] = o[3]; g1[1] = o[4]; g1[2] = o[5];
     g2[0] = o[6]; g2[1] = o[7]; g2[2] = o[8];
     double* v = reinterpret_cast<double*>(&D.V4.p[k]);
@@ -539,6 +556,44 @@ __global__ void k_apply_totals(const __grid_constant__ DevParams P, sphg_body* _
   }
 }
 
+// Periodic-face crossings since the rebuild (record_wrap, common.cuh): phase 1 shifts the codes of the
+// crossing particle's own row, phase 2 those of the entries of its neighbours' rows that reference it
+// (the candidate lists are symmetric).  Warp per crossing particle, grid-stride over the device-side count
+// so the launch is graph-capturable.  Two launches: every entry is then changed by exactly one warp per
+// phase and the two shifts (x_i's and x_j's) add up.
+__global__ void k_wrap_patch_own(const uint32_t* __restrict__ list, const DevFlags* __restrict__ fl, NbrList L) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t m = fl->n_wrapped;
+  for (uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < m; e += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t i = list[2 * e], w = list[2 * e + 1];
+    uint32_t* row = const_cast<uint32_t*>(L.nbr) + (size_t)i * L.cap;
+    const uint32_t nn = cnt_total(L.cnt[i]);
+    for (uint32_t k = lane; k < nn; k += 32) {
+      const uint32_t en = row[k];
+      row[k] = (en & kIdxMask) | (shift_code(en >> kIdxBits, w, +1) << kIdxBits);
+    }
+  }
+}
+
+__global__ void k_wrap_patch_peer(const uint32_t* __restrict__ list, const DevFlags* __restrict__ fl, NbrList L) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t m = fl->n_wrapped;
+  for (uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < m; e += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t i = list[2 * e], w = list[2 * e + 1];
+    const uint32_t* rowi = L.nbr + (size_t)i * L.cap;
+    const uint32_t ni = cnt_total(L.cnt[i]);
+    for (uint32_t q = 0; q < ni; ++q) {
+      const uint32_t j = rowi[q] & kIdxMask;
+      uint32_t* rowj = const_cast<uint32_t*>(L.nbr) + (size_t)j * L.cap;
+      const uint32_t nj = cnt_total(L.cnt[j]);
+      for (uint32_t k = lane; k < nj; k += 32) {
+        const uint32_t en = rowj[k];
+        if ((en & kIdxMask) == i) rowj[k] = i | (shift_code(en >> kIdxBits, w, -1) << kIdxBits);
+      }
+    }
+  }
+}
+
 // global body totals from the ranks' compensated partials, merged in rank order with TwoSum (the same
 // single IEEE adds as parallel._merge_partials, so every rank gets bit-identical totals)
 __global__ void k_merge_partials(const double* __restrict__ g, size_t nb, int world, double* __restrict__ tot) {
@@ -556,20 +611,29 @@ __global__ void k_merge_partials(const double* __restrict__ g, size_t nb, int wo
   tot[q] = __dadd_rn(s, c);
 }
 
-__global__ void k_scatter_state(Particles D, size_t n, const uint32_t* __restrict__ idx, const double* __restrict__ pos,
-                                const double* __restrict__ vel) {
+__global__ void k_scatter_state(const __grid_constant__ DevParams P, Particles D, size_t n,
+                                const uint32_t* __restrict__ idx, const double* __restrict__ pos,
+                                const double* __restrict__ vel, DevFlags* __restrict__ fl, uint32_t* __restrict__ wl) {
   const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
   const uint32_t k = idx[g];
-  if (pos) stpos(&D.G0.p[k], make_double3(pos[3 * g], pos[3 * g + 1], pos[3 * g + 2]));
+  if (pos) {
+    const double3 pn = make_double3(pos[3 * g], pos[3 * g + 1], pos[3 * g + 2]);
+    record_wrap(P, fl, wl, k, ldpos(&D.G0.p[k]), pn);
+    stpos(&D.G0.p[k], pn);
+  }
   if (vel) stpos(&D.V4.p[k], make_double3(vel[3 * g], vel[3 * g + 1], vel[3 * g + 2]));
 }
 
 }  // namespace
 
 void scatter_state(Ctx& c, const double* pos, const double* vel) {
-  k_scatter_state<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.cur, c.n, c.idx_of_gid.p, pos, vel);
+  c.wrap_list.alloc(2 * c.n);
+  SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->n_wrapped, 0, sizeof(uint32_t), c.stream));
+  uint32_t* wl = c.P.img_mode == kImgCode && c.built ? c.wrap_list.p : nullptr;
+  k_scatter_state<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, c.idx_of_gid.p, pos, vel, c.dflags, wl);
   c.launches++;
+  launch_wrap_patch(c);
 }
 
 void build_idx_of_gid(Ctx& c) {
@@ -589,7 +653,24 @@ void halo_pack(Ctx& c, int phase, int slot, double* buf) {
 void halo_unpack(Ctx& c, int phase, int slot, const double* buf) {
   const size_t m = c.halo_n[slot];
   if (m == 0) return;
-  k_halo_unpack<<<grid_for(m, 256), 256, 0, c.stream>>>(c.cur, phase, c.halo_ids[slot].p, m, c.idx_of_gid.p, buf);
+  const int continuous = c.built && c.P.img_mode == kImgCode ? 1 : 0;
+  k_halo_unpack<<<grid_for(m, 256), 256, 0, c.stream>>>(c.P, c.cur, phase, c.halo_ids[slot].p, m, c.idx_of_gid.p, buf,
+                                                        continuous);
+  c.launches++;
+}
+
+namespace {
+__global__ void k_wrap_ghosts(const __grid_constant__ DevParams P, Particles D, size_t n) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || !is_ghost(D.kmd.p[k])) return;
+  const double3 p = ldpos(&D.G0.p[k]);
+  stpos(&D.G0.p[k], make_double3(wrap1(P, p.x, 0), wrap1(P, p.y, 1), wrap1(P, p.z, 2)));
+}
+}  // namespace
+
+void wrap_ghosts(Ctx& c) {  // before binning: ghosts kept continuous across periodic faces (k_halo_unpack)
+  if (c.nghost == 0 || c.P.img_mode != kImgCode) return;
+  k_wrap_ghosts<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n);
   c.launches++;
 }
 
@@ -664,14 +745,25 @@ void launch_step_tail(Ctx& c) {
   c.launches++;
 }
 
+void launch_wrap_patch(Ctx& c) {
+  if (c.P.img_mode != kImgCode || !c.built || c.n == 0) return;
+  k_wrap_patch_own<<<64, 256, 0, c.stream>>>(c.wrap_list.p, c.dflags, c.nl());
+  k_wrap_patch_peer<<<64, 256, 0, c.stream>>>(c.wrap_list.p, c.dflags, c.nl());
+  c.launches += 2;
+}
+
 void launch_kick_drift(Ctx& c) {
   if (c.n == 0) return;
+  c.wrap_list.alloc(2 * c.n);
+  SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->n_wrapped, 0, sizeof(uint32_t), c.stream));
+  uint32_t* wl = c.P.img_mode == kImgCode && c.built ? c.wrap_list.p : nullptr;
   if (c.final_pending)  // the previous step deferred its particle final kick into this pass
-    k_kick_drift<true><<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.n, c.dflags);
+    k_kick_drift<true><<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.n, c.dflags, wl);
   else
-    k_kick_drift<false><<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.n, c.dflags);
+    k_kick_drift<false><<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.bodies.p, c.n, c.dflags, wl);
   c.final_pending = false;
   c.launches++;
+  launch_wrap_patch(c);  // rows stay valid across periodic faces until the next rebuild
 }
 
 void launch_bodies(Ctx& c) {

@@ -95,10 +95,30 @@ def _worker(rank, world, port, case, out):
     dist.destroy_process_group()
 
 
-NSTEPS = {"c1": 6, "c2": 6, "c1fast": 16, "c3": 6, "diff": 6, "bigbody": 0}
+NSTEPS = {"c1": 6, "c2": 6, "c1fast": 16, "c3": 6, "diff": 6, "bigbody": 0, "c1wrap": 6}
+
+
+def crossing_case():
+    """C1 (20^3, 3 spheres) with 60 fluid particles a hair inside the periodic faces, moving out: they
+    cross in the first steps, long before any Verlet rebuild (image-coded rows must follow them)."""
+    sc = scenarios.config1(nside=20, n_spheres=3, r_range=(3.0, 4.0), seed=11)
+    st = sc.store
+    L = sc.params.hi[0] - sc.params.lo[0]
+    fl = np.nonzero(st.kind == abi.FLUID)[0]
+    rng = np.random.default_rng(23)
+    pick = rng.choice(fl, 60, replace=False)
+    for q, i in enumerate(pick):
+        a = q % 3
+        hi_side = (q // 3) % 2 == 0
+        st.pos[i, a] = L - 2e-7 if hi_side else 2e-7
+        st.vel[i, a] = 0.05 if hi_side else -0.05
+    st.vel_adv[:] = st.vel
+    return sc
 
 
 def _case(case):
+    if case == "c1wrap":
+        return crossing_case()
     if case == "bigbody":  # one body of ~1e4 particles in a periodic fluid box (SPEC acceptance 5)
         return scenarios.config1(nside=36, n_spheres=1, r_range=(13.0, 13.0), seed=17)
     if case == "c1":
@@ -116,7 +136,8 @@ def _case(case):
     return sc
 
 
-@pytest.mark.parametrize("case,world", [("c1", 2), ("c2", 2), ("c1fast", 2), ("c3", 2), ("diff", 2), ("c1", 4)])
+@pytest.mark.parametrize("case,world", [("c1", 2), ("c2", 2), ("c1fast", 2), ("c3", 2), ("diff", 2), ("c1", 4),
+                                        ("c1wrap", 2)])
 def test_ranks_match_one_rank(case, world, tmp_path, oracle_mod):
     out = str(tmp_path / "ds.npz")
     mp.spawn(_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)

@@ -71,7 +71,7 @@ def test_gpu_two_ranks_one_step_parity(tmp_path):
     assert vec_err(d["btorque"][al], b["torque"][al], s["body_torque"][al]) <= 1
 
 
-@pytest.mark.parametrize("case", ["c1fast", "c2"])
+@pytest.mark.parametrize("case", ["c1fast", "c2", "c1wrap"])
 def test_gpu_two_ranks_match_single_rank(case, tmp_path):
     from paper_2103_07925_b200 import Simulation, abi
     from oracle.oracle import Oracle

@@ -682,6 +682,27 @@ def test_graph_replay_is_bit_identical(monkeypatch, name, steps):
     assert np.array_equal(ba, bb)
 
 
+def test_periodic_face_crossing_between_rebuilds(Oracle):
+    """Particles that cross a periodic face between Verlet rebuilds: the image codes stored in the rows
+    (fixed at build time) are patched for them and for the entries referencing them, so every step
+    matches the oracle (minimum image throughout) and no rebuild is triggered by the crossing."""
+    from tests.test_decomposition import crossing_case
+    sc = crossing_case()
+    sim, orc = run_pair(sc, sim_factory, Oracle)
+    for k in range(4):
+        sim.step(1)
+        orc.step(1)
+        compare_state(sim, orc, sc.params, tol=1e-10 if k == 0 else 1e-8, what=f"crossing step {k + 1}")
+    assert sim.stats().rebuilds == orc.stats().rebuilds == 1
+    g, _ = sim.download()
+    L = sc.params.hi[0] - sc.params.lo[0]
+    moved = np.abs(g.pos - sc.store.pos) > 0.5 * L
+    assert moved.sum() == 60  # every planted particle crossed its face
+    sim.step(6)  # graph-replayed steps carry the patch as well
+    orc.step(6)
+    compare_state(sim, orc, sc.params, tol=1e-7, what="crossing 10 steps")
+
+
 def _fast(sc, u):
     """Fluid velocities raised to |u_i| ~ u so Verlet rebuilds happen within a few steps."""
     fl = sc.store.kind == abi.FLUID
