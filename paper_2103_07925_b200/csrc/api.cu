@@ -1152,6 +1152,7 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     c.alt.alloc(na, c.P.diffusion != 0);
     c.H2new.alloc(na);
     c.pin_list.alloc(na);
+    c.wrap_list.alloc(2 * na);  // periodic-face crossings of a step (allocated here: the kick chain is captured)
     if (!c.pin_any) SPHG_CUDA_CHECK(cudaMalloc(&c.pin_any, sizeof(uint32_t)));
     if (c.P.diffusion) c.C2new.alloc(na);
     if (c.P.heat_source) {

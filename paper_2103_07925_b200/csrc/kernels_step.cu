@@ -628,7 +628,6 @@ __global__ void k_scatter_state(const __grid_constant__ DevParams P, Particles D
 }  // namespace
 
 void scatter_state(Ctx& c, const double* pos, const double* vel) {
-  c.wrap_list.alloc(2 * c.n);
   SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->n_wrapped, 0, sizeof(uint32_t), c.stream));
   uint32_t* wl = c.P.img_mode == kImgCode && c.built ? c.wrap_list.p : nullptr;
   k_scatter_state<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.P, c.cur, c.n, c.idx_of_gid.p, pos, vel, c.dflags, wl);
@@ -754,7 +753,6 @@ void launch_wrap_patch(Ctx& c) {
 
 void launch_kick_drift(Ctx& c) {
   if (c.n == 0) return;
-  c.wrap_list.alloc(2 * c.n);
   SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->n_wrapped, 0, sizeof(uint32_t), c.stream));
   uint32_t* wl = c.P.img_mode == kImgCode && c.built ? c.wrap_list.p : nullptr;
   if (c.final_pending)  // the previous step deferred its particle final kick into this pass
