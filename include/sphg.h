@@ -43,7 +43,9 @@ enum {
   SPHG_ERR_CONFIG = 2,
   SPHG_ERR_RUNTIME = 3,
   SPHG_ERR_CUDA = 4,
-  SPHG_NEED_PARTITION = 5 /* not an error: sphg_step stopped before a step its partition may not cover */
+  SPHG_NEED_PARTITION = 5, /* not an error: sphg_step stopped before a step its partition may not cover */
+  SPHG_NEED_TRANSITIONS = 6 /* not an error: a decomposed step detected phase transitions on some rank;
+                               the caller applies the batch (sphg_event_*, sphg_record_*) and steps on */
 };
 
 /* POD mirror of sphfsi::Material (material.hpp:17-36) plus the per-material
@@ -351,6 +353,33 @@ int sphg_body_partials(sphg_ctx* ctx, double* out);
 int sphg_body_apply_totals(sphg_ctx* ctx, const double* totals);
 /* Max displacement since the last rebuild over owned particles (after a KICK_DRIFT stage). */
 int sphg_max_displacement(sphg_ctx* ctx, double* out);
+/* Phase transitions under decomposition ("Event detection is worker-local; application is
+ * serialized per affected body at the owner, followed by a broadcast of updated body state and re-linking
+ * of affected particles").  With transitions on, a decomposed step ends with detection over the owned
+ * particles and a MAX exchange of the event counts; when any rank has events, sphg_step returns
+ * SPHG_NEED_TRANSITIONS after completing that step.  The caller then
+ *   1. sphg_event_bodies: the bodies a batch can touch (bodies of melting particles, bodies with a rigid
+ *      particle within r_c of a solidifying one, ghosts included), OR-ed over ranks;
+ *   2. sphg_event_members: the owned event particles and owned members of those bodies (local ids);
+ *   3. sphg_record_pack of them, gathered at one rank, which uploads them (global gid order) into a
+ *      single-rank context, applies the batch there with the single-rank kernels (sphg_run_stage
+ *      TRANSITIONS: the sub-store holds every particle the batch reads) and broadcasts the records
+ *      and the new body table;
+ *   4. sphg_record_unpack (keep_position = 1) of every listed particle present on the rank (owned or
+ *      ghost) and sphg_replace_bodies, then the body force/torque of the new membership (body partials).
+ * Records are sphg_record_doubles() doubles: [0..2] position, [3] kind, [4] material, [5] group,
+ * [6] mass, then the engine's own per-particle state (opaque; only the same engine reads it back).
+ * `mask` holds n_bodies bytes; ids are local ids in ascending order; buffers are host memory. */
+int sphg_event_bodies(sphg_ctx* ctx, uint8_t* mask, size_t n_bodies);
+int sphg_event_members(sphg_ctx* ctx, const uint8_t* mask, size_t n_bodies, uint32_t* ids, size_t cap, size_t* n);
+int sphg_record_doubles(void);
+int sphg_record_pack(sphg_ctx* ctx, const uint32_t* ids, size_t m, double* recs);
+/* keep_position = 1: the local copy keeps its coordinates (ghosts may be unwrapped across a periodic face)
+ * and its ghost/owned role; 0: the record's position is written too (the single-rank batch context) */
+int sphg_record_unpack(sphg_ctx* ctx, const uint32_t* ids, size_t m, const double* recs, int keep_position);
+/* replaces the body table after record_unpack changed kinds / groups and refreshes the index lists
+ * (rigid body-major list, kind lists, row partitions, contact order) */
+int sphg_replace_bodies(sphg_ctx* ctx, const sphg_body* bodies, size_t n_bodies);
 /* Transition event log ("Event log (CSV): step, particle id, direction, body ids"): when enabled,
  * every applied transition is recorded as (step, gid, direction 1 melt / 2 solidify, body it left (melt)
  * or -1, body it ended the batch in (solidify, after splits) or -1), ordered by step then gid.

@@ -106,6 +106,7 @@ struct Ctx {
     double* body_gath = nullptr;
     int world = 1;
     bool has_ghosts = false;
+    std::vector<uint8_t> ev;        // events of the last decomposed detection (1 melt, 2 solidify)
     double disp_since_partition = 0.0;
     double partition_limit = 0.0;
     int dt_term = -1;
@@ -1011,12 +1012,13 @@ bool stage_final_kick(Ctx& c) {
 // ------------------------------------------------------------ transitions
 // detect_transitions / apply_transitions / post_transition_body_velocity /
 // split_disconnected_bodies [P12]
-bool stage_transitions(Ctx& c) {
-    if (c.P.transitions != 1 && c.P.transitions != 2) return true;
+// detect_transitions over the owned particles (a decomposed rank leaves its ghosts to their owners)
+void detect_events(const Ctx& c, std::vector<uint32_t>& melt, std::vector<uint32_t>& solid) {
     const bool conc = c.P.transitions == 2;  // TransitionMode::Concentration (config.hpp:61) [P19]
-    const size_t n = c.S.size();
-    std::vector<uint32_t> melt, solid;
-    for (size_t i = 0; i < n; ++i) {
+    melt.clear();
+    solid.clear();
+    for (size_t i = 0; i < c.S.size(); ++i) {
+        if (ghost(c, i)) continue;
         const sphg_material& m = c.P.mat[c.S.material[i]];
         const double thr = conc ? m.C_t : m.T_t;
         const double x = conc ? c.S.concentration[i] : c.S.temperature[i];
@@ -1025,6 +1027,13 @@ bool stage_transitions(Ctx& c) {
         else if (c.S.kind[i] == Kind::Fluid && m.solidify_target >= 0 && x < thr)
             solid.push_back((uint32_t)i);
     }
+}
+
+bool stage_transitions(Ctx& c) {
+    if (c.P.transitions != 1 && c.P.transitions != 2) return true;
+    const size_t n = c.S.size();
+    std::vector<uint32_t> melt, solid;
+    detect_events(c, melt, solid);
     if (melt.empty() && solid.empty()) return true;
     c.n_melt += (int64_t)melt.size();
     c.n_solid += (int64_t)solid.size();
@@ -1208,7 +1217,10 @@ bool run_stage(Ctx& c, int s) {
         case SPHG_STAGE_BODIES: return stage_bodies(c);
         case SPHG_STAGE_KICK_DRIFT: return stage_kick_drift(c);
         case SPHG_STAGE_FINAL_KICK: return stage_final_kick(c);
-        case SPHG_STAGE_TRANSITIONS: return stage_transitions(c);
+        case SPHG_STAGE_TRANSITIONS:
+            if (c.P.transitions && c.has_ghosts)
+                return fail(c, "with ghost particles, transitions are applied by the decomposed batch");
+            return stage_transitions(c);
         case SPHG_STAGE_MASS: return stage_mass(c);
     }
     return fail(c, "unknown stage");
@@ -1362,10 +1374,6 @@ int orc_upload(orc_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t nb
     for (size_t i = 0; i < n; ++i) any_ghost |= ghost(c, i);
     c.has_ghosts = any_ghost;
     c.disp_since_partition = 0.0;
-    if (any_ghost && c.P.transitions) {
-        c.err = "phase transitions are single-rank only (ghost particles present)";
-        return SPHG_ERR_CONFIG;
-    }
     resize_aux(c);
     c.m_r = 0.0;  // [P22]: rigid particles, and fluid particles that may solidify
     for (size_t i = 0; i < n; ++i) {
@@ -1830,7 +1838,6 @@ static int halo_xchg(orc_ctx* h, int phase) {
 
 int decomposed_step(orc_ctx* h) {
     Ctx& c = *reinterpret_cast<Ctx*>(h);
-    if (c.P.transitions) return SPHG_ERR_CONFIG;
     if (!c.max_words) return SPHG_ERR_CONFIG;
     const bool ok = stage_kick_drift(c);
     // global max displacement and speed (a local error travels as +inf)
@@ -1883,7 +1890,132 @@ int decomposed_step(orc_ctx* h) {
     }
     if (!stage_final_kick(c)) return SPHG_ERR_RUNTIME;
     c.steps++;
-    return check_dt(c) ? SPHG_OK : SPHG_ERR_RUNTIME;
+    if (!check_dt(c)) return SPHG_ERR_RUNTIME;
+    if (c.P.transitions) {  // owned detection + global counts (api.cu one_step_decomposed)
+        std::vector<uint32_t> melt, solid;
+        detect_events(c, melt, solid);
+        c.ev.assign(c.S.size(), 0);
+        for (uint32_t i : melt) c.ev[i] = 1;
+        for (uint32_t i : solid) c.ev[i] = 2;
+        c.max_words[0] = melt.size();
+        c.max_words[1] = solid.size();
+        if ((rc = xchg(c, SPHG_XCHG_MAX))) return rc;
+        if (c.max_words[0] || c.max_words[1]) return SPHG_NEED_TRANSITIONS;
+    }
+    return SPHG_OK;
+}
+
+// ---- decomposed transition batches (sphg.h sphg_event_* / sphg_record_*), the oracle's records
+int orc_event_bodies(orc_ctx* h, uint8_t* mask, size_t nb) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (nb != c.bodies.size()) return SPHG_ERR_CONFIG;
+    const double rc2 = c.rc * c.rc;
+    for (size_t i = 0; i < c.ev.size() && i < c.S.size(); ++i) {
+        if (c.ev[i] == 1) mask[c.S.group[i]] = 1;
+        if (c.ev[i] != 2) continue;
+        for (uint32_t j : c.nl[i])
+            if (c.S.kind[j] == Kind::Rigid && r2of(mi3(c, c.S.pos[i], c.S.pos[j])) <= rc2) mask[c.S.group[j]] = 1;
+    }
+    return SPHG_OK;
+}
+
+int orc_event_members(orc_ctx* h, const uint8_t* mask, size_t nb, uint32_t* ids, size_t cap, size_t* n) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (nb != c.bodies.size()) return SPHG_ERR_CONFIG;
+    std::vector<uint32_t> out;
+    for (size_t i = 0; i < c.S.size(); ++i) {
+        if (ghost(c, i)) continue;
+        const bool ev = i < c.ev.size() && c.ev[i] != 0;
+        const bool member = c.S.kind[i] == Kind::Rigid && c.S.group[i] < nb && mask[c.S.group[i]];
+        if (ev || member) out.push_back((uint32_t)i);
+    }
+    *n = out.size();
+    if (!ids) return SPHG_OK;
+    if (cap < out.size()) return SPHG_ERR_CONFIG;
+    std::copy(out.begin(), out.end(), ids);
+    return SPHG_OK;
+}
+
+constexpr int kOrcRecord = 40;
+int orc_record_doubles(void) { return kOrcRecord; }
+
+int orc_record_pack(orc_ctx* h, const uint32_t* ids, size_t m, double* recs) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    auto& S = c.S;
+    for (size_t s = 0; s < m; ++s) {
+        const size_t i = ids[s];
+        if (i >= S.size()) return SPHG_ERR_CONFIG;
+        double* o = recs + s * kOrcRecord;
+        put3(o, S.pos[i]);
+        o[3] = (double)static_cast<int>(S.kind[i]);
+        o[4] = (double)S.material[i];
+        o[5] = (double)S.group[i];
+        o[6] = S.mass[i];
+        put3(o + 7, S.vel[i]);
+        put3(o + 10, S.vel_adv[i]);
+        put3(o + 13, S.acc[i]);
+        put3(o + 16, S.acc_bg[i]);
+        o[19] = S.density[i];
+        o[20] = S.pressure[i];
+        o[21] = S.temperature[i];
+        o[22] = S.dT_dt[i];
+        o[23] = S.concentration[i];
+        o[24] = S.dC_dt[i];
+        put3(o + 25, S.body_frame_pos[i]);
+        o[28] = S.wall_pressure[i];
+        put3(o + 29, S.wall_velocity[i]);
+        o[32] = S.dirichlet_T[i];
+        o[33] = S.dirichlet_C[i];
+        put3(o + 34, c.force[i]);
+        o[37] = c.rho_w[i];
+        o[38] = c.V_w[i];
+        o[39] = c.wall_mat[i];
+    }
+    return SPHG_OK;
+}
+
+int orc_record_unpack(orc_ctx* h, const uint32_t* ids, size_t m, const double* recs, int keep_position) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    auto& S = c.S;
+    for (size_t s = 0; s < m; ++s) {
+        const size_t i = ids[s];
+        if (i >= S.size()) return SPHG_ERR_CONFIG;
+        const double* o = recs + s * kOrcRecord;
+        if (!keep_position) S.pos[i] = v3(o);
+        S.kind[i] = static_cast<Kind>((int)o[3]);
+        S.material[i] = (uint16_t)o[4];
+        S.group[i] = (uint32_t)o[5];
+        S.mass[i] = o[6];
+        S.vel[i] = v3(o + 7);
+        S.vel_adv[i] = v3(o + 10);
+        S.acc[i] = v3(o + 13);
+        S.acc_bg[i] = v3(o + 16);
+        S.density[i] = o[19];
+        S.pressure[i] = o[20];
+        S.temperature[i] = o[21];
+        S.dT_dt[i] = o[22];
+        S.concentration[i] = o[23];
+        S.dC_dt[i] = o[24];
+        S.body_frame_pos[i] = v3(o + 25);
+        S.wall_pressure[i] = o[28];
+        S.wall_velocity[i] = v3(o + 29);
+        S.dirichlet_T[i] = (uint8_t)o[32];
+        S.dirichlet_C[i] = (uint8_t)o[33];
+        c.force[i] = v3(o + 34);
+        c.rho_w[i] = o[37];
+        c.V_w[i] = o[38];
+        c.wall_mat[i] = (int)o[39];
+    }
+    return SPHG_OK;
+}
+
+int orc_replace_bodies(orc_ctx* h, const sphg_body* bodies, size_t nb) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    c.bodies.assign(bodies, bodies + nb);
+    c.body_fscale.resize(nb, 0.0);
+    c.body_tscale.resize(nb, 0.0);
+    rebuild_members(c);
+    return SPHG_OK;
 }
 
 int orc_max_displacement(orc_ctx* h, double* out) {

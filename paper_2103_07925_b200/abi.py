@@ -15,6 +15,7 @@ FLUID, RIGID, BOUNDARY = 0, 1, 2  # store.hpp:11 Kind
 
 OK, ERR_CONFIG, ERR_RUNTIME, ERR_CUDA = 0, 2, 3, 4
 NEED_PARTITION = 5  # sphg_step stopped before a step its partition may not cover (not an error)
+NEED_TRANSITIONS = 6  # a decomposed step detected phase transitions: the caller applies the batch (not an error)
 DT_REFUSE, DT_WARN, DT_OFF = 0, 1, 2  # sphg_params.dt_check
 DT_TERMS = ("cfl", "viscous", "body force", "contact", "conduction")  # compute_dt order
 
@@ -187,6 +188,13 @@ def declare(lib, prefix):
         "set_partition_limit": (C.c_int, [vp, C.c_double]),
         "counters": (C.c_int, [vp, C.POINTER(C.c_int64)]),
         "transition_events": (C.c_int, [vp, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t)]),
+        "event_bodies": (C.c_int, [vp, C.POINTER(C.c_uint8), C.c_size_t]),
+        "event_members": (C.c_int, [vp, C.POINTER(C.c_uint8), C.c_size_t, C.POINTER(C.c_uint32), C.c_size_t,
+                                    C.POINTER(C.c_size_t)]),
+        "record_doubles": (C.c_int, []),
+        "record_pack": (C.c_int, [vp, C.POINTER(C.c_uint32), C.c_size_t, C.POINTER(C.c_double)]),
+        "record_unpack": (C.c_int, [vp, C.POINTER(C.c_uint32), C.c_size_t, C.POINTER(C.c_double), C.c_int]),
+        "replace_bodies": (C.c_int, [vp, C.POINTER(Body), C.c_size_t]),
         "shepard_grid": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                    C.c_int32, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint8)]),
     }

@@ -411,6 +411,9 @@ int do_stage(sphg_ctx* h, int stage) {
       h->mid_step = false;
       break;
     case SPHG_STAGE_TRANSITIONS:
+      if (c.P.transitions != 0 && c.nghost)
+        return fail(h, SPHG_ERR_CONFIG, "with ghost particles, transitions are applied by the decomposed batch "
+                                        "(SPHG_NEED_TRANSITIONS, sphg_event_bodies / sphg_record_*)");
       if (c.P.transitions != 0) {
         const int rc = launch_transitions(c);
         if (rc) return fail(h, rc, c.err);
@@ -608,9 +611,13 @@ __global__ void k_flag_error_global(DevFlags* fl) {  // a local error becomes an
   if (fl->err) fl->max_disp2_bits = 0x7FF0000000000000ull;
 }
 
+__global__ void k_event_counts_to_words(const DevFlags* fl, uint64_t* words) {
+  words[0] = fl->n_events;  // melt
+  words[1] = fl->pad[0];    // solidify
+}
+
 int one_step_decomposed(sphg_ctx* h) {
   Ctx& c = h->c;
-  if (c.P.transitions) return fail(h, SPHG_ERR_CONFIG, "phase transitions are single-rank only");
   reset_step_flags(c);
   kick_all(c);
   k_flag_error_global<<<1, 1, 0, c.stream>>>(c.dflags);
@@ -672,7 +679,20 @@ int one_step_decomposed(sphg_ctx* h) {
   launch_final_kick(c);
   h->mid_step = false;
   c.steps++;
-  return check_dt(h);
+  if ((rc = check_dt(h))) return rc;
+  if (c.P.transitions) {
+    // detection over the owned particles, then the global event counts (MAX over ranks): when any rank
+    // has events the caller applies the batch before the next step (sphg.h)
+    launch_detect(c);
+    k_event_counts_to_words<<<1, 1, 0, c.stream>>>(c.dflags, c.max_words);
+    c.launches++;
+    if ((rc = exchange(h, SPHG_XCHG_MAX))) return rc;
+    uint64_t w[2] = {0, 0};
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(w, c.max_words, sizeof w, cudaMemcpyDeviceToHost, c.stream));
+    host_sync(c, c.stream);
+    if (w[0] || w[1]) return SPHG_NEED_TRANSITIONS;
+  }
+  return SPHG_OK;
 }
 
 int one_step(sphg_ctx* h) {
@@ -1135,8 +1155,6 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     size_t ng = 0;
     if (s->owner)
       for (size_t i = 0; i < n; ++i) ng += s->owner[i] != (uint32_t)c.params.rank ? 1 : 0;
-    if (ng && c.params.transitions)
-      return fail(h, SPHG_ERR_CONFIG, "phase transitions are single-rank only (ghost particles present)");
     c.nghost = ng;
     c.disp_since_partition = 0.0;
     // buffers below may be reallocated (and a freed address handed out again): no captured graph may
@@ -1687,6 +1705,98 @@ int sphg_body_bind(sphg_ctx* h, double* part, double* gath, int32_t world) {
   h->c.body_gath = gath;
   h->c.world = world;
   return SPHG_OK;
+}
+
+int sphg_event_bodies(sphg_ctx* h, uint8_t* mask, size_t nb) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (nb != c.nb) return fail(h, SPHG_ERR_CONFIG, "event_bodies: body count mismatch");
+    if (nb == 0) return SPHG_OK;
+    c.tscratch.alloc(nb);
+    SPHG_CUDA_CHECK(cudaMemsetAsync(c.tscratch.p, 0, nb * sizeof(uint32_t), c.stream));
+    event_bodies(c, c.tscratch.p);
+    std::vector<uint32_t> m(nb);
+    d2h(m.data(), c.tscratch.p, nb, c.stream);
+    host_sync(c, c.stream);
+    for (size_t k = 0; k < nb; ++k) mask[k] = (uint8_t)(mask[k] | (m[k] ? 1 : 0));
+    return SPHG_OK;
+  });
+}
+
+int sphg_event_members(sphg_ctx* h, const uint8_t* mask, size_t nb, uint32_t* ids, size_t cap, size_t* n) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (nb != c.nb) return fail(h, SPHG_ERR_CONFIG, "event_members: body count mismatch");
+    std::vector<uint32_t> m32(std::max<size_t>(nb, 1), 0u);
+    for (size_t k = 0; k < nb; ++k) m32[k] = mask[k] ? 1u : 0u;
+    c.tscratch.alloc(m32.size());
+    h2d(c.tscratch.p, m32.data(), m32.size(), c.stream);
+    c.rec_ids.alloc(std::max<size_t>(c.n, 1));
+    const size_t m = event_members(c, c.tscratch.p, nb, c.rec_ids.p);
+    *n = m;
+    if (!ids) return SPHG_OK;
+    if (cap < m) return fail(h, SPHG_ERR_CONFIG, "event_members: buffer too small");
+    d2h(ids, c.rec_ids.p, m, c.stream);
+    host_sync(c, c.stream);
+    std::sort(ids, ids + m);
+    return SPHG_OK;
+  });
+}
+
+int sphg_record_doubles(void) { return kRecordDoubles; }
+
+int sphg_record_pack(sphg_ctx* h, const uint32_t* ids, size_t m, double* recs) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    for (size_t s = 0; s < m; ++s)
+      if (ids[s] >= c.n) return fail(h, SPHG_ERR_CONFIG, "record_pack: id out of range");
+    if (m == 0) return SPHG_OK;
+    c.rec_ids.alloc(m);
+    c.rec_buf.alloc(m * kRecordDoubles);
+    h2d(c.rec_ids.p, ids, m, c.stream);
+    record_pack(c, c.rec_ids.p, m, c.rec_buf.p);
+    d2h(recs, c.rec_buf.p, m * kRecordDoubles, c.stream);
+    host_sync(c, c.stream);
+    return SPHG_OK;
+  });
+}
+
+int sphg_record_unpack(sphg_ctx* h, const uint32_t* ids, size_t m, const double* recs, int keep_position) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    for (size_t s = 0; s < m; ++s) {
+      if (ids[s] >= c.n) return fail(h, SPHG_ERR_CONFIG, "record_unpack: id out of range");
+      const double* o = recs + s * kRecordDoubles;
+      if (!(o[3] >= 0.0 && o[3] <= 2.0) || !(o[4] >= 0.0 && o[4] < c.params.n_mat))
+        return fail(h, SPHG_ERR_CONFIG, "record_unpack: invalid kind/material");
+    }
+    if (m == 0) return SPHG_OK;
+    c.rec_ids.alloc(m);
+    c.rec_buf.alloc(m * kRecordDoubles);
+    h2d(c.rec_ids.p, ids, m, c.stream);
+    h2d(c.rec_buf.p, recs, m * kRecordDoubles, c.stream);
+    record_unpack(c, c.rec_ids.p, m, c.rec_buf.p, keep_position);
+    host_sync(c, c.stream);
+    return SPHG_OK;
+  });
+}
+
+int sphg_replace_bodies(sphg_ctx* h, const sphg_body* bodies, size_t nb) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    destroy_graphs(c);
+    ensure_bodies(c, nb);
+    c.nb = nb;
+    h2d(c.bodies.p, bodies, nb, c.stream);
+    if (c.built) {  // kinds / groups changed under the rows
+      launch_rigid_index(c);
+      launch_repartition_rows(c);
+      if (c.built) launch_contact_order(c);
+      launch_ghost_split(c);
+    }
+    host_sync(c, c.stream);
+    return check_flags(h, true);
+  });
 }
 
 int sphg_set_event_log(sphg_ctx* h, int enabled) {

@@ -105,7 +105,7 @@ struct Ctx {
   DBuf<uint32_t> fidx, widx, ridx, body_start;
   DBuf<uint32_t> ncon;  // per rigid particle: contact candidates at the front of its non-fluid row part
   DBuf<uint32_t> brick_buf, scan_cells;
-  DBuf<uint8_t> dl_buf;  // download: requested store fields in gid order  // kind-list construction in brick order
+  DBuf<uint8_t> dl_buf;  // download: requested store fields in gid order
   size_t nf = 0, nw = 0, nrigid = 0;
   int group_density = 0, group_forces = 0;  // lanes per particle in the pair kernels (0 = lanes_for)
   size_t fill_groups = 37888;  // particles that fill the GPU at 4 lanes: SMs x 2048 threads / 4 / 2
@@ -114,8 +114,11 @@ struct Ctx {
   void* wall_user = nullptr;
   // transitions scratch
   DBuf<uint32_t> ev_idx, ev_flag, label, tscratch;
-  DBuf<uint32_t> label_list, label_flags;
-  DBuf<uint32_t> wrap_list;  // (index, wrap code) of the particles that crossed a periodic face this step  // compact list of labelled particles; sweep flags + count
+  DBuf<uint32_t> label_list, label_flags;  // compact list of labelled particles; sweep flags + count
+  DBuf<uint32_t> wrap_list;  // (index, wrap code) of the particles that crossed a periodic face this step
+  // decomposed transition batches (sphg_event_*, sphg_record_*): id lists and records
+  DBuf<uint32_t> rec_ids;
+  DBuf<double> rec_buf;
   // transition event log (sphg_set_event_log): device buffer of the current batch, host accumulation
   bool event_log = false;
   DBuf<sphg_event> ev_log;
@@ -278,6 +281,12 @@ void body_apply_totals(Ctx& c, const double* dev_tot);
 
 // kernels_transition.cu
 int launch_transitions(Ctx& c);  // 0 ok, else error code
+void launch_detect(Ctx& c);      // event flags (ev_flag) of the owned particles; counts in dflags
+void event_bodies(Ctx& c, uint32_t* dev_mask);  // bodies a batch can touch (sphg_event_bodies)
+size_t event_members(Ctx& c, const uint32_t* dev_mask, size_t nb, uint32_t* dev_ids);  // unsorted local ids
+constexpr int kRecordDoubles = 44;
+void record_pack(Ctx& c, const uint32_t* dev_ids, size_t m, double* dev_out);
+void record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_in, int keep_position);
 void launch_repartition_rows(Ctx& c);
 void launch_contact_order(Ctx& c);
 

@@ -32,6 +32,10 @@ __global__ void k_detect(const __grid_constant__ DevParams P, Particles D, size_
   const uint32_t kind = kind_of(kmd);
   const DevMat& M = P.mat[mat_of(kmd)];
   uint32_t e = 0;
+  if (is_ghost(kmd)) {  // decomposed runs: every rank detects over the particles it owns
+    ev[k] = 0;
+    return;
+  }
   // trigger field by TransitionMode (config.hpp:61): 1 temperature, 2 concentration [P19]
   const bool conc = P.transitions == 2;
   if (conc ? M.has_Ct : M.has_Tt) {
@@ -397,7 +401,144 @@ __global__ void __launch_bounds__(32 * kRepartWarps) k_repartition_rows(const ui
   if (lane == 0) cnt[i] = pack_cnt(nf, tot - nf);
 }
 
+// ------------------------------------------------ decomposed batches (sphg.h)
+// bodies a batch can touch: the body of a melting particle; every body with a rigid particle (ghosts
+// included) within r_c of a solidifying one — a superset of the attach targets (k_solid_target)
+__global__ void k_event_bodies(const __grid_constant__ DevParams P, Particles D, size_t n,
+                               const uint32_t* __restrict__ ev, NbrList L, uint32_t* __restrict__ mask) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || ev[i] == 0) return;
+  if (ev[i] == 1) {
+    mask[D.group.p[i]] = 1u;
+    return;
+  }
+  const double4 pi = D.G0.p[i];
+  const uint32_t nn = cnt_total(L.cnt[i]);
+  const uint32_t* row = L.nbr + (size_t)i * L.cap;
+  for (uint32_t k = 0; k < nn; ++k) {
+    const uint32_t j = entry_index(P, row[k]);
+    if (kind_of(D.kmd.p[j]) != SPHG_RIGID) continue;
+    const double4 pj = D.G0.p[j];
+    if (r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) > P.rc2) continue;
+    mask[D.group.p[j]] = 1u;
+  }
+}
+
+// owned event particles and owned rigid members of the masked bodies
+__global__ void k_event_member_flags(Particles D, size_t n, const uint32_t* __restrict__ ev,
+                                     const uint32_t* __restrict__ mask, size_t nb, uint32_t* __restrict__ flag) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t kmd = D.kmd.p[k];
+  const uint32_t g = D.group.p[k];
+  const bool member = kind_of(kmd) == SPHG_RIGID && g < nb && mask[g] != 0u;
+  flag[k] = (!is_ghost(kmd) && (ev[k] != 0u || member)) ? 1u : 0u;
+}
+
+__global__ void k_compact_gid(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                              const uint32_t* __restrict__ gid, size_t n, uint32_t* __restrict__ out) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n && flag[k]) out[pos[k]] = gid[k];
+}
+
+// records (sphg.h): [0..2] x, [3] kind, [4] material, [5] group, [6] mass, then the device records
+__global__ void k_record_pack(Particles D, const uint32_t* __restrict__ ids, size_t m,
+                              const uint32_t* __restrict__ idx, double* __restrict__ out) {
+  const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  const uint32_t k = idx[ids[s]];
+  double* o = out + s * kRecordDoubles;
+  const uint32_t kmd = D.kmd.p[k];
+  const double4 g0 = D.G0.p[k];
+  o[0] = g0.x; o[1] = g0.y; o[2] = g0.z;
+  o[3] = (double)kind_of(kmd);
+  o[4] = (double)mat_of(kmd);
+  o[5] = (double)D.group.p[k];
+  o[6] = D.V4.p[k].w;
+  o[7] = g0.w;
+  const double4* rec[7] = {&D.G1.p[k], &D.G2.p[k], &D.V4.p[k], &D.A4.p[k], &D.B4.p[k], &D.F4.p[k], &D.X4.p[k]};
+#pragma unroll
+  for (int r = 0; r < 7; ++r) {
+    const double4 v = *rec[r];
+    o[8 + 4 * r] = v.x; o[9 + 4 * r] = v.y; o[10 + 4 * r] = v.z; o[11 + 4 * r] = v.w;
+  }
+  o[36] = D.H2.p[k].x; o[37] = D.H2.p[k].y;
+  o[38] = D.dTdt.p[k];
+  o[39] = D.p_static.p[k];
+  o[40] = D.C2.p ? D.C2.p[k].x : 0.0;
+  o[41] = D.C2.p ? D.C2.p[k].y : 0.0;
+  o[42] = D.dCdt.p ? D.dCdt.p[k] : 0.0;
+  o[43] = (double)(kmd & ~kGhostBit);
+}
+
+__global__ void k_record_unpack(Particles D, const uint32_t* __restrict__ ids, size_t m,
+                                const uint32_t* __restrict__ idx, const double* __restrict__ in, int keep_position) {
+  const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  const uint32_t k = idx[ids[s]];
+  const double* o = in + s * kRecordDoubles;
+  double4 g0 = D.G0.p[k];
+  if (!keep_position) {
+    g0.x = o[0]; g0.y = o[1]; g0.z = o[2];
+  }
+  g0.w = o[7];
+  D.G0.p[k] = g0;
+  double4* rec[7] = {&D.G1.p[k], &D.G2.p[k], &D.V4.p[k], &D.A4.p[k], &D.B4.p[k], &D.F4.p[k], &D.X4.p[k]};
+#pragma unroll
+  for (int r = 0; r < 7; ++r) *rec[r] = make_double4(o[8 + 4 * r], o[9 + 4 * r], o[10 + 4 * r], o[11 + 4 * r]);
+  D.H2.p[k] = make_double2(o[36], o[37]);
+  D.dTdt.p[k] = o[38];
+  D.p_static.p[k] = o[39];
+  if (D.C2.p) D.C2.p[k] = make_double2(o[40], o[41]);
+  if (D.dCdt.p) D.dCdt.p[k] = o[42];
+  const uint32_t kmd = (uint32_t)o[43];
+  D.kmd.p[k] = (kmd & ~kGhostBit) | (D.kmd.p[k] & kGhostBit);  // the local copy keeps its role
+  D.group.p[k] = (uint32_t)o[5];
+}
+
 }  // namespace
+
+void launch_detect(Ctx& c) {
+  const size_t n = c.n;
+  cudaStream_t s = c.stream;
+  c.ev_flag.alloc(std::max<size_t>(n, 1));
+  SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->n_events, 0, sizeof(uint32_t), s));
+  SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->pad[0], 0, 2 * sizeof(uint32_t), s));
+  if (n == 0) return;
+  k_detect<<<grid_for(n, 256), 256, 0, s>>>(c.P, c.cur, n, c.ev_flag.p, c.dflags);
+  c.launches++;
+}
+
+void event_bodies(Ctx& c, uint32_t* dev_mask) {
+  if (c.n == 0 || !c.ev_flag.p) return;
+  k_event_bodies<<<grid_for(c.n, 128), 128, 0, c.stream>>>(c.P, c.cur, c.n, c.ev_flag.p, c.nl(), dev_mask);
+  c.launches++;
+}
+
+size_t event_members(Ctx& c, const uint32_t* dev_mask, size_t nb, uint32_t* dev_ids) {
+  const size_t n = c.n;
+  if (n == 0 || !c.ev_flag.p) return 0;
+  uint32_t* flag = c.vals_alt.p;
+  uint32_t* pos = c.vals.p;
+  k_event_member_flags<<<grid_for(n, 256), 256, 0, c.stream>>>(c.cur, n, c.ev_flag.p, dev_mask, nb, flag);
+  exclusive_scan_u32(flag, pos, n, c.scan_tmp.p, c.stream, &c.launches);
+  const size_t m = (size_t)read_u32(c, pos + n - 1) + read_u32(c, flag + n - 1);
+  if (dev_ids && m) k_compact_gid<<<grid_for(n, 256), 256, 0, c.stream>>>(flag, pos, c.cur.gid.p, n, dev_ids);
+  c.launches += 2;
+  return m;
+}
+
+void record_pack(Ctx& c, const uint32_t* dev_ids, size_t m, double* dev_out) {
+  if (m == 0) return;
+  k_record_pack<<<grid_for(m, 128), 128, 0, c.stream>>>(c.cur, dev_ids, m, c.idx_of_gid.p, dev_out);
+  c.launches++;
+}
+
+void record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_in, int keep_position) {
+  if (m == 0) return;
+  k_record_unpack<<<grid_for(m, 128), 128, 0, c.stream>>>(c.cur, dev_ids, m, c.idx_of_gid.p, dev_in, keep_position);
+  c.launches++;
+}
 
 void launch_repartition_rows(Ctx& c) {
   if (c.n == 0) return;
@@ -418,11 +559,7 @@ int launch_transitions(Ctx& c) {
   const size_t n = c.n;
   cudaStream_t s = c.stream;
   if (n == 0) return 0;
-  c.ev_flag.alloc(n);
-  SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->n_events, 0, sizeof(uint32_t), s));
-  SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->pad[0], 0, 2 * sizeof(uint32_t), s));
-  k_detect<<<grid_for(n, 256), 256, 0, s>>>(c.P, c.cur, n, c.ev_flag.p, c.dflags);
-  c.launches++;
+  launch_detect(c);
   const uint32_t nmelt = read_u32(c, &c.dflags->n_events);
   const uint32_t nsolid = read_u32(c, &c.dflags->pad[0]);
   if (nmelt == 0 && nsolid == 0) return 0;

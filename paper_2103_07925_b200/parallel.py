@@ -17,8 +17,17 @@ Per step (bulk-synchronous; the same stage sequence as sphg_step):
   -> FINAL_KICK.
 Halo records are packed/unpacked by the engine (device kernels for the GPU
 engine, host loops for the oracle) into tensors exchanged with point-to-point
-send/recv (NCCL on GPUs, gloo in the CPU tests).  Phase transitions are
-single-rank only (the engine refuses ghosts with transitions enabled).
+send/recv (NCCL on GPUs, gloo in the CPU tests).
+
+Phase transitions ("Event detection is worker-local; application is
+serialized per affected body at the owner, followed by a broadcast of updated
+body state and re-linking of affected particles"): each rank detects over the
+particles it owns at the end of the step; when any rank has events the engine
+returns NEED_TRANSITIONS and `_transition_batch` gathers, at rank 0, every
+particle the batch reads (the events and all members of the bodies they can
+touch), applies the batch there with the single-rank kernels in a scratch
+context, and broadcasts the updated particle records and body table, which every
+rank writes into its owned and ghost copies.
 """
 import ctypes as C
 import math
@@ -137,6 +146,9 @@ class DistributedSimulation:
         # in-library decomposed step (sphg_set_exchange): the engine runs the whole step on its stream
         # and calls back for the transfers; False = the stage-by-stage driver below
         self.fused = fused
+        self.event_log = False
+        self.events = []      # transition event log, global gids; filled on rank 0
+        self.batches = 0      # decomposed transition batches applied
         self._cb = None
         self._ext = None
         self._xerr = None
@@ -397,6 +409,9 @@ class DistributedSimulation:
                 if rc == abi.NEED_PARTITION:
                     self.repartition()
                     continue
+                if rc == abi.NEED_TRANSITIONS:  # the step completed; its transition batch is applied here
+                    self._transition_batch()
+                    continue
                 if rc != 0:
                     if self._xerr is not None:
                         raise RuntimeError(f"exchange failed: {self._xerr!r}") from self._xerr
@@ -405,6 +420,9 @@ class DistributedSimulation:
             r1 = e.counters()[1]
             self.rebuilds += r1 - r0
             return
+        if self.params.transitions:
+            raise RuntimeError("phase transitions under decomposition need the in-library decomposed step "
+                               "(fused=True)")
         thermal = bool(self.params.thermal) or bool(self.params.diffusion)  # one stage for T and C
         for _ in range(nsteps):
             e.run_stage(abi.STAGE_KICK_DRIFT)
@@ -421,6 +439,87 @@ class DistributedSimulation:
             self._evaluate(thermal)
             e.run_stage(abi.STAGE_FINAL_KICK)
             self.steps += 1
+
+    # ------------------------------------------------------------ transitions
+    def _single_rank_params(self):
+        p = type(self.params)()
+        C.memmove(C.byref(p), C.byref(self.params), C.sizeof(p))
+        p.rank, p.nranks = 0, 1
+        return p
+
+    def _apply_batch(self, gids, recs, bodies):
+        """Rank 0: the batch on a scratch single-rank context holding exactly the gathered particles
+        (global gid order, so every gid-ordered rule — spawn ids, attach ties, split ids — and every
+        body-major sum runs as in the single-rank run).  Returns (records, bodies, events)."""
+        m = len(gids)
+        st = ParticleStore(m)
+        st.pos[:] = recs[:, 0:3]
+        st.kind[:] = recs[:, 3].astype(np.uint8)
+        st.material[:] = recs[:, 4].astype(np.uint16)
+        st.group[:] = recs[:, 5].astype(np.uint32)
+        st.mass[:] = recs[:, 6]
+        st.density[:] = [self.params.mat[int(k)].rho0 for k in st.material]
+        eng = self.make_engine(self._single_rank_params())
+        try:
+            if self.event_log:
+                eng.set_event_log(True)
+            eng.upload(st, bodies)
+            ids = np.arange(m, dtype=np.uint32)
+            eng.record_unpack(ids, recs, keep_position=False)
+            eng.run_stage(abi.STAGE_TRANSITIONS)
+            out = eng.record_pack(ids)
+            _, nbodies = eng.download(ParticleStore(m), fields=())
+            ev = eng.transition_events() if self.event_log else None
+        finally:
+            eng.close()
+        if ev is not None and len(ev):
+            ev["gid"] = gids[ev["gid"]].astype(ev["gid"].dtype)  # scratch ids -> global gids
+            ev["step"] = self.engine.counters()[0]
+        return out, nbodies, ev
+
+    def _transition_batch(self):
+        """apply the transition batch the last decomposed step detected (see the module doc)."""
+        e = self.engine
+        nb = e.num_bodies()
+        _, bodies = e.download(ParticleStore(e.n), fields=())
+        mask = e.event_bodies(np.zeros(nb, np.uint8))
+        t = torch.from_numpy(mask.astype(np.int32)).to(self.dev)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        mask = t.cpu().numpy().astype(np.uint8)
+        ids = e.event_members(mask)
+        mine = (self.gids[ids].astype(np.int64), e.record_pack(ids))
+        allp = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(allp, mine, group=self.group)
+        else:
+            allp = [mine]
+        if self.rank == 0:
+            gids = np.concatenate([a[0] for a in allp])
+            recs = np.concatenate([a[1] for a in allp])
+            order = np.argsort(gids, kind="stable")
+            gids, recs = gids[order], recs[order]
+            out, nbodies, ev = self._apply_batch(gids, recs, bodies)
+            res = [(gids, out, nbodies)]
+            if ev is not None:
+                self.events.extend(ev.tolist())
+        else:
+            res = [None]
+        if self.world > 1:
+            dist.broadcast_object_list(res, src=0, group=self.group)
+        gids, out, nbodies = res[0]
+        # every listed particle present here, owned or ghost: local ids through the sorted gid map
+        order = np.argsort(self.gids, kind="stable")
+        pos = np.searchsorted(self.gids[order], gids)
+        pos = np.minimum(pos, len(order) - 1)
+        here = self.gids[order][pos] == gids
+        local = order[pos[here]].astype(np.uint32)
+        e.record_unpack(local, out[here], keep_position=True)
+        e.replace_bodies(nbodies)
+        if len(nbodies) != self._nb and self._fused_ok():
+            self._bind_fused()  # body buffers are sized by the body count
+        self._bodies()  # reduce_force_torque of the new membership (the single-rank batch ends with it)
+        self.batches += 1
 
     # ------------------------------------------------------------ global views
     def gather(self):

@@ -261,6 +261,47 @@ class Simulation:
         assert dt.itemsize == C.sizeof(abi.Event)
         return np.frombuffer(bytes(buf), dt, count=n.value).copy()
 
+    # ------------------------------------------------ decomposed transition batches (sphg.h)
+    def event_bodies(self, mask):
+        """OR into `mask` (uint8, one per body) the bodies this rank's detected events can touch."""
+        assert mask.dtype == np.uint8 and mask.flags.c_contiguous
+        self._check(self._fn("event_bodies")(self._h, mask.ctypes.data_as(C.POINTER(C.c_uint8)), len(mask)),
+                    "event_bodies")
+        return mask
+
+    def event_members(self, mask):
+        """Local ids (ascending) of the owned event particles and owned members of the masked bodies."""
+        mask = np.ascontiguousarray(mask, np.uint8)
+        mp = mask.ctypes.data_as(C.POINTER(C.c_uint8))
+        n = C.c_size_t(0)
+        self._check(self._fn("event_members")(self._h, mp, len(mask), None, 0, C.byref(n)), "event_members")
+        ids = np.zeros(max(n.value, 1), np.uint32)
+        self._check(self._fn("event_members")(self._h, mp, len(mask), ids.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                              len(ids), C.byref(n)), "event_members")
+        return ids[: n.value]
+
+    def record_doubles(self):
+        return int(self._fn("record_doubles")())
+
+    def record_pack(self, ids):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        recs = np.zeros((len(ids), self.record_doubles()))
+        self._check(self._fn("record_pack")(self._h, ids.ctypes.data_as(C.POINTER(C.c_uint32)), len(ids),
+                                            recs.ctypes.data_as(C.POINTER(C.c_double))), "record_pack")
+        return recs
+
+    def record_unpack(self, ids, recs, keep_position=True):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        recs = np.ascontiguousarray(recs, np.float64)
+        assert recs.shape == (len(ids), self.record_doubles())
+        self._check(self._fn("record_unpack")(self._h, ids.ctypes.data_as(C.POINTER(C.c_uint32)), len(ids),
+                                              recs.ctypes.data_as(C.POINTER(C.c_double)), int(bool(keep_position))),
+                    "record_unpack")
+
+    def replace_bodies(self, bodies):
+        bodies = np.ascontiguousarray(bodies, BODY_DTYPE)
+        self._check(self._fn("replace_bodies")(self._h, bodies_ptr(bodies), len(bodies)), "replace_bodies")
+
     def counters(self):
         """Cheap host counters: (steps, rebuilds, host_syncs, kernel_launches)."""
         out = (C.c_int64 * 4)()

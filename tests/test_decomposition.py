@@ -67,6 +67,7 @@ def _worker(rank, world, port, case, out):
     from paper_2103_07925_b200.parallel import DistributedSimulation
     sc = _case(case)
     ds = DistributedSimulation(sc.params, lambda p: Oracle(p), tensor_device="cpu", margin_h=0.3)
+    ds.event_log = True
     ds.distribute(sc.store, sc.bodies)
     ds.initialize()
     ds.step(NSTEPS[case])
@@ -90,12 +91,16 @@ def _worker(rank, world, port, case, out):
     if rank == 0:
         np.savez(out, pos=g.pos, vel=g.vel, acc=g.acc, acc_bg=g.acc_bg, density=g.density, pressure=g.pressure,
                  force=g.force, T=g.temperature, dT=g.dT_dt, kind=g.kind, C=g.concentration,
+                 group=g.group, material=g.material, chi=g.body_frame_pos,
                  bforce=b["force"], btorque=b["torque"], binertia=b["inertia"], bvel=b["vel"], bcom=b["com"],
-                 rebuilds=ds.rebuilds, repart=ds.repartitions)
+                 bmass=b["mass"], balive=b["alive"], bomega=b["omega"],
+                 rebuilds=ds.rebuilds, repart=ds.repartitions, batches=ds.batches,
+                 events=np.array([tuple(e) for e in ds.events], np.int64).reshape(-1, 5))
     dist.destroy_process_group()
 
 
-NSTEPS = {"c1": 6, "c2": 6, "c1fast": 16, "c3": 6, "diff": 6, "bigbody": 0, "c1wrap": 6}
+NSTEPS = {"c1": 6, "c2": 6, "c1fast": 16, "c3": 6, "diff": 6, "bigbody": 0, "c1wrap": 6, "c2melt": 6,
+          "dissolve": 6}
 
 
 def crossing_case():
@@ -129,21 +134,26 @@ def _case(case):
         sc = scenarios.dissolving_bodies(nside=16, n_bodies=2, r_range=(2.0, 3.0), seed=13)
         sc.params.transitions = 0
         return sc
+    if case == "c2melt":  # transitions under decomposition (flags flip at step 1, App. B5)
+        return scenarios.config2(nside=16, n_grid=2, r_range=(2.0, 3.0), seed=5, melt_forcing=True)
+    if case == "dissolve":  # concentration-mode transitions (bodies dissolve into the bath from step 1)
+        return scenarios.dissolving_bodies(nside=16, n_bodies=3, r_range=(2.0, 3.0), seed=13, forcing=True)
     if case == "c3":  # two phases, cubes and spheres
         return scenarios.config3(nside=20, n_bodies=4, r_range=(2.0, 3.0), seed=7)
     sc = scenarios.config2(nside=16, n_grid=2, r_range=(2.0, 3.0), seed=5)
-    sc.params.transitions = 0  # transitions are single-rank only
+    sc.params.transitions = 0  # the heat path alone (c2melt adds the transitions)
     return sc
 
 
 @pytest.mark.parametrize("case,world", [("c1", 2), ("c2", 2), ("c1fast", 2), ("c3", 2), ("diff", 2), ("c1", 4),
-                                        ("c1wrap", 2)])
+                                        ("c1wrap", 2), ("c2melt", 2), ("c2melt", 4), ("dissolve", 2)])
 def test_ranks_match_one_rank(case, world, tmp_path, oracle_mod):
     out = str(tmp_path / "ds.npz")
     mp.spawn(_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
     d = np.load(out)
     sc = _case(case)
     o = oracle_mod.Oracle(sc.params)
+    o.set_event_log(True)
     o.upload(sc.store, sc.bodies)
     o.initialize()
     o.step(NSTEPS[case])
@@ -152,6 +162,17 @@ def test_ranks_match_one_rank(case, world, tmp_path, oracle_mod):
     fl = g.kind == abi.FLUID
     rg = g.kind == abi.RIGID
     from tests.helpers import vec_err
+    if sc.params.transitions:
+        # SPEC:500 under decomposition: flags, materials, body ids, the body table's liveness, the event log
+        # and the body masses (summed over the same members in the same gid order) bit-exact against the
+        # single rank; COMs are integrated from forces summed in rank order (multistep bar)
+        ev1 = o.transition_events()
+        assert len(ev1) > 0 and int(d["batches"]) >= 1
+        assert np.array_equal(d["events"], np.array([tuple(e) for e in ev1.tolist()], np.int64).reshape(-1, 5))
+        assert np.array_equal(d["group"][rg], g.group[rg]) and np.array_equal(d["material"], g.material)
+        assert np.array_equal(d["balive"], b["alive"]) and len(d["bmass"]) == len(b)
+        assert np.array_equal(d["bmass"], b["mass"])
+        assert vec_err(d["bcom"], b["com"], float(sc.params.hi[0] - sc.params.lo[0]), 1e-12) <= 1
     if case == "c1fast":
         # the displacement-triggered rebuilds are the single rank's; a repartition between steps adds at
         # most one (the re-uploaded store is binned afresh on the next step)

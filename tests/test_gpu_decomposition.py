@@ -23,6 +23,7 @@ def _gpu_worker(rank, world, port, case, out, nsteps=None):
     sc = _case(case)
     ds = DistributedSimulation(sc.params, lambda p: Simulation(p, device=0), tensor_device="cpu",
                                engine_device="cuda:0", margin_h=0.3)
+    ds.event_log = True
     ds.distribute(sc.store, sc.bodies)
     ds.initialize()
     k = NSTEPS[case] if nsteps is None else nsteps
@@ -36,7 +37,9 @@ def _gpu_worker(rank, world, port, case, out, nsteps=None):
         np.savez(out, pos=g.pos, acc=g.acc, density=g.density, force=g.force, T=g.temperature,
                  bforce=b["force"], btorque=b["torque"], binertia=b["inertia"], rebuilds=ds.rebuilds,
                  repart=ds.repartitions, syncs=c1[2] - c0[2], steps=k - 1,
-                 rebuilds_late=ds.rebuilds - r0)
+                 rebuilds_late=ds.rebuilds - r0, kind=g.kind, group=g.group, material=g.material,
+                 bmass=b["mass"], balive=b["alive"], batches=ds.batches,
+                 events=np.array([tuple(e) for e in ds.events], np.int64).reshape(-1, 5))
     dist.destroy_process_group()
 
 
@@ -102,6 +105,42 @@ def test_gpu_two_ranks_match_single_rank(case, tmp_path):
     assert vec_err(d["force"][rg], g.force[rg], s["force"][rg], 1e-8) <= 1
     al = b["alive"] == 1
     assert vec_err(d["bforce"][al], b["force"][al], s["body_force"][al], 1e-8) <= 1
+
+
+@pytest.mark.parametrize("case", ["c2melt", "dissolve"])
+def test_gpu_two_ranks_transitions(case, tmp_path):
+    """SPEC:500 on the device engine: 2 decomposed GPU ranks (transition batch applied at rank 0 in a
+    scratch single-rank context, records broadcast) against the single-rank GPU run: flags, materials, body
+    ids, liveness, body masses and the event log bit-exact; fields at the multistep bar."""
+    from paper_2103_07925_b200 import Simulation, abi
+    from oracle.oracle import Oracle
+    from tests.helpers import vec_err
+    out = str(tmp_path / "gt.npz")
+    mp.spawn(_gpu_worker, args=(2, _free_port(), case, out), nprocs=2, join=True)
+    d = np.load(out)
+    sc = _case(case)
+    sim = Simulation(sc.params)
+    sim.set_event_log(True)
+    sim.upload(sc.store, sc.bodies)
+    sim.initialize()
+    sim.step(NSTEPS[case])
+    g, b = sim.download()
+    ev = sim.transition_events()
+    assert len(ev) > 0 and int(d["batches"]) >= 1
+    assert np.array_equal(d["events"], np.array([tuple(e) for e in ev.tolist()], np.int64).reshape(-1, 5))
+    assert np.array_equal(d["kind"], g.kind) and np.array_equal(d["material"], g.material)
+    rg = g.kind == abi.RIGID
+    assert np.array_equal(d["group"][rg], g.group[rg])
+    assert np.array_equal(d["balive"], b["alive"]) and np.array_equal(d["bmass"], b["mass"])
+    o = Oracle(sc.params)
+    o.upload(sc.store, sc.bodies)
+    o.initialize()
+    o.step(NSTEPS[case])
+    s = o.scales()
+    fl = g.kind == abi.FLUID
+    assert vec_err(d["density"][fl], g.density[fl], 0.0, 1e-10) <= 1
+    assert vec_err(d["acc"][fl], g.acc[fl], s["acc"][fl], 1e-7) <= 1
+    assert vec_err(d["T"], g.temperature, 0.0, 1e-12) <= 1
 
 
 def test_body_partials_device_pointers():
