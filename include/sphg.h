@@ -353,6 +353,10 @@ int sphg_body_partials(sphg_ctx* ctx, double* out);
 int sphg_body_apply_totals(sphg_ctx* ctx, const double* totals);
 /* Max displacement since the last rebuild over owned particles (after a KICK_DRIFT stage). */
 int sphg_max_displacement(sphg_ctx* ctx, double* out);
+/* Cell-occupancy histogram of the last Verlet rebuild ("diagnostic dump of cell occupancy histogram
+ * as CSV"): hist[k] = number of cells holding k particles (owned and ghost), the last bin counting every
+ * cell with >= nbins - 1; *max_count (may be NULL) = the fullest cell's count. */
+int sphg_cell_occupancy(sphg_ctx* ctx, int64_t* hist, size_t nbins, int64_t* max_count);
 /* Phase transitions under decomposition ("Event detection is worker-local; application is
  * serialized per affected body at the owner, followed by a broadcast of updated body state and re-linking
  * of affected particles").  With transitions on, a decomposed step ends with detection over the owned

@@ -1504,6 +1504,23 @@ int orc_get_cells(orc_ctx* h, int64_t* cell_of_gid, uint32_t* sorted_gid) {
     return SPHG_OK;
 }
 
+int orc_cell_occupancy(orc_ctx* h, int64_t* hist, size_t nbins, int64_t* max_count) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (nbins == 0) return SPHG_ERR_CONFIG;
+    if (!c.built && !stage_rebuild(c)) return SPHG_ERR_RUNTIME;
+    const int64_t ncells = (int64_t)c.ncell[0] * c.ncell[1] * c.ncell[2];
+    std::vector<int64_t> cnt(ncells, 0);
+    for (int64_t k : c.cell_of) cnt[k]++;
+    std::fill(hist, hist + nbins, 0);
+    int64_t mx = 0;
+    for (int64_t m : cnt) {
+        hist[std::min<int64_t>(m, (int64_t)nbins - 1)]++;
+        mx = std::max(mx, m);
+    }
+    if (max_count) *max_count = mx;
+    return SPHG_OK;
+}
+
 int orc_get_nlist(orc_ctx* h, int64_t* offsets, uint32_t* nbr) {
     Ctx& c = *reinterpret_cast<Ctx*>(h);
     if (!c.built && !stage_rebuild(c)) return SPHG_ERR_RUNTIME;

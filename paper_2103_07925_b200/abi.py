@@ -188,6 +188,7 @@ def declare(lib, prefix):
         "set_partition_limit": (C.c_int, [vp, C.c_double]),
         "counters": (C.c_int, [vp, C.POINTER(C.c_int64)]),
         "transition_events": (C.c_int, [vp, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t)]),
+        "cell_occupancy": (C.c_int, [vp, C.POINTER(C.c_int64), C.c_size_t, C.POINTER(C.c_int64)]),
         "event_bodies": (C.c_int, [vp, C.POINTER(C.c_uint8), C.c_size_t]),
         "event_members": (C.c_int, [vp, C.POINTER(C.c_uint8), C.c_size_t, C.POINTER(C.c_uint32), C.c_size_t,
                                     C.POINTER(C.c_size_t)]),

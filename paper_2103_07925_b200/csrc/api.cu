@@ -1424,6 +1424,32 @@ int sphg_get_cells(sphg_ctx* h, int64_t* cell_of_gid, uint32_t* sorted_gid) {
   });
 }
 
+int sphg_cell_occupancy(sphg_ctx* h, int64_t* hist, size_t nbins, int64_t* max_count) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    if (nbins == 0 || nbins > (1u << 20)) return fail(h, SPHG_ERR_CONFIG, "cell_occupancy: 1 <= nbins <= 2^20");
+    if (!c.built) {
+      const int rc = do_stage(h, SPHG_STAGE_REBUILD);
+      if (rc) return rc;
+    }
+    DBuf<unsigned long long> d;
+    d.alloc(nbins + 1);
+    SPHG_CUDA_CHECK(cudaMemsetAsync(d.p, 0, (nbins + 1) * sizeof(unsigned long long), c.stream));
+    uint32_t* dmax = reinterpret_cast<uint32_t*>(d.p + nbins);
+    cell_occupancy(c, d.p, (uint32_t)nbins, dmax);
+    std::vector<unsigned long long> out(nbins + 1);
+    d2h(out.data(), d.p, nbins + 1, c.stream);
+    host_sync(c, c.stream);
+    for (size_t k = 0; k < nbins; ++k) hist[k] = (int64_t)out[k];
+    if (max_count) {
+      uint32_t mx;
+      std::memcpy(&mx, &out[nbins], sizeof mx);
+      *max_count = mx;
+    }
+    return SPHG_OK;
+  });
+}
+
 int sphg_get_nlist(sphg_ctx* h, int64_t* offsets, uint32_t* nbr_gid) {
   return guarded(h, [&]() -> int {
     Ctx& c = h->c;

@@ -270,6 +270,7 @@ bool displacement_exceeds(Ctx& c);   // max |r - r_ref| > half skin (syncs)
 void iota_gid(Ctx& c);
 void scatter_state(Ctx& c, const double* pos, const double* vel);  // gid-ordered xyz -> G0.xyz / V4.xyz
 void count_pairs(Ctx& c, int64_t out[4]);
+void cell_occupancy(Ctx& c, unsigned long long* dev_hist, uint32_t nbins, uint32_t* dev_max);
 void shepard_grid(Ctx& c, const double origin[3], const double spacing[3], const int32_t dims[3], int field,
                   uint32_t kind_mask, double* dev_out, uint8_t* dev_support);
 void build_idx_of_gid(Ctx& c);

@@ -117,4 +117,23 @@ void shepard_grid(Ctx& c, const double origin[3], const double spacing[3], const
   c.launches++;
 }
 
+namespace {
+// SPEC:218 occupancy histogram: one thread per cell of the last rebuild's ranges
+__global__ void k_cell_occupancy(const uint32_t* __restrict__ start, const uint32_t* __restrict__ end, int64_t ncells,
+                                 unsigned long long* __restrict__ hist, uint32_t nbins, uint32_t* __restrict__ maxc) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= ncells) return;
+  const uint32_t m = end[k] > start[k] ? end[k] - start[k] : 0u;
+  atomicAdd(&hist[m < nbins - 1 ? m : nbins - 1], 1ull);
+  atomicMax(maxc, m);
+}
+}  // namespace
+
+void cell_occupancy(Ctx& c, unsigned long long* dev_hist, uint32_t nbins, uint32_t* dev_max) {
+  if (c.ncells == 0 || nbins == 0) return;
+  k_cell_occupancy<<<(unsigned)((c.ncells + 255) / 256), 256, 0, c.stream>>>(c.cell_start.p, c.cell_end.p, c.ncells,
+                                                                           dev_hist, nbins, dev_max);
+  c.launches++;
+}
+
 }  // namespace sphg

@@ -165,6 +165,7 @@ class OutputPlan:
     grid: GridSpec = None
     prefix: str = "sph"
     event_log: bool = False  # transition event log CSV: step,particle,direction,body_from,body_to
+    occupancy: bool = False  # cell-occupancy histogram CSV at every snapshot point
 
 
 def _wants(plan, step, traj):
@@ -173,10 +174,21 @@ def _wants(plan, step, traj):
     return snap, tr, (SNAPSHOT_FIELDS if snap else ("kind",)) if (snap or tr) else None
 
 
-def _write_outputs(sim, plan, step, traj, store, downloaded=None):
+def write_occupancy(fh, step, hist, max_count):
+    """SPEC:218 diagnostic dump: rows (step, particles per cell, cells); the last bin is 'or more'."""
+    last = len(hist) - 1
+    for k, m in enumerate(hist):
+        if m:
+            fh.write("%d,%s%d,%d\n" % (step, ">=" if k == last else "", k, m))
+    fh.write("%d,max,%d\n" % (step, max_count))
+
+
+def _write_outputs(sim, plan, step, traj, store, downloaded=None, occ=None):
     st = sim.stats()
     t = st.time
     snap, tr, fields = _wants(plan, step, traj)
+    if occ is not None and snap:
+        write_occupancy(occ, step, *sim.cell_occupancy())
     gr = plan.grid is not None and plan.grid_interval and step % plan.grid_interval == 0
     if snap or tr:
         if downloaded is not None:
@@ -209,13 +221,17 @@ def run(sim, nsteps, plan, log=None):
         sim.set_event_log(True)
         events = open(os.path.join(plan.out_dir, plan.prefix + "_transitions.csv"), "w", newline="\n")
         events.write("step,particle,direction,body_from,body_to\n")
+    occ = None
+    if plan.occupancy:
+        occ = open(os.path.join(plan.out_dir, plan.prefix + "_occupancy.csv"), "w", newline="\n")
+        occ.write("step,particles_per_cell,cells\n")
     traj = TrajectoryWriter(os.path.join(plan.out_dir, plan.prefix + "_bodies.csv")) if plan.trajectory_interval else None
     intervals = [i for i in (plan.snapshot_interval, plan.trajectory_interval,
                              plan.grid_interval if plan.grid is not None else 0) if i]
     store = ParticleStore(sim.n)
     step = 0
     try:
-        store = _write_outputs(sim, plan, 0, traj, store)
+        store = _write_outputs(sim, plan, 0, traj, store, occ=occ)
         while step < nsteps:
             nxt = min([nsteps] + [(step // i + 1) * i for i in intervals])
             fields = _wants(plan, nxt, traj)[2]
@@ -225,7 +241,7 @@ def run(sim, nsteps, plan, log=None):
                 sim.step(nxt - step)
                 got = None
             step = nxt
-            store = _write_outputs(sim, plan, step, traj, store, got)
+            store = _write_outputs(sim, plan, step, traj, store, got, occ=occ)
             if events is not None:
                 _write_events(events, sim.transition_events())
             if log:
@@ -237,6 +253,8 @@ def run(sim, nsteps, plan, log=None):
     finally:
         if events is not None:
             events.close()
+        if occ is not None:
+            occ.close()
     return 0, "ok"
 
 

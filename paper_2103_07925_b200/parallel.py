@@ -440,6 +440,19 @@ class DistributedSimulation:
             e.run_stage(abi.STAGE_FINAL_KICK)
             self.steps += 1
 
+    def imbalance(self):
+        """SPEC:222 (static blocks; imbalance is only reported): owned particles per rank and
+        max / mean - 1."""
+        t = torch.tensor([float(self.n_own)], dtype=torch.float64, device=self.dev)
+        allc = [torch.zeros_like(t) for _ in range(self.world)]
+        if self.world > 1:
+            dist.all_gather(allc, t, group=self.group)
+        else:
+            allc = [t]
+        counts = [int(x.item()) for x in allc]
+        mean = sum(counts) / len(counts)
+        return counts, (max(counts) / mean - 1.0) if mean > 0 else 0.0
+
     # ------------------------------------------------------------ transitions
     def _single_rank_params(self):
         p = type(self.params)()
@@ -758,6 +771,7 @@ def bench_multi(args, clock_factory=None):
                "path": "per rank: upload_state(pos, vel of owned + ghost particles from pinned host) -> "
                        "DistributedSimulation.step(1) -> download(pos, vel, density, pressure into pinned host); "
                        "host wall clock, max over ranks"}
+    counts, imb = ds.imbalance()
     n = n_total
     if rank == 0:
         weak = getattr(args, "scaling", "strong") == "weak"
@@ -769,7 +783,8 @@ def bench_multi(args, clock_factory=None):
                 "config": {"workload": f"C5 {round(n ** (1 / 3))}^3 periodic, {info['n_bodies']} spheres"
                                        + (" (8M per GPU)" if weak else ""),
                            "particles": n, "parallelism": f"domain decomposition {ds.grid.dims}, {backend} halo",
-                           "ghost_width_h": ds.width / ds.h},
+                           "ghost_width_h": ds.width / ds.h, "owned_per_rank": counts,
+                           "imbalance": imb},
                 "timing": "CUDA events on each rank's stream between barriers + cuda synchronize, "
                           "max over ranks (the per-rank step mixes kernels and NCCL exchanges)",
                 "comm_s_rank0": ds.comm_s, "rebuilds": ds.rebuilds, "repartitions": ds.repartitions,

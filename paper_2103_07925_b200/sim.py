@@ -261,6 +261,15 @@ class Simulation:
         assert dt.itemsize == C.sizeof(abi.Event)
         return np.frombuffer(bytes(buf), dt, count=n.value).copy()
 
+    def cell_occupancy(self, nbins=1024):
+        """SPEC:218 cell-occupancy histogram of the last rebuild: (hist[k] = cells holding k particles, the
+        last bin >= nbins - 1; the fullest cell's count)."""
+        hist = np.zeros(nbins, np.int64)
+        mx = C.c_int64(0)
+        self._check(self._fn("cell_occupancy")(self._h, hist.ctypes.data_as(C.POINTER(C.c_int64)), nbins,
+                                               C.byref(mx)), "cell_occupancy")
+        return hist, mx.value
+
     # ------------------------------------------------ decomposed transition batches (sphg.h)
     def event_bodies(self, mask):
         """OR into `mask` (uint8, one per body) the bodies this rank's detected events can touch."""

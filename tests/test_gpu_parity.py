@@ -511,6 +511,17 @@ def test_minimum_image_entry_mode(Oracle):
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 
 
+def test_cell_occupancy_matches_oracle(Oracle):  # SPEC:218 histogram from the device cell ranges
+    sc = CASES["c2_small"]()
+    sim, orc = Simulation(sc.params), Oracle(sc.params)
+    for e in (sim, orc):
+        e.upload(sc.store, sc.bodies)
+        e.initialize()
+    hg, mg = sim.cell_occupancy(nbins=48)
+    ho, mo = orc.cell_occupancy(nbins=48)
+    assert np.array_equal(hg, ho) and mg == mo and hg.sum() > 0
+
+
 def test_count_pairs(Oracle):
     """sphg_count_pairs (the bench's flop model input) against the oracle's lists and positions."""
     sc = CASES["c2_small"]()

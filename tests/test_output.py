@@ -181,3 +181,22 @@ def test_transition_event_log_device_matches_oracle():
         e.step(3)
         out.append(e.transition_events())
     assert len(out[0]) > 0 and np.array_equal(out[0], out[1])
+
+
+def test_cell_occupancy_histogram_csv(tmp_path, oracle_mod):  # SPEC:218 diagnostic dump
+    sc = scenarios.config1(nside=12, n_spheres=1, r_range=(2.0, 2.0), seed=3)
+    sim = oracle_mod.Oracle(sc.params)
+    sim.upload(sc.store, sc.bodies)
+    sim.initialize()
+    hist, mx = sim.cell_occupancy(nbins=256)
+    assert hist.sum() == np.prod([int(sc.params.hi[a] / (3.1 * sc.params.dx)) for a in range(3)])
+    assert (np.arange(256) * hist).sum() == sc.store.n and hist[mx] > 0 and hist[mx + 1:].sum() == 0
+    plan = OutputPlan(out_dir=str(tmp_path), snapshot_interval=2, occupancy=True)
+    assert run(sim, 2, plan)[0] == 0
+    rows = open(tmp_path / "sph_occupancy.csv").read().splitlines()
+    assert rows[0] == "step,particles_per_cell,cells"
+    steps = {r.split(",")[0] for r in rows[1:]}
+    assert steps == {"0", "2"}
+    tot = sum(int(r.split(",")[1]) * int(r.split(",")[2]) for r in rows[1:]
+              if r.startswith("2,") and r.split(",")[1] not in ("max",) and not r.split(",")[1].startswith(">="))
+    assert tot == sc.store.n
