@@ -299,7 +299,15 @@ void reset_step_flags(Ctx& c) {
   SPHG_CUDA_CHECK(cudaMemsetAsync(c.dflags, 0, 2 * sizeof(unsigned long long), c.stream));
 }
 
+const char* stage_name(int stage) {
+  static const char* names[16] = {"rebuild", "density", "heat", "extrapolate", "forces", "bodies", "kick_drift",
+                                  "final_kick", "transitions", "mass", "forces_fluid", "forces_rigid",
+                                  "", "", "", ""};
+  return stage >= 0 && stage < 16 ? names[stage] : "stage";
+}
+
 void timed(Ctx& c, int stage, void (*fn)(Ctx&)) {
+  NvtxRange nv(stage_name(stage));
   if (!c.timing) {
     fn(c);
     return;
@@ -585,6 +593,8 @@ int check_dt(sphg_ctx* h) {
 // decision.
 int exchange(sphg_ctx* h, int phase) {
   Ctx& c = h->c;
+  static const char* names[5] = {"halo_state", "halo_density", "halo_wall", "xchg_max", "xchg_bodies"};
+  NvtxRange nv(phase >= 0 && phase < 5 ? names[phase] : "exchange");
   const int rc = c.exch_fn(phase, reinterpret_cast<void*>(c.stream), c.exch_user);
   if (rc) return fail(h, SPHG_ERR_CUDA, "exchange callback failed in phase " + std::to_string(phase));
   return SPHG_OK;
@@ -1278,6 +1288,7 @@ namespace {
 // kick.  Same values as sphg_step followed by sphg_download.
 int run_steps(sphg_ctx* h, int nsteps, sphg_soa* out) {
   Ctx& c = h->c;
+  NvtxRange nv(out ? "sphg_step_download" : "sphg_step");
   if (!c.have_state) return fail(h, SPHG_ERR_RUNTIME, "no particle state uploaded");
   if (out && out->n != c.n) return fail(h, SPHG_ERR_RUNTIME, "download: store size mismatch");
   SPHG_CUDA_CHECK(cudaSetDevice(c.device));

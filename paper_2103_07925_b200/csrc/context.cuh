@@ -20,6 +20,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 
 namespace sphg {
@@ -225,6 +227,15 @@ inline void host_sync_event(Ctx& c, cudaEvent_t e) {
   SPHG_CUDA_CHECK(cudaEventSynchronize(e));
   c.host_syncs++;
 }
+
+// NVTX ranges (SURVEY §5 tracing): stages, exchanges and API calls show up by name under nsys / ncu
+// --nvtx; header-only NVTX3, a no-op without an attached tool
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ------------------------------------------------------------ launchers
 // radix_sort.cu

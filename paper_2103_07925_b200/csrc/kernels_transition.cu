@@ -556,6 +556,7 @@ void launch_repartition_rows(Ctx& c) {
 }
 
 int launch_transitions(Ctx& c) {
+  NvtxRange nv("transitions");
   const size_t n = c.n;
   cudaStream_t s = c.stream;
   if (n == 0) return 0;
