@@ -281,7 +281,12 @@ def run_sph(args):
     if world > 1:
         from paper_2103_07925_b200 import parallel
         line = parallel.bench_multi(args, clock_factory=ClockSampler)
-        if line is not None:
+        if line is not None:  # rank 0 (the process group is gone; the other ranks have finished)
+            k0 = line["kernel_per_rank"][0]
+            line["roofline"] = make_roofline(k0["forces_fluid_ms"], k0["pairs_fluid_i"], k0["fluid_owned"], None)
+            line["roofline"]["scope"] = "rank 0's k_forces_fluid (its owned fluid particles), stage-timed pass"
+            if not args.no_cpu_baseline:
+                line["cpu_baseline"] = cpu_baseline(args.cpu_nside, args.spheres, args.nside)
             print(json.dumps(line))
         return
     torch.cuda.set_device(local)
@@ -322,13 +327,39 @@ def run_sph(args):
     rebuild_ms = (sc1.stage_ms[abi.STAGE_REBUILD] - sc0.stage_ms[abi.STAGE_REBUILD]) / 2
     launches = (st1.kernel_launches - st0.kernel_launches)
     value = n / (ms_step * 1e-3)
-    peaks = load_peaks()
     info = sc.info
     nf = info["n_fluid"]
     # dominant kernel: k_forces_fluid (stage 10), average launch duration from CUDA events on
     # the library stream over the breakdown pass; algorithmic flops = 91 per interacting pair
     # with a fluid i; algorithmic bytes = 156 B per fluid particle (CSM model).
-    t_ff = stage_ms["forces_fluid"] * 1e-3
+    roofline = make_roofline(stage_ms["forces_fluid"], inter_fluid, nf, n)
+    fp64 = {"pairs_candidate": cand, "pairs_interacting": inter, "pairs_fluid_i": inter_fluid,
+            "pairs_nonfluid_i": inter_other,
+            "step_tflops": (FLOPS_PER_PAIR_FORCES * inter_fluid + FLOPS_PER_PAIR_DENSITY * inter_fluid)
+                           / (ms_step * 1e-3) / 1e12}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64 lattice + jitter)",
+            "config": dict(workload_config(args, info, n), parallelism="1 GPU",
+                           fluid_rigid_rate=(nf + info["n_rigid"]) / (ms_step * 1e-3),
+                           l2="inputs larger than L2 (state ~%.1f GB)" % (store_bytes(sc.store) / 1e9)),
+            "roofline": roofline, "fp64": fp64, "stage_ms": stage_ms, "rebuild_ms": rebuild_ms,
+            "step_roofline": {"bytes_per_particle": STEP_BYTES_PER_PARTICLE,
+                              "achieved_gbs": STEP_BYTES_PER_PARTICLE * n / (ms_step * 1e-3) / 1e9},
+            "wall_s_timed": wall, "gpu_launches": int(launches),
+            "rebuilds_in_timed_region": int(st1.rebuilds - st0.rebuilds),
+            "clocks": clk.summary(), "gen_s": t_gen,
+            "device_memory_gb": round((torch.cuda.mem_get_info(local)[1] - torch.cuda.mem_get_info(local)[0]) / 1e9, 1)}
+    return finish_line(args, sim, sc, n, line, rank)
+
+
+def make_roofline(forces_ms, inter_fluid, nf, n):
+    """The dominant kernel, k_forces_fluid: average launch duration (CUDA events on the library stream,
+    stage-timed pass), algorithmic flops = 91 per interacting pair with a fluid i,
+    algorithmic bytes = 156 B per fluid particle (CSM model).  n = store size when the committed ncu
+    capture is of the same store (64M), for the measured DRAM traffic and L1 figures."""
+    peaks = load_peaks()
+    t_ff = forces_ms * 1e-3
     flops = FLOPS_PER_PAIR_FORCES * inter_fluid
     achieved_tf = flops / t_ff / 1e12
     fp64_peak = peaks.get("fp64_tflops")
@@ -359,23 +390,13 @@ def run_sph(args):
                 "hbm": {"achieved": hbm_achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": hbm_achieved / peaks["hbm_gbs"], "bytes_model": "156 B per fluid particle (CSM)",
                         "peak_source": peaks["source"]}}
-    fp64 = {"pairs_candidate": cand, "pairs_interacting": inter, "pairs_fluid_i": inter_fluid,
-            "pairs_nonfluid_i": inter_other,
-            "step_tflops": (FLOPS_PER_PAIR_FORCES * inter_fluid + FLOPS_PER_PAIR_DENSITY * inter_fluid)
-                           / (ms_step * 1e-3) / 1e12}
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64 lattice + jitter)",
-            "config": dict(workload_config(args, info, n), parallelism="1 GPU",
-                           fluid_rigid_rate=(nf + info["n_rigid"]) / (ms_step * 1e-3),
-                           l2="inputs larger than L2 (state ~%.1f GB)" % (store_bytes(sc.store) / 1e9)),
-            "roofline": roofline, "fp64": fp64, "stage_ms": stage_ms, "rebuild_ms": rebuild_ms,
-            "step_roofline": {"bytes_per_particle": STEP_BYTES_PER_PARTICLE,
-                              "achieved_gbs": STEP_BYTES_PER_PARTICLE * n / (ms_step * 1e-3) / 1e9},
-            "wall_s_timed": wall, "gpu_launches": int(launches),
-            "rebuilds_in_timed_region": int(st1.rebuilds - st0.rebuilds),
-            "clocks": clk.summary(), "gen_s": t_gen,
-            "device_memory_gb": round((torch.cuda.mem_get_info(local)[1] - torch.cuda.mem_get_info(local)[0]) / 1e9, 1)}
+    if fp64_peak:
+        roofline["frac_nominal"] = achieved_tf / 37.2  # against the datasheet FP64 figure as well
+    return roofline
+
+
+def finish_line(args, sim, sc, n, line, rank):
+    import torch
     # e2e: through the public API with host buffers, every step: H2D of the step's kinematic input
     # (positions + velocities from pinned host memory, Simulation.upload_state) -> step(1) ->
     # D2H of the step's fields (positions, velocities, density, pressure) into the ParticleStore

@@ -671,8 +671,10 @@ def bench_multi(args, clock_factory=None):
         meta = [None, None, None, None]
     dist.broadcast_object_list(meta, src=0)
     params, bodies, info, n_total = meta
+    # ghost margin 1h (shell r_c + skin + 1h = 4.1h): particles may drift h/2 before a migration, ~170 steps
+    # of C5 flow; the default 2h costs ~30 % more ghosts at 8 ranks
     ds = DistributedSimulation(params, lambda p: Simulation(p, device=gpu), tensor_device=str(comm),
-                               engine_device=f"cuda:{gpu}")
+                               engine_device=f"cuda:{gpu}", margin_h=getattr(args, "margin_h", 1.0))
     fields = VEC_FIELDS + SCALAR_FIELDS + tuple(TAG_FIELDS)
     if rank == 0:
         owner = ds.grid.owner_of(sc.store.pos)
@@ -772,6 +774,21 @@ def bench_multi(args, clock_factory=None):
                        "DistributedSimulation.step(1) -> download(pos, vel, density, pressure into pinned host); "
                        "host wall clock, max over ranks"}
     counts, imb = ds.imbalance()
+    # dominant kernel on this rank: a stage-timed pass (CUDA events per stage, after the timed region)
+    eng = ds.engine
+    kk = max(2, min(10, args.steps // 2))
+    eng.set_timing(True)
+    sa = eng.stats()
+    ds.step(kk)
+    sb = eng.stats()
+    eng.set_timing(False)
+    _, _, inter_fluid, _ = eng.count_pairs()
+    loc, _ = eng.download(ParticleStore(eng.n), fields=("kind", "owner"))
+    nf_own = int(((loc.kind == abi.FLUID) & (loc.owner == rank)).sum())
+    kern = {"forces_fluid_ms": (sb.stage_ms[10] - sa.stage_ms[10]) / kk, "pairs_fluid_i": int(inter_fluid),
+            "fluid_owned": nf_own, "rank": rank}
+    kern_all = [None] * world
+    dist.all_gather_object(kern_all, kern)
     n = n_total
     if rank == 0:
         weak = getattr(args, "scaling", "strong") == "weak"
@@ -788,8 +805,8 @@ def bench_multi(args, clock_factory=None):
                 "timing": "CUDA events on each rank's stream between barriers + cuda synchronize, "
                           "max over ranks (the per-rank step mixes kernels and NCCL exchanges)",
                 "comm_s_rank0": ds.comm_s, "rebuilds": ds.rebuilds, "repartitions": ds.repartitions,
-                "gpu_launches": int(tl.item()), "e2e": e2e, "roofline": None,
-                "roofline_note": "per-kernel roofline is reported by the N=1 line; N>1 adds halo/body exchanges"}
+                "gpu_launches": int(tl.item()), "e2e": e2e,
+                "kernel_per_rank": kern_all}  # bench.py turns rank 0's entry into the roofline object
         if clock_factory is not None:
             line["clocks"] = clk.summary()
     dist.destroy_process_group()

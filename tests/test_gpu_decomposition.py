@@ -174,3 +174,26 @@ def test_body_partials_device_pointers():
     assert np.array_equal(out[0][0], out[1][0])
     for f in ("force", "torque", "acc", "alpha"):
         assert np.array_equal(out[0][1][f], out[1][1][f]), f
+
+
+def test_bench_two_ranks_line(tmp_path):
+    """bench.py under torchrun with 2 ranks (gloo, both on this GPU): one JSON line from rank 0 with the
+    whole-job value, max-over-ranks timing, the rank-0 roofline object, imbalance and a CPU baseline."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SPHG_DIST_BACKEND="gloo", OMP_NUM_THREADS="4")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--steps", "4", "--warmup", "3", "--nside", "40", "--spheres", "20", "--e2e-steps", "1",
+           "--cpu-nside", "16"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["steps"] == 4 and d["warmup"] == 3
+    assert d["roofline"]["bound"] == "fp64" and 0 < d["roofline"]["frac"] < 1
+    assert d["config"]["imbalance"] < 0.2 and sum(d["config"]["owned_per_rank"]) == d["config"]["particles"]
+    assert d["cpu_baseline"]["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
