@@ -384,7 +384,7 @@ def make_roofline(forces_ms, inter_fluid, nf, n):
     roofline = {"bound": "fp64", "kernel": "k_forces_fluid (momentum_rhs + TVF)",
                 "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": (achieved_tf / fp64_peak) if fp64_peak else None,
-                "traffic": traffic, "l1": l1, "launch_ms": stage_ms["forces_fluid"],
+                "traffic": traffic, "l1": l1, "launch_ms": forces_ms,
                 "flops_per_launch": flops, "flops_model": "91 flop per interacting fluid pair (SURVEY 8(d))",
                 "peak_source": "profiles/fp64_peak.json (DFMA microbenchmark, tools/fp64_peak.cu)",
                 "hbm": {"achieved": hbm_achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
