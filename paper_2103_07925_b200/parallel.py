@@ -649,6 +649,10 @@ def bench_multi(args, clock_factory=None):
     # NCCL over NVLink on a real multi-GPU node; SPHG_DIST_BACKEND=gloo runs the same code with
     # host-staged buffers (used to smoke-test this path with several ranks sharing one GPU)
     backend = os.environ.get("SPHG_DIST_BACKEND", "nccl")
+    # communicator evidence (ranks, transports, NVLS) in the log; INIT only, so the one JSON line stays
+    # easy to find
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if backend == "nccl":
         dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
     else:
