@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(128) k_build_nlist(const __grid_constant__ Dev
 #define SPHG_BUILD_WARPS 1
 #endif
 #ifndef SPHG_BUILD_MINB
-#define SPHG_BUILD_MINB 1
+#define SPHG_BUILD_MINB 20  // <= 96 registers: 64M rebuild 80.5 ms vs 97 ms at the compiler's 132 (r02 sweep)
 #endif
 constexpr int kStage = SPHG_BUILD_STAGE;  // staged candidates per batch (20 B each)
 constexpr int kBuildWarps = SPHG_BUILD_WARPS;  // independent home cells per block (one per warp)
@@ -225,7 +225,7 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
                                             uint32_t h0, uint32_t h1, double ox0, double oy0, double oz0,
                                             const Staged* st, const uint32_t* se, int ns, uint32_t* hc,
                                             const uint32_t* hs, uint32_t batch, uint32_t* fmask, uint32_t* bmask,
-                                            uint32_t* hmask, uint32_t emask) {
+                                            uint32_t emask) {
   const int lane = threadIdx.x & 31;
   const float rv2 = (float)(P.rv2 * P.inv_h * P.inv_h);
   const float lo_band = rv2 * (1.0f - 1e-4f), hi_band = rv2 * (1.0f + 1e-4f);
@@ -259,8 +259,7 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
       const uint32_t h = hs[i - h0];
       if ((h >> 16) == batch) self = (int)(h & 0xffffu);
     }
-    const uint32_t nf = cnt_fluid(count), no = cnt_other(count);
-    uint32_t nft = nf, not_ = no;  // row lengths after this batch
+    uint32_t nf = cnt_fluid(count), no = cnt_other(count);
     uint32_t* row = nbr + (size_t)i * cap;
     uint32_t* back = row + cap - 1;
     const float2 xi2 = make_float2(xi, xi), yi2 = make_float2(yi, yi), zi2 = make_float2(zi, zi);
@@ -294,49 +293,38 @@ __device__ __forceinline__ void build_batch(const DevParams& P, const double4* _
       if (self >= tb && self < tb + 32) in &= ~(1u << (self - tb));
       if (bi) in &= ~bmask[tb >> 5];
       const uint32_t fm = fmask[tb >> 5];
-      hmask[tb + lane] = in & fm;                 // fluid hits of chunk tb / 32
-      hmask[kStage + tb + lane] = in & ~fm;       // rigid / boundary hits
-      nft += __popc(in & fm);
-      not_ += __popc(in & ~fm);
-    }
-    // emission after the whole batch: a lane's loop runs (its hits + chunks) times, so the warp waits for
-    // the batch's most-connected lane once instead of for each chunk's (~2x fewer divergent iterations)
-    const bool fits = nft <= (uint32_t)cap && not_ <= (uint32_t)cap;  // else count only (the caller regrows)
-    const int nch = ns >> 5;
-    {  // fluid neighbours from the front of the row
-      uint32_t k = nf;
-      int c = 0;
-      uint32_t m = hmask[lane];
-      for (;;) {
-        if (m == 0u) {
-          if (++c >= nch) break;
-          m = hmask[(c << 5) + lane];
-          continue;
+      uint32_t hf = in & fm, ho = in & ~fm;
+      const uint32_t cf = __popc(hf), co = __popc(ho);
+      const uint32_t* seb = se + tb;
+      if (nf + cf <= (uint32_t)cap && no + co <= (uint32_t)cap) {  // common case: no bound checks
+        uint32_t* wp = row + nf;
+        while (hf) {  // fluid neighbours from the front
+          const int u = __ffs(hf) - 1;
+          hf &= hf - 1;
+          *wp++ = seb[u];
         }
-        const int u = __ffs(m) - 1;
-        m &= m - 1u;
-        if (fits || k < (uint32_t)cap) row[k] = se[(c << 5) + u];
-        ++k;
-      }
-    }
-    {  // rigid / boundary neighbours from the back
-      uint32_t k = no;
-      int c = 0;
-      uint32_t m = hmask[kStage + lane];
-      for (;;) {
-        if (m == 0u) {
-          if (++c >= nch) break;
-          m = hmask[kStage + (c << 5) + lane];
-          continue;
+        uint32_t* bp = back - no;
+        while (ho) {  // rigid / boundary neighbours from the back
+          const int u = __ffs(ho) - 1;
+          ho &= ho - 1;
+          *bp-- = seb[u];
         }
-        const int u = __ffs(m) - 1;
-        m &= m - 1u;
-        if (fits || k < (uint32_t)cap) back[-(int)k] = se[(c << 5) + u];
-        ++k;
+      } else {  // overflowing row: count only what fits (the caller rebuilds with a larger cap)
+        for (uint32_t k = nf; hf; ++k) {
+          const int u = __ffs(hf) - 1;
+          hf &= hf - 1;
+          if ((int)k < cap) row[k] = seb[u];
+        }
+        for (uint32_t k = no; ho; ++k) {
+          const int u = __ffs(ho) - 1;
+          ho &= ho - 1;
+          if ((int)k < cap) back[-(int)k] = seb[u];
+        }
       }
+      nf += cf;
+      no += co;
     }
-    __syncwarp();  // hmask is rewritten by the next 32 home particles
-    if (act) hc[i - h0] = pack_cnt(nft, not_);
+    if (act) hc[i - h0] = pack_cnt(nf, no);
   }
 }
 
@@ -352,7 +340,6 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
   __shared__ uint32_t hc_all[kBuildWarps][kHomeMax]; // running row length per home particle
   __shared__ uint32_t hs_all[kBuildWarps][kHomeMax]; // (batch << 16 | stage index) of each home particle
   __shared__ uint32_t fm_all[kBuildWarps][kStage / 32], bm_all[kBuildWarps][kStage / 32];
-  __shared__ uint32_t hm_all[kBuildWarps][2 * kStage];  // per (chunk, lane): fluid / other hit masks
   const int wib = threadIdx.x >> 5;
   Staged* st = &st_all[wib];
   uint32_t* se = se_all[wib];
@@ -428,7 +415,7 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
             }
             __syncwarp();
             build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, st, se, padded, hc, hs, batch, fm_all[wib],
-                        bm_all[wib], hm_all[wib], emask);
+                        bm_all[wib], emask);
             __syncwarp();
             ns = 0;
             ++batch;
@@ -472,7 +459,7 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
     }
     __syncwarp();
     build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, st, se, padded, hc, hs, batch, fm_all[wib],
-                bm_all[wib], hm_all[wib], emask);
+                bm_all[wib], emask);
   }
   __syncwarp();
   uint32_t mx = 0;

@@ -1,5 +1,5 @@
 # Verlet-builder variants (tools/build_variants.py): rebuild_ms of the bench line at 64M
-for v in default mb16 mb20 mb24 mb32 w2; do
+for v in ${VARIANTS:-default orig p16 p20}; do
   if [ $v = default ]; then L=libsphg.so; else L=libsphg_$v.so; fi
   SPHG_LIB=$L timeout 600 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/sb_$v.log 2>&1
   python -c "
