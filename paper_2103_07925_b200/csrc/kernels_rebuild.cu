@@ -340,6 +340,8 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
   __shared__ uint32_t hc_all[kBuildWarps][kHomeMax]; // running row length per home particle
   __shared__ uint32_t hs_all[kBuildWarps][kHomeMax]; // (batch << 16 | stage index) of each home particle
   __shared__ uint32_t fm_all[kBuildWarps][kStage / 32], bm_all[kBuildWarps][kStage / 32];
+  __shared__ uint32_t cpre_all[kBuildWarps][28], cj0_all[kBuildWarps][27], ctag_all[kBuildWarps][27];
+  __shared__ double csh_all[kBuildWarps][81];
   const int wib = threadIdx.x >> 5;
   Staged* st = &st_all[wib];
   uint32_t* se = se_all[wib];
@@ -369,84 +371,129 @@ __global__ void __launch_bounds__(32 * kBuildWarps, SPHG_BUILD_MINB) k_build_nli
   const float ex = (float)(1.0 / (P.inv_edge[0] * P.h)), ey = (float)(1.0 / (P.inv_edge[1] * P.h)),
               ez = (float)(1.0 / (P.inv_edge[2] * P.h));
   const float box_lim = (float)(P.rv2 * P.inv_h * P.inv_h) * 1.001f;
+  // the 27 neighbour cells (x-major, then y, then z: the pinned staging order): lane k < 27 resolves
+  // cell k — periodic image, shift, candidate range — so the 27 range loads are in flight together
+  // instead of one dependent round trip per cell; the candidates are then staged from the flattened
+  // list, two per lane per round (both loads issued before either is used)
+  uint32_t* cpre = cpre_all[wib];  // exclusive prefix of the cells' counts; [27] = total
+  uint32_t* cj0 = cj0_all[wib];
+  uint32_t* ctag = ctag_all[wib];
+  double* csh = csh_all[wib];      // 3 per cell: the image shift
+  {
+    uint32_t cntk = 0, j0k = 0, tagk = 0;
+    double shk[3] = {0.0, 0.0, 0.0};
+    if (lane < 27) {
+      const int o[3] = {lane / 9 - 1, (lane / 3) % 3 - 1, lane % 3 - 1};
+      const int64_t cc[3] = {cx, cy, cz}, nn[3] = {nx, ny, nz};
+      int64_t q[3];
+      uint32_t im[3] = {0u, 0u, 0u};
+      bool ok = true;
+      for (int a = 0; a < 3; ++a) {
+        q[a] = cc[a] + o[a];
+        if (q[a] < 0 || q[a] >= nn[a]) {
+          if (!P.periodic[a]) ok = false;
+          im[a] = q[a] < 0 ? 1u : 2u;
+          shk[a] = q[a] < 0 ? -P.L[a] : P.L[a];
+          q[a] = (q[a] + nn[a]) % nn[a];
+        }
+      }
+      if (ok) {
+        const int64_t cj = (q[0] * ny + q[1]) * nz + q[2];
+        j0k = cstart[cj];
+        cntk = cend[cj] - j0k;
+        tagk = code ? img_tag(im[0], im[1], im[2]) : 0u;
+      }
+    }
+    uint32_t incl = cntk;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    if (lane < 27) {
+      cpre[lane] = incl - cntk;
+      cj0[lane] = j0k;
+      ctag[lane] = tagk;
+      csh[3 * lane] = shk[0];
+      csh[3 * lane + 1] = shk[1];
+      csh[3 * lane + 2] = shk[2];
+    }
+    if (lane == 26) cpre[27] = incl;
+  }
+  __syncwarp();
+  const uint32_t total = cpre[27];
   int ns = 0;
   uint32_t batch = 0;
-  for (int ox = -1; ox <= 1; ++ox) {
-    int64_t qx = cx + ox;
-    uint32_t ix = 0;
-    double sx = 0.0;
-    if (qx < 0 || qx >= nx) {
-      if (!P.periodic[0]) continue;
-      ix = qx < 0 ? 1u : 2u;
-      sx = qx < 0 ? -P.L[0] : P.L[0];
-      qx = (qx + nx) % nx;
+  // flattened candidate t -> (cell k, particle j): the last cell whose prefix is <= t
+  auto locate = [&](uint32_t t, int& k) {
+    k = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1)
+      if (k + step < 27 && cpre[k + step] <= t) k += step;
+  };
+  for (uint32_t base = 0; base < total; base += 64) {
+    if (ns > kStage - 64) {  // room for a full round of 64: flush the batch (padded to whole chunks)
+      const int padded = (ns + 31) & ~31;
+      for (int t = ns + lane; t < padded; t += 32) {
+        st->nx[t] = st->ny[t] = st->nz[t] = -1e30f;
+        st->kind[t] = 0.f;
+        se[t] = 0u;
+      }
+      __syncwarp();
+      build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, st, se, padded, hc, hs, batch, fm_all[wib],
+                  bm_all[wib], emask);
+      __syncwarp();
+      ns = 0;
+      ++batch;
     }
-    for (int oy = -1; oy <= 1; ++oy) {
-      int64_t qy = cy + oy;
-      uint32_t iy = 0;
-      double sy = 0.0;
-      if (qy < 0 || qy >= ny) {
-        if (!P.periodic[1]) continue;
-        iy = qy < 0 ? 1u : 2u;
-        sy = qy < 0 ? -P.L[1] : P.L[1];
-        qy = (qy + ny) % ny;
+    const uint32_t ta = base + lane, tb2 = base + 32 + lane;
+    int ka = 0, kb = 0;
+    uint32_t ja = 0, jbb = 0;
+    double4 pa = make_double4(0, 0, 0, 0), pb = make_double4(0, 0, 0, 0);
+    uint32_t kda = 0, kdb = 0;
+    if (ta < total) {
+      locate(ta, ka);
+      ja = cj0[ka] + (ta - cpre[ka]);
+      pa = G0[ja];
+      kda = kmd[ja];
+    }
+    if (tb2 < total) {
+      locate(tb2, kb);
+      jbb = cj0[kb] + (tb2 - cpre[kb]);
+      pb = G0[jbb];
+      kdb = kmd[jbb];
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool in_range = h == 0 ? ta < total : tb2 < total;
+      const int k = h == 0 ? ka : kb;
+      const uint32_t j = h == 0 ? ja : jbb;
+      const double4 pj = h == 0 ? pa : pb;
+      const uint32_t kdj = h == 0 ? kda : kdb;
+      // stage the candidate only if it can be within r_v of the home cell's box (conservative fp32 box
+      // distance with a 1e-3 margin; the exact rule decides later); the home cell (k = 13) always
+      bool keep = in_range;
+      const bool home = k == 13;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (keep) {
+        // the periodic image of the cell: x_j + s sits next to the home cell
+        q = make_float4((float)((pj.x + csh[3 * k] - ox0) * P.inv_h), (float)((pj.y + csh[3 * k + 1] - oy0) * P.inv_h),
+                        (float)((pj.z + csh[3 * k + 2] - oz0) * P.inv_h), (float)kind_of(kdj));  // 0 fluid 1 rigid 2 wall
+        const float dx = fmaxf(0.f, fmaxf(-q.x, q.x - ex)), dy = fmaxf(0.f, fmaxf(-q.y, q.y - ey)),
+                    dz = fmaxf(0.f, fmaxf(-q.z, q.z - ez));
+        keep = home || (dx * dx + dy * dy + dz * dz <= box_lim);
       }
-      for (int oz = -1; oz <= 1; ++oz) {
-        int64_t qz = cz + oz;
-        uint32_t iz = 0;
-        double sz = 0.0;
-        if (qz < 0 || qz >= nz) {
-          if (!P.periodic[2]) continue;
-          iz = qz < 0 ? 1u : 2u;
-          sz = qz < 0 ? -P.L[2] : P.L[2];
-          qz = (qz + nz) % nz;
-        }
-        const uint32_t tag = code ? img_tag(ix, iy, iz) : 0u;
-        const int64_t cj = (qx * ny + qy) * nz + qz;
-        const bool home = ox == 0 && oy == 0 && oz == 0;
-        const uint32_t j0 = cstart[cj], j1 = cend[cj];
-        for (uint32_t jb = j0; jb < j1; jb += 32) {
-          if (ns > kStage - 32) {  // room for a full round: flush the batch (padded to whole chunks)
-            const int padded = (ns + 31) & ~31;
-            for (int t = ns + lane; t < padded; t += 32) {
-              st->nx[t] = st->ny[t] = st->nz[t] = -1e30f;
-              st->kind[t] = 0.f;
-              se[t] = 0u;
-            }
-            __syncwarp();
-            build_batch(P, G0, kmd, nbr, cap, h0, h1, ox0, oy0, oz0, st, se, padded, hc, hs, batch, fm_all[wib],
-                        bm_all[wib], emask);
-            __syncwarp();
-            ns = 0;
-            ++batch;
-          }
-          // one candidate per lane: stage it only if it can be within r_v of the home cell's box
-          // (conservative fp32 box distance with a 1e-3 margin; the exact rule decides later)
-          const uint32_t j = jb + lane;
-          bool keep = j < j1;
-          float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (keep) {
-            const double4 pj = G0[j];
-            // the periodic image of the cell: x_j + s sits next to the home cell
-            q = make_float4((float)((pj.x + sx - ox0) * P.inv_h), (float)((pj.y + sy - oy0) * P.inv_h),
-                            (float)((pj.z + sz - oz0) * P.inv_h), (float)kind_of(kmd[j]));  // 0 fluid 1 rigid 2 wall
-            const float dx = fmaxf(0.f, fmaxf(-q.x, q.x - ex)), dy = fmaxf(0.f, fmaxf(-q.y, q.y - ey)),
-                        dz = fmaxf(0.f, fmaxf(-q.z, q.z - ez));
-            keep = home || (dx * dx + dy * dy + dz * dz <= box_lim);
-          }
-          const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-          if (keep) {
-            const int at = ns + __popc(bal & ((1u << lane) - 1u));
-            st->nx[at] = -q.x;
-            st->ny[at] = -q.y;
-            st->nz[at] = -q.z;
-            st->kind[at] = q.w;
-            se[at] = j | tag;
-            if (home) hs[j - h0] = (batch << 16) | (uint32_t)at;
-          }
-          ns += __popc(bal);
-        }
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int at = ns + __popc(bal & ((1u << lane) - 1u));
+        st->nx[at] = -q.x;
+        st->ny[at] = -q.y;
+        st->nz[at] = -q.z;
+        st->kind[at] = q.w;
+        se[at] = j | ctag[k];
+        if (home) hs[j - h0] = (batch << 16) | (uint32_t)at;
       }
+      ns += __popc(bal);
     }
   }
   __syncwarp();
