@@ -373,7 +373,8 @@ int sphg_cell_occupancy(sphg_ctx* ctx, int64_t* hist, size_t nbins, int64_t* max
  *      ghost) and sphg_replace_bodies, then the body force/torque of the new membership (body partials).
  * Records are sphg_record_doubles() doubles: [0..2] position, [3] kind, [4] material, [5] group,
  * [6] mass, then the engine's own per-particle state (opaque; only the same engine reads it back).
- * `mask` holds n_bodies bytes; ids are local ids in ascending order; buffers are host memory. */
+ * `mask` holds n_bodies bytes; ids are local ids in ascending order; record buffers and their id lists may
+ * be host or device memory. */
 int sphg_event_bodies(sphg_ctx* ctx, uint8_t* mask, size_t n_bodies);
 int sphg_event_members(sphg_ctx* ctx, const uint8_t* mask, size_t n_bodies, uint32_t* ids, size_t cap, size_t* n);
 int sphg_record_doubles(void);
@@ -381,6 +382,12 @@ int sphg_record_pack(sphg_ctx* ctx, const uint32_t* ids, size_t m, double* recs)
 /* keep_position = 1: the local copy keeps its coordinates (ghosts may be unwrapped across a periodic face)
  * and its ghost/owned role; 0: the record's position is written too (the single-rank batch context) */
 int sphg_record_unpack(sphg_ctx* ctx, const uint32_t* ids, size_t m, const double* recs, int keep_position);
+/* Replaces the whole store with n records (the first n_owned owned, the rest ghosts; local ids = record
+ * order) and the body table: the device-resident migration of parallel.py rebuilds a
+ * rank's owned + ghost set from exchanged records without a host round trip.  recs / bodies may be host
+ * or device pointers; the Verlet list is rebuilt on the next step. */
+int sphg_upload_records(sphg_ctx* ctx, size_t n, size_t n_owned, const double* recs, const sphg_body* bodies,
+                        size_t n_bodies);
 /* replaces the body table after record_unpack changed kinds / groups and refreshes the index lists
  * (rigid body-major list, kind lists, row partitions, contact order) */
 int sphg_replace_bodies(sphg_ctx* ctx, const sphg_body* bodies, size_t n_bodies);

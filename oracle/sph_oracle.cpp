@@ -2026,6 +2026,37 @@ int orc_record_unpack(orc_ctx* h, const uint32_t* ids, size_t m, const double* r
     return SPHG_OK;
 }
 
+// sphg_upload_records: the whole store from records (first n_owned owned), host pointers
+int orc_upload_records(orc_ctx* h, size_t n, size_t n_owned, const double* recs, const sphg_body* bodies, size_t nb) {
+    Ctx& c = *reinterpret_cast<Ctx*>(h);
+    if (n_owned > n) return SPHG_ERR_CONFIG;
+    auto& S = c.S;
+    S.pos.assign(n, V3::zero()); S.vel.assign(n, V3::zero()); S.vel_adv.assign(n, V3::zero());
+    S.acc.assign(n, V3::zero()); S.acc_bg.assign(n, V3::zero());
+    S.density.assign(n, 0.0); S.pressure.assign(n, 0.0); S.mass.assign(n, 0.0);
+    S.temperature.assign(n, 0.0); S.dT_dt.assign(n, 0.0); S.concentration.assign(n, 0.0); S.dC_dt.assign(n, 0.0);
+    S.kind.assign(n, Kind::Fluid); S.group.assign(n, 0u); S.material.assign(n, (uint16_t)0);
+    S.body_frame_pos.assign(n, V3::zero()); S.wall_pressure.assign(n, 0.0); S.wall_velocity.assign(n, V3::zero());
+    S.dirichlet_T.assign(n, (uint8_t)0xff); S.dirichlet_C.assign(n, (uint8_t)0xff);
+    S.owner.assign(n, (uint32_t)c.P.rank);
+    for (size_t i = n_owned; i < n; ++i) S.owner[i] = 0xffffffffu;
+    resize_aux(c);
+    std::vector<uint32_t> ids(n);
+    std::iota(ids.begin(), ids.end(), 0u);
+    const int rc = orc_record_unpack(h, ids.data(), n, recs, 0);
+    if (rc) return rc;
+    c.halo.assign(SPHG_MAX_HALO_SLOTS, {});
+    c.has_ghosts = n_owned < n;
+    c.disp_since_partition = 0.0;
+    c.bodies.assign(bodies, bodies + nb);
+    c.body_fscale.assign(nb, 0.0);
+    c.body_tscale.assign(nb, 0.0);
+    rebuild_members(c);
+    c.ev.clear();
+    c.built = false;
+    return SPHG_OK;
+}
+
 int orc_replace_bodies(orc_ctx* h, const sphg_body* bodies, size_t nb) {
     Ctx& c = *reinterpret_cast<Ctx*>(h);
     c.bodies.assign(bodies, bodies + nb);

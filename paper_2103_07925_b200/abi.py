@@ -193,9 +193,10 @@ def declare(lib, prefix):
         "event_members": (C.c_int, [vp, C.POINTER(C.c_uint8), C.c_size_t, C.POINTER(C.c_uint32), C.c_size_t,
                                     C.POINTER(C.c_size_t)]),
         "record_doubles": (C.c_int, []),
-        "record_pack": (C.c_int, [vp, C.POINTER(C.c_uint32), C.c_size_t, C.POINTER(C.c_double)]),
-        "record_unpack": (C.c_int, [vp, C.POINTER(C.c_uint32), C.c_size_t, C.POINTER(C.c_double), C.c_int]),
+        "record_pack": (C.c_int, [vp, C.c_void_p, C.c_size_t, C.c_void_p]),
+        "record_unpack": (C.c_int, [vp, C.c_void_p, C.c_size_t, C.c_void_p, C.c_int]),
         "replace_bodies": (C.c_int, [vp, C.POINTER(Body), C.c_size_t]),
+        "upload_records": (C.c_int, [vp, C.c_size_t, C.c_size_t, C.c_void_p, C.c_void_p, C.c_size_t]),
         "shepard_grid": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                    C.c_int32, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint8)]),
     }

@@ -955,6 +955,16 @@ __global__ void k_pack_store(const __grid_constant__ DevParams P, Particles D, s
   if (o.dirichlet_C) o.dirichlet_C[g] = (uint8_t)dirc_of(kmd);
 }
 
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
 bool is_pinned(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -1141,6 +1151,42 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
   return SPHG_OK;
 }
 
+// device arrays for a store of n particles (sphg_upload, sphg_upload_records)
+void alloc_store(Ctx& c, size_t n) {
+  c.n = n;
+  const size_t na = std::max<size_t>(n, 1);
+  c.cur.alloc(na, c.P.diffusion != 0);
+  c.alt.alloc(na, c.P.diffusion != 0);
+  c.H2new.alloc(na);
+  c.pin_list.alloc(na);
+  c.wrap_list.alloc(2 * na);  // periodic-face crossings of a step (allocated here: the kick chain is captured)
+  if (!c.pin_any) SPHG_CUDA_CHECK(cudaMalloc(&c.pin_any, sizeof(uint32_t)));
+  if (c.P.diffusion) c.C2new.alloc(na);
+  if (c.P.heat_source) {
+    c.hsrc.alloc(na);
+    c.P.hsrc = c.hsrc.p;
+  }
+  c.keys.alloc(na);
+  c.keys_alt.alloc(na);
+  c.vals.alloc(na);
+  c.vals_alt.alloc(na);
+  c.hist.alloc(radix_scratch_words(na));
+  c.scan_tmp.alloc(radix_scratch_words(na));
+  c.cell_start.alloc(c.ncells);
+  c.cell_end.alloc(c.ncells);
+  c.cell_key.alloc(na);
+  c.cnt.alloc(na);
+  const bool any_periodic = c.P.periodic[0] || c.P.periodic[1] || c.P.periodic[2];
+  // image-coded entries need the index in 27 bits; larger stores use the minimum image
+  // (SPHG_IMG_MIN=1 forces that path for testing at small sizes)
+  static const bool force_min = std::getenv("SPHG_IMG_MIN") && std::atoi(std::getenv("SPHG_IMG_MIN")) != 0;
+  const int mode = !any_periodic ? kImgNone : ((n < (size_t(1) << kIdxBits) && !force_min) ? kImgCode : kImgMin);
+  if (mode != c.P.img_mode) {
+    c.P.img_mode = mode;
+    c.built = false;
+  }
+}
+
 int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t nb) {
   return guarded(h, [&]() -> int {
     Ctx& c = h->c;
@@ -1174,38 +1220,7 @@ int sphg_upload(sphg_ctx* h, const sphg_soa* s, const sphg_body* bodies, size_t 
     // warm upload: same store size and a valid Verlet list -> keep the device order and the list,
     // scatter the host (gid-ordered) data through the gid permutation
     const bool warm = c.built && c.have_state && n == c.n && n > 0;
-    c.n = n;
-    const size_t na = std::max<size_t>(n, 1);
-    c.cur.alloc(na, c.P.diffusion != 0);
-    c.alt.alloc(na, c.P.diffusion != 0);
-    c.H2new.alloc(na);
-    c.pin_list.alloc(na);
-    c.wrap_list.alloc(2 * na);  // periodic-face crossings of a step (allocated here: the kick chain is captured)
-    if (!c.pin_any) SPHG_CUDA_CHECK(cudaMalloc(&c.pin_any, sizeof(uint32_t)));
-    if (c.P.diffusion) c.C2new.alloc(na);
-    if (c.P.heat_source) {
-      c.hsrc.alloc(na);
-      c.P.hsrc = c.hsrc.p;
-    }
-    c.keys.alloc(na);
-    c.keys_alt.alloc(na);
-    c.vals.alloc(na);
-    c.vals_alt.alloc(na);
-    c.hist.alloc(radix_scratch_words(na));
-    c.scan_tmp.alloc(radix_scratch_words(na));
-    c.cell_start.alloc(c.ncells);
-    c.cell_end.alloc(c.ncells);
-    c.cell_key.alloc(na);
-    c.cnt.alloc(na);
-    const bool any_periodic = c.P.periodic[0] || c.P.periodic[1] || c.P.periodic[2];
-    // image-coded entries need the index in 27 bits; larger stores use the minimum image
-    // (SPHG_IMG_MIN=1 forces that path for testing at small sizes)
-    static const bool force_min = std::getenv("SPHG_IMG_MIN") && std::atoi(std::getenv("SPHG_IMG_MIN")) != 0;
-    const int mode = !any_periodic ? kImgNone : ((n < (size_t(1) << kIdxBits) && !force_min) ? kImgCode : kImgMin);
-    if (mode != c.P.img_mode) {
-      c.P.img_mode = mode;
-      c.built = false;
-    }
+    alloc_store(c, n);
     Particles& dst = (warm && c.built) ? c.alt : c.cur;
     stage_upload(c, s, dst);
     if (warm && c.built) {
@@ -1785,14 +1800,17 @@ int sphg_record_doubles(void) { return kRecordDoubles; }
 int sphg_record_pack(sphg_ctx* h, const uint32_t* ids, size_t m, double* recs) {
   return guarded(h, [&]() -> int {
     Ctx& c = h->c;
-    for (size_t s = 0; s < m; ++s)
-      if (ids[s] >= c.n) return fail(h, SPHG_ERR_CONFIG, "record_pack: id out of range");
+    if (!is_device_ptr(ids))
+      for (size_t s = 0; s < m; ++s)
+        if (ids[s] >= c.n) return fail(h, SPHG_ERR_CONFIG, "record_pack: id out of range");
     if (m == 0) return SPHG_OK;
     c.rec_ids.alloc(m);
     c.rec_buf.alloc(m * kRecordDoubles);
-    h2d(c.rec_ids.p, ids, m, c.stream);
+    // host or device buffers (unified addressing: the multi-rank driver keeps records on the device)
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(c.rec_ids.p, ids, m * sizeof(uint32_t), cudaMemcpyDefault, c.stream));
     record_pack(c, c.rec_ids.p, m, c.rec_buf.p);
-    d2h(recs, c.rec_buf.p, m * kRecordDoubles, c.stream);
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(recs, c.rec_buf.p, m * kRecordDoubles * sizeof(double), cudaMemcpyDefault,
+                                    c.stream));
     host_sync(c, c.stream);
     return SPHG_OK;
   });
@@ -1801,19 +1819,58 @@ int sphg_record_pack(sphg_ctx* h, const uint32_t* ids, size_t m, double* recs) {
 int sphg_record_unpack(sphg_ctx* h, const uint32_t* ids, size_t m, const double* recs, int keep_position) {
   return guarded(h, [&]() -> int {
     Ctx& c = h->c;
-    for (size_t s = 0; s < m; ++s) {
-      if (ids[s] >= c.n) return fail(h, SPHG_ERR_CONFIG, "record_unpack: id out of range");
-      const double* o = recs + s * kRecordDoubles;
-      if (!(o[3] >= 0.0 && o[3] <= 2.0) || !(o[4] >= 0.0 && o[4] < c.params.n_mat))
-        return fail(h, SPHG_ERR_CONFIG, "record_unpack: invalid kind/material");
-    }
+    if (!is_device_ptr(ids) && !is_device_ptr(recs))
+      for (size_t s = 0; s < m; ++s) {
+        if (ids[s] >= c.n) return fail(h, SPHG_ERR_CONFIG, "record_unpack: id out of range");
+        const double* o = recs + s * kRecordDoubles;
+        if (!(o[3] >= 0.0 && o[3] <= 2.0) || !(o[4] >= 0.0 && o[4] < c.params.n_mat))
+          return fail(h, SPHG_ERR_CONFIG, "record_unpack: invalid kind/material");
+      }
     if (m == 0) return SPHG_OK;
     c.rec_ids.alloc(m);
     c.rec_buf.alloc(m * kRecordDoubles);
-    h2d(c.rec_ids.p, ids, m, c.stream);
-    h2d(c.rec_buf.p, recs, m * kRecordDoubles, c.stream);
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(c.rec_ids.p, ids, m * sizeof(uint32_t), cudaMemcpyDefault, c.stream));
+    SPHG_CUDA_CHECK(cudaMemcpyAsync(c.rec_buf.p, recs, m * kRecordDoubles * sizeof(double), cudaMemcpyDefault,
+                                    c.stream));
     record_unpack(c, c.rec_ids.p, m, c.rec_buf.p, keep_position);
     host_sync(c, c.stream);
+    return SPHG_OK;
+  });
+}
+
+int sphg_upload_records(sphg_ctx* h, size_t n, size_t n_owned, const double* recs, const sphg_body* bodies,
+                        size_t nb) {
+  return guarded(h, [&]() -> int {
+    Ctx& c = h->c;
+    SPHG_CUDA_CHECK(cudaSetDevice(c.device));
+    if (n >= (size_t)UINT32_MAX) return fail(h, SPHG_ERR_CONFIG, "too many particles for 32-bit gids");
+    if (n_owned > n) return fail(h, SPHG_ERR_CONFIG, "upload_records: n_owned > n");
+    host_sync(c, c.stream);
+    destroy_graphs(c);
+    c.nghost = n - n_owned;
+    c.disp_since_partition = 0.0;
+    alloc_store(c, n);
+    c.built = false;
+    c.final_pending = false;
+    iota_gid(c);
+    build_idx_of_gid(c);
+    const double* dr = recs;
+    if (!is_device_ptr(recs) && n) {
+      c.rec_buf.alloc(n * kRecordDoubles);
+      SPHG_CUDA_CHECK(cudaMemcpyAsync(c.rec_buf.p, recs, n * kRecordDoubles * sizeof(double), cudaMemcpyDefault,
+                                      c.stream));
+      dr = c.rec_buf.p;
+    }
+    record_load(c, dr, n, n_owned);
+    c.nb = 0;
+    ensure_bodies(c, nb);
+    c.nb = nb;
+    if (nb) SPHG_CUDA_CHECK(cudaMemcpyAsync(c.bodies.p, bodies, nb * sizeof(sphg_body), cudaMemcpyDefault, c.stream));
+    SPHG_CUDA_CHECK(cudaMemsetAsync(c.dflags, 0, sizeof(DevFlags), c.stream));
+    SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->err_gid, 0xff, 2 * sizeof(uint32_t), c.stream));
+    host_sync(c, c.stream);
+    c.have_state = true;
+    h->mid_step = false;
     return SPHG_OK;
   });
 }

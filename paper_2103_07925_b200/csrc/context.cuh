@@ -299,6 +299,7 @@ size_t event_members(Ctx& c, const uint32_t* dev_mask, size_t nb, uint32_t* dev_
 constexpr int kRecordDoubles = 44;
 void record_pack(Ctx& c, const uint32_t* dev_ids, size_t m, double* dev_out);
 void record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_in, int keep_position);
+void record_load(Ctx& c, const double* dev_recs, size_t n, size_t n_owned);  // whole store (sphg_upload_records)
 void launch_repartition_rows(Ctx& c);
 void launch_contact_order(Ctx& c);
 

@@ -496,7 +496,34 @@ __global__ void k_record_unpack(Particles D, const uint32_t* __restrict__ ids, s
   D.group.p[k] = (uint32_t)o[5];
 }
 
+// a whole store from records (sphg_upload_records): record s -> index s, positions included; the first
+// n_owned are owned, the rest ghosts; R4 (the Verlet reference) = the position
+__global__ void k_record_load(Particles D, size_t n, size_t n_owned, const double* __restrict__ in) {
+  const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double* o = in + s * kRecordDoubles;
+  D.G0.p[s] = make_double4(o[0], o[1], o[2], o[7]);
+  D.R4.p[s] = make_double4(o[0], o[1], o[2], 0.0);
+  double4* rec[7] = {&D.G1.p[s], &D.G2.p[s], &D.V4.p[s], &D.A4.p[s], &D.B4.p[s], &D.F4.p[s], &D.X4.p[s]};
+#pragma unroll
+  for (int r = 0; r < 7; ++r) *rec[r] = make_double4(o[8 + 4 * r], o[9 + 4 * r], o[10 + 4 * r], o[11 + 4 * r]);
+  D.H2.p[s] = make_double2(o[36], o[37]);
+  D.dTdt.p[s] = o[38];
+  D.p_static.p[s] = o[39];
+  if (D.C2.p) D.C2.p[s] = make_double2(o[40], o[41]);
+  if (D.dCdt.p) D.dCdt.p[s] = o[42];
+  const uint32_t kmd = (uint32_t)o[43] & ~kGhostBit;
+  D.kmd.p[s] = s >= n_owned ? (kmd | kGhostBit) : kmd;
+  D.group.p[s] = (uint32_t)o[5];
+}
+
 }  // namespace
+
+void record_load(Ctx& c, const double* dev_recs, size_t n, size_t n_owned) {
+  if (n == 0) return;
+  k_record_load<<<grid_for(n, 128), 128, 0, c.stream>>>(c.cur, n, n_owned, dev_recs);
+  c.launches++;
+}
 
 void launch_detect(Ctx& c) {
   const size_t n = c.n;

@@ -549,90 +549,118 @@ class DistributedSimulation:
                 getattr(g, f)[p["gid"]] = p[f]
         return g, bodies
 
-    # ------------------------------------------------------------ migration
-    _FIELDS = VEC_FIELDS + SCALAR_FIELDS + tuple(TAG_FIELDS)
+    # ------------------------------------------------------------ migration (device-resident)
+    def _owner_t(self, pos):
+        """Grid.owner_of on a (m, 3) float64 tensor (the same IEEE operations as the numpy form)."""
+        g = self.grid
+        dev = pos.device
+        lo = torch.tensor(g.lo, dtype=torch.float64, device=dev)
+        w = torch.tensor(g.L / np.array(g.dims), dtype=torch.float64, device=dev)
+        dims = torch.tensor(g.dims, dtype=torch.int64, device=dev)
+        c = torch.floor((pos - lo) / w).to(torch.int64)
+        c = torch.minimum(torch.clamp(c, min=0), dims - 1)
+        return (c[:, 0] * dims[1] + c[:, 1]) * dims[2] + c[:, 2]
 
-    def _record_dtype(self):
-        st = ParticleStore(1)
-        spec = [("gid", np.int64)]
-        for f in self._FIELDS:
-            a = getattr(st, f)
-            spec.append((f, a.dtype, a.shape[1:]))
-        return np.dtype(spec)
+    def _near_box_t(self, pos, r, width):
+        """Grid.near_box on a tensor: within L-infinity distance `width` of rank r's box (periodic images)."""
+        g = self.grid
+        lo, hi = g.box(r)
+        ok = torch.ones(pos.shape[0], dtype=torch.bool, device=pos.device)
+        for a in range(3):
+            x = pos[:, a]
+            inside = (x >= lo[a] - width) & (x <= hi[a] + width)
+            if g.periodic[a]:
+                inside |= (x + g.L[a] >= lo[a] - width) & (x + g.L[a] <= hi[a] + width)
+                inside |= (x - g.L[a] >= lo[a] - width) & (x - g.L[a] <= hi[a] + width)
+            ok &= inside
+        return ok
 
-    def _pack(self, local, idx, gids):
-        rec = np.zeros(len(idx), self._record_dtype())
-        rec["gid"] = gids
-        for f in self._FIELDS:
-            rec[f] = getattr(local, f)[idx]
-        return rec
-
-    def _exchange(self, outgoing):
-        """outgoing[q] = record array for rank q -> list of record arrays received from every rank
-        (point-to-point: counts first, then payload bytes; NCCL or gloo)."""
-        rd = self._record_dtype()
-        counts_out = {q: torch.tensor([len(outgoing.get(q, ()))], dtype=torch.int64, device=self.dev)
-                      for q in range(self.world) if q != self.rank}
-        counts_in = {q: torch.zeros(1, dtype=torch.int64, device=self.dev)
-                     for q in range(self.world) if q != self.rank}
+    def _exchange_t(self, outgoing, width):
+        """outgoing[q] = (m, width) float64 tensor for rank q -> {q: tensor received from q} (on the
+        engine's device): counts first, then the payload, point to point (NCCL on the device; gloo
+        through host copies)."""
+        peers = [q for q in range(self.world) if q != self.rank]
+        cnt_out = {q: torch.tensor([int(outgoing[q].shape[0]) if q in outgoing else 0], dtype=torch.int64,
+                                   device=self.dev) for q in peers}
+        cnt_in = {q: torch.zeros(1, dtype=torch.int64, device=self.dev) for q in peers}
         ops = []
-        for q in counts_out:
-            ops.append(dist.P2POp(dist.isend, counts_out[q], q, group=self.group))
-            ops.append(dist.P2POp(dist.irecv, counts_in[q], q, group=self.group))
+        for q in peers:
+            ops.append(dist.P2POp(dist.isend, cnt_out[q], q, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, cnt_in[q], q, group=self.group))
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
-        ops, bufs = [], {}
-        for q in counts_out:
-            m_out = int(counts_out[q].item())
-            m_in = int(counts_in[q].item())
+        ops, recv = [], {}
+        for q in peers:
+            m_out, m_in = int(cnt_out[q].item()), int(cnt_in[q].item())
             if m_out:
-                data = torch.from_numpy(np.ascontiguousarray(outgoing[q]).view(np.uint8)).to(self.dev)
-                ops.append(dist.P2POp(dist.isend, data, q, group=self.group))
-                bufs[("s", q)] = data
+                ops.append(dist.P2POp(dist.isend, outgoing[q].contiguous().to(self.dev), q, group=self.group))
             if m_in:
-                bufs[("r", q)] = torch.empty(m_in * rd.itemsize, dtype=torch.uint8, device=self.dev)
-                ops.append(dist.P2POp(dist.irecv, bufs[("r", q)], q, group=self.group))
+                recv[q] = torch.empty((m_in, width), dtype=torch.float64, device=self.dev)
+                ops.append(dist.P2POp(dist.irecv, recv[q], q, group=self.group))
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
         if self.dev.type == "cuda":
             torch.cuda.current_stream(self.dev).synchronize()
-        got = {q: bufs[("r", q)].cpu().numpy().view(rd) for q in counts_in if ("r", q) in bufs}
-        return got
+        return {q: t.to(self.edev) for q, t in recv.items()}
 
     def repartition(self):
-        """Particle migration: every rank sends the owned particles that left its box
-        to their new owner, then ships each peer the owned particles inside that peer's ghost shell;
-        no rank ever holds more than its own owned + ghost set.  Rare: after margin/2 of motion."""
-        local, bodies = self.engine.download()
+        """Particle migration, device-resident: each rank packs its owned particles as
+        engine records (sphg_record_pack into a device tensor), sends the ones that left its box to their
+        new owner, then ships every peer the owned particles inside that peer's ghost shell, and reloads
+        its owned + ghost set from the records (sphg_upload_records): no rank holds more than its own
+        owned + ghost set and nothing crosses to the host but counts.  Rare: after margin/2 of motion."""
+        e = self.engine
+        R = e.record_doubles()
         n_own = self.n_own
-        pos = local.pos[:n_own]
-        gids = self.gids[:n_own].astype(np.int64)
-        new_owner = self.grid.owner_of(pos)
-        keep = np.nonzero(new_owner == self.rank)[0]
-        outgoing = {q: self._pack(local, np.nonzero(new_owner == q)[0], gids[new_owner == q])
-                    for q in range(self.world) if q != self.rank}
-        got = self._exchange(outgoing)
-        owned = np.concatenate([self._pack(local, keep, gids[keep])] + [got[q] for q in sorted(got)])
-        owned = owned[np.argsort(owned["gid"], kind="stable")]
-        # ghosts: each peer gets my (new) owned particles within its shell
-        opos = owned["pos"]
-        shells = {q: owned[self.grid.near_box(opos, q, self.width)] for q in range(self.world) if q != self.rank}
-        got = self._exchange(shells)
-        ghosts = [got[q] for q in sorted(got)]  # (owner rank, gid) order, as local_gids
-        ghost_owner = np.concatenate([np.full(len(got[q]), q, np.uint32) for q in sorted(got)]) \
-            if ghosts else np.zeros(0, np.uint32)
-        for k, q in enumerate(sorted(got)):
-            ghosts[k] = ghosts[k][np.argsort(ghosts[k]["gid"], kind="stable")]
-        allrec = np.concatenate([owned] + ghosts) if ghosts else owned
-        new = ParticleStore(len(allrec))
-        for f in self._FIELDS:
-            getattr(new, f)[:] = allrec[f]
-        new.owner[: len(owned)] = self.rank
-        new.owner[len(owned):] = ghost_owner
+        ids = torch.arange(n_own, dtype=torch.int32, device=self.edev)
+        recs = e.record_pack(ids, out=torch.empty((n_own, R), dtype=torch.float64, device=self.edev))
+        gid = torch.from_numpy(self.gids[:n_own].astype(np.float64)).to(self.edev)  # exact below 2^53
+        full = torch.cat([gid[:, None], recs], dim=1)
+        new_owner = self._owner_t(full[:, 1:4])
+        outgoing = {q: full[new_owner == q] for q in range(self.world) if q != self.rank}
+        got = self._exchange_t(outgoing, R + 1)
+        owned = torch.cat([full[new_owner == self.rank]] + [got[q] for q in sorted(got)])
+        owned = owned[torch.argsort(owned[:, 0], stable=True)]
+        shells = {q: owned[self._near_box_t(owned[:, 1:4], q, self.width)]
+                  for q in range(self.world) if q != self.rank}
+        got = self._exchange_t(shells, R + 1)
+        ghosts, gowner = [], []
+        for q in sorted(got):  # (owner rank, gid) order, as local_gids
+            t = got[q][torch.argsort(got[q][:, 0], stable=True)]
+            ghosts.append(t)
+            gowner.append(np.full(t.shape[0], q, np.int64))
+        allrec = torch.cat([owned] + ghosts) if ghosts else owned
+        _, bodies = e.download(ParticleStore(e.n), fields=())
         self.repartitions += 1
-        self.distribute_local(new, allrec["gid"], len(owned), self.global_n, bodies)
+        self._install(allrec, int(owned.shape[0]), np.concatenate(gowner) if gowner else np.zeros(0, np.int64),
+                      bodies)
+
+    def _install(self, allrec, n_own, ghost_owner, bodies):
+        """Load an owned + ghost set given as [gid | record] rows (owned by gid, then ghosts by (owner,
+        gid)) into the engine and derive the per-peer halo lists, all from device tensors."""
+        e = self.engine
+        self.gids = allrec[:, 0].to(torch.int64).cpu().numpy()
+        self.n_own = n_own
+        e.upload_records(allrec[:, 1:].contiguous(), n_own, bodies)
+        pos_own = allrec[:n_own, 1:4]
+        self.peers = []
+        for q in range(self.world):
+            if q == self.rank:
+                continue
+            send_l = torch.nonzero(self._near_box_t(pos_own, q, self.width)).flatten().cpu().numpy()  # gid order
+            recv_l = n_own + np.nonzero(ghost_owner == q)[0]  # one block, gid order
+            if len(send_l) == 0 and len(recv_l) == 0:
+                continue
+            self.peers.append((q, send_l.astype(np.uint32), recv_l.astype(np.uint32)))
+        for k, (q, snd, rcv) in enumerate(self.peers):
+            self._halo_set(2 * k, snd)
+            self._halo_set(2 * k + 1, rcv)
+        self.disp_since_partition = 0.0
+        self._bufs = {}
+        if self._fused_ok():
+            self._bind_fused()
 
 
 # ---------------------------------------------------------------- bench N>1

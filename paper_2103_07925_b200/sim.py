@@ -292,20 +292,40 @@ class Simulation:
     def record_doubles(self):
         return int(self._fn("record_doubles")())
 
-    def record_pack(self, ids):
-        ids = np.ascontiguousarray(ids, np.uint32)
-        recs = np.zeros((len(ids), self.record_doubles()))
-        self._check(self._fn("record_pack")(self._h, ids.ctypes.data_as(C.POINTER(C.c_uint32)), len(ids),
-                                            recs.ctypes.data_as(C.POINTER(C.c_double))), "record_pack")
-        return recs
+    @staticmethod
+    def _ptr(a):
+        """Address of a C-contiguous numpy array or torch tensor (host or device)."""
+        return C.c_void_p(a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data)
+
+    def record_pack(self, ids, out=None):
+        """Records (sphg.h) of the particles with local ids `ids` -> (m, record_doubles) float64; ids / out
+        may be numpy arrays or torch tensors (uint32 / int32 ids; device tensors stay on the device)."""
+        if not hasattr(ids, "data_ptr"):
+            ids = np.ascontiguousarray(ids, np.uint32)
+        if out is None:
+            out = np.zeros((len(ids), self.record_doubles()))
+        self._check(self._fn("record_pack")(self._h, self._ptr(ids), len(ids), self._ptr(out)), "record_pack")
+        return out
 
     def record_unpack(self, ids, recs, keep_position=True):
-        ids = np.ascontiguousarray(ids, np.uint32)
-        recs = np.ascontiguousarray(recs, np.float64)
-        assert recs.shape == (len(ids), self.record_doubles())
-        self._check(self._fn("record_unpack")(self._h, ids.ctypes.data_as(C.POINTER(C.c_uint32)), len(ids),
-                                              recs.ctypes.data_as(C.POINTER(C.c_double)), int(bool(keep_position))),
-                    "record_unpack")
+        if not hasattr(ids, "data_ptr"):
+            ids = np.ascontiguousarray(ids, np.uint32)
+            recs = np.ascontiguousarray(recs, np.float64)
+            assert recs.shape == (len(ids), self.record_doubles())
+        self._check(self._fn("record_unpack")(self._h, self._ptr(ids), len(ids), self._ptr(recs),
+                                              int(bool(keep_position))), "record_unpack")
+
+    def upload_records(self, recs, n_owned, bodies):
+        """Replace the whole store by `recs` (the first n_owned owned, the rest ghosts) and the body table;
+        recs may be a device tensor (no host round trip)."""
+        n = int(recs.shape[0])
+        if not hasattr(recs, "data_ptr"):
+            recs = np.ascontiguousarray(recs, np.float64)
+        bodies = np.ascontiguousarray(bodies, BODY_DTYPE)
+        self._check(self._fn("upload_records")(self._h, n, int(n_owned), self._ptr(recs) if n else None,
+                                               self._ptr(bodies) if len(bodies) else None, len(bodies)),
+                    "upload_records")
+        self.n = n
 
     def replace_bodies(self, bodies):
         bodies = np.ascontiguousarray(bodies, BODY_DTYPE)
