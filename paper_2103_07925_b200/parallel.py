@@ -238,6 +238,7 @@ class DistributedSimulation:
         self._nb = nb
         if self._cb is None:
             self._cb = abi.EXCHANGE_FN(self._exchange_cb)  # keep the thunk alive with the context
+        self._sync_engine_dev()  # the zero-filled buffers before the library writes into them
         e._check(f("set_exchange")(e._h, self._cb, None), "set_exchange")
 
     def _exchange_cb(self, phase, stream, user):
@@ -605,6 +606,11 @@ class DistributedSimulation:
             torch.cuda.current_stream(self.dev).synchronize()
         return {q: t.to(self.edev) for q, t in recv.items()}
 
+    def _sync_engine_dev(self):
+        """Device tensors made on torch's stream are read on the library's own stream: finish them first."""
+        if self.edev.type == "cuda":
+            torch.cuda.current_stream(self.edev).synchronize()
+
     def repartition(self):
         """Particle migration, device-resident: each rank packs its owned particles as
         engine records (sphg_record_pack into a device tensor), sends the ones that left its box to their
@@ -615,7 +621,9 @@ class DistributedSimulation:
         R = e.record_doubles()
         n_own = self.n_own
         ids = torch.arange(n_own, dtype=torch.int32, device=self.edev)
-        recs = e.record_pack(ids, out=torch.empty((n_own, R), dtype=torch.float64, device=self.edev))
+        out = torch.empty((n_own, R), dtype=torch.float64, device=self.edev)
+        self._sync_engine_dev()
+        recs = e.record_pack(ids, out=out)  # complete on return (the library syncs its stream)
         gid = torch.from_numpy(self.gids[:n_own].astype(np.float64)).to(self.edev)  # exact below 2^53
         full = torch.cat([gid[:, None], recs], dim=1)
         new_owner = self._owner_t(full[:, 1:4])
@@ -643,7 +651,9 @@ class DistributedSimulation:
         e = self.engine
         self.gids = allrec[:, 0].to(torch.int64).cpu().numpy()
         self.n_own = n_own
-        e.upload_records(allrec[:, 1:].contiguous(), n_own, bodies)
+        recs = allrec[:, 1:].contiguous()
+        self._sync_engine_dev()
+        e.upload_records(recs, n_own, bodies)
         pos_own = allrec[:n_own, 1:4]
         self.peers = []
         for q in range(self.world):
