@@ -763,8 +763,16 @@ int one_step(sphg_ctx* h) {
   if (!spec || rebuild) forces();
   h->mid_step = false;
   if (c.P.transitions != 0) {
+    float ms = 0.f;
+    if (c.timing) SPHG_CUDA_CHECK(cudaEventRecord(c.ev[0], c.stream));
     rc = launch_transitions(c);
     if (rc) return fail(h, rc, c.err);
+    if (c.timing) {
+      SPHG_CUDA_CHECK(cudaEventRecord(c.ev[1], c.stream));
+      SPHG_CUDA_CHECK(cudaEventSynchronize(c.ev[1]));
+      SPHG_CUDA_CHECK(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+      c.stage_ms[SPHG_STAGE_TRANSITIONS] += ms;
+    }
   }
   c.steps++;
   return check_dt(h);

@@ -753,11 +753,11 @@ static void launch_kind_lists(Ctx& c) {
   c.launches += 2;
 }
 
-void launch_rigid_index(Ctx& c) {
+void launch_rigid_index(Ctx& c, bool kinds_changed) {
   const size_t n = c.n;
   cudaStream_t s = c.stream;
   if (n == 0) return;
-  launch_kind_lists(c);
+  if (kinds_changed) launch_kind_lists(c);  // fluid / non-fluid lists (a split only moves body ids)
   c.ridx.alloc(std::max<size_t>(n, 1));
   c.body_start.alloc(2 * std::max<size_t>(c.nb, 1));
   uint32_t* flag = c.vals_alt.p;  // scratch

@@ -13,6 +13,7 @@
 //  * affected bodies: reduce_mass_quantities (chi recomputed), u_k = u'_k + w x (r_k - r'_k),
 //    members follow the rigid motion, then reduce_force_torque for all bodies.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -362,15 +363,18 @@ void grow_bodies(Ctx& c, size_t need) {
 // rebuild on transitions either.  Warp per row; rows whose partition is still valid are skipped.
 constexpr int kRepartWarps = 8;
 constexpr int kRepartMaxCap = 1024;
+// list != nullptr: only the listed rows (k_mark_rows: the rows of the changed particles and of their
+// neighbours — the candidate lists are symmetric without ghosts)
 template <int M>
 __global__ void __launch_bounds__(32 * kRepartWarps) k_repartition_rows(const uint32_t* __restrict__ kmd,
                                                                          uint32_t* __restrict__ nbr,
                                                                          uint32_t* __restrict__ cnt, int cap,
-                                                                         size_t n) {
+                                                                         size_t n, const uint32_t* __restrict__ list) {
   __shared__ uint32_t buf[kRepartWarps][kRepartMaxCap];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const size_t i = (size_t)blockIdx.x * kRepartWarps + wib;
-  if (i >= n) return;  // warp-uniform
+  const size_t w = (size_t)blockIdx.x * kRepartWarps + wib;
+  if (w >= n) return;  // warp-uniform
+  const size_t i = list ? list[w] : w;
   const uint32_t c = cnt[i];
   const uint32_t tot = cnt_total(c), nf_old = cnt_fluid(c);
   uint32_t* row = nbr + i * (size_t)cap;
@@ -567,19 +571,64 @@ void record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_
   c.launches++;
 }
 
+// rows whose fluid / non-fluid partition a batch can invalidate: the changed particles' own rows and the
+// rows of their neighbours (= the entries of their rows)
+static __global__ void k_mark_rows(const uint32_t* __restrict__ ev, size_t n, NbrList L, int img_mode,
+                                   uint32_t* __restrict__ dirty) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || ev[k] == 0u) return;
+  dirty[k] = 1u;
+  const uint32_t nn = cnt_total(L.cnt[k]);
+  const uint32_t* row = L.nbr + k * L.cap;
+  for (uint32_t q = 0; q < nn; ++q) dirty[img_mode == kImgCode ? (row[q] & kIdxMask) : row[q]] = 1u;
+}
+
+static __global__ void k_compact_flagged(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                                         size_t n, uint32_t* __restrict__ out) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n && flag[k]) out[pos[k]] = (uint32_t)k;
+}
+
+static void repartition_launch(Ctx& c, size_t m, const uint32_t* list) {
+  const unsigned blocks = (unsigned)((m + kRepartWarps - 1) / kRepartWarps);
+  switch (c.P.img_mode) {
+    case kImgNone: k_repartition_rows<kImgNone><<<blocks, 32 * kRepartWarps, 0, c.stream>>>(c.cur.kmd.p, c.nbr.p, c.cnt.p, c.cap, m, list); break;
+    case kImgCode: k_repartition_rows<kImgCode><<<blocks, 32 * kRepartWarps, 0, c.stream>>>(c.cur.kmd.p, c.nbr.p, c.cnt.p, c.cap, m, list); break;
+    default: k_repartition_rows<kImgMin><<<blocks, 32 * kRepartWarps, 0, c.stream>>>(c.cur.kmd.p, c.nbr.p, c.cnt.p, c.cap, m, list); break;
+  }
+  c.launches++;
+}
+
 void launch_repartition_rows(Ctx& c) {
   if (c.n == 0) return;
   if (c.cap > kRepartMaxCap) {  // very wide rows: rebuild instead
     c.built = false;
     return;
   }
-  const unsigned blocks = (unsigned)((c.n + kRepartWarps - 1) / kRepartWarps);
-  switch (c.P.img_mode) {
-    case kImgNone: k_repartition_rows<kImgNone><<<blocks, 32 * kRepartWarps, 0, c.stream>>>(c.cur.kmd.p, c.nbr.p, c.cnt.p, c.cap, c.n); break;
-    case kImgCode: k_repartition_rows<kImgCode><<<blocks, 32 * kRepartWarps, 0, c.stream>>>(c.cur.kmd.p, c.nbr.p, c.cnt.p, c.cap, c.n); break;
-    default: k_repartition_rows<kImgMin><<<blocks, 32 * kRepartWarps, 0, c.stream>>>(c.cur.kmd.p, c.nbr.p, c.cnt.p, c.cap, c.n); break;
+  repartition_launch(c, c.n, nullptr);
+}
+
+// after a single-rank batch: only the rows its kind changes can touch (symmetric lists, no ghosts)
+static void repartition_changed_rows(Ctx& c) {
+  const size_t n = c.n;
+  if (n == 0) return;
+  static const bool all_rows = std::getenv("SPHG_REPART_ALL") && std::atoi(std::getenv("SPHG_REPART_ALL")) != 0;
+  if (c.cap > kRepartMaxCap || c.nghost || all_rows) {
+    launch_repartition_rows(c);
+    return;
   }
+  uint32_t* dirty = c.vals_alt.p;
+  uint32_t* pos = c.vals.p;
+  SPHG_CUDA_CHECK(cudaMemsetAsync(dirty, 0, n * sizeof(uint32_t), c.stream));
+  k_mark_rows<<<grid_for(n, 256), 256, 0, c.stream>>>(c.ev_flag.p, n, c.nl(), c.P.img_mode, dirty);
+  exclusive_scan_u32(dirty, pos, n, c.scan_tmp.p, c.stream, &c.launches);
+  const size_t m = (size_t)read_u32(c, pos + n - 1) + read_u32(c, dirty + n - 1);
   c.launches++;
+  if (m == 0) return;
+  c.rec_ids.alloc(m);
+  k_compact_flagged<<<grid_for(n, 256), 256, 0, c.stream>>>(dirty, pos, n, c.rec_ids.p);
+  c.launches++;
+  repartition_launch(c, m, c.rec_ids.p);
 }
 
 int launch_transitions(Ctx& c) {
@@ -685,7 +734,7 @@ int launch_transitions(Ctx& c) {
                                                        gbits, c.nb);
       // old state of split products = their source body's pre-batch state (via src)
       c.nb += nsplit;
-      launch_rigid_index(c);
+      launch_rigid_index(c, false);
       c.launches += 2;
     }
   }
@@ -712,7 +761,7 @@ int launch_transitions(Ctx& c) {
   c.n_melt += nmelt;
   c.n_solid += nsolid;
   // kinds changed: the rows' fluid / non-fluid partition is stale; body ids changed: contact order
-  launch_repartition_rows(c);
+  repartition_changed_rows(c);
   if (c.built) launch_contact_order(c);
   return 0;
 }
