@@ -120,6 +120,8 @@ struct Ctx {
   DBuf<uint32_t> wrap_list;  // (index, wrap code) of the particles that crossed a periodic face this step
   // decomposed transition batches (sphg_event_*, sphg_record_*): id lists and records
   DBuf<uint32_t> rec_ids;
+  DBuf<uint32_t> group0;  // body ids at the start of a transition batch
+  DBuf<sphg_body> bodies_old;  // the body table at the start of a transition batch
   DBuf<double> rec_buf;
   // transition event log (sphg_set_event_log): device buffer of the current batch, host accumulation
   bool event_log = false;
@@ -301,7 +303,7 @@ void record_pack(Ctx& c, const uint32_t* dev_ids, size_t m, double* dev_out);
 void record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_in, int keep_position);
 void record_load(Ctx& c, const double* dev_recs, size_t n, size_t n_owned);  // whole store (sphg_upload_records)
 void launch_repartition_rows(Ctx& c);
-void launch_contact_order(Ctx& c);
+void launch_contact_order(Ctx& c, const uint32_t* list = nullptr, size_t m = 0);
 
 inline int grid_for(size_t n, int block) { return (int)((n + block - 1) / block); }
 

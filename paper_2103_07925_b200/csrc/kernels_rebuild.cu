@@ -578,22 +578,29 @@ __global__ void __launch_bounds__(32 * kConWarps) k_contact_order(const uint32_t
 
 }  // namespace
 
-void launch_contact_order(Ctx& c) {
+// list = nullptr: every rigid particle (ridx); else the m listed rigid particles (a transition batch's
+// changed neighbourhood)
+void launch_contact_order(Ctx& c, const uint32_t* list, size_t m) {
   if (c.nrigid == 0) return;
   c.ncon.alloc(std::max<size_t>(c.n, 1));
-  const unsigned blocks = (unsigned)((c.nrigid + kConWarps - 1) / kConWarps);
+  if (!list) {
+    list = c.ridx.p;
+    m = c.nrigid;
+  }
+  if (m == 0) return;
+  const unsigned blocks = (unsigned)((m + kConWarps - 1) / kConWarps);
   switch (c.P.img_mode) {
     case kImgNone:
       k_contact_order<kImgNone><<<blocks, 32 * kConWarps, 0, c.stream>>>(c.cur.kmd.p, c.cur.group.p, c.nbr.p, c.cnt.p,
-                                                                          c.cap, c.ridx.p, c.nrigid, c.ncon.p);
+                                                                          c.cap, list, m, c.ncon.p);
       break;
     case kImgCode:
       k_contact_order<kImgCode><<<blocks, 32 * kConWarps, 0, c.stream>>>(c.cur.kmd.p, c.cur.group.p, c.nbr.p, c.cnt.p,
-                                                                          c.cap, c.ridx.p, c.nrigid, c.ncon.p);
+                                                                          c.cap, list, m, c.ncon.p);
       break;
     default:
       k_contact_order<kImgMin><<<blocks, 32 * kConWarps, 0, c.stream>>>(c.cur.kmd.p, c.cur.group.p, c.nbr.p, c.cnt.p,
-                                                                         c.cap, c.ridx.p, c.nrigid, c.ncon.p);
+                                                                         c.cap, list, m, c.ncon.p);
       break;
   }
   c.launches++;

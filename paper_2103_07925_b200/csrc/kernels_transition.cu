@@ -573,10 +573,11 @@ void record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_
 
 // rows whose fluid / non-fluid partition a batch can invalidate: the changed particles' own rows and the
 // rows of their neighbours (= the entries of their rows)
-static __global__ void k_mark_rows(const uint32_t* __restrict__ ev, size_t n, NbrList L, int img_mode,
+static __global__ void k_mark_rows(const uint32_t* __restrict__ ev, const uint32_t* __restrict__ group,
+                                   const uint32_t* __restrict__ group0, size_t n, NbrList L, int img_mode,
                                    uint32_t* __restrict__ dirty) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n || ev[k] == 0u) return;
+  if (k >= n || (ev[k] == 0u && group[k] == group0[k])) return;
   dirty[k] = 1u;
   const uint32_t nn = cnt_total(L.cnt[k]);
   const uint32_t* row = L.nbr + k * L.cap;
@@ -587,6 +588,18 @@ static __global__ void k_compact_flagged(const uint32_t* __restrict__ flag, cons
                                          size_t n, uint32_t* __restrict__ out) {
   const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n && flag[k]) out[pos[k]] = (uint32_t)k;
+}
+
+static __global__ void k_rigid_of(const uint32_t* __restrict__ list, size_t m, const uint32_t* __restrict__ kmd,
+                                  uint32_t* __restrict__ flag) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < m) flag[e] = kind_of(kmd[list[e]]) == SPHG_RIGID ? 1u : 0u;
+}
+
+static __global__ void k_compact_list(const uint32_t* __restrict__ list, const uint32_t* __restrict__ flag,
+                                      const uint32_t* __restrict__ pos, size_t m, uint32_t* __restrict__ out) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < m && flag[e]) out[pos[e]] = list[e];
 }
 
 static void repartition_launch(Ctx& c, size_t m, const uint32_t* list) {
@@ -608,27 +621,45 @@ void launch_repartition_rows(Ctx& c) {
   repartition_launch(c, c.n, nullptr);
 }
 
-// after a single-rank batch: only the rows its kind changes can touch (symmetric lists, no ghosts)
-static void repartition_changed_rows(Ctx& c) {
+// After a single-rank batch only the rows of the particles whose kind or body changed, and of their
+// neighbours (the candidate lists are symmetric without ghosts), can hold a stale fluid / non-fluid
+// partition or contact order: re-partition those rows and re-order the rigid ones among them.
+// group0 = the body ids before the batch.
+static void refresh_changed_rows(Ctx& c, const uint32_t* group0) {
   const size_t n = c.n;
   if (n == 0) return;
   static const bool all_rows = std::getenv("SPHG_REPART_ALL") && std::atoi(std::getenv("SPHG_REPART_ALL")) != 0;
-  if (c.cap > kRepartMaxCap || c.nghost || all_rows) {
+  if (c.cap > kRepartMaxCap || c.nghost || all_rows || !group0) {
     launch_repartition_rows(c);
+    if (c.built) launch_contact_order(c);
     return;
   }
   uint32_t* dirty = c.vals_alt.p;
   uint32_t* pos = c.vals.p;
   SPHG_CUDA_CHECK(cudaMemsetAsync(dirty, 0, n * sizeof(uint32_t), c.stream));
-  k_mark_rows<<<grid_for(n, 256), 256, 0, c.stream>>>(c.ev_flag.p, n, c.nl(), c.P.img_mode, dirty);
+  k_mark_rows<<<grid_for(n, 256), 256, 0, c.stream>>>(c.ev_flag.p, c.cur.group.p, group0, n, c.nl(), c.P.img_mode,
+                                                       dirty);
   exclusive_scan_u32(dirty, pos, n, c.scan_tmp.p, c.stream, &c.launches);
   const size_t m = (size_t)read_u32(c, pos + n - 1) + read_u32(c, dirty + n - 1);
   c.launches++;
   if (m == 0) return;
-  c.rec_ids.alloc(m);
-  k_compact_flagged<<<grid_for(n, 256), 256, 0, c.stream>>>(dirty, pos, n, c.rec_ids.p);
+  c.rec_ids.alloc(2 * m + 1);
+  uint32_t* rows = c.rec_ids.p;
+  k_compact_flagged<<<grid_for(n, 256), 256, 0, c.stream>>>(dirty, pos, n, rows);
   c.launches++;
-  repartition_launch(c, m, c.rec_ids.p);
+  repartition_launch(c, m, rows);
+  if (!c.built || c.nrigid == 0) return;
+  // the rigid ones among them: contact candidates first again
+  uint32_t* rflag = dirty;  // reused: m <= n
+  uint32_t* rpos = pos;
+  k_rigid_of<<<grid_for(m, 256), 256, 0, c.stream>>>(rows, m, c.cur.kmd.p, rflag);
+  exclusive_scan_u32(rflag, rpos, m, c.scan_tmp.p, c.stream, &c.launches);
+  const size_t mr = (size_t)read_u32(c, rpos + m - 1) + read_u32(c, rflag + m - 1);
+  if (mr == 0) return;
+  uint32_t* rl = rows + m;
+  k_compact_list<<<grid_for(m, 256), 256, 0, c.stream>>>(rows, rflag, rpos, m, rl);
+  c.launches += 2;
+  launch_contact_order(c, rl, mr);
 }
 
 int launch_transitions(Ctx& c) {
@@ -641,11 +672,15 @@ int launch_transitions(Ctx& c) {
   const uint32_t nsolid = read_u32(c, &c.dflags->pad[0]);
   if (nmelt == 0 && nsolid == 0) return 0;
   if (!c.built) launch_rebuild(c);
+  c.group0.alloc(n);  // body ids before the batch (refresh_changed_rows)
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(c.group0.p, c.cur.group.p, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
   const size_t nb0 = c.nb;
   // capacity: spawned + split products are bounded by the rigid count after the batch
   grow_bodies(c, nb0 + nsolid + c.nrigid + nsolid + 1);
   const size_t cap = c.bodies_cap;
-  DBuf<sphg_body> old;
+  // the pre-batch body table (u'_k, r'_k): a grow-only context buffer — a per-batch cudaMalloc / cudaFree
+  // of the table's capacity (~1 GB at C4's bound) would synchronise the device and cost milliseconds
+  DBuf<sphg_body>& old = c.bodies_old;
   old.alloc(cap);
   c.tscratch.alloc(3 * cap + 3 * (size_t)std::max<uint32_t>(nsolid, 1));
   uint32_t* bmask = c.tscratch.p;
@@ -701,7 +736,9 @@ int launch_transitions(Ctx& c) {
     SPHG_CUDA_CHECK(cudaMemsetAsync(c.label_flags.p, 0, 4 * sizeof(uint32_t), s));
     k_label_init<<<grid_for(n, 256), 256, 0, s>>>(c.cur, n, blost, c.label.p, c.label_list.p, c.label_flags.p + 3);
     const double adj2 = (1.5 * c.P.dx) * (1.5 * c.P.dx);
-    // one cooperative launch: as many blocks as can be co-resident
+    // one cooperative launch: as many blocks as the labelled particles need (each sweep ends in two grid
+    // barriers, whose cost grows with the grid), at most as many as can be co-resident
+    const uint32_t nlab = read_u32(c, c.label_flags.p + 3);
     static int coop_blocks = 0;
     if (!coop_blocks) {
       int per_sm = 0, sms = 0;
@@ -718,7 +755,8 @@ int launch_transitions(Ctx& c) {
     double a2 = adj2;
     uint32_t* fp = c.label_flags.p;
     void* args[] = {&Pv, &Dv, &Lv, &lp, &cp, &labp, &a2, &fp};
-    SPHG_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_label_coop, dim3(coop_blocks), dim3(256), args, 0, s));
+    const int blocks = std::max(1, std::min(coop_blocks, (int)((nlab + 255) / 256)));
+    SPHG_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_label_coop, dim3(blocks), dim3(256), args, 0, s));
     c.launches += 2;
     const int gbits = bits_for(n - 1);
     k_split_roots<<<grid_for(n, 256), 256, 0, s>>>(c.cur, n, c.label.p, c.ridx.p, c.body_start.p, gbits, c.keys.p,
@@ -750,7 +788,6 @@ int launch_transitions(Ctx& c) {
   // 5. force/torque with the new membership
   launch_bodies(c);
   host_sync(c, s);
-  old.free();
   if (elog) {  // drain this batch's events to the host, ordered by gid (each particle once per batch)
     const size_t m = (size_t)nmelt + nsolid;
     std::vector<sphg_event> ev(m);
@@ -761,8 +798,7 @@ int launch_transitions(Ctx& c) {
   c.n_melt += nmelt;
   c.n_solid += nsolid;
   // kinds changed: the rows' fluid / non-fluid partition is stale; body ids changed: contact order
-  repartition_changed_rows(c);
-  if (c.built) launch_contact_order(c);
+  refresh_changed_rows(c, c.built ? c.group0.p : nullptr);
   return 0;
 }
 

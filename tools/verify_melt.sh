@@ -1,2 +1,3 @@
-timeout 900 python tools/bench_melt.py 20 > gpurun_out/melt2.log 2>&1; tail -2 gpurun_out/melt2.log
-SPHG_REPART_ALL=1 timeout 900 python tools/bench_melt.py 20 > gpurun_out/melt3.log 2>&1; tail -2 gpurun_out/melt3.log
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/melt_l_a.csv python tools/melt_steps.py > gpurun_out/melt_ncu_a.log 2>&1
+SPHG_REPART_ALL=1 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/melt_l_b.csv python tools/melt_steps.py > gpurun_out/melt_ncu_b.log 2>&1
+echo done
