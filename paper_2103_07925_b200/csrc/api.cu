@@ -1947,6 +1947,7 @@ void sphg_destroy(sphg_ctx* h) {
   c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();
   c.label_list.free(); c.label_flags.free(); c.ev_log.free(); c.ev_count.free();
   c.rec_ids.free(); c.rec_buf.free(); c.group0.free(); c.bodies_old.free(); c.wrap_list.free(); c.state_buf.free();
+  c.label_adj.free();
   c.fidx.free(); c.widx.free(); c.ncon.free(); c.brick_buf.free(); c.scan_cells.free(); c.dl_buf.free(); c.idx_of_gid.free(); c.body_buf.free();
   for (auto& b : c.halo_ids) b.free();
   if (c.dflags) cudaFree(c.dflags);

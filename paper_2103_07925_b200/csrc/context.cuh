@@ -122,6 +122,7 @@ struct Ctx {
   DBuf<uint32_t> rec_ids;
   DBuf<uint32_t> group0;  // body ids at the start of a transition batch
   DBuf<sphg_body> bodies_old;  // the body table at the start of a transition batch
+  DBuf<uint32_t> label_adj;    // labelled particles' same-body adjacency (split_disconnected_bodies)
   DBuf<double> rec_buf;
   // transition event log (sphg_set_event_log): device buffer of the current batch, host accumulation
   bool event_log = false;

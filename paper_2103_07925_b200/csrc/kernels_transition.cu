@@ -223,11 +223,56 @@ __device__ __forceinline__ bool label_relax(const DevParams& P, const Particles&
   return false;
 }
 
+// The adjacency of each labelled particle (same-body rigid neighbours within 1.5 dx: at most 18 on the
+// lattice the bodies are cut from) extracted once from its row, so a sweep reads ~18 labels instead of
+// re-testing the ~120 row entries; nadj > kAdjMax marks a particle the sweeps relax from its row.
+constexpr uint32_t kAdjMax = 32;
+__global__ void k_label_adj(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                            const uint32_t* __restrict__ list, const uint32_t* __restrict__ count, double adj2,
+                            uint32_t* __restrict__ adj, uint32_t* __restrict__ nadj) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= *count) return;
+  const uint32_t i = list[e];
+  const uint32_t body = D.group.p[i];
+  const double4 pi = D.G0.p[i];
+  const uint32_t nn = cnt_total(L.cnt[i]);
+  const uint32_t* row = L.nbr + (size_t)i * L.cap;
+  uint32_t c = 0;
+  for (uint32_t k = 0; k < nn; ++k) {
+    const uint32_t j = P.img_mode == kImgCode ? (row[k] & kIdxMask) : row[k];
+    if (kind_of(D.kmd.p[j]) != SPHG_RIGID || D.group.p[j] != body) continue;
+    const double4 pj = D.G0.p[j];
+    if (r2_exact(mimg3(P, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z)) > adj2) continue;
+    if (c < kAdjMax) adj[e * kAdjMax + c] = j;
+    ++c;
+  }
+  nadj[e] = c;
+}
+
+// one relaxation of labelled particle e: the minimum over its adjacency, then a pointer jump through the
+// particle whose gid is that minimum (it is in the same component and its label is <= its gid)
+__device__ __forceinline__ bool label_relax_adj(const DevParams& P, const Particles& D, const NbrList& L,
+                                                uint32_t* label, double adj2, uint32_t i, uint32_t e,
+                                                const uint32_t* adj, const uint32_t* nadj, const uint32_t* idx) {
+  const uint32_t na = nadj[e];
+  if (na > kAdjMax) return label_relax(P, D, L, label, adj2, i);
+  const uint32_t l = label[i];
+  uint32_t best = l;
+  for (uint32_t k = 0; k < na; ++k) best = min(best, label[adj[(size_t)e * kAdjMax + k]]);
+  best = min(best, label[idx[best]]);
+  if (best < l) {
+    atomicMin(&label[i], best);
+    return true;
+  }
+  return false;
+}
+
 // cooperative: grid-stride sweeps over the list, grid barrier, stop when a sweep changed nothing.
 // flags[0..1]: double-buffered "changed" words (cleared one sweep ahead); flags[2]: sweeps done
 __global__ void k_label_coop(const __grid_constant__ DevParams P, Particles D, NbrList L, const uint32_t* __restrict__ list,
                              const uint32_t* __restrict__ count, uint32_t* __restrict__ label, double adj2,
-                             uint32_t* __restrict__ flags) {
+                             uint32_t* __restrict__ flags, const uint32_t* __restrict__ adj,
+                             const uint32_t* __restrict__ nadj, const uint32_t* __restrict__ idx) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   const uint32_t m = *count;
@@ -240,7 +285,8 @@ __global__ void k_label_coop(const __grid_constant__ DevParams P, Particles D, N
     uint32_t* changed = flags + (sweep & 1u);
     if (tid == 0) flags[(sweep + 1) & 1u] = 0u;  // the next sweep's word; nobody reads it this sweep
     bool any = false;
-    for (size_t e = tid; e < m; e += stride) any |= label_relax(P, D, L, label, adj2, list[e]);
+    for (size_t e = tid; e < m; e += stride)
+      any |= label_relax_adj(P, D, L, label, adj2, list[e], (uint32_t)e, adj, nadj, idx);
     if (any) atomicOr(changed, 1u);
     grid.sync();
     const uint32_t c = *reinterpret_cast<volatile uint32_t*>(changed);
@@ -754,7 +800,15 @@ int launch_transitions(Ctx& c) {
     uint32_t* labp = c.label.p;
     double a2 = adj2;
     uint32_t* fp = c.label_flags.p;
-    void* args[] = {&Pv, &Dv, &Lv, &lp, &cp, &labp, &a2, &fp};
+    c.label_adj.alloc((size_t)std::max<uint32_t>(nlab, 1) * (kAdjMax + 1));
+    uint32_t* adjp = c.label_adj.p;
+    uint32_t* nadjp = adjp + (size_t)std::max<uint32_t>(nlab, 1) * kAdjMax;
+    const uint32_t* idxp = c.idx_of_gid.p;
+    if (nlab) {
+      k_label_adj<<<grid_for(nlab, 128), 128, 0, s>>>(c.P, c.cur, c.nl(), lp, cp, adj2, adjp, nadjp);
+      c.launches++;
+    }
+    void* args[] = {&Pv, &Dv, &Lv, &lp, &cp, &labp, &a2, &fp, &adjp, &nadjp, &idxp};
     const int blocks = std::max(1, std::min(coop_blocks, (int)((nlab + 255) / 256)));
     SPHG_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_label_coop, dim3(blocks), dim3(256), args, 0, s));
     c.launches += 2;
