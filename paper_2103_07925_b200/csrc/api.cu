@@ -1854,6 +1854,18 @@ int sphg_upload_records(sphg_ctx* h, size_t n, size_t n_owned, const double* rec
     if (n >= (size_t)UINT32_MAX) return fail(h, SPHG_ERR_CONFIG, "too many particles for 32-bit gids");
     if (n_owned > n) return fail(h, SPHG_ERR_CONFIG, "upload_records: n_owned > n");
     host_sync(c, c.stream);
+    // records on the device and validated before anything of the context changes
+    const double* dr = recs;
+    if (!is_device_ptr(recs) && n) {
+      c.rec_buf.alloc(n * kRecordDoubles);
+      SPHG_CUDA_CHECK(cudaMemcpyAsync(c.rec_buf.p, recs, n * kRecordDoubles * sizeof(double), cudaMemcpyDefault,
+                                      c.stream));
+      dr = c.rec_buf.p;
+    }
+    const uint32_t bad = record_check(c, dr, n, nb);
+    if (bad != 0xffffffffu)
+      return fail(h, SPHG_ERR_CONFIG, "upload_records: record " + std::to_string(bad) +
+                                          " has an invalid kind / material / body id");
     destroy_graphs(c);
     c.nghost = n - n_owned;
     c.disp_since_partition = 0.0;
@@ -1862,13 +1874,6 @@ int sphg_upload_records(sphg_ctx* h, size_t n, size_t n_owned, const double* rec
     c.final_pending = false;
     iota_gid(c);
     build_idx_of_gid(c);
-    const double* dr = recs;
-    if (!is_device_ptr(recs) && n) {
-      c.rec_buf.alloc(n * kRecordDoubles);
-      SPHG_CUDA_CHECK(cudaMemcpyAsync(c.rec_buf.p, recs, n * kRecordDoubles * sizeof(double), cudaMemcpyDefault,
-                                      c.stream));
-      dr = c.rec_buf.p;
-    }
     record_load(c, dr, n, n_owned);
     c.nb = 0;
     ensure_bodies(c, nb);

@@ -303,6 +303,7 @@ constexpr int kRecordDoubles = 44;
 void record_pack(Ctx& c, const uint32_t* dev_ids, size_t m, double* dev_out);
 void record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_in, int keep_position);
 void record_load(Ctx& c, const double* dev_recs, size_t n, size_t n_owned);  // whole store (sphg_upload_records)
+uint32_t record_check(Ctx& c, const double* dev_recs, size_t n, size_t nb);  // first invalid record or ~0u
 void launch_repartition_rows(Ctx& c);
 void launch_contact_order(Ctx& c, const uint32_t* list = nullptr, size_t m = 0);
 

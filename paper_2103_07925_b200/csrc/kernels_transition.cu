@@ -567,7 +567,27 @@ __global__ void k_record_load(Particles D, size_t n, size_t n_owned, const doubl
   D.group.p[s] = (uint32_t)o[5];
 }
 
+// validation of records about to be loaded: kind, material and (rigid) body id in range
+__global__ void k_record_check(const double* __restrict__ in, size_t n, int n_mat, size_t nb,
+                               uint32_t* __restrict__ bad) {
+  const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double* o = in + s * kRecordDoubles;
+  const bool ok = o[3] >= 0.0 && o[3] <= 2.0 && o[4] >= 0.0 && o[4] < (double)n_mat &&
+                  (o[3] != (double)SPHG_RIGID || (o[5] >= 0.0 && o[5] < (double)nb));
+  if (!ok) atomicMin(bad, (uint32_t)s);
+}
+
 }  // namespace
+
+uint32_t record_check(Ctx& c, const double* dev_recs, size_t n, size_t nb) {
+  if (n == 0) return 0xffffffffu;
+  c.label_flags.alloc(4);
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.label_flags.p + 2, 0xff, sizeof(uint32_t), c.stream));
+  k_record_check<<<grid_for(n, 256), 256, 0, c.stream>>>(dev_recs, n, c.params.n_mat, nb, c.label_flags.p + 2);
+  c.launches++;
+  return read_u32(c, c.label_flags.p + 2);
+}
 
 void record_load(Ctx& c, const double* dev_recs, size_t n, size_t n_owned) {
   if (n == 0) return;

@@ -197,3 +197,40 @@ def test_bench_two_ranks_line(tmp_path):
     assert d["roofline"]["bound"] == "fp64" and 0 < d["roofline"]["frac"] < 1
     assert d["config"]["imbalance"] < 0.2 and sum(d["config"]["owned_per_rank"]) == d["config"]["particles"]
     assert d["cpu_baseline"]["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+
+
+def test_upload_records_roundtrip_and_validation():
+    """sphg_record_pack of a whole store -> sphg_upload_records into a fresh context gives the same state
+    (download bit-identical) and the same next step; a record with an invalid body id is refused with code 2
+    and leaves the context unchanged."""
+    import torch
+    from paper_2103_07925_b200 import scenarios, Simulation
+    from paper_2103_07925_b200.sim import SPHError
+    sc = scenarios.config1(nside=16, n_spheres=2, r_range=(3.0, 3.0), seed=5)
+    a = Simulation(sc.params)
+    a.upload(sc.store, sc.bodies)
+    a.initialize()
+    a.step(2)
+    ids = torch.arange(a.n, dtype=torch.int32, device="cuda")
+    recs = a.record_pack(ids, out=torch.empty((a.n, a.record_doubles()), dtype=torch.float64, device="cuda"))
+    _, bodies = a.download()
+    b = Simulation(sc.params)
+    b.upload(sc.store, sc.bodies)
+    torch.cuda.synchronize()
+    b.upload_records(recs, a.n, bodies)
+    for e in (a, b):
+        e.step(1)
+    ga, ba = a.download()
+    gb, bb = b.download()
+    for f in ("pos", "vel", "density", "pressure", "acc", "force", "kind", "group"):
+        assert np.array_equal(getattr(ga, f), getattr(gb, f)), f
+    assert np.array_equal(ba["com"], bb["com"])
+    bad = recs.clone()
+    rg = np.nonzero(ga.kind == 1)[0][0]
+    bad[rg, 5] = 1e6  # body id out of range
+    torch.cuda.synchronize()
+    with pytest.raises(SPHError) as ei:
+        b.upload_records(bad, a.n, bodies)
+    assert ei.value.code == 2 and "invalid" in str(ei.value)
+    g2, _ = b.download()
+    assert np.array_equal(g2.pos, gb.pos)
