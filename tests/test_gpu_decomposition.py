@@ -211,6 +211,7 @@ def test_upload_records_roundtrip_and_validation():
     a.upload(sc.store, sc.bodies)
     a.initialize()
     a.step(2)
+    a.build_pairs()  # storage order and lists from the current positions, as the reloaded context will build
     ids = torch.arange(a.n, dtype=torch.int32, device="cuda")
     recs = a.record_pack(ids, out=torch.empty((a.n, a.record_doubles()), dtype=torch.float64, device="cuda"))
     _, bodies = a.download()
