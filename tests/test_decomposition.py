@@ -272,3 +272,22 @@ def _worker1(rank, world, port, out):
     if rank == 0:
         np.savez(out, pos=g.pos, acc=g.acc, density=g.density, force=g.force, bforce=b["force"], btorque=b["torque"])
     dist.destroy_process_group()
+
+
+def test_device_migration_geometry_matches_host():
+    """The tensor forms used by the device-resident migration (owner of a position, ghost-shell membership
+    with periodic images) give exactly the numpy Grid's answers."""
+    import torch
+    from paper_2103_07925_b200.parallel import DistributedSimulation
+    sc = scenarios.config1(nside=20, n_spheres=3, r_range=(3.0, 4.0), seed=11)
+    for world in (2, 4, 8):
+        ds = DistributedSimulation.__new__(DistributedSimulation)
+        ds.grid = Grid(sc.params, world)
+        pos = sc.store.pos.copy()
+        pos[:7] = [[0.0, 0.0, 0.0], [sc.params.hi[0], 0.01, 0.01], [0.016, 0.016, 0.016], [1e-12, 0.02, 0.0319],
+                   [0.0159999, 0.016, 0.0160001], [0.032, 0.032, 0.032], [0.031999999, 1e-9, 0.016]]
+        pt = torch.from_numpy(pos)
+        assert np.array_equal(ds._owner_t(pt).numpy(), ds.grid.owner_of(pos))
+        for r in range(world):
+            for w in (3.1e-3, 4.1e-3, 5.1e-3):
+                assert np.array_equal(ds._near_box_t(pt, r, w).numpy(), ds.grid.near_box(pos, r, w))
