@@ -42,6 +42,10 @@ from . import abi
 from .store import ParticleStore, VEC_FIELDS, SCALAR_FIELDS, TAG_FIELDS, BODY_DTYPE
 
 
+# SPHG_HALO_P2P=1: halos as per-peer isend / irecv pairs instead of one all_to_all_single per phase
+_HALO_P2P = os.environ.get("SPHG_HALO_P2P", "0") not in ("", "0")
+
+
 def factor_dims(nranks, extent):
     """Rank grid: repeatedly halve the currently longest per-rank extent (powers of 2),
     falling back to a 1D split along the longest axis otherwise."""
@@ -221,13 +225,24 @@ class DistributedSimulation:
         f = lambda name: getattr(e.lib, e.prefix + name)
         mk = lambda m, dt=torch.float64: torch.zeros(max(int(m), 1), dtype=dt, device=self.edev)
         self._fb = {}
+        self._a2a = {}
         for phase in (abi.HALO_STATE, abi.HALO_DENSITY, abi.HALO_WALL):
             d = f("halo_doubles")(phase)
+            # one send and one receive tensor per phase, the peers' slots at rank-ordered offsets, so a halo
+            # is a single all_to_all_single (NCCL groups the sends / receives) instead of 2 P2P ops per peer
+            ins, outs = [0] * self.world, [0] * self.world
+            for q, snd, rcv in self.peers:
+                ins[q], outs[q] = len(snd) * d, len(rcv) * d
+            send, recv = mk(sum(ins)), mk(sum(outs))
+            self._a2a[phase] = (send[: sum(ins)], recv[: sum(outs)], ins, outs)
+            so, ro = 0, 0
             for k, (q, snd, rcv) in enumerate(self.peers):
-                for slot, m in ((2 * k, len(snd)), (2 * k + 1, len(rcv))):
-                    b = mk(m * d)
+                for slot, buf, off, m in ((2 * k, send, so, len(snd) * d), (2 * k + 1, recv, ro, len(rcv) * d)):
+                    b = buf[off: off + m]
                     self._fb[(phase, slot)] = b
-                    e._check(f("halo_bind")(e._h, phase, slot, C.c_void_p(b.data_ptr())), "halo_bind")
+                    e._check(f("halo_bind")(e._h, phase, slot, C.c_void_p(buf.data_ptr() + 8 * off)), "halo_bind")
+                so += len(snd) * d
+                ro += len(rcv) * d
         self._maxw = mk(2, torch.int64)
         e._check(f("max_bind")(e._h, C.c_void_p(self._maxw.data_ptr())), "max_bind")
         nb = e.num_bodies()
@@ -263,7 +278,14 @@ class DistributedSimulation:
     def _transfer(self, phase):
         staged = self.edev != self.dev  # engine on the GPU, transport (gloo) on the host
         to_t = (lambda t: t.to(self.dev)) if staged else (lambda t: t)  # D2H in stream order (blocking)
-        if phase in (abi.HALO_STATE, abi.HALO_DENSITY, abi.HALO_WALL):
+        if phase in (abi.HALO_STATE, abi.HALO_DENSITY, abi.HALO_WALL) and not _HALO_P2P:
+            send, recv, ins, outs = self._a2a[phase]
+            st = to_t(send)
+            rt = torch.empty(recv.numel(), dtype=recv.dtype, device=self.dev) if staged else recv
+            dist.all_to_all_single(rt, st, output_split_sizes=outs, input_split_sizes=ins, group=self.group)
+            if staged:
+                recv.copy_(rt)
+        elif phase in (abi.HALO_STATE, abi.HALO_DENSITY, abi.HALO_WALL):
             d = getattr(self.engine.lib, self.engine.prefix + "halo_doubles")(phase)
             ops, recv = [], []
             for k, (q, snd, rcv) in enumerate(self.peers):
