@@ -1816,7 +1816,8 @@ int sphg_record_pack(sphg_ctx* h, const uint32_t* ids, size_t m, double* recs) {
     c.rec_buf.alloc(m * kRecordDoubles);
     // host or device buffers (unified addressing: the multi-rank driver keeps records on the device)
     SPHG_CUDA_CHECK(cudaMemcpyAsync(c.rec_ids.p, ids, m * sizeof(uint32_t), cudaMemcpyDefault, c.stream));
-    record_pack(c, c.rec_ids.p, m, c.rec_buf.p);
+    if (record_pack(c, c.rec_ids.p, m, c.rec_buf.p) != 0xffffffffu)
+      return fail(h, SPHG_ERR_CONFIG, "record_pack: id out of range");
     SPHG_CUDA_CHECK(cudaMemcpyAsync(recs, c.rec_buf.p, m * kRecordDoubles * sizeof(double), cudaMemcpyDefault,
                                     c.stream));
     host_sync(c, c.stream);
@@ -1840,7 +1841,8 @@ int sphg_record_unpack(sphg_ctx* h, const uint32_t* ids, size_t m, const double*
     SPHG_CUDA_CHECK(cudaMemcpyAsync(c.rec_ids.p, ids, m * sizeof(uint32_t), cudaMemcpyDefault, c.stream));
     SPHG_CUDA_CHECK(cudaMemcpyAsync(c.rec_buf.p, recs, m * kRecordDoubles * sizeof(double), cudaMemcpyDefault,
                                     c.stream));
-    record_unpack(c, c.rec_ids.p, m, c.rec_buf.p, keep_position);
+    if (record_unpack(c, c.rec_ids.p, m, c.rec_buf.p, keep_position) != 0xffffffffu)
+      return fail(h, SPHG_ERR_CONFIG, "record_unpack: id out of range");
     host_sync(c, c.stream);
     return SPHG_OK;
   });

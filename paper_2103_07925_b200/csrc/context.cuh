@@ -300,8 +300,8 @@ void launch_detect(Ctx& c);      // event flags (ev_flag) of the owned particles
 void event_bodies(Ctx& c, uint32_t* dev_mask);  // bodies a batch can touch (sphg_event_bodies)
 size_t event_members(Ctx& c, const uint32_t* dev_mask, size_t nb, uint32_t* dev_ids);  // unsorted local ids
 constexpr int kRecordDoubles = 44;
-void record_pack(Ctx& c, const uint32_t* dev_ids, size_t m, double* dev_out);
-void record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_in, int keep_position);
+uint32_t record_pack(Ctx& c, const uint32_t* dev_ids, size_t m, double* dev_out);  // ~0u or first bad id
+uint32_t record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_in, int keep_position);
 void record_load(Ctx& c, const double* dev_recs, size_t n, size_t n_owned);  // whole store (sphg_upload_records)
 uint32_t record_check(Ctx& c, const double* dev_recs, size_t n, size_t nb);  // first invalid record or ~0u
 void launch_repartition_rows(Ctx& c);

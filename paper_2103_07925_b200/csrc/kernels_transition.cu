@@ -493,11 +493,16 @@ __global__ void k_compact_gid(const uint32_t* __restrict__ flag, const uint32_t*
 
 // records (sphg.h): [0..2] x, [3] kind, [4] material, [5] group, [6] mass, then the device records
 __global__ void k_record_pack(Particles D, const uint32_t* __restrict__ ids, size_t m,
-                              const uint32_t* __restrict__ idx, double* __restrict__ out) {
+                              const uint32_t* __restrict__ idx, size_t n, double* __restrict__ out,
+                              uint32_t* __restrict__ bad) {
   const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= m) return;
-  const uint32_t k = idx[ids[s]];
   double* o = out + s * kRecordDoubles;
+  if (ids[s] >= n) {  // device id lists are not checked on the host: flag, never read out of bounds
+    atomicMin(bad, (uint32_t)s);
+    return;
+  }
+  const uint32_t k = idx[ids[s]];
   const uint32_t kmd = D.kmd.p[k];
   const double4 g0 = D.G0.p[k];
   o[0] = g0.x; o[1] = g0.y; o[2] = g0.z;
@@ -522,9 +527,14 @@ __global__ void k_record_pack(Particles D, const uint32_t* __restrict__ ids, siz
 }
 
 __global__ void k_record_unpack(Particles D, const uint32_t* __restrict__ ids, size_t m,
-                                const uint32_t* __restrict__ idx, const double* __restrict__ in, int keep_position) {
+                                const uint32_t* __restrict__ idx, size_t n, const double* __restrict__ in,
+                                int keep_position, uint32_t* __restrict__ bad) {
   const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= m) return;
+  if (ids[s] >= n) {
+    atomicMin(bad, (uint32_t)s);
+    return;
+  }
   const uint32_t k = idx[ids[s]];
   const double* o = in + s * kRecordDoubles;
   double4 g0 = D.G0.p[k];
@@ -625,16 +635,25 @@ size_t event_members(Ctx& c, const uint32_t* dev_mask, size_t nb, uint32_t* dev_
   return m;
 }
 
-void record_pack(Ctx& c, const uint32_t* dev_ids, size_t m, double* dev_out) {
-  if (m == 0) return;
-  k_record_pack<<<grid_for(m, 128), 128, 0, c.stream>>>(c.cur, dev_ids, m, c.idx_of_gid.p, dev_out);
+// returns the first out-of-range id's position, or ~0u
+uint32_t record_pack(Ctx& c, const uint32_t* dev_ids, size_t m, double* dev_out) {
+  if (m == 0) return 0xffffffffu;
+  c.label_flags.alloc(4);
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.label_flags.p + 2, 0xff, sizeof(uint32_t), c.stream));
+  k_record_pack<<<grid_for(m, 128), 128, 0, c.stream>>>(c.cur, dev_ids, m, c.idx_of_gid.p, c.n, dev_out,
+                                                        c.label_flags.p + 2);
   c.launches++;
+  return read_u32(c, c.label_flags.p + 2);
 }
 
-void record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_in, int keep_position) {
-  if (m == 0) return;
-  k_record_unpack<<<grid_for(m, 128), 128, 0, c.stream>>>(c.cur, dev_ids, m, c.idx_of_gid.p, dev_in, keep_position);
+uint32_t record_unpack(Ctx& c, const uint32_t* dev_ids, size_t m, const double* dev_in, int keep_position) {
+  if (m == 0) return 0xffffffffu;
+  c.label_flags.alloc(4);
+  SPHG_CUDA_CHECK(cudaMemsetAsync(c.label_flags.p + 2, 0xff, sizeof(uint32_t), c.stream));
+  k_record_unpack<<<grid_for(m, 128), 128, 0, c.stream>>>(c.cur, dev_ids, m, c.idx_of_gid.p, c.n, dev_in,
+                                                          keep_position, c.label_flags.p + 2);
   c.launches++;
+  return read_u32(c, c.label_flags.p + 2);
 }
 
 // rows whose fluid / non-fluid partition a batch can invalidate: the changed particles' own rows and the
