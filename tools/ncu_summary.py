@@ -35,7 +35,8 @@ launch = {"source": "ncu --metrics gpu__time_duration.sum --clock-control none, 
 json.dump(launch, open(os.path.join(out, f"{tag}_launches_64m.json"), "w"), indent=1)
 full = []
 for rep in (os.path.join(ROOT, "gpurun_out", f"prof_{tag}.ncu-rep"),
-            os.path.join(ROOT, "gpurun_out", f"prof_{tag}_build.ncu-rep")):  # pair kernels; the Verlet builder
+            os.path.join(ROOT, "gpurun_out", f"prof_{tag}_build.ncu-rep"),     # the Verlet builder
+            os.path.join(ROOT, "gpurun_out", f"prof_{tag}_density.ncu-rep")):  # k_density (tools/prof_density.sh)
     if not os.path.exists(rep):
         continue
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
