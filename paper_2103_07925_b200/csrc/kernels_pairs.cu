@@ -22,8 +22,6 @@
 #include <cmath>
 #include <cstring>
 
-#include <cstdlib>
-
 #include "context.cuh"
 
 namespace sphg {

@@ -819,7 +819,8 @@ void launch_rebuild(Ctx& c) {
   c.launches += 5;
   // 5. neighbour list, grown on overflow
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if (c.cap <= 0) c.cap = c.params.nlist_capacity > 0 ? c.params.nlist_capacity : 144;
+    // a multiple of 8 entries: 32-byte aligned rows (the pair kernels read them 16 bytes at a time)
+    if (c.cap <= 0) c.cap = c.params.nlist_capacity > 0 ? (c.params.nlist_capacity + 7) / 8 * 8 : 144;
     c.nbr.alloc((size_t)c.cap * n);
     SPHG_CUDA_CHECK(cudaMemsetAsync(&c.dflags->max_count, 0, sizeof(uint32_t), s));
     uint32_t mc = 0, err = 0;
