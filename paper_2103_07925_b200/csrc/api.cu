@@ -289,6 +289,9 @@ int check_flags(sphg_ctx* h, bool sync, bool copy = true) {  // copy=false: the 
     const std::string step = " at step " + std::to_string(c.steps + (h->mid_step ? 1 : 0));
     if (!(f.err & (kErrEscape | kErrCoincident)) && (f.err & kErrNaN))
       return fail(h, SPHG_ERR_RUNTIME, "non-finite state of particle " + std::to_string(f.err_gid2) + step);
+    if (f.err & kErrInvariant)  // -DSPHG_CHECKED builds only
+      return fail(h, SPHG_ERR_RUNTIME, "device invariant violated (row / index list out of bounds) at particle " +
+                                           std::to_string(f.err_gid) + step);
     std::string what = (f.err & kErrEscape) ? "escaped particle " : (f.err & kErrCoincident) ? "coincident particles at particle " : "runtime assertion at particle ";
     return fail(h, SPHG_ERR_RUNTIME, what + std::to_string(f.err_gid) + step);
   }

@@ -438,7 +438,7 @@ __device__ __forceinline__ KSum warp_merge(KSum k) {
 }
 
 // ------------------------------------------------------- device error word
-enum : uint32_t { kErrEscape = 1u, kErrCoincident = 2u, kErrNaN = 4u, kErrOverflow = 8u };
+enum : uint32_t { kErrEscape = 1u, kErrCoincident = 2u, kErrNaN = 4u, kErrOverflow = 8u, kErrInvariant = 16u };
 
 struct DevFlags {
   unsigned long long max_disp2_bits;  // atomicMax on non-negative double bits

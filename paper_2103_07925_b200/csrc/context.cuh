@@ -253,6 +253,7 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, uint32_t* t
 // kernels_rebuild.cu
 void launch_rebuild(Ctx& c);
 void launch_rigid_index(Ctx& c, bool kinds_changed = true);
+void check_structures(Ctx& c);  // -DSPHG_CHECKED: rows and index lists in bounds (kErrInvariant)
 
 // kernels_step.cu
 void launch_body_kick(Ctx& c);

@@ -576,7 +576,47 @@ __global__ void __launch_bounds__(32 * kConWarps) k_contact_order(const uint32_t
   if (lane == 0) ncon[r] = fo;
 }
 
+// Checked builds (-DSPHG_CHECKED, tools/build_variants.py; compute-sanitizer is closed on this GPU pool):
+// every row entry and index-list entry a kernel will decode is verified against the store once, when the
+// rows / lists are (re)built, so each decode site downstream reads in bounds.  gid of the first bad row.
+__global__ void k_check_rows(NbrList L, size_t n, int cap, DevFlags* __restrict__ fl) {
+  const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const uint32_t c = L.cnt[i], tot = cnt_total(c);
+  bool bad = tot > (uint32_t)cap || cnt_fluid(c) > tot;
+  const uint32_t* row = L.nbr + i * L.cap;
+  for (uint32_t k = lane; !bad && k < tot; k += 32) {
+    const uint32_t j = row[k] & kIdxMask;  // the index bits (image codes above them below 2^27 particles)
+    bad = j >= n || j == i || (n >= (1u << kIdxBits) && row[k] >= n);
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) {
+    atomicOr(&fl->err, kErrInvariant);
+    atomicMin(&fl->err_gid, (uint32_t)i);
+  }
+}
+__global__ void k_check_list(const uint32_t* __restrict__ list, size_t m, size_t n, DevFlags* __restrict__ fl) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < m && list[k] >= n) {
+    atomicOr(&fl->err, kErrInvariant);
+    atomicMin(&fl->err_gid, list[k]);
+  }
+}
+
 }  // namespace
+
+void check_structures(Ctx& c) {
+#ifdef SPHG_CHECKED
+  if (c.n == 0 || !c.built) return;
+  k_check_rows<<<grid_for(c.n * 32, 256), 256, 0, c.stream>>>(c.nl(), c.n, c.cap, c.dflags);
+  if (c.nf) k_check_list<<<grid_for(c.nf, 256), 256, 0, c.stream>>>(c.fidx.p, c.nf, c.n, c.dflags);
+  if (c.nw) k_check_list<<<grid_for(c.nw, 256), 256, 0, c.stream>>>(c.widx.p, c.nw, c.n, c.dflags);
+  if (c.nrigid) k_check_list<<<grid_for(c.nrigid, 256), 256, 0, c.stream>>>(c.ridx.p, c.nrigid, c.n, c.dflags);
+  c.launches += 4;
+#else
+  (void)c;
+#endif
+}
 
 // list = nullptr: every rigid particle (ridx); else the m listed rigid particles (a transition batch's
 // changed neighbourhood)
@@ -851,6 +891,7 @@ void launch_rebuild(Ctx& c) {
   launch_ghost_split(c);
   c.built = true;
   c.rebuilds++;
+  check_structures(c);
 }
 
 }  // namespace sphg

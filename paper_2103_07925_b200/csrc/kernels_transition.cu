@@ -892,6 +892,7 @@ int launch_transitions(Ctx& c) {
   c.n_solid += nsolid;
   // kinds changed: the rows' fluid / non-fluid partition is stale; body ids changed: contact order
   refresh_changed_rows(c, c.built ? c.group0.p : nullptr);
+  check_structures(c);
   return 0;
 }
 
