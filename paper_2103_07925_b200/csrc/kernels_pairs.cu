@@ -22,8 +22,6 @@
 #include <cmath>
 #include <cstring>
 
-#include <cstdlib>
-
 #include "context.cuh"
 
 namespace sphg {
@@ -140,131 +138,6 @@ __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevP
   reinterpret_cast<double*>(&D.G2.p[i])[3] = Mt.c2 * (rho - Mt.rho0);
   if (P.thermal) reinterpret_cast<double*>(&D.H2.p[i])[1] = V;
   if (P.diffusion) reinterpret_cast<double*>(&D.C2.p[i])[1] = V;
-}
-
-// ------------------------------------------------- density, cell-staged (SPHG_DENSITY_SMEM=1)
-// A block per home cell: the 27 neighbour cells' G0 records are copied into shared memory by the TMA
-// engine (one cp.async.bulk per cell, completion on an mbarrier; no LSU traffic), and the home cell's
-// fluid particles walk their Verlet rows as k_density does (same lanes, same order, same arithmetic:
-// the same bits) but read each neighbour record from shared memory: a lane maps an entry to its cell by
-// a forward walk over the 27 staged cell ranges (a fluid row lists its fluid part, then its non-fluid
-// part, each in the builder's cell order).  Blocks whose neighbourhood exceeds the stage read global.
-constexpr int kDsStage = 1440;  // records (45 KB)
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-template <int M>
-__global__ void __launch_bounds__(128) k_density_smem(const __grid_constant__ DevParams P, Particles D, NbrList L,
-                                                      const uint32_t* __restrict__ cstart,
-                                                      const uint32_t* __restrict__ cend) {
-  SPHG_SKIP_IF_FLAGGED(P);
-  __shared__ alignas(128) double4 rec[kDsStage];
-  __shared__ uint32_t cs[27], ce[27], off[28];
-  __shared__ alignas(8) unsigned long long bar;
-  __shared__ int staged;
-  const int64_t c = brick_to_cell(P.ncell, blockIdx.x);
-  if (c < 0) return;
-  const uint32_t h0 = cstart[c], h1 = cend[c];
-  if (h1 <= h0) return;  // block-uniform
-  const int tid = threadIdx.x;
-  if (tid < 27) {
-    const int64_t nn[3] = {P.ncell[0], P.ncell[1], P.ncell[2]};
-    const int64_t cc[3] = {c / (nn[1] * nn[2]), (c / nn[2]) % nn[1], c % nn[2]};
-    const int o[3] = {tid / 9 - 1, (tid / 3) % 3 - 1, tid % 3 - 1};
-    int64_t q[3];
-    bool ok = true;
-    for (int a = 0; a < 3; ++a) {
-      q[a] = cc[a] + o[a];
-      if (q[a] < 0 || q[a] >= nn[a]) {
-        if (!P.periodic[a]) ok = false;
-        q[a] = (q[a] + nn[a]) % nn[a];
-      }
-    }
-    const int64_t cj = (q[0] * nn[1] + q[1]) * nn[2] + q[2];
-    cs[tid] = ok ? cstart[cj] : 0u;
-    ce[tid] = ok ? cend[cj] : 0u;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    uint32_t tot = 0;
-    for (int k = 0; k < 27; ++k) {
-      off[k] = tot;
-      tot += ce[k] - cs[k];
-    }
-    off[27] = tot;
-    staged = tot <= (uint32_t)kDsStage ? 1 : 0;
-    if (staged) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(tot * 32u)
-                   : "memory");
-      for (int k = 0; k < 27; ++k)
-        if (ce[k] > cs[k])
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_u32(&rec[off[k]])),
-              "l"(D.G0.p + cs[k]), "r"((ce[k] - cs[k]) * 32u), "r"(smem_u32(&bar))
-              : "memory");
-    }
-  }
-  __syncthreads();
-  const bool st = staged != 0;
-  if (st)
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
-            smem_u32(&bar))
-        : "memory");
-  const int lane = tid & 3;
-  for (uint32_t base = h0; base < h1; base += 32) {
-    const uint32_t i = base + (uint32_t)(tid >> 2);
-    const bool active = i < h1 && kind_of(D.kmd.p[i]) == SPHG_FLUID && !is_ghost(D.kmd.p[i]);
-    double s = 0.0;
-    if (active) {
-      const double3 pi = ldpos(&D.G0.p[i]);
-      const Row R = row_of(L, i);
-      int kc = 0;  // staged cell of the lane's last entry (forward walk; reset at the non-fluid part)
-      bool other = false;
-      auto rec_of = [&](int k, uint32_t e) -> double3 {
-        const uint32_t j = nb_index<M>(e);
-        if (st) {
-          if (!other && k >= R.nf) {
-            other = true;
-            kc = 0;
-          }
-          while (kc < 27 && !(j >= cs[kc] && j < ce[kc])) ++kc;
-          if (kc < 27) return ld3(rec[off[kc] + (j - cs[kc])]);
-          kc = 0;
-        }
-        return ldpos(&D.G0.p[j]);
-      };
-      int k = lane;
-      uint32_t e0 = k < R.n ? R.at(k) : 0u;
-      uint32_t e1 = k + 4 < R.n ? R.at(k + 4) : 0u;
-      for (; k + 4 < R.n; k += 8) {
-        const uint32_t f0 = k + 8 < R.n ? R.at(k + 8) : 0u;
-        const uint32_t f1 = k + 12 < R.n ? R.at(k + 12) : 0u;
-        const double3 p0 = rec_of(k, e0);
-        const double3 p1 = rec_of(k + 4, e1);
-        s += density_term<M>(P, pi, p0, e0);
-        s += density_term<M>(P, pi, p1, e1);
-        e0 = f0;
-        e1 = f1;
-      }
-      if (k < R.n) s += density_term<M>(P, pi, rec_of(k, e0), e0);
-    }
-    s = gsum<4>(s);
-    if (active && lane == 0) {
-      const uint32_t kmd = D.kmd.p[i];
-      const DevMat& Mt = P.mat[mat_of(kmd)];
-      const double m = D.V4.p[i].w;
-      const double rho = m * (P.sigma * (66.0 + s));  // self term shape(0) = 66
-      const double V = m / rho;
-      reinterpret_cast<double*>(&D.G0.p[i])[3] = V * V;
-      reinterpret_cast<double*>(&D.G1.p[i])[3] = rho;
-      reinterpret_cast<double*>(&D.G2.p[i])[3] = Mt.c2 * (rho - Mt.rho0);
-      if (P.thermal) reinterpret_cast<double*>(&D.H2.p[i])[1] = V;
-      if (P.diffusion) reinterpret_cast<double*>(&D.C2.p[i])[1] = V;
-    }
-  }
 }
 
 // ------------------------------------------------------------------- heat
@@ -1063,17 +936,7 @@ static void launch_density_list(Ctx& c, const uint32_t* list, size_t m, cudaStre
   c.launches++;
 }
 
-void launch_density(Ctx& c) {
-  static const bool smem = std::getenv("SPHG_DENSITY_SMEM") && std::atoi(std::getenv("SPHG_DENSITY_SMEM")) != 0;
-  if (smem && c.nf && c.group_density == 0 && lanes_for(c, c.nf) == 4) {
-    const unsigned blocks = (unsigned)brick_positions(c.P.ncell);
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_density_smem<M><<<blocks, 128, 0, c.stream>>>(c.P, c.cur, c.nl(),
-                                                                                     c.cell_start.p, c.cell_end.p)));
-    c.launches++;
-    return;
-  }
-  launch_density_list(c, c.fidx.p, c.nf, c.stream);
-}
+void launch_density(Ctx& c) { launch_density_list(c, c.fidx.p, c.nf, c.stream); }
 
 // decomposed steps: the fluid list is ordered [interior | next to a ghost] (launch_ghost_split); the
 // interior part reads only owned neighbours, so it runs before the STATE halo has landed
