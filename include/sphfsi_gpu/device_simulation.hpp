@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cmath>
+#include <array>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -186,6 +187,36 @@ class DeviceSimulation {
     sphg_stats_t s;
     check(sphg_stats(ctx_, &s), "stats");
     return s;
+  }
+  /// compute_dt: cfl, viscous, body force, contact, conduction (+inf = absent)
+  std::array<double, 5> compute_dt() {
+    std::array<double, 5> lim{};
+    check(sphg_compute_dt(ctx_, lim.data()), "compute_dt");
+    return lim;
+  }
+  /// shepard_interpolate on an OutputPlan grid; NaN where no particle supports a point
+  std::vector<double> shepard_grid(const double origin[3], const double spacing[3], const int32_t dims[3],
+                                   int32_t field, uint32_t kind_mask = 1u << SPHG_FLUID) {
+    const size_t np = (size_t)dims[0] * dims[1] * dims[2];
+    std::vector<double> out(np * (field == SPHG_FIELD_VELOCITY ? 3 : 1));
+    check(sphg_shepard_grid(ctx_, origin, spacing, dims, field, kind_mask, out.data(), nullptr), "shepard_grid");
+    return out;
+  }
+  /// transition event log: enable, then drain the events recorded since the last call
+  void set_event_log(bool on) { check(sphg_set_event_log(ctx_, on ? 1 : 0), "set_event_log"); }
+  std::vector<sphg_event> transition_events() {
+    size_t n = 0;
+    check(sphg_transition_events(ctx_, nullptr, 0, &n), "transition_events");
+    std::vector<sphg_event> ev(n);
+    check(sphg_transition_events(ctx_, ev.data(), n, &n), "transition_events");
+    ev.resize(n);
+    return ev;
+  }
+  /// cell-occupancy histogram of the last rebuild: hist[k] = cells holding k particles
+  std::vector<int64_t> cell_occupancy(size_t nbins, int64_t* max_count = nullptr) {
+    std::vector<int64_t> hist(nbins);
+    check(sphg_cell_occupancy(ctx_, hist.data(), nbins, max_count), "cell_occupancy");
+    return hist;
   }
 
  private:

@@ -42,6 +42,19 @@ int main() {
   double lo = 1e300, hi = -1e300;
   for (double r : store.density) { lo = std::min(lo, r); hi = std::max(hi, r); }
   if (!(lo > 950.0 && hi < 1050.0)) { std::printf("density out of range %g %g\n", lo, hi); return 3; }
+  // the aux entry points through the adapter: occupancy (every particle in some cell), dt limits, a grid
+  int64_t mx = 0;
+  const std::vector<int64_t> hist = sim.cell_occupancy(256, &mx);
+  int64_t np = 0;
+  for (size_t k = 0; k < hist.size(); ++k) np += (int64_t)k * hist[k];
+  if (np != (int64_t)store.size() || mx <= 0) { std::printf("occupancy mismatch %lld\n", (long long)np); return 4; }
+  const auto lim = sim.compute_dt();
+  if (!(lim[0] > 0.0 && lim[0] < 1.0)) { std::printf("cfl limit %g\n", lim[0]); return 5; }
+  const double o[3] = {4e-3, 4e-3, 4e-3}, sp[3] = {4e-3, 4e-3, 4e-3};
+  const int32_t dims[3] = {2, 2, 2};
+  const std::vector<double> rho = sim.shepard_grid(o, sp, dims, SPHG_FIELD_DENSITY);
+  for (double r : rho)
+    if (!(r > 950.0 && r < 1050.0)) { std::printf("grid density %g\n", r); return 6; }
   std::printf("ok n=%zu rho_min=%.6f rho_max=%.6f steps=%lld\n", store.size(), lo, hi, (long long)sim.stats().steps);
   return 0;
 }
