@@ -291,3 +291,22 @@ def test_device_migration_geometry_matches_host():
         for r in range(world):
             for w in (3.1e-3, 4.1e-3, 5.1e-3):
                 assert np.array_equal(ds._near_box_t(pt, r, w).numpy(), ds.grid.near_box(pos, r, w))
+
+
+def test_halo_p2p_path_matches(tmp_path, oracle_mod):
+    """SPHG_HALO_P2P=1 (per-peer isend / irecv halos) gives the same state as the default all_to_all path."""
+    outs = {}
+    for flag in ("0", "1"):
+        old = os.environ.get("SPHG_HALO_P2P")
+        os.environ["SPHG_HALO_P2P"] = flag
+        try:
+            out = str(tmp_path / f"h{flag}.npz")
+            mp.spawn(_worker, args=(2, _free_port(), "c1", out), nprocs=2, join=True)
+            outs[flag] = np.load(out)
+        finally:
+            if old is None:
+                os.environ.pop("SPHG_HALO_P2P", None)
+            else:
+                os.environ["SPHG_HALO_P2P"] = old
+    for f in ("pos", "vel", "acc", "density", "force", "bforce"):
+        assert np.array_equal(outs["0"][f], outs["1"][f]), f

@@ -242,3 +242,21 @@ def test_upload_records_roundtrip_and_validation():
     assert ei.value.code == 2 and "invalid" in str(ei.value)
     g2, _ = b.download()
     assert np.array_equal(g2.pos, gb.pos)
+
+
+def test_record_ids_out_of_range_on_device():
+    """Device id lists are checked where they are read: an id >= n fails with code 2, nothing is read out
+    of bounds."""
+    import torch
+    from paper_2103_07925_b200 import scenarios, Simulation
+    from paper_2103_07925_b200.sim import SPHError
+    sc = scenarios.config1(nside=12, n_spheres=1, r_range=(2.0, 2.0), seed=3)
+    sim = Simulation(sc.params)
+    sim.upload(sc.store, sc.bodies)
+    sim.initialize()
+    ids = torch.tensor([0, 1, sim.n], dtype=torch.int32, device="cuda")
+    out = torch.empty((3, sim.record_doubles()), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    with pytest.raises(SPHError) as ei:
+        sim.record_pack(ids, out=out)
+    assert ei.value.code == 2 and "out of range" in str(ei.value)
