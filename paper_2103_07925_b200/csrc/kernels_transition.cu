@@ -388,6 +388,21 @@ uint32_t read_u32(Ctx& c, const uint32_t* p) {
   return v;
 }
 
+// two device words with one host synchronisation (a batch's readbacks are its latency)
+void read_u32x2(Ctx& c, const uint32_t* p, const uint32_t* q, uint32_t& a, uint32_t& b) {
+  uint32_t v[2] = {0, 0};
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&v[0], p, 4, cudaMemcpyDeviceToHost, c.stream));
+  SPHG_CUDA_CHECK(cudaMemcpyAsync(&v[1], q, 4, cudaMemcpyDeviceToHost, c.stream));
+  host_sync(c, c.stream);
+  a = v[0];
+  b = v[1];
+}
+uint32_t read_sum2(Ctx& c, const uint32_t* p, const uint32_t* q) {
+  uint32_t a, b;
+  read_u32x2(c, p, q, a, b);
+  return a + b;
+}
+
 void grow_bodies(Ctx& c, size_t need) {
   if (need <= c.bodies_cap && c.bodies.p) return;
   const size_t cap = std::max<size_t>(need * 2, 64);
@@ -629,7 +644,7 @@ size_t event_members(Ctx& c, const uint32_t* dev_mask, size_t nb, uint32_t* dev_
   uint32_t* pos = c.vals.p;
   k_event_member_flags<<<grid_for(n, 256), 256, 0, c.stream>>>(c.cur, n, c.ev_flag.p, dev_mask, nb, flag);
   exclusive_scan_u32(flag, pos, n, c.scan_tmp.p, c.stream, &c.launches);
-  const size_t m = (size_t)read_u32(c, pos + n - 1) + read_u32(c, flag + n - 1);
+  const size_t m = read_sum2(c, pos + n - 1, flag + n - 1);
   if (dev_ids && m) k_compact_gid<<<grid_for(n, 256), 256, 0, c.stream>>>(flag, pos, c.cur.gid.p, n, dev_ids);
   c.launches += 2;
   return m;
@@ -725,7 +740,7 @@ static void refresh_changed_rows(Ctx& c, const uint32_t* group0) {
   k_mark_rows<<<grid_for(n, 256), 256, 0, c.stream>>>(c.ev_flag.p, c.cur.group.p, group0, n, c.nl(), c.P.img_mode,
                                                        dirty);
   exclusive_scan_u32(dirty, pos, n, c.scan_tmp.p, c.stream, &c.launches);
-  const size_t m = (size_t)read_u32(c, pos + n - 1) + read_u32(c, dirty + n - 1);
+  const size_t m = read_sum2(c, pos + n - 1, dirty + n - 1);
   c.launches++;
   if (m == 0) return;
   c.rec_ids.alloc(2 * m + 1);
@@ -739,7 +754,7 @@ static void refresh_changed_rows(Ctx& c, const uint32_t* group0) {
   uint32_t* rpos = pos;
   k_rigid_of<<<grid_for(m, 256), 256, 0, c.stream>>>(rows, m, c.cur.kmd.p, rflag);
   exclusive_scan_u32(rflag, rpos, m, c.scan_tmp.p, c.stream, &c.launches);
-  const size_t mr = (size_t)read_u32(c, rpos + m - 1) + read_u32(c, rflag + m - 1);
+  const size_t mr = read_sum2(c, rpos + m - 1, rflag + m - 1);
   if (mr == 0) return;
   uint32_t* rl = rows + m;
   k_compact_list<<<grid_for(m, 256), 256, 0, c.stream>>>(rows, rflag, rpos, m, rl);
@@ -753,8 +768,8 @@ int launch_transitions(Ctx& c) {
   cudaStream_t s = c.stream;
   if (n == 0) return 0;
   launch_detect(c);
-  const uint32_t nmelt = read_u32(c, &c.dflags->n_events);
-  const uint32_t nsolid = read_u32(c, &c.dflags->pad[0]);
+  uint32_t nmelt = 0, nsolid = 0;
+  read_u32x2(c, &c.dflags->n_events, &c.dflags->pad[0], nmelt, nsolid);
   if (nmelt == 0 && nsolid == 0) return 0;
   if (!c.built) launch_rebuild(c);
   c.group0.alloc(n);  // body ids before the batch (refresh_changed_rows)
@@ -806,7 +821,7 @@ int launch_transitions(Ctx& c) {
     SPHG_CUDA_CHECK(cudaMemcpyAsync(c.ev_idx.p, list, nsolid * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     k_solid_target<<<grid_for(nsolid, 128), 128, 0, s>>>(c.P, c.cur, c.ev_idx.p, nsolid, c.nl(), target, spawn);
     exclusive_scan_u32(spawn, rank, nsolid, c.scan_tmp.p, s, &c.launches);
-    nspawn = read_u32(c, rank + nsolid - 1) + read_u32(c, spawn + nsolid - 1);
+    nspawn = read_sum2(c, rank + nsolid - 1, spawn + nsolid - 1);
     k_solid_apply<<<grid_for(nsolid, 128), 128, 0, s>>>(c.P, c.cur, c.ev_idx.p, nsolid, target, rank, nb0,
                                                         c.bodies.p, bmask, src);
     c.launches += 5;
