@@ -182,6 +182,8 @@ class DeviceSimulation {
     check(sphg_set_wall_motion(ctx_, ng, ng ? &DeviceSimulation::wall_thunk : nullptr, this), "set_wall_motion");
   }
   void initialize() { check(sphg_initialize(ctx_), "initialize"); }
+  /// the C-ABI context (for entry points without a wrapper here)
+  sphg_ctx* raw() { return ctx_; }
   void step(int n = 1) { check(sphg_step(ctx_, n), "step"); }
   sphg_stats_t stats() {
     sphg_stats_t s;

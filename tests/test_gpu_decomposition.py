@@ -260,3 +260,18 @@ def test_record_ids_out_of_range_on_device():
     with pytest.raises(SPHError) as ei:
         sim.record_pack(ids, out=out)
     assert ei.value.code == 2 and "out of range" in str(ei.value)
+
+
+def test_cpp_decomposed_host_matches_single_rank():
+    """The C++ multi-GPU host (include/sphfsi_gpu/decomposed_simulation.hpp) as 2 and 4 ranks (threads on
+    this GPU, LocalTransport) against one DeviceSimulation: fluid + bodies with rebuilds and a migration,
+    and melting / solidification through the SPEC:500 batch (tests/cpp/test_decomposed.cpp)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "tests", "cpp", "_build", "test_decomposed")
+    assert os.path.exists(exe), "build() compiles tests/cpp (make -C tests/cpp)"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = [x for x in r.stdout.splitlines() if x.startswith("ok ")]
+    assert len(lines) == 4, r.stdout
+    assert any("melting ranks=2" in x for x in lines) and any("fluid+bodies ranks=4" in x for x in lines)
