@@ -73,26 +73,29 @@ class LocalTransport final : public Transport {
   LocalTransport(LocalHub& hub, int rank) : hub_(hub), rank_(rank) {}
   int rank() const override { return rank_; }
   int size() const override { return hub_.n_; }
+  // Every copy is enqueued on `stream` and waited for there: a blocking cudaMemcpy from pageable memory may
+  // return before its DMA has landed, and the library's stream does not wait for the legacy stream.
   void exchange(const std::vector<Msg>& sends, const std::vector<Msg>& recvs, cudaStream_t stream) override {
-    cudaStreamSynchronize(stream);
     for (const Msg& m : sends) {
       auto& b = hub_.box_[rank_][m.peer];
       b.resize(m.bytes);
-      if (m.bytes) cudaMemcpy(b.data(), m.ptr, m.bytes, cudaMemcpyDefault);
+      if (m.bytes) copy(b.data(), m.ptr, m.bytes, stream);
     }
+    sync(stream);
     hub_.bar_.arrive_and_wait();
     for (const Msg& m : recvs) {
       const auto& b = hub_.box_[m.peer][rank_];
       if (b.size() != m.bytes) throw Error(SPHG_ERR_RUNTIME, "LocalTransport: message size mismatch");
-      if (m.bytes) cudaMemcpy(m.ptr, b.data(), m.bytes, cudaMemcpyDefault);
+      if (m.bytes) copy(m.ptr, b.data(), m.bytes, stream);
     }
+    sync(stream);
     hub_.bar_.arrive_and_wait();
   }
   void allreduce_max_u64(uint64_t* dev, int count, cudaStream_t stream) override {
-    cudaStreamSynchronize(stream);
     auto& b = hub_.box_[rank_][rank_];
     b.resize(count * sizeof(uint64_t));
-    cudaMemcpy(b.data(), dev, b.size(), cudaMemcpyDefault);
+    copy(b.data(), dev, b.size(), stream);
+    sync(stream);
     hub_.bar_.arrive_and_wait();
     std::vector<uint64_t> v(count, 0);
     for (int r = 0; r < hub_.n_; ++r) {
@@ -100,16 +103,18 @@ class LocalTransport final : public Transport {
       for (int k = 0; k < count; ++k) v[k] = std::max(v[k], w[k]);
     }
     hub_.bar_.arrive_and_wait();
-    cudaMemcpy(dev, v.data(), count * sizeof(uint64_t), cudaMemcpyDefault);
+    copy(dev, v.data(), count * sizeof(uint64_t), stream);
+    sync(stream);
   }
   void allgather(const void* dev_in, void* dev_out, size_t bytes, cudaStream_t stream) override {
-    cudaStreamSynchronize(stream);
     auto& b = hub_.box_[rank_][rank_];
     b.resize(bytes);
-    if (bytes) cudaMemcpy(b.data(), dev_in, bytes, cudaMemcpyDefault);
+    if (bytes) copy(b.data(), dev_in, bytes, stream);
+    sync(stream);
     hub_.bar_.arrive_and_wait();
     for (int r = 0; r < hub_.n_; ++r)
-      if (bytes) cudaMemcpy(static_cast<uint8_t*>(dev_out) + r * bytes, hub_.box_[r][r].data(), bytes, cudaMemcpyDefault);
+      if (bytes) copy(static_cast<uint8_t*>(dev_out) + r * bytes, hub_.box_[r][r].data(), bytes, stream);
+    sync(stream);
     hub_.bar_.arrive_and_wait();
   }
   std::vector<std::vector<uint8_t>> alltoall_host(const std::vector<std::vector<uint8_t>>& out) override {
@@ -122,6 +127,13 @@ class LocalTransport final : public Transport {
   }
 
  private:
+  static void copy(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+    if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream) != cudaSuccess)
+      throw Error(SPHG_ERR_CUDA, "LocalTransport: copy failed");
+  }
+  static void sync(cudaStream_t stream) {
+    if (cudaStreamSynchronize(stream) != cudaSuccess) throw Error(SPHG_ERR_CUDA, "LocalTransport: sync failed");
+  }
   LocalHub& hub_;
   int rank_;
 };
@@ -159,7 +171,7 @@ class NcclTransport final : public Transport {
     uint64_t *drow, *dall;
     cudaMalloc(&drow, size_ * 8);
     cudaMalloc(&dall, size_ * size_ * 8);
-    cudaMemcpy(drow, row.data(), size_ * 8, cudaMemcpyHostToDevice);
+    cudaMemcpyAsync(drow, row.data(), size_ * 8, cudaMemcpyHostToDevice, host_stream_);  // ordered before the collective
     check(ncclAllGather(drow, dall, size_, ncclUint64, comm_, host_stream_));
     cudaMemcpyAsync(all.data(), dall, size_ * size_ * 8, cudaMemcpyDeviceToHost, host_stream_);
     cudaStreamSynchronize(host_stream_);
@@ -171,7 +183,7 @@ class NcclTransport final : public Transport {
       const uint64_t ns = out[q].size(), nr = all[q * size_ + rank_];
       if (ns) {
         cudaMalloc(&sb[q], ns);
-        cudaMemcpy(sb[q], out[q].data(), ns, cudaMemcpyHostToDevice);
+        cudaMemcpyAsync(sb[q], out[q].data(), ns, cudaMemcpyHostToDevice, host_stream_);
         check(ncclSend(sb[q], ns, ncclUint8, q, comm_, host_stream_));
       }
       if (nr) {
@@ -466,6 +478,7 @@ class DecomposedSimulation {
     gids_ = std::move(gids);
     n_own_ = n_own;
     sphg_soa v = views(loc);
+    v.owner = loc.owner.data();  // owner != rank marks the ghost copies (views() leaves it NULL: all owned)
     check(sphg_upload(ctx_, &v, bodies.data(), bodies.size()), "upload");
     std::vector<int> owner(loc.owner.begin(), loc.owner.end());
     std::vector<double> pos(3 * loc.size());

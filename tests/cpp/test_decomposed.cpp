@@ -7,6 +7,7 @@
 // Prints "ok <case> ranks=<n> ..." lines or fails with a non-zero exit code.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <thread>
 
 #include "sphfsi/lattice.hpp"
@@ -159,8 +160,9 @@ int compare(const char* name, int ranks, const ParticleStore<3>& a, const Partic
   return 0;
 }
 
-int run(bool melting) {
+int run(bool melting, int steps_override = 0, int ranks_only = 0) {
   Case c = make_case(melting);
+  if (steps_override > 0) c.steps = steps_override;
   const char* name = melting ? "melting" : "fluid+bodies";
   const double L = c.cfg.domain.hi[0] - c.cfg.domain.lo[0];
   ParticleStore<3> one = c.store;
@@ -173,6 +175,7 @@ int run(bool melting) {
     s.download(one, b1);
   }
   for (int ranks : {2, 4}) {
+    if (ranks_only && ranks != ranks_only) continue;
     sphfsi_gpu::LocalHub hub(ranks);
     std::vector<ParticleStore<3>> out(ranks);
     std::vector<std::vector<sphg_body>> bout(ranks);
@@ -212,8 +215,11 @@ int run(bool melting) {
 
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
   try {
+    if (argc > 2) {  // diagnostics: test_decomposed <melting 0|1> <steps> [ranks]
+      return run(std::atoi(argv[1]) != 0, std::atoi(argv[2]), argc > 3 ? std::atoi(argv[3]) : 0);
+    }
     int rc = run(false);
     if (rc) return rc;
     return run(true);
