@@ -1141,6 +1141,9 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
     int sms = 148;
     SPHG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     c.fill_groups = (size_t)sms * 2048 / 4 / 2;
+    c.n_sms = sms;
+    if (const char* e = std::getenv("SPHG_SM_LOCAL")) c.sm_local = std::atoi(e);
+    if (c.sm_local) c.sm_next.alloc(2 * (size_t)sms);
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     SPHG_CUDA_CHECK(cudaMalloc(&c.dflags, sizeof(DevFlags)));
     SPHG_CUDA_CHECK(cudaMemset(c.dflags, 0, sizeof(DevFlags)));
@@ -1953,7 +1956,7 @@ void sphg_destroy(sphg_ctx* h) {
   if (c.dens_join) cudaEventDestroy(c.dens_join);
   c.body_tot.free();
   c.keys.free(); c.keys_alt.free(); c.vals.free(); c.vals_alt.free(); c.hist.free(); c.scan_tmp.free();
-  c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free();
+  c.cell_start.free(); c.cell_end.free(); c.cell_key.free(); c.nbr.free(); c.cnt.free(); c.sm_next.free();
   c.ridx.free(); c.body_start.free(); c.ev_idx.free(); c.ev_flag.free(); c.label.free(); c.tscratch.free();
   c.label_list.free(); c.label_flags.free(); c.ev_log.free(); c.ev_count.free();
   c.rec_ids.free(); c.rec_buf.free(); c.group0.free(); c.bodies_old.free(); c.wrap_list.free(); c.state_buf.free();

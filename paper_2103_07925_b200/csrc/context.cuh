@@ -103,6 +103,9 @@ struct Ctx {
   DBuf<uint32_t> nbr, cnt;
   int cap = 0;
   NbrList nl() const { return {nbr.p, cnt.p, (size_t)cap}; }
+  // SM-local persistent pair kernels (SPHG_SM_LOCAL: 1 = fluid forces, 2 = density, 3 = both; experiment)
+  int sm_local = 0, n_sms = 148;
+  DBuf<uint32_t> sm_next;  // per-SM tile counters: [0, n_sms) density, [n_sms, 2 n_sms) forces
   // per-kind index lists: fluid, non-fluid (rigid + boundary), rigid body-major
   DBuf<uint32_t> fidx, widx, ridx, body_start;
   DBuf<uint32_t> ncon;  // per rigid particle: contact candidates at the front of its non-fluid row part

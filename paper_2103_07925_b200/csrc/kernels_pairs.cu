@@ -98,12 +98,8 @@ __device__ __forceinline__ double density_term(const DevParams& P, double3 pi, d
 // rho_i = m_i sigma (66 + sum_j shape(r_ij/h)); p_i = c^2 (rho_i - rho0); V_i = m_i/rho_i
 // (j over neighbours of any kind)
 template <int G, int M>
-__global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevParams P, Particles D, NbrList L,
-                                                     const uint32_t* __restrict__ list, size_t nlist) {
-  SPHG_SKIP_IF_FLAGGED(P);
-  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
-  const size_t g = t / G;
-  const int lane = (int)(t % G);
+__device__ __forceinline__ void density_group(const DevParams& P, const Particles& D, const NbrList& L,
+                                              const uint32_t* __restrict__ list, size_t nlist, size_t g, int lane) {
   const bool active = g < nlist;
   const uint32_t i = active ? list[g] : 0u;
   double s = 0.0;
@@ -138,6 +134,52 @@ __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevP
   reinterpret_cast<double*>(&D.G2.p[i])[3] = Mt.c2 * (rho - Mt.rho0);
   if (P.thermal) reinterpret_cast<double*>(&D.H2.p[i])[1] = V;
   if (P.diffusion) reinterpret_cast<double*>(&D.C2.p[i])[1] = V;
+}
+
+template <int G, int M>
+__global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                     const uint32_t* __restrict__ list, size_t nlist) {
+  SPHG_SKIP_IF_FLAGGED(P);
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  density_group<G, M>(P, D, L, list, nlist, t / G, (int)(t % G));
+}
+
+// SM-local persistent variants (SPHG_SM_LOCAL, experiment): the list is cut into one contiguous range per SM;
+// the resident warps of an SM take 8-particle tiles of its range in order (next[q], zeroed before the
+// launch), so the warps sharing an L1 walk adjacent particles of the brick-ordered list; a warp whose range
+// is finished helps the next ranges.
+__device__ __forceinline__ unsigned sm_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+// the next tile (8 list slots) for this warp, or false when every range is finished
+__device__ __forceinline__ bool next_tile(uint32_t* __restrict__ next, int nq, size_t ntiles, int& q, int& done,
+                                          size_t& tile) {
+  while (done < nq) {
+    const size_t q0 = ntiles * (size_t)q / nq, q1 = ntiles * (size_t)(q + 1) / nq;
+    uint32_t t = 0;
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(&next[q], 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (q0 + t < q1) {
+      tile = q0 + t;
+      return true;
+    }
+    q = q + 1 == nq ? 0 : q + 1;
+    ++done;
+  }
+  return false;
+}
+template <int M>
+__global__ void __launch_bounds__(kBlock) k_density_sm(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                        const uint32_t* __restrict__ list, size_t nlist,
+                                                        uint32_t* __restrict__ next, int nq) {
+  SPHG_SKIP_IF_FLAGGED(P);
+  const int lw = threadIdx.x & 31;
+  int q = (int)(sm_id() % (unsigned)nq), done = 0;
+  size_t tile;
+  while (next_tile(next, nq, (nlist + 7) / 8, q, done, tile))
+    density_group<4, M>(P, D, L, list, nlist, tile * 8 + (lw >> 2), lw & 3);
 }
 
 // ------------------------------------------------------------------- heat
@@ -593,16 +635,13 @@ __device__ __forceinline__ void fluid_row(const DevParams& P, const Particles& D
   }
 }
 
-template <int G, int M, bool kTvf, bool kSingleEta, bool kHeat = false>
-__global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__ DevParams P, Particles D, NbrList L,
-                                                          const uint32_t* __restrict__ list, size_t nlist,
-                                                          DevFlags* __restrict__ fl,
-                                                          double2* __restrict__ Hout = nullptr,
-                                                          const double2* __restrict__ Sin = nullptr, int sdiff = 0) {
-  SPHG_SKIP_IF_FLAGGED(P);
-  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
-  const size_t g = t / G;
-  const int lane = (int)(t % G);
+// one particle of the fluid list per G-lane group: g = its slot in the list, lane = the lane within the group
+// (called by whole warps: the group sums are warp shuffles)
+template <int G, int M, bool kTvf, bool kSingleEta, bool kHeat>
+__device__ __forceinline__ void forces_fluid_group(const DevParams& P, const Particles& D, const NbrList& L,
+                                                   const uint32_t* __restrict__ list, size_t nlist,
+                                                   DevFlags* __restrict__ fl, double2* __restrict__ Hout,
+                                                   const double2* __restrict__ Sin, int sdiff, size_t g, int lane) {
   const bool active = g < nlist;
   const uint32_t i = active ? list[g] : 0u;
   double3 acc = make_double3(0, 0, 0), bg = make_double3(0, 0, 0);
@@ -674,6 +713,31 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
   }
 }
 
+
+template <int G, int M, bool kTvf, bool kSingleEta, bool kHeat = false>
+__global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                          const uint32_t* __restrict__ list, size_t nlist,
+                                                          DevFlags* __restrict__ fl,
+                                                          double2* __restrict__ Hout = nullptr,
+                                                          const double2* __restrict__ Sin = nullptr, int sdiff = 0) {
+  SPHG_SKIP_IF_FLAGGED(P);
+  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+  forces_fluid_group<G, M, kTvf, kSingleEta, kHeat>(P, D, L, list, nlist, fl, Hout, Sin, sdiff, t / G, (int)(t % G));
+}
+
+template <int M, bool kTvf, bool kSingleEta>
+__global__ void __launch_bounds__(kBlock) k_forces_fluid_sm(const __grid_constant__ DevParams P, Particles D,
+                                                             NbrList L, const uint32_t* __restrict__ list,
+                                                             size_t nlist, DevFlags* __restrict__ fl,
+                                                             uint32_t* __restrict__ next, int nq) {
+  SPHG_SKIP_IF_FLAGGED(P);
+  const int lw = threadIdx.x & 31;
+  int q = (int)(sm_id() % (unsigned)nq), done = 0;
+  size_t tile;
+  while (next_tile(next, nq, (nlist + 7) / 8, q, done, tile))
+    forces_fluid_group<4, M, kTvf, kSingleEta, false>(P, D, L, list, nlist, fl, nullptr, nullptr, 0,
+                                                      tile * 8 + (lw >> 2), lw & 3);
+}
 
 // f_r = sum_i -m_i a_ir over the fluid part of the row (a_ir from the fluid's view)
 //     + contact over the rigid/boundary part
@@ -928,8 +992,23 @@ inline int lanes_for(const Ctx& c, size_t nlist) { return 2 * nlist < c.fill_gro
     }                                                             \
   } while (0)
 
+// persistent grid of an SM-local kernel: every block resident at once (occupancy x SMs), counters zeroed
+template <class K>
+static int sm_local_grid(Ctx& c, K kernel, uint32_t* next, cudaStream_t st) {
+  int per_sm = 0;
+  SPHG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+  SPHG_CUDA_CHECK(cudaMemsetAsync(next, 0, c.n_sms * sizeof(uint32_t), st));
+  return std::max(per_sm, 1) * c.n_sms;
+}
+
 static void launch_density_list(Ctx& c, const uint32_t* list, size_t m, cudaStream_t st) {
   if (m == 0) return;
+  if ((c.sm_local & 2) && (c.group_density ? c.group_density : lanes_for(c, m)) == 4) {
+    SPHG_IMG_DISPATCH(c.P.img_mode, (k_density_sm<M><<<sm_local_grid(c, k_density_sm<M>, c.sm_next.p, st), kBlock, 0,
+                                                      st>>>(c.P, c.cur, c.nl(), list, m, c.sm_next.p, c.n_sms)));
+    c.launches++;
+    return;
+  }
   SPHG_G_DISPATCH(c, c.group_density, m,
                   SPHG_IMG_DISPATCH(c.P.img_mode, (k_density<G, M><<<blocks_for<G>(m), kBlock, 0, st>>>(
                                                        c.P, c.cur, c.nl(), list, m))));
@@ -1046,6 +1125,15 @@ static void launch_forces_fluid_t(Ctx& c) {
     SPHG_L_DISPATCH(c, c.nf, SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, true>
                                      <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
                                          c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, out, sin, dif ? 1 : 0))));
+    c.launches++;
+    return;
+  }
+  if (c.nf && (c.sm_local & 1) && (c.group_forces ? c.group_forces : lanes_for(c, c.nf)) == 4) {
+    uint32_t* next = c.sm_next.p + c.n_sms;
+    SPHG_IMG_DISPATCH(c.P.img_mode,
+                      (k_forces_fluid_sm<M, kTvf, kSingleEta>
+                       <<<sm_local_grid(c, k_forces_fluid_sm<M, kTvf, kSingleEta>, next, c.stream), kBlock, 0,
+                          c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, next, c.n_sms)));
     c.launches++;
     return;
   }
