@@ -86,7 +86,7 @@ struct DevParams {
 
 // ------------------------------------------------------ brick traversal
 // Work order of the cell-structured kernels (Verlet build, pair kernels): cells are visited brick
-// by brick (kBrick^3 cells, bricks and cells inside a brick z-fastest).  Storage stays in the pinned
+// by brick (kBrick^3 cells, bricks z-fastest; inside a brick 2x2x2 blocks of cells, z-fastest).  Storage stays in the pinned
 // z-fastest (cell, gid) order [P1]; only the order in which cells / particles are PROCESSED
 // changes, so the neighbourhood of the cells in flight (~(kBrick+2)^3 cells) stays in L2 instead
 // of three whole x-planes of the grid.
@@ -102,7 +102,17 @@ __host__ __device__ __forceinline__ int64_t brick_to_cell(const int32_t* nc, int
   const int64_t nby = (nc[1] + kBrick - 1) / kBrick, nbz = (nc[2] + kBrick - 1) / kBrick;
   const int64_t brick = b / B3, loc = b % B3;
   const int64_t bz = brick % nbz, by = (brick / nbz) % nby, bx = brick / (nbz * nby);
+#ifndef SPHG_BRICK_ZLINE
+  // 2x2x2 blocks of cells inside the brick (blocks and the cells of a block z-fastest): the ~8 cells whose
+  // particles are in flight on one SM (SM-local pair kernels) share a 4x4x4-cell neighbourhood instead of
+  // the 3x3x10 cells of a z-line
+  constexpr int64_t H = kBrick / 2;
+  const int64_t blk = loc >> 3, in = loc & 7;
+  const int64_t lz = 2 * (blk % H) + (in & 1), ly = 2 * ((blk / H) % H) + ((in >> 1) & 1),
+                lx = 2 * (blk / (H * H)) + (in >> 2);
+#else
   const int64_t lz = loc % kBrick, ly = (loc / kBrick) % kBrick, lx = loc / (kBrick * kBrick);
+#endif
   const int64_t cx = bx * kBrick + lx, cy = by * kBrick + ly, cz = bz * kBrick + lz;
   if (cx >= nc[0] || cy >= nc[1] || cz >= nc[2]) return -1;
   return (cx * nc[1] + cy) * nc[2] + cz;

@@ -103,8 +103,8 @@ struct Ctx {
   DBuf<uint32_t> nbr, cnt;
   int cap = 0;
   NbrList nl() const { return {nbr.p, cnt.p, (size_t)cap}; }
-  // SM-local persistent pair kernels (SPHG_SM_LOCAL: 1 = fluid forces, 2 = density, 3 = both; experiment)
-  int sm_local = 0, n_sms = 148;
+  // SM-local persistent pair kernels (SPHG_SM_LOCAL: bit 0 = fluid forces, bit 1 = density; 0 = flat grids)
+  int sm_local = 3, n_sms = 148;
   DBuf<uint32_t> sm_next;  // per-SM tile counters: [0, n_sms) density, [n_sms, 2 n_sms) forces
   // per-kind index lists: fluid, non-fluid (rigid + boundary), rigid body-major
   DBuf<uint32_t> fidx, widx, ridx, body_start;

@@ -144,10 +144,13 @@ __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevP
   density_group<G, M>(P, D, L, list, nlist, t / G, (int)(t % G));
 }
 
-// SM-local persistent variants (SPHG_SM_LOCAL, experiment): the list is cut into one contiguous range per SM;
-// the resident warps of an SM take 8-particle tiles of its range in order (next[q], zeroed before the
-// launch), so the warps sharing an L1 walk adjacent particles of the brick-ordered list; a warp whose range
-// is finished helps the next ranges.
+// SM-local persistent variants (the 4-lane density and fluid forces passes; SPHG_SM_LOCAL=0 restores one
+// group per thread of a flat grid): the list is cut into one contiguous range per SM and the resident warps
+// of an SM take 8-particle tiles of its range in order (next[q], zeroed before the launch).  The list is in
+// brick order (2x2x2 blocks of cells, common.cuh), so the ~190 particles in flight on an SM share one
+// 4x4x4-cell neighbourhood that stays in that SM's L1, where a flat grid's co-resident blocks sit 148 blocks
+// apart in the list.  A warp whose range is finished helps the next ranges.  Each particle is still summed by
+// its own 4 lanes in row order: results are bit-identical to the flat grid's.
 __device__ __forceinline__ unsigned sm_id() {
   unsigned r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -725,17 +728,19 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
   forces_fluid_group<G, M, kTvf, kSingleEta, kHeat>(P, D, L, list, nlist, fl, Hout, Sin, sdiff, t / G, (int)(t % G));
 }
 
-template <int M, bool kTvf, bool kSingleEta>
+template <int M, bool kTvf, bool kSingleEta, bool kHeat>
 __global__ void __launch_bounds__(kBlock) k_forces_fluid_sm(const __grid_constant__ DevParams P, Particles D,
                                                              NbrList L, const uint32_t* __restrict__ list,
                                                              size_t nlist, DevFlags* __restrict__ fl,
-                                                             uint32_t* __restrict__ next, int nq) {
+                                                             uint32_t* __restrict__ next, int nq,
+                                                             double2* __restrict__ Hout,
+                                                             const double2* __restrict__ Sin, int sdiff) {
   SPHG_SKIP_IF_FLAGGED(P);
   const int lw = threadIdx.x & 31;
   int q = (int)(sm_id() % (unsigned)nq), done = 0;
   size_t tile;
   while (next_tile(next, nq, (nlist + 7) / 8, q, done, tile))
-    forces_fluid_group<4, M, kTvf, kSingleEta, false>(P, D, L, list, nlist, fl, nullptr, nullptr, 0,
+    forces_fluid_group<4, M, kTvf, kSingleEta, kHeat>(P, D, L, list, nlist, fl, Hout, Sin, sdiff,
                                                       tile * 8 + (lw >> 2), lw & 3);
 }
 
@@ -995,10 +1000,13 @@ inline int lanes_for(const Ctx& c, size_t nlist) { return 2 * nlist < c.fill_gro
 // persistent grid of an SM-local kernel: every block resident at once (occupancy x SMs), counters zeroed
 template <class K>
 static int sm_local_grid(Ctx& c, K kernel, uint32_t* next, cudaStream_t st) {
-  int per_sm = 0;
-  SPHG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+  static int per_sm = 0;  // one instance per kernel instantiation
+  if (per_sm == 0) {
+    SPHG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+    per_sm = std::max(per_sm, 1);
+  }
   SPHG_CUDA_CHECK(cudaMemsetAsync(next, 0, c.n_sms * sizeof(uint32_t), st));
-  return std::max(per_sm, 1) * c.n_sms;
+  return per_sm * c.n_sms;
 }
 
 static void launch_density_list(Ctx& c, const uint32_t* list, size_t m, cudaStream_t st) {
@@ -1117,27 +1125,32 @@ void launch_extrapolate(Ctx& c) {
 
 template <bool kTvf, bool kSingleEta>
 static void launch_forces_fluid_t(Ctx& c) {
+  uint32_t* next = c.sm_next.p + c.n_sms;
   if (c.nf && (c.fuse_heat || c.fuse_diff)) {  // conduction / diffusion of the fluid particles in the same
                                                // row walk (k_heat's / k_diffusion's width and order)
     const bool dif = !c.fuse_heat;
     const double2* sin = dif ? c.cur.C2.p : c.cur.H2.p;
     double2* out = dif ? c.C2new.p : c.H2new.p;
-    SPHG_L_DISPATCH(c, c.nf, SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, true>
-                                     <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, out, sin, dif ? 1 : 0))));
+    if ((c.sm_local & 1) && lanes_for(c, c.nf) == 4)
+      SPHG_IMG_DISPATCH(c.P.img_mode,
+                        (k_forces_fluid_sm<M, kTvf, kSingleEta, true>
+                         <<<sm_local_grid(c, k_forces_fluid_sm<M, kTvf, kSingleEta, true>, next, c.stream), kBlock, 0,
+                            c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, next, c.n_sms, out, sin,
+                                        dif ? 1 : 0)));
+    else
+      SPHG_L_DISPATCH(c, c.nf, SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta, true>
+                                       <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
+                                           c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, out, sin, dif ? 1 : 0))));
     c.launches++;
     return;
   }
-  if (c.nf && (c.sm_local & 1) && (c.group_forces ? c.group_forces : lanes_for(c, c.nf)) == 4) {
-    uint32_t* next = c.sm_next.p + c.n_sms;
+  if (c.nf && (c.sm_local & 1) && (c.group_forces ? c.group_forces : lanes_for(c, c.nf)) == 4)
     SPHG_IMG_DISPATCH(c.P.img_mode,
-                      (k_forces_fluid_sm<M, kTvf, kSingleEta>
-                       <<<sm_local_grid(c, k_forces_fluid_sm<M, kTvf, kSingleEta>, next, c.stream), kBlock, 0,
-                          c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, next, c.n_sms)));
-    c.launches++;
-    return;
-  }
-  if (c.nf)
+                      (k_forces_fluid_sm<M, kTvf, kSingleEta, false>
+                       <<<sm_local_grid(c, k_forces_fluid_sm<M, kTvf, kSingleEta, false>, next, c.stream), kBlock, 0,
+                          c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, next, c.n_sms, nullptr, nullptr,
+                                      0)));
+  else if (c.nf)
     SPHG_G_DISPATCH(c, c.group_forces, c.nf,
                     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta>
                                                      <<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(

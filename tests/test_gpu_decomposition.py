@@ -275,3 +275,15 @@ def test_cpp_decomposed_host_matches_single_rank():
     lines = [x for x in r.stdout.splitlines() if x.startswith("ok ")]
     assert len(lines) == 4, r.stdout
     assert any("melting ranks=2" in x for x in lines) and any("fluid+bodies ranks=4" in x for x in lines)
+
+
+def test_cpp_nccl_transport_single_rank():
+    """NcclTransport on a one-rank NCCL communicator (tests/cpp/test_nccl_transport.cpp): the grouped
+    send / receive of a halo phase, the MAX all-reduce of the displacement words, the all-gather of the body
+    partials and the host byte all-to-all are issued through NCCL on this GPU, stream-ordered, and checked."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "tests", "cpp", "_build", "test_nccl_transport")
+    assert os.path.exists(exe), "build() compiles tests/cpp (make -C tests/cpp)"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok nccl transport" in r.stdout, r.stdout + r.stderr
