@@ -20,6 +20,7 @@
 // rebuild.  These kernels are gather-bound, not FP64-bound (a loads-only twin of
 // k_forces_fluid takes 97 % of its time).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "context.cuh"
@@ -156,7 +157,7 @@ __device__ __forceinline__ unsigned sm_id() {
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
   return r;
 }
-// the next tile (8 list slots) for this warp, or false when every range is finished
+// the next tile (32 / G list slots) for this warp, or false when every range is finished
 __device__ __forceinline__ bool next_tile(uint32_t* __restrict__ next, int nq, size_t ntiles, int& q, int& done,
                                           size_t& tile) {
   while (done < nq) {
@@ -173,7 +174,7 @@ __device__ __forceinline__ bool next_tile(uint32_t* __restrict__ next, int nq, s
   }
   return false;
 }
-template <int M>
+template <int G, int M>
 __global__ void __launch_bounds__(kBlock) k_density_sm(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                         const uint32_t* __restrict__ list, size_t nlist,
                                                         uint32_t* __restrict__ next, int nq) {
@@ -181,8 +182,9 @@ __global__ void __launch_bounds__(kBlock) k_density_sm(const __grid_constant__ D
   const int lw = threadIdx.x & 31;
   int q = (int)(sm_id() % (unsigned)nq), done = 0;
   size_t tile;
-  while (next_tile(next, nq, (nlist + 7) / 8, q, done, tile))
-    density_group<4, M>(P, D, L, list, nlist, tile * 8 + (lw >> 2), lw & 3);
+  constexpr int T = 32 / G;  // particles per warp tile
+  while (next_tile(next, nq, (nlist + T - 1) / T, q, done, tile))
+    density_group<G, M>(P, D, L, list, nlist, tile * T + lw / G, lw % G);
 }
 
 // ------------------------------------------------------------------- heat
@@ -728,7 +730,7 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
   forces_fluid_group<G, M, kTvf, kSingleEta, kHeat>(P, D, L, list, nlist, fl, Hout, Sin, sdiff, t / G, (int)(t % G));
 }
 
-template <int M, bool kTvf, bool kSingleEta, bool kHeat>
+template <int G, int M, bool kTvf, bool kSingleEta, bool kHeat>
 __global__ void __launch_bounds__(kBlock) k_forces_fluid_sm(const __grid_constant__ DevParams P, Particles D,
                                                              NbrList L, const uint32_t* __restrict__ list,
                                                              size_t nlist, DevFlags* __restrict__ fl,
@@ -739,9 +741,10 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid_sm(const __grid_constan
   const int lw = threadIdx.x & 31;
   int q = (int)(sm_id() % (unsigned)nq), done = 0;
   size_t tile;
-  while (next_tile(next, nq, (nlist + 7) / 8, q, done, tile))
-    forces_fluid_group<4, M, kTvf, kSingleEta, kHeat>(P, D, L, list, nlist, fl, Hout, Sin, sdiff,
-                                                      tile * 8 + (lw >> 2), lw & 3);
+  constexpr int T = 32 / G;  // particles per warp tile
+  while (next_tile(next, nq, (nlist + T - 1) / T, q, done, tile))
+    forces_fluid_group<G, M, kTvf, kSingleEta, kHeat>(P, D, L, list, nlist, fl, Hout, Sin, sdiff,
+                                                      tile * T + lw / G, lw % G);
 }
 
 // f_r = sum_i -m_i a_ir over the fluid part of the row (a_ir from the fluid's view)
@@ -1002,6 +1005,8 @@ template <class K>
 static int sm_local_grid(Ctx& c, K kernel, uint32_t* next, cudaStream_t st) {
   static int per_sm = 0;  // one instance per kernel instantiation
   if (per_sm == 0) {
+    if (const char* e = std::getenv("SPHG_SMEM_CARVEOUT"))  // experiment: shared-memory share of the L1 array, %
+      SPHG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)));
     SPHG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
     per_sm = std::max(per_sm, 1);
   }
@@ -1011,9 +1016,15 @@ static int sm_local_grid(Ctx& c, K kernel, uint32_t* next, cudaStream_t st) {
 
 static void launch_density_list(Ctx& c, const uint32_t* list, size_t m, cudaStream_t st) {
   if (m == 0) return;
-  if ((c.sm_local & 2) && (c.group_density ? c.group_density : lanes_for(c, m)) == 4) {
-    SPHG_IMG_DISPATCH(c.P.img_mode, (k_density_sm<M><<<sm_local_grid(c, k_density_sm<M>, c.sm_next.p, st), kBlock, 0,
-                                                      st>>>(c.P, c.cur, c.nl(), list, m, c.sm_next.p, c.n_sms)));
+  const int gd = c.group_density ? c.group_density : lanes_for(c, m);
+  if ((c.sm_local & 2) && (gd == 4 || gd == 8)) {
+#define SPHG_DENS_SM(GV)                                                                                            \
+  SPHG_IMG_DISPATCH(c.P.img_mode,                                                                                   \
+                    (k_density_sm<GV, M><<<sm_local_grid(c, k_density_sm<GV, M>, c.sm_next.p, st), kBlock, 0, st>>>( \
+                        c.P, c.cur, c.nl(), list, m, c.sm_next.p, c.n_sms)))
+    if (gd == 8) SPHG_DENS_SM(8);
+    else SPHG_DENS_SM(4);
+#undef SPHG_DENS_SM
     c.launches++;
     return;
   }
@@ -1133,8 +1144,8 @@ static void launch_forces_fluid_t(Ctx& c) {
     double2* out = dif ? c.C2new.p : c.H2new.p;
     if ((c.sm_local & 1) && lanes_for(c, c.nf) == 4)
       SPHG_IMG_DISPATCH(c.P.img_mode,
-                        (k_forces_fluid_sm<M, kTvf, kSingleEta, true>
-                         <<<sm_local_grid(c, k_forces_fluid_sm<M, kTvf, kSingleEta, true>, next, c.stream), kBlock, 0,
+                        (k_forces_fluid_sm<4, M, kTvf, kSingleEta, true>
+                         <<<sm_local_grid(c, k_forces_fluid_sm<4, M, kTvf, kSingleEta, true>, next, c.stream), kBlock, 0,
                             c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, next, c.n_sms, out, sin,
                                         dif ? 1 : 0)));
     else
@@ -1144,12 +1155,16 @@ static void launch_forces_fluid_t(Ctx& c) {
     c.launches++;
     return;
   }
-  if (c.nf && (c.sm_local & 1) && (c.group_forces ? c.group_forces : lanes_for(c, c.nf)) == 4)
-    SPHG_IMG_DISPATCH(c.P.img_mode,
-                      (k_forces_fluid_sm<M, kTvf, kSingleEta, false>
-                       <<<sm_local_grid(c, k_forces_fluid_sm<M, kTvf, kSingleEta, false>, next, c.stream), kBlock, 0,
-                          c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, next, c.n_sms, nullptr, nullptr,
-                                      0)));
+  const int gf = c.group_forces ? c.group_forces : lanes_for(c, c.nf);
+#define SPHG_FORCES_SM(GV)                                                                                          \
+  SPHG_IMG_DISPATCH(c.P.img_mode,                                                                                   \
+                    (k_forces_fluid_sm<GV, M, kTvf, kSingleEta, false>                                              \
+                     <<<sm_local_grid(c, k_forces_fluid_sm<GV, M, kTvf, kSingleEta, false>, next, c.stream), kBlock, \
+                        0, c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, next, c.n_sms, nullptr,         \
+                                       nullptr, 0)))
+  if (c.nf && (c.sm_local & 1) && gf == 4) SPHG_FORCES_SM(4);
+  else if (c.nf && (c.sm_local & 1) && gf == 8) SPHG_FORCES_SM(8);
+#undef SPHG_FORCES_SM
   else if (c.nf)
     SPHG_G_DISPATCH(c, c.group_forces, c.nf,
                     SPHG_IMG_DISPATCH(c.P.img_mode, (k_forces_fluid<G, M, kTvf, kSingleEta>
