@@ -356,7 +356,7 @@ def run_sph(args):
 
 
 def make_roofline(forces_ms, inter_fluid, nf, n):
-    """The dominant kernel, k_forces_fluid: average launch duration (CUDA events on the library stream,
+    """The dominant kernel, k_forces_fluid_sm (k_forces_fluid on its SM-local persistent grid): average launch duration (CUDA events on the library stream,
     stage-timed pass), algorithmic flops = 91 per interacting pair with a fluid i,
     algorithmic bytes = 156 B per fluid particle (CSM model).  n = store size when the committed ncu
     capture is of the same store (64M), for the measured DRAM traffic and L1 figures."""
@@ -376,14 +376,18 @@ def make_roofline(forces_ms, inter_fluid, nf, n):
                 wr = float(k["dram__bytes_write.sum"].split()[0]) * 1e9
                 src = os.path.relpath(tp, ROOT) + " (ncu --set full, one launch)"
                 traffic = {"bytes_per_launch": rd + wr, "source": src,
-                           "note": "Verlet rows (~29 GB) + neighbour records re-read past L2; the CSM bytes model is 8.8 GB"}
+                           "note": "Verlet rows (~29 GB) + neighbour records that miss L1 and L2 (SM-local ranges: an "
+                                   "SM's records stay in its L1, neighbouring SMs share little in L2); the CSM "
+                                   "bytes model is 8.8 GB"}
                 wf = k.get("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed")
                 fp = k.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active")
                 if wf:
+                    hit = k.get("l1tex__t_sector_hit_rate.pct")
                     l1 = {"lsu_wavefronts_pct": float(wf.split()[0]), "fp64_pipe_pct": float(fp.split()[0]) if fp else None,
+                          "l1_sector_hit_pct": float(hit.split()[0]) if hit else None,
                           "source": src, "note": "the binding unit: L1 data-pipe wavefronts (one per distinct 32 B "
                                                  "sector of a gather), see DESIGN.md section 4"}
-    roofline = {"bound": "fp64", "kernel": "k_forces_fluid (momentum_rhs + TVF)",
+    roofline = {"bound": "fp64", "kernel": "k_forces_fluid_sm (momentum_rhs + TVF; SM-local persistent grid)",
                 "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": (achieved_tf / fp64_peak) if fp64_peak else None,
                 "traffic": traffic, "l1": l1, "launch_ms": forces_ms,

@@ -18,7 +18,9 @@
 // sum is a gather (no fp64 atomics), hence deterministic.  Groups iterate over
 // compact per-kind index lists (fluid / non-fluid in brick order, rigid body-major) built at
 // rebuild.  These kernels are gather-bound, not FP64-bound (a loads-only twin of
-// k_forces_fluid takes 97 % of its time).
+// k_forces_fluid takes 97 % of its time).  The two big passes (density, fluid forces) run as
+// SM-local persistent grids (k_density_sm, k_forces_fluid_sm): the warps of one SM take adjacent
+// tiles of the brick-ordered list, so the records they gather stay in that SM's L1.
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
