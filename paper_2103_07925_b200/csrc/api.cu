@@ -1143,7 +1143,8 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
     c.fill_groups = (size_t)sms * 2048 / 4 / 2;
     c.n_sms = sms;
     if (const char* e = std::getenv("SPHG_SM_LOCAL")) c.sm_local = std::atoi(e);
-    c.sm_next.alloc(2 * (size_t)sms);
+    if (const char* e = std::getenv("SPHG_SM_LOCAL_MIN")) c.sm_local_min = (size_t)std::atoll(e);
+    c.sm_next.alloc(4 * (size_t)sms);  // density, fluid forces, extrapolation, rigid forces
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     SPHG_CUDA_CHECK(cudaMalloc(&c.dflags, sizeof(DevFlags)));
     SPHG_CUDA_CHECK(cudaMemset(c.dflags, 0, sizeof(DevFlags)));

@@ -103,9 +103,11 @@ struct Ctx {
   DBuf<uint32_t> nbr, cnt;
   int cap = 0;
   NbrList nl() const { return {nbr.p, cnt.p, (size_t)cap}; }
-  // SM-local persistent pair kernels (SPHG_SM_LOCAL: bit 0 = fluid forces, bit 1 = density; 0 = flat grids)
+  // SM-local persistent pair kernels (SPHG_SM_LOCAL: bit 0 = fluid forces, bit 1 = density, bit 2 =
+  // extrapolation, bit 3 = rigid forces; 0 = flat grids)
   int sm_local = 3, n_sms = 148;
-  DBuf<uint32_t> sm_next;  // per-SM tile counters: [0, n_sms) density, [n_sms, 2 n_sms) forces
+  size_t sm_local_min = 1u << 20;  // shortest list that gets a persistent grid (SPHG_SM_LOCAL_MIN)
+  DBuf<uint32_t> sm_next;  // per-SM tile counters, n_sms each: density, fluid forces, extrapolation, rigid forces
   // per-kind index lists: fluid, non-fluid (rigid + boundary), rigid body-major
   DBuf<uint32_t> fidx, widx, ridx, body_start;
   DBuf<uint32_t> ncon;  // per rigid particle: contact candidates at the front of its non-fluid row part

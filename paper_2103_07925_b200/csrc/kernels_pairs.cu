@@ -159,22 +159,34 @@ __device__ __forceinline__ unsigned sm_id() {
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
   return r;
 }
-// the next tile (32 / G list slots) for this warp, or false when every range is finished
-__device__ __forceinline__ bool next_tile(uint32_t* __restrict__ next, int nq, size_t ntiles, int& q, int& done,
-                                          size_t& tile) {
-  while (done < nq) {
+// the next tile (32 list slots' worth of lanes) for this warp, or false when every range is finished.  Own
+// range first; when it is exhausted the 32 lanes probe 32 other counters at a time (L2 reads: a counter only
+// grows, so a stale value can only show work that is already gone, which the atomic then finds out).
+__device__ __forceinline__ bool next_tile(uint32_t* __restrict__ next, int nq, size_t ntiles, int& q, size_t& tile) {
+  const int lw = threadIdx.x & 31;
+  for (;;) {
     const size_t q0 = ntiles * (size_t)q / nq, q1 = ntiles * (size_t)(q + 1) / nq;
     uint32_t t = 0;
-    if ((threadIdx.x & 31) == 0) t = atomicAdd(&next[q], 1u);
+    if (lw == 0) t = atomicAdd(&next[q], 1u);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (q0 + t < q1) {
       tile = q0 + t;
       return true;
     }
-    q = q + 1 == nq ? 0 : q + 1;
-    ++done;
+    int found = -1;
+    for (int base = 1; base < nq && found < 0; base += 32) {
+      bool has = false;
+      if (base + lw < nq) {
+        const int qq = (q + base + lw) % nq;
+        const size_t a0 = ntiles * (size_t)qq / nq, a1 = ntiles * (size_t)(qq + 1) / nq;
+        has = a0 + __ldcg(&next[qq]) < a1;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, has);
+      if (m) found = (q + base + __ffs((int)m) - 1) % nq;
+    }
+    if (found < 0) return false;
+    q = found;
   }
-  return false;
 }
 template <int G, int M>
 __global__ void __launch_bounds__(kBlock) k_density_sm(const __grid_constant__ DevParams P, Particles D, NbrList L,
@@ -182,10 +194,10 @@ __global__ void __launch_bounds__(kBlock) k_density_sm(const __grid_constant__ D
                                                         uint32_t* __restrict__ next, int nq) {
   SPHG_SKIP_IF_FLAGGED(P);
   const int lw = threadIdx.x & 31;
-  int q = (int)(sm_id() % (unsigned)nq), done = 0;
+  int q = (int)(sm_id() % (unsigned)nq);
   size_t tile;
   constexpr int T = 32 / G;  // particles per warp tile
-  while (next_tile(next, nq, (nlist + T - 1) / T, q, done, tile))
+  while (next_tile(next, nq, (nlist + T - 1) / T, q, tile))
     density_group<G, M>(P, D, L, list, nlist, tile * T + lw / G, lw % G);
 }
 
@@ -390,20 +402,13 @@ __global__ void __launch_bounds__(kBlock) k_diffusion(const __grid_constant__ De
 // r_c^2 is appended to pin_list and not written (there the weights' relative errors ~15 eps/(3-q)
 // reach the ratios; a lone weight can even be 0 on one side and tiny on the other).  kPin = true: only those particles, with
 // pinned_q (see common.cuh).
+// t: the thread's slot (group t / G, lane t % G); called by whole warps
 template <int G, int M, bool kMultiEos, bool kPin>
-// (the fast variant fits 56 registers without spills: 9 blocks of 128 per SM)
-__global__ void __launch_bounds__(kBlock, kPin ? 1 : 9) k_extrapolate(const __grid_constant__ DevParams P, Particles D, NbrList L,
-                                                         const sphg_body* __restrict__ B,
-                                                         const uint32_t* __restrict__ list, size_t nlist,
-                                                         uint32_t* __restrict__ pin_list, uint32_t* __restrict__ any) {
-  SPHG_SKIP_IF_FLAGGED(P);
-  // kPin: the flagged particles, compacted by the fast pass into pin_list[0 .. *any)
-  if (kPin) {
-    nlist = *any;
-    list = pin_list;
-    if ((size_t)blockIdx.x * (kBlock / G) >= nlist) return;  // the common case: nothing flagged
-  }
-  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+__device__ __forceinline__ void extrapolate_group(const DevParams& P, const Particles& D, const NbrList& L,
+                                                  const sphg_body* __restrict__ B,
+                                                  const uint32_t* __restrict__ list, size_t nlist,
+                                                  uint32_t* __restrict__ pin_list, uint32_t* __restrict__ any,
+                                                  size_t t) {
   const size_t g = t / G;
   const int lane = (int)(t % G);
   const uint32_t w = g < nlist ? list[g] : 0u;
@@ -505,6 +510,38 @@ __global__ void __launch_bounds__(kBlock, kPin ? 1 : 9) k_extrapolate(const __gr
   reinterpret_cast<double*>(&D.G0.p[w])[3] = V_w * V_w;
   D.G1.p[w] = make_double4(ut.x, ut.y, ut.z, rho_w);
   D.G2.p[w] = make_double4(0.0, 0.0, 0.0, p_w);
+}
+
+template <int G, int M, bool kMultiEos, bool kPin>
+// (the fast variant fits 56 registers without spills: 9 blocks of 128 per SM)
+__global__ void __launch_bounds__(kBlock, kPin ? 1 : 9) k_extrapolate(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                         const sphg_body* __restrict__ B,
+                                                         const uint32_t* __restrict__ list, size_t nlist,
+                                                         uint32_t* __restrict__ pin_list, uint32_t* __restrict__ any) {
+  SPHG_SKIP_IF_FLAGGED(P);
+  // kPin: the flagged particles, compacted by the fast pass into pin_list[0 .. *any)
+  if (kPin) {
+    nlist = *any;
+    list = pin_list;
+    if ((size_t)blockIdx.x * (kBlock / G) >= nlist) return;  // the common case: nothing flagged
+  }
+  extrapolate_group<G, M, kMultiEos, kPin>(P, D, L, B, list, nlist, pin_list, any,
+                                           (size_t)blockIdx.x * kBlock + threadIdx.x);
+}
+
+// the fast pass on an SM-local persistent grid (see k_density_sm)
+template <int M, bool kMultiEos>
+__global__ void __launch_bounds__(kBlock, 9) k_extrapolate_sm(const __grid_constant__ DevParams P, Particles D,
+                                                               NbrList L, const sphg_body* __restrict__ B,
+                                                               const uint32_t* __restrict__ list, size_t nlist,
+                                                               uint32_t* __restrict__ pin_list,
+                                                               uint32_t* __restrict__ any, uint32_t* __restrict__ next,
+                                                               int nq) {
+  SPHG_SKIP_IF_FLAGGED(P);
+  int q = (int)(sm_id() % (unsigned)nq);
+  size_t tile;
+  while (next_tile(next, nq, (nlist + 7) / 8, q, tile))
+    extrapolate_group<4, M, kMultiEos, false>(P, D, L, B, list, nlist, pin_list, any, tile * 32 + (threadIdx.x & 31));
 }
 
 // ---------------------------------------------------------------- forces
@@ -741,10 +778,10 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid_sm(const __grid_constan
                                                              const double2* __restrict__ Sin, int sdiff) {
   SPHG_SKIP_IF_FLAGGED(P);
   const int lw = threadIdx.x & 31;
-  int q = (int)(sm_id() % (unsigned)nq), done = 0;
+  int q = (int)(sm_id() % (unsigned)nq);
   size_t tile;
   constexpr int T = 32 / G;  // particles per warp tile
-  while (next_tile(next, nq, (nlist + T - 1) / T, q, done, tile))
+  while (next_tile(next, nq, (nlist + T - 1) / T, q, tile))
     forces_fluid_group<G, M, kTvf, kSingleEta, kHeat>(P, D, L, list, nlist, fl, Hout, Sin, sdiff,
                                                       tile * T + lw / G, lw % G);
 }
@@ -754,19 +791,11 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid_sm(const __grid_constan
 // kPin = false: the fast root; a particle whose fluid pairs all sit within 2e-4 below r_c^2 is appended
 // to pin_list and not written.  kPin = true: only those particles, coupling with pinned_q.
 template <int G, int M, bool kTvf, bool kSingleEta, bool kPin>
-__global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__ DevParams P, Particles D, NbrList L,
-                                                          const uint32_t* __restrict__ list, size_t nlist,
-                                                          const uint32_t* __restrict__ ncon,
-                                                          DevFlags* __restrict__ fl, uint32_t* __restrict__ pin_list,
-                                                          uint32_t* __restrict__ any) {
-  SPHG_SKIP_IF_FLAGGED(P);
-  // kPin: the flagged particles, compacted by the fast pass into pin_list[0 .. *any)
-  if (kPin) {
-    nlist = *any;
-    list = pin_list;
-    if ((size_t)blockIdx.x * (kBlock / G) >= nlist) return;  // the common case: nothing flagged
-  }
-  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+__device__ __forceinline__ void forces_rigid_group(const DevParams& P, const Particles& D, const NbrList& L,
+                                                   const uint32_t* __restrict__ list, size_t nlist,
+                                                   const uint32_t* __restrict__ ncon, DevFlags* __restrict__ fl,
+                                                   uint32_t* __restrict__ pin_list, uint32_t* __restrict__ any,
+                                                   size_t t) {
   const size_t g = t / G;
   const int lane = (int)(t % G);
   const uint32_t r = g < nlist ? list[g] : 0u;
@@ -869,6 +898,40 @@ __global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__
     atomicMin(&fl->err_gid, D.gid.p[r]);
   }
   if (lane == 0) D.F4.p[r] = make_double4(f.x, f.y, f.z, 0.0);
+}
+
+template <int G, int M, bool kTvf, bool kSingleEta, bool kPin>
+__global__ void __launch_bounds__(kBlock) k_forces_rigid(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                          const uint32_t* __restrict__ list, size_t nlist,
+                                                          const uint32_t* __restrict__ ncon,
+                                                          DevFlags* __restrict__ fl, uint32_t* __restrict__ pin_list,
+                                                          uint32_t* __restrict__ any) {
+  SPHG_SKIP_IF_FLAGGED(P);
+  // kPin: the flagged particles, compacted by the fast pass into pin_list[0 .. *any)
+  if (kPin) {
+    nlist = *any;
+    list = pin_list;
+    if ((size_t)blockIdx.x * (kBlock / G) >= nlist) return;  // the common case: nothing flagged
+  }
+  forces_rigid_group<G, M, kTvf, kSingleEta, kPin>(P, D, L, list, nlist, ncon, fl, pin_list, any,
+                                                   (size_t)blockIdx.x * kBlock + threadIdx.x);
+}
+
+// the fast pass on an SM-local persistent grid (see k_density_sm); the rigid list is body-major
+template <int M, bool kTvf, bool kSingleEta>
+__global__ void __launch_bounds__(kBlock) k_forces_rigid_sm(const __grid_constant__ DevParams P, Particles D,
+                                                             NbrList L, const uint32_t* __restrict__ list,
+                                                             size_t nlist, const uint32_t* __restrict__ ncon,
+                                                             DevFlags* __restrict__ fl,
+                                                             uint32_t* __restrict__ pin_list,
+                                                             uint32_t* __restrict__ any, uint32_t* __restrict__ next,
+                                                             int nq) {
+  SPHG_SKIP_IF_FLAGGED(P);
+  int q = (int)(sm_id() % (unsigned)nq);
+  size_t tile;
+  while (next_tile(next, nq, (nlist + 7) / 8, q, tile))
+    forces_rigid_group<4, M, kTvf, kSingleEta, false>(P, D, L, list, nlist, ncon, fl, pin_list, any,
+                                                      tile * 32 + (threadIdx.x & 31));
 }
 
 // Verlet candidates and pairs within r_c (exact test), all particles; split by kind of i
@@ -980,6 +1043,9 @@ int blocks_for(size_t groups) {
 // length, so fused and unfused variants of a sum take the same summation order.
 // SPHG_GROUP_DENSITY / SPHG_GROUP_FORCES (2, 4, 8) fix the width for tuning sweeps.
 inline int lanes_for(const Ctx& c, size_t nlist) { return 2 * nlist < c.fill_groups ? 32 : 4; }
+// SM-local persistent grids pay once a list's records no longer sit in L2 as a whole (measured: C3 2.4M and
+// paper46 3.8M neutral, C4 16M and C5 64M faster); below, flat grids
+inline bool sm_local_for(const Ctx& c, int bit, size_t nlist) { return (c.sm_local & bit) && nlist >= c.sm_local_min; }
 #define SPHG_L_DISPATCH(C, NLIST, CALL)                              \
   do {                                                              \
     if (lanes_for(C, NLIST) == 32) { constexpr int G = 32; CALL; }  \
@@ -1019,7 +1085,7 @@ static int sm_local_grid(Ctx& c, K kernel, uint32_t* next, cudaStream_t st) {
 static void launch_density_list(Ctx& c, const uint32_t* list, size_t m, cudaStream_t st) {
   if (m == 0) return;
   const int gd = c.group_density ? c.group_density : lanes_for(c, m);
-  if ((c.sm_local & 2) && (gd == 4 || gd == 8)) {
+  if (sm_local_for(c, 2, m) && (gd == 4 || gd == 8)) {
 #define SPHG_DENS_SM(GV)                                                                                            \
   SPHG_IMG_DISPATCH(c.P.img_mode,                                                                                   \
                     (k_density_sm<GV, M><<<sm_local_grid(c, k_density_sm<GV, M>, c.sm_next.p, st), kBlock, 0, st>>>( \
@@ -1121,6 +1187,19 @@ void launch_diffusion(Ctx& c) {
 template <bool kMultiEos>
 static void launch_extrapolate_t(Ctx& c) {
   SPHG_CUDA_CHECK(cudaMemsetAsync(c.pin_any, 0, sizeof(uint32_t), c.stream));
+  if (sm_local_for(c, 4, c.nw) && lanes_for(c, c.nw) == 4) {
+    constexpr int G = 4;
+    uint32_t* next = c.sm_next.p + 2 * c.n_sms;
+    SPHG_IMG_DISPATCH(c.P.img_mode, ({
+      k_extrapolate_sm<M, kMultiEos><<<sm_local_grid(c, k_extrapolate_sm<M, kMultiEos>, next, c.stream), kBlock, 0,
+                                       c.stream>>>(c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw, c.pin_list.p,
+                                                   c.pin_any, next, c.n_sms);
+      k_extrapolate<G, M, kMultiEos, true><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
+          c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw, c.pin_list.p, c.pin_any);
+    }));
+    c.launches += 2;
+    return;
+  }
   SPHG_L_DISPATCH(c, c.nw, SPHG_IMG_DISPATCH(c.P.img_mode, ({
     k_extrapolate<G, M, kMultiEos, false><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
         c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw, c.pin_list.p, c.pin_any);
@@ -1144,7 +1223,7 @@ static void launch_forces_fluid_t(Ctx& c) {
     const bool dif = !c.fuse_heat;
     const double2* sin = dif ? c.cur.C2.p : c.cur.H2.p;
     double2* out = dif ? c.C2new.p : c.H2new.p;
-    if ((c.sm_local & 1) && lanes_for(c, c.nf) == 4)
+    if (sm_local_for(c, 1, c.nf) && lanes_for(c, c.nf) == 4)
       SPHG_IMG_DISPATCH(c.P.img_mode,
                         (k_forces_fluid_sm<4, M, kTvf, kSingleEta, true>
                          <<<sm_local_grid(c, k_forces_fluid_sm<4, M, kTvf, kSingleEta, true>, next, c.stream), kBlock, 0,
@@ -1164,8 +1243,8 @@ static void launch_forces_fluid_t(Ctx& c) {
                      <<<sm_local_grid(c, k_forces_fluid_sm<GV, M, kTvf, kSingleEta, false>, next, c.stream), kBlock, \
                         0, c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, next, c.n_sms, nullptr,         \
                                        nullptr, 0)))
-  if (c.nf && (c.sm_local & 1) && gf == 4) SPHG_FORCES_SM(4);
-  else if (c.nf && (c.sm_local & 1) && gf == 8) SPHG_FORCES_SM(8);
+  if (c.nf && sm_local_for(c, 1, c.nf) && gf == 4) SPHG_FORCES_SM(4);
+  else if (c.nf && sm_local_for(c, 1, c.nf) && gf == 8) SPHG_FORCES_SM(8);
 #undef SPHG_FORCES_SM
   else if (c.nf)
     SPHG_G_DISPATCH(c, c.group_forces, c.nf,
@@ -1186,9 +1265,23 @@ static void launch_forces_rigid_t(Ctx& c) {
     k_forces_rigid<G, M, kTvf, SE, true><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(                 \
         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags, c.pin_list.p, c.pin_any);                     \
   })))
-  if (c.P.single_eta) SPHG_RIGID_PAIR(true);
+#define SPHG_RIGID_PAIR_SM(SE)                                                                              \
+  SPHG_IMG_DISPATCH(c.P.img_mode, ({                                                                        \
+    constexpr int G = 4;                                                                                    \
+    uint32_t* next = c.sm_next.p + 3 * c.n_sms;                                                             \
+    k_forces_rigid_sm<M, kTvf, SE><<<sm_local_grid(c, k_forces_rigid_sm<M, kTvf, SE>, next, c.stream), kBlock, 0, \
+                                     c.stream>>>(c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags,  \
+                                                 c.pin_list.p, c.pin_any, next, c.n_sms);                    \
+    k_forces_rigid<G, M, kTvf, SE, true><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(                 \
+        c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags, c.pin_list.p, c.pin_any);               \
+  }))
+  const bool sm = sm_local_for(c, 8, c.nrigid) && lanes_for(c, c.nrigid) == 4;
+  if (sm && c.P.single_eta) SPHG_RIGID_PAIR_SM(true);
+  else if (sm) SPHG_RIGID_PAIR_SM(false);
+  else if (c.P.single_eta) SPHG_RIGID_PAIR(true);
   else SPHG_RIGID_PAIR(false);
 #undef SPHG_RIGID_PAIR
+#undef SPHG_RIGID_PAIR_SM
   c.launches += 2;
 }
 
