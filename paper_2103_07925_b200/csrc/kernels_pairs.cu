@@ -159,33 +159,38 @@ __device__ __forceinline__ unsigned sm_id() {
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
   return r;
 }
-// the next tile (32 list slots' worth of lanes) for this warp, or false when every range is finished.  Own
-// range first; when it is exhausted the 32 lanes probe 32 other counters at a time (L2 reads: a counter only
-// grows, so a stale value can only show work that is already gone, which the atomic then finds out).
-__device__ __forceinline__ bool next_tile(uint32_t* __restrict__ next, int nq, size_t ntiles, int& q, size_t& tile) {
+// A range with tiles left, searched from q + 1 on, or -1: the 32 lanes probe 32 counters at a time (L2 reads:
+// a counter only grows, so a stale value can only show work that is already gone, which the caller's atomic
+// then finds out).  Out of line: the steal path must not shape the register allocation of the pair loops.
+__device__ __noinline__ int find_range(const uint32_t* next, int nq, size_t ntiles, int q) {
   const int lw = threadIdx.x & 31;
+  for (int base = 1; base < nq; base += 32) {
+    bool has = false;
+    if (base + lw < nq) {
+      const int qq = (q + base + lw) % nq;
+      const size_t a0 = ntiles * (size_t)qq / nq, a1 = ntiles * (size_t)(qq + 1) / nq;
+      has = a0 + __ldcg(&next[qq]) < a1;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, has);
+    if (m) return (q + base + __ffs((int)m) - 1) % nq;
+  }
+  return -1;
+}
+// the next tile (32 list slots' worth of lanes) for this warp, or false when every range is finished: the
+// current range first (the SM's own until it is exhausted), then the nearest following range with work
+__device__ __forceinline__ bool next_tile(uint32_t* __restrict__ next, int nq, size_t ntiles, int& q, size_t& tile) {
   for (;;) {
     const size_t q0 = ntiles * (size_t)q / nq, q1 = ntiles * (size_t)(q + 1) / nq;
     uint32_t t = 0;
-    if (lw == 0) t = atomicAdd(&next[q], 1u);
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(&next[q], 1u);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (q0 + t < q1) {
       tile = q0 + t;
       return true;
     }
-    int found = -1;
-    for (int base = 1; base < nq && found < 0; base += 32) {
-      bool has = false;
-      if (base + lw < nq) {
-        const int qq = (q + base + lw) % nq;
-        const size_t a0 = ntiles * (size_t)qq / nq, a1 = ntiles * (size_t)(qq + 1) / nq;
-        has = a0 + __ldcg(&next[qq]) < a1;
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, has);
-      if (m) found = (q + base + __ffs((int)m) - 1) % nq;
-    }
-    if (found < 0) return false;
-    q = found;
+    const int f = find_range(next, nq, ntiles, q);
+    if (f < 0) return false;
+    q = f;
   }
 }
 template <int G, int M>
@@ -1043,8 +1048,9 @@ int blocks_for(size_t groups) {
 // length, so fused and unfused variants of a sum take the same summation order.
 // SPHG_GROUP_DENSITY / SPHG_GROUP_FORCES (2, 4, 8) fix the width for tuning sweeps.
 inline int lanes_for(const Ctx& c, size_t nlist) { return 2 * nlist < c.fill_groups ? 32 : 4; }
-// SM-local persistent grids pay once a list's records no longer sit in L2 as a whole (measured: C3 2.4M and
-// paper46 3.8M neutral, C4 16M and C5 64M faster); below, flat grids
+// SM-local persistent grids pay for long lists (measured against flat grids: C3 2.4M -2.5 %, paper46 3.8M
+// -8 %, C5 8M -5 %, C4 16M -3 %, C5 64M -6 % per step; C1 32k and C2 343k lose to the persistent grid's
+// fixed costs); shorter lists keep flat grids
 inline bool sm_local_for(const Ctx& c, int bit, size_t nlist) { return (c.sm_local & bit) && nlist >= c.sm_local_min; }
 #define SPHG_L_DISPATCH(C, NLIST, CALL)                              \
   do {                                                              \
