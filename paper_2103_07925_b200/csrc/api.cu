@@ -1144,7 +1144,7 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
     c.n_sms = sms;
     if (const char* e = std::getenv("SPHG_SM_LOCAL")) c.sm_local = std::atoi(e);
     if (const char* e = std::getenv("SPHG_SM_LOCAL_MIN")) c.sm_local_min = (size_t)std::atoll(e);
-    c.sm_next.alloc(4 * (size_t)sms);  // density, fluid forces, extrapolation, rigid forces
+    c.sm_next.alloc(5 * (size_t)sms);  // density, fluid forces, extrapolation, rigid forces, interior density
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     SPHG_CUDA_CHECK(cudaMalloc(&c.dflags, sizeof(DevFlags)));
     SPHG_CUDA_CHECK(cudaMemset(c.dflags, 0, sizeof(DevFlags)));

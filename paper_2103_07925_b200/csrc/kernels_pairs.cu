@@ -1088,14 +1088,17 @@ static int sm_local_grid(Ctx& c, K kernel, uint32_t* next, cudaStream_t st) {
   return per_sm * c.n_sms;
 }
 
-static void launch_density_list(Ctx& c, const uint32_t* list, size_t m, cudaStream_t st) {
+// slot: which counter array a persistent grid uses (0 density, 4 the interior density pass that overlaps the
+// STATE halo on its own stream; 1-3 belong to the forces / extrapolation kernels)
+static void launch_density_list(Ctx& c, const uint32_t* list, size_t m, cudaStream_t st, int slot = 0) {
   if (m == 0) return;
   const int gd = c.group_density ? c.group_density : lanes_for(c, m);
   if (sm_local_for(c, 2, m) && (gd == 4 || gd == 8)) {
+    uint32_t* next = c.sm_next.p + (size_t)slot * c.n_sms;
 #define SPHG_DENS_SM(GV)                                                                                            \
   SPHG_IMG_DISPATCH(c.P.img_mode,                                                                                   \
-                    (k_density_sm<GV, M><<<sm_local_grid(c, k_density_sm<GV, M>, c.sm_next.p, st), kBlock, 0, st>>>( \
-                        c.P, c.cur, c.nl(), list, m, c.sm_next.p, c.n_sms)))
+                    (k_density_sm<GV, M><<<sm_local_grid(c, k_density_sm<GV, M>, next, st), kBlock, 0, st>>>(        \
+                        c.P, c.cur, c.nl(), list, m, next, c.n_sms)))
     if (gd == 8) SPHG_DENS_SM(8);
     else SPHG_DENS_SM(4);
 #undef SPHG_DENS_SM
@@ -1112,7 +1115,7 @@ void launch_density(Ctx& c) { launch_density_list(c, c.fidx.p, c.nf, c.stream); 
 
 // decomposed steps: the fluid list is ordered [interior | next to a ghost] (launch_ghost_split); the
 // interior part reads only owned neighbours, so it runs before the STATE halo has landed
-void launch_density_interior(Ctx& c, cudaStream_t st) { launch_density_list(c, c.fidx.p, c.nf_interior, st); }
+void launch_density_interior(Ctx& c, cudaStream_t st) { launch_density_list(c, c.fidx.p, c.nf_interior, st, 4); }
 void launch_density_boundary(Ctx& c) {
   launch_density_list(c, c.fidx.p + c.nf_interior, c.nf - c.nf_interior, c.stream);
 }

@@ -287,3 +287,14 @@ def test_cpp_nccl_transport_single_rank():
     assert os.path.exists(exe), "build() compiles tests/cpp (make -C tests/cpp)"
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok nccl transport" in r.stdout, r.stdout + r.stderr
+
+
+def test_gpu_two_ranks_sm_local_grids(tmp_path, monkeypatch):
+    """The decomposed step with the SM-local persistent grids forced on its short lists (SPHG_SM_LOCAL_MIN=0,
+    4 lanes per particle): the interior density pass (own stream, own tile counters) overlaps the STATE halo
+    and the boundary density pass; rebuilds and a repartition included.  Same checks as the flat grids."""
+    monkeypatch.setenv("SPHG_SM_LOCAL_MIN", "0")
+    monkeypatch.setenv("SPHG_GROUP_DENSITY", "4")
+    monkeypatch.setenv("SPHG_GROUP_FORCES", "4")
+    test_gpu_two_ranks_match_single_rank("c1fast", tmp_path)
+    test_gpu_two_ranks_match_single_rank("c2", tmp_path)
