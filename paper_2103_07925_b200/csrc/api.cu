@@ -1141,10 +1141,11 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
     int sms = 148;
     SPHG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     c.fill_groups = (size_t)sms * 2048 / 4 / 2;
+    if (const char* e = std::getenv("SPHG_FILL_GROUPS")) c.fill_groups = (size_t)std::atoll(e);  // tests: 0 = always 4 lanes
     c.n_sms = sms;
     if (const char* e = std::getenv("SPHG_SM_LOCAL")) c.sm_local = std::atoi(e);
     if (const char* e = std::getenv("SPHG_SM_LOCAL_MIN")) c.sm_local_min = (size_t)std::atoll(e);
-    c.sm_next.alloc(5 * (size_t)sms);  // density, fluid forces, extrapolation, rigid forces, interior density
+    c.sm_next.alloc(6 * (size_t)sms);  // density, fluid forces, extrapolation, rigid forces, interior density, heat
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     SPHG_CUDA_CHECK(cudaMalloc(&c.dflags, sizeof(DevFlags)));
     SPHG_CUDA_CHECK(cudaMemset(c.dflags, 0, sizeof(DevFlags)));

@@ -104,11 +104,11 @@ struct Ctx {
   int cap = 0;
   NbrList nl() const { return {nbr.p, cnt.p, (size_t)cap}; }
   // SM-local persistent pair kernels (SPHG_SM_LOCAL: bit 0 = fluid forces, bit 1 = density, bit 2 =
-  // extrapolation, bit 3 = rigid forces; 0 = flat grids)
-  int sm_local = 15, n_sms = 148;
+  // extrapolation, bit 3 = rigid forces, bit 4 = conduction; 0 = flat grids)
+  int sm_local = 31, n_sms = 148;
   size_t sm_local_min = 1u << 20;  // shortest list that gets a persistent grid (SPHG_SM_LOCAL_MIN)
   DBuf<uint32_t> sm_next;  // per-SM tile counters, n_sms each: density, fluid forces, extrapolation, rigid
-                           // forces, interior density (kernels that may run concurrently never share one)
+                           // forces, interior density, conduction (kernels that may run concurrently never share one)
   // per-kind index lists: fluid, non-fluid (rigid + boundary), rigid body-major
   DBuf<uint32_t> fidx, widx, ridx, body_start;
   DBuf<uint32_t> ncon;  // per rigid particle: contact candidates at the front of its non-fluid row part

@@ -210,11 +210,9 @@ __global__ void __launch_bounds__(kBlock) k_density_sm(const __grid_constant__ D
 // c_p,a dT_a/dt = (1/rho_a) sum_b V_b 4 k_a k_b/(k_a+k_b) (T_ab/r_ab) dW/dr (Cleary & Monaghan).
 // b over fluid, rigid and Dirichlet boundary particles (V_heat == 0 marks the others).
 template <int G, int M>
-__global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevParams P, Particles D, NbrList L,
-                                                  const uint32_t* __restrict__ list, size_t nlist,
-                                                  double2* __restrict__ Hout, DevFlags* __restrict__ fl) {
-  SPHG_SKIP_IF_FLAGGED(P);
-  const size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x;
+__device__ __forceinline__ void heat_group(const DevParams& P, const Particles& D, const NbrList& L,
+                                           const uint32_t* __restrict__ list, size_t nlist,
+                                           double2* __restrict__ Hout, DevFlags* __restrict__ fl, size_t t) {
   const size_t g = t / G;
   const int lane = (int)(t % G);
   const bool active = g < nlist;
@@ -274,6 +272,27 @@ __global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevPara
   }
   Hout[i] = make_double2(hi.x + P.dt * rate, hi.y);
   D.dTdt.p[i] = rate;
+}
+
+template <int G, int M>
+__global__ void __launch_bounds__(kBlock) k_heat(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                  const uint32_t* __restrict__ list, size_t nlist,
+                                                  double2* __restrict__ Hout, DevFlags* __restrict__ fl) {
+  SPHG_SKIP_IF_FLAGGED(P);
+  heat_group<G, M>(P, D, L, list, nlist, Hout, fl, (size_t)blockIdx.x * kBlock + threadIdx.x);
+}
+
+// on an SM-local persistent grid (see k_density_sm); the rigid list is body-major, a grain's particles adjacent
+template <int M>
+__global__ void __launch_bounds__(kBlock) k_heat_sm(const __grid_constant__ DevParams P, Particles D, NbrList L,
+                                                     const uint32_t* __restrict__ list, size_t nlist,
+                                                     double2* __restrict__ Hout, DevFlags* __restrict__ fl,
+                                                     uint32_t* __restrict__ next, int nq) {
+  SPHG_SKIP_IF_FLAGGED(P);
+  int q = (int)(sm_id() % (unsigned)nq);
+  size_t tile;
+  while (next_tile(next, nq, (nlist + 7) / 8, q, tile))
+    heat_group<4, M>(P, D, L, list, nlist, Hout, fl, tile * 32 + (threadIdx.x & 31));
 }
 
 // ------------------------------------------------------- surface heat flux
@@ -1136,12 +1155,20 @@ void launch_heat_begin(Ctx& c) {
                                        c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, t_new, c.capturing ? c.dtime : nullptr)));
     c.launches += 2;
   }
-  if (c.nf && !c.fuse_heat)
-    SPHG_L_DISPATCH(c, c.nf, SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nf), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.H2new.p, c.dflags))));
-  if (c.nrigid)
-    SPHG_L_DISPATCH(c, c.nrigid, SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(
-                                         c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.H2new.p, c.dflags))));
+  // (the two launches run one after the other on the stream: they share a counter array)
+  auto heat_list = [&](const uint32_t* list, size_t m) {
+    if (sm_local_for(c, 16, m) && lanes_for(c, m) == 4) {
+      uint32_t* next = c.sm_next.p + 5 * (size_t)c.n_sms;
+      SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat_sm<M><<<sm_local_grid(c, k_heat_sm<M>, next, c.stream), kBlock, 0,
+                                                    c.stream>>>(c.P, c.cur, c.nl(), list, m, c.H2new.p, c.dflags,
+                                                                next, c.n_sms)));
+    } else {
+      SPHG_L_DISPATCH(c, m, SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat<G, M><<<blocks_for<G>(m), kBlock, 0, c.stream>>>(
+                                           c.P, c.cur, c.nl(), list, m, c.H2new.p, c.dflags))));
+    }
+  };
+  if (c.nf && !c.fuse_heat) heat_list(c.fidx.p, c.nf);
+  if (c.nrigid) heat_list(c.ridx.p, c.nrigid);
   c.launches += 3;
 }
 

@@ -841,11 +841,11 @@ def test_full_size_parity(case, Oracle):
     step_from_identical_inputs(sim, orc, Oracle, sc.params, f"{case} step1")
 
 
-@pytest.mark.parametrize("name,steps", [("c1", 30), ("c1_small", 12), ("c3_small", 8), ("c2_melt", 6)])
+@pytest.mark.parametrize("name,steps", [("c1", 30), ("c1_small", 12), ("c3_small", 8), ("c2_melt", 6), ("c4_small", 5)])
 def test_sm_local_grids_bit_identical(monkeypatch, name, steps):
     """The 4-lane pair passes of long lists run as SM-local persistent grids (per-SM tile queues over the
-    brick-ordered lists; density, fluid forces with and without the fused conduction, and — SPHG_SM_LOCAL
-    bits 2, 3 — extrapolation and rigid forces); a context created with SPHG_SM_LOCAL=0 uses flat grids.
+    brick-ordered lists; density, fluid forces with and without the fused conduction, extrapolation, rigid
+    forces and conduction); a context created with SPHG_SM_LOCAL=0 uses flat grids.
     Every particle is summed by the same lanes in the same order, so the states are identical bit for bit,
     across rebuilds, transitions and CUDA-graph replay.  Forced here for short lists (SPHG_SM_LOCAL_MIN=0)
     and 4 lanes per particle."""
@@ -855,7 +855,8 @@ def test_sm_local_grids_bit_identical(monkeypatch, name, steps):
     monkeypatch.setenv("SPHG_GROUP_DENSITY", "4")
     monkeypatch.setenv("SPHG_GROUP_FORCES", "4")
     monkeypatch.setenv("SPHG_SM_LOCAL_MIN", "0")
-    monkeypatch.setenv("SPHG_SM_LOCAL", "15")
+    monkeypatch.setenv("SPHG_FILL_GROUPS", "0")  # 4 lanes per particle for the short wall / rigid lists too
+    monkeypatch.setenv("SPHG_SM_LOCAL", "31")
     a = sim_factory(sc.params)
     monkeypatch.setenv("SPHG_SM_LOCAL", "0")
     b = sim_factory(sc.params)
