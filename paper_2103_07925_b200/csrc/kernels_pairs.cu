@@ -1102,6 +1102,8 @@ static int sm_local_grid(Ctx& c, K kernel, uint32_t* next, cudaStream_t st) {
       SPHG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)));
     SPHG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
     per_sm = std::max(per_sm, 1);
+    if (const char* e = std::getenv("SPHG_SM_BLOCKS"))  // experiment: fewer resident blocks per SM than fit
+      per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
   }
   SPHG_CUDA_CHECK(cudaMemsetAsync(next, 0, c.n_sms * sizeof(uint32_t), st));
   return per_sm * c.n_sms;
