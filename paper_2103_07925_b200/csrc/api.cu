@@ -139,6 +139,7 @@ DevParams make_dev_params(const sphg_params& p) {
     if (s.c > 0.0 && s.nu >= 0.0) {  // a fluid-capable material
       if (first_fluid) {
         eta0 = d.eta;
+        P.eta_single = d.eta;
         rho00 = s.rho0;
         c0 = s.c;
         first_fluid = false;

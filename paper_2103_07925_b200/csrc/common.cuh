@@ -49,6 +49,7 @@ struct DevParams {
   double Ir_over_m;     // particle inertia / mass
   int32_t tvf, thermal, transitions, default_fluid_mat;
   int32_t single_eta;   // all fluid materials share eta   -> eta~ = eta_i
+  double eta_single;    // that shared eta (read from the parameter bank instead of a register per thread)
   int32_t single_kappa; // all materials share kappa       -> kappa~ = 2 kappa
   int32_t single_eos;   // all fluid materials share rho0,c -> wall EOS material fixed
   int32_t img_mode;     // neighbour-entry image mode (kImgNone / kImgCode / kImgMin)

@@ -664,7 +664,7 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
   const double pw = -fma(rho_j, I.p, I.rho * p_j) * rcp_fast(I.rho + rho_j) * w;
   double et;
   if (kSingleEta) {
-    et = I.eta;  // 2 eta eta / (eta + eta)
+    et = P.eta_single;  // 2 eta eta / (eta + eta), eta of every fluid material
   } else {
     const uint32_t kj = __ldg(&D.kmd.p[nb_index<M>(e)]);
     const double eta_j = kind_of(kj) == SPHG_FLUID ? P.mat[mat_of(kj)].eta : I.eta;  // eta_w := eta_i [P7]

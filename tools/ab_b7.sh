@@ -1,0 +1,6 @@
+# fluid forces at 7 resident blocks per SM (72 registers, 32 B spilled) against 6 (80 registers), 64M
+for v in "" _b7; do
+  SPHG_LIB=libsphg$v.so timeout 900 python bench.py --steps 30 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/abb7$v.log 2>&1
+  tail -1 gpurun_out/abb7$v.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('lib$v', round(d['ms_per_step'],2), {k: round(v,2) for k,v in d['stage_ms'].items() if k in ('density','forces_fluid','extrapolate','forces_rigid')})"
+done
+echo done
