@@ -119,6 +119,49 @@ __host__ __device__ __forceinline__ int64_t brick_to_cell(const int32_t* nc, int
   return (cx * nc[1] + cy) * nc[2] + cz;
 }
 
+// ------------------------------------------------ SM-local tile queues
+// Work distribution of the persistent (SM-local) kernels: a list of ntiles tiles is cut into nq contiguous
+// ranges, one per SM (%smid), each with a counter in next[] (zeroed before the launch); see kernels_pairs.cu.
+__device__ __forceinline__ unsigned sm_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+// A range with tiles left, searched from q + 1 on, or -1: the 32 lanes probe 32 counters at a time (L2 reads:
+// a counter only grows, so a stale value can only show work that is already gone, which the caller's atomic
+// then finds out).  Out of line: the steal path must not shape the register allocation of the pair loops.
+static __device__ __noinline__ int find_range(const uint32_t* next, int nq, size_t ntiles, int q) {
+  const int lw = threadIdx.x & 31;
+  for (int base = 1; base < nq; base += 32) {
+    bool has = false;
+    if (base + lw < nq) {
+      const int qq = (q + base + lw) % nq;
+      const size_t a0 = ntiles * (size_t)qq / nq, a1 = ntiles * (size_t)(qq + 1) / nq;
+      has = a0 + __ldcg(&next[qq]) < a1;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, has);
+    if (m) return (q + base + __ffs((int)m) - 1) % nq;
+  }
+  return -1;
+}
+// the next tile (32 list slots' worth of lanes) for this warp, or false when every range is finished: the
+// current range first (the SM's own until it is exhausted), then the nearest following range with work
+__device__ __forceinline__ bool next_tile(uint32_t* __restrict__ next, int nq, size_t ntiles, int& q, size_t& tile) {
+  for (;;) {
+    const size_t q0 = ntiles * (size_t)q / nq, q1 = ntiles * (size_t)(q + 1) / nq;
+    uint32_t t = 0;
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(&next[q], 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (q0 + t < q1) {
+      tile = q0 + t;
+      return true;
+    }
+    const int f = find_range(next, nq, ntiles, q);
+    if (f < 0) return false;
+    q = f;
+  }
+}
+
 // ---------------------------------------------------------------- tags
 // kmd word: bits 0-1 kind, 2-7 material, 8-15 temperature Dirichlet group, 16 ghost,
 // 24-31 concentration Dirichlet group (0xff none for both groups)

@@ -147,52 +147,14 @@ __global__ void __launch_bounds__(kBlock) k_density(const __grid_constant__ DevP
   density_group<G, M>(P, D, L, list, nlist, t / G, (int)(t % G));
 }
 
-// SM-local persistent variants (the 4-lane density and fluid forces passes; SPHG_SM_LOCAL=0 restores one
-// group per thread of a flat grid): the list is cut into one contiguous range per SM and the resident warps
+// SM-local persistent variants (the 4-lane density, fluid forces, extrapolation, rigid forces and conduction
+// passes over lists of sm_local_min particles or more; SPHG_SM_LOCAL=0 restores one group per thread of a
+// flat grid): the list is cut into one contiguous range per SM and the resident warps
 // of an SM take 8-particle tiles of its range in order (next[q], zeroed before the launch).  The list is in
 // brick order (2x2x2 blocks of cells, common.cuh), so the ~190 particles in flight on an SM share one
 // 4x4x4-cell neighbourhood that stays in that SM's L1, where a flat grid's co-resident blocks sit 148 blocks
 // apart in the list.  A warp whose range is finished helps the next ranges.  Each particle is still summed by
 // its own 4 lanes in row order: results are bit-identical to the flat grid's.
-__device__ __forceinline__ unsigned sm_id() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-  return r;
-}
-// A range with tiles left, searched from q + 1 on, or -1: the 32 lanes probe 32 counters at a time (L2 reads:
-// a counter only grows, so a stale value can only show work that is already gone, which the caller's atomic
-// then finds out).  Out of line: the steal path must not shape the register allocation of the pair loops.
-__device__ __noinline__ int find_range(const uint32_t* next, int nq, size_t ntiles, int q) {
-  const int lw = threadIdx.x & 31;
-  for (int base = 1; base < nq; base += 32) {
-    bool has = false;
-    if (base + lw < nq) {
-      const int qq = (q + base + lw) % nq;
-      const size_t a0 = ntiles * (size_t)qq / nq, a1 = ntiles * (size_t)(qq + 1) / nq;
-      has = a0 + __ldcg(&next[qq]) < a1;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, has);
-    if (m) return (q + base + __ffs((int)m) - 1) % nq;
-  }
-  return -1;
-}
-// the next tile (32 list slots' worth of lanes) for this warp, or false when every range is finished: the
-// current range first (the SM's own until it is exhausted), then the nearest following range with work
-__device__ __forceinline__ bool next_tile(uint32_t* __restrict__ next, int nq, size_t ntiles, int& q, size_t& tile) {
-  for (;;) {
-    const size_t q0 = ntiles * (size_t)q / nq, q1 = ntiles * (size_t)(q + 1) / nq;
-    uint32_t t = 0;
-    if ((threadIdx.x & 31) == 0) t = atomicAdd(&next[q], 1u);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (q0 + t < q1) {
-      tile = q0 + t;
-      return true;
-    }
-    const int f = find_range(next, nq, ntiles, q);
-    if (f < 0) return false;
-    q = f;
-  }
-}
 template <int G, int M>
 __global__ void __launch_bounds__(kBlock) k_density_sm(const __grid_constant__ DevParams P, Particles D, NbrList L,
                                                         const uint32_t* __restrict__ list, size_t nlist,
