@@ -1146,6 +1146,10 @@ int sphg_create(const sphg_params* p, int device, sphg_ctx** out) {
     c.n_sms = sms;
     if (const char* e = std::getenv("SPHG_SM_LOCAL")) c.sm_local = std::atoi(e);
     if (const char* e = std::getenv("SPHG_SM_LOCAL_MIN")) c.sm_local_min = (size_t)std::atoll(e);
+    if (const char* e = std::getenv("SPHG_SM_THREADS")) {
+      const int t = std::atoi(e);
+      if (t == 32 || t == 64 || t == 128) c.sm_threads = t;
+    }
     c.sm_next.alloc(6 * (size_t)sms);  // density, fluid forces, extrapolation, rigid forces, interior density, heat
     SPHG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     SPHG_CUDA_CHECK(cudaMalloc(&c.dflags, sizeof(DevFlags)));

@@ -106,6 +106,7 @@ struct Ctx {
   // SM-local persistent pair kernels (SPHG_SM_LOCAL: bit 0 = fluid forces, bit 1 = density, bit 2 =
   // extrapolation, bit 3 = rigid forces, bit 4 = conduction; 0 = flat grids)
   int sm_local = 31, n_sms = 148;
+  int sm_threads = 128;            // block size of the persistent grids (SPHG_SM_THREADS: 32, 64, 128)
   size_t sm_local_min = 1u << 20;  // shortest list that gets a persistent grid (SPHG_SM_LOCAL_MIN)
   DBuf<uint32_t> sm_next;  // per-SM tile counters, n_sms each: density, fluid forces, extrapolation, rigid
                            // forces, interior density, conduction (kernels that may run concurrently never share one)

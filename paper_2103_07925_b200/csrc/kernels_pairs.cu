@@ -1062,7 +1062,7 @@ static int sm_local_grid(Ctx& c, K kernel, uint32_t* next, cudaStream_t st) {
   if (per_sm == 0) {
     if (const char* e = std::getenv("SPHG_SMEM_CARVEOUT"))  // experiment: shared-memory share of the L1 array, %
       SPHG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)));
-    SPHG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+    SPHG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, c.sm_threads, 0));
     per_sm = std::max(per_sm, 1);
     if (const char* e = std::getenv("SPHG_SM_BLOCKS"))  // experiment: fewer resident blocks per SM than fit
       per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
@@ -1080,7 +1080,7 @@ static void launch_density_list(Ctx& c, const uint32_t* list, size_t m, cudaStre
     uint32_t* next = c.sm_next.p + (size_t)slot * c.n_sms;
 #define SPHG_DENS_SM(GV)                                                                                            \
   SPHG_IMG_DISPATCH(c.P.img_mode,                                                                                   \
-                    (k_density_sm<GV, M><<<sm_local_grid(c, k_density_sm<GV, M>, next, st), kBlock, 0, st>>>(        \
+                    (k_density_sm<GV, M><<<sm_local_grid(c, k_density_sm<GV, M>, next, st), c.sm_threads, 0, st>>>(        \
                         c.P, c.cur, c.nl(), list, m, next, c.n_sms)))
     if (gd == 8) SPHG_DENS_SM(8);
     else SPHG_DENS_SM(4);
@@ -1123,7 +1123,7 @@ void launch_heat_begin(Ctx& c) {
   auto heat_list = [&](const uint32_t* list, size_t m) {
     if (sm_local_for(c, 16, m) && lanes_for(c, m) == 4) {
       uint32_t* next = c.sm_next.p + 5 * (size_t)c.n_sms;
-      SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat_sm<M><<<sm_local_grid(c, k_heat_sm<M>, next, c.stream), kBlock, 0,
+      SPHG_IMG_DISPATCH(c.P.img_mode, (k_heat_sm<M><<<sm_local_grid(c, k_heat_sm<M>, next, c.stream), c.sm_threads, 0,
                                                     c.stream>>>(c.P, c.cur, c.nl(), list, m, c.H2new.p, c.dflags,
                                                                 next, c.n_sms)));
     } else {
@@ -1191,7 +1191,7 @@ static void launch_extrapolate_t(Ctx& c) {
     constexpr int G = 4;
     uint32_t* next = c.sm_next.p + 2 * c.n_sms;
     SPHG_IMG_DISPATCH(c.P.img_mode, ({
-      k_extrapolate_sm<M, kMultiEos><<<sm_local_grid(c, k_extrapolate_sm<M, kMultiEos>, next, c.stream), kBlock, 0,
+      k_extrapolate_sm<M, kMultiEos><<<sm_local_grid(c, k_extrapolate_sm<M, kMultiEos>, next, c.stream), c.sm_threads, 0,
                                        c.stream>>>(c.P, c.cur, c.nl(), c.bodies.p, c.widx.p, c.nw, c.pin_list.p,
                                                    c.pin_any, next, c.n_sms);
       k_extrapolate<G, M, kMultiEos, true><<<blocks_for<G>(c.nw), kBlock, 0, c.stream>>>(
@@ -1226,7 +1226,7 @@ static void launch_forces_fluid_t(Ctx& c) {
     if (sm_local_for(c, 1, c.nf) && lanes_for(c, c.nf) == 4)
       SPHG_IMG_DISPATCH(c.P.img_mode,
                         (k_forces_fluid_sm<4, M, kTvf, kSingleEta, true>
-                         <<<sm_local_grid(c, k_forces_fluid_sm<4, M, kTvf, kSingleEta, true>, next, c.stream), kBlock, 0,
+                         <<<sm_local_grid(c, k_forces_fluid_sm<4, M, kTvf, kSingleEta, true>, next, c.stream), c.sm_threads, 0,
                             c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, next, c.n_sms, out, sin,
                                         dif ? 1 : 0)));
     else
@@ -1240,7 +1240,7 @@ static void launch_forces_fluid_t(Ctx& c) {
 #define SPHG_FORCES_SM(GV)                                                                                          \
   SPHG_IMG_DISPATCH(c.P.img_mode,                                                                                   \
                     (k_forces_fluid_sm<GV, M, kTvf, kSingleEta, false>                                              \
-                     <<<sm_local_grid(c, k_forces_fluid_sm<GV, M, kTvf, kSingleEta, false>, next, c.stream), kBlock, \
+                     <<<sm_local_grid(c, k_forces_fluid_sm<GV, M, kTvf, kSingleEta, false>, next, c.stream), c.sm_threads, \
                         0, c.stream>>>(c.P, c.cur, c.nl(), c.fidx.p, c.nf, c.dflags, next, c.n_sms, nullptr,         \
                                        nullptr, 0)))
   if (c.nf && sm_local_for(c, 1, c.nf) && gf == 4) SPHG_FORCES_SM(4);
@@ -1269,7 +1269,7 @@ static void launch_forces_rigid_t(Ctx& c) {
   SPHG_IMG_DISPATCH(c.P.img_mode, ({                                                                        \
     constexpr int G = 4;                                                                                    \
     uint32_t* next = c.sm_next.p + 3 * c.n_sms;                                                             \
-    k_forces_rigid_sm<M, kTvf, SE><<<sm_local_grid(c, k_forces_rigid_sm<M, kTvf, SE>, next, c.stream), kBlock, 0, \
+    k_forces_rigid_sm<M, kTvf, SE><<<sm_local_grid(c, k_forces_rigid_sm<M, kTvf, SE>, next, c.stream), c.sm_threads, 0, \
                                      c.stream>>>(c.P, c.cur, c.nl(), c.ridx.p, c.nrigid, c.ncon.p, c.dflags,  \
                                                  c.pin_list.p, c.pin_any, next, c.n_sms);                    \
     k_forces_rigid<G, M, kTvf, SE, true><<<blocks_for<G>(c.nrigid), kBlock, 0, c.stream>>>(                 \
