@@ -1,4 +1,5 @@
-# A/B of the in-range pair masks (density pass -> fluid forces pass) at 64M, plus the suites they touch
+# A/B of the in-range pair masks (density pass -> fluid forces pass) at 64M; the knob SPHG_PAIR_MASK existed only in the
+# experiment (reverted, profiles/r02_experiments.json pair_masks_64M): kept as the record of what was run
 for m in 0 1; do
   SPHG_PAIR_MASK=$m timeout 900 python bench.py --steps 30 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ab_mask_$m.log 2>&1
   tail -1 gpurun_out/ab_mask_$m.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('mask=$m', d['ms_per_step'], {k: round(v,2) for k,v in d['stage_ms'].items()})"
