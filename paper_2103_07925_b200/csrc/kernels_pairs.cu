@@ -579,9 +579,9 @@ __device__ __forceinline__ void pair_term(const PairSide& I, const PairSide& J, 
 }
 
 // Fluid-side pair, with the pair weight w = (V_i^2 + V_j^2) (dW/dr) / r factored out of every term:
-//   acc += -p~ w d + eta~ w (u_i - u_j) + w (rho_j/2) (du_j . d) u_j,   bg += w d.
-// The i-side TVF term (1/2) A_i gradW summed over j equals (rho_i/2) u_i (du_i . bg): it is applied
-// once per particle from bg (k_forces_fluid), not per pair.
+//   acc += -p~ w d - eta~ w u_j + w (rho_j/2) (du_j . d) u_j,   svf += eta~ w,   bg += w d.
+// The i-side TVF term (1/2) A_i gradW summed over j equals (rho_i/2) u_i (du_i . bg), and the i-side of
+// the viscous sum is u_i svf: both are applied once per particle (forces_fluid_group), not per pair.
 // conduction folded into the fluid forces pass (one row walk; see launch_heat_begin): T_i, kappa_i
 // of the fluid particle and the running sum of k_heat
 // (kHeat with diff = 1: the same fold for the concentration sums of k_diffusion, D for kappa)
@@ -593,7 +593,7 @@ struct HeatSide {
 template <int M, bool kTvf, bool kSingleEta, bool kHeat = false>
 __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
                                            uint32_t e, double4 h0, double4 h1, double4 h2, double3& acc,
-                                           double3& bg, bool& coincident, HeatSide* heat = nullptr,
+                                           double3& bg, double& svf, bool& coincident, HeatSide* heat = nullptr,
                                            double2 hj = double2{0.0, 0.0}) {
   const double3 d = pair_delta<M>(P, pi, ld3(h0), e);
   const double r2 = d.x * d.x + d.y * d.y + d.z * d.z;
@@ -633,10 +633,15 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
     const double es = I.eta + eta_j;
     et = es > 0.0 ? 2.0 * I.eta * eta_j * rcp_fast(es) : 0.0;
   }
+  // viscous sum split: sum_j eta~ w (u_i - u_j) = u_i sum_j eta~ w - sum_j eta~ w u_j.  u_i leaves the row
+  // walk's registers (applied once per particle from svf in forces_fluid_group), which is what lets the
+  // SM-local kernel hold a seventh block per SM; the round-off it adds, ~1e-16 |u| sum |eta~ w|, sits below
+  // that of the pressure terms of the same sum
   const double vf = et * w;
-  acc.x = fma(pw, d.x, fma(vf, I.u.x - h1.x, acc.x));
-  acc.y = fma(pw, d.y, fma(vf, I.u.y - h1.y, acc.y));
-  acc.z = fma(pw, d.z, fma(vf, I.u.z - h1.z, acc.z));
+  svf += vf;
+  acc.x = fma(pw, d.x, fma(-vf, h1.x, acc.x));
+  acc.y = fma(pw, d.y, fma(-vf, h1.y, acc.y));
+  acc.z = fma(pw, d.z, fma(-vf, h1.z, acc.z));
   if (kTvf) {  // wall / rigid records carry du = 0 (A_j = 0)
     const double cj = w * (0.5 * rho_j) * (h2.x * d.x + h2.y * d.y + h2.z * d.z);
     acc.x = fma(cj, h1.x, acc.x);
@@ -650,7 +655,7 @@ __device__ __forceinline__ void fluid_pair(const DevParams& P, const Particles& 
 template <int G, int M, bool kTvf, bool kSingleEta, bool kHeat = false>
 __device__ __forceinline__ void fluid_row(const DevParams& P, const Particles& D, const PairSide& I, double3 pi,
                                           const uint32_t* base, int n, int lane, double3& acc, double3& bg,
-                                          bool& coincident, HeatSide* heat = nullptr,
+                                          double& svf, bool& coincident, HeatSide* heat = nullptr,
                                           const double2* __restrict__ Sin = nullptr) {
   int k = lane;
   uint32_t e = k < n ? ldrow(base + k) : 0u;
@@ -660,7 +665,7 @@ __device__ __forceinline__ void fluid_row(const DevParams& P, const Particles& D
     const double4 h0 = ldg4(&D.G0.p[j]), h1 = ldg4(&D.G1.p[j]), h2 = ldg4(&D.G2.p[j]);
     double2 hj = double2{0.0, 0.0};
     if (kHeat) hj = __ldg(&Sin[j]);
-    fluid_pair<M, kTvf, kSingleEta, kHeat>(P, D, I, pi, e, h0, h1, h2, acc, bg, coincident, heat, hj);
+    fluid_pair<M, kTvf, kSingleEta, kHeat>(P, D, I, pi, e, h0, h1, h2, acc, bg, svf, coincident, heat, hj);
     e = en;
   }
 }
@@ -675,6 +680,7 @@ __device__ __forceinline__ void forces_fluid_group(const DevParams& P, const Par
   const bool active = g < nlist;
   const uint32_t i = active ? list[g] : 0u;
   double3 acc = make_double3(0, 0, 0), bg = make_double3(0, 0, 0);
+  double svf = 0.0;  // sum_j eta~ w of the viscous term (fluid_pair)
   bool coincident = false;
   uint32_t kmd = 0;
   HeatSide heat{0.0, 0.0, 0.0, sdiff};
@@ -699,9 +705,10 @@ __device__ __forceinline__ void forces_fluid_group(const DevParams& P, const Par
     const Row R = row_of(L, i);
     // one pass over the whole contiguous row: wall/rigid records carry du = 0 (A_w = 0) and, with
     // several viscosities, fluid_pair looks up eta_j by kind (eta_w := eta_i)
-    fluid_row<G, M, kTvf, kSingleEta, kHeat>(P, D, I, pi, R.f, R.n, lane, acc, bg, coincident, &heat, Sin);
+    fluid_row<G, M, kTvf, kSingleEta, kHeat>(P, D, I, pi, R.f, R.n, lane, acc, bg, svf, coincident, &heat, Sin);
   }
   if (kHeat) heat.s = gsum<G>(heat.s);
+  svf = gsum<G>(svf);
   acc.x = gsum<G>(acc.x);
   acc.y = gsum<G>(acc.y);
   acc.z = gsum<G>(acc.z);
@@ -714,6 +721,12 @@ __device__ __forceinline__ void forces_fluid_group(const DevParams& P, const Par
     atomicMin(&fl->err_gid, D.gid.p[i]);
   }
   if (lane != 0) return;
+  {  // i-side of the viscous sum: u_i sum_j eta~ w
+    const double4 gu = ldg4(&D.G1.p[i]);
+    acc.x = fma(svf, gu.x, acc.x);
+    acc.y = fma(svf, gu.y, acc.y);
+    acc.z = fma(svf, gu.z, acc.z);
+  }
   if (kTvf) {  // i-side TVF term: (rho_i/2) u_i (du_i . sum_j (V_i^2+V_j^2) gradW)
     const double4 g1 = ldg4(&D.G1.p[i]), g2 = ldg4(&D.G2.p[i]);
     const double ai = 0.5 * g1.w * (g2.x * bg.x + g2.y * bg.y + g2.z * bg.z);
@@ -755,8 +768,9 @@ __global__ void __launch_bounds__(kBlock) k_forces_fluid(const __grid_constant__
   forces_fluid_group<G, M, kTvf, kSingleEta, kHeat>(P, D, L, list, nlist, fl, Hout, Sin, sdiff, t / G, (int)(t % G));
 }
 
+// (without the fused conduction: 7 blocks of 128 per SM at 72 registers, 12 bytes spilled outside the row walk)
 template <int G, int M, bool kTvf, bool kSingleEta, bool kHeat>
-__global__ void __launch_bounds__(kBlock) k_forces_fluid_sm(const __grid_constant__ DevParams P, Particles D,
+__global__ void __launch_bounds__(kBlock, kHeat ? 4 : 7) k_forces_fluid_sm(const __grid_constant__ DevParams P, Particles D,
                                                              NbrList L, const uint32_t* __restrict__ list,
                                                              size_t nlist, DevFlags* __restrict__ fl,
                                                              uint32_t* __restrict__ next, int nq,
